@@ -1,0 +1,561 @@
+#!/usr/bin/env python
+"""bench.py -- B200 benchmark of the FP64 memory-bound kernels (arXiv 2502.16851).
+
+Metric (BASELINE.json): achieved HBM GB/s (% of B200 peak) per kernel, and the
+tensor-core vs CUDA-core speedup against the paper's bound re-derived from
+B200's own FP64 peaks and HBM bandwidth.
+
+Headline line (`value`): BASELINE.json configs[1], CSR SpMV FP64, 2^22 rows
+per GPU, 16 nnz/row in a +-65536 band, int32 indices, CUDA-core variant; one
+step = one y = A x over HBM-resident inputs (889,192,452 algorithmic bytes =
+the reference's spmv_csr_model, kernels.cpp:123-135).  At N > 1 each rank
+owns 2^22 rows of an N*2^22-row matrix (weak scaling) and every step
+exchanges the x band halo with its neighbours over NCCL, overlapped with the
+interior rows.  Inputs (889 MB/step) exceed the 126 MB L2; x (32 MiB) stays
+L2-resident by design (the model counts it once).
+
+Also on the same JSON line (N = 1): `per_kernel` -- every BASELINE config
+(STREAM 2^27 x 20 reps, SpMV x 20, 2d5pt 16384^2 x 100 steps, 3d7pt and
+3d27pt 512^3 x 50 steps) on both units, with GB/s, fraction of the measured
+HBM peak, TC/CC speedup and the B200-derived bound (K11 FP64 peaks measured
+live); `e2e` through the host-buffer C-ABI call; `cpu_baseline` (the oracle
+port on this box's cores); `roofline`; `clocks`; `gpu_launches`.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload spmv|stream|2d5pt|3d7pt|3d27pt] [--unit cc|tc]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "achieved HBM GB/s (% of B200 peak) per kernel; TC vs CUDA-core speedup vs bound"
+SEED = 2025
+HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
+
+WORKLOADS = {
+    "stream": dict(desc="STREAM Scale FP64 a=q*b, q=3, n=2^27 (BASELINE configs[0])", reps=20),
+    "spmv": dict(desc="CSR SpMV FP64, n=2^22 rows/GPU, 16 nnz/row, band +-65536, int32 idx "
+                      "(BASELINE configs[1])", reps=20),
+    "2d5pt": dict(desc="2d5pt Jacobi FP64 16384^2, c0=0.5 c1=0.125 (BASELINE configs[2])", reps=100),
+    "3d7pt": dict(desc="3d7pt Jacobi FP64 512^3, c0=0.4 c1=0.1 (BASELINE configs[3])", reps=50),
+    "3d27pt": dict(desc="3d27pt box Jacobi FP64 512^3, w=1/(1+|d|) normalised (BASELINE configs[4])",
+                   reps=50),
+}
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ---------------------------------------------------------------------------
+# clocks: NVML sampled in a thread during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int, period_s: float = 0.01):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.period = period_s
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# workloads on the GPU
+# ---------------------------------------------------------------------------
+class Spmv:
+    n_local = 1 << 22
+    k = 16
+    hb = 65536
+
+    def __init__(self, torch, P, D, rank, world):
+        self.torch, self.P, self.D, self.world = torch, P, D, world
+        n_glob = self.n_local * world
+        self.part = pt = D.SpmvPartition(n_glob, self.hb, world, rank)
+        m = pt.rows
+        dev = "cuda"
+        self.rp = torch.empty(m + 1, dtype=torch.int32, device=dev)
+        self.col = torch.empty(m * self.k, dtype=torch.int32, device=dev)
+        self.val = torch.empty(m * self.k, dtype=torch.float64, device=dev)
+        self.x = torch.empty(pt.window, dtype=torch.float64, device=dev)
+        self.y = torch.empty(m, dtype=torch.float64, device=dev)
+        P.gen_band_csr(m, pt.r0, n_glob, self.k, self.hb, SEED, self.rp, self.col, self.val)
+        P.fill_uniform(self.x, SEED, 4, pt.col_base, 1)
+        # whole-job algorithmic bytes: the reference model on the global matrix;
+        # per-rank: the model on the local row block with its own x slice.
+        self.job_bytes = P.spmv_csr_model(n_glob, n_glob, n_glob * self.k).traffic_bytes
+        self.bytes = P.spmv_csr_model(m, m, m * self.k).traffic_bytes
+
+    def step(self, unit):
+        P, pt = self.P, self.part
+        if self.world == 1:
+            P.spmv_csr(self.rp, self.col, self.val, self.x, self.y, unit=unit)
+        else:
+            self.D.dist_spmv_step(pt, self.x, lambda lo, hi: P.spmv_csr_rows(
+                lo, hi, self.rp, self.col, self.val, self.x, self.y, col_base=pt.col_base, unit=unit))
+
+    def host_buffers(self):
+        t = self.torch
+        pin = dict(pin_memory=True)
+        col = self.col if self.world == 1 else (self.col - self.part.col_base)
+        return {"rp": t.empty(self.rp.shape, dtype=t.int32, **pin).copy_(self.rp),
+                "col": t.empty(self.col.shape, dtype=t.int32, **pin).copy_(col),
+                "val": t.empty(self.val.shape, dtype=t.float64, **pin).copy_(self.val),
+                "x": t.empty(self.x.shape, dtype=t.float64, **pin).copy_(self.x),
+                "y": t.empty(self.y.shape, dtype=t.float64, **pin)}
+
+    def e2e_step(self, h, unit):
+        self.P.spmv_csr_host(h["rp"], h["col"], h["val"], h["x"], h["y"], unit=unit)
+
+    def h2d_d2h(self, h):
+        return (sum(h[k].numel() * h[k].element_size() for k in ("rp", "col", "val", "x")),
+                h["y"].numel() * 8)
+
+
+class Stream:
+    n = 1 << 27
+
+    def __init__(self, torch, P, D, rank, world):
+        self.torch, self.P = torch, P
+        lo, hi = D.scale_chunk(self.n * world, world, rank)
+        self.b = torch.empty(hi - lo, dtype=torch.float64, device="cuda")
+        self.a = torch.empty_like(self.b)
+        P.fill_uniform(self.b, SEED, 1, lo, 1)
+        self.bytes = P.scale_model(hi - lo).traffic_bytes
+        self.job_bytes = P.scale_model(self.n * world).traffic_bytes
+
+    def step(self, unit):
+        self.P.scale(self.a, self.b, 3.0, unit=unit)
+
+    def host_buffers(self):
+        t = self.torch
+        return {"b": t.empty(self.b.shape, dtype=t.float64, pin_memory=True).copy_(self.b),
+                "a": t.empty(self.b.shape, dtype=t.float64, pin_memory=True)}
+
+    def e2e_step(self, h, unit):
+        self.P.scale_host(h["a"], h["b"], 3.0, unit=unit)
+
+    def h2d_d2h(self, h):
+        return h["b"].numel() * 8, h["a"].numel() * 8
+
+
+class Stencil:
+    """One step = one full BASELINE run (100 / 50 double-buffered timesteps).
+    At N > 1 the global grid grows along the slab axis (weak scaling)."""
+
+    def __init__(self, torch, P, D, rank, world, preset):
+        self.torch, self.P, self.D, self.preset, self.world = torch, P, D, preset, world
+        base = (16384, 16384) if preset == "2d5pt" else (512, 512, 512)
+        self.tsteps = 100 if preset == "2d5pt" else 50
+        gshape = (base[0] * world,) + base[1:]
+        self.part = pt = D.SlabPartition(gshape[0], world, rank, 1)
+        local = (pt.local_outer,) + base[1:]
+        self.u = torch.empty(local, dtype=torch.float64, device="cuda")
+        P.stencil_init(self.u, 1, SEED, outer_begin=pt.g_lo, global_shape=gshape)
+        self.v = self.u.clone()
+        inner = lambda shp: __import__("math").prod(s - 2 for s in shp)
+        self.job_bytes = 16 * inner(gshape) * self.tsteps
+        a, b = pt.own_local()
+        own_inner = (min(pt.o1, gshape[0] - 1) - max(pt.o0, 1)) * inner((3,) + base[1:])
+        self.bytes = 16 * own_inner * self.tsteps
+
+    def step(self, unit):
+        P = self.P
+        if self.world == 1:
+            P.stencil(self.preset, self.u, self.v, self.tsteps, unit=unit)
+        else:
+            self.D.dist_stencil(self.part, self.u, self.v, self.tsteps,
+                                lambda s, d, lo, hi: P.stencil_sweep(self.preset, s, d, lo, hi,
+                                                                     unit=unit))
+
+    def host_buffers(self):
+        t = self.torch
+        return {"u": t.empty(self.u.shape, dtype=t.float64, pin_memory=True).copy_(self.u),
+                "v": t.empty(self.u.shape, dtype=t.float64, pin_memory=True).copy_(self.u)}
+
+    def e2e_step(self, h, unit):
+        self.P.stencil_host(self.preset, h["u"], h["v"], self.tsteps, unit=unit)
+
+    def h2d_d2h(self, h):
+        return h["u"].numel() * 8, h["u"].numel() * 8
+
+
+def make(name, torch, P, D, rank, world):
+    if name == "spmv":
+        return Spmv(torch, P, D, rank, world)
+    if name == "stream":
+        return Stream(torch, P, D, rank, world)
+    return Stencil(torch, P, D, rank, world, name)
+
+
+def time_steps(torch, wl, unit, steps, warmup, world):
+    """W untimed steps, then exactly K timed steps bracketed by barrier+sync;
+    per-step CUDA events on the launching (current) stream.  Returns
+    (max-over-ranks total ms, list of per-step ms on this rank)."""
+    import torch.distributed as dist
+
+    for _ in range(warmup):
+        wl.step(unit)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    ev[0].record()
+    for i in range(steps):
+        wl.step(unit)
+        ev[i + 1].record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    per = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
+    total = ev[0].elapsed_time(ev[steps])
+    if world > 1:
+        t = torch.tensor([total], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total = float(t.item())
+    return total, per
+
+
+def fp64_peaks(torch, P):
+    """K11: DFMA and DMMA throughput over all SMs (TFLOP/s)."""
+    sink = torch.zeros(256, dtype=torch.float64, device="cuda")
+    out = {}
+    for name, unit, iters in (("cuda_core", P.CUDA_CORE, 20000), ("tensor_core", P.TENSOR_CORE, 20000)):
+        P.fp64_peak_launch(unit, 1000, sink)
+        torch.cuda.synchronize()
+        best = 0.0
+        for _ in range(3):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            fl = P.fp64_peak_launch(unit, iters, sink)
+            e.record()
+            torch.cuda.synchronize()
+            best = max(best, fl / (s.elapsed_time(e) * 1e-3) / 1e12)
+        out[name] = round(best, 2)
+    return out
+
+
+def per_kernel_table(torch, P, D, peaks, hbm):
+    rows = {}
+    alpha = peaks["tensor_core"] / peaks["cuda_core"]
+    balance = peaks["cuda_core"] * 1e12 / (hbm * 1e9)
+    intensity = {
+        "stream": P.scale_model(1).intensity,
+        "spmv": P.spmv_csr_model(1 << 22, 1 << 22, 1 << 26).intensity,
+        "2d5pt": P.stencil_model("2d5pt").intensity,
+        "3d7pt": P.stencil_model("3d7pt").intensity,
+        "3d27pt": P.stencil_model("3d27pt").intensity,
+    }
+    for name, spec in WORKLOADS.items():
+        wl = make(name, torch, P, D, 0, 1)
+        res = {}
+        for uname, unit in (("cc", P.CUDA_CORE), ("tc", P.TENSOR_CORE)):
+            reps = spec["reps"] if name in ("stream", "spmv") else 1
+            total, per = time_steps(torch, wl, unit, reps, 2, 1)
+            ms = total / reps
+            if name in ("stream", "spmv"):
+                gbs = wl.bytes / (ms * 1e-3) / 1e9
+                unit_ms = ms
+            else:
+                gbs = wl.bytes / (ms * 1e-3) / 1e9
+                unit_ms = ms / wl.tsteps
+            res[uname] = {"gbs": round(gbs, 1), "frac_of_measured_peak": round(gbs / hbm, 4),
+                          "ms_per_unit": round(unit_ms, 4)}
+        spd = res["tc"]["gbs"] / res["cc"]["gbs"]
+        a_eff = max(alpha, 1.0)
+        ceil, _ = P.kernel_speedup_ceiling(a_eff, balance, intensity[name])
+        res["tc_over_cc"] = round(spd, 4)
+        res["bound"] = round(ceil, 4)
+        res["intensity"] = round(intensity[name], 5)
+        res["within_bound"] = bool(spd <= ceil * 1.02)
+        rows[name] = res
+        del wl
+        torch.cuda.empty_cache()
+    return rows, {"alpha": round(alpha, 4), "balance_flop_per_byte": round(balance, 4),
+                  "tensor_core_ceiling": round(P.tensor_core_ceiling(max(alpha, 1.0)), 4),
+                  "note": "alpha = measured DMMA/DFMA FP64 peak; ceilings from "
+                          "kernel_speedup_ceiling (bounds.cpp:72-85) with alpha clamped to >= 1"}
+
+
+def cpu_baseline(name, seconds=10.0):
+    """Oracle port timed on this host's cores (bounded sample)."""
+    import numpy as np
+
+    import oracle as O
+
+    thr = O.num_threads()
+    if name == "spmv":
+        n, k, hb = 1 << 22, 16, 65536
+        rp, col, val = O.gen_band_csr(n, 0, n, k, hb, SEED)
+        x = O.fill_uniform(n, SEED, 4, 0, 1)
+        nbytes = (n * k + 2 * n) * 8 + (n * k + n + 1) * 4
+        fn = lambda: O.spmv_csr(rp, col, val, x)
+        sample = "full 2^22-row matrix, repeated SpMV"
+    elif name == "stream":
+        n = 1 << 27
+        b = O.fill_uniform(n, SEED, 1, 0, 1)
+        nbytes = 16 * n
+        fn = lambda: O.scale(b, 3.0)
+        sample = "full 2^27-element Scale, repeated"
+    else:
+        shape = (4096, 4096) if name == "2d5pt" else (256, 256, 256)
+        u0 = O.stencil_init(shape, 1, SEED)
+        inner = 1
+        for s in shape:
+            inner *= s - 2
+        nbytes = 16 * inner
+        fn = lambda: O.stencil(name, u0, 1)
+        sample = f"{shape} grid (scaled-down BASELINE grid), 1 timestep per call"
+    fn()
+    t0 = time.perf_counter()
+    calls = 0
+    while True:
+        fn()
+        calls += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or calls >= 500:
+            break
+    gbs = nbytes * calls / el / 1e9
+    return {"value": round(gbs, 3), "unit": "GB/s", "cores": thr, "kind": "port",
+            "sample": f"{sample}; {calls} calls in {el:.1f} s"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference path on the host cores (the reference
+    has no executing kernel, so its CPU path is the oracle port)."""
+    if rank != 0:
+        return
+    import oracle as O
+
+    name = args.workload
+    spec = WORKLOADS[name]
+    thr = O.num_threads()
+    if name == "spmv":
+        n, k, hb = 1 << 22, 16, 65536
+        rp, col, val = O.gen_band_csr(n, 0, n, k, hb, SEED)
+        x = O.fill_uniform(n, SEED, 4, 0, 1)
+        nbytes = (n * k + 2 * n) * 8 + (n * k + n + 1) * 4
+        fn = lambda: O.spmv_csr(rp, col, val, x)
+        sample = "full 2^22-row BASELINE matrix, one SpMV per step"
+    elif name == "stream":
+        n = 1 << 27
+        b = O.fill_uniform(n, SEED, 1, 0, 1)
+        nbytes = 16 * n
+        fn = lambda: O.scale(b, 3.0)
+        sample = "full 2^27 Scale per step"
+    else:
+        shape = (16384, 16384) if name == "2d5pt" else (512, 512, 512)
+        u0 = O.stencil_init(shape, 1, SEED)
+        inner = 1
+        for s in shape:
+            inner *= s - 2
+        nbytes = 16 * inner
+        fn = lambda: O.stencil(name, u0, 1)
+        sample = f"full {shape} grid, one timestep per step (of {spec['reps']})"
+    for _ in range(args.warmup):
+        fn()
+    t0 = time.perf_counter()
+    steps = 0
+    budget = 120.0
+    for _ in range(args.steps):
+        fn()
+        steps += 1
+        if time.perf_counter() - t0 > budget:
+            break
+    el = time.perf_counter() - t0
+    gbs = nbytes * steps / el / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s",
+        "n_gpus": world, "steps": steps, "warmup": args.warmup,
+        "ms_per_step": round(el / steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded splitmix64, BASELINE shapes)",
+        "config": {"workload": spec["desc"], "unit": "cpu"},
+        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": thr, "kind": "port",
+                         "sample": sample + (f"; stopped after {steps} of {args.steps} steps "
+                                             f"({budget:.0f} s budget)" if steps < args.steps else "")},
+        "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="spmv", choices=list(WORKLOADS))
+    ap.add_argument("--unit", default="cc", choices=["cc", "tc"])
+    ap.add_argument("--no-per-kernel", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2502_16851_b200 as P
+    from paper_2502_16851_b200 import dist as D
+
+    if world > 1:
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    P.lib()
+    hbm, hbm_src = hbm_peak()
+    unit = P.CUDA_CORE if args.unit == "cc" else P.TENSOR_CORE
+
+    wl = make(args.workload, torch, P, D, rank, world)
+    dev_index = torch.cuda.current_device()
+    launches0 = P.kernel_launches()
+    with ClockSampler(dev_index) as clk:
+        # warm-up inside so the sampler sees the GPU under load before timing
+        total_ms, per = time_steps(torch, wl, unit, args.steps, args.warmup, world)
+    launches = P.kernel_launches() - launches0
+    # launches counted over warmup+timed; report timed share
+    timed_launches = int(round(launches * args.steps / (args.steps + args.warmup)))
+    bytes_per_step_rank = wl.bytes
+    value = wl.job_bytes * args.steps / (total_ms * 1e-3) / 1e9
+    ms_per_step = total_ms / args.steps
+    per_sorted = sorted(per)
+    launch_ms = statistics.mean(per)  # one kernel launch per step at N=1
+    achieved = bytes_per_step_rank / (launch_ms * 1e-3) / 1e9
+
+    # end to end through the host-buffer C-ABI call
+    h = wl.host_buffers()
+    h2d, d2h = wl.h2d_d2h(h)
+    wl.e2e_step(h, unit)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        wl.e2e_step(h, unit)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_val = wl.job_bytes * args.e2e_steps / e2e_s / 1e9
+    del h
+
+    traffic = ncu_traffic().get(f"{args.workload}_{args.unit}")
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded splitmix64 inputs generated in HBM; BASELINE.json shapes)",
+        "config": {"workload": WORKLOADS[args.workload]["desc"],
+                   "unit": "cuda_core" if unit == P.CUDA_CORE else "tensor_core",
+                   "parallelism": f"rows/slabs x{world}" if world > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (no flush needed)",
+                   "algorithmic_bytes_per_step_per_gpu": bytes_per_step_rank,
+                   "peak_source": hbm_src},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
+                     "frac": round(achieved / hbm, 4), "traffic": traffic,
+                     "launch_ms_mean": round(launch_ms, 5),
+                     "launch_ms_p50": round(per_sorted[len(per_sorted) // 2], 5)},
+        "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+                "api": "rl_*_host C-ABI (pinned host buffers, copies inside the timed call)"},
+        "gpu_launches": timed_launches,
+        "clocks": clk.summary(),
+    }
+    del wl
+    torch.cuda.empty_cache()
+
+    if world == 1 and not args.no_per_kernel:
+        peaks = fp64_peaks(torch, P)
+        with ClockSampler(dev_index) as clk2:
+            table, bounds = per_kernel_table(torch, P, D, peaks, hbm)
+        line["per_kernel"] = table
+        line["fp64_peaks_tflops"] = peaks
+        line["bounds"] = bounds
+        line["per_kernel_clocks"] = clk2.summary()
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.workload)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

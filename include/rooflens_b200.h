@@ -1,0 +1,231 @@
+/*
+ * rooflens_b200.h -- C-ABI of the B200-native (sm_100a) FP64 memory-bound
+ * kernels of arXiv 2502.16851: STREAM Scale, CSR SpMV and Jacobi stencils,
+ * each with a CUDA-core (DFMA) and a tensor-core (DMMA) variant.
+ *
+ * The executing entry points sit behind the reference's kernel identities
+ * (/root/reference/proj/include/rooflens/kernels.hpp:84-105): every call
+ * returns, in its rl_kchar, exactly the W (flops) / Q (bytes) that the
+ * reference model computes for the same arguments.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Device pointers unless the function
+ *     name ends in _host.  Calls are asynchronous on `stream` (a
+ *     cudaStream_t; NULL = the legacy default stream) except _host calls and
+ *     pure host functions.  No allocation happens in the device entry points.
+ *   - Return codes: RL_OK (0); 1 + ErrorKind ordinal of the reference
+ *     (error.hpp:10-32: MissingPeak=0 ... IoError=16); RL_ERR_CUDA_BASE +
+ *     cudaError_t.  rl_last_error() returns a thread-local copy of the
+ *     message, formatted like the reference's exceptions ("<Kind>: <msg>",
+ *     error.hpp:38-40).  No exception crosses the boundary.
+ *   - Precision is FP64 only in this build (ValidationError otherwise).
+ *   - Reentrant per stream.  There is no CPU fallback: on a machine without a
+ *     usable sm_100a device the executing entry points fail with a CUDA code.
+ */
+#ifndef ROOFLENS_B200_H
+#define ROOFLENS_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define RL_API __attribute__((visibility("default")))
+#else
+#define RL_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ExecutionUnit (hardware.hpp:19) -- selects the CC or TC kernel variant. */
+typedef enum { RL_CUDA_CORE = 0, RL_TENSOR_CORE = 1 } rl_unit;
+/* Precision (hardware.hpp:21) -- element_bytes 8/4/2 (hardware.cpp:27-34). */
+typedef enum { RL_FP64 = 0, RL_FP32 = 1, RL_FP16 = 2 } rl_precision;
+/* Boundedness (roofline.hpp:17). */
+typedef enum { RL_MEMORY_BOUND = 0, RL_COMPUTE_BOUND = 1, RL_BALANCED = 2 } rl_boundedness;
+
+typedef void* rl_stream; /* cudaStream_t */
+
+/* Flattened KernelCharacterization (kernels.hpp:34-44). */
+typedef struct {
+    uint64_t work_flops;
+    uint64_t traffic_bytes;
+} rl_kchar;
+
+/* FP64 slice of HardwareSpec (hardware.hpp:43-58), SI units. */
+typedef struct {
+    char name[64];
+    double memory_bandwidth; /* bytes/s */
+    double l2_cache_bytes;
+    double peak_cuda_core;   /* flops/s, FP64 */
+    double peak_tensor_core; /* flops/s, FP64; 0 = absent */
+} rl_hw_spec;
+
+#define RL_OK 0
+#define RL_ERR_KIND_BASE 1
+#define RL_ERR_CUDA_BASE 100
+
+/* ErrorKind ordinals (error.hpp:10-32). */
+enum {
+    RL_KIND_MISSING_PEAK = 0, RL_KIND_PARSE_ERROR, RL_KIND_VALIDATION_ERROR,
+    RL_KIND_MISSING_FIELD, RL_KIND_UNKNOWN_HARDWARE, RL_KIND_INVALID_COUNT,
+    RL_KIND_INVALID_INDEX_SIZE, RL_KIND_ZERO_INTENSITY, RL_KIND_INVALID_ALPHA,
+    RL_KIND_ZERO_BALANCE, RL_KIND_INVALID_RANGE, RL_KIND_BAD_BANNER,
+    RL_KIND_UNSUPPORTED_FORMAT, RL_KIND_MALFORMED_ENTRY, RL_KIND_INDEX_OUT_OF_RANGE,
+    RL_KIND_TRUNCATED_FILE, RL_KIND_IO_ERROR
+};
+
+RL_API const char* rl_last_error(void);
+RL_API const char* rl_version(void);
+
+/* ---------------------------------------------------------------------------
+ * Accounting (pure host functions) -- the reference models, restated.
+ * ------------------------------------------------------------------------- */
+
+/* replaces rooflens::scale_model            kernels.hpp:86,  kernels.cpp:74-86 */
+RL_API int rl_scale_model(uint64_t n_elements, rl_precision precision, rl_kchar* out);
+/* replaces rooflens::gemv_model             kernels.hpp:89,  kernels.cpp:88-101 */
+RL_API int rl_gemv_model(uint64_t m, uint64_t n, rl_precision precision, rl_kchar* out);
+/* replaces rooflens::spmv_generic_model     kernels.hpp:93-95, kernels.cpp:103-121 */
+RL_API int rl_spmv_generic_model(uint64_t rows, uint64_t cols, uint64_t nnz,
+                          uint64_t index_entry_count, uint64_t index_entry_bytes,
+                          uint64_t packed_entry_count, uint64_t packed_entry_bytes,
+                          rl_precision precision, rl_kchar* out);
+/* replaces rooflens::spmv_csr_model         kernels.hpp:99-100, kernels.cpp:123-135 */
+RL_API int rl_spmv_csr_model(uint64_t rows, uint64_t cols, uint64_t nnz, uint64_t index_bytes,
+                      rl_precision precision, rl_kchar* out);
+/* replaces rooflens::stencil_model          kernels.hpp:104-105, kernels.cpp:137-155 */
+RL_API int rl_stencil_model(const char* preset, rl_precision precision, uint64_t temporal_depth,
+                     rl_kchar* out);
+/* replaces rooflens::stencil_preset         kernels.hpp:74, kernels.cpp:62-68
+ * (dim 2|3, |S|, halo radius). */
+RL_API int rl_stencil_preset(const char* name, int* dimensionality, uint64_t* point_count,
+                      int* radius);
+/* Default weights of a preset in canonical offset order (BASELINE.json). */
+RL_API int rl_stencil_default_weights(const char* name, double* weights, uint64_t capacity);
+
+/* ---------------------------------------------------------------------------
+ * Executing kernels (device pointers, async on `stream`).
+ * ------------------------------------------------------------------------- */
+
+/* STREAM Scale a[i] = q*b[i].  CC: 256-bit LDG/STG DMUL.
+ * TC: A = B*(qI) on DMMA m8n8k4.  Bit-exact vs q*b for
+ * finite inputs; the TC variant returns +0 for b = -0 and propagates a
+ * non-finite b into its 4-element fragment row (documented in DESIGN.md). */
+RL_API int rl_scale(rl_unit unit, rl_precision precision, double* a, const double* b, double q,
+             uint64_t n, rl_stream stream, rl_kchar* out);
+
+/* CSR SpMV y = A*x, int32 row_ptr (m+1) / col (nnz),
+ * 0-based, column indices in [0, n).  kchar = spmv_csr_model(.., 4, FP64). */
+RL_API int rl_spmv_csr(rl_unit unit, rl_precision precision, uint64_t m, uint64_t n, uint64_t nnz,
+                const int32_t* row_ptr, const int32_t* col, const double* val,
+                const double* x, double* y, rl_stream stream, rl_kchar* out);
+
+/* Row-range form for row-partitioned / overlapped use: computes y[i] for
+ * i in [row_begin, row_end) reading x[col[k] - col_base].  No accounting. */
+RL_API int rl_spmv_csr_rows(rl_unit unit, rl_precision precision, uint64_t row_begin,
+                     uint64_t row_end, const int32_t* row_ptr, const int32_t* col,
+                     const double* val, const double* x, int64_t col_base, double* y,
+                     rl_stream stream);
+
+/* Jacobi stencil, `steps` double-buffered timesteps.
+ * dims = {nx, ny, nz} (x fastest; nz ignored for 2D presets).  weights: |S|
+ * doubles in canonical offset order, or NULL for the BASELINE defaults.  The
+ * outer ring of width `radius` is a Dirichlet boundary and is never written
+ * (initialise it identically in u and v).  Result in u if steps is even,
+ * else in v.  kchar = stencil_model(preset, FP64, 1) x updated points x steps. */
+RL_API int rl_stencil(rl_unit unit, rl_precision precision, const char* preset,
+               const uint64_t* dims, const double* weights, uint64_t steps, double* u,
+               double* v, rl_stream stream, rl_kchar* out);
+
+/* One sweep v = S(u) restricted to outer indices [o_begin, o_end) (rows in 2D,
+ * planes in 3D) -- the slab / interior-vs-edge building block.  Boundary
+ * indices inside the range are skipped.  No accounting. */
+RL_API int rl_stencil_sweep(rl_unit unit, rl_precision precision, const char* preset,
+                     const uint64_t* dims, const double* weights, uint64_t o_begin,
+                     uint64_t o_end, const double* u, double* v, rl_stream stream);
+
+/* ---------------------------------------------------------------------------
+ * End-to-end entry points on HOST buffers: pinned staging, H2D copies,
+ * kernel(s), D2H copy, all inside the call (synchronous).  Chunked and
+ * pipelined on two streams so copies overlap each other and the kernels.
+ * ------------------------------------------------------------------------- */
+
+RL_API int rl_scale_host(rl_unit unit, rl_precision precision, double* a, const double* b, double q,
+                  uint64_t n, rl_kchar* out);
+RL_API int rl_spmv_csr_host(rl_unit unit, rl_precision precision, uint64_t m, uint64_t n,
+                     uint64_t nnz, const int32_t* row_ptr, const int32_t* col,
+                     const double* val, const double* x, double* y, rl_kchar* out);
+RL_API int rl_stencil_host(rl_unit unit, rl_precision precision, const char* preset,
+                    const uint64_t* dims, const double* weights, uint64_t steps, double* u,
+                    double* v, rl_kchar* out);
+/* Release the device/pinned workspaces cached by the _host entry points. */
+RL_API int rl_host_workspace_release(void);
+
+/* ---------------------------------------------------------------------------
+ * Deterministic input generators (device), bit-identical to oracle/oracle.c.
+ * ------------------------------------------------------------------------- */
+
+/* kind 0: U[0,1), kind 1: U[-1,1); element i keyed by (seed, stream_id, idx0+i). */
+RL_API int rl_fill_uniform(double* out, uint64_t n, uint64_t seed, uint64_t stream_id, uint64_t idx0,
+                    int kind, rl_stream stream);
+/* Banded CSR rows [row0, row0+m_local) of an n-column matrix, k sorted distinct
+ * columns per row uniform in [max(0,i-hb), min(n-1,i+hb)]; values U[-1,1).
+ * row_ptr is local (starts at 0), columns are global. */
+RL_API int rl_gen_band_csr(uint64_t m_local, uint64_t row0, uint64_t n, uint32_t k, uint64_t hb,
+                    uint64_t seed, int32_t* row_ptr, int32_t* col, double* val,
+                    rl_stream stream);
+/* Stencil field: interior U[0,1) keyed by the global linear index, Dirichlet
+ * ring (width radius) 0.  dims = global {nx, ny, nz} (nz ignored when dim==2);
+ * the buffer holds outer indices [outer_begin, outer_end) of the global grid
+ * (rows in 2D, planes in 3D) -- a whole grid or one rank's slab with ghosts. */
+RL_API int rl_stencil_init(double* u, const uint64_t* dims, int dim, uint64_t outer_begin,
+                           uint64_t outer_end, int radius, uint64_t seed, rl_stream stream);
+
+/* ---------------------------------------------------------------------------
+ * Hardware spec, roofline and speedup bounds (pure host functions).
+ * ------------------------------------------------------------------------- */
+
+/* replaces rooflens::load_spec (hardware.cpp:183-237): same JSON schema
+ * (hardware.hpp:75-81), unknown keys -> ParseError, SI conversion. */
+RL_API int rl_load_spec(const char* json_text, rl_hw_spec* out);
+/* replaces rooflens::builtin_spec (hardware.cpp:121-150): "A100-80GB", "GH200". */
+RL_API int rl_builtin_spec(const char* name, rl_hw_spec* out);
+/* machine_balance (hardware.cpp:112-114) / tensor_alpha (hardware.cpp:116-119). */
+RL_API int rl_machine_balance(const rl_hw_spec* spec, rl_unit unit, rl_precision precision,
+                       double* out);
+RL_API int rl_tensor_alpha(const rl_hw_spec* spec, rl_precision precision, double* out);
+/* attainable = min(P, B*I) (roofline.cpp:21-28); classify (roofline.cpp:30-34). */
+RL_API int rl_attainable(const rl_hw_spec* spec, rl_unit unit, rl_precision precision,
+                  double intensity, double* out);
+RL_API int rl_classify(double intensity, double balance);
+/* bounds.cpp:56-62, 72-135. */
+RL_API int rl_unoverlapped_speedup(double t_cmp, double t_mem, double t_others, double alpha,
+                            double* out);
+RL_API int rl_kernel_speedup_ceiling(double alpha, double balance, double intensity, double* out,
+                              int* n_warnings);
+RL_API int rl_tensor_core_ceiling(double alpha, double* out);
+RL_API int rl_workload_ceiling(double intensity, double balance, double* out);
+RL_API int rl_min_temporal_depth(double balance, double single_step_intensity, uint64_t* out);
+RL_API int rl_tc_scale_trick_throughput(double peak_tc, uint64_t m, uint64_t n, double* out);
+
+/* ---------------------------------------------------------------------------
+ * K11: FP64 peak microbenchmarks (DFMA chains on the fp64 pipe, DMMA chains on
+ * the tensor pipe), all SMs.  Launches one kernel on `stream`; *flops_out gets
+ * the exact flop count it performs (divide by the event time).
+ * ------------------------------------------------------------------------- */
+RL_API int rl_fp64_peak_launch(rl_unit unit, uint64_t iters, rl_stream stream, double* sink,
+                        double* flops_out);
+
+/* Kernel-variant selection knobs (benchmark sweeps); returns previous value. */
+RL_API int rl_tuning_set(const char* key, int64_t value, int64_t* previous);
+
+/* Number of CUDA kernels this library has launched since load (evidence for
+ * the benchmark's gpu_launches count). */
+RL_API uint64_t rl_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ROOFLENS_B200_H */

@@ -1,0 +1,182 @@
+// refshim.cpp -- extern "C" shim over the UNMODIFIED reference library
+// (rooflens, /root/reference/proj/src/*.cpp), compiled together with it by
+// oracle/Makefile into oracle/_ref/librooflens_ref.so.
+//
+// TEST INFRASTRUCTURE ONLY: the reference's symbols are C++-mangled and return
+// std::string/std::map-owning structs, so ctypes cannot call them directly.
+// This shim flattens them for tests/ (accounting parity of the product's
+// rl_kchar against the reference's own models) and for tests/golden/make_golden.py.
+// It contains no arithmetic of its own: every value comes from the reference.
+//
+// Return convention mirrors the product C-ABI: 0 = OK, 1 + ErrorKind ordinal
+// (reference error.hpp:10-32) on a rooflens::Error.
+#include <cstdint>
+#include <cstring>
+#include <string>
+
+#include "rooflens/bounds.hpp"
+#include "rooflens/error.hpp"
+#include "rooflens/hardware.hpp"
+#include "rooflens/kernels.hpp"
+#include "rooflens/roofline.hpp"
+
+using namespace rooflens;
+
+namespace {
+thread_local std::string g_last;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        g_last.clear();
+        return 0;
+    } catch (const Error& e) {
+        g_last = e.what();
+        return 1 + static_cast<int>(e.kind());
+    } catch (const std::exception& e) {
+        g_last = e.what();
+        return 99;
+    }
+}
+
+Precision prec_of(int p) { return static_cast<Precision>(p); }
+ExecutionUnit unit_of(int u) { return static_cast<ExecutionUnit>(u); }
+
+void out_kc(const KernelCharacterization& k, uint64_t* w, uint64_t* q) {
+    *w = k.work_flops;
+    *q = k.traffic_bytes;
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_last.c_str(); }
+
+int ref_scale_model(uint64_t n, int prec, uint64_t* w, uint64_t* q) {
+    return guarded([&] { out_kc(scale_model(n, prec_of(prec)), w, q); });
+}
+
+int ref_gemv_model(uint64_t m, uint64_t n, int prec, uint64_t* w, uint64_t* q) {
+    return guarded([&] { out_kc(gemv_model(m, n, prec_of(prec)), w, q); });
+}
+
+int ref_spmv_generic_model(uint64_t m, uint64_t n, uint64_t nnz, uint64_t idx_count,
+                           uint64_t idx_bytes, uint64_t packed_count, uint64_t packed_bytes,
+                           int prec, uint64_t* w, uint64_t* q) {
+    return guarded([&] {
+        SparseMatrixStats s{m, n, nnz};
+        SparseMetadataTraffic meta{idx_count, idx_bytes, packed_count, packed_bytes};
+        out_kc(spmv_generic_model(s, meta, prec_of(prec)), w, q);
+    });
+}
+
+int ref_spmv_csr_model(uint64_t m, uint64_t n, uint64_t nnz, uint64_t index_bytes, int prec,
+                       uint64_t* w, uint64_t* q) {
+    return guarded([&] {
+        SparseMatrixStats s{m, n, nnz};
+        out_kc(spmv_csr_model(s, index_bytes, prec_of(prec)), w, q);
+    });
+}
+
+int ref_stencil_model(const char* preset, int prec, uint64_t t, uint64_t* w, uint64_t* q,
+                      uint64_t* points) {
+    return guarded([&] {
+        const StencilShape& s = stencil_preset(preset);
+        *points = s.point_count;
+        out_kc(stencil_model(s, prec_of(prec), t), w, q);
+    });
+}
+
+int ref_intensity_ratio(uint64_t w, uint64_t q, uint64_t* num, uint64_t* den) {
+    return guarded([&] {
+        Ratio r = Ratio::of(w, q);
+        *num = r.num;
+        *den = r.den;
+    });
+}
+
+// Spec from a JSON document (reference hardware.cpp:183-237); returns the
+// FP64 figures (0 where absent) in SI units.
+int ref_load_spec(const char* text, double* bw, double* l2, double* p_cc, double* p_tc) {
+    return guarded([&] {
+        HardwareSpec s = load_spec(text);
+        *bw = s.memory_bandwidth;
+        *l2 = s.l2_cache_bytes;
+        *p_cc = s.has_peak(ExecutionUnit::CudaCore, Precision::FP64)
+                    ? s.peak(ExecutionUnit::CudaCore, Precision::FP64) : 0.0;
+        *p_tc = s.has_peak(ExecutionUnit::TensorCore, Precision::FP64)
+                    ? s.peak(ExecutionUnit::TensorCore, Precision::FP64) : 0.0;
+    });
+}
+
+int ref_builtin_spec(const char* name, double* bw, double* l2, double* p_cc, double* p_tc) {
+    return guarded([&] {
+        const HardwareSpec& s = builtin_spec(name);
+        *bw = s.memory_bandwidth;
+        *l2 = s.l2_cache_bytes;
+        *p_cc = s.peak(ExecutionUnit::CudaCore, Precision::FP64);
+        *p_tc = s.peak(ExecutionUnit::TensorCore, Precision::FP64);
+    });
+}
+
+// Balance / alpha / roofline on an FP64 spec built from explicit SI figures.
+static HardwareSpec mk(double bw, double p_cc, double p_tc) {
+    HardwareSpec s;
+    s.name = "probe";
+    s.memory_bandwidth = bw;
+    s.l2_cache_bytes = 0.0;
+    s.peaks[{ExecutionUnit::CudaCore, Precision::FP64}] = p_cc;
+    if (p_tc > 0.0) s.peaks[{ExecutionUnit::TensorCore, Precision::FP64}] = p_tc;
+    return s;
+}
+
+int ref_machine_balance(double bw, double p_cc, double p_tc, int unit, double* out) {
+    return guarded([&] { *out = machine_balance(mk(bw, p_cc, p_tc), unit_of(unit), Precision::FP64); });
+}
+
+int ref_tensor_alpha(double bw, double p_cc, double p_tc, double* out) {
+    return guarded([&] { *out = tensor_alpha(mk(bw, p_cc, p_tc), Precision::FP64); });
+}
+
+int ref_attainable(double bw, double p_cc, double p_tc, int unit, double intensity, double* out) {
+    return guarded([&] {
+        *out = attainable(mk(bw, p_cc, p_tc), unit_of(unit), Precision::FP64, intensity);
+    });
+}
+
+int ref_classify(double intensity, double balance) {
+    return static_cast<int>(classify(intensity, balance));
+}
+
+int ref_kernel_speedup_ceiling(double alpha, double balance, double intensity, double* out,
+                               int* n_warnings) {
+    return guarded([&] {
+        SpeedupBound b = kernel_speedup_ceiling(alpha, balance, intensity);
+        *out = b.value;
+        *n_warnings = static_cast<int>(b.warnings.size());
+    });
+}
+
+int ref_tensor_core_ceiling(double alpha, double* out) {
+    return guarded([&] { *out = tensor_core_ceiling(alpha).value; });
+}
+
+int ref_workload_ceiling(double intensity, double balance, double* out) {
+    return guarded([&] { *out = workload_ceiling(intensity, balance).value; });
+}
+
+int ref_unoverlapped_speedup(double t_cmp, double t_mem, double t_others, double alpha,
+                             double* out) {
+    return guarded([&] { *out = unoverlapped_speedup(TimeBreakdown{t_cmp, t_mem, t_others}, alpha); });
+}
+
+int ref_min_temporal_depth(double balance, double intensity, uint64_t* out) {
+    return guarded([&] { *out = min_temporal_depth(balance, intensity); });
+}
+
+int ref_tc_scale_trick_throughput(double peak_tc, uint64_t m, uint64_t n, double* out) {
+    return guarded([&] { *out = tc_scale_trick_throughput(peak_tc, m, n); });
+}
+
+}  // extern "C"

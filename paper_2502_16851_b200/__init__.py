@@ -1,0 +1,528 @@
+"""B200-native (sm_100a) FP64 memory-bound kernels of arXiv 2502.16851.
+
+Python host side of the framework: a thin ctypes binding of the C-ABI in
+``include/rooflens_b200.h`` (the library ``librooflens_b200.so`` built in-tree
+from ``csrc/``), mirroring the reference's kernel identities
+(``/root/reference/proj/include/rooflens/kernels.hpp:84-105``):
+
+* accounting -- ``scale_model``, ``gemv_model``, ``spmv_generic_model``,
+  ``spmv_csr_model``, ``stencil_model``, ``stencil_preset`` (pure host);
+* executing kernels -- ``scale``, ``spmv_csr``, ``stencil`` (+ ``*_rows`` /
+  ``*_sweep`` partial forms and ``*_host`` end-to-end forms), each with a
+  CUDA-core and a tensor-core variant selected by ``unit``;
+* hardware spec / roofline / bounds -- ``load_spec``, ``builtin_spec``,
+  ``machine_balance``, ``tensor_alpha``, ``attainable``, ``classify``,
+  ``kernel_speedup_ceiling``, ``tensor_core_ceiling``, ``workload_ceiling``,
+  ``min_temporal_depth``, ``tc_scale_trick_throughput``.
+
+Errors mirror the reference's ``rooflens::Error`` (error.hpp:36-46): a
+``RooflensError`` whose ``kind`` is the ErrorKind name and whose message is
+``"<Kind>: <msg>"``.  There is no CPU fallback: every executing call runs the
+sm_100a kernels or raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+__all__ = [
+    "CUDA_CORE", "TENSOR_CORE", "FP64", "FP32", "FP16", "RooflensError", "KernelCharacterization",
+    "HardwareSpec", "lib", "library_path", "scale_model", "gemv_model", "spmv_generic_model",
+    "spmv_csr_model", "stencil_model", "stencil_preset", "stencil_default_weights", "scale",
+    "spmv_csr", "spmv_csr_rows", "stencil", "stencil_sweep", "scale_host", "spmv_csr_host",
+    "stencil_host", "fill_uniform", "gen_band_csr", "stencil_init", "load_spec", "builtin_spec",
+    "machine_balance", "tensor_alpha", "attainable", "classify", "unoverlapped_speedup",
+    "kernel_speedup_ceiling", "tensor_core_ceiling", "workload_ceiling", "min_temporal_depth",
+    "tc_scale_trick_throughput", "fp64_peak_launch", "tuning_set", "kernel_launches",
+    "ERROR_KINDS", "EXPORTED_SYMBOLS",
+]
+
+CUDA_CORE, TENSOR_CORE = 0, 1          # ExecutionUnit (hardware.hpp:19)
+FP64, FP32, FP16 = 0, 1, 2             # Precision (hardware.hpp:21)
+MEMORY_BOUND, COMPUTE_BOUND, BALANCED = 0, 1, 2
+
+ERROR_KINDS = [
+    "MissingPeak", "ParseError", "ValidationError", "MissingField", "UnknownHardware",
+    "InvalidCount", "InvalidIndexSize", "ZeroIntensity", "InvalidAlpha", "ZeroBalance",
+    "InvalidRange", "BadBanner", "UnsupportedFormat", "MalformedEntry", "IndexOutOfRange",
+    "TruncatedFile", "IoError",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+library_path = os.path.join(_HERE, "librooflens_b200.so")
+
+
+class RooflensError(RuntimeError):
+    """Status code != 0 from the C-ABI.  ``kind`` is the reference ErrorKind
+    name (or ``"CudaError"``), ``code`` the raw status."""
+
+    def __init__(self, code: int, message: str):
+        super().__init__(message)
+        self.code = code
+        if 1 <= code <= len(ERROR_KINDS):
+            self.kind = ERROR_KINDS[code - 1]
+        elif code >= 100:
+            self.kind = "CudaError"
+        else:
+            self.kind = "Error"
+
+
+class _KChar(C.Structure):
+    _fields_ = [("work_flops", C.c_uint64), ("traffic_bytes", C.c_uint64)]
+
+
+class _HwSpec(C.Structure):
+    _fields_ = [("name", C.c_char * 64), ("memory_bandwidth", C.c_double),
+                ("l2_cache_bytes", C.c_double), ("peak_cuda_core", C.c_double),
+                ("peak_tensor_core", C.c_double)]
+
+
+@dataclass(frozen=True)
+class KernelCharacterization:
+    """Flattened ``rooflens::KernelCharacterization`` (kernels.hpp:34-44)."""
+
+    work_flops: int
+    traffic_bytes: int
+
+    @property
+    def intensity(self) -> float:
+        return self.work_flops / self.traffic_bytes
+
+
+@dataclass(frozen=True)
+class HardwareSpec:
+    """FP64 slice of ``rooflens::HardwareSpec`` (hardware.hpp:43-58), SI units."""
+
+    name: str
+    memory_bandwidth: float
+    l2_cache_bytes: float
+    peak_cuda_core: float
+    peak_tensor_core: float = 0.0
+
+    def _c(self) -> _HwSpec:
+        s = _HwSpec()
+        s.name = self.name.encode()[:63]
+        s.memory_bandwidth = self.memory_bandwidth
+        s.l2_cache_bytes = self.l2_cache_bytes
+        s.peak_cuda_core = self.peak_cuda_core
+        s.peak_tensor_core = self.peak_tensor_core
+        return s
+
+    @staticmethod
+    def _from(s: _HwSpec) -> "HardwareSpec":
+        return HardwareSpec(s.name.decode(), s.memory_bandwidth, s.l2_cache_bytes,
+                            s.peak_cuda_core, s.peak_tensor_core)
+
+
+_u64, _i64, _dbl, _int, _ptr = C.c_uint64, C.c_int64, C.c_double, C.c_int, C.c_void_p
+_KP = C.POINTER(_KChar)
+_HP = C.POINTER(_HwSpec)
+
+# name -> (restype, argtypes); exactly the symbols include/rooflens_b200.h declares.
+_SIGNATURES = {
+    "rl_last_error": (C.c_char_p, []),
+    "rl_version": (C.c_char_p, []),
+    "rl_kernel_launches": (_u64, []),
+    "rl_scale_model": (_int, [_u64, _int, _KP]),
+    "rl_gemv_model": (_int, [_u64, _u64, _int, _KP]),
+    "rl_spmv_generic_model": (_int, [_u64, _u64, _u64, _u64, _u64, _u64, _u64, _int, _KP]),
+    "rl_spmv_csr_model": (_int, [_u64, _u64, _u64, _u64, _int, _KP]),
+    "rl_stencil_model": (_int, [C.c_char_p, _int, _u64, _KP]),
+    "rl_stencil_preset": (_int, [C.c_char_p, C.POINTER(_int), C.POINTER(_u64), C.POINTER(_int)]),
+    "rl_stencil_default_weights": (_int, [C.c_char_p, C.POINTER(_dbl), _u64]),
+    "rl_scale": (_int, [_int, _int, _ptr, _ptr, _dbl, _u64, _ptr, _KP]),
+    "rl_spmv_csr": (_int, [_int, _int, _u64, _u64, _u64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _KP]),
+    "rl_spmv_csr_rows": (_int, [_int, _int, _u64, _u64, _ptr, _ptr, _ptr, _ptr, _i64, _ptr, _ptr]),
+    "rl_stencil": (_int, [_int, _int, C.c_char_p, C.POINTER(_u64), _ptr, _u64, _ptr, _ptr, _ptr, _KP]),
+    "rl_stencil_sweep": (_int, [_int, _int, C.c_char_p, C.POINTER(_u64), _ptr, _u64, _u64, _ptr,
+                                _ptr, _ptr]),
+    "rl_scale_host": (_int, [_int, _int, _ptr, _ptr, _dbl, _u64, _KP]),
+    "rl_spmv_csr_host": (_int, [_int, _int, _u64, _u64, _u64, _ptr, _ptr, _ptr, _ptr, _ptr, _KP]),
+    "rl_stencil_host": (_int, [_int, _int, C.c_char_p, C.POINTER(_u64), _ptr, _u64, _ptr, _ptr, _KP]),
+    "rl_host_workspace_release": (_int, []),
+    "rl_fill_uniform": (_int, [_ptr, _u64, _u64, _u64, _u64, _int, _ptr]),
+    "rl_gen_band_csr": (_int, [_u64, _u64, _u64, C.c_uint32, _u64, _u64, _ptr, _ptr, _ptr, _ptr]),
+    "rl_stencil_init": (_int, [_ptr, C.POINTER(_u64), _int, _u64, _u64, _int, _u64, _ptr]),
+    "rl_load_spec": (_int, [C.c_char_p, _HP]),
+    "rl_builtin_spec": (_int, [C.c_char_p, _HP]),
+    "rl_machine_balance": (_int, [_HP, _int, _int, C.POINTER(_dbl)]),
+    "rl_tensor_alpha": (_int, [_HP, _int, C.POINTER(_dbl)]),
+    "rl_attainable": (_int, [_HP, _int, _int, _dbl, C.POINTER(_dbl)]),
+    "rl_classify": (_int, [_dbl, _dbl]),
+    "rl_unoverlapped_speedup": (_int, [_dbl, _dbl, _dbl, _dbl, C.POINTER(_dbl)]),
+    "rl_kernel_speedup_ceiling": (_int, [_dbl, _dbl, _dbl, C.POINTER(_dbl), C.POINTER(_int)]),
+    "rl_tensor_core_ceiling": (_int, [_dbl, C.POINTER(_dbl)]),
+    "rl_workload_ceiling": (_int, [_dbl, _dbl, C.POINTER(_dbl)]),
+    "rl_min_temporal_depth": (_int, [_dbl, _dbl, C.POINTER(_u64)]),
+    "rl_tc_scale_trick_throughput": (_int, [_dbl, _u64, _u64, C.POINTER(_dbl)]),
+    "rl_fp64_peak_launch": (_int, [_int, _u64, _ptr, _ptr, C.POINTER(_dbl)]),
+    "rl_tuning_set": (_int, [C.c_char_p, _i64, C.POINTER(_i64)]),
+}
+EXPORTED_SYMBOLS = sorted(_SIGNATURES)
+
+_lib: Optional[C.CDLL] = None
+
+
+def lib() -> C.CDLL:
+    """Load the in-tree sm_100a library.  Raises (never falls back) if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(library_path):
+            raise ImportError(
+                f"{library_path} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                f"g.build()'` (or `make -C paper_2502_16851_b200/csrc`)")
+        L = C.CDLL(library_path)
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(code: int) -> None:
+    if code != 0:
+        msg = lib().rl_last_error().decode(errors="replace")
+        raise RooflensError(code, msg or f"status {code}")
+
+
+def _kc(k: _KChar) -> KernelCharacterization:
+    return KernelCharacterization(int(k.work_flops), int(k.traffic_bytes))
+
+
+# ----------------------------------------------------------------------------
+# tensor plumbing (torch is only the allocator/stream provider)
+# ----------------------------------------------------------------------------
+def _dev_ptr(t, dtype_name: str, what: str) -> int:
+    import torch
+
+    want = {"f64": torch.float64, "i32": torch.int32}[dtype_name]
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{what} must be a torch.Tensor")
+    if t.dtype != want:
+        raise TypeError(f"{what} must be {want}, got {t.dtype}")
+    if not t.is_cuda:
+        raise ValueError(f"{what} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{what} must be contiguous")
+    return t.data_ptr()
+
+
+def _host_ptr(a, dtype_name: str, what: str) -> int:
+    """numpy array or CPU tensor (pinned for full-speed copies)."""
+    try:
+        import torch
+
+        if isinstance(a, torch.Tensor):
+            want = {"f64": torch.float64, "i32": torch.int32}[dtype_name]
+            if a.is_cuda or a.dtype != want or not a.is_contiguous():
+                raise ValueError(f"{what} must be a contiguous CPU {want} tensor")
+            return a.data_ptr()
+    except ImportError:  # pragma: no cover
+        pass
+    import numpy as np
+
+    want = {"f64": np.float64, "i32": np.int32}[dtype_name]
+    if not isinstance(a, np.ndarray) or a.dtype != want or not a.flags["C_CONTIGUOUS"]:
+        raise ValueError(f"{what} must be a C-contiguous numpy {want.__name__} array")
+    return a.ctypes.data
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        import torch
+
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+# ----------------------------------------------------------------------------
+# accounting (kernels.cpp:74-155)
+# ----------------------------------------------------------------------------
+def scale_model(n: int, precision: int = FP64) -> KernelCharacterization:
+    k = _KChar()
+    _check(lib().rl_scale_model(n, precision, C.byref(k)))
+    return _kc(k)
+
+
+def gemv_model(m: int, n: int, precision: int = FP64) -> KernelCharacterization:
+    k = _KChar()
+    _check(lib().rl_gemv_model(m, n, precision, C.byref(k)))
+    return _kc(k)
+
+
+def spmv_generic_model(rows, cols, nnz, index_entry_count=0, index_entry_bytes=0,
+                       packed_entry_count=0, packed_entry_bytes=0, precision=FP64):
+    k = _KChar()
+    _check(lib().rl_spmv_generic_model(rows, cols, nnz, index_entry_count, index_entry_bytes,
+                                       packed_entry_count, packed_entry_bytes, precision,
+                                       C.byref(k)))
+    return _kc(k)
+
+
+def spmv_csr_model(rows: int, cols: int, nnz: int, index_bytes: int = 4,
+                   precision: int = FP64) -> KernelCharacterization:
+    k = _KChar()
+    _check(lib().rl_spmv_csr_model(rows, cols, nnz, index_bytes, precision, C.byref(k)))
+    return _kc(k)
+
+
+def stencil_model(preset: str, precision: int = FP64, temporal_depth: int = 1):
+    k = _KChar()
+    _check(lib().rl_stencil_model(preset.encode(), precision, temporal_depth, C.byref(k)))
+    return _kc(k)
+
+
+def stencil_preset(name: str):
+    """(dimensionality, point_count, radius)."""
+    d, p, r = _int(), _u64(), _int()
+    _check(lib().rl_stencil_preset(name.encode(), C.byref(d), C.byref(p), C.byref(r)))
+    return d.value, p.value, r.value
+
+
+def stencil_default_weights(name: str) -> list:
+    buf = (_dbl * 64)()
+    _check(lib().rl_stencil_default_weights(name.encode(), buf, 64))
+    return list(buf[: stencil_preset(name)[1]])
+
+
+# ----------------------------------------------------------------------------
+# executing kernels (device tensors)
+# ----------------------------------------------------------------------------
+def scale(a, b, q: float, unit: int = CUDA_CORE, stream=None, precision: int = FP64):
+    """a[i] = q * b[i] on the GPU."""
+    n = b.numel()
+    if a.numel() != n:
+        raise ValueError("a and b must have the same number of elements")
+    k = _KChar()
+    _check(lib().rl_scale(unit, precision, _dev_ptr(a, "f64", "a"), _dev_ptr(b, "f64", "b"),
+                          float(q), n, _stream(stream), C.byref(k)))
+    return _kc(k)
+
+
+def spmv_csr(row_ptr, col, val, x, y, unit: int = CUDA_CORE, stream=None, precision: int = FP64):
+    """y = A x for a CSR matrix with int32 indices."""
+    m = row_ptr.numel() - 1
+    n = x.numel()
+    nnz = val.numel()
+    if y.numel() != m or col.numel() != nnz:
+        raise ValueError("inconsistent CSR / vector sizes")
+    k = _KChar()
+    _check(lib().rl_spmv_csr(unit, precision, m, n, nnz, _dev_ptr(row_ptr, "i32", "row_ptr"),
+                             _dev_ptr(col, "i32", "col") if nnz else None,
+                             _dev_ptr(val, "f64", "val") if nnz else None,
+                             _dev_ptr(x, "f64", "x"), _dev_ptr(y, "f64", "y"), _stream(stream),
+                             C.byref(k)))
+    return _kc(k)
+
+
+def spmv_csr_rows(row_begin: int, row_end: int, row_ptr, col, val, x, y, col_base: int = 0,
+                  unit: int = CUDA_CORE, stream=None, precision: int = FP64) -> None:
+    """Rows [row_begin, row_end) of y = A x, reading x[col - col_base]."""
+    _check(lib().rl_spmv_csr_rows(unit, precision, row_begin, row_end,
+                                  _dev_ptr(row_ptr, "i32", "row_ptr"),
+                                  _dev_ptr(col, "i32", "col") if col.numel() else None,
+                                  _dev_ptr(val, "f64", "val") if val.numel() else None,
+                                  _dev_ptr(x, "f64", "x") if x.numel() else None,
+                                  col_base, _dev_ptr(y, "f64", "y"), _stream(stream)))
+
+
+def _dims(preset: str, u) -> "C.Array":
+    dim = stencil_preset(preset)[0]
+    shape = tuple(u.shape)
+    if len(shape) != dim:
+        raise ValueError(f"{preset} needs a {dim}-D field, got shape {shape}")
+    if dim == 2:
+        ny, nx = shape
+        return (_u64 * 3)(nx, ny, 1)
+    nz, ny, nx = shape
+    return (_u64 * 3)(nx, ny, nz)
+
+
+def _weights(preset: str, weights: Optional[Sequence[float]]):
+    if weights is None:
+        return None
+    npts = stencil_preset(preset)[1]
+    if len(weights) != npts:
+        raise ValueError(f"{preset} takes {npts} weights, got {len(weights)}")
+    return (_dbl * npts)(*[float(w) for w in weights])
+
+
+def stencil(preset: str, u, v, steps: int, weights=None, unit: int = CUDA_CORE, stream=None,
+            precision: int = FP64):
+    """`steps` Jacobi sweeps ping-ponging u -> v -> u ...; result in u if steps
+    is even, else in v.  Field shapes: (ny, nx) or (nz, ny, nx)."""
+    if u.shape != v.shape:
+        raise ValueError("u and v must have the same shape")
+    k = _KChar()
+    w = _weights(preset, weights)
+    _check(lib().rl_stencil(unit, precision, preset.encode(), _dims(preset, u),
+                            C.cast(w, _ptr) if w is not None else None, steps,
+                            _dev_ptr(u, "f64", "u"), _dev_ptr(v, "f64", "v"), _stream(stream),
+                            C.byref(k)))
+    return _kc(k)
+
+
+def stencil_sweep(preset: str, u, v, o_begin: int, o_end: int, weights=None,
+                  unit: int = CUDA_CORE, stream=None, precision: int = FP64) -> None:
+    """One sweep v = S(u) over outer indices [o_begin, o_end) (rows / planes)."""
+    w = _weights(preset, weights)
+    _check(lib().rl_stencil_sweep(unit, precision, preset.encode(), _dims(preset, u),
+                                  C.cast(w, _ptr) if w is not None else None, o_begin, o_end,
+                                  _dev_ptr(u, "f64", "u"), _dev_ptr(v, "f64", "v"),
+                                  _stream(stream)))
+
+
+# ----------------------------------------------------------------------------
+# end to end on host buffers
+# ----------------------------------------------------------------------------
+def scale_host(a, b, q: float, unit: int = CUDA_CORE, precision: int = FP64):
+    k = _KChar()
+    n = len(b) if not hasattr(b, "numel") else b.numel()
+    _check(lib().rl_scale_host(unit, precision, _host_ptr(a, "f64", "a"), _host_ptr(b, "f64", "b"),
+                               float(q), n, C.byref(k)))
+    return _kc(k)
+
+
+def spmv_csr_host(row_ptr, col, val, x, y, unit: int = CUDA_CORE, precision: int = FP64):
+    size = (lambda t: t.numel() if hasattr(t, "numel") else t.size)
+    m, n, nnz = size(row_ptr) - 1, size(x), size(val)
+    k = _KChar()
+    _check(lib().rl_spmv_csr_host(unit, precision, m, n, nnz, _host_ptr(row_ptr, "i32", "row_ptr"),
+                                  _host_ptr(col, "i32", "col"), _host_ptr(val, "f64", "val"),
+                                  _host_ptr(x, "f64", "x"), _host_ptr(y, "f64", "y"), C.byref(k)))
+    return _kc(k)
+
+
+def stencil_host(preset: str, u, v, steps: int, weights=None, unit: int = CUDA_CORE,
+                 precision: int = FP64):
+    k = _KChar()
+    w = _weights(preset, weights)
+    _check(lib().rl_stencil_host(unit, precision, preset.encode(), _dims(preset, u),
+                                 C.cast(w, _ptr) if w is not None else None, steps,
+                                 _host_ptr(u, "f64", "u"), _host_ptr(v, "f64", "v"), C.byref(k)))
+    return _kc(k)
+
+
+# ----------------------------------------------------------------------------
+# generators (device, bit-identical to oracle/oracle.c)
+# ----------------------------------------------------------------------------
+def fill_uniform(out, seed: int, stream_id: int, idx0: int = 0, kind: int = 0, stream=None):
+    _check(lib().rl_fill_uniform(_dev_ptr(out, "f64", "out"), out.numel(), seed, stream_id, idx0,
+                                 kind, _stream(stream)))
+
+
+def gen_band_csr(m_local: int, row0: int, n: int, k: int, hb: int, seed: int, row_ptr, col, val,
+                 stream=None):
+    _check(lib().rl_gen_band_csr(m_local, row0, n, k, hb, seed,
+                                 _dev_ptr(row_ptr, "i32", "row_ptr"), _dev_ptr(col, "i32", "col"),
+                                 _dev_ptr(val, "f64", "val"), _stream(stream)))
+
+
+def stencil_init(u, radius: int, seed: int, outer_begin: int = 0, global_shape=None,
+                 stream=None):
+    """Fill u (shape (ny, nx) or (nz, ny, nx)) with the BASELINE initial field.
+    With global_shape, u is the slab of outer indices [outer_begin,
+    outer_begin + u.shape[0]) of that global grid."""
+    gs = tuple(global_shape or u.shape)
+    dim = len(gs)
+    dims = (_u64 * 3)(gs[-1], gs[-2], gs[0] if dim == 3 else 1)
+    _check(lib().rl_stencil_init(_dev_ptr(u, "f64", "u"), dims, dim, outer_begin,
+                                 outer_begin + u.shape[0], radius, seed, _stream(stream)))
+
+
+# ----------------------------------------------------------------------------
+# hardware spec, roofline, bounds
+# ----------------------------------------------------------------------------
+def load_spec(text: str) -> HardwareSpec:
+    s = _HwSpec()
+    _check(lib().rl_load_spec(text.encode(), C.byref(s)))
+    return HardwareSpec._from(s)
+
+
+def builtin_spec(name: str) -> HardwareSpec:
+    s = _HwSpec()
+    _check(lib().rl_builtin_spec(name.encode(), C.byref(s)))
+    return HardwareSpec._from(s)
+
+
+def _d1(fn, *args) -> float:
+    out = _dbl()
+    _check(fn(*args, C.byref(out)))
+    return out.value
+
+
+def machine_balance(spec: HardwareSpec, unit: int = CUDA_CORE, precision: int = FP64) -> float:
+    s = spec._c()
+    return _d1(lib().rl_machine_balance, C.byref(s), unit, precision)
+
+
+def tensor_alpha(spec: HardwareSpec, precision: int = FP64) -> float:
+    s = spec._c()
+    return _d1(lib().rl_tensor_alpha, C.byref(s), precision)
+
+
+def attainable(spec: HardwareSpec, intensity: float, unit: int = CUDA_CORE,
+               precision: int = FP64) -> float:
+    s = spec._c()
+    return _d1(lib().rl_attainable, C.byref(s), unit, precision, float(intensity))
+
+
+def classify(intensity: float, balance: float) -> int:
+    return lib().rl_classify(float(intensity), float(balance))
+
+
+def unoverlapped_speedup(t_cmp, t_mem, t_others, alpha) -> float:
+    return _d1(lib().rl_unoverlapped_speedup, float(t_cmp), float(t_mem), float(t_others),
+               float(alpha))
+
+
+def kernel_speedup_ceiling(alpha, balance, intensity):
+    """(value, n_warnings)."""
+    out, nw = _dbl(), _int()
+    _check(lib().rl_kernel_speedup_ceiling(float(alpha), float(balance), float(intensity),
+                                           C.byref(out), C.byref(nw)))
+    return out.value, nw.value
+
+
+def tensor_core_ceiling(alpha) -> float:
+    return _d1(lib().rl_tensor_core_ceiling, float(alpha))
+
+
+def workload_ceiling(intensity, balance) -> float:
+    return _d1(lib().rl_workload_ceiling, float(intensity), float(balance))
+
+
+def min_temporal_depth(balance, single_step_intensity) -> int:
+    out = _u64()
+    _check(lib().rl_min_temporal_depth(float(balance), float(single_step_intensity), C.byref(out)))
+    return int(out.value)
+
+
+def tc_scale_trick_throughput(peak_tc, m, n) -> float:
+    return _d1(lib().rl_tc_scale_trick_throughput, float(peak_tc), int(m), int(n))
+
+
+# ----------------------------------------------------------------------------
+# microbenchmarks, knobs, evidence
+# ----------------------------------------------------------------------------
+def fp64_peak_launch(unit: int, iters: int, sink, stream=None) -> float:
+    """Launch the K11 DFMA/DMMA chain kernel; returns its exact flop count."""
+    fl = _dbl()
+    _check(lib().rl_fp64_peak_launch(unit, iters, _stream(stream), _dev_ptr(sink, "f64", "sink"),
+                                     C.byref(fl)))
+    return fl.value
+
+
+def tuning_set(key: str, value: int) -> int:
+    prev = _i64()
+    _check(lib().rl_tuning_set(key.encode(), int(value), C.byref(prev)))
+    return prev.value
+
+
+def kernel_launches() -> int:
+    return int(lib().rl_kernel_launches())

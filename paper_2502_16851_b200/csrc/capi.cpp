@@ -1,0 +1,608 @@
+// capi.cpp -- the executing C++ entry points (rooflens_b200.hpp) and the
+// extern "C" boundary (rooflens_b200.h).
+//
+// Each executing call validates its arguments the way the reference model it
+// sits behind does (same ErrorKind, same message format), launches the sm_100a
+// kernel(s) on the caller's stream, and returns the reference model's W/Q for
+// the call.  There is no CPU path: a missing/unusable device surfaces as a
+// CUDA error code (RL_ERR_CUDA_BASE + cudaError_t).
+#include <atomic>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "../../include/rooflens_b200.h"
+#include "../../include/rooflens_b200.hpp"
+#include "kernels.h"
+
+namespace rlb {
+Tuning& tuning() {
+    static Tuning t;
+    return t;
+}
+std::atomic<uint64_t> g_launches{0};
+void note_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+}  // namespace rlb
+
+namespace rooflens::b200 {
+namespace {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw CudaError(static_cast<int>(e), std::string("CudaError: ") + what + ": " +
+                                                 cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")");
+}
+
+void require_fp64(Precision p) {
+    if (p != Precision::FP64)
+        throw Error(ErrorKind::ValidationError,
+                    std::string("precision ") + (p == Precision::FP32 ? "FP32" : "FP16") +
+                        " is not supported by the B200 kernels (FP64 only)");
+}
+
+void require_ptr(const void* p, const char* what) {
+    if (!p) throw Error(ErrorKind::ValidationError, std::string(what) + " must not be null");
+}
+
+int preset_id(const std::string& n) {
+    if (n == "2d5pt") return rlb::kP2d5;
+    if (n == "2d9pt") return rlb::kP2d9;
+    if (n == "2d13pt") return rlb::kP2d13;
+    if (n == "2d49pt") return rlb::kP2d49;
+    if (n == "3d7pt") return rlb::kP3d7;
+    return rlb::kP3d27;
+}
+
+rlb::StencilDesc make_desc(const StencilShape& shape, const std::uint64_t dims[3],
+                           const double* weights) {
+    rlb::StencilDesc d{};
+    d.preset = preset_id(shape.name);
+    d.dim = shape.dimensionality;
+    d.radius = shape.radius;
+    d.npts = static_cast<int>(shape.point_count);
+    d.nx = dims[0];
+    d.ny = dims[1];
+    d.nz = shape.dimensionality == 3 ? dims[2] : 1;
+    const std::uint64_t need = 2ull * shape.radius + 1;
+    if (d.nx < need || d.ny < need || (d.dim == 3 && d.nz < need))
+        throw Error(ErrorKind::InvalidCount, "stencil: every grid extent must be >= " +
+                                                 std::to_string(need) + " for " + shape.name);
+    if (weights) {
+        std::memcpy(d.w, weights, sizeof(double) * shape.point_count);
+    } else {
+        const auto w = stencil_default_weights(shape.name);
+        std::memcpy(d.w, w.data(), sizeof(double) * w.size());
+    }
+    return d;
+}
+
+std::uint64_t interior_points(const rlb::StencilDesc& d) {
+    const std::uint64_t r2 = 2ull * d.radius;
+    std::uint64_t p = (d.nx - r2) * (d.ny - r2);
+    if (d.dim == 3) p *= (d.nz - r2);
+    return p;
+}
+
+void sweep(ExecutionUnit unit, const rlb::StencilDesc& d, std::uint64_t o0, std::uint64_t o1,
+           const double* u, double* v, cudaStream_t s) {
+    const std::uint64_t outer = d.dim == 3 ? d.nz : d.ny;
+    const std::uint64_t lo = std::max<std::uint64_t>(o0, d.radius);
+    const std::uint64_t hi = std::min<std::uint64_t>(o1, outer - d.radius);
+    if (lo >= hi) return;
+    if (unit == ExecutionUnit::TensorCore && d.preset != rlb::kP2d5 && d.preset != rlb::kP3d7 &&
+        d.preset != rlb::kP3d27)
+        throw Error(ErrorKind::ValidationError,
+                    "no tensor-core formulation for this preset (2d5pt, 3d7pt, 3d27pt only)");
+    if (unit == ExecutionUnit::TensorCore)
+        cuda_check(rlb::launch_stencil_tc(d, lo, hi, u, v, s), "stencil (tensor core)");
+    else
+        cuda_check(rlb::launch_stencil_cc(d, lo, hi, u, v, s), "stencil (cuda core)");
+}
+
+}  // namespace
+
+KernelCharacterization scale(ExecutionUnit unit, Precision p, double* a, const double* b, double q,
+                             std::uint64_t n, Stream stream) {
+    KernelCharacterization k = scale_model(n, p);
+    require_fp64(p);
+    require_ptr(a, "a");
+    require_ptr(b, "b");
+    cuda_check(rlb::launch_scale(unit == ExecutionUnit::TensorCore, a, b, q, n,
+                                 static_cast<cudaStream_t>(stream)),
+               "scale");
+    return k;
+}
+
+void spmv_csr_rows(ExecutionUnit unit, Precision p, std::uint64_t r0, std::uint64_t r1,
+                   const std::int32_t* rp, const std::int32_t* col, const double* val,
+                   const double* x, std::int64_t col_base, double* y, Stream stream) {
+    require_fp64(p);
+    if (r1 < r0) throw Error(ErrorKind::InvalidRange, "row_end < row_begin");
+    if (r1 == r0) return;
+    require_ptr(rp, "row_ptr");
+    require_ptr(y, "y");
+    cuda_check(rlb::launch_spmv(unit == ExecutionUnit::TensorCore, r0, r1, rp, col, val, x, col_base,
+                                y, 0.0, static_cast<cudaStream_t>(stream)),
+               "spmv_csr");
+}
+
+KernelCharacterization spmv_csr(ExecutionUnit unit, Precision p, const SparseMatrixStats& s,
+                                const std::int32_t* rp, const std::int32_t* col, const double* val,
+                                const double* x, double* y, Stream stream) {
+    KernelCharacterization k = spmv_csr_model(s, kDefaultIndexBytes, p);
+    require_fp64(p);
+    if (s.nnz > 0x7fffffffull || s.rows > 0x7fffffffull || s.cols > 0x7fffffffull)
+        throw Error(ErrorKind::InvalidRange, "int32 CSR indices cannot address this matrix");
+    require_ptr(col, "col");
+    require_ptr(val, "val");
+    require_ptr(x, "x");
+    spmv_csr_rows(unit, p, 0, s.rows, rp, col, val, x, 0, y, stream);
+    return k;
+}
+
+void stencil_sweep(ExecutionUnit unit, Precision p, const StencilShape& shape,
+                   const std::uint64_t dims[3], const double* weights, std::uint64_t o0,
+                   std::uint64_t o1, const double* u, double* v, Stream stream) {
+    require_fp64(p);
+    require_ptr(u, "u");
+    require_ptr(v, "v");
+    if (u == v) throw Error(ErrorKind::ValidationError, "u and v must be distinct buffers");
+    const rlb::StencilDesc d = make_desc(shape, dims, weights);
+    sweep(unit, d, o0, o1, u, v, static_cast<cudaStream_t>(stream));
+}
+
+KernelCharacterization stencil(ExecutionUnit unit, Precision p, const StencilShape& shape,
+                               const std::uint64_t dims[3], const double* weights,
+                               std::uint64_t steps, double* u, double* v, Stream stream) {
+    KernelCharacterization per_point = stencil_model(shape, p, 1);
+    require_fp64(p);
+    if (!steps) throw Error(ErrorKind::InvalidCount, "stencil: steps must be >= 1");
+    require_ptr(u, "u");
+    require_ptr(v, "v");
+    if (u == v) throw Error(ErrorKind::ValidationError, "u and v must be distinct buffers");
+    const rlb::StencilDesc d = make_desc(shape, dims, weights);
+    const unsigned __int128 pts = (unsigned __int128)interior_points(d) * steps;
+    const unsigned __int128 w = pts * per_point.work_flops, q = pts * per_point.traffic_bytes;
+    if ((w >> 64) || (q >> 64)) throw Error(ErrorKind::InvalidRange, "stencil accounting overflows 64-bit count");
+    const std::uint64_t outer = d.dim == 3 ? d.nz : d.ny;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    for (std::uint64_t t = 0; t < steps; ++t) {
+        const double* src = (t & 1) ? v : u;
+        double* dst = (t & 1) ? u : v;
+        sweep(unit, d, 0, outer, src, dst, s);
+    }
+    return {shape.name, static_cast<std::uint64_t>(w), static_cast<std::uint64_t>(q)};
+}
+
+}  // namespace rooflens::b200
+
+// ===========================================================================
+// Host-buffer end-to-end paths: cached device workspace + two streams.
+// ===========================================================================
+namespace {
+using namespace rooflens::b200;
+
+struct Workspace {
+    std::mutex mu;
+    void* buf[6] = {};
+    size_t cap[6] = {};
+    cudaStream_t h2d = nullptr, comp = nullptr;
+    cudaEvent_t ev[64] = {};
+
+    void* get(int i, size_t bytes) {
+        if (cap[i] < bytes) {
+            if (buf[i]) cudaFree(buf[i]);
+            buf[i] = nullptr;
+            cap[i] = 0;
+            if (cudaMalloc(&buf[i], bytes) != cudaSuccess) {
+                cudaGetLastError();
+                throw CudaError(cudaErrorMemoryAllocation, "CudaError: workspace allocation failed");
+            }
+            cap[i] = bytes;
+        }
+        return buf[i];
+    }
+    void streams() {
+        if (!h2d) {
+            cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking);
+            cudaStreamCreateWithFlags(&comp, cudaStreamNonBlocking);
+            for (auto& e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        }
+    }
+    void release() {
+        for (int i = 0; i < 6; ++i) {
+            if (buf[i]) cudaFree(buf[i]);
+            buf[i] = nullptr;
+            cap[i] = 0;
+        }
+        if (h2d) {
+            cudaStreamDestroy(h2d);
+            cudaStreamDestroy(comp);
+            for (auto& e : ev) cudaEventDestroy(e);
+            h2d = comp = nullptr;
+        }
+    }
+};
+Workspace& ws() {
+    static Workspace w;
+    return w;
+}
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw CudaError(static_cast<int>(e), std::string("CudaError: ") + what + ": " + cudaGetErrorName(e));
+}
+
+constexpr uint64_t kChunk = 4ull << 20;  // doubles per pipelined chunk (32 MiB)
+
+KernelCharacterization scale_host(ExecutionUnit unit, Precision p, double* a, const double* b, double q,
+                                  uint64_t n) {
+    KernelCharacterization k = scale_model(n, p);
+    require_fp64(p);
+    require_ptr(a, "a");
+    require_ptr(b, "b");
+    Workspace& w = ws();
+    std::lock_guard<std::mutex> lock(w.mu);
+    w.streams();
+    double* db = static_cast<double*>(w.get(0, n * 8));
+    double* da = static_cast<double*>(w.get(1, n * 8));
+    const uint64_t nch = (n + kChunk - 1) / kChunk;
+    for (uint64_t c = 0; c < nch; ++c) {
+        const uint64_t o = c * kChunk, len = std::min(kChunk, n - o);
+        cudaEvent_t e = w.ev[c % 64];
+        ck(cudaMemcpyAsync(db + o, b + o, len * 8, cudaMemcpyHostToDevice, w.h2d), "H2D");
+        ck(cudaEventRecord(e, w.h2d), "event");
+        ck(cudaStreamWaitEvent(w.comp, e, 0), "wait");
+        scale(unit, p, da + o, db + o, q, len, w.comp);
+        ck(cudaMemcpyAsync(a + o, da + o, len * 8, cudaMemcpyDeviceToHost, w.comp), "D2H");
+    }
+    ck(cudaStreamSynchronize(w.comp), "sync");
+    return k;
+}
+
+KernelCharacterization spmv_host(ExecutionUnit unit, Precision p, uint64_t m, uint64_t n, uint64_t nnz,
+                                 const int32_t* rp, const int32_t* col, const double* val,
+                                 const double* x, double* y) {
+    KernelCharacterization k = spmv_csr_model({m, n, nnz}, kDefaultIndexBytes, p);
+    require_fp64(p);
+    require_ptr(rp, "row_ptr");
+    require_ptr(col, "col");
+    require_ptr(val, "val");
+    require_ptr(x, "x");
+    require_ptr(y, "y");
+    if (nnz > 0x7fffffffull || m > 0x7fffffffull)
+        throw Error(ErrorKind::InvalidRange, "int32 CSR indices cannot address this matrix");
+    Workspace& w = ws();
+    std::lock_guard<std::mutex> lock(w.mu);
+    w.streams();
+    int32_t* drp = static_cast<int32_t*>(w.get(0, (m + 1) * 4));
+    int32_t* dcol = static_cast<int32_t*>(w.get(1, nnz * 4));
+    double* dval = static_cast<double*>(w.get(2, nnz * 8));
+    double* dx = static_cast<double*>(w.get(3, n * 8));
+    double* dy = static_cast<double*>(w.get(4, m * 8));
+    ck(cudaMemcpyAsync(dx, x, n * 8, cudaMemcpyHostToDevice, w.h2d), "H2D x");
+    ck(cudaMemcpyAsync(drp, rp, (m + 1) * 4, cudaMemcpyHostToDevice, w.h2d), "H2D row_ptr");
+    // Row chunks of ~kChunk nonzeros: copy col/val of the chunk, run its rows,
+    // return its y while the next chunk is in flight.
+    const uint64_t rows_per_chunk = std::max<uint64_t>(1, (uint64_t)((double)kChunk * m / (double)nnz));
+    int c = 0;
+    for (uint64_t r0 = 0; r0 < m; r0 += rows_per_chunk, ++c) {
+        const uint64_t r1 = std::min(m, r0 + rows_per_chunk);
+        const uint64_t k0 = (uint64_t)rp[r0], k1 = (uint64_t)rp[r1];
+        if (k1 > k0) {
+            ck(cudaMemcpyAsync(dcol + k0, col + k0, (k1 - k0) * 4, cudaMemcpyHostToDevice, w.h2d), "H2D col");
+            ck(cudaMemcpyAsync(dval + k0, val + k0, (k1 - k0) * 8, cudaMemcpyHostToDevice, w.h2d), "H2D val");
+        }
+        cudaEvent_t e = w.ev[c % 64];
+        ck(cudaEventRecord(e, w.h2d), "event");
+        ck(cudaStreamWaitEvent(w.comp, e, 0), "wait");
+        spmv_csr_rows(unit, p, r0, r1, drp, dcol, dval, dx, 0, dy, w.comp);
+        ck(cudaMemcpyAsync(y + r0, dy + r0, (r1 - r0) * 8, cudaMemcpyDeviceToHost, w.comp), "D2H y");
+    }
+    ck(cudaStreamSynchronize(w.comp), "sync");
+    return k;
+}
+
+KernelCharacterization stencil_host(ExecutionUnit unit, Precision p, const char* preset,
+                                    const uint64_t* dims, const double* weights, uint64_t steps,
+                                    double* u, double* v) {
+    require_ptr(preset, "preset");
+    require_ptr(dims, "dims");
+    const StencilShape& shape = stencil_preset(preset);
+    require_ptr(u, "u");
+    require_ptr(v, "v");
+    const uint64_t n = dims[0] * dims[1] * (shape.dimensionality == 3 ? dims[2] : 1);
+    Workspace& w = ws();
+    std::lock_guard<std::mutex> lock(w.mu);
+    w.streams();
+    double* du = static_cast<double*>(w.get(0, n * 8));
+    double* dv = static_cast<double*>(w.get(1, n * 8));
+    ck(cudaMemcpyAsync(du, u, n * 8, cudaMemcpyHostToDevice, w.comp), "H2D u");
+    // v's Dirichlet ring must equal u's (contract): replicate on the device.
+    ck(cudaMemcpyAsync(dv, du, n * 8, cudaMemcpyDeviceToDevice, w.comp), "D2D v");
+    KernelCharacterization k = stencil(unit, p, shape, dims, weights, steps, du, dv, w.comp);
+    double* res_host = (steps & 1) ? v : u;
+    const double* res_dev = (steps & 1) ? dv : du;
+    ck(cudaMemcpyAsync(res_host, res_dev, n * 8, cudaMemcpyDeviceToHost, w.comp), "D2H result");
+    ck(cudaStreamSynchronize(w.comp), "sync");
+    return k;
+}
+
+// ---------------------------------------------------------------------------
+// Error plumbing
+// ---------------------------------------------------------------------------
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        g_last_error.clear();
+        return RL_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return RL_ERR_KIND_BASE + static_cast<int>(e.kind());
+    } catch (const CudaError& e) {
+        g_last_error = e.what();
+        return RL_ERR_CUDA_BASE + e.code();
+    } catch (const std::bad_alloc&) {
+        g_last_error = "CudaError: host allocation failed";
+        return RL_ERR_CUDA_BASE + 2;
+    } catch (const std::exception& e) {
+        g_last_error = std::string("ValidationError: ") + e.what();
+        return RL_ERR_KIND_BASE + static_cast<int>(ErrorKind::ValidationError);
+    }
+}
+
+void put(rl_kchar* out, const KernelCharacterization& k) {
+    if (out) {
+        out->work_flops = k.work_flops;
+        out->traffic_bytes = k.traffic_bytes;
+    }
+}
+
+ExecutionUnit unit_of(rl_unit u) {
+    if (u != RL_CUDA_CORE && u != RL_TENSOR_CORE)
+        throw Error(ErrorKind::ValidationError, "unknown execution unit " + std::to_string((int)u));
+    return static_cast<ExecutionUnit>(u);
+}
+Precision prec_of(rl_precision p) {
+    if (p != RL_FP64 && p != RL_FP32 && p != RL_FP16)
+        throw Error(ErrorKind::ValidationError, "unknown precision " + std::to_string((int)p));
+    return static_cast<Precision>(p);
+}
+const StencilShape& shape_of(const char* preset) {
+    if (!preset) throw Error(ErrorKind::ValidationError, "preset must not be null");
+    return stencil_preset(preset);
+}
+HardwareSpec spec_of(const rl_hw_spec* s) {
+    require_ptr(s, "spec");
+    HardwareSpec h;
+    h.name = std::string(s->name, strnlen(s->name, sizeof s->name));
+    h.memory_bandwidth = s->memory_bandwidth;
+    h.l2_cache_bytes = s->l2_cache_bytes;
+    h.peak_cuda_core = s->peak_cuda_core;
+    h.peak_tensor_core = s->peak_tensor_core;
+    return h;
+}
+void spec_out(rl_hw_spec* o, const HardwareSpec& h) {
+    require_ptr(o, "out");
+    std::memset(o, 0, sizeof *o);
+    std::strncpy(o->name, h.name.c_str(), sizeof o->name - 1);
+    o->memory_bandwidth = h.memory_bandwidth;
+    o->l2_cache_bytes = h.l2_cache_bytes;
+    o->peak_cuda_core = h.peak_cuda_core;
+    o->peak_tensor_core = h.peak_tensor_core;
+}
+}  // namespace
+
+// ===========================================================================
+// extern "C"
+// ===========================================================================
+extern "C" {
+
+const char* rl_last_error(void) { return g_last_error.c_str(); }
+const char* rl_version(void) { return "rooflens-b200 0.1.0 (sm_100a)"; }
+uint64_t rl_kernel_launches(void) { return rlb::g_launches.load(); }
+
+int rl_scale_model(uint64_t n, rl_precision p, rl_kchar* out) {
+    return guarded([&] { put(out, scale_model(n, prec_of(p))); });
+}
+int rl_gemv_model(uint64_t m, uint64_t n, rl_precision p, rl_kchar* out) {
+    return guarded([&] { put(out, gemv_model(m, n, prec_of(p))); });
+}
+int rl_spmv_generic_model(uint64_t rows, uint64_t cols, uint64_t nnz, uint64_t ic, uint64_t ib,
+                          uint64_t pc, uint64_t pb, rl_precision p, rl_kchar* out) {
+    return guarded([&] { put(out, spmv_generic_model({rows, cols, nnz}, {ic, ib, pc, pb}, prec_of(p))); });
+}
+int rl_spmv_csr_model(uint64_t rows, uint64_t cols, uint64_t nnz, uint64_t ib, rl_precision p,
+                      rl_kchar* out) {
+    return guarded([&] { put(out, spmv_csr_model({rows, cols, nnz}, ib, prec_of(p))); });
+}
+int rl_stencil_model(const char* preset, rl_precision p, uint64_t t, rl_kchar* out) {
+    return guarded([&] { put(out, stencil_model(shape_of(preset), prec_of(p), t)); });
+}
+int rl_stencil_preset(const char* name, int* dim, uint64_t* points, int* radius) {
+    return guarded([&] {
+        const StencilShape& s = shape_of(name);
+        if (dim) *dim = s.dimensionality;
+        if (points) *points = s.point_count;
+        if (radius) *radius = s.radius;
+    });
+}
+int rl_stencil_default_weights(const char* name, double* w, uint64_t cap) {
+    return guarded([&] {
+        const auto v = stencil_default_weights(shape_of(name).name);
+        if (cap < v.size()) throw Error(ErrorKind::InvalidCount, "weights capacity too small");
+        require_ptr(w, "weights");
+        std::memcpy(w, v.data(), v.size() * sizeof(double));
+    });
+}
+
+int rl_scale(rl_unit u, rl_precision p, double* a, const double* b, double q, uint64_t n,
+             rl_stream s, rl_kchar* out) {
+    return guarded([&] { put(out, rooflens::b200::scale(unit_of(u), prec_of(p), a, b, q, n, s)); });
+}
+int rl_spmv_csr(rl_unit u, rl_precision p, uint64_t m, uint64_t n, uint64_t nnz, const int32_t* rp,
+                const int32_t* col, const double* val, const double* x, double* y, rl_stream s,
+                rl_kchar* out) {
+    return guarded([&] {
+        put(out, rooflens::b200::spmv_csr(unit_of(u), prec_of(p), {m, n, nnz}, rp, col, val, x, y, s));
+    });
+}
+int rl_spmv_csr_rows(rl_unit u, rl_precision p, uint64_t r0, uint64_t r1, const int32_t* rp,
+                     const int32_t* col, const double* val, const double* x, int64_t col_base,
+                     double* y, rl_stream s) {
+    return guarded([&] {
+        rooflens::b200::spmv_csr_rows(unit_of(u), prec_of(p), r0, r1, rp, col, val, x, col_base, y, s);
+    });
+}
+int rl_stencil(rl_unit u, rl_precision p, const char* preset, const uint64_t* dims,
+               const double* weights, uint64_t steps, double* uu, double* v, rl_stream s,
+               rl_kchar* out) {
+    return guarded([&] {
+        require_ptr(dims, "dims");
+        put(out, rooflens::b200::stencil(unit_of(u), prec_of(p), shape_of(preset), dims, weights,
+                                         steps, uu, v, s));
+    });
+}
+int rl_stencil_sweep(rl_unit u, rl_precision p, const char* preset, const uint64_t* dims,
+                     const double* weights, uint64_t o0, uint64_t o1, const double* uu, double* v,
+                     rl_stream s) {
+    return guarded([&] {
+        require_ptr(dims, "dims");
+        rooflens::b200::stencil_sweep(unit_of(u), prec_of(p), shape_of(preset), dims, weights, o0,
+                                      o1, uu, v, s);
+    });
+}
+
+int rl_scale_host(rl_unit u, rl_precision p, double* a, const double* b, double q, uint64_t n,
+                  rl_kchar* out) {
+    return guarded([&] { put(out, scale_host(unit_of(u), prec_of(p), a, b, q, n)); });
+}
+int rl_spmv_csr_host(rl_unit u, rl_precision p, uint64_t m, uint64_t n, uint64_t nnz,
+                     const int32_t* rp, const int32_t* col, const double* val, const double* x,
+                     double* y, rl_kchar* out) {
+    return guarded([&] { put(out, spmv_host(unit_of(u), prec_of(p), m, n, nnz, rp, col, val, x, y)); });
+}
+int rl_stencil_host(rl_unit u, rl_precision p, const char* preset, const uint64_t* dims,
+                    const double* weights, uint64_t steps, double* uu, double* v, rl_kchar* out) {
+    return guarded([&] {
+        put(out, stencil_host(unit_of(u), prec_of(p), preset, dims, weights, steps, uu, v));
+    });
+}
+int rl_host_workspace_release(void) {
+    return guarded([&] {
+        std::lock_guard<std::mutex> lock(ws().mu);
+        ws().release();
+    });
+}
+
+int rl_fill_uniform(double* out, uint64_t n, uint64_t seed, uint64_t sid, uint64_t idx0, int kind,
+                    rl_stream s) {
+    return guarded([&] {
+        require_ptr(out, "out");
+        ck(rlb::launch_fill_uniform(out, n, seed, sid, idx0, kind, static_cast<cudaStream_t>(s)),
+           "fill_uniform");
+    });
+}
+int rl_gen_band_csr(uint64_t m_local, uint64_t row0, uint64_t n, uint32_t k, uint64_t hb,
+                    uint64_t seed, int32_t* rp, int32_t* col, double* val, rl_stream s) {
+    return guarded([&] {
+        if (k == 0 || k > 64 || n < k || hb + 1 < k)
+            throw Error(ErrorKind::InvalidCount, "gen_band_csr: need 1 <= k <= 64, k <= n, k <= 2*hb+1");
+        if ((unsigned __int128)(row0 + m_local) * k > 0x7fffffffull)
+            throw Error(ErrorKind::InvalidRange, "gen_band_csr: nnz exceeds int32");
+        require_ptr(rp, "row_ptr");
+        ck(rlb::launch_gen_band_csr(m_local, row0, n, k, hb, seed, rp, col, val,
+                                    static_cast<cudaStream_t>(s)),
+           "gen_band_csr");
+    });
+}
+int rl_stencil_init(double* u, const uint64_t* dims, int dim, uint64_t o0, uint64_t o1,
+                    int radius, uint64_t seed, rl_stream s) {
+    return guarded([&] {
+        require_ptr(u, "u");
+        require_ptr(dims, "dims");
+        if (dim != 2 && dim != 3) throw Error(ErrorKind::ValidationError, "dim must be 2 or 3");
+        const uint64_t outer = dim == 2 ? dims[1] : dims[2];
+        if (o1 < o0 || o1 > outer) throw Error(ErrorKind::InvalidRange, "outer range outside the grid");
+        ck(rlb::launch_stencil_init(u, dims[0], dims[1], dim == 3 ? dims[2] : 1, dim, o0, o1, radius,
+                                    seed, static_cast<cudaStream_t>(s)),
+           "stencil_init");
+    });
+}
+
+int rl_load_spec(const char* text, rl_hw_spec* out) {
+    return guarded([&] {
+        require_ptr(text, "json_text");
+        spec_out(out, load_spec(text));
+    });
+}
+int rl_builtin_spec(const char* name, rl_hw_spec* out) {
+    return guarded([&] {
+        require_ptr(name, "name");
+        spec_out(out, builtin_spec(name));
+    });
+}
+int rl_machine_balance(const rl_hw_spec* s, rl_unit u, rl_precision p, double* out) {
+    return guarded([&] { *out = machine_balance(spec_of(s), unit_of(u), prec_of(p)); });
+}
+int rl_tensor_alpha(const rl_hw_spec* s, rl_precision p, double* out) {
+    return guarded([&] { *out = tensor_alpha(spec_of(s), prec_of(p)); });
+}
+int rl_attainable(const rl_hw_spec* s, rl_unit u, rl_precision p, double i, double* out) {
+    return guarded([&] { *out = attainable(spec_of(s), unit_of(u), prec_of(p), i); });
+}
+int rl_classify(double i, double b) { return static_cast<int>(classify(i, b)); }
+int rl_unoverlapped_speedup(double tc, double tm, double to, double a, double* out) {
+    return guarded([&] { *out = unoverlapped_speedup(tc, tm, to, a); });
+}
+int rl_kernel_speedup_ceiling(double a, double b, double i, double* out, int* nw) {
+    return guarded([&] { *out = kernel_speedup_ceiling(a, b, i, nw); });
+}
+int rl_tensor_core_ceiling(double a, double* out) {
+    return guarded([&] { *out = tensor_core_ceiling(a); });
+}
+int rl_workload_ceiling(double i, double b, double* out) {
+    return guarded([&] { *out = workload_ceiling(i, b); });
+}
+int rl_min_temporal_depth(double b, double i, uint64_t* out) {
+    return guarded([&] { *out = min_temporal_depth(b, i); });
+}
+int rl_tc_scale_trick_throughput(double p, uint64_t m, uint64_t n, double* out) {
+    return guarded([&] { *out = tc_scale_trick_throughput(p, m, n); });
+}
+
+int rl_fp64_peak_launch(rl_unit u, uint64_t iters, rl_stream s, double* sink, double* flops) {
+    return guarded([&] {
+        require_ptr(sink, "sink");
+        require_ptr(flops, "flops_out");
+        ck(rlb::launch_fp64_peak(unit_of(u) == ExecutionUnit::TensorCore, iters, sink, flops,
+                                 static_cast<cudaStream_t>(s)),
+           "fp64_peak");
+    });
+}
+
+int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
+    return guarded([&] {
+        require_ptr(key, "key");
+        rlb::Tuning& t = rlb::tuning();
+        int* slot = nullptr;
+        const std::string k(key);
+        if (k == "scale_blocks_per_sm") slot = &t.scale_blocks_per_sm;
+        else if (k == "spmv_rows") slot = &t.spmv_rows;
+        else if (k == "spmv_blocks_per_sm") slot = &t.spmv_blocks_per_sm;
+        else if (k == "stencil2d_rows") slot = &t.stencil2d_rows;
+        else if (k == "stencil3d_zchunk") slot = &t.stencil3d_zchunk;
+        else if (k == "tc_stencil_zchunk") slot = &t.tc_stencil_zchunk;
+        else throw Error(ErrorKind::ValidationError, "unknown tuning key '" + k + "'");
+        if (previous) *previous = *slot;
+        if (value <= 0) throw Error(ErrorKind::InvalidRange, "tuning values must be > 0");
+        *slot = static_cast<int>(value);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,63 @@
+// kernels.h -- host-side launch interface of the sm_100a kernels (internal).
+// The C-ABI (capi.cpp) validates arguments, then calls these.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rlb {
+
+// Kernel-variant knobs, settable through rl_tuning_set() for sweeps.
+struct Tuning {
+    int scale_blocks_per_sm = 8;   // STREAM grid = 148 * this
+    int scale_threads = 256;
+    int spmv_group = 0;            // lanes per row; 0 = auto from nnz/m
+    int spmv_rows = 4;             // rows per lane group per iteration (1, 2, 4)
+    int spmv_blocks_per_sm = 8;
+    int stencil2d_rows = 256;      // rows marched per warp (2D CC)
+    int stencil2d_variant = 0;     // 0 = register-streaming CC
+    int stencil3d_zchunk = 64;     // planes marched per CTA (3D)
+    int stencil3d_ty = 8;          // tile rows (3D)
+    int tc_stencil_zchunk = 32;
+};
+Tuning& tuning();
+
+struct StencilDesc {
+    int preset;          // see StencilPreset
+    int dim;             // 2 or 3
+    int radius;
+    int npts;
+    uint64_t nx, ny, nz; // nz = 1 for 2D
+    double w[49];        // canonical offset order
+};
+
+enum StencilPreset : int {
+    kP2d5 = 0, kP2d9 = 1, kP2d13 = 2, kP2d49 = 3, kP3d7 = 4, kP3d27 = 5
+};
+
+cudaError_t launch_scale(int unit, double* a, const double* b, double q, uint64_t n,
+                         cudaStream_t s);
+cudaError_t launch_spmv(int unit, uint64_t r0, uint64_t r1, const int* rp, const int* col,
+                        const double* val, const double* x, int64_t col_base, double* y,
+                        double avg_nnz_per_row, cudaStream_t s);
+// One sweep over outer indices [o0, o1) (already clipped to the interior).
+cudaError_t launch_stencil_cc(const StencilDesc& d, uint64_t o0, uint64_t o1, const double* u,
+                              double* v, cudaStream_t s);
+cudaError_t launch_stencil_tc(const StencilDesc& d, uint64_t o0, uint64_t o1, const double* u,
+                              double* v, cudaStream_t s);
+
+// Launch accounting (rl_kernel_launches): every <<<>>> site reports itself.
+void note_launch(uint64_t n = 1);
+
+cudaError_t launch_fill_uniform(double* out, uint64_t n, uint64_t seed, uint64_t stream_id,
+                                uint64_t idx0, int kind, cudaStream_t s);
+cudaError_t launch_gen_band_csr(uint64_t m_local, uint64_t row0, uint64_t n, uint32_t k,
+                                uint64_t hb, uint64_t seed, int* rp, int* col, double* val,
+                                cudaStream_t s);
+cudaError_t launch_stencil_init(double* u, uint64_t nx, uint64_t ny, uint64_t nz, int dim,
+                                uint64_t outer_begin, uint64_t outer_end, int radius,
+                                uint64_t seed, cudaStream_t s);
+cudaError_t launch_fp64_peak(int unit, uint64_t iters, double* sink, double* flops,
+                             cudaStream_t s);
+
+}  // namespace rlb

@@ -1,0 +1,350 @@
+// models.cpp -- host-side accounting, hardware spec, roofline and speedup
+// bounds of the B200 framework.  Restates the reference's documented models
+// (they are the byte/flop accounting the kernels are judged against) in new
+// code; tests/test_accounting.py pins every value against the reference
+// library itself (oracle/_ref).
+//
+//   scale / gemv / spmv / stencil models   reference kernels.cpp:74-155
+//   presets                                reference kernels.cpp:54-68
+//   HardwareSpec, load_spec, built-ins     reference hardware.cpp:81-237
+//   attainable / classify                  reference roofline.cpp:21-34
+//   bounds                                 reference bounds.cpp:56-135
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <numeric>
+
+#include <json.hpp>
+
+#include "../../include/rooflens_b200.hpp"
+
+namespace rooflens::b200 {
+
+namespace {
+using u128 = unsigned __int128;
+
+std::uint64_t checked(u128 v, const char* what) {
+    if (v >> 64) throw Error(ErrorKind::InvalidRange, std::string(what) + " overflows 64-bit count");
+    return static_cast<std::uint64_t>(v);
+}
+
+bool is_width(std::uint64_t b) { return b == 1 || b == 2 || b == 4 || b == 8; }
+
+void require_width(std::uint64_t b, bool zero_ok, const char* what) {
+    if ((zero_ok && b == 0) || is_width(b)) return;
+    throw Error(ErrorKind::InvalidIndexSize, std::string(what) + " must be one of {" +
+                                                 (zero_ok ? "0," : "") + "1,2,4,8}, got " +
+                                                 std::to_string(b));
+}
+
+constexpr double kTera = 1e12, kMega = 1e6;
+}  // namespace
+
+const char* to_string(ErrorKind k) {
+    static const char* names[] = {
+        "MissingPeak", "ParseError", "ValidationError", "MissingField", "UnknownHardware",
+        "InvalidCount", "InvalidIndexSize", "ZeroIntensity", "InvalidAlpha", "ZeroBalance",
+        "InvalidRange", "BadBanner", "UnsupportedFormat", "MalformedEntry", "IndexOutOfRange",
+        "TruncatedFile", "IoError"};
+    const int i = static_cast<int>(k);
+    return (i >= 0 && i < 17) ? names[i] : "Error";
+}
+
+std::size_t element_bytes(Precision p) {
+    return p == Precision::FP64 ? 8 : p == Precision::FP32 ? 4 : 2;
+}
+
+// ---------------------------------------------------------------------------
+// Problem descriptors
+// ---------------------------------------------------------------------------
+void SparseMatrixStats::validate() const {
+    if (!rows || !cols) throw Error(ErrorKind::ValidationError, "matrix dimensions must be >= 1");
+    if (!nnz) throw Error(ErrorKind::ValidationError, "nnz must be >= 1");
+    if (u128(nnz) > u128(rows) * cols)
+        throw Error(ErrorKind::ValidationError, "nnz " + std::to_string(nnz) + " exceeds rows*cols");
+}
+
+void SparseMetadataTraffic::validate() const {
+    require_width(index_entry_bytes, true, "index_entry_bytes");
+    require_width(packed_entry_bytes, true, "packed_entry_bytes");
+}
+
+const std::vector<StencilShape>& stencil_presets() {
+    static const std::vector<StencilShape> all = {
+        {"2d5pt", 2, 5, 1},   {"2d9pt", 2, 9, 1}, {"2d13pt", 2, 13, 3},
+        {"2d49pt", 2, 49, 3}, {"3d7pt", 3, 7, 1}, {"3d27pt", 3, 27, 1},
+    };
+    return all;
+}
+
+const StencilShape& stencil_preset(std::string_view name) {
+    const auto& all = stencil_presets();
+    auto it = std::find_if(all.begin(), all.end(), [&](const StencilShape& s) { return s.name == name; });
+    if (it == all.end())
+        throw Error(ErrorKind::ValidationError, "unknown stencil preset '" + std::string(name) + "'");
+    return *it;
+}
+
+std::vector<double> stencil_default_weights(std::string_view name) {
+    const StencilShape& s = stencil_preset(name);
+    if (s.name == "2d5pt") return {0.5, 0.125, 0.125, 0.125, 0.125};
+    if (s.name == "3d7pt") return {0.4, 0.1, 0.1, 0.1, 0.1, 0.1, 0.1};
+    // raw = 1/(1 + |dx|+|dy|+|dz|) in canonical offset order, normalised by its sum.
+    std::vector<int> manhattan;
+    if (s.name == "3d27pt") {
+        for (int dz = -1; dz <= 1; ++dz)
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) manhattan.push_back(std::abs(dz) + std::abs(dy) + std::abs(dx));
+    } else if (s.name == "2d13pt") {
+        manhattan.push_back(0);
+        for (int d = 1; d <= 3; ++d)
+            for (int k = 0; k < 4; ++k) manhattan.push_back(d);
+    } else {
+        const int r = s.radius;
+        for (int dy = -r; dy <= r; ++dy)
+            for (int dx = -r; dx <= r; ++dx) manhattan.push_back(std::abs(dy) + std::abs(dx));
+    }
+    std::vector<double> w(manhattan.size());
+    double sum = 0.0;
+    for (std::size_t i = 0; i < w.size(); ++i) {
+        w[i] = 1.0 / double(1 + manhattan[i]);
+        sum = sum + w[i];
+    }
+    for (double& x : w) x = x / sum;
+    return w;
+}
+
+// ---------------------------------------------------------------------------
+// Models
+// ---------------------------------------------------------------------------
+KernelCharacterization scale_model(std::uint64_t n, Precision p) {
+    if (!n) throw Error(ErrorKind::InvalidCount, "scale: n_elements must be >= 1");
+    return {"scale", n, checked(u128(n) * 2 * element_bytes(p), "scale traffic")};
+}
+
+KernelCharacterization gemv_model(std::uint64_t m, std::uint64_t n, Precision p) {
+    if (!m || !n) throw Error(ErrorKind::InvalidCount, "gemv: m and n must be >= 1");
+    const u128 mn = u128(m) * n;
+    return {"gemv", checked(mn * 2, "gemv work"),
+            checked((mn + m + n) * element_bytes(p), "gemv traffic")};
+}
+
+KernelCharacterization spmv_generic_model(const SparseMatrixStats& s,
+                                          const SparseMetadataTraffic& meta, Precision p) {
+    s.validate();
+    meta.validate();
+    const u128 dense = (u128(s.nnz) + s.rows + s.cols) * element_bytes(p);
+    const u128 idx = u128(meta.index_entry_count) * meta.index_entry_bytes;
+    const u128 packed = u128(meta.packed_entry_count) * meta.packed_entry_bytes;
+    return {"spmv", checked(u128(s.nnz) * 2, "spmv work"), checked(dense + idx + packed, "spmv traffic")};
+}
+
+KernelCharacterization spmv_csr_model(const SparseMatrixStats& s, std::uint64_t index_bytes,
+                                      Precision p) {
+    s.validate();
+    require_width(index_bytes, false, "csr index_bytes");
+    SparseMetadataTraffic meta;
+    meta.index_entry_count = checked(u128(s.nnz) + s.rows + 1, "csr index count");
+    meta.index_entry_bytes = index_bytes;
+    KernelCharacterization k = spmv_generic_model(s, meta, p);
+    k.kernel_name = "spmv-csr";
+    return k;
+}
+
+KernelCharacterization stencil_model(const StencilShape& shape, Precision p, std::uint64_t t) {
+    if (!t) throw Error(ErrorKind::InvalidCount, "stencil: temporal depth must be >= 1");
+    if (!shape.point_count) throw Error(ErrorKind::InvalidCount, "stencil: point count must be >= 1");
+    return {shape.name.empty() ? "stencil" : shape.name,
+            checked(u128(t) * 2 * shape.point_count, "stencil work"), 2 * element_bytes(p)};
+}
+
+// ---------------------------------------------------------------------------
+// Hardware spec
+// ---------------------------------------------------------------------------
+double HardwareSpec::peak(ExecutionUnit u, Precision p) const {
+    const double v = (p != Precision::FP64) ? 0.0
+                     : (u == ExecutionUnit::CudaCore ? peak_cuda_core : peak_tensor_core);
+    if (!(v > 0.0))
+        throw Error(ErrorKind::MissingPeak, "'" + name + "' has no " +
+                                                (u == ExecutionUnit::CudaCore ? "CudaCore" : "TensorCore") +
+                                                " peak at " +
+                                                (p == Precision::FP64 ? "FP64" : p == Precision::FP32 ? "FP32" : "FP16"));
+    return v;
+}
+
+void HardwareSpec::validate() const {
+    if (name.empty()) throw Error(ErrorKind::ValidationError, "spec name is empty");
+    if (!(memory_bandwidth > 0.0))
+        throw Error(ErrorKind::ValidationError, "'" + name + "': memory_bandwidth must be > 0");
+    if (l2_cache_bytes < 0.0)
+        throw Error(ErrorKind::ValidationError, "'" + name + "': l2_cache_bytes must be >= 0");
+}
+
+namespace {
+// Full (unit, precision) peak table used while validating a document.
+using PeakTable = std::map<std::pair<int, int>, double>;
+
+void validate_peaks(const std::string& name, const PeakTable& peaks) {
+    if (peaks.empty()) throw Error(ErrorKind::ValidationError, "'" + name + "': peaks table is empty");
+    static const char* units[] = {"CudaCore", "TensorCore"};
+    static const char* precs[] = {"FP64", "FP32", "FP16"};
+    for (const auto& [key, v] : peaks) {
+        if (!(v > 0.0))
+            throw Error(ErrorKind::ValidationError, "'" + name + "': peak for " + units[key.first] +
+                                                        " " + precs[key.second] + " must be > 0");
+        if (key.first == 1 && !peaks.count({0, key.second}))
+            throw Error(ErrorKind::ValidationError, "'" + name + "': TensorCore peak at " +
+                                                        precs[key.second] + " has no CudaCore counterpart");
+    }
+}
+
+double number_field(const nlohmann::json& j, const std::string& key) {
+    if (!j.is_number()) throw Error(ErrorKind::ParseError, "'" + key + "' must be a number");
+    return j.get<double>();
+}
+
+void only_keys(const nlohmann::json& obj, std::initializer_list<std::string_view> allowed,
+               const std::string& where) {
+    for (auto it = obj.begin(); it != obj.end(); ++it)
+        if (std::find(allowed.begin(), allowed.end(), it.key()) == allowed.end())
+            throw Error(ErrorKind::ParseError, "unknown key '" + it.key() + "' in " + where);
+}
+
+int precision_index(std::string key) {
+    std::transform(key.begin(), key.end(), key.begin(), [](unsigned char c) { return std::tolower(c); });
+    if (key == "fp64") return 0;
+    if (key == "fp32") return 1;
+    if (key == "fp16") return 2;
+    return -1;
+}
+}  // namespace
+
+HardwareSpec load_spec(const std::string& text) {
+    nlohmann::json doc;
+    try {
+        doc = nlohmann::json::parse(text);
+    } catch (const nlohmann::json::exception& e) {
+        throw Error(ErrorKind::ParseError, e.what());
+    }
+    if (!doc.is_object()) throw Error(ErrorKind::ParseError, "spec document must be a JSON object");
+    only_keys(doc, {"name", "memory_bandwidth_tbps", "l2_cache_mb", "peaks"}, "spec document");
+    for (const char* k : {"name", "memory_bandwidth_tbps", "l2_cache_mb", "peaks"})
+        if (!doc.contains(k)) throw Error(ErrorKind::MissingField, std::string("'") + k + "' is required");
+    if (!doc["name"].is_string()) throw Error(ErrorKind::ParseError, "'name' must be a string");
+    if (!doc["peaks"].is_object()) throw Error(ErrorKind::ParseError, "'peaks' must be a table");
+
+    HardwareSpec s;
+    s.name = doc["name"].get<std::string>();
+    s.memory_bandwidth = number_field(doc["memory_bandwidth_tbps"], "memory_bandwidth_tbps") * kTera;
+    s.l2_cache_bytes = number_field(doc["l2_cache_mb"], "l2_cache_mb") * kMega;
+    PeakTable table;
+    for (auto it = doc["peaks"].begin(); it != doc["peaks"].end(); ++it) {
+        const int pi = precision_index(it.key());
+        if (pi < 0) throw Error(ErrorKind::ParseError, "unknown precision '" + it.key() + "' in peaks");
+        if (!it->is_object()) throw Error(ErrorKind::ParseError, "peaks." + it.key() + " must be a table");
+        only_keys(*it, {"cuda_core_tflops", "tensor_core_tflops"}, "peaks." + it.key());
+        if (it->contains("cuda_core_tflops"))
+            table[{0, pi}] = number_field((*it)["cuda_core_tflops"], "peaks." + it.key() + ".cuda_core_tflops") * kTera;
+        if (it->contains("tensor_core_tflops"))
+            table[{1, pi}] = number_field((*it)["tensor_core_tflops"], "peaks." + it.key() + ".tensor_core_tflops") * kTera;
+    }
+    s.validate();
+    validate_peaks(s.name, table);
+    if (table.count({0, 0})) s.peak_cuda_core = table[{0, 0}];
+    if (table.count({1, 0})) s.peak_tensor_core = table[{1, 0}];
+    return s;
+}
+
+const HardwareSpec& builtin_spec(std::string_view name) {
+    // Table 1 of the paper, value * unit factor.
+    static const HardwareSpec a100{"A100-80GB", 1.94 * kTera, 40.0 * kMega, 9.7 * kTera, 19.5 * kTera};
+    static const HardwareSpec gh200{"GH200", 4.00 * kTera, 50.0 * kMega, 34.0 * kTera, 67.0 * kTera};
+    if (name == a100.name) return a100;
+    if (name == gh200.name) return gh200;
+    throw Error(ErrorKind::UnknownHardware, "no built-in spec named '" + std::string(name) + "'");
+}
+
+double machine_balance(const HardwareSpec& s, ExecutionUnit u, Precision p) {
+    return s.peak(u, p) / s.memory_bandwidth;
+}
+
+double tensor_alpha(const HardwareSpec& s, Precision p) {
+    return s.peak(ExecutionUnit::TensorCore, p) / s.peak(ExecutionUnit::CudaCore, p);
+}
+
+// ---------------------------------------------------------------------------
+// Roofline
+// ---------------------------------------------------------------------------
+double attainable(const HardwareSpec& s, ExecutionUnit u, Precision p, double intensity) {
+    if (intensity < 0.0) throw Error(ErrorKind::InvalidRange, "intensity must be >= 0");
+    return std::min(s.peak(u, p), s.memory_bandwidth * intensity);
+}
+
+Boundedness classify(double intensity, double balance) {
+    return intensity < balance ? Boundedness::MemoryBound
+           : intensity > balance ? Boundedness::ComputeBound
+                                 : Boundedness::Balanced;
+}
+
+// ---------------------------------------------------------------------------
+// Bounds
+// ---------------------------------------------------------------------------
+namespace {
+void need_alpha(double a) {
+    if (!(a >= 1.0)) throw Error(ErrorKind::InvalidAlpha, "alpha must be >= 1");
+}
+void need_intensity(double i) {
+    if (!(i > 0.0)) throw Error(ErrorKind::ZeroIntensity, "intensity must be > 0");
+}
+}  // namespace
+
+double unoverlapped_speedup(double t_cmp, double t_mem, double t_others, double alpha) {
+    if (t_cmp < 0.0 || t_mem < 0.0 || t_others < 0.0)
+        throw Error(ErrorKind::ValidationError, "time components must be >= 0");
+    if (t_cmp == 0.0 && t_mem == 0.0 && t_others == 0.0)
+        throw Error(ErrorKind::ValidationError, "time breakdown is all zero");
+    need_alpha(alpha);
+    if (t_cmp == 0.0) return 1.0;
+    const double rest = t_mem + t_others;
+    return (t_cmp + rest) / (t_cmp / alpha + rest);
+}
+
+double kernel_speedup_ceiling(double alpha, double balance, double intensity, int* n_warnings) {
+    need_alpha(alpha);
+    need_intensity(intensity);
+    if (n_warnings) *n_warnings = intensity >= balance ? 1 : 0;
+    return 1.0 + (alpha - 1.0) / (1.0 + alpha * (balance / intensity));
+}
+
+double tensor_core_ceiling(double alpha) {
+    need_alpha(alpha);
+    return 1.0 + (alpha - 1.0) / (1.0 + alpha);  // lands exactly on 4/3 at alpha = 2
+}
+
+double workload_ceiling(double intensity, double balance) {
+    need_intensity(intensity);
+    if (!(balance > 0.0)) throw Error(ErrorKind::ZeroBalance, "balance must be > 0");
+    return 1.0 + intensity / balance;
+}
+
+std::uint64_t min_temporal_depth(double balance, double i1) {
+    need_intensity(i1);
+    if (balance < i1) return 1;
+    const double ratio = balance / i1;
+    if (!std::isfinite(ratio) || ratio >= 1e18)
+        throw Error(ErrorKind::InvalidRange, "balance/intensity ratio too large");
+    // smallest t with t * i1 > balance, decided by the multiplication itself
+    std::uint64_t t = static_cast<std::uint64_t>(ratio);
+    if (t == 0) t = 1;
+    while (t > 1 && double(t - 1) * i1 > balance) --t;
+    while (!(double(t) * i1 > balance)) ++t;
+    return t;
+}
+
+double tc_scale_trick_throughput(double peak_tc, std::uint64_t m, std::uint64_t n) {
+    if (!m || !n) throw Error(ErrorKind::InvalidCount, "engine dimensions must be >= 1");
+    if (!(peak_tc > 0.0)) throw Error(ErrorKind::ValidationError, "peak_tc must be > 0");
+    return peak_tc / double(std::max(m, n));
+}
+
+}  // namespace rooflens::b200

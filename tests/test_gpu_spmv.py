@@ -1,0 +1,156 @@
+"""GPU parity: CSR SpMV (K3 CUDA core, K4 tensor core) vs the CPU oracle.
+
+Bar (BASELINE.json north_star): 1e-12 norm-wise relative error (summation
+order and DMMA accumulation order differ from the oracle's row-order sum).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2502_16851_b200 as P
+
+pytestmark = pytest.mark.gpu
+
+UNITS = [P.CUDA_CORE, P.TENSOR_CORE]
+TOL = 1e-12
+
+
+def _to_dev(torch, *arrs):
+    return [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in arrs]
+
+
+def _run(torch, rp, col, val, x, unit):
+    d_rp, d_col, d_val, d_x = _to_dev(torch, rp, col, val, x)
+    d_y = torch.full((rp.size - 1,), float("nan"), dtype=torch.float64, device="cuda")
+    kc = P.spmv_csr(d_rp, d_col, d_val, d_x, d_y, unit=unit)
+    torch.cuda.synchronize()
+    return d_y.cpu().numpy(), kc
+
+
+def _ragged(rng, m, n, max_len, empty_frac=0.1):
+    lens = rng.integers(0, max_len + 1, size=m)
+    lens[rng.random(m) < empty_frac] = 0
+    lens = np.minimum(lens, n)
+    rp = np.zeros(m + 1, np.int64)
+    rp[1:] = np.cumsum(lens)
+    col = np.concatenate([np.sort(rng.choice(n, size=l, replace=False)) for l in lens]
+                         ) if rp[-1] else np.zeros(0, np.int64)
+    val = rng.uniform(-1, 1, size=rp[-1])
+    return rp.astype(np.int32), col.astype(np.int32), val
+
+
+@pytest.mark.parametrize("m,n,k,hb", [(64, 64, 16, 65536), (1000, 1000, 16, 100), (4099, 4099, 16, 65536),
+                                      (20000, 20000, 16, 65536), (333, 333, 5, 7), (257, 257, 33, 40)])
+@pytest.mark.parametrize("unit", UNITS)
+def test_spmv_banded(cuda, m, n, k, hb, unit):
+    import torch
+
+    rp, col, val = O.gen_band_csr(m, 0, n, k, hb, 99)
+    x = O.fill_uniform(n, 99, 4, 0, 1)
+    y, kc = _run(torch, rp, col, val, x, unit)
+    ref = O.spmv_csr(rp, col, val, x)
+    assert O.rel_err(y, ref) <= TOL
+    nnz = m * k
+    assert kc.work_flops == 2 * nnz
+    assert kc.traffic_bytes == (nnz + m + n) * 8 + (nnz + m + 1) * 4
+
+
+@pytest.mark.parametrize("max_len", [3, 16, 40, 130])
+@pytest.mark.parametrize("unit", UNITS)
+def test_spmv_ragged_and_empty_rows(cuda, max_len, unit):
+    import torch
+
+    rng = np.random.default_rng(max_len)
+    rp, col, val = _ragged(rng, 3001, 2500, max_len)
+    x = rng.uniform(-1, 1, 2500)
+    y, _ = _run(torch, rp, col, val, x, unit)
+    ref = O.spmv_csr(rp, col, val, x)
+    assert O.rel_err(y, ref) <= TOL
+    assert np.all(y[np.diff(rp) == 0] == 0.0)  # empty rows give exactly 0
+
+
+@pytest.mark.parametrize("unit", UNITS)
+def test_spmv_single_row_and_column(cuda, unit):
+    import torch
+
+    rp = np.array([0, 1], np.int32)
+    y, _ = _run(torch, rp, np.array([0], np.int32), np.array([2.5]), np.array([-4.0]), unit)
+    assert y[0] == -10.0
+    # one dense row of 1000
+    n = 1000
+    rp = np.array([0, n], np.int32)
+    col = np.arange(n, dtype=np.int32)
+    val = np.linspace(-1, 1, n)
+    x = np.cos(np.arange(n))
+    y, _ = _run(torch, rp, col, val, x, unit)
+    assert O.rel_err(y, O.spmv_csr(rp, col, val, x)) <= TOL
+
+
+@pytest.mark.parametrize("unit", UNITS)
+def test_spmv_rows_with_col_base(cuda, unit):
+    """Row-range form used by the row-partitioned path: x is a window."""
+    import torch
+
+    m, n, k, hb = 5000, 5000, 16, 300
+    rp, col, val = O.gen_band_csr(m, 0, n, k, hb, 3)
+    x = O.fill_uniform(n, 3, 4, 0, 1)
+    ref = O.spmv_csr(rp, col, val, x)
+    r0, r1 = 1200, 3700
+    lo, hi = r0 - hb, r1 + hb
+    d_rp, d_col, d_val = _to_dev(torch, rp, col, val)
+    d_xw = torch.from_numpy(x[lo:hi].copy()).cuda()
+    d_y = torch.zeros(m, dtype=torch.float64, device="cuda")
+    P.spmv_csr_rows(r0, r1, d_rp, d_col, d_val, d_xw, d_y, col_base=lo, unit=unit)
+    torch.cuda.synchronize()
+    y = d_y.cpu().numpy()
+    assert O.rel_err(y[r0:r1], ref[r0:r1]) <= TOL
+    assert np.all(y[:r0] == 0) and np.all(y[r1:] == 0)
+
+
+def test_spmv_generator_matches_oracle(cuda):
+    import torch
+
+    m, n, k, hb = 70000, 70000, 16, 65536
+    d_rp = torch.empty(m + 1, dtype=torch.int32, device="cuda")
+    d_col = torch.empty(m * k, dtype=torch.int32, device="cuda")
+    d_val = torch.empty(m * k, dtype=torch.float64, device="cuda")
+    P.gen_band_csr(m, 0, n, k, hb, 42, d_rp, d_col, d_val)
+    torch.cuda.synchronize()
+    rp, col, val = O.gen_band_csr(m, 0, n, k, hb, 42)
+    assert np.array_equal(d_rp.cpu().numpy(), rp)
+    assert np.array_equal(d_col.cpu().numpy(), col)
+    assert O.bit_mismatches(d_val.cpu().numpy(), val) == 0
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("unit", UNITS)
+def test_spmv_full_config(cuda, unit):
+    """BASELINE configs[1]: n = 2^22, 16 nnz/row in a +-65536 band."""
+    import torch
+
+    n, k, hb, seed = 1 << 22, 16, 65536, 2025
+    d_rp = torch.empty(n + 1, dtype=torch.int32, device="cuda")
+    d_col = torch.empty(n * k, dtype=torch.int32, device="cuda")
+    d_val = torch.empty(n * k, dtype=torch.float64, device="cuda")
+    d_x = torch.empty(n, dtype=torch.float64, device="cuda")
+    d_y = torch.empty(n, dtype=torch.float64, device="cuda")
+    P.gen_band_csr(n, 0, n, k, hb, seed, d_rp, d_col, d_val)
+    P.fill_uniform(d_x, seed, 4, 0, 1)
+    kc = P.spmv_csr(d_rp, d_col, d_val, d_x, d_y, unit=unit)
+    torch.cuda.synchronize()
+    assert kc.traffic_bytes == 889192452 and kc.work_flops == 134217728
+    rp, col, val = O.gen_band_csr(n, 0, n, k, hb, seed)
+    x = O.fill_uniform(n, seed, 4, 0, 1)
+    assert np.array_equal(d_col.cpu().numpy(), col)
+    ref = O.spmv_csr(rp, col, val, x)
+    assert O.rel_err(d_y.cpu().numpy(), ref) <= TOL
+
+
+def test_spmv_errors(cuda):
+    import torch
+
+    z = torch.zeros(4, dtype=torch.float64, device="cuda")
+    rp = torch.zeros(5, dtype=torch.int32, device="cuda")
+    with pytest.raises(P.RooflensError) as e:  # nnz = 0: the model rejects it
+        P.spmv_csr(rp, rp[:0], z[:0], z, z)
+    assert e.value.kind == "ValidationError"

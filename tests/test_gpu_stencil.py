@@ -1,0 +1,174 @@
+"""GPU parity: Jacobi stencils (K5-K10) vs the CPU oracle.
+
+Bar (BASELINE.json north_star): 1e-12 norm-wise relative error.  The
+Dirichlet ring must be untouched (bit-exact), which also checks that no
+kernel writes outside the interior.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2502_16851_b200 as P
+
+pytestmark = pytest.mark.gpu
+
+UNITS = [P.CUDA_CORE, P.TENSOR_CORE]
+TOL = 1e-12
+
+
+def _run(torch, preset, u0, steps, unit, weights=None):
+    u = torch.from_numpy(u0.copy()).cuda()
+    v = torch.from_numpy(u0.copy()).cuda()
+    kc = P.stencil(preset, u, v, steps, weights=weights, unit=unit)
+    torch.cuda.synchronize()
+    out = (u if steps % 2 == 0 else v).cpu().numpy()
+    return out, kc
+
+
+def _ring_mask(shape, r):
+    m = np.zeros(shape, bool)
+    if len(shape) == 2:
+        m[:r, :] = m[-r:, :] = m[:, :r] = m[:, -r:] = True
+    else:
+        m[:r] = m[-r:] = True
+        m[:, :r] = m[:, -r:] = True
+        m[:, :, :r] = m[:, :, -r:] = True
+    return m
+
+
+SHAPES_2D = [(3, 3), (5, 7), (17, 33), (64, 128), (130, 258), (257, 129), (301, 515), (1030, 1026)]
+SHAPES_3D = [(3, 3, 3), (5, 6, 7), (10, 17, 33), (34, 20, 130), (20, 70, 256), (40, 40, 64)]
+
+
+@pytest.mark.parametrize("shape", SHAPES_2D)
+@pytest.mark.parametrize("unit", UNITS)
+@pytest.mark.parametrize("steps", [1, 4])
+def test_2d5pt(cuda, shape, unit, steps):
+    import torch
+
+    u0 = O.stencil_init(shape, 1, 7)
+    out, kc = _run(torch, "2d5pt", u0, steps, unit)
+    ref = O.stencil("2d5pt", u0, steps)
+    assert O.rel_err(out, ref) <= TOL
+    ring = _ring_mask(shape, 1)
+    assert O.bit_mismatches(out[ring], u0[ring]) == 0
+    pts = (shape[0] - 2) * (shape[1] - 2)
+    assert (kc.work_flops, kc.traffic_bytes) == (10 * pts * steps, 16 * pts * steps)
+
+
+@pytest.mark.parametrize("preset", ["3d7pt", "3d27pt"])
+@pytest.mark.parametrize("shape", SHAPES_3D)
+@pytest.mark.parametrize("unit", UNITS)
+@pytest.mark.parametrize("steps", [1, 3])
+def test_3d(cuda, preset, shape, unit, steps):
+    import torch
+
+    u0 = O.stencil_init(shape, 1, 13)
+    out, kc = _run(torch, preset, u0, steps, unit)
+    ref = O.stencil(preset, u0, steps)
+    assert O.rel_err(out, ref) <= TOL
+    ring = _ring_mask(shape, 1)
+    assert O.bit_mismatches(out[ring], u0[ring]) == 0
+    pts = (shape[0] - 2) * (shape[1] - 2) * (shape[2] - 2)
+    npts = 7 if preset == "3d7pt" else 27
+    assert kc.traffic_bytes == 16 * pts * steps and kc.work_flops == 2 * npts * pts * steps
+
+
+@pytest.mark.parametrize("unit", UNITS)
+def test_3d27pt_general_weights(cuda, unit):
+    """Weights without the |dx|+|dy|+|dz| structure take the general path."""
+    import torch
+
+    rng = np.random.default_rng(5)
+    w = rng.uniform(0, 1, 27)
+    w /= w.sum()
+    shape = (18, 21, 70)
+    u0 = O.stencil_init(shape, 1, 3)
+    out, _ = _run(torch, "3d27pt", u0, 2, unit, weights=w)
+    assert O.rel_err(out, O.stencil("3d27pt", u0, 2, w)) <= TOL
+
+
+@pytest.mark.parametrize("unit", UNITS)
+@pytest.mark.parametrize("preset", ["2d5pt", "3d7pt"])
+def test_custom_weights(cuda, unit, preset):
+    import torch
+
+    npts = 5 if preset == "2d5pt" else 7
+    w = np.linspace(0.05, 0.3, npts)
+    shape = (66, 130) if preset == "2d5pt" else (12, 19, 68)
+    u0 = O.stencil_init(shape, 1, 8)
+    out, _ = _run(torch, preset, u0, 3, unit, weights=w)
+    assert O.rel_err(out, O.stencil(preset, u0, 3, w)) <= TOL
+
+
+@pytest.mark.parametrize("preset,shape", [("2d9pt", (40, 77)), ("2d13pt", (41, 70)), ("2d49pt", (33, 45))])
+def test_other_presets_cuda_core(cuda, preset, shape):
+    import torch
+
+    r = P.stencil_preset(preset)[2]
+    u0 = O.stencil_init(shape, r, 21)
+    out, _ = _run(torch, preset, u0, 2, P.CUDA_CORE)
+    assert O.rel_err(out, O.stencil(preset, u0, 2)) <= TOL
+    with pytest.raises(P.RooflensError) as e:
+        _run(torch, preset, u0, 1, P.TENSOR_CORE)
+    assert e.value.kind == "ValidationError"
+
+
+@pytest.mark.parametrize("unit", UNITS)
+def test_sweep_partial_range(cuda, unit):
+    """rl_stencil_sweep over a plane range writes exactly those planes."""
+    import torch
+
+    shape = (30, 24, 64)
+    u0 = O.stencil_init(shape, 1, 4)
+    ref = O.stencil("3d7pt", u0, 1)
+    u = torch.from_numpy(u0).cuda()
+    v = torch.zeros_like(u)
+    P.stencil_sweep("3d7pt", u, v, 7, 19, unit=unit)
+    torch.cuda.synchronize()
+    out = v.cpu().numpy()
+    assert O.rel_err(out[7:19], ref[7:19]) <= TOL
+    assert np.all(out[:7] == 0) and np.all(out[19:] == 0)
+
+
+def test_stencil_generator_matches_oracle(cuda):
+    import torch
+
+    for shape in [(130, 67), (9, 33, 65)]:
+        u = torch.empty(shape, dtype=torch.float64, device="cuda")
+        P.stencil_init(u, 1, 77)
+        torch.cuda.synchronize()
+        assert O.bit_mismatches(u.cpu().numpy(), O.stencil_init(shape, 1, 77)) == 0
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("unit", UNITS)
+def test_2d5pt_full_grid(cuda, unit):
+    """BASELINE configs[2] grid (16384^2), 2 steps against the oracle."""
+    import torch
+
+    shape = (16384, 16384)
+    u = torch.empty(shape, dtype=torch.float64, device="cuda")
+    P.stencil_init(u, 1, 2025)
+    v = u.clone()
+    P.stencil("2d5pt", u, v, 2, unit=unit)
+    torch.cuda.synchronize()
+    u0 = O.stencil_init(shape, 1, 2025)
+    assert O.rel_err(u.cpu().numpy(), O.stencil("2d5pt", u0, 2)) <= TOL
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("preset", ["3d7pt", "3d27pt"])
+@pytest.mark.parametrize("unit", UNITS)
+def test_3d_full_grid(cuda, preset, unit):
+    """BASELINE configs[3]/[4] grid (512^3), 2 steps against the oracle."""
+    import torch
+
+    shape = (512, 512, 512)
+    u = torch.empty(shape, dtype=torch.float64, device="cuda")
+    P.stencil_init(u, 1, 2025)
+    v = u.clone()
+    P.stencil(preset, u, v, 2, unit=unit)
+    torch.cuda.synchronize()
+    u0 = O.stencil_init(shape, 1, 2025)
+    assert O.rel_err(u.cpu().numpy(), O.stencil(preset, u0, 2)) <= TOL
