@@ -595,12 +595,19 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         if (k == "scale_blocks_per_sm") slot = &t.scale_blocks_per_sm;
         else if (k == "spmv_rows") slot = &t.spmv_rows;
         else if (k == "spmv_blocks_per_sm") slot = &t.spmv_blocks_per_sm;
+        else if (k == "spmv_sched") slot = &t.spmv_sched;
+        else if (k == "spmv_xhint") slot = &t.spmv_xhint;
+        else if (k == "scale_unroll") slot = &t.scale_unroll;
         else if (k == "stencil2d_rows") slot = &t.stencil2d_rows;
         else if (k == "stencil3d_zchunk") slot = &t.stencil3d_zchunk;
         else if (k == "tc_stencil_zchunk") slot = &t.tc_stencil_zchunk;
+        else if (k == "stencil_tma") slot = &t.stencil_tma;
+        else if (k == "stencil_ctas_per_sm") slot = &t.stencil_ctas_per_sm;
+        else if (k == "stencil_tc_ctas_per_sm") slot = &t.stencil_tc_ctas_per_sm;
+        else if (k == "stencil_tc3d_ctas_per_sm") slot = &t.stencil_tc3d_ctas_per_sm;
         else throw Error(ErrorKind::ValidationError, "unknown tuning key '" + k + "'");
         if (previous) *previous = *slot;
-        if (value <= 0) throw Error(ErrorKind::InvalidRange, "tuning values must be > 0");
+        if (value < 0) throw Error(ErrorKind::InvalidRange, "tuning values must be >= 0");
         *slot = static_cast<int>(value);
     });
 }

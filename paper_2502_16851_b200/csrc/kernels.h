@@ -9,16 +9,22 @@ namespace rlb {
 
 // Kernel-variant knobs, settable through rl_tuning_set() for sweeps.
 struct Tuning {
-    int scale_blocks_per_sm = 8;   // STREAM grid = 148 * this
-    int scale_threads = 256;
+    int scale_blocks_per_sm = 32;  // STREAM grid = 148 * this (swept: tools/sweep.py)
+    int scale_unroll = 8;          // 1, 2, 4, 8
     int spmv_group = 0;            // lanes per row; 0 = auto from nnz/m
-    int spmv_rows = 4;             // rows per lane group per iteration (1, 2, 4)
-    int spmv_blocks_per_sm = 8;
+    int spmv_rows = 2;             // rows per lane group per iteration (1, 2, 4)
+    int spmv_blocks_per_sm = 16;
+    int spmv_sched = 1;            // 0 grid-stride, 1 contiguous row range per CTA
+    int spmv_xhint = 0;            // x gathers: 0 L1 default, 1 L1::evict_last, 2 L1::no_allocate
     int stencil2d_rows = 256;      // rows marched per warp (2D CC)
     int stencil2d_variant = 0;     // 0 = register-streaming CC
     int stencil3d_zchunk = 64;     // planes marched per CTA (3D)
     int stencil3d_ty = 8;          // tile rows (3D)
     int tc_stencil_zchunk = 32;
+    int stencil_tma = 1;           // 1: TMA-pipelined kernels when eligible
+    int stencil_ctas_per_sm = 2;   // grid sizing target, TMA CUDA-core kernels
+    int stencil_tc_ctas_per_sm = 2;    // ... 2D tensor-core kernel
+    int stencil_tc3d_ctas_per_sm = 5;  // ... 3D tensor-core kernels
 };
 Tuning& tuning();
 
@@ -45,6 +51,11 @@ cudaError_t launch_stencil_cc(const StencilDesc& d, uint64_t o0, uint64_t o1, co
                               double* v, cudaStream_t s);
 cudaError_t launch_stencil_tc(const StencilDesc& d, uint64_t o0, uint64_t o1, const double* u,
                               double* v, cudaStream_t s);
+
+// TMA-pipelined stencils (2d5pt, 3d7pt, 3d27pt; even nx, 16-byte aligned).
+bool stencil_tma_eligible(const StencilDesc& d, const double* u, const double* v);
+cudaError_t launch_stencil_tma(int unit, const StencilDesc& d, uint64_t o0, uint64_t o1,
+                               const double* u, double* v, cudaStream_t s);
 
 // Launch accounting (rl_kernel_launches): every <<<>>> site reports itself.
 void note_launch(uint64_t n = 1);

@@ -57,17 +57,31 @@ __device__ __forceinline__ Nz4 load_nz4(const int* __restrict__ col,
     return z;
 }
 
+__device__ __forceinline__ double ld_x(const double* p, uint64_t pol, int hint) {
+    double v;
+    if (hint == 1)
+        asm("ld.global.nc.L1::evict_last.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    else if (hint == 2)
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    else
+        asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
 // Gather x for 4 nonzeros; padded slots get 0 (so 0*x never meets a non-finite x).
+template <int XH = 0>
 __device__ __forceinline__ void gather4(double (&xv)[4], const Nz4& z,
                                         const double* __restrict__ x, int64_t col_base,
                                         uint64_t polx) {
 #pragma unroll
     for (int k = 0; k < 4; ++k)
-        xv[k] = k < z.n ? ld_policy(x + ((int64_t)z.c[k] - col_base), polx) : 0.0;
+        xv[k] = k < z.n ? ld_x(x + ((int64_t)z.c[k] - col_base), polx, XH) : 0.0;
 }
 
 // K3: CUDA core.  Row of warp-step u for group q: wbase + 8u + q.
-template <int R>
+// SCHED 0: warps stride over the whole row range (grid-stride);
+// SCHED 1: each CTA owns one contiguous row range (x-window locality in L1).
+template <int R, int SCHED, int XH>
 __global__ void __launch_bounds__(256) spmv_cc_v4(uint64_t r0, uint64_t r1,
                                                   const int* __restrict__ rp,
                                                   const int* __restrict__ col,
@@ -80,12 +94,25 @@ __global__ void __launch_bounds__(256) spmv_cc_v4(uint64_t r0, uint64_t r1,
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const int col_pad = 0;
-    for (uint64_t wbase = r0 + warp * 8 * R; wbase < r1; wbase += nwarps * 8 * R) {
+    uint64_t first, stride, last;
+    if (SCHED == 0) {
+        first = r0 + warp * 8 * R;
+        stride = nwarps * 8 * R;
+        last = r1;
+    } else {
+        const uint64_t per = ((r1 - r0) + gridDim.x - 1) / gridDim.x;
+        const uint64_t b0 = r0 + (uint64_t)blockIdx.x * per;
+        first = b0 + (threadIdx.x >> 5) * 8 * R;
+        stride = (blockDim.x >> 5) * 8 * R;
+        last = min(r1, b0 + per);
+    }
+    for (uint64_t wbase = first; wbase < last; wbase += stride) {
+        const uint64_t rend = last;
         int64_t s[R], e[R];
 #pragma unroll
         for (int u = 0; u < R; ++u) {
             const uint64_t row = wbase + 8 * u + q;
-            const bool ok = row < r1;
+            const bool ok = row < rend;
             s[u] = ok ? __ldg(rp + row) : 0;
             e[u] = ok ? __ldg(rp + row + 1) : 0;
         }
@@ -96,7 +123,7 @@ __global__ void __launch_bounds__(256) spmv_cc_v4(uint64_t r0, uint64_t r1,
 #pragma unroll
         for (int u = 0; u < R; ++u) {
             double xv[4];
-            gather4(xv, z[u], x, col_base, polx);
+            gather4<XH>(xv, z[u], x, col_base, polx);
             double a = z[u].v[0] * xv[0];
             a = fma(z[u].v[1], xv[1], a);
             a = fma(z[u].v[2], xv[2], a);
@@ -109,7 +136,7 @@ __global__ void __launch_bounds__(256) spmv_cc_v4(uint64_t r0, uint64_t r1,
             for (int64_t j = s[u] + 16 + 4 * c; j < e[u]; j += 16) {
                 Nz4 t = load_nz4(col, val, j, e[u], col_pad, pol);
                 double xv[4];
-                gather4(xv, t, x, col_base, polx);
+                gather4<XH>(xv, t, x, col_base, polx);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) acc[u] = fma(t.v[k], xv[k], acc[u]);
             }
@@ -120,7 +147,7 @@ __global__ void __launch_bounds__(256) spmv_cc_v4(uint64_t r0, uint64_t r1,
             a += __shfl_xor_sync(0xffffffffu, a, 1);
             a += __shfl_xor_sync(0xffffffffu, a, 2);
             const uint64_t row = wbase + 8 * u + q;
-            if (c == 0 && row < r1) y[row] = a;
+            if (c == 0 && row < rend) y[row] = a;
         }
     }
 }
@@ -182,11 +209,23 @@ cudaError_t launch_spmv(int unit, uint64_t r0, uint64_t r1, const int* rp, const
     const uint64_t rows_per_block = 8ull * 8ull * (uint64_t)R;
     uint64_t blocks = (rows + rows_per_block - 1) / rows_per_block;
     if (blocks > max_blocks) blocks = max_blocks;
-    switch (R) {
-        case 1: spmv_cc_v4<1><<<(unsigned)blocks, threads, 0, s>>>(r0, r1, rp, col, val, x, col_base, y); note_launch(); break;
-        case 2: spmv_cc_v4<2><<<(unsigned)blocks, threads, 0, s>>>(r0, r1, rp, col, val, x, col_base, y); note_launch(); break;
-        default: spmv_cc_v4<4><<<(unsigned)blocks, threads, 0, s>>>(r0, r1, rp, col, val, x, col_base, y); note_launch(); break;
+    const int sched = t.spmv_sched, xh = t.spmv_xhint;
+#define RLB_SPMV(RR, SS, XX) \
+    spmv_cc_v4<RR, SS, XX><<<(unsigned)blocks, threads, 0, s>>>(r0, r1, rp, col, val, x, col_base, y)
+#define RLB_SPMV_R(SS, XX)                        \
+    do {                                          \
+        if (R == 1) RLB_SPMV(1, SS, XX);          \
+        else if (R == 2) RLB_SPMV(2, SS, XX);     \
+        else RLB_SPMV(4, SS, XX);                 \
+    } while (0)
+    if (sched == 0) {
+        if (xh == 1) RLB_SPMV_R(0, 1); else if (xh == 2) RLB_SPMV_R(0, 2); else RLB_SPMV_R(0, 0);
+    } else {
+        if (xh == 1) RLB_SPMV_R(1, 1); else if (xh == 2) RLB_SPMV_R(1, 2); else RLB_SPMV_R(1, 0);
     }
+#undef RLB_SPMV_R
+#undef RLB_SPMV
+    note_launch();
     return cudaGetLastError();
 }
 

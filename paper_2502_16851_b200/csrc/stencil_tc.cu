@@ -311,6 +311,7 @@ cudaError_t with_smem(K kernel, size_t bytes) {
 
 cudaError_t launch_stencil_tc(const StencilDesc& d, uint64_t o0, uint64_t o1, const double* u,
                               double* v, cudaStream_t s) {
+    if (stencil_tma_eligible(d, u, v)) return launch_stencil_tma(1, d, o0, o1, u, v, s);
     const Tuning& t = tuning();
     const bool v16 = (d.nx % 2 == 0) && ((reinterpret_cast<uintptr_t>(u) & 15) == 0) &&
                      ((reinterpret_cast<uintptr_t>(v) & 15) == 0);

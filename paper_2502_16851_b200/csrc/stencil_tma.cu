@@ -1,0 +1,670 @@
+// stencil_tma.cu -- TMA-pipelined Jacobi stencils (K5-K10, the default path
+// on sm_100a when rows are 16-byte aligned).
+//
+// Every CTA (4 warps) owns a 64-column x 16-row tile and marches the slowest
+// axis (y in 2D, z in 3D) through a chunk of it.  One elected thread streams
+// the input through a ring of shared-memory stages with
+// cp.async.bulk.tensor (TMA) and mbarrier transaction counts: a stage is the
+// tile with its one-cell halo (18 rows x 68 columns; OOB cells arrive as
+// zeros).  Measured on this B200/driver: the innermost start coordinate of
+// a box must be 16-byte aligned (an odd FP64 x start raises "illegal
+// instruction"; negative or past-the-end boxes are fine and zero-filled), so
+// boxes start at x0 - 2 and are 68 wide (x0-2 .. x0+65): the stage column of
+// x is x - x0 + 2.  Consumers read neighbours from the stage, release it with an
+// mbarrier arrive, and the producer refills it S planes ahead, so 3-4 stages
+// (~30 KB) are always in flight per CTA and ~150 KB per SM -- enough to cover
+// HBM latency with no register prefetch queues.  Each u value crosses HBM
+// once per sweep; halo rows/columns are L2 hits of the neighbouring tiles.
+//
+// CUDA core (DFMA):
+//   2D: a stage holds 16 output rows + halo; thread = 1 column x 8 rows.
+//   3D: a stage holds one plane of the tile; plane p contributes
+//       P_{-1}(p) to output plane p+1, P_0(p) to p and P_{+1}(p) to p-1, so
+//       one stage at a time suffices (7pt: P_{+-1} = w_z+- u; 27pt: 3x3 sums,
+//       through class sums when w depends only on |dx|+|dy|+|dz|).
+// Tensor core (DMMA m8n8k4, banded products as in stencil_tc.cu):
+//   2D: 16 8x8 output tiles per stage, 4 per warp, 6 DMMA each.
+//   3D: three consecutive planes stay resident (5-stage ring) and each output
+//       plane is formed directly: 7pt 6 DMMA + DFMA z terms, 27pt class 9 DMMA,
+//       27pt general 27 DMMA per 8x8 tile.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace rlb {
+namespace {
+
+constexpr int kTX = 64, kTY = 16, kRY = 8, kBY = kTY + 2;
+constexpr int kBX = 68;   // box / stage row width (doubles)
+constexpr int kCofs = 2;  // stage column of the tile's first x
+
+// ---------------------------------------------------------------------------
+// mbarrier / TMA primitives
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t sptr(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sptr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sptr(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sptr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred P;\n"
+        "RLB_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+        " @!P bra RLB_WAIT_%=;\n}" ::"r"(sptr(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* m, uint64_t* bar, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            sptr(dst)),
+        "l"(m), "r"(sptr(bar)), "r"(x), "r"(y)
+        : "memory");
+}
+__device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* m, uint64_t* bar, int x, int y, int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+            sptr(dst)),
+        "l"(m), "r"(sptr(bar)), "r"(x), "r"(y), "r"(z)
+        : "memory");
+}
+
+// Ring bookkeeping shared by all kernels: S stages of STAGE doubles, then
+// S full + S empty barriers.
+template <int S, int STAGE>
+struct Ring {
+    double* base;
+    uint64_t* full;
+    uint64_t* empty;
+    __device__ Ring(double* smem) : base(smem) {
+        full = reinterpret_cast<uint64_t*>(smem + S * STAGE);
+        empty = full + S;
+    }
+    __device__ double* stage(int k) const { return base + (k % S) * STAGE; }
+    __device__ void init(int consumers) {
+        if (threadIdx.x == 0) {
+            for (int s = 0; s < S; ++s) {
+                mbar_init(full + s, 1);
+                mbar_init(empty + s, consumers);
+            }
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+    }
+    __device__ void wait_full(int k) { mbar_wait(full + (k % S), (uint32_t)((k / S) & 1)); }
+    // One arrive per warp once the whole warp has finished reading stage k.
+    __device__ void release(int k) {
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(empty + (k % S));
+    }
+    // Producer: before refilling the stage that held item k, wait until every
+    // consumer warp released item k.
+    __device__ void wait_empty(int k) { mbar_wait(empty + (k % S), (uint32_t)((k / S) & 1)); }
+};
+
+__host__ __device__ constexpr int stage_doubles(int bx) { return ((kBY * bx * 8 + 127) / 128) * 128 / 8; }
+template <int S, int BX>
+constexpr size_t ring_bytes() {
+    return (size_t)S * stage_doubles(BX) * 8 + 2 * S * 8;
+}
+
+// Element (k, n) of band(a, b, c) (see stencil_tc.cu).
+__device__ __forceinline__ double bandv(int k, int n, double a, double b, double c) {
+    return k == n ? a : (k == n + 1 ? b : (k == n + 2 ? c : 0.0));
+}
+
+// ===========================================================================
+// CUDA core, 2d5pt.  w: centre, y-1, y+1, x-1, x+1.
+// ===========================================================================
+template <int S>
+__global__ void __launch_bounds__(128) st2d_tma_cc(const __grid_constant__ CUtensorMap tm,
+                                                   double* __restrict__ v, uint64_t nx, uint64_t y_begin,
+                                                   uint64_t y_end, int seg_rows, int strips, StencilDesc d) {
+    constexpr int BX = kBX, STAGE = stage_doubles(BX);
+    extern __shared__ __align__(128) double smem[];
+    Ring<S, STAGE> ring(smem);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wx = warp & 1, wy = warp >> 1;
+    const int64_t x0 = (int64_t)(blockIdx.x % strips) * kTX;
+    const uint64_t ya = y_begin + (uint64_t)(blockIdx.x / strips) * seg_rows;
+    if (ya >= y_end) return;
+    const uint64_t yb = min(ya + (uint64_t)seg_rows, y_end);
+    const int nblk = (int)((yb - ya + kTY - 1) / kTY);
+    const int64_t xs = x0 - kCofs;
+    const int cofs = kCofs;
+    ring.init(4);
+    auto issue = [&](int k) {
+        mbar_expect_tx(ring.full + (k % S), kBY * BX * 8);
+        tma2d(ring.stage(k), &tm, ring.full + (k % S), (int)xs, (int)(ya + (uint64_t)k * kTY) - 1);
+    };
+    if (tid == 0)
+        for (int k = 0; k < S && k < nblk; ++k) issue(k);
+    const double w0 = d.w[0], w1 = d.w[1], w2 = d.w[2], w3 = d.w[3], w4 = d.w[4];
+    const int col = 32 * wx + lane + cofs;
+    const int cl = col > 0 ? col - 1 : 0;  // x-1 (clamped: only x = 0, a boundary column)
+    const int64_t x = x0 + 32 * wx + lane;
+    const bool xin = x >= 1 && x <= (int64_t)nx - 2;
+    for (int k = 0; k < nblk; ++k) {
+        ring.wait_full(k);
+        const double* T = ring.stage(k);
+        double o[kRY];
+        double cp = T[(kRY * wy) * BX + col], c = T[(kRY * wy + 1) * BX + col];
+#pragma unroll
+        for (int j = 0; j < kRY; ++j) {
+            const int r = kRY * wy + j + 1;
+            const double cn = T[(r + 1) * BX + col];
+            double a = w0 * c;
+            a = fma(w1, cp, a);
+            a = fma(w2, cn, a);
+            a = fma(w3, T[r * BX + cl], a);
+            a = fma(w4, T[r * BX + col + 1], a);
+            o[j] = a;
+            cp = c;
+            c = cn;
+        }
+        ring.release(k);
+        if (tid == 0 && k + S < nblk) {
+            ring.wait_empty(k);
+            issue(k + S);
+        }
+        const uint64_t yr = ya + (uint64_t)k * kTY + kRY * wy;
+        if (xin) {
+#pragma unroll
+            for (int j = 0; j < kRY; ++j)
+                if (yr + j < yb) v[(yr + j) * nx + x] = o[j];
+        }
+    }
+}
+
+// ===========================================================================
+// CUDA core, 3D.  KIND 0: 3d7pt (c, z-, z+, y-, y+, x-, x+); 1: 3d27pt
+// general; 2: 3d27pt class weights g0..g3 in w[0..3].
+// ===========================================================================
+template <int KIND, int S>
+__global__ void __launch_bounds__(128) st3d_tma_cc(const __grid_constant__ CUtensorMap tm,
+                                                   double* __restrict__ v, StencilDesc d, uint64_t z_begin,
+                                                   uint64_t z_end, int zchunk, int tiles_x, int tiles_xy) {
+    constexpr int BX = kBX, STAGE = stage_doubles(BX);
+    extern __shared__ __align__(128) double smem[];
+    Ring<S, STAGE> ring(smem);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wx = warp & 1, wy = warp >> 1;
+    const int tile = blockIdx.x % tiles_xy;
+    const uint64_t za = z_begin + (uint64_t)(blockIdx.x / tiles_xy) * zchunk;
+    if (za >= z_end) return;
+    const uint64_t zb = min(za + (uint64_t)zchunk, z_end);
+    const int np = (int)(zb - za) + 2;  // planes za-1 .. zb
+    const int64_t x0 = (int64_t)(tile % tiles_x) * kTX, y0 = (int64_t)(tile / tiles_x) * kTY;
+    const uint64_t nx = d.nx, ny = d.ny;
+    const int64_t xs = x0 - kCofs;
+    const int cofs = kCofs, rofs = 1;  // stage column/row of (x0, y0); boxes may start OOB
+    ring.init(4);
+    auto issue = [&](int k) {
+        mbar_expect_tx(ring.full + (k % S), kBY * BX * 8);
+        tma3d(ring.stage(k), &tm, ring.full + (k % S), (int)xs, (int)(y0 - rofs), (int)(za - 1 + k));
+    };
+    if (tid == 0)
+        for (int k = 0; k < S && k < np; ++k) issue(k);
+    const int col = 32 * wx + lane + cofs;
+    const int cl = col > 0 ? col - 1 : 0;
+    const int rbase = kRY * wy + rofs;  // stage row of this thread's first output row
+    const int64_t x = x0 + 32 * wx + lane;
+    const bool xin = x >= 1 && x <= (int64_t)nx - 2;
+    const int64_t yr0 = y0 + kRY * wy;
+    double acc_a[kRY], acc_b[kRY];
+#pragma unroll
+    for (int j = 0; j < kRY; ++j) acc_a[j] = acc_b[j] = 0.0;
+    const double* w = d.w;
+    for (int k = 0; k < np; ++k) {
+        ring.wait_full(k);
+        const double* T = ring.stage(k);
+        double pm[kRY], p0[kRY], pp[kRY];
+        if (KIND == 0) {
+            // rows rbase-1 .. rbase+kRY; rbase-1 < 0 only at y0 == 0, where
+            // output row 0 is boundary and never stored
+            double cp = T[max(rbase - 1, 0) * BX + col], c = T[rbase * BX + col];
+#pragma unroll
+            for (int j = 0; j < kRY; ++j) {
+                const int r = rbase + j;
+                const double cn = T[(r + 1) * BX + col];
+                double a = w[0] * c;
+                a = fma(w[3], cp, a);
+                a = fma(w[4], cn, a);
+                a = fma(w[5], T[r * BX + cl], a);
+                a = fma(w[6], T[r * BX + col + 1], a);
+                p0[j] = a;
+                pm[j] = w[1] * c;  // u(p) is the z-1 neighbour of plane p+1
+                pp[j] = w[2] * c;  // ... and the z+1 neighbour of plane p-1
+                cp = c;
+                c = cn;
+            }
+        } else {
+            // rolling 3x3 window: A = row above, B = centre row, C = row below
+            const double* ra = T + max(rbase - 1, 0) * BX;
+            const double* rb0 = T + rbase * BX;
+            double al = ra[cl], ac = ra[col], ar = ra[col + 1];
+            double bl = rb0[cl], bc = rb0[col], br = rb0[col + 1];
+#pragma unroll
+            for (int j = 0; j < kRY; ++j) {
+                const double* rc = T + (rbase + j + 1) * BX;
+                const double cL = rc[cl], cc = rc[col], cr = rc[col + 1];
+                if (KIND == 2) {
+                    const double s0 = bc;
+                    const double s1 = (ac + cc) + (bl + br);
+                    const double s2 = (al + ar) + (cL + cr);
+                    p0[j] = fma(w[2], s2, fma(w[1], s1, w[0] * s0));
+                    pm[j] = fma(w[3], s2, fma(w[2], s1, w[1] * s0));
+                    pp[j] = pm[j];
+                } else {
+                    const double nb[9] = {al, ac, ar, bl, bc, br, cL, cc, cr};
+                    double a = 0.0, b = 0.0, c = 0.0;
+#pragma unroll
+                    for (int q = 0; q < 9; ++q) {
+                        a = fma(w[q], nb[q], a);        // dz = -1 weights -> output p+1
+                        b = fma(w[9 + q], nb[q], b);    // dz =  0
+                        c = fma(w[18 + q], nb[q], c);   // dz = +1 weights -> output p-1
+                    }
+                    pm[j] = a;
+                    p0[j] = b;
+                    pp[j] = c;
+                }
+                al = bl; ac = bc; ar = br;
+                bl = cL; bc = cc; br = cr;
+            }
+        }
+        ring.release(k);
+        if (tid == 0 && k + S < np) {
+            ring.wait_empty(k);
+            issue(k + S);
+        }
+        double o[kRY];
+#pragma unroll
+        for (int j = 0; j < kRY; ++j) {
+            o[j] = acc_a[j] + pp[j];
+            acc_a[j] = acc_b[j] + p0[j];
+            acc_b[j] = pm[j];
+        }
+        if (k >= 2 && xin) {
+            const uint64_t p = za - 2 + (uint64_t)k;
+#pragma unroll
+            for (int j = 0; j < kRY; ++j) {
+                const int64_t y = yr0 + j;
+                if (y >= 1 && y <= (int64_t)ny - 2) v[(p * ny + (uint64_t)y) * nx + x] = o[j];
+            }
+        }
+    }
+}
+
+// ===========================================================================
+// Tensor core, 2d5pt: 16 8x8 tiles per stage; warp w -> row block w>>1,
+// column blocks 4*(w&1) .. +3.
+// ===========================================================================
+template <int S>
+__global__ void __launch_bounds__(128) st2d_tma_tc(const __grid_constant__ CUtensorMap tm,
+                                                   double* __restrict__ v, uint64_t nx, uint64_t y_begin,
+                                                   uint64_t y_end, int seg_rows, int strips, StencilDesc d) {
+    constexpr int BX = kBX, STAGE = stage_doubles(BX);
+    extern __shared__ __align__(128) double smem[];
+    Ring<S, STAGE> ring(smem);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int r = lane >> 2, c = lane & 3;
+    const int rb = warp >> 1, cb0 = 4 * (warp & 1);
+    const int64_t x0 = (int64_t)(blockIdx.x % strips) * kTX;
+    const uint64_t ya = y_begin + (uint64_t)(blockIdx.x / strips) * seg_rows;
+    if (ya >= y_end) return;
+    const uint64_t yb = min(ya + (uint64_t)seg_rows, y_end);
+    const int nblk = (int)((yb - ya + kTY - 1) / kTY);
+    const int64_t xs = x0 - kCofs;
+    const int cofs = kCofs;
+    ring.init(4);
+    auto issue = [&](int k) {
+        mbar_expect_tx(ring.full + (k % S), kBY * BX * 8);
+        tma2d(ring.stage(k), &tm, ring.full + (k % S), (int)xs, (int)(ya + (uint64_t)k * kTY) - 1);
+    };
+    auto cc = [&](int i) { return min(max(i, 0), BX - 1); };  // clamp a stage column
+    if (tid == 0)
+        for (int k = 0; k < S && k < nblk; ++k) issue(k);
+    double ty[3], tx[3];
+#pragma unroll
+    for (int kb = 0; kb < 3; ++kb) {
+        ty[kb] = bandv(4 * kb + c, r, d.w[1], d.w[0], d.w[2]);
+        tx[kb] = bandv(4 * kb + c, r, d.w[3], 0.0, d.w[4]);
+    }
+    for (int k = 0; k < nblk; ++k) {
+        ring.wait_full(k);
+        const double* T = ring.stage(k);
+        double D0[4], D1[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int cb = cb0 + t;
+            double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+            for (int kb = 0; kb < 3; ++kb) {
+                const int j = min(4 * kb + c, 9);
+                dmma_m8n8k4(d0, d1, ty[kb], T[(8 * rb + j) * BX + cc(8 * cb + r + cofs)], d0, d1);
+            }
+#pragma unroll
+            for (int kb = 0; kb < 3; ++kb) {
+                const int j = min(4 * kb + c, 9);
+                dmma_m8n8k4(d0, d1, T[(8 * rb + r + 1) * BX + cc(8 * cb + j - 1 + cofs)], tx[kb], d0, d1);
+            }
+            D0[t] = d0;
+            D1[t] = d1;
+        }
+        ring.release(k);
+        if (tid == 0 && k + S < nblk) {
+            ring.wait_empty(k);
+            issue(k + S);
+        }
+        const uint64_t y = ya + (uint64_t)k * kTY + 8 * rb + r;
+        if (y < yb) {
+            double* vr = v + y * nx;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const int64_t xx = x0 + 8 * (cb0 + t) + 2 * c;
+                const bool i0 = xx >= 1 && xx <= (int64_t)nx - 2, i1 = xx + 1 <= (int64_t)nx - 2;
+                if (i0 && i1)
+                    asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(vr + xx), "d"(D0[t]), "d"(D1[t]) : "memory");
+                else {
+                    if (i0) vr[xx] = D0[t];
+                    if (xx + 1 >= 1 && i1) vr[xx + 1] = D1[t];
+                }
+            }
+        }
+    }
+}
+
+// ===========================================================================
+// Tensor core, 3D: planes z-1, z, z+1 resident (S >= 5).
+// KIND 0: 3d7pt, 1: 3d27pt class weights, 2: 3d27pt general.
+// ===========================================================================
+template <int KIND, int S>
+__global__ void __launch_bounds__(128) st3d_tma_tc(const __grid_constant__ CUtensorMap tm,
+                                                   double* __restrict__ v, StencilDesc d, uint64_t z_begin,
+                                                   uint64_t z_end, int zchunk, int tiles_x, int tiles_xy) {
+    constexpr int BX = kBX, STAGE = stage_doubles(BX);
+    extern __shared__ __align__(128) double smem[];
+    Ring<S, STAGE> ring(smem);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int r = lane >> 2, c = lane & 3;
+    const int rb = warp >> 1, cb0 = 4 * (warp & 1);
+    const int tile = blockIdx.x % tiles_xy;
+    const uint64_t za = z_begin + (uint64_t)(blockIdx.x / tiles_xy) * zchunk;
+    if (za >= z_end) return;
+    const uint64_t zb = min(za + (uint64_t)zchunk, z_end);
+    const int np = (int)(zb - za) + 2;
+    const int64_t x0 = (int64_t)(tile % tiles_x) * kTX, y0 = (int64_t)(tile / tiles_x) * kTY;
+    const uint64_t nx = d.nx, ny = d.ny;
+    const int64_t xs = x0 - kCofs;
+    const int cofs = kCofs;
+    ring.init(4);
+    auto issue = [&](int k) {
+        mbar_expect_tx(ring.full + (k % S), kBY * BX * 8);
+        tma3d(ring.stage(k), &tm, ring.full + (k % S), (int)xs, (int)(y0 - 1), (int)(za - 1 + k));
+    };
+    // stage index of (row y0-1+j, column x0-1+i), column clamped into the box
+    auto at = [&](int j, int i) { return j * BX + min(max(i - 1 + cofs, 0), BX - 1); };
+    if (tid == 0)
+        for (int k = 0; k < S && k < np; ++k) issue(k);
+
+    double fa[3], fb[3], fc[3];
+#pragma unroll
+    for (int kb = 0; kb < 3; ++kb) {
+        const int kk = 4 * kb + c;
+        if (KIND == 0) {
+            fa[kb] = bandv(kk, r, d.w[3], d.w[0], d.w[4]);
+            fb[kb] = bandv(kk, r, d.w[5], 0.0, d.w[6]);
+            fc[kb] = 0.0;
+        } else {
+            fa[kb] = bandv(kk, r, d.w[1], d.w[0], d.w[1]);
+            fb[kb] = bandv(kk, r, d.w[2], d.w[1], d.w[2]);
+            fc[kb] = bandv(kk, r, d.w[3], d.w[2], d.w[3]);
+        }
+    }
+    double gen[KIND == 2 ? 27 : 1];
+    if (KIND == 2) {
+#pragma unroll
+        for (int q = 0; q < 9; ++q)
+#pragma unroll
+            for (int kb = 0; kb < 3; ++kb)
+                gen[q * 3 + kb] = bandv(4 * kb + c, r, d.w[q * 3 + 0], d.w[q * 3 + 1], d.w[q * 3 + 2]);
+    }
+
+    const int64_t yo = y0 + 8 * rb + r;
+    const bool row_ok = yo >= 1 && yo <= (int64_t)ny - 2;
+    for (int i = 0; i + 2 < np; ++i) {  // output plane za + i uses items i, i+1, i+2
+        if (i == 0) {
+            ring.wait_full(0);
+            ring.wait_full(1);
+        }
+        ring.wait_full(i + 2);
+        const double* Pm = ring.stage(i);
+        const double* P0 = ring.stage(i + 1);
+        const double* Pp = ring.stage(i + 2);
+        double D0[4], D1[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int cb = cb0 + t;
+            double d0 = 0.0, d1 = 0.0;
+            if (KIND == 0) {
+                const int s = at(8 * rb + r + 1, 8 * cb + 2 * c + 1);
+                d0 = fma(d.w[2], Pp[s], d.w[1] * Pm[s]);
+                d1 = fma(d.w[2], Pp[s + 1], d.w[1] * Pm[s + 1]);
+#pragma unroll
+                for (int kb = 0; kb < 3; ++kb) {
+                    const int j = min(4 * kb + c, 9);
+                    dmma_m8n8k4(d0, d1, fa[kb], P0[at(8 * rb + j, 8 * cb + r + 1)], d0, d1);
+                }
+#pragma unroll
+                for (int kb = 0; kb < 3; ++kb) {
+                    const int j = min(4 * kb + c, 9);
+                    dmma_m8n8k4(d0, d1, P0[at(8 * rb + r + 1, 8 * cb + j)], fb[kb], d0, d1);
+                }
+            } else if (KIND == 1) {
+#pragma unroll
+                for (int kb = 0; kb < 3; ++kb) {
+                    const int colj = 8 * cb + min(4 * kb + c, 9);
+                    const int up = at(8 * rb + r, colj), mid = at(8 * rb + r + 1, colj),
+                              dn = at(8 * rb + r + 2, colj);
+                    const double a0 = P0[mid];
+                    const double a1 = (P0[up] + P0[dn]) + (Pm[mid] + Pp[mid]);
+                    const double a2 = (Pm[up] + Pm[dn]) + (Pp[up] + Pp[dn]);
+                    dmma_m8n8k4(d0, d1, a0, fa[kb], d0, d1);
+                    dmma_m8n8k4(d0, d1, a1, fb[kb], d0, d1);
+                    dmma_m8n8k4(d0, d1, a2, fc[kb], d0, d1);
+                }
+            } else {
+#pragma unroll
+                for (int dz = 0; dz < 3; ++dz) {
+                    const double* P = dz == 0 ? Pm : (dz == 1 ? P0 : Pp);
+#pragma unroll
+                    for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+                        for (int kb = 0; kb < 3; ++kb) {
+                            const int colj = 8 * cb + min(4 * kb + c, 9);
+                            dmma_m8n8k4(d0, d1, P[at(8 * rb + r + dy, colj)], gen[(dz * 3 + dy) * 3 + kb], d0,
+                                        d1);
+                        }
+                }
+            }
+            D0[t] = d0;
+            D1[t] = d1;
+        }
+        ring.release(i);
+        if (tid == 0 && i + S < np) {
+            ring.wait_empty(i);
+            issue(i + S);
+        }
+        if (row_ok) {
+            const uint64_t z = za + (uint64_t)i;
+            double* vr = v + (z * ny + (uint64_t)yo) * nx;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const int64_t xx = x0 + 8 * (cb0 + t) + 2 * c;
+                const bool i0 = xx >= 1 && xx <= (int64_t)nx - 2, i1 = xx + 1 <= (int64_t)nx - 2;
+                if (i0 && i1)
+                    asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(vr + xx), "d"(D0[t]), "d"(D1[t]) : "memory");
+                else {
+                    if (i0) vr[xx] = D0[t];
+                    if (xx + 1 >= 1 && i1) vr[xx + 1] = D1[t];
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host: tensor maps
+// ---------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+bool make_map(CUtensorMap* m, const double* base, int rank, const uint64_t* dims, uint32_t box_x) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t gdim[3] = {dims[0], dims[1], rank == 3 ? dims[2] : 1};
+    cuuint64_t gstride[2] = {dims[0] * 8, dims[0] * dims[1] * 8};
+    cuuint32_t box[3] = {box_x, (cuuint32_t)kBY, 1};
+    cuuint32_t estride[3] = {1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)rank, const_cast<double*>(base), gdim, gstride,
+              box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <class K>
+cudaError_t prep(K kernel, size_t smem) {
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+bool class_weights(const double* w, double g[4]) {
+    bool seen[4] = {false, false, false, false};
+    for (int dz = -1; dz <= 1; ++dz)
+        for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                const int m = (dz != 0) + (dy != 0) + (dx != 0);
+                const double ww = w[(dz + 1) * 9 + (dy + 1) * 3 + (dx + 1)];
+                if (!seen[m]) { g[m] = ww; seen[m] = true; }
+                else if (g[m] != ww) return false;
+            }
+    return true;
+}
+
+// Split the marched axis so the grid fills about `per_sm` CTAs per SM.  For
+// the CUDA-core kernels the measured optimum is one chunk per tile (a full
+// march, ~1.7 CTAs/SM at the BASELINE grids); the tensor-core 3D kernels
+// need more warps in flight to cover the DMMA chains.
+int split_count(uint64_t tiles, uint64_t extent, int min_chunk, int per_sm) {
+    const uint64_t slots = (uint64_t)kNumSMs * (uint64_t)per_sm;
+    uint64_t n = tiles >= slots ? 1 : slots / tiles;
+    const uint64_t cap = (extent + min_chunk - 1) / min_chunk;
+    if (n > cap) n = cap;
+    if (n < 1) n = 1;
+    return (int)n;
+}
+
+}  // namespace
+
+bool stencil_tma_eligible(const StencilDesc& d, const double* u, const double* v) {
+    if (!tuning().stencil_tma) return false;
+    if (d.preset != kP2d5 && d.preset != kP3d7 && d.preset != kP3d27) return false;
+    if (d.nx % 2 != 0) return false;  // row pitch must be a multiple of 16 bytes
+    if ((reinterpret_cast<uintptr_t>(u) & 15) || (reinterpret_cast<uintptr_t>(v) & 15)) return false;
+    if (d.nx > (1ull << 31) || d.ny > (1ull << 31) || d.nz > (1ull << 31)) return false;
+    return encode_fn() != nullptr;
+}
+
+cudaError_t launch_stencil_tma(int unit, const StencilDesc& d, uint64_t o0, uint64_t o1, const double* u,
+                               double* v, cudaStream_t s) {
+    const uint64_t dims[3] = {d.nx, d.ny, d.nz};
+    CUtensorMap m;
+    if (!make_map(&m, u, d.dim, dims, kBX)) return cudaErrorInvalidValue;
+    cudaError_t e;
+    if (d.dim == 2) {
+        const int strips = (int)((d.nx + kTX - 1) / kTX);
+        const int nseg = split_count(strips, o1 - o0, 64,
+                                     unit == 1 ? tuning().stencil_tc_ctas_per_sm : tuning().stencil_ctas_per_sm);
+        int seg_rows = (int)(((o1 - o0 + nseg - 1) / nseg + kTY - 1) / kTY * kTY);
+        const int segs = (int)((o1 - o0 + seg_rows - 1) / seg_rows);
+        const unsigned grid = (unsigned)(strips * segs);
+        if (unit == 1) {
+            constexpr int S = 4;
+            const size_t sm = ring_bytes<S, kBX>();
+            if ((e = prep(st2d_tma_tc<S>, sm)) != cudaSuccess) return e;
+            st2d_tma_tc<S><<<grid, 128, sm, s>>>(m, v, d.nx, o0, o1, seg_rows, strips, d);
+        } else {
+            constexpr int S = 4;
+            const size_t sm = ring_bytes<S, kBX>();
+            if ((e = prep(st2d_tma_cc<S>, sm)) != cudaSuccess) return e;
+            st2d_tma_cc<S><<<grid, 128, sm, s>>>(m, v, d.nx, o0, o1, seg_rows, strips, d);
+        }
+        note_launch();
+        return cudaGetLastError();
+    }
+    const int tiles_x = (int)((d.nx + kTX - 1) / kTX);
+    const int tiles_xy = tiles_x * (int)((d.ny + kTY - 1) / kTY);
+    const int nch = split_count(tiles_xy, o1 - o0, 8,
+                                unit == 1 ? tuning().stencil_tc3d_ctas_per_sm : tuning().stencil_ctas_per_sm);
+    const int zchunk = (int)((o1 - o0 + nch - 1) / nch);
+    const int zch = (int)((o1 - o0 + zchunk - 1) / zchunk);
+    const unsigned grid = (unsigned)(tiles_xy * zch);
+    StencilDesc dd = d;
+    int kind = 0;
+    if (d.preset == kP3d27) {
+        double g[4];
+        if (class_weights(d.w, g)) {
+            kind = 2;
+            for (int i = 0; i < 4; ++i) dd.w[i] = g[i];
+        } else {
+            kind = 1;
+        }
+    }
+    if (unit == 1) {
+        constexpr int S = 5;
+        const size_t sm = ring_bytes<S, kBX>();
+        const int tk = kind == 0 ? 0 : (kind == 2 ? 1 : 2);  // TC kinds: 0 7pt, 1 class, 2 general
+#define RLB_TC3(K)                                                                            \
+    do {                                                                                      \
+        if ((e = prep(st3d_tma_tc<K, S>, sm)) != cudaSuccess) return e;                      \
+        st3d_tma_tc<K, S><<<grid, 128, sm, s>>>(m, v, dd, o0, o1, zchunk, tiles_x, tiles_xy); \
+    } while (0)
+        if (tk == 0) RLB_TC3(0); else if (tk == 1) RLB_TC3(1); else RLB_TC3(2);
+#undef RLB_TC3
+    } else {
+        constexpr int S = 4;
+        const size_t sm = ring_bytes<S, kBX>();
+#define RLB_CC3(K)                                                                            \
+    do {                                                                                      \
+        if ((e = prep(st3d_tma_cc<K, S>, sm)) != cudaSuccess) return e;                      \
+        st3d_tma_cc<K, S><<<grid, 128, sm, s>>>(m, v, dd, o0, o1, zchunk, tiles_x, tiles_xy); \
+    } while (0)
+        if (kind == 0) RLB_CC3(0); else if (kind == 1) RLB_CC3(1); else RLB_CC3(2);
+#undef RLB_CC3
+    }
+    note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace rlb

@@ -159,10 +159,14 @@ cudaError_t launch_scale(int unit, double* a, const double* b, double q, uint64_
     const uint64_t body = n - head;
     const uint64_t nvec = body / 4;
     if (nvec) {
-        constexpr int kUnroll = 4;
-        uint64_t blocks = (nvec + (uint64_t)threads * kUnroll - 1) / ((uint64_t)threads * kUnroll);
+        const int U = t.scale_unroll;
+        uint64_t blocks = (nvec + (uint64_t)threads * U - 1) / ((uint64_t)threads * U);
         if (blocks > max_blocks) blocks = max_blocks;
-        scale_cc_v4<kUnroll><<<(unsigned)blocks, threads, 0, s>>>(a + head, b + head, q, nvec); note_launch();
+        if (U == 1) scale_cc_v4<1><<<(unsigned)blocks, threads, 0, s>>>(a + head, b + head, q, nvec);
+        else if (U == 2) scale_cc_v4<2><<<(unsigned)blocks, threads, 0, s>>>(a + head, b + head, q, nvec);
+        else if (U == 8) scale_cc_v4<8><<<(unsigned)blocks, threads, 0, s>>>(a + head, b + head, q, nvec);
+        else scale_cc_v4<4><<<(unsigned)blocks, threads, 0, s>>>(a + head, b + head, q, nvec);
+        note_launch();
     }
     const uint64_t tail = body - nvec * 4;
     if (tail) { scale_cc_scalar<<<1, 32, 0, s>>>(a + head + nvec * 4, b + head + nvec * 4, q, tail); note_launch(); }

@@ -1,0 +1,53 @@
+"""Run each hot kernel a few times at its BASELINE config (for ncu captures).
+
+  python tools/prof_kernels.py [names...]   names: stream_cc stream_tc spmv_cc spmv_tc
+        2d5pt_cc 2d5pt_tc 3d7pt_cc 3d7pt_tc 3d27pt_cc 3d27pt_tc (default: all)
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2502_16851_b200 as P  # noqa: E402
+
+REPS = int(os.environ.get("PROF_REPS", "3"))
+
+
+def run(name):
+    kern, unit = name.rsplit("_", 1)
+    unit = P.CUDA_CORE if unit == "cc" else P.TENSOR_CORE
+    if kern == "stream":
+        n = 1 << 27
+        b = torch.empty(n, dtype=torch.float64, device="cuda")
+        P.fill_uniform(b, 1, 1, 0, 1)
+        a = torch.empty_like(b)
+        for _ in range(REPS):
+            P.scale(a, b, 3.0, unit=unit)
+    elif kern == "spmv":
+        n, k, hb = 1 << 22, 16, 65536
+        rp = torch.empty(n + 1, dtype=torch.int32, device="cuda")
+        col = torch.empty(n * k, dtype=torch.int32, device="cuda")
+        val = torch.empty(n * k, dtype=torch.float64, device="cuda")
+        x = torch.empty(n, dtype=torch.float64, device="cuda")
+        y = torch.empty(n, dtype=torch.float64, device="cuda")
+        P.gen_band_csr(n, 0, n, k, hb, 1, rp, col, val)
+        P.fill_uniform(x, 1, 4, 0, 1)
+        for _ in range(REPS):
+            P.spmv_csr(rp, col, val, x, y, unit=unit)
+    else:
+        shape = (16384, 16384) if kern == "2d5pt" else (512, 512, 512)
+        u = torch.empty(shape, dtype=torch.float64, device="cuda")
+        P.stencil_init(u, 1, 1)
+        v = u.clone()
+        P.stencil(kern, u, v, REPS, unit=unit)
+    torch.cuda.synchronize()
+
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or ["stream_cc", "stream_tc", "spmv_cc", "spmv_tc", "2d5pt_cc", "2d5pt_tc",
+                             "3d7pt_cc", "3d7pt_tc", "3d27pt_cc", "3d27pt_tc"]
+    for nm in names:
+        run(nm)
+        torch.cuda.empty_cache()
+    print("ok", names)

@@ -1,0 +1,83 @@
+"""Tuning sweeps over the rl_tuning_set knobs (CUDA-event timing, GB/s of
+algorithmic bytes).  python tools/sweep.py stream|spmv|... > out.jsonl"""
+import itertools
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2502_16851_b200 as P  # noqa: E402
+
+
+def timeit(fn, reps=20, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / reps
+
+
+def sweep(name, fn, nbytes, grid):
+    keys = list(grid)
+    for vals in itertools.product(*[grid[k] for k in keys]):
+        for k, v in zip(keys, vals):
+            P.tuning_set(k, v)
+        ms = timeit(fn)
+        print(json.dumps({"kernel": name, **dict(zip(keys, vals)), "ms": round(ms, 5),
+                          "gbs": round(nbytes / ms / 1e6, 1)}), flush=True)
+
+
+def main(which):
+    if which == "stream":
+        n = 1 << 27
+        b = torch.empty(n, dtype=torch.float64, device="cuda")
+        P.fill_uniform(b, 1, 1, 0, 1)
+        a = torch.empty_like(b)
+        for unit in (0, 1):
+            sweep(f"stream_{'cc' if unit == 0 else 'tc'}", lambda: P.scale(a, b, 3.0, unit=unit), 16 * n,
+                  {"scale_unroll": [1, 2, 4, 8] if unit == 0 else [4],
+                   "scale_blocks_per_sm": [1, 2, 4, 8, 16, 32]})
+    elif which == "spmv":
+        n, k, hb = 1 << 22, 16, 65536
+        rp = torch.empty(n + 1, dtype=torch.int32, device="cuda")
+        col = torch.empty(n * k, dtype=torch.int32, device="cuda")
+        val = torch.empty(n * k, dtype=torch.float64, device="cuda")
+        x = torch.empty(n, dtype=torch.float64, device="cuda")
+        y = torch.empty(n, dtype=torch.float64, device="cuda")
+        P.gen_band_csr(n, 0, n, k, hb, 1, rp, col, val)
+        P.fill_uniform(x, 1, 4, 0, 1)
+        nbytes = P.spmv_csr_model(n, n, n * k).traffic_bytes
+        sweep("spmv_cc", lambda: P.spmv_csr(rp, col, val, x, y, unit=0), nbytes,
+              {"spmv_rows": [1, 2, 4], "spmv_sched": [0, 1], "spmv_xhint": [0, 1, 2],
+               "spmv_blocks_per_sm": [4, 8, 16, 32]})
+        sweep("spmv_tc", lambda: P.spmv_csr(rp, col, val, x, y, unit=1), nbytes,
+              {"spmv_blocks_per_sm": [4, 8, 16, 32]})
+
+
+def stencils():
+    import math
+    for preset, shape in (("2d5pt", (16384, 16384)), ("3d7pt", (512, 512, 512)), ("3d27pt", (512, 512, 512))):
+        u = torch.empty(shape, dtype=torch.float64, device="cuda")
+        P.stencil_init(u, 1, 1)
+        v = u.clone()
+        nbytes = 2 * 16 * math.prod(s - 2 for s in shape)
+        for unit in (0, 1):
+            sweep(f"{preset}_{'cc' if unit == 0 else 'tc'}", lambda: P.stencil(preset, u, v, 2, unit=unit),
+                  nbytes, {"stencil_tma": [0, 1], "stencil_ctas_per_sm": [2, 3, 4, 5, 8]})
+        del u, v
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    for w in sys.argv[1:]:
+        if w == "stencil":
+            stencils()
+        else:
+            main(w)
