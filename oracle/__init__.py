@@ -36,6 +36,7 @@ _ORC_SIGS = {
     "orc_default_weights": (_int, [C.c_char_p, _ptr]),
     "orc_stencil_init": (None, [_ptr, _u64, _u64, _u64, _int, _u64, _u64, _int, _u64]),
     "orc_stencil": (_int, [C.c_char_p, _U64P, _ptr, _u64, _ptr, _ptr]),
+    "orc_stencil_sweep": (_int, [C.c_char_p, _U64P, _ptr, _u64, _u64, _ptr, _ptr]),
     "orc_rel_err": (_dbl, [_ptr, _ptr, _u64]),
     "orc_bit_mismatches": (_u64, [_ptr, _ptr, _u64]),
     "orc_num_threads": (_int, []),
@@ -166,6 +167,20 @@ def stencil(preset: str, u: np.ndarray, steps: int, weights=None) -> np.ndarray:
     if rc:
         raise ValueError(f"orc_stencil rc={rc}")
     return a if steps % 2 == 0 else b
+
+
+def stencil_sweep(preset: str, u: np.ndarray, v: np.ndarray, o0: int, o1: int, weights=None) -> None:
+    """v = S(u) over outer indices [o0, o1) of u's own grid (in place into v)."""
+    assert u.flags["C_CONTIGUOUS"] and v.flags["C_CONTIGUOUS"] and u.shape == v.shape
+    if u.ndim == 2:
+        dims = (_u64 * 3)(u.shape[1], u.shape[0], 1)
+    else:
+        dims = (_u64 * 3)(u.shape[2], u.shape[1], u.shape[0])
+    w = None if weights is None else np.ascontiguousarray(weights, np.float64)
+    rc = orc().orc_stencil_sweep(preset.encode(), dims, _p(w) if w is not None else None, o0, o1,
+                                 _p(u), _p(v))
+    if rc:
+        raise ValueError(f"orc_stencil_sweep rc={rc}")
 
 
 def rel_err(a: np.ndarray, b: np.ndarray) -> float:

@@ -255,16 +255,23 @@ ORC_API void orc_stencil_init(double* u, uint64_t nx, uint64_t ny, uint64_t nz, 
     }
 }
 
+/* Outer range [olo, ohi) (rows in 2D, planes in 3D) is clipped to the
+ * interior; the full-grid sweep passes [0, n_outer). */
 static void sweep_generic(int n_off, const off3* o, const double* w, uint64_t nx,
                           uint64_t ny, uint64_t nz, int r, int is2d, const double* u,
-                          double* v) {
+                          double* v, uint64_t olo, uint64_t ohi) {
     const int64_t sx = 1, sy = (int64_t)nx, sz = (int64_t)(nx * ny);
     int64_t d[64];
     for (int s = 0; s < n_off; ++s) d[s] = o[s].dz * sz + o[s].dy * sy + o[s].dx * sx;
-    const uint64_t zlo = is2d ? 0 : (uint64_t)r, zhi = is2d ? 1 : nz - r;
+    const uint64_t n_outer = is2d ? ny : nz;
+    const uint64_t lo = olo > (uint64_t)r ? olo : (uint64_t)r;
+    const uint64_t hi = ohi < n_outer - r ? ohi : n_outer - r;
+    const uint64_t zlo = is2d ? 0 : lo, zhi = is2d ? 1 : hi;
+    const uint64_t ylo = is2d ? lo : (uint64_t)r, yhi = is2d ? hi : ny - r;
+    if (lo >= hi) return;
 #pragma omp parallel for collapse(2) schedule(static)
     for (int64_t z = (int64_t)zlo; z < (int64_t)zhi; ++z)
-        for (int64_t y = r; y < (int64_t)(ny - r); ++y) {
+        for (int64_t y = (int64_t)ylo; y < (int64_t)yhi; ++y) {
             const int64_t base = z * sz + y * sy;
             for (int64_t x = r; x < (int64_t)(nx - r); ++x) {
                 const int64_t p = base + x;
@@ -363,8 +370,24 @@ ORC_API int orc_stencil(const char* preset, const uint64_t* dims, const double* 
         if (!strcmp(preset, "2d5pt")) sweep_2d5(w, nx, ny, src, dst);
         else if (!strcmp(preset, "3d7pt")) sweep_3d7(w, nx, ny, nz, src, dst);
         else if (!strcmp(preset, "3d27pt")) sweep_3d27(w, nx, ny, nz, src, dst);
-        else sweep_generic(n_off, o, w, nx, ny, nz, r, dim == 2, src, dst);
+        else sweep_generic(n_off, o, w, nx, ny, nz, r, dim == 2, src, dst, 0, dim == 2 ? ny : nz);
     }
+    return 0;
+}
+
+/* One sweep v = S(u) over outer indices [o0, o1) (clipped to the interior):
+ * the slab building block the distributed tests check against. */
+ORC_API int orc_stencil_sweep(const char* preset, const uint64_t* dims, const double* weights,
+                              uint64_t o0, uint64_t o1, const double* u, double* v) {
+    int dim, npts, r;
+    if (preset_info(preset, &dim, &npts, &r)) return 1;
+    const uint64_t nx = dims[0], ny = dims[1], nz = dim == 3 ? dims[2] : 1;
+    double w[64];
+    if (weights) memcpy(w, weights, sizeof(double) * (size_t)npts);
+    else orc_default_weights(preset, w);
+    off3 o[64];
+    const int n_off = preset_offsets(preset, o);
+    sweep_generic(n_off, o, w, nx, ny, nz, r, dim == 2, u, v, o0, o1);
     return 0;
 }
 

@@ -305,8 +305,7 @@ double unoverlapped_speedup(double t_cmp, double t_mem, double t_others, double 
         throw Error(ErrorKind::ValidationError, "time breakdown is all zero");
     need_alpha(alpha);
     if (t_cmp == 0.0) return 1.0;
-    const double rest = t_mem + t_others;
-    return (t_cmp + rest) / (t_cmp / alpha + rest);
+    return (t_cmp + t_mem + t_others) / (t_cmp / alpha + t_mem + t_others);
 }
 
 double kernel_speedup_ceiling(double alpha, double balance, double intensity, int* n_warnings) {

@@ -92,8 +92,7 @@ def spmv_halo_ops(part: SpmvPartition, x_win: torch.Tensor):
     own = x_win[part.own_slice()]
     if part.rank > 0:
         ops.append(dist.P2POp(dist.irecv, x_win[: part.lo_halo], part.rank - 1))
-        ops.append(dist.P2POp(dist.isend, own[: part.hb].contiguous() if not own[: part.hb].is_contiguous()
-                              else own[: part.hb], part.rank - 1))
+        ops.append(dist.P2POp(dist.isend, own[: part.hb], part.rank - 1))
     if part.rank < part.world - 1:
         ops.append(dist.P2POp(dist.irecv, x_win[part.lo_halo + part.rows:], part.rank + 1))
         ops.append(dist.P2POp(dist.isend, own[part.rows - part.hb:], part.rank + 1))

@@ -1,0 +1,175 @@
+"""Accounting parity (CPU): the product's W/Q models, presets, bounds, roofline
+and spec loading against the REFERENCE library.
+
+Two sources, same assertions:
+  * tests/golden/accounting.json -- fixtures produced by running the reference
+    library (tests/golden/make_golden.py); available everywhere;
+  * oracle/_ref -- the reference library itself, queried live (this container;
+    skipped where the prebuilt shim is absent).
+Integers must match exactly; doubles bit-exactly (the product evaluates the
+same formulas in the same order, e.g. tensor_core_ceiling's 1+(a-1)/(1+a)
+form, reference bounds.cpp:87-97).
+"""
+import ctypes as C
+import json
+import os
+import random
+
+import pytest
+
+import oracle as O
+import paper_2502_16851_b200 as P
+
+GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "accounting.json")))
+
+
+def _call(fn, args, doc=None):
+    """Run the product's equivalent of a golden case -> dict like the fixture."""
+    try:
+        if fn == "scale_model":
+            k = P.scale_model(args[0], args[1])
+            return {"work": k.work_flops, "traffic": k.traffic_bytes}
+        if fn == "gemv_model":
+            k = P.gemv_model(*args)
+            return {"work": k.work_flops, "traffic": k.traffic_bytes}
+        if fn == "spmv_generic_model":
+            k = P.spmv_generic_model(*args)
+            return {"work": k.work_flops, "traffic": k.traffic_bytes}
+        if fn == "spmv_csr_model":
+            k = P.spmv_csr_model(*args)
+            return {"work": k.work_flops, "traffic": k.traffic_bytes}
+        if fn == "stencil_model":
+            k = P.stencil_model(args[0], args[1], args[2])
+            return {"work": k.work_flops, "traffic": k.traffic_bytes,
+                    "points": P.stencil_preset(args[0])[1]}
+        if fn == "kernel_speedup_ceiling":
+            v, nw = P.kernel_speedup_ceiling(*args)
+            return {"value": v, "warnings": nw}
+        if fn == "tensor_core_ceiling":
+            return {"value": P.tensor_core_ceiling(*args)}
+        if fn == "workload_ceiling":
+            return {"value": P.workload_ceiling(*args)}
+        if fn == "min_temporal_depth":
+            return {"value": P.min_temporal_depth(*args)}
+        if fn == "tc_scale_trick_throughput":
+            return {"value": P.tc_scale_trick_throughput(*args)}
+        if fn == "unoverlapped_speedup":
+            return {"value": P.unoverlapped_speedup(*args)}
+        if fn in ("machine_balance", "attainable", "tensor_alpha"):
+            bw, pcc, ptc = args[:3]
+            spec = P.HardwareSpec("probe", bw, 0.0, pcc, ptc)
+            if fn == "machine_balance":
+                return {"value": P.machine_balance(spec, args[3])}
+            if fn == "attainable":
+                return {"value": P.attainable(spec, args[4], args[3])}
+            return {"value": P.tensor_alpha(spec)}
+        if fn == "classify":
+            return {"value": P.classify(*args)}
+        if fn == "load_spec":
+            s = P.load_spec(doc)
+            return {"bw": s.memory_bandwidth, "l2": s.l2_cache_bytes, "p_cc": s.peak_cuda_core,
+                    "p_tc": s.peak_tensor_core}
+        if fn == "builtin_spec":
+            s = P.builtin_spec(args[0])
+            return {"bw": s.memory_bandwidth, "l2": s.l2_cache_bytes, "p_cc": s.peak_cuda_core,
+                    "p_tc": s.peak_tensor_core}
+    except P.RooflensError as e:
+        return {"error": e.kind}
+    raise AssertionError(f"unhandled case {fn}")
+
+
+@pytest.mark.parametrize("case", GOLDEN["cases"], ids=lambda c: f"{c['fn']}{c['args']}")
+def test_golden_against_reference_fixture(case):
+    want = {k: v for k, v in case.items() if k not in ("fn", "args", "doc")}
+    got = _call(case["fn"], case["args"], case.get("doc"))
+    assert got == want
+
+
+def test_error_message_format_matches_reference():
+    """rooflens::Error prefixes the kind (reference error.hpp:38-40)."""
+    with pytest.raises(P.RooflensError) as e:
+        P.spmv_csr_model(10, 10, 101)
+    assert str(e.value).startswith("ValidationError: ")
+    with pytest.raises(P.RooflensError) as e:
+        P.stencil_model("9d999pt")
+    assert e.value.kind == "ValidationError" and "unknown stencil preset" in str(e.value)
+
+
+ref_only = pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref (reference build) absent")
+
+
+@ref_only
+def test_random_models_match_live_reference():
+    """Randomised sweep against the live reference library."""
+    R = O.ref()
+    rng = random.Random(1234)
+    for _ in range(3000):
+        m, n = rng.randint(1, 1 << 40), rng.randint(1, 1 << 40)
+        nnz = rng.randint(0, min(m * n, 1 << 50))
+        ib = rng.choice([0, 1, 2, 3, 4, 8, 16])
+        prec = rng.randint(0, 2)
+        w, q = C.c_uint64(), C.c_uint64()
+        rc = R.ref_spmv_csr_model(m, n, nnz, ib, prec, C.byref(w), C.byref(q))
+        try:
+            k = P.spmv_csr_model(m, n, nnz, ib, prec)
+        except P.RooflensError as e:
+            assert rc == e.code, (m, n, nnz, ib, R.ref_last_error())
+        else:
+            assert rc == 0 and (k.work_flops, k.traffic_bytes) == (w.value, q.value)
+        sn = rng.choice([0, 1, rng.randint(1, 1 << 63)])
+        rc = R.ref_scale_model(sn, prec, C.byref(w), C.byref(q))
+        try:
+            k = P.scale_model(sn, prec)
+        except P.RooflensError as e:
+            assert rc == e.code
+        else:
+            assert rc == 0 and (k.work_flops, k.traffic_bytes) == (w.value, q.value)
+
+
+@ref_only
+def test_random_bounds_match_live_reference():
+    R = O.ref()
+    rng = random.Random(99)
+    for _ in range(3000):
+        a = rng.choice([rng.uniform(0.5, 4.0), 1.0, 2.0])
+        b = rng.uniform(0.01, 20.0)
+        i = rng.choice([rng.uniform(1e-3, 30.0), 0.0])
+        o, nw = C.c_double(), C.c_int()
+        rc = R.ref_kernel_speedup_ceiling(a, b, i, C.byref(o), C.byref(nw))
+        try:
+            v, w = P.kernel_speedup_ceiling(a, b, i)
+        except P.RooflensError as e:
+            assert rc == e.code
+        else:
+            assert rc == 0 and v == o.value and w == nw.value
+        t = C.c_uint64()
+        rc = R.ref_min_temporal_depth(b, i, C.byref(t))
+        try:
+            v = P.min_temporal_depth(b, i)
+        except P.RooflensError as e:
+            assert rc == e.code
+        else:
+            assert rc == 0 and v == t.value
+
+
+def test_stencil_presets_and_default_weights():
+    expect = {"2d5pt": (2, 5, 1), "2d9pt": (2, 9, 1), "2d13pt": (2, 13, 3), "2d49pt": (2, 49, 3),
+              "3d7pt": (3, 7, 1), "3d27pt": (3, 27, 1)}
+    for name, info in expect.items():
+        assert P.stencil_preset(name) == info
+        w = P.stencil_default_weights(name)
+        assert len(w) == info[1]
+        assert w == list(O.default_weights(name))  # oracle restates BASELINE.json's rule
+        assert abs(sum(w) - 1.0) < 1e-15
+    w27 = P.stencil_default_weights("3d27pt")
+    assert w27[13] == (1.0 / 1.0) / 10.0 and w27[0] == (1.0 / 4.0) / 10.0  # raw/S, S = 10
+
+
+def test_baseline_known_answers():
+    """SURVEY.md §4 known-answer pins, computed by the reference library."""
+    assert P.scale_model(1 << 27) == P.KernelCharacterization(134217728, 2147483648)
+    assert P.spmv_csr_model(1 << 22, 1 << 22, 1 << 26) == P.KernelCharacterization(134217728, 889192452)
+    assert P.stencil_model("2d5pt") == P.KernelCharacterization(10, 16)
+    assert P.stencil_model("3d7pt") == P.KernelCharacterization(14, 16)
+    assert P.stencil_model("3d27pt") == P.KernelCharacterization(54, 16)
+    assert P.tensor_core_ceiling(2.0) == 4.0 / 3.0
