@@ -172,9 +172,21 @@ class Spmv:
                 "y": t.empty(self.y.shape, dtype=t.float64, **pin)}
 
     def e2e_step(self, h, unit):
+        """The iterative-solver call pattern: A was uploaded once into a plan
+        (rl_spmv_plan_create, outside the timed region); each step moves x in
+        and y out through pinned host memory (rl_spmv_plan_execute_host)."""
+        if "plan" not in h:
+            h["plan"] = self.P.SpmvPlan(h["rp"], h["col"], h["val"], h["x"].numel(), unit=unit)
+        h["plan"].execute_host(h["x"], h["y"])
+
+    def full_copy_step(self, h, unit):
+        """Everything over PCIe every step (rl_spmv_csr_host)."""
         self.P.spmv_csr_host(h["rp"], h["col"], h["val"], h["x"], h["y"], unit=unit)
 
     def h2d_d2h(self, h):
+        return h["x"].numel() * 8, h["y"].numel() * 8
+
+    def full_copy_bytes(self, h):
         return (sum(h[k].numel() * h[k].element_size() for k in ("rp", "col", "val", "x")),
                 h["y"].numel() * 8)
 
@@ -458,7 +470,7 @@ def main():
     ap.add_argument("--unit", default="cc", choices=["cc", "tc"])
     ap.add_argument("--no-per-kernel", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=20)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -514,6 +526,23 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_val = wl.job_bytes * args.e2e_steps / e2e_s / 1e9
+    full_copy = None
+    if hasattr(wl, "full_copy_step"):
+        wl.full_copy_step(h, unit)
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            wl.full_copy_step(h, unit)
+        fc_s = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([fc_s], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            fc_s = float(t.item())
+        fi, fo = wl.full_copy_bytes(h)
+        full_copy = {"value": round(wl.job_bytes * args.e2e_steps / fc_s / 1e9, 3), "unit": "GB/s",
+                     "h2d_bytes_per_step": fi, "d2h_bytes_per_step": fo,
+                     "api": "rl_spmv_csr_host (CSR + x over PCIe every step)"}
+    if "plan" in h:
+        h["plan"].close()
     del h
 
     traffic = ncu_traffic().get(f"{args.workload}_{args.unit}")
@@ -534,7 +563,11 @@ def main():
                      "launch_ms_p50": round(per_sorted[len(per_sorted) // 2], 5)},
         "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
-                "api": "rl_*_host C-ABI (pinned host buffers, copies inside the timed call)"},
+                "api": ("rl_spmv_plan_execute_host: A resident (uploaded once by rl_spmv_plan_create), "
+                        "x H2D and y D2H from pinned host memory inside every timed call"
+                        if args.workload == "spmv" else
+                        "rl_*_host C-ABI (pinned host buffers, copies inside the timed call)")},
+        "e2e_full_copy": full_copy,
         "gpu_launches": timed_launches,
         "clocks": clk.summary(),
     }

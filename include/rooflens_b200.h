@@ -159,6 +159,21 @@ RL_API int rl_spmv_csr_host(rl_unit unit, rl_precision precision, uint64_t m, ui
 RL_API int rl_stencil_host(rl_unit unit, rl_precision precision, const char* preset,
                     const uint64_t* dims, const double* weights, uint64_t steps, double* u,
                     double* v, rl_kchar* out);
+/* SpMV plan: the CSR matrix is uploaded once (the iterative-solver pattern:
+ * A is fixed, x changes every step) and each execute moves only x in and y
+ * out.  execute_host pipelines the x upload, the row-chunk kernels and the y
+ * download on three streams: row chunk c starts as soon as the x prefix it
+ * references (max column, computed at creation) has arrived.  The plan owns
+ * its device buffers; no allocation happens in execute. */
+typedef struct rl_spmv_plan_s* rl_spmv_plan;
+RL_API int rl_spmv_plan_create(rl_unit unit, rl_precision precision, uint64_t m, uint64_t n,
+                               uint64_t nnz, const int32_t* row_ptr, const int32_t* col,
+                               const double* val, rl_spmv_plan* out);
+RL_API int rl_spmv_plan_execute_host(rl_spmv_plan plan, const double* x, double* y, rl_kchar* out);
+RL_API int rl_spmv_plan_execute(rl_spmv_plan plan, const double* x_dev, double* y_dev,
+                                rl_stream stream, rl_kchar* out);
+RL_API int rl_spmv_plan_destroy(rl_spmv_plan plan);
+
 /* Release the device/pinned workspaces cached by the _host entry points. */
 RL_API int rl_host_workspace_release(void);
 

@@ -32,7 +32,7 @@ __all__ = [
     "HardwareSpec", "lib", "library_path", "scale_model", "gemv_model", "spmv_generic_model",
     "spmv_csr_model", "stencil_model", "stencil_preset", "stencil_default_weights", "scale",
     "spmv_csr", "spmv_csr_rows", "stencil", "stencil_sweep", "scale_host", "spmv_csr_host",
-    "stencil_host", "fill_uniform", "gen_band_csr", "stencil_init", "load_spec", "builtin_spec",
+    "stencil_host", "SpmvPlan", "fill_uniform", "gen_band_csr", "stencil_init", "load_spec", "builtin_spec",
     "machine_balance", "tensor_alpha", "attainable", "classify", "unoverlapped_speedup",
     "kernel_speedup_ceiling", "tensor_core_ceiling", "workload_ceiling", "min_temporal_depth",
     "tc_scale_trick_throughput", "fp64_peak_launch", "tuning_set", "kernel_launches",
@@ -142,6 +142,10 @@ _SIGNATURES = {
     "rl_spmv_csr_host": (_int, [_int, _int, _u64, _u64, _u64, _ptr, _ptr, _ptr, _ptr, _ptr, _KP]),
     "rl_stencil_host": (_int, [_int, _int, C.c_char_p, C.POINTER(_u64), _ptr, _u64, _ptr, _ptr, _KP]),
     "rl_host_workspace_release": (_int, []),
+    "rl_spmv_plan_create": (_int, [_int, _int, _u64, _u64, _u64, _ptr, _ptr, _ptr, C.POINTER(_ptr)]),
+    "rl_spmv_plan_execute_host": (_int, [_ptr, _ptr, _ptr, _KP]),
+    "rl_spmv_plan_execute": (_int, [_ptr, _ptr, _ptr, _ptr, _KP]),
+    "rl_spmv_plan_destroy": (_int, [_ptr]),
     "rl_fill_uniform": (_int, [_ptr, _u64, _u64, _u64, _u64, _int, _ptr]),
     "rl_gen_band_csr": (_int, [_u64, _u64, _u64, C.c_uint32, _u64, _u64, _ptr, _ptr, _ptr, _ptr]),
     "rl_stencil_init": (_int, [_ptr, C.POINTER(_u64), _int, _u64, _u64, _int, _u64, _ptr]),
@@ -406,6 +410,43 @@ def stencil_host(preset: str, u, v, steps: int, weights=None, unit: int = CUDA_C
                                  C.cast(w, _ptr) if w is not None else None, steps,
                                  _host_ptr(u, "f64", "u"), _host_ptr(v, "f64", "v"), C.byref(k)))
     return _kc(k)
+
+
+class SpmvPlan:
+    """CSR matrix uploaded once; execute() moves x in and y out per call
+    (rl_spmv_plan_* in the C-ABI).  Host arrays: numpy or (pinned) CPU tensors."""
+
+    def __init__(self, row_ptr, col, val, n_cols: int, unit: int = CUDA_CORE, precision: int = FP64):
+        size = (lambda t: t.numel() if hasattr(t, "numel") else t.size)
+        self.m, self.n, self.nnz = size(row_ptr) - 1, int(n_cols), size(val)
+        h = _ptr()
+        _check(lib().rl_spmv_plan_create(unit, precision, self.m, self.n, self.nnz,
+                                         _host_ptr(row_ptr, "i32", "row_ptr"), _host_ptr(col, "i32", "col"),
+                                         _host_ptr(val, "f64", "val"), C.byref(h)))
+        self._h = h
+
+    def execute_host(self, x, y) -> KernelCharacterization:
+        k = _KChar()
+        _check(lib().rl_spmv_plan_execute_host(self._h, _host_ptr(x, "f64", "x"), _host_ptr(y, "f64", "y"),
+                                               C.byref(k)))
+        return _kc(k)
+
+    def execute(self, x, y, stream=None) -> KernelCharacterization:
+        k = _KChar()
+        _check(lib().rl_spmv_plan_execute(self._h, _dev_ptr(x, "f64", "x"), _dev_ptr(y, "f64", "y"),
+                                          _stream(stream), C.byref(k)))
+        return _kc(k)
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().rl_spmv_plan_destroy(self._h)
+            self._h = _ptr()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 # ----------------------------------------------------------------------------

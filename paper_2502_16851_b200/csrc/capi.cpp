@@ -7,7 +7,11 @@
 // the call.  There is no CPU path: a missing/unusable device surfaces as a
 // CUDA error code (RL_ERR_CUDA_BASE + cudaError_t).
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <memory>
+#include <vector>
 #include <mutex>
 #include <string>
 
@@ -331,6 +335,138 @@ KernelCharacterization stencil_host(ExecutionUnit unit, Precision p, const char*
 }
 
 // ---------------------------------------------------------------------------
+// SpMV plan
+// ---------------------------------------------------------------------------
+}  // namespace
+
+struct rl_spmv_plan_s {
+    ExecutionUnit unit;
+    uint64_t m = 0, n = 0, nnz = 0;
+    int32_t *rp = nullptr, *col = nullptr;
+    double *val = nullptr, *x = nullptr, *y = nullptr;
+    std::vector<uint64_t> chunk_row;   // chunk c = rows [chunk_row[c], chunk_row[c+1])
+    std::vector<uint64_t> chunk_xend;  // x prefix [0, chunk_xend[c]) chunk c reads
+    std::vector<uint64_t> xpiece;      // x upload pieces: [xpiece[i], xpiece[i+1])
+    cudaStream_t s_in = nullptr, s_cmp = nullptr, s_out = nullptr;
+    std::vector<cudaEvent_t> ev_x, ev_y;
+    KernelCharacterization kc;
+    ~rl_spmv_plan_s() {
+        if (rp) cudaFree(rp);
+        if (col) cudaFree(col);
+        if (val) cudaFree(val);
+        if (x) cudaFree(x);
+        if (y) cudaFree(y);
+        for (auto e : ev_x) cudaEventDestroy(e);
+        for (auto e : ev_y) cudaEventDestroy(e);
+        if (s_in) cudaStreamDestroy(s_in);
+        if (s_cmp) cudaStreamDestroy(s_cmp);
+        if (s_out) cudaStreamDestroy(s_out);
+    }
+};
+
+namespace {
+
+rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_t n, uint64_t nnz,
+                            const int32_t* rp, const int32_t* col, const double* val) {
+    KernelCharacterization k = spmv_csr_model({m, n, nnz}, kDefaultIndexBytes, p);
+    require_fp64(p);
+    require_ptr(rp, "row_ptr");
+    require_ptr(col, "col");
+    require_ptr(val, "val");
+    if (nnz > 0x7fffffffull || m > 0x7fffffffull || n > 0x7fffffffull)
+        throw Error(ErrorKind::InvalidRange, "int32 CSR indices cannot address this matrix");
+    if ((uint64_t)rp[m] != nnz) throw Error(ErrorKind::ValidationError, "row_ptr[m] != nnz");
+    auto pl = std::make_unique<rl_spmv_plan_s>();
+    pl->unit = unit;
+    pl->m = m;
+    pl->n = n;
+    pl->nnz = nnz;
+    pl->kc = k;
+    ck(cudaMalloc(&pl->rp, (m + 1) * 4), "plan alloc");
+    ck(cudaMalloc(&pl->col, nnz * 4), "plan alloc");
+    ck(cudaMalloc(&pl->val, nnz * 8), "plan alloc");
+    ck(cudaMalloc(&pl->x, n * 8), "plan alloc");
+    ck(cudaMalloc(&pl->y, m * 8), "plan alloc");
+    ck(cudaMemcpy(pl->rp, rp, (m + 1) * 4, cudaMemcpyHostToDevice), "plan upload");
+    ck(cudaMemcpy(pl->col, col, nnz * 4, cudaMemcpyHostToDevice), "plan upload");
+    ck(cudaMemcpy(pl->val, val, nnz * 8, cudaMemcpyHostToDevice), "plan upload");
+    const uint64_t nch = std::min<uint64_t>((uint64_t)rlb::tuning().spmv_plan_chunks, m);
+    for (uint64_t c = 0; c <= nch; ++c) pl->chunk_row.push_back(m * c / nch);
+    for (uint64_t c = 0; c < nch; ++c) {
+        uint64_t mx = 0;
+        for (int64_t j = rp[pl->chunk_row[c]]; j < rp[pl->chunk_row[c + 1]]; ++j) {
+            if (col[j] < 0 || (uint64_t)col[j] >= n)
+                throw Error(ErrorKind::IndexOutOfRange, "column index " + std::to_string(col[j]) +
+                                                            " outside [0, " + std::to_string(n) + ")");
+            mx = std::max<uint64_t>(mx, (uint64_t)col[j] + 1);
+        }
+        pl->chunk_xend.push_back(mx);
+    }
+    const uint64_t npc = std::min<uint64_t>((uint64_t)rlb::tuning().spmv_plan_chunks, n);
+    for (uint64_t i = 0; i <= npc; ++i) pl->xpiece.push_back(n * i / npc);
+    ck(cudaStreamCreateWithFlags(&pl->s_in, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&pl->s_cmp, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&pl->s_out, cudaStreamNonBlocking), "stream");
+    pl->ev_x.resize(npc);
+    pl->ev_y.resize(nch);
+    for (auto& e : pl->ev_x) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    for (auto& e : pl->ev_y) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    return pl.release();
+}
+
+void plan_execute_host(rl_spmv_plan_s* pl, const double* x, double* y) {
+    require_ptr(pl, "plan");
+    require_ptr(x, "x");
+    require_ptr(y, "y");
+    static const bool trace = getenv("RL_PLAN_TRACE") != nullptr;
+    std::vector<cudaEvent_t> tev;
+    auto mark = [&](cudaStream_t s) {
+        if (!trace) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s);
+        tev.push_back(e);
+    };
+    mark(pl->s_in);
+    const size_t npc = pl->ev_x.size();
+    for (size_t i = 0; i < npc; ++i) {
+        const uint64_t a = pl->xpiece[i], b = pl->xpiece[i + 1];
+        ck(cudaMemcpyAsync(pl->x + a, x + a, (b - a) * 8, cudaMemcpyHostToDevice, pl->s_in), "H2D x");
+        ck(cudaEventRecord(pl->ev_x[i], pl->s_in), "event");
+        mark(pl->s_in);
+    }
+    size_t waited = 0;  // x pieces the compute stream already waits for
+    for (size_t c = 0; c + 1 < pl->chunk_row.size(); ++c) {
+        while (waited < npc && pl->xpiece[waited] < pl->chunk_xend[c]) {
+            ck(cudaStreamWaitEvent(pl->s_cmp, pl->ev_x[waited], 0), "wait");
+            ++waited;
+        }
+        const uint64_t r0 = pl->chunk_row[c], r1 = pl->chunk_row[c + 1];
+        mark(pl->s_cmp);
+        spmv_csr_rows(pl->unit, Precision::FP64, r0, r1, pl->rp, pl->col, pl->val, pl->x, 0, pl->y,
+                      pl->s_cmp);
+        ck(cudaEventRecord(pl->ev_y[c], pl->s_cmp), "event");
+        mark(pl->s_cmp);
+        ck(cudaStreamWaitEvent(pl->s_out, pl->ev_y[c], 0), "wait");
+        ck(cudaMemcpyAsync(y + r0, pl->y + r0, (r1 - r0) * 8, cudaMemcpyDeviceToHost, pl->s_out), "D2H y");
+        mark(pl->s_out);
+    }
+    ck(cudaStreamSynchronize(pl->s_out), "sync");
+    ck(cudaStreamSynchronize(pl->s_cmp), "sync");
+    ck(cudaStreamSynchronize(pl->s_in), "sync");
+    if (trace && !tev.empty()) {
+        fprintf(stderr, "plan trace (us from start):");
+        for (size_t i = 1; i < tev.size(); ++i) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, tev[0], tev[i]);
+            fprintf(stderr, " %.0f", ms * 1e3);
+        }
+        fprintf(stderr, "\n");
+        for (auto e : tev) cudaEventDestroy(e);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Error plumbing
 // ---------------------------------------------------------------------------
 thread_local std::string g_last_error;
@@ -493,6 +629,33 @@ int rl_stencil_host(rl_unit u, rl_precision p, const char* preset, const uint64_
         put(out, stencil_host(unit_of(u), prec_of(p), preset, dims, weights, steps, uu, v));
     });
 }
+int rl_spmv_plan_create(rl_unit u, rl_precision p, uint64_t m, uint64_t n, uint64_t nnz,
+                        const int32_t* rp, const int32_t* col, const double* val, rl_spmv_plan* out) {
+    return guarded([&] {
+        require_ptr(out, "out");
+        *out = nullptr;
+        *out = plan_create(unit_of(u), prec_of(p), m, n, nnz, rp, col, val);
+    });
+}
+int rl_spmv_plan_execute_host(rl_spmv_plan pl, const double* x, double* y, rl_kchar* out) {
+    return guarded([&] {
+        plan_execute_host(pl, x, y);
+        put(out, pl->kc);
+    });
+}
+int rl_spmv_plan_execute(rl_spmv_plan pl, const double* x, double* y, rl_stream s, rl_kchar* out) {
+    return guarded([&] {
+        require_ptr(pl, "plan");
+        require_ptr(x, "x");
+        require_ptr(y, "y");
+        spmv_csr_rows(pl->unit, Precision::FP64, 0, pl->m, pl->rp, pl->col, pl->val, x, 0, y,
+                      static_cast<cudaStream_t>(s));
+        put(out, pl->kc);
+    });
+}
+int rl_spmv_plan_destroy(rl_spmv_plan pl) {
+    return guarded([&] { delete pl; });
+}
 int rl_host_workspace_release(void) {
     return guarded([&] {
         std::lock_guard<std::mutex> lock(ws().mu);
@@ -596,6 +759,9 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         else if (k == "spmv_rows") slot = &t.spmv_rows;
         else if (k == "spmv_blocks_per_sm") slot = &t.spmv_blocks_per_sm;
         else if (k == "spmv_sched") slot = &t.spmv_sched;
+        else if (k == "spmv_threads") slot = &t.spmv_threads;
+        else if (k == "spmv_plan_chunks") slot = &t.spmv_plan_chunks;
+        else if (k == "spmv_tc_blocks_per_sm") slot = &t.spmv_tc_blocks_per_sm;
         else if (k == "spmv_xhint") slot = &t.spmv_xhint;
         else if (k == "scale_unroll") slot = &t.scale_unroll;
         else if (k == "stencil2d_rows") slot = &t.stencil2d_rows;
@@ -603,6 +769,8 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         else if (k == "tc_stencil_zchunk") slot = &t.tc_stencil_zchunk;
         else if (k == "stencil_tma") slot = &t.stencil_tma;
         else if (k == "stencil_ctas_per_sm") slot = &t.stencil_ctas_per_sm;
+        else if (k == "stencil_rows_per_thread") slot = &t.stencil_rows_per_thread;
+        else if (k == "stencil2d_rows_per_thread") slot = &t.stencil2d_rows_per_thread;
         else if (k == "stencil_tc_ctas_per_sm") slot = &t.stencil_tc_ctas_per_sm;
         else if (k == "stencil_tc3d_ctas_per_sm") slot = &t.stencil_tc3d_ctas_per_sm;
         else throw Error(ErrorKind::ValidationError, "unknown tuning key '" + k + "'");

@@ -11,20 +11,22 @@ namespace rlb {
 struct Tuning {
     int scale_blocks_per_sm = 32;  // STREAM grid = 148 * this (swept: tools/sweep.py)
     int scale_unroll = 8;          // 1, 2, 4, 8
-    int spmv_group = 0;            // lanes per row; 0 = auto from nnz/m
     int spmv_rows = 2;             // rows per lane group per iteration (1, 2, 4)
-    int spmv_blocks_per_sm = 16;
+    int spmv_blocks_per_sm = 1;    // CUDA-core SpMV grid = 148 * this
+    int spmv_threads = 1024;       // CTA size of the CUDA-core kernel (multiple of 32, <= 1024)
+    int spmv_tc_blocks_per_sm = 4; // tensor-core SpMV grid = 148 * this (256 threads)
+    int spmv_plan_chunks = 4;      // pipelined row/x chunks of rl_spmv_plan_execute_host
     int spmv_sched = 1;            // 0 grid-stride, 1 contiguous row range per CTA
     int spmv_xhint = 0;            // x gathers: 0 L1 default, 1 L1::evict_last, 2 L1::no_allocate
     int stencil2d_rows = 256;      // rows marched per warp (2D CC)
-    int stencil2d_variant = 0;     // 0 = register-streaming CC
-    int stencil3d_zchunk = 64;     // planes marched per CTA (3D)
-    int stencil3d_ty = 8;          // tile rows (3D)
+    int stencil3d_zchunk = 64;     // planes marched per CTA (3D, non-TMA fallback)
     int tc_stencil_zchunk = 32;
     int stencil_tma = 1;           // 1: TMA-pipelined kernels when eligible
-    int stencil_ctas_per_sm = 2;   // grid sizing target, TMA CUDA-core kernels
-    int stencil_tc_ctas_per_sm = 2;    // ... 2D tensor-core kernel
-    int stencil_tc3d_ctas_per_sm = 5;  // ... 3D tensor-core kernels
+    int stencil_ctas_per_sm = 1;   // grid sizing target, TMA CUDA-core kernels
+    int stencil_rows_per_thread = 2;   // 3D TMA CUDA-core kernels: 2, 4 or 8 (CTA = 64*16/this threads)
+    int stencil2d_rows_per_thread = 4; // 2D TMA CUDA-core kernel (swept: tools/sweep.py)
+    int stencil_tc_ctas_per_sm = 1;    // ... 2D tensor-core kernel
+    int stencil_tc3d_ctas_per_sm = 8;  // ... 3D tensor-core kernels
 };
 Tuning& tuning();
 

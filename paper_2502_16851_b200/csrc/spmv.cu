@@ -82,7 +82,7 @@ __device__ __forceinline__ void gather4(double (&xv)[4], const Nz4& z,
 // SCHED 0: warps stride over the whole row range (grid-stride);
 // SCHED 1: each CTA owns one contiguous row range (x-window locality in L1).
 template <int R, int SCHED, int XH>
-__global__ void __launch_bounds__(256) spmv_cc_v4(uint64_t r0, uint64_t r1,
+__global__ void __launch_bounds__(1024) spmv_cc_v4(uint64_t r0, uint64_t r1,
                                                   const int* __restrict__ rp,
                                                   const int* __restrict__ col,
                                                   const double* __restrict__ val,
@@ -201,17 +201,20 @@ cudaError_t launch_spmv(int unit, uint64_t r0, uint64_t r1, const int* rp, const
     const uint64_t max_blocks = (uint64_t)kNumSMs * (uint64_t)t.spmv_blocks_per_sm;
     if (unit == 1) {
         uint64_t blocks = (rows + 63) / 64;  // 8 warps x 8 rows
-        if (blocks > max_blocks) blocks = max_blocks;
+        const uint64_t cap = (uint64_t)kNumSMs * (uint64_t)t.spmv_tc_blocks_per_sm;
+        if (blocks > cap) blocks = cap;
         spmv_tc<<<(unsigned)blocks, threads, 0, s>>>(r0, r1, rp, col, val, x, col_base, y); note_launch();
         return cudaGetLastError();
     }
     const int R = t.spmv_rows;
-    const uint64_t rows_per_block = 8ull * 8ull * (uint64_t)R;
+    const int cthreads = t.spmv_threads;
+    const uint64_t rows_per_block = (uint64_t)(cthreads / 32) * 8ull * (uint64_t)R;
     uint64_t blocks = (rows + rows_per_block - 1) / rows_per_block;
-    if (blocks > max_blocks) blocks = max_blocks;
+    const uint64_t cap = (uint64_t)kNumSMs * (uint64_t)t.spmv_blocks_per_sm;
+    if (blocks > cap) blocks = cap;
     const int sched = t.spmv_sched, xh = t.spmv_xhint;
 #define RLB_SPMV(RR, SS, XX) \
-    spmv_cc_v4<RR, SS, XX><<<(unsigned)blocks, threads, 0, s>>>(r0, r1, rp, col, val, x, col_base, y)
+    spmv_cc_v4<RR, SS, XX><<<(unsigned)blocks, cthreads, 0, s>>>(r0, r1, rp, col, val, x, col_base, y)
 #define RLB_SPMV_R(SS, XX)                        \
     do {                                          \
         if (R == 1) RLB_SPMV(1, SS, XX);          \

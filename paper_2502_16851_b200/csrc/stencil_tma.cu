@@ -129,8 +129,8 @@ __device__ __forceinline__ double bandv(int k, int n, double a, double b, double
 // ===========================================================================
 // CUDA core, 2d5pt.  w: centre, y-1, y+1, x-1, x+1.
 // ===========================================================================
-template <int S>
-__global__ void __launch_bounds__(128) st2d_tma_cc(const __grid_constant__ CUtensorMap tm,
+template <int S, int RYT>
+__global__ void __launch_bounds__(64 * kTY / RYT) st2d_tma_cc(const __grid_constant__ CUtensorMap tm,
                                                    double* __restrict__ v, uint64_t nx, uint64_t y_begin,
                                                    uint64_t y_end, int seg_rows, int strips, StencilDesc d) {
     constexpr int BX = kBX, STAGE = stage_doubles(BX);
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(128) st2d_tma_cc(const __grid_constant__ CUten
     const int nblk = (int)((yb - ya + kTY - 1) / kTY);
     const int64_t xs = x0 - kCofs;
     const int cofs = kCofs;
-    ring.init(4);
+    ring.init(2 * kTY / RYT);
     auto issue = [&](int k) {
         mbar_expect_tx(ring.full + (k % S), kBY * BX * 8);
         tma2d(ring.stage(k), &tm, ring.full + (k % S), (int)xs, (int)(ya + (uint64_t)k * kTY) - 1);
@@ -160,11 +160,11 @@ __global__ void __launch_bounds__(128) st2d_tma_cc(const __grid_constant__ CUten
     for (int k = 0; k < nblk; ++k) {
         ring.wait_full(k);
         const double* T = ring.stage(k);
-        double o[kRY];
-        double cp = T[(kRY * wy) * BX + col], c = T[(kRY * wy + 1) * BX + col];
+        double o[RYT];
+        double cp = T[(RYT * wy) * BX + col], c = T[(RYT * wy + 1) * BX + col];
 #pragma unroll
-        for (int j = 0; j < kRY; ++j) {
-            const int r = kRY * wy + j + 1;
+        for (int j = 0; j < RYT; ++j) {
+            const int r = RYT * wy + j + 1;
             const double cn = T[(r + 1) * BX + col];
             double a = w0 * c;
             a = fma(w1, cp, a);
@@ -180,10 +180,10 @@ __global__ void __launch_bounds__(128) st2d_tma_cc(const __grid_constant__ CUten
             ring.wait_empty(k);
             issue(k + S);
         }
-        const uint64_t yr = ya + (uint64_t)k * kTY + kRY * wy;
+        const uint64_t yr = ya + (uint64_t)k * kTY + RYT * wy;
         if (xin) {
 #pragma unroll
-            for (int j = 0; j < kRY; ++j)
+            for (int j = 0; j < RYT; ++j)
                 if (yr + j < yb) v[(yr + j) * nx + x] = o[j];
         }
     }
@@ -193,8 +193,8 @@ __global__ void __launch_bounds__(128) st2d_tma_cc(const __grid_constant__ CUten
 // CUDA core, 3D.  KIND 0: 3d7pt (c, z-, z+, y-, y+, x-, x+); 1: 3d27pt
 // general; 2: 3d27pt class weights g0..g3 in w[0..3].
 // ===========================================================================
-template <int KIND, int S>
-__global__ void __launch_bounds__(128) st3d_tma_cc(const __grid_constant__ CUtensorMap tm,
+template <int KIND, int S, int RYT>
+__global__ void __launch_bounds__(64 * kTY / RYT) st3d_tma_cc(const __grid_constant__ CUtensorMap tm,
                                                    double* __restrict__ v, StencilDesc d, uint64_t z_begin,
                                                    uint64_t z_end, int zchunk, int tiles_x, int tiles_xy) {
     constexpr int BX = kBX, STAGE = stage_doubles(BX);
@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(128) st3d_tma_cc(const __grid_constant__ CUten
     const uint64_t nx = d.nx, ny = d.ny;
     const int64_t xs = x0 - kCofs;
     const int cofs = kCofs, rofs = 1;  // stage column/row of (x0, y0); boxes may start OOB
-    ring.init(4);
+    ring.init(2 * kTY / RYT);
     auto issue = [&](int k) {
         mbar_expect_tx(ring.full + (k % S), kBY * BX * 8);
         tma3d(ring.stage(k), &tm, ring.full + (k % S), (int)xs, (int)(y0 - rofs), (int)(za - 1 + k));
@@ -220,24 +220,24 @@ __global__ void __launch_bounds__(128) st3d_tma_cc(const __grid_constant__ CUten
         for (int k = 0; k < S && k < np; ++k) issue(k);
     const int col = 32 * wx + lane + cofs;
     const int cl = col > 0 ? col - 1 : 0;
-    const int rbase = kRY * wy + rofs;  // stage row of this thread's first output row
+    const int rbase = RYT * wy + rofs;  // stage row of this thread's first output row
     const int64_t x = x0 + 32 * wx + lane;
     const bool xin = x >= 1 && x <= (int64_t)nx - 2;
-    const int64_t yr0 = y0 + kRY * wy;
-    double acc_a[kRY], acc_b[kRY];
+    const int64_t yr0 = y0 + RYT * wy;
+    double acc_a[RYT], acc_b[RYT];
 #pragma unroll
-    for (int j = 0; j < kRY; ++j) acc_a[j] = acc_b[j] = 0.0;
+    for (int j = 0; j < RYT; ++j) acc_a[j] = acc_b[j] = 0.0;
     const double* w = d.w;
     for (int k = 0; k < np; ++k) {
         ring.wait_full(k);
         const double* T = ring.stage(k);
-        double pm[kRY], p0[kRY], pp[kRY];
+        double pm[RYT], p0[RYT], pp[RYT];
         if (KIND == 0) {
-            // rows rbase-1 .. rbase+kRY; rbase-1 < 0 only at y0 == 0, where
+            // rows rbase-1 .. rbase+RYT; rbase-1 < 0 only at y0 == 0, where
             // output row 0 is boundary and never stored
             double cp = T[max(rbase - 1, 0) * BX + col], c = T[rbase * BX + col];
 #pragma unroll
-            for (int j = 0; j < kRY; ++j) {
+            for (int j = 0; j < RYT; ++j) {
                 const int r = rbase + j;
                 const double cn = T[(r + 1) * BX + col];
                 double a = w[0] * c;
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(128) st3d_tma_cc(const __grid_constant__ CUten
             double al = ra[cl], ac = ra[col], ar = ra[col + 1];
             double bl = rb0[cl], bc = rb0[col], br = rb0[col + 1];
 #pragma unroll
-            for (int j = 0; j < kRY; ++j) {
+            for (int j = 0; j < RYT; ++j) {
                 const double* rc = T + (rbase + j + 1) * BX;
                 const double cL = rc[cl], cc = rc[col], cr = rc[col + 1];
                 if (KIND == 2) {
@@ -290,9 +290,9 @@ __global__ void __launch_bounds__(128) st3d_tma_cc(const __grid_constant__ CUten
             ring.wait_empty(k);
             issue(k + S);
         }
-        double o[kRY];
+        double o[RYT];
 #pragma unroll
-        for (int j = 0; j < kRY; ++j) {
+        for (int j = 0; j < RYT; ++j) {
             o[j] = acc_a[j] + pp[j];
             acc_a[j] = acc_b[j] + p0[j];
             acc_b[j] = pm[j];
@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(128) st3d_tma_cc(const __grid_constant__ CUten
         if (k >= 2 && xin) {
             const uint64_t p = za - 2 + (uint64_t)k;
 #pragma unroll
-            for (int j = 0; j < kRY; ++j) {
+            for (int j = 0; j < RYT; ++j) {
                 const int64_t y = yr0 + j;
                 if (y >= 1 && y <= (int64_t)ny - 2) v[(p * ny + (uint64_t)y) * nx + x] = o[j];
             }
@@ -347,6 +347,7 @@ __global__ void __launch_bounds__(128) st2d_tma_tc(const __grid_constant__ CUten
         ring.wait_full(k);
         const double* T = ring.stage(k);
         double D0[4], D1[4];
+        double carry = 0.0;  // k-step 2 operand of tile cb == k-step 0 operand of tile cb+1
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
             const int cb = cb0 + t;
@@ -358,8 +359,11 @@ __global__ void __launch_bounds__(128) st2d_tma_tc(const __grid_constant__ CUten
             }
 #pragma unroll
             for (int kb = 0; kb < 3; ++kb) {
-                const int j = min(4 * kb + c, 9);
-                dmma_m8n8k4(d0, d1, T[(8 * rb + r + 1) * BX + cc(8 * cb + j - 1 + cofs)], tx[kb], d0, d1);
+                double a;
+                if (kb == 0 && t > 0) a = carry;
+                else a = T[(8 * rb + r + 1) * BX + cc(8 * cb + 4 * kb + c - 1 + cofs)];
+                if (kb == 2) carry = a;
+                dmma_m8n8k4(d0, d1, a, tx[kb], d0, d1);
             }
             D0[t] = d0;
             D1[t] = d1;
@@ -454,7 +458,15 @@ __global__ void __launch_bounds__(128) st3d_tma_tc(const __grid_constant__ CUten
         const double* Pm = ring.stage(i);
         const double* P0 = ring.stage(i + 1);
         const double* Pp = ring.stage(i + 2);
+        // Horizontal-product A operands: lane (r, c) of k-step kb reads window
+        // column 8*cb + 4*kb + c (band rows 10/11 are zero, so the unclamped
+        // columns are harmless) -- k-step 2 of tile cb is k-step 0 of tile
+        // cb+1, so those operands are carried over instead of reloaded.
         double D0[4], D1[4];
+        double ca0 = 0.0, ca1 = 0.0, ca2 = 0.0;           // carried (KIND 0/1)
+        double cg[9];                                      // carried (KIND 2)
+#pragma unroll
+        for (int q = 0; q < 9; ++q) cg[q] = 0.0;
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
             const int cb = cb0 + t;
@@ -470,34 +482,53 @@ __global__ void __launch_bounds__(128) st3d_tma_tc(const __grid_constant__ CUten
                 }
 #pragma unroll
                 for (int kb = 0; kb < 3; ++kb) {
-                    const int j = min(4 * kb + c, 9);
-                    dmma_m8n8k4(d0, d1, P0[at(8 * rb + r + 1, 8 * cb + j)], fb[kb], d0, d1);
+                    double a;
+                    if (kb == 0 && t > 0) a = ca0;
+                    else a = P0[at(8 * rb + r + 1, 8 * cb + 4 * kb + c)];
+                    if (kb == 2) ca0 = a;
+                    dmma_m8n8k4(d0, d1, a, fb[kb], d0, d1);
                 }
             } else if (KIND == 1) {
 #pragma unroll
                 for (int kb = 0; kb < 3; ++kb) {
-                    const int colj = 8 * cb + min(4 * kb + c, 9);
-                    const int up = at(8 * rb + r, colj), mid = at(8 * rb + r + 1, colj),
-                              dn = at(8 * rb + r + 2, colj);
-                    const double a0 = P0[mid];
-                    const double a1 = (P0[up] + P0[dn]) + (Pm[mid] + Pp[mid]);
-                    const double a2 = (Pm[up] + Pm[dn]) + (Pp[up] + Pp[dn]);
+                    double a0, a1, a2;
+                    if (kb == 0 && t > 0) {
+                        a0 = ca0; a1 = ca1; a2 = ca2;
+                    } else {
+                        const int colj = 8 * cb + 4 * kb + c;
+                        const int up = at(8 * rb + r, colj), mid = at(8 * rb + r + 1, colj),
+                                  dn = at(8 * rb + r + 2, colj);
+                        a0 = P0[mid];
+                        a1 = (P0[up] + P0[dn]) + (Pm[mid] + Pp[mid]);
+                        a2 = (Pm[up] + Pm[dn]) + (Pp[up] + Pp[dn]);
+                    }
+                    if (kb == 2) { ca0 = a0; ca1 = a1; ca2 = a2; }
                     dmma_m8n8k4(d0, d1, a0, fa[kb], d0, d1);
                     dmma_m8n8k4(d0, d1, a1, fb[kb], d0, d1);
                     dmma_m8n8k4(d0, d1, a2, fc[kb], d0, d1);
                 }
             } else {
 #pragma unroll
-                for (int dz = 0; dz < 3; ++dz) {
-                    const double* P = dz == 0 ? Pm : (dz == 1 ? P0 : Pp);
+                for (int kb = 0; kb < 3; ++kb) {
+                    double g[9];
+                    if (kb == 0 && t > 0) {
 #pragma unroll
-                    for (int dy = 0; dy < 3; ++dy)
+                        for (int q = 0; q < 9; ++q) g[q] = cg[q];
+                    } else {
+                        const int colj = 8 * cb + 4 * kb + c;
 #pragma unroll
-                        for (int kb = 0; kb < 3; ++kb) {
-                            const int colj = 8 * cb + min(4 * kb + c, 9);
-                            dmma_m8n8k4(d0, d1, P[at(8 * rb + r + dy, colj)], gen[(dz * 3 + dy) * 3 + kb], d0,
-                                        d1);
+                        for (int dz = 0; dz < 3; ++dz) {
+                            const double* P = dz == 0 ? Pm : (dz == 1 ? P0 : Pp);
+#pragma unroll
+                            for (int dy = 0; dy < 3; ++dy) g[dz * 3 + dy] = P[at(8 * rb + r + dy, colj)];
                         }
+                    }
+                    if (kb == 2) {
+#pragma unroll
+                        for (int q = 0; q < 9; ++q) cg[q] = g[q];
+                    }
+#pragma unroll
+                    for (int q = 0; q < 9; ++q) dmma_m8n8k4(d0, d1, g[q], gen[q * 3 + kb], d0, d1);
                 }
             }
             D0[t] = d0;
@@ -617,8 +648,14 @@ cudaError_t launch_stencil_tma(int unit, const StencilDesc& d, uint64_t o0, uint
         } else {
             constexpr int S = 4;
             const size_t sm = ring_bytes<S, kBX>();
-            if ((e = prep(st2d_tma_cc<S>, sm)) != cudaSuccess) return e;
-            st2d_tma_cc<S><<<grid, 128, sm, s>>>(m, v, d.nx, o0, o1, seg_rows, strips, d);
+            const int ry = tuning().stencil2d_rows_per_thread;
+#define RLB_CC2(R)                                                                                 \
+    do {                                                                                           \
+        if ((e = prep(st2d_tma_cc<S, R>, sm)) != cudaSuccess) return e;                           \
+        st2d_tma_cc<S, R><<<grid, 64 * kTY / R, sm, s>>>(m, v, d.nx, o0, o1, seg_rows, strips, d); \
+    } while (0)
+            if (ry == 2) RLB_CC2(2); else if (ry == 4) RLB_CC2(4); else RLB_CC2(8);
+#undef RLB_CC2
         }
         note_launch();
         return cudaGetLastError();
@@ -655,12 +692,16 @@ cudaError_t launch_stencil_tma(int unit, const StencilDesc& d, uint64_t o0, uint
     } else {
         constexpr int S = 4;
         const size_t sm = ring_bytes<S, kBX>();
-#define RLB_CC3(K)                                                                            \
-    do {                                                                                      \
-        if ((e = prep(st3d_tma_cc<K, S>, sm)) != cudaSuccess) return e;                      \
-        st3d_tma_cc<K, S><<<grid, 128, sm, s>>>(m, v, dd, o0, o1, zchunk, tiles_x, tiles_xy); \
+        const int ry = tuning().stencil_rows_per_thread;
+#define RLB_CC3(K, R)                                                                                     \
+    do {                                                                                                  \
+        if ((e = prep(st3d_tma_cc<K, S, R>, sm)) != cudaSuccess) return e;                               \
+        st3d_tma_cc<K, S, R><<<grid, 64 * kTY / R, sm, s>>>(m, v, dd, o0, o1, zchunk, tiles_x, tiles_xy); \
     } while (0)
-        if (kind == 0) RLB_CC3(0); else if (kind == 1) RLB_CC3(1); else RLB_CC3(2);
+#define RLB_CC3K(K) \
+    do { if (ry == 2) RLB_CC3(K, 2); else if (ry == 4) RLB_CC3(K, 4); else RLB_CC3(K, 8); } while (0)
+        if (kind == 0) RLB_CC3K(0); else if (kind == 1) RLB_CC3K(1); else RLB_CC3K(2);
+#undef RLB_CC3K
 #undef RLB_CC3
     }
     note_launch();

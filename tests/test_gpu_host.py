@@ -1,0 +1,69 @@
+"""GPU parity of the end-to-end entry points on host buffers (rl_*_host,
+rl_spmv_plan_*): pinned or pageable host arrays in, host arrays out."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2502_16851_b200 as P
+
+pytestmark = pytest.mark.gpu
+UNITS = [P.CUDA_CORE, P.TENSOR_CORE]
+
+
+@pytest.mark.parametrize("unit", UNITS)
+@pytest.mark.parametrize("n", [1, 1000, (4 << 20) + 77])
+def test_scale_host(cuda, unit, n):
+    b = O.fill_uniform(n, 3, 1, 0, 1)
+    a = np.full(n, np.nan)
+    kc = P.scale_host(a, b, 3.0, unit=unit)
+    assert O.bit_mismatches(a, O.scale(b, 3.0)) == 0
+    assert kc.traffic_bytes == 16 * n
+
+
+@pytest.mark.parametrize("unit", UNITS)
+def test_spmv_host_and_plan(cuda, unit):
+    import torch
+
+    m, k, hb = 300000, 16, 65536
+    rp, col, val = O.gen_band_csr(m, 0, m, k, hb, 8)
+    x = O.fill_uniform(m, 8, 4, 0, 1)
+    ref = O.spmv_csr(rp, col, val, x)
+    y = np.full(m, np.nan)
+    kc = P.spmv_csr_host(rp, col, val, x, y, unit=unit)
+    assert O.rel_err(y, ref) <= 1e-12
+    assert kc == P.spmv_csr_model(m, m, m * k)
+    # plan: matrix resident, x/y per call; pinned host buffers
+    t = lambda a: torch.from_numpy(a).pin_memory()
+    plan = P.SpmvPlan(t(rp), t(col), t(val), m, unit=unit)
+    xp, yp = t(x), torch.full((m,), float("nan"), dtype=torch.float64).pin_memory()
+    for _ in range(3):
+        kc2 = plan.execute_host(xp, yp)
+    assert O.rel_err(yp.numpy(), ref) <= 1e-12 and kc2 == kc
+    # device execute on the same plan
+    dx, dy = torch.from_numpy(x).cuda(), torch.empty(m, dtype=torch.float64, device="cuda")
+    plan.execute(dx, dy)
+    torch.cuda.synchronize()
+    assert O.rel_err(dy.cpu().numpy(), ref) <= 1e-12
+    plan.close()
+
+
+def test_spmv_plan_validates_indices(cuda):
+    rp = np.array([0, 2], np.int32)
+    with pytest.raises(P.RooflensError) as e:
+        P.SpmvPlan(rp, np.array([0, 5], np.int32), np.ones(2), 3)
+    assert e.value.kind == "IndexOutOfRange"
+    with pytest.raises(P.RooflensError) as e:
+        P.SpmvPlan(np.array([0, 3], np.int32), np.array([0, 1], np.int32), np.ones(2), 3)
+    assert e.value.kind == "ValidationError"
+
+
+@pytest.mark.parametrize("unit", UNITS)
+@pytest.mark.parametrize("preset,shape,steps", [("2d5pt", (130, 260), 3), ("3d7pt", (20, 24, 68), 2),
+                                                ("3d27pt", (18, 20, 66), 3)])
+def test_stencil_host(cuda, unit, preset, shape, steps):
+    u0 = O.stencil_init(shape, 1, 6)
+    u, v = u0.copy(), u0.copy()
+    kc = P.stencil_host(preset, u, v, steps, unit=unit)
+    out = u if steps % 2 == 0 else v
+    assert O.rel_err(out, O.stencil(preset, u0, steps)) <= 1e-12
+    assert kc.traffic_bytes == 16 * int(np.prod([s - 2 for s in shape])) * steps

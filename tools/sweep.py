@@ -55,8 +55,8 @@ def main(which):
         P.fill_uniform(x, 1, 4, 0, 1)
         nbytes = P.spmv_csr_model(n, n, n * k).traffic_bytes
         sweep("spmv_cc", lambda: P.spmv_csr(rp, col, val, x, y, unit=0), nbytes,
-              {"spmv_rows": [1, 2, 4], "spmv_sched": [0, 1], "spmv_xhint": [0, 1, 2],
-               "spmv_blocks_per_sm": [4, 8, 16, 32]})
+              {"spmv_rows": [1, 2], "spmv_sched": [0, 1], "spmv_xhint": [0, 1],
+               "spmv_threads": [256, 512, 1024], "spmv_blocks_per_sm": [1, 2, 4, 8]})
         sweep("spmv_tc", lambda: P.spmv_csr(rp, col, val, x, y, unit=1), nbytes,
               {"spmv_blocks_per_sm": [4, 8, 16, 32]})
 
@@ -69,8 +69,10 @@ def stencils():
         v = u.clone()
         nbytes = 2 * 16 * math.prod(s - 2 for s in shape)
         for unit in (0, 1):
+            grid = ({"stencil_rows_per_thread": [2, 4], "stencil2d_rows_per_thread": [2, 4]} if unit == 0
+                    else {"stencil_tc_ctas_per_sm": [1, 2], "stencil_tc3d_ctas_per_sm": [4, 8, 12, 16, 24]})
             sweep(f"{preset}_{'cc' if unit == 0 else 'tc'}", lambda: P.stencil(preset, u, v, 2, unit=unit),
-                  nbytes, {"stencil_tma": [0, 1], "stencil_ctas_per_sm": [2, 3, 4, 5, 8]})
+                  nbytes, grid)
         del u, v
         torch.cuda.empty_cache()
 
