@@ -762,6 +762,8 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         else if (k == "spmv_threads") slot = &t.spmv_threads;
         else if (k == "spmv_plan_chunks") slot = &t.spmv_plan_chunks;
         else if (k == "spmv_tc_blocks_per_sm") slot = &t.spmv_tc_blocks_per_sm;
+        else if (k == "spmv_tc_threads") slot = &t.spmv_tc_threads;
+        else if (k == "spmv_tc_rows") slot = &t.spmv_tc_rows;
         else if (k == "spmv_xhint") slot = &t.spmv_xhint;
         else if (k == "scale_unroll") slot = &t.scale_unroll;
         else if (k == "stencil2d_rows") slot = &t.stencil2d_rows;

@@ -14,7 +14,9 @@ struct Tuning {
     int spmv_rows = 2;             // rows per lane group per iteration (1, 2, 4)
     int spmv_blocks_per_sm = 1;    // CUDA-core SpMV grid = 148 * this
     int spmv_threads = 1024;       // CTA size of the CUDA-core kernel (multiple of 32, <= 1024)
-    int spmv_tc_blocks_per_sm = 4; // tensor-core SpMV grid = 148 * this (256 threads)
+    int spmv_tc_blocks_per_sm = 1; // tensor-core SpMV grid = 148 * this
+    int spmv_tc_threads = 1024;
+    int spmv_tc_rows = 1;          // 8-row blocks per warp iteration (1, 2)
     int spmv_plan_chunks = 4;      // pipelined row/x chunks of rl_spmv_plan_execute_host
     int spmv_sched = 1;            // 0 grid-stride, 1 contiguous row range per CTA
     int spmv_xhint = 0;            // x gathers: 0 L1 default, 1 L1::evict_last, 2 L1::no_allocate

@@ -152,39 +152,69 @@ __global__ void __launch_bounds__(1024) spmv_cc_v4(uint64_t r0, uint64_t r1,
     }
 }
 
-// K4: tensor core, one 8-row block per warp-iteration.
-__global__ void __launch_bounds__(256) spmv_tc(uint64_t r0, uint64_t r1,
-                                               const int* __restrict__ rp,
-                                               const int* __restrict__ col,
-                                               const double* __restrict__ val,
-                                               const double* __restrict__ x, int64_t col_base,
-                                               double* __restrict__ y) {
+// K4: tensor core.  A warp owns RB 8-row blocks per iteration (independent
+// DMMA accumulator chains); SCHED as in K3.
+template <int RB, int SCHED>
+__global__ void __launch_bounds__(1024) spmv_tc(uint64_t r0, uint64_t r1,
+                                                const int* __restrict__ rp,
+                                                const int* __restrict__ col,
+                                                const double* __restrict__ val,
+                                                const double* __restrict__ x, int64_t col_base,
+                                                double* __restrict__ y) {
     const int lane = threadIdx.x & 31;
     const int r = lane >> 2, c = lane & 3;
     const uint64_t pol = policy_evict_first(), polx = policy_evict_last();
-    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const int col_pad = 0;
-    for (uint64_t base = r0 + warp * 8; base < r1; base += nwarps * 8) {
-        const uint64_t row = base + r;
-        const bool ok = row < r1;
-        const int64_t s = ok ? __ldg(rp + row) : 0;
-        const int64_t e = ok ? __ldg(rp + row + 1) : 0;
-        const int len = (int)(e - s);
+    uint64_t first, stride, last;
+    if (SCHED == 0) {
+        const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+        const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+        first = r0 + warp * 8 * RB;
+        stride = nwarps * 8 * RB;
+        last = r1;
+    } else {
+        const uint64_t per = ((r1 - r0) + gridDim.x - 1) / gridDim.x;
+        const uint64_t b0 = r0 + (uint64_t)blockIdx.x * per;
+        first = b0 + (threadIdx.x >> 5) * 8 * RB;
+        stride = (blockDim.x >> 5) * 8 * RB;
+        last = min(r1, b0 + per);
+    }
+    for (uint64_t base = first; base < last; base += stride) {
+        int64_t s[RB], e[RB];
+        int len = 0;
+#pragma unroll
+        for (int q = 0; q < RB; ++q) {
+            const uint64_t row = base + 8 * q + r;
+            const bool ok = row < last;
+            s[q] = ok ? __ldg(rp + row) : 0;
+            e[q] = ok ? __ldg(rp + row + 1) : 0;
+            len = max(len, (int)(e[q] - s[q]));
+        }
         const int maxlen = __reduce_max_sync(0xffffffffu, len);
-        double d0 = 0.0, d1 = 0.0;
+        double d0[RB], d1[RB];
+#pragma unroll
+        for (int q = 0; q < RB; ++q) d0[q] = d1[q] = 0.0;
         for (int off = 0; off < maxlen; off += 16) {
-            const Nz4 z = load_nz4(col, val, s + off + 4 * c, e, col_pad, pol);
-            double xv[4];
-            gather4(xv, z, x, col_base, polx);
-            // A[r][c] = val, B[c][r] = x[col]: one k-slice per vector component.
-            dmma_m8n8k4(d0, d1, z.v[0], xv[0], d0, d1);
-            dmma_m8n8k4(d0, d1, z.v[1], xv[1], d0, d1);
-            dmma_m8n8k4(d0, d1, z.v[2], xv[2], d0, d1);
-            dmma_m8n8k4(d0, d1, z.v[3], xv[3], d0, d1);
+            Nz4 z[RB];
+#pragma unroll
+            for (int q = 0; q < RB; ++q) z[q] = load_nz4(col, val, s[q] + off + 4 * c, e[q], col_pad, pol);
+#pragma unroll
+            for (int q = 0; q < RB; ++q) {
+                double xv[4];
+                gather4(xv, z[q], x, col_base, polx);
+                // A[r][c] = val, B[c][r] = x[col]: one k-slice per vector component.
+                dmma_m8n8k4(d0[q], d1[q], z[q].v[0], xv[0], d0[q], d1[q]);
+                dmma_m8n8k4(d0[q], d1[q], z[q].v[1], xv[1], d0[q], d1[q]);
+                dmma_m8n8k4(d0[q], d1[q], z[q].v[2], xv[2], d0[q], d1[q]);
+                dmma_m8n8k4(d0[q], d1[q], z[q].v[3], xv[3], d0[q], d1[q]);
+            }
         }
         // D[r][r] lives in lane 4r + r/2, element r%2.
-        if (c == (r >> 1) && ok) y[row] = (r & 1) ? d1 : d0;
+#pragma unroll
+        for (int q = 0; q < RB; ++q) {
+            const uint64_t row = base + 8 * q + r;
+            if (c == (r >> 1) && row < last) y[row] = (r & 1) ? d1[q] : d0[q];
+        }
     }
 }
 
@@ -200,10 +230,15 @@ cudaError_t launch_spmv(int unit, uint64_t r0, uint64_t r1, const int* rp, const
     const uint64_t rows = r1 - r0;
     const uint64_t max_blocks = (uint64_t)kNumSMs * (uint64_t)t.spmv_blocks_per_sm;
     if (unit == 1) {
-        uint64_t blocks = (rows + 63) / 64;  // 8 warps x 8 rows
+        const int tthreads = t.spmv_tc_threads, RB = t.spmv_tc_rows;
+        uint64_t blocks = (rows + (uint64_t)(tthreads / 32) * 8 * RB - 1) / ((uint64_t)(tthreads / 32) * 8 * RB);
         const uint64_t cap = (uint64_t)kNumSMs * (uint64_t)t.spmv_tc_blocks_per_sm;
         if (blocks > cap) blocks = cap;
-        spmv_tc<<<(unsigned)blocks, threads, 0, s>>>(r0, r1, rp, col, val, x, col_base, y); note_launch();
+#define RLB_TC(R, S) spmv_tc<R, S><<<(unsigned)blocks, tthreads, 0, s>>>(r0, r1, rp, col, val, x, col_base, y)
+        if (t.spmv_sched == 0) { if (RB == 2) RLB_TC(2, 0); else RLB_TC(1, 0); }
+        else { if (RB == 2) RLB_TC(2, 1); else RLB_TC(1, 1); }
+#undef RLB_TC
+        note_launch();
         return cudaGetLastError();
     }
     const int R = t.spmv_rows;
