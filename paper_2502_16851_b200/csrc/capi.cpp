@@ -764,6 +764,7 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         else if (k == "spmv_tc_blocks_per_sm") slot = &t.spmv_tc_blocks_per_sm;
         else if (k == "spmv_tc_threads") slot = &t.spmv_tc_threads;
         else if (k == "spmv_tc_rows") slot = &t.spmv_tc_rows;
+        else if (k == "spmv_l1_carveout") slot = &t.spmv_l1_carveout;
         else if (k == "spmv_xhint") slot = &t.spmv_xhint;
         else if (k == "scale_unroll") slot = &t.scale_unroll;
         else if (k == "stencil2d_rows") slot = &t.stencil2d_rows;
@@ -777,7 +778,7 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         else if (k == "stencil_tc3d_ctas_per_sm") slot = &t.stencil_tc3d_ctas_per_sm;
         else throw Error(ErrorKind::ValidationError, "unknown tuning key '" + k + "'");
         if (previous) *previous = *slot;
-        if (value < 0) throw Error(ErrorKind::InvalidRange, "tuning values must be >= 0");
+        if (value < -1) throw Error(ErrorKind::InvalidRange, "tuning values must be >= -1");
         *slot = static_cast<int>(value);
     });
 }

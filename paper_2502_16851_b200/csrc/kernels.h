@@ -16,6 +16,7 @@ struct Tuning {
     int spmv_threads = 1024;       // CTA size of the CUDA-core kernel (multiple of 32, <= 1024)
     int spmv_tc_blocks_per_sm = 1; // tensor-core SpMV grid = 148 * this
     int spmv_tc_threads = 1024;
+    int spmv_l1_carveout = -1;     // shared-memory carveout % for the CC kernel (-1 = driver default)
     int spmv_tc_rows = 1;          // 8-row blocks per warp iteration (1, 2)
     int spmv_plan_chunks = 4;      // pipelined row/x chunks of rl_spmv_plan_execute_host
     int spmv_sched = 1;            // 0 grid-stride, 1 contiguous row range per CTA

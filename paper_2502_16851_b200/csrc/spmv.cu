@@ -248,8 +248,13 @@ cudaError_t launch_spmv(int unit, uint64_t r0, uint64_t r1, const int* rp, const
     const uint64_t cap = (uint64_t)kNumSMs * (uint64_t)t.spmv_blocks_per_sm;
     if (blocks > cap) blocks = cap;
     const int sched = t.spmv_sched, xh = t.spmv_xhint;
-#define RLB_SPMV(RR, SS, XX) \
-    spmv_cc_v4<RR, SS, XX><<<(unsigned)blocks, cthreads, 0, s>>>(r0, r1, rp, col, val, x, col_base, y)
+#define RLB_SPMV(RR, SS, XX)                                                                      \
+    do {                                                                                          \
+        if (t.spmv_l1_carveout >= 0)                                                              \
+            cudaFuncSetAttribute(spmv_cc_v4<RR, SS, XX>,                                          \
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, t.spmv_l1_carveout); \
+        spmv_cc_v4<RR, SS, XX><<<(unsigned)blocks, cthreads, 0, s>>>(r0, r1, rp, col, val, x, col_base, y); \
+    } while (0)
 #define RLB_SPMV_R(SS, XX)                        \
     do {                                          \
         if (R == 1) RLB_SPMV(1, SS, XX);          \

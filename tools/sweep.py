@@ -55,7 +55,8 @@ def main(which):
         P.fill_uniform(x, 1, 4, 0, 1)
         nbytes = P.spmv_csr_model(n, n, n * k).traffic_bytes
         sweep("spmv_cc", lambda: P.spmv_csr(rp, col, val, x, y, unit=0), nbytes,
-              {"spmv_rows": [2], "spmv_sched": [1], "spmv_threads": [1024], "spmv_blocks_per_sm": [1]})
+              {"spmv_l1_carveout": [-1, 0, 25, 50], "spmv_xhint": [0, 1], "spmv_threads": [512, 1024],
+               "spmv_blocks_per_sm": [1, 2]})
         sweep("spmv_tc", lambda: P.spmv_csr(rp, col, val, x, y, unit=1), nbytes,
               {"spmv_tc_rows": [1, 2], "spmv_tc_threads": [256, 1024], "spmv_tc_blocks_per_sm": [1, 2, 4, 8],
                "spmv_sched": [0, 1]})
