@@ -348,6 +348,31 @@ def per_kernel_table(torch, P, D, hbm):
     return rows
 
 
+def temporal_blocking(torch, P, hbm, t1_ms_per_step):
+    """2d5pt with temporal depth 2 on the BASELINE grid
+    (100 timesteps = 50 fused sweeps).  Model bytes are stencil_model(2d5pt,
+    FP64, 2): 16 B per point per fused sweep (reference kernels.cpp:137-155)."""
+    shape = (16384, 16384)
+    u = torch.empty(shape, dtype=torch.float64, device="cuda")
+    P.stencil_init(u, 1, SEED)
+    v = u.clone()
+    P.stencil_temporal("2d5pt", u, v, 4, 2)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    kc, _ = P.stencil_temporal("2d5pt", u, v, 100, 2)
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e)
+    del u, v
+    torch.cuda.empty_cache()
+    gbs = kc.traffic_bytes / (ms * 1e-3) / 1e9
+    return {"2d5pt_t2": {"ms_per_timestep": round(ms / 100, 4), "model_gbs": round(gbs, 1),
+                         "frac_of_measured_peak": round(gbs / hbm, 4),
+                         "timestep_speedup_vs_t1": round(t1_ms_per_step / (ms / 100), 3),
+                         "note": "50 fused sweeps of 2 timesteps; bytes = stencil_model(t=2)"}}
+
+
 def add_bounds(P, rows, peaks, hbm):
     """TC/CC speedup ceiling per kernel from the measured B200 figures
     (kernel_speedup_ceiling, reference bounds.cpp:72-85)."""
@@ -582,6 +607,8 @@ def main():
     if world == 1 and not args.no_per_kernel:
         with ClockSampler(dev_index) as clk2:
             table = per_kernel_table(torch, P, D, hbm)
+            line["temporal_blocking"] = temporal_blocking(torch, P, hbm,
+                                                          table["2d5pt"]["cc"]["ms_per_unit"])
         # FP64 peaks last: the DFMA/DMMA chains run at the power cap and would
         # throttle the memory-bound kernels measured after them.
         peaks = fp64_peaks(torch, P)

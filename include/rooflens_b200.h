@@ -138,6 +138,19 @@ RL_API int rl_stencil(rl_unit unit, rl_precision precision, const char* preset,
                const uint64_t* dims, const double* weights, uint64_t steps, double* u,
                double* v, rl_stream stream, rl_kchar* out);
 
+/* Temporal blocking (stencil_model's temporal_depth t, kernels.cpp:137-155;
+ * PAPER.md:223-236): `steps` timesteps executed as steps/t fused sweeps of t
+ * timesteps each (plus steps%t single sweeps).  HBM sees one read of u and one
+ * write of v per fused sweep.  t = 1 behaves like rl_stencil; t = 2 is
+ * implemented for 2d5pt on the CUDA core (even nx, 16-byte aligned rows).
+ * Buffers swap once per sweep: *result_in_v (optional) reports where the
+ * final field is.  kchar = stencil_model(preset, FP64, t) x points x (steps/t)
+ * + stencil_model(preset, FP64, 1) x points x (steps%t). */
+RL_API int rl_stencil_temporal(rl_unit unit, rl_precision precision, const char* preset,
+                               const uint64_t* dims, const double* weights, uint64_t steps,
+                               uint64_t temporal_depth, double* u, double* v, rl_stream stream,
+                               int* result_in_v, rl_kchar* out);
+
 /* One sweep v = S(u) restricted to outer indices [o_begin, o_end) (rows in 2D,
  * planes in 3D) -- the slab / interior-vs-edge building block.  Boundary
  * indices inside the range are skipped.  No accounting. */

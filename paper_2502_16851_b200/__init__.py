@@ -31,7 +31,7 @@ __all__ = [
     "CUDA_CORE", "TENSOR_CORE", "FP64", "FP32", "FP16", "RooflensError", "KernelCharacterization",
     "HardwareSpec", "lib", "library_path", "scale_model", "gemv_model", "spmv_generic_model",
     "spmv_csr_model", "stencil_model", "stencil_preset", "stencil_default_weights", "scale",
-    "spmv_csr", "spmv_csr_rows", "stencil", "stencil_sweep", "scale_host", "spmv_csr_host",
+    "spmv_csr", "spmv_csr_rows", "stencil", "stencil_temporal", "stencil_sweep", "scale_host", "spmv_csr_host",
     "stencil_host", "SpmvPlan", "fill_uniform", "gen_band_csr", "stencil_init", "load_spec", "builtin_spec",
     "machine_balance", "tensor_alpha", "attainable", "classify", "unoverlapped_speedup",
     "kernel_speedup_ceiling", "tensor_core_ceiling", "workload_ceiling", "min_temporal_depth",
@@ -136,6 +136,8 @@ _SIGNATURES = {
     "rl_spmv_csr": (_int, [_int, _int, _u64, _u64, _u64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _KP]),
     "rl_spmv_csr_rows": (_int, [_int, _int, _u64, _u64, _ptr, _ptr, _ptr, _ptr, _i64, _ptr, _ptr]),
     "rl_stencil": (_int, [_int, _int, C.c_char_p, C.POINTER(_u64), _ptr, _u64, _ptr, _ptr, _ptr, _KP]),
+    "rl_stencil_temporal": (_int, [_int, _int, C.c_char_p, C.POINTER(_u64), _ptr, _u64, _u64, _ptr, _ptr,
+                                   _ptr, C.POINTER(_int), _KP]),
     "rl_stencil_sweep": (_int, [_int, _int, C.c_char_p, C.POINTER(_u64), _ptr, _u64, _u64, _ptr,
                                 _ptr, _ptr]),
     "rl_scale_host": (_int, [_int, _int, _ptr, _ptr, _dbl, _u64, _KP]),
@@ -369,6 +371,21 @@ def stencil(preset: str, u, v, steps: int, weights=None, unit: int = CUDA_CORE, 
                             _dev_ptr(u, "f64", "u"), _dev_ptr(v, "f64", "v"), _stream(stream),
                             C.byref(k)))
     return _kc(k)
+
+
+def stencil_temporal(preset: str, u, v, steps: int, temporal_depth: int, weights=None,
+                     unit: int = CUDA_CORE, stream=None, precision: int = FP64):
+    """Temporal blocking: steps/t fused sweeps of t timesteps.  Returns
+    (KernelCharacterization, result_tensor)."""
+    if u.shape != v.shape:
+        raise ValueError("u and v must have the same shape")
+    k, inv = _KChar(), _int()
+    w = _weights(preset, weights)
+    _check(lib().rl_stencil_temporal(unit, precision, preset.encode(), _dims(preset, u),
+                                     C.cast(w, _ptr) if w is not None else None, steps, temporal_depth,
+                                     _dev_ptr(u, "f64", "u"), _dev_ptr(v, "f64", "v"), _stream(stream),
+                                     C.byref(inv), C.byref(k)))
+    return _kc(k), (v if inv.value else u)
 
 
 def stencil_sweep(preset: str, u, v, o_begin: int, o_end: int, weights=None,

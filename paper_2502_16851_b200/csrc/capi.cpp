@@ -180,6 +180,46 @@ KernelCharacterization stencil(ExecutionUnit unit, Precision p, const StencilSha
     return {shape.name, static_cast<std::uint64_t>(w), static_cast<std::uint64_t>(q)};
 }
 
+KernelCharacterization stencil_temporal(ExecutionUnit unit, Precision p, const StencilShape& shape,
+                                        const std::uint64_t dims[3], const double* weights,
+                                        std::uint64_t steps, std::uint64_t t, double* u, double* v,
+                                        Stream stream, int* result_in_v) {
+    const KernelCharacterization kt = stencil_model(shape, p, t);  // validates t >= 1
+    const KernelCharacterization k1 = stencil_model(shape, p, 1);
+    require_fp64(p);
+    if (!steps) throw Error(ErrorKind::InvalidCount, "stencil: steps must be >= 1");
+    require_ptr(u, "u");
+    require_ptr(v, "v");
+    if (u == v) throw Error(ErrorKind::ValidationError, "u and v must be distinct buffers");
+    if (t > 2) throw Error(ErrorKind::InvalidRange, "temporal depth > 2 is not implemented");
+    const rlb::StencilDesc d = make_desc(shape, dims, weights);
+    if (t == 2 && (unit != ExecutionUnit::CudaCore || d.preset != rlb::kP2d5 ||
+                   !rlb::stencil_tma_eligible(d, u, v)))
+        throw Error(ErrorKind::ValidationError,
+                    "temporal depth 2 is implemented for 2d5pt on the CUDA core with even nx and "
+                    "16-byte aligned rows");
+    const std::uint64_t fused = steps / t, rem = steps % t;
+    const unsigned __int128 pts = interior_points(d);
+    const unsigned __int128 w = pts * ((unsigned __int128)fused * kt.work_flops + (unsigned __int128)rem * k1.work_flops);
+    const unsigned __int128 q = pts * ((unsigned __int128)fused * kt.traffic_bytes + (unsigned __int128)rem * k1.traffic_bytes);
+    if ((w >> 64) || (q >> 64)) throw Error(ErrorKind::InvalidRange, "stencil accounting overflows 64-bit count");
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const std::uint64_t outer = d.dim == 3 ? d.nz : d.ny;
+    std::uint64_t sweeps = 0;
+    for (std::uint64_t i = 0; i < fused + rem; ++i, ++sweeps) {
+        const double* src = (sweeps & 1) ? v : u;
+        double* dst = (sweeps & 1) ? u : v;
+        if (i < fused && t == 2) {
+            const std::uint64_t lo = std::max<std::uint64_t>(1, 0), hi = outer - 1;
+            cuda_check(rlb::launch_stencil_tma_t2(d, lo, hi, src, dst, s), "stencil (temporal depth 2)");
+        } else {
+            sweep(unit, d, 0, outer, src, dst, s);
+        }
+    }
+    if (result_in_v) *result_in_v = (int)(sweeps & 1);
+    return {shape.name, static_cast<std::uint64_t>(w), static_cast<std::uint64_t>(q)};
+}
+
 }  // namespace rooflens::b200
 
 // ===========================================================================
@@ -604,6 +644,15 @@ int rl_stencil(rl_unit u, rl_precision p, const char* preset, const uint64_t* di
                                          steps, uu, v, s));
     });
 }
+int rl_stencil_temporal(rl_unit u, rl_precision p, const char* preset, const uint64_t* dims,
+                        const double* weights, uint64_t steps, uint64_t t, double* uu, double* v,
+                        rl_stream s, int* result_in_v, rl_kchar* out) {
+    return guarded([&] {
+        require_ptr(dims, "dims");
+        put(out, rooflens::b200::stencil_temporal(unit_of(u), prec_of(p), shape_of(preset), dims, weights,
+                                                  steps, t, uu, v, s, result_in_v));
+    });
+}
 int rl_stencil_sweep(rl_unit u, rl_precision p, const char* preset, const uint64_t* dims,
                      const double* weights, uint64_t o0, uint64_t o1, const double* uu, double* v,
                      rl_stream s) {
@@ -774,6 +823,7 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         else if (k == "stencil_ctas_per_sm") slot = &t.stencil_ctas_per_sm;
         else if (k == "stencil_rows_per_thread") slot = &t.stencil_rows_per_thread;
         else if (k == "stencil2d_rows_per_thread") slot = &t.stencil2d_rows_per_thread;
+        else if (k == "stencil_t2_ctas_per_sm") slot = &t.stencil_t2_ctas_per_sm;
         else if (k == "stencil_tc_ctas_per_sm") slot = &t.stencil_tc_ctas_per_sm;
         else if (k == "stencil_tc3d_ctas_per_sm") slot = &t.stencil_tc3d_ctas_per_sm;
         else throw Error(ErrorKind::ValidationError, "unknown tuning key '" + k + "'");

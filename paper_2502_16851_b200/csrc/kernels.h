@@ -28,6 +28,7 @@ struct Tuning {
     int stencil_ctas_per_sm = 1;   // grid sizing target, TMA CUDA-core kernels
     int stencil_rows_per_thread = 2;   // 3D TMA CUDA-core kernels: 2, 4 or 8 (CTA = 64*16/this threads)
     int stencil2d_rows_per_thread = 4; // 2D TMA CUDA-core kernel (swept: tools/sweep.py)
+    int stencil_t2_ctas_per_sm = 8;    // temporal-depth-2 2d5pt kernel (swept)
     int stencil_tc_ctas_per_sm = 1;    // ... 2D tensor-core kernel
     int stencil_tc3d_ctas_per_sm = 8;  // ... 3D tensor-core kernels
 };
@@ -61,6 +62,10 @@ cudaError_t launch_stencil_tc(const StencilDesc& d, uint64_t o0, uint64_t o1, co
 bool stencil_tma_eligible(const StencilDesc& d, const double* u, const double* v);
 cudaError_t launch_stencil_tma(int unit, const StencilDesc& d, uint64_t o0, uint64_t o1,
                                const double* u, double* v, cudaStream_t s);
+
+// Two fused timesteps of 2d5pt (temporal blocking, CUDA core, TMA-eligible grids).
+cudaError_t launch_stencil_tma_t2(const StencilDesc& d, uint64_t o0, uint64_t o1, const double* u,
+                                  double* v, cudaStream_t s);
 
 // Launch accounting (rl_kernel_launches): every <<<>>> site reports itself.
 void note_launch(uint64_t n = 1);

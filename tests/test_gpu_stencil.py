@@ -172,3 +172,37 @@ def test_3d_full_grid(cuda, preset, unit):
     torch.cuda.synchronize()
     u0 = O.stencil_init(shape, 1, 2025)
     assert O.rel_err(u.cpu().numpy(), O.stencil(preset, u0, 2)) <= TOL
+
+
+@pytest.mark.parametrize("shape", [(64, 128), (130, 258), (301, 516), (1030, 1026)])
+@pytest.mark.parametrize("steps", [1, 2, 5, 8])
+def test_2d5pt_temporal_depth2(cuda, shape, steps):
+    """Temporal blocking (t = 2) equals `steps` single timesteps."""
+    import torch
+
+    u0 = O.stencil_init(shape, 1, 19)
+    u = torch.from_numpy(u0.copy()).cuda()
+    v = torch.from_numpy(u0.copy()).cuda()
+    kc, out = P.stencil_temporal("2d5pt", u, v, steps, 2)
+    torch.cuda.synchronize()
+    ref = O.stencil("2d5pt", u0, steps)
+    got = out.cpu().numpy()
+    assert O.rel_err(got, ref) <= TOL
+    ring = _ring_mask(shape, 1)
+    assert O.bit_mismatches(got[ring], u0[ring]) == 0
+    pts = (shape[0] - 2) * (shape[1] - 2)
+    fused, rem = steps // 2, steps % 2
+    assert kc.traffic_bytes == 16 * pts * (fused + rem)
+    assert kc.work_flops == pts * (fused * 20 + rem * 10)
+
+
+def test_temporal_depth_restrictions(cuda):
+    import torch
+
+    u = torch.zeros((20, 24, 64), dtype=torch.float64, device="cuda")
+    with pytest.raises(P.RooflensError) as e:
+        P.stencil_temporal("3d7pt", u, u.clone(), 4, 2)
+    assert e.value.kind == "ValidationError"
+    with pytest.raises(P.RooflensError) as e:
+        P.stencil_temporal("2d5pt", u[0], u[1].clone(), 4, 0)
+    assert e.value.kind == "InvalidCount"

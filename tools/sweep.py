@@ -62,6 +62,16 @@ def main(which):
                "spmv_sched": [0, 1]})
 
 
+def temporal():
+    import math
+    u = torch.empty((16384, 16384), dtype=torch.float64, device="cuda")
+    P.stencil_init(u, 1, 1)
+    v = u.clone()
+    nbytes = 16 * math.prod(s - 2 for s in u.shape)  # per fused sweep (t = 2)
+    sweep("2d5pt_t2", lambda: P.stencil_temporal("2d5pt", u, v, 2, 2), nbytes,
+          {"stencil_t2_ctas_per_sm": [8, 12, 16, 24, 32, 48]})
+
+
 def stencils():
     import math
     for preset, shape in (("2d5pt", (16384, 16384)), ("3d7pt", (512, 512, 512)), ("3d27pt", (512, 512, 512))):
@@ -82,5 +92,7 @@ if __name__ == "__main__":
     for w in sys.argv[1:]:
         if w == "stencil":
             stencils()
+        elif w == "temporal":
+            temporal()
         else:
             main(w)
