@@ -826,6 +826,8 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         else if (k == "stencil_t2_ctas_per_sm") slot = &t.stencil_t2_ctas_per_sm;
         else if (k == "stencil_tc_ctas_per_sm") slot = &t.stencil_tc_ctas_per_sm;
         else if (k == "stencil_tc3d_ctas_per_sm") slot = &t.stencil_tc3d_ctas_per_sm;
+        else if (k == "stencil_tc3d_mode") slot = &t.stencil_tc3d_mode;
+        else if (k == "stencil_tc1_ctas_per_sm") slot = &t.stencil_tc1_ctas_per_sm;
         else throw Error(ErrorKind::ValidationError, "unknown tuning key '" + k + "'");
         if (previous) *previous = *slot;
         if (value < -1) throw Error(ErrorKind::InvalidRange, "tuning values must be >= -1");

@@ -648,6 +648,180 @@ __global__ void __launch_bounds__(128) st3d_tma_tc(const __grid_constant__ CUten
     }
 }
 
+// ===========================================================================
+// Tensor core, 3D, one plane at a time (partial sums, like the CUDA-core 3D
+// kernel): plane p contributes P_-1(p) to output p+1, P_0(p) to p and P_+1(p)
+// to p-1, accumulated in D-fragment registers.
+//   KIND 0 (3d7pt): P_0 = in-plane banded products (6 DMMA), P_-1/P_+1 =
+//     w_z-/w_z+ times the centre values at the accumulator positions.
+//   KIND 1 (3d27pt class weights): with a = U[y] and b = U[y-1] + U[y+1],
+//     P_0 = a*band(g1,g0,g1) + b*band(g2,g1,g2) and
+//     P_+-1 = a*band(g2,g1,g2) + b*band(g3,g2,g3)                 12 DMMA
+//   KIND 2 (general 27pt): P_dz = sum_dy U[y+dy]*band(w[dz][dy])    27 DMMA
+// Only one stage is live, so shared-memory operand traffic is 3x lower than
+// the 3-plane formulation for 27pt, at the price of more DMMA.
+// ===========================================================================
+template <int KIND, int S>
+__global__ void __launch_bounds__(128) st3d_tma_tc1(const __grid_constant__ CUtensorMap tm,
+                                                    double* __restrict__ v, StencilDesc d, uint64_t z_begin,
+                                                    uint64_t z_end, int zchunk, int tiles_x, int tiles_xy) {
+    constexpr int BX = kBX, STAGE = stage_doubles(BX);
+    extern __shared__ __align__(128) double smem[];
+    Ring<S, STAGE> ring(smem);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int r = lane >> 2, c = lane & 3;
+    const int rb = warp >> 1, cb0 = 4 * (warp & 1);
+    const int tile = blockIdx.x % tiles_xy;
+    const uint64_t za = z_begin + (uint64_t)(blockIdx.x / tiles_xy) * zchunk;
+    if (za >= z_end) return;
+    const uint64_t zb = min(za + (uint64_t)zchunk, z_end);
+    const int np = (int)(zb - za) + 2;
+    const int64_t x0 = (int64_t)(tile % tiles_x) * kTX, y0 = (int64_t)(tile / tiles_x) * kTY;
+    const uint64_t nx = d.nx, ny = d.ny;
+    ring.init(4);
+    auto issue = [&](int k) {
+        mbar_expect_tx(ring.full + (k % S), kBY * BX * 8);
+        tma3d(ring.stage(k), &tm, ring.full + (k % S), (int)(x0 - kCofs), (int)(y0 - 1), (int)(za - 1 + k));
+    };
+    if (tid == 0)
+        for (int k = 0; k < S && k < np; ++k) issue(k);
+    auto at = [&](int j, int i) { return j * BX + min(max(i - 1 + kCofs, 0), BX - 1); };
+
+    // band fragments (B operand of the horizontal products, A of the vertical one)
+    double f0[3], f1[3], f2[3];
+#pragma unroll
+    for (int kb = 0; kb < 3; ++kb) {
+        const int kk = 4 * kb + c;
+        if (KIND == 0) {
+            f0[kb] = bandv(kk, r, d.w[3], d.w[0], d.w[4]);  // Ty (vertical, with centre)
+            f1[kb] = bandv(kk, r, d.w[5], 0.0, d.w[6]);     // Tx
+            f2[kb] = 0.0;
+        } else {
+            f0[kb] = bandv(kk, r, d.w[1], d.w[0], d.w[1]);  // g1 g0 g1
+            f1[kb] = bandv(kk, r, d.w[2], d.w[1], d.w[2]);  // g2 g1 g2
+            f2[kb] = bandv(kk, r, d.w[3], d.w[2], d.w[3]);  // g3 g2 g3
+        }
+    }
+    double gen[KIND == 2 ? 27 : 1];
+    if (KIND == 2) {
+#pragma unroll
+        for (int q = 0; q < 9; ++q)
+#pragma unroll
+            for (int kb = 0; kb < 3; ++kb)
+                gen[q * 3 + kb] = bandv(4 * kb + c, r, d.w[q * 3 + 0], d.w[q * 3 + 1], d.w[q * 3 + 2]);
+    }
+
+    double acc_a[4][2], acc_b[4][2];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) acc_a[t][0] = acc_a[t][1] = acc_b[t][0] = acc_b[t][1] = 0.0;
+    const int64_t yo = y0 + 8 * rb + r;
+    const bool row_ok = yo >= 1 && yo <= (int64_t)ny - 2;
+    for (int k = 0; k < np; ++k) {
+        ring.wait_full(k);
+        const double* P = ring.stage(k);
+        double pm[4][2], p0[4][2], pp[4][2];
+        double ca = 0.0, cbp = 0.0;  // operands carried from k-step 2 to the next tile's k-step 0
+        double cg[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int cb = cb0 + t;
+            if (KIND == 0) {
+                double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                for (int kb = 0; kb < 3; ++kb) {
+                    const int j = min(4 * kb + c, 9);
+                    dmma_m8n8k4(d0, d1, f0[kb], P[at(8 * rb + j, 8 * cb + r + 1)], d0, d1);
+                }
+#pragma unroll
+                for (int kb = 0; kb < 3; ++kb) {
+                    double a;
+                    if (kb == 0 && t > 0) a = ca;
+                    else a = P[at(8 * rb + r + 1, 8 * cb + 4 * kb + c)];
+                    if (kb == 2) ca = a;
+                    dmma_m8n8k4(d0, d1, a, f1[kb], d0, d1);
+                }
+                const int s = at(8 * rb + r + 1, 8 * cb + 2 * c + 1);
+                const double z0 = P[s], z1 = P[s + 1];
+                p0[t][0] = d0; p0[t][1] = d1;
+                pm[t][0] = d.w[1] * z0; pm[t][1] = d.w[1] * z1;
+                pp[t][0] = d.w[2] * z0; pp[t][1] = d.w[2] * z1;
+            } else if (KIND == 1) {
+                double e0 = 0.0, e1 = 0.0, g0 = 0.0, g1 = 0.0;
+#pragma unroll
+                for (int kb = 0; kb < 3; ++kb) {
+                    double a, b;
+                    if (kb == 0 && t > 0) {
+                        a = ca; b = cbp;
+                    } else {
+                        const int colj = 8 * cb + 4 * kb + c;
+                        a = P[at(8 * rb + r + 1, colj)];
+                        b = P[at(8 * rb + r, colj)] + P[at(8 * rb + r + 2, colj)];
+                    }
+                    if (kb == 2) { ca = a; cbp = b; }
+                    dmma_m8n8k4(e0, e1, a, f0[kb], e0, e1);  // P_0
+                    dmma_m8n8k4(e0, e1, b, f1[kb], e0, e1);
+                    dmma_m8n8k4(g0, g1, a, f1[kb], g0, g1);  // P_+-1
+                    dmma_m8n8k4(g0, g1, b, f2[kb], g0, g1);
+                }
+                p0[t][0] = e0; p0[t][1] = e1;
+                pm[t][0] = pp[t][0] = g0; pm[t][1] = pp[t][1] = g1;
+            } else {
+                double m0 = 0.0, m1 = 0.0, e0 = 0.0, e1 = 0.0, q0 = 0.0, q1 = 0.0;
+#pragma unroll
+                for (int kb = 0; kb < 3; ++kb) {
+                    double g[3];
+                    if (kb == 0 && t > 0) {
+                        g[0] = cg[0]; g[1] = cg[1]; g[2] = cg[2];
+                    } else {
+                        const int colj = 8 * cb + 4 * kb + c;
+#pragma unroll
+                        for (int dy = 0; dy < 3; ++dy) g[dy] = P[at(8 * rb + r + dy, colj)];
+                    }
+                    if (kb == 2) { cg[0] = g[0]; cg[1] = g[1]; cg[2] = g[2]; }
+#pragma unroll
+                    for (int dy = 0; dy < 3; ++dy) {
+                        dmma_m8n8k4(m0, m1, g[dy], gen[(0 * 3 + dy) * 3 + kb], m0, m1);  // dz = -1
+                        dmma_m8n8k4(e0, e1, g[dy], gen[(1 * 3 + dy) * 3 + kb], e0, e1);  // dz =  0
+                        dmma_m8n8k4(q0, q1, g[dy], gen[(2 * 3 + dy) * 3 + kb], q0, q1);  // dz = +1
+                    }
+                }
+                pm[t][0] = m0; pm[t][1] = m1;
+                p0[t][0] = e0; p0[t][1] = e1;
+                pp[t][0] = q0; pp[t][1] = q1;
+            }
+        }
+        ring.release(k);
+        if (tid == 0 && k + S < np) {
+            ring.wait_empty(k);
+            issue(k + S);
+        }
+        double o[4][2];
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                o[t][h] = acc_a[t][h] + pp[t][h];
+                acc_a[t][h] = acc_b[t][h] + p0[t][h];
+                acc_b[t][h] = pm[t][h];
+            }
+        if (k >= 2 && row_ok) {
+            const uint64_t z = za - 2 + (uint64_t)k;
+            double* vr = v + (z * ny + (uint64_t)yo) * nx;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const int64_t xx = x0 + 8 * (cb0 + t) + 2 * c;
+                const bool i0 = xx >= 1 && xx <= (int64_t)nx - 2, i1 = xx + 1 <= (int64_t)nx - 2;
+                if (i0 && i1)
+                    asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(vr + xx), "d"(o[t][0]), "d"(o[t][1]) : "memory");
+                else {
+                    if (i0) vr[xx] = o[t][0];
+                    if (i1) vr[xx + 1] = o[t][1];
+                }
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // host: tensor maps
 // ---------------------------------------------------------------------------
@@ -780,7 +954,10 @@ cudaError_t launch_stencil_tma(int unit, const StencilDesc& d, uint64_t o0, uint
     const int tiles_x = (int)((d.nx + kTX - 1) / kTX);
     const int tiles_xy = tiles_x * (int)((d.ny + kTY - 1) / kTY);
     const int nch = split_count(tiles_xy, o1 - o0, 8,
-                                unit == 1 ? tuning().stencil_tc3d_ctas_per_sm : tuning().stencil_ctas_per_sm);
+                                unit == 1 ? (((tuning().stencil_tc3d_mode >> (d.preset == kP3d7 ? 0 : 1)) & 1)
+                                                 ? tuning().stencil_tc1_ctas_per_sm
+                                                 : tuning().stencil_tc3d_ctas_per_sm)
+                                          : tuning().stencil_ctas_per_sm);
     const int zchunk = (int)((o1 - o0 + nch - 1) / nch);
     const int zch = (int)((o1 - o0 + zchunk - 1) / zchunk);
     const unsigned grid = (unsigned)(tiles_xy * zch);
@@ -795,7 +972,19 @@ cudaError_t launch_stencil_tma(int unit, const StencilDesc& d, uint64_t o0, uint
             kind = 1;
         }
     }
-    if (unit == 1) {
+    const bool tc_onepl = unit == 1 && ((tuning().stencil_tc3d_mode >> (kind == 0 ? 0 : 1)) & 1);
+    if (tc_onepl) {
+        constexpr int S = 4;
+        const size_t sm = ring_bytes<S, kBX>();
+        const int tk = kind == 0 ? 0 : (kind == 2 ? 1 : 2);
+#define RLB_TC1(K)                                                                             \
+    do {                                                                                       \
+        if ((e = prep(st3d_tma_tc1<K, S>, sm)) != cudaSuccess) return e;                      \
+        st3d_tma_tc1<K, S><<<grid, 128, sm, s>>>(m, v, dd, o0, o1, zchunk, tiles_x, tiles_xy); \
+    } while (0)
+        if (tk == 0) RLB_TC1(0); else if (tk == 1) RLB_TC1(1); else RLB_TC1(2);
+#undef RLB_TC1
+    } else if (unit == 1) {
         constexpr int S = 5;
         const size_t sm = ring_bytes<S, kBX>();
         const int tk = kind == 0 ? 0 : (kind == 2 ? 1 : 2);  // TC kinds: 0 7pt, 1 class, 2 general

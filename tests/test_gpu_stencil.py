@@ -206,3 +206,25 @@ def test_temporal_depth_restrictions(cuda):
     with pytest.raises(P.RooflensError) as e:
         P.stencil_temporal("2d5pt", u[0], u[1].clone(), 4, 0)
     assert e.value.kind == "InvalidCount"
+
+
+@pytest.mark.parametrize("mode", [0, 3])
+@pytest.mark.parametrize("preset", ["3d7pt", "3d27pt"])
+@pytest.mark.parametrize("shape", [(10, 17, 66), (34, 20, 130), (40, 40, 64)])
+def test_3d_tensor_core_formulations(cuda, mode, preset, shape):
+    """Both 3D tensor-core formulations (3 planes resident / one plane with
+    partial sums) match the oracle, for class and general 27pt weights."""
+    import torch
+
+    prev = P.tuning_set("stencil_tc3d_mode", mode)
+    try:
+        u0 = O.stencil_init(shape, 1, 23)
+        out, _ = _run(torch, preset, u0, 3, P.TENSOR_CORE)
+        assert O.rel_err(out, O.stencil(preset, u0, 3)) <= TOL
+        if preset == "3d27pt":
+            w = np.random.default_rng(7).uniform(0, 1, 27)
+            w /= w.sum()
+            out, _ = _run(torch, preset, u0, 2, P.TENSOR_CORE, weights=w)
+            assert O.rel_err(out, O.stencil(preset, u0, 2, w)) <= TOL
+    finally:
+        P.tuning_set("stencil_tc3d_mode", prev)

@@ -80,8 +80,9 @@ def stencils():
         v = u.clone()
         nbytes = 2 * 16 * math.prod(s - 2 for s in shape)
         for unit in (0, 1):
-            grid = ({"stencil_rows_per_thread": [2, 4], "stencil2d_rows_per_thread": [2, 4]} if unit == 0
-                    else {"stencil_tc_ctas_per_sm": [1, 2], "stencil_tc3d_ctas_per_sm": [4, 8, 12, 16, 24]})
+            if preset == "2d5pt" or unit == 0:
+                continue
+            grid = {"stencil_tc3d_mode": [0, 1], "stencil_tc1_ctas_per_sm": [1, 2, 4, 8, 16]}
             sweep(f"{preset}_{'cc' if unit == 0 else 'tc'}", lambda: P.stencil(preset, u, v, 2, unit=unit),
                   nbytes, grid)
         del u, v
