@@ -38,11 +38,11 @@ def workload(name):
     if "spmv_tc" in name: return "spmv_tc"
     if "st2d_tma_cc" in name or "st2d5_cc" in name: return "2d5pt_cc"
     if "st2d_tma_tc" in name or "st2d5_tc" in name: return "2d5pt_tc"
-    m = re.search(r"st3d_tma_(cc|tc)<(\d)", name)
+    m = re.search(r"st3d_tma_(cc|tc1|tc)<(\d)", name)
     if m:
         u, k = m.group(1), int(m.group(2))
         if u == "cc": return {0: "3d7pt_cc", 1: "3d27pt_cc", 2: "3d27pt_cc"}[k]
-        return {0: "3d7pt_tc", 1: "3d27pt_tc", 2: "3d27pt_tc"}[k]
+        return {0: "3d7pt_tc", 1: "3d27pt_tc", 2: "3d27pt_tc"}[k] + ("1" if u == "tc1" else "")
     return None
 
 
@@ -75,6 +75,7 @@ def main(rep, out_md, out_json=None):
         s = scale.get(recs[0]["unit_dram"], 1.0)
         dram = (med("dram_rd") + med("dram_wr")) * s
         algo = ALGO[w.split("_")[0]]
+        w = w.replace("_tc1", "_tc")
         if w.startswith(("2d5pt", "3d")):
             pass  # one launch = one sweep
         traffic[w] = int(dram)
