@@ -373,6 +373,38 @@ def temporal_blocking(torch, P, hbm, t1_ms_per_step):
                          "note": "50 fused sweeps of 2 timesteps; bytes = stencil_model(t=2)"}}
 
 
+def gemv_rows(torch, P, hbm, reps=10):
+    """dense GEMV y = A x (gemv_model bytes, kernels.cpp:88-101),
+    A 16384 x 65536 FP64 (8 GiB, row-major)."""
+    m, n = 16384, 65536
+    A = torch.empty((m, n), dtype=torch.float64, device="cuda")
+    P.fill_uniform(A.view(-1), SEED, 6, 0, 1)
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    P.fill_uniform(x, SEED, 4, 0, 1)
+    y = torch.empty(m, dtype=torch.float64, device="cuda")
+    res = {}
+    for uname, unit in (("cc", P.CUDA_CORE), ("tc", P.TENSOR_CORE)):
+        kc = P.gemv(A, x, y, unit=unit)
+        for _ in range(2):
+            P.gemv(A, x, y, unit=unit)
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            P.gemv(A, x, y, unit=unit)
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / reps
+        gbs = kc.traffic_bytes / (ms * 1e-3) / 1e9
+        res[uname] = {"gbs": round(gbs, 1), "frac_of_measured_peak": round(gbs / hbm, 4), "ms": round(ms, 4)}
+    res["tc_over_cc"] = round(res["tc"]["gbs"] / res["cc"]["gbs"], 4)
+    res["intensity"] = round(P.gemv_model(m, n).intensity, 5)
+    res["config"] = "16384 x 65536 row-major FP64"
+    del A
+    torch.cuda.empty_cache()
+    return res
+
+
 def add_bounds(P, rows, peaks, hbm):
     """TC/CC speedup ceiling per kernel from the measured B200 figures
     (kernel_speedup_ceiling, reference bounds.cpp:72-85)."""
@@ -609,10 +641,12 @@ def main():
             table = per_kernel_table(torch, P, D, hbm)
             line["temporal_blocking"] = temporal_blocking(torch, P, hbm,
                                                           table["2d5pt"]["cc"]["ms_per_unit"])
+            line["next_rows"] = {"gemv": gemv_rows(torch, P, hbm)}
         # FP64 peaks last: the DFMA/DMMA chains run at the power cap and would
         # throttle the memory-bound kernels measured after them.
         peaks = fp64_peaks(torch, P)
         bounds = add_bounds(P, table, peaks, hbm)
+        add_bounds(P, line["next_rows"], peaks, hbm)
         line["per_kernel"] = table
         line["fp64_peaks_tflops"] = peaks
         line["bounds"] = bounds

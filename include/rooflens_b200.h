@@ -115,6 +115,11 @@ RL_API int rl_stencil_default_weights(const char* name, double* weights, uint64_
 RL_API int rl_scale(rl_unit unit, rl_precision precision, double* a, const double* b, double q,
              uint64_t n, rl_stream stream, rl_kchar* out);
 
+/* Dense GEMV y = A*x, row-major A (m x n) (next row #4).
+ * kchar = gemv_model(m, n, FP64) (kernels.cpp:88-101). */
+RL_API int rl_gemv(rl_unit unit, rl_precision precision, uint64_t m, uint64_t n, const double* A,
+                   const double* x, double* y, rl_stream stream, rl_kchar* out);
+
 /* CSR SpMV y = A*x, int32 row_ptr (m+1) / col (nnz),
  * 0-based, column indices in [0, n).  kchar = spmv_csr_model(.., 4, FP64). */
 RL_API int rl_spmv_csr(rl_unit unit, rl_precision precision, uint64_t m, uint64_t n, uint64_t nnz,
@@ -209,6 +214,36 @@ RL_API int rl_gen_band_csr(uint64_t m_local, uint64_t row0, uint64_t n, uint32_t
  * (rows in 2D, planes in 3D) -- a whole grid or one rank's slab with ghosts. */
 RL_API int rl_stencil_init(double* u, const uint64_t* dims, int dim, uint64_t outer_begin,
                            uint64_t outer_end, int radius, uint64_t seed, rl_stream stream);
+
+/* ---------------------------------------------------------------------------
+ * Matrix Market ingestion (host) and per-matrix roofline analysis.
+ * ------------------------------------------------------------------------- */
+
+/* replaces rooflens::parse_stats_file (matrix_market.cpp:126-201): rows, cols
+ * and the expanded nnz (symmetric storage counted twice off the diagonal);
+ * same ErrorKinds (BadBanner, UnsupportedFormat, MalformedEntry,
+ * IndexOutOfRange, TruncatedFile, IoError, ValidationError). */
+RL_API int rl_mtx_stats(const char* path, uint64_t* rows, uint64_t* cols, uint64_t* nnz);
+/* Extension: materialise the CSR (0-based int32, columns sorted per row,
+ * symmetric/skew storage expanded, pattern = 1.0) into caller buffers of at
+ * least rows+1 / nnz entries (sizes from rl_mtx_stats). */
+RL_API int rl_mtx_read_csr(const char* path, uint64_t row_capacity, uint64_t nnz_capacity,
+                           int32_t* row_ptr, int32_t* col, double* val, uint64_t* rows,
+                           uint64_t* cols, uint64_t* nnz);
+
+/* replaces rooflens::stats_to_report (matrix_market.cpp:203-216). */
+typedef struct {
+    uint64_t work_flops;
+    uint64_t traffic_bytes;
+    int boundedness;          /* rl_boundedness vs the CUDA-core balance */
+    double kernel_ceiling;    /* kernel_speedup_ceiling at the spec's alpha */
+    int kernel_ceiling_warnings;
+    double workload_ceiling;
+    uint64_t csr_bytes;
+    int fits_in_l2;
+} rl_matrix_analysis;
+RL_API int rl_matrix_analysis_of(uint64_t rows, uint64_t cols, uint64_t nnz, const rl_hw_spec* spec,
+                                 rl_precision precision, rl_matrix_analysis* out);
 
 /* ---------------------------------------------------------------------------
  * Hardware spec, roofline and speedup bounds (pure host functions).

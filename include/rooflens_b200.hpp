@@ -91,6 +91,8 @@ KernelCharacterization stencil_model(const StencilShape& shape, Precision precis
 // Executing kernels (device pointers, asynchronous on `stream`).
 KernelCharacterization scale(ExecutionUnit unit, Precision precision, double* a, const double* b,
                              double q, std::uint64_t n, Stream stream);
+KernelCharacterization gemv(ExecutionUnit unit, Precision precision, std::uint64_t m, std::uint64_t n,
+                            const double* A, const double* x, double* y, Stream stream);
 KernelCharacterization spmv_csr(ExecutionUnit unit, Precision precision,
                                 const SparseMatrixStats& stats, const std::int32_t* row_ptr,
                                 const std::int32_t* col, const double* val, const double* x,
@@ -105,6 +107,11 @@ KernelCharacterization stencil(ExecutionUnit unit, Precision precision, const St
 void stencil_sweep(ExecutionUnit unit, Precision precision, const StencilShape& shape,
                    const std::uint64_t dims[3], const double* weights, std::uint64_t o_begin,
                    std::uint64_t o_end, const double* u, double* v, Stream stream);
+
+// Matrix Market (matrix_market.cpp:126-201) + CSR materialisation.
+SparseMatrixStats mtx_stats(const std::string& path);
+SparseMatrixStats mtx_read_csr(const std::string& path, std::vector<std::int32_t>& row_ptr,
+                               std::vector<std::int32_t>& col, std::vector<double>& val);
 
 // Hardware spec (hardware.hpp:43-89), FP64 slice.
 struct HardwareSpec {

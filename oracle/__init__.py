@@ -30,6 +30,7 @@ _ORC_SIGS = {
     "orc_fill_uniform": (None, [_ptr, _u64, _u64, _u64, _u64, _int]),
     "orc_scale": (None, [_ptr, _ptr, _dbl, _u64]),
     "orc_gen_band_csr": (_int, [_u64, _u64, _u64, C.c_uint32, _u64, _u64, _ptr, _ptr, _ptr]),
+    "orc_gemv": (None, [_u64, _u64, _ptr, _ptr, _ptr]),
     "orc_spmv_csr": (None, [_u64, _ptr, _ptr, _ptr, _ptr, _i64, _ptr]),
     "orc_preset_points": (_int, [C.c_char_p]),
     "orc_preset_offsets": (_int, [C.c_char_p, _ptr]),
@@ -62,6 +63,9 @@ _REF_SIGS = {
     "ref_unoverlapped_speedup": (_int, [_dbl, _dbl, _dbl, _dbl, _DP]),
     "ref_min_temporal_depth": (_int, [_dbl, _dbl, _U64P]),
     "ref_tc_scale_trick_throughput": (_int, [_dbl, _u64, _u64, _DP]),
+    "ref_parse_stats_file": (_int, [C.c_char_p, _U64P, _U64P, _U64P]),
+    "ref_stats_to_report": (_int, [_u64, _u64, _u64, _dbl, _dbl, _dbl, _dbl, _U64P, _U64P, C.POINTER(_int), _DP,
+                                   C.POINTER(_int), _DP, _U64P, C.POINTER(_int)]),
 }
 
 _orc = None
@@ -128,6 +132,13 @@ def spmv_csr(rp, col, val, x, col_base=0) -> np.ndarray:
     y = np.empty(m, np.float64)
     orc().orc_spmv_csr(m, _p(rp), _p(col) if col.size else None, _p(val) if val.size else None,
                        _p(x) if x.size else None, col_base, _p(y))
+    return y
+
+
+def gemv(A: np.ndarray, x: np.ndarray) -> np.ndarray:
+    A = np.ascontiguousarray(A, np.float64)
+    y = np.empty(A.shape[0], np.float64)
+    orc().orc_gemv(A.shape[0], A.shape[1], _p(A), _p(np.ascontiguousarray(x, np.float64)), _p(y))
     return y
 
 

@@ -78,6 +78,16 @@ ORC_API void orc_scale(double* a, const double* b, double q, uint64_t n) {
     for (int64_t i = 0; i < (int64_t)n; ++i) a[i] = q * b[i];
 }
 
+/* Dense GEMV y = A x, row-major (model kernels.cpp:88-101). */
+ORC_API void orc_gemv(uint64_t m, uint64_t n, const double* A, const double* x, double* y) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < (int64_t)m; ++i) {
+        double acc = 0.0;
+        for (uint64_t k = 0; k < n; ++k) acc = acc + A[(uint64_t)i * n + k] * x[k];
+        y[i] = acc;
+    }
+}
+
 /* ------------------------------------------------------------------------ */
 /* Banded CSR generator (BASELINE.json configs[1]).                         */
 /* Row i (global) gets k distinct columns drawn uniformly from              */

@@ -18,6 +18,7 @@
 #include "rooflens/error.hpp"
 #include "rooflens/hardware.hpp"
 #include "rooflens/kernels.hpp"
+#include "rooflens/matrix_market.hpp"
 #include "rooflens/roofline.hpp"
 
 using namespace rooflens;
@@ -177,6 +178,34 @@ int ref_min_temporal_depth(double balance, double intensity, uint64_t* out) {
 
 int ref_tc_scale_trick_throughput(double peak_tc, uint64_t m, uint64_t n, double* out) {
     return guarded([&] { *out = tc_scale_trick_throughput(peak_tc, m, n); });
+}
+
+int ref_parse_stats_file(const char* path, uint64_t* rows, uint64_t* cols, uint64_t* nnz) {
+    return guarded([&] {
+        SparseMatrixStats s = parse_stats_file(path);
+        *rows = s.rows;
+        *cols = s.cols;
+        *nnz = s.nnz;
+    });
+}
+
+// stats_to_report on an FP64 spec built from SI figures.
+int ref_stats_to_report(uint64_t rows, uint64_t cols, uint64_t nnz, double bw, double l2, double p_cc,
+                        double p_tc, uint64_t* w, uint64_t* q, int* bound, double* kceil, int* kwarn,
+                        double* wceil, uint64_t* csr_bytes, int* fits) {
+    return guarded([&] {
+        HardwareSpec s = mk(bw, p_cc, p_tc);
+        s.l2_cache_bytes = l2;
+        MatrixAnalysis a = stats_to_report(SparseMatrixStats{rows, cols, nnz}, s, Precision::FP64);
+        *w = a.kernel.work_flops;
+        *q = a.kernel.traffic_bytes;
+        *bound = static_cast<int>(a.boundedness);
+        *kceil = a.kernel_ceiling.value;
+        *kwarn = static_cast<int>(a.kernel_ceiling.warnings.size());
+        *wceil = a.workload_ceiling.value;
+        *csr_bytes = a.csr_bytes;
+        *fits = a.fits_in_l2 ? 1 : 0;
+    });
 }
 
 }  // extern "C"

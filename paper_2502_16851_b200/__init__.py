@@ -31,8 +31,8 @@ __all__ = [
     "CUDA_CORE", "TENSOR_CORE", "FP64", "FP32", "FP16", "RooflensError", "KernelCharacterization",
     "HardwareSpec", "lib", "library_path", "scale_model", "gemv_model", "spmv_generic_model",
     "spmv_csr_model", "stencil_model", "stencil_preset", "stencil_default_weights", "scale",
-    "spmv_csr", "spmv_csr_rows", "stencil", "stencil_temporal", "stencil_sweep", "scale_host", "spmv_csr_host",
-    "stencil_host", "SpmvPlan", "fill_uniform", "gen_band_csr", "stencil_init", "load_spec", "builtin_spec",
+    "gemv", "spmv_csr", "spmv_csr_rows", "stencil", "stencil_temporal", "stencil_sweep", "scale_host", "spmv_csr_host",
+    "stencil_host", "SpmvPlan", "mtx_stats", "mtx_read_csr", "matrix_analysis", "fill_uniform", "gen_band_csr", "stencil_init", "load_spec", "builtin_spec",
     "machine_balance", "tensor_alpha", "attainable", "classify", "unoverlapped_speedup",
     "kernel_speedup_ceiling", "tensor_core_ceiling", "workload_ceiling", "min_temporal_depth",
     "tc_scale_trick_throughput", "fp64_peak_launch", "tuning_set", "kernel_launches",
@@ -133,6 +133,7 @@ _SIGNATURES = {
     "rl_stencil_preset": (_int, [C.c_char_p, C.POINTER(_int), C.POINTER(_u64), C.POINTER(_int)]),
     "rl_stencil_default_weights": (_int, [C.c_char_p, C.POINTER(_dbl), _u64]),
     "rl_scale": (_int, [_int, _int, _ptr, _ptr, _dbl, _u64, _ptr, _KP]),
+    "rl_gemv": (_int, [_int, _int, _u64, _u64, _ptr, _ptr, _ptr, _ptr, _KP]),
     "rl_spmv_csr": (_int, [_int, _int, _u64, _u64, _u64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _KP]),
     "rl_spmv_csr_rows": (_int, [_int, _int, _u64, _u64, _ptr, _ptr, _ptr, _ptr, _i64, _ptr, _ptr]),
     "rl_stencil": (_int, [_int, _int, C.c_char_p, C.POINTER(_u64), _ptr, _u64, _ptr, _ptr, _ptr, _KP]),
@@ -151,6 +152,10 @@ _SIGNATURES = {
     "rl_fill_uniform": (_int, [_ptr, _u64, _u64, _u64, _u64, _int, _ptr]),
     "rl_gen_band_csr": (_int, [_u64, _u64, _u64, C.c_uint32, _u64, _u64, _ptr, _ptr, _ptr, _ptr]),
     "rl_stencil_init": (_int, [_ptr, C.POINTER(_u64), _int, _u64, _u64, _int, _u64, _ptr]),
+    "rl_mtx_stats": (_int, [C.c_char_p, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64)]),
+    "rl_mtx_read_csr": (_int, [C.c_char_p, _u64, _u64, _ptr, _ptr, _ptr, C.POINTER(_u64), C.POINTER(_u64),
+                               C.POINTER(_u64)]),
+    "rl_matrix_analysis_of": (_int, [_u64, _u64, _u64, _HP, _int, _ptr]),
     "rl_load_spec": (_int, [C.c_char_p, _HP]),
     "rl_builtin_spec": (_int, [C.c_char_p, _HP]),
     "rl_machine_balance": (_int, [_HP, _int, _int, C.POINTER(_dbl)]),
@@ -307,6 +312,17 @@ def scale(a, b, q: float, unit: int = CUDA_CORE, stream=None, precision: int = F
     k = _KChar()
     _check(lib().rl_scale(unit, precision, _dev_ptr(a, "f64", "a"), _dev_ptr(b, "f64", "b"),
                           float(q), n, _stream(stream), C.byref(k)))
+    return _kc(k)
+
+
+def gemv(A, x, y, unit: int = CUDA_CORE, stream=None, precision: int = FP64):
+    """y = A x for a row-major (m, n) float64 tensor A."""
+    m, n = A.shape
+    if x.numel() != n or y.numel() != m:
+        raise ValueError("inconsistent GEMV sizes")
+    k = _KChar()
+    _check(lib().rl_gemv(unit, precision, m, n, _dev_ptr(A, "f64", "A"), _dev_ptr(x, "f64", "x"),
+                         _dev_ptr(y, "f64", "y"), _stream(stream), C.byref(k)))
     return _kc(k)
 
 
@@ -491,6 +507,44 @@ def stencil_init(u, radius: int, seed: int, outer_begin: int = 0, global_shape=N
     dims = (_u64 * 3)(gs[-1], gs[-2], gs[0] if dim == 3 else 1)
     _check(lib().rl_stencil_init(_dev_ptr(u, "f64", "u"), dims, dim, outer_begin,
                                  outer_begin + u.shape[0], radius, seed, _stream(stream)))
+
+
+# ----------------------------------------------------------------------------
+# Matrix Market
+# ----------------------------------------------------------------------------
+class _MatrixAnalysis(C.Structure):
+    _fields_ = [("work_flops", C.c_uint64), ("traffic_bytes", C.c_uint64), ("boundedness", C.c_int),
+                ("kernel_ceiling", C.c_double), ("kernel_ceiling_warnings", C.c_int),
+                ("workload_ceiling", C.c_double), ("csr_bytes", C.c_uint64), ("fits_in_l2", C.c_int)]
+
+
+def mtx_stats(path: str):
+    """(rows, cols, expanded nnz) -- reference parse_stats_file semantics."""
+    r, c, n = _u64(), _u64(), _u64()
+    _check(lib().rl_mtx_stats(os.fsencode(path), C.byref(r), C.byref(c), C.byref(n)))
+    return r.value, c.value, n.value
+
+
+def mtx_read_csr(path: str):
+    """CSR (row_ptr int32, col int32, val float64) and the column count."""
+    import numpy as np
+
+    rows, cols, nnz = mtx_stats(path)
+    rp = np.empty(rows + 1, np.int32)
+    col = np.empty(max(nnz, 1), np.int32)
+    val = np.empty(max(nnz, 1), np.float64)
+    r, c, n = _u64(), _u64(), _u64()
+    _check(lib().rl_mtx_read_csr(os.fsencode(path), rows + 1, nnz, rp.ctypes.data, col.ctypes.data,
+                                 val.ctypes.data, C.byref(r), C.byref(c), C.byref(n)))
+    return rp, col[:nnz], val[:nnz], cols
+
+
+def matrix_analysis(rows: int, cols: int, nnz: int, spec: HardwareSpec, precision: int = FP64) -> dict:
+    """reference stats_to_report (matrix_market.cpp:203-216)."""
+    out = _MatrixAnalysis()
+    s = spec._c()
+    _check(lib().rl_matrix_analysis_of(rows, cols, nnz, C.byref(s), precision, C.byref(out)))
+    return {f: getattr(out, f) for f, _ in _MatrixAnalysis._fields_}
 
 
 # ----------------------------------------------------------------------------

@@ -119,6 +119,19 @@ KernelCharacterization scale(ExecutionUnit unit, Precision p, double* a, const d
     return k;
 }
 
+KernelCharacterization gemv(ExecutionUnit unit, Precision p, std::uint64_t m, std::uint64_t n,
+                            const double* A, const double* x, double* y, Stream stream) {
+    KernelCharacterization k = gemv_model(m, n, p);
+    require_fp64(p);
+    require_ptr(A, "A");
+    require_ptr(x, "x");
+    require_ptr(y, "y");
+    cuda_check(rlb::launch_gemv(unit == ExecutionUnit::TensorCore, m, n, A, x, y,
+                                static_cast<cudaStream_t>(stream)),
+               "gemv");
+    return k;
+}
+
 void spmv_csr_rows(ExecutionUnit unit, Precision p, std::uint64_t r0, std::uint64_t r1,
                    const std::int32_t* rp, const std::int32_t* col, const double* val,
                    const double* x, std::int64_t col_base, double* y, Stream stream) {
@@ -475,6 +488,19 @@ void plan_execute_host(rl_spmv_plan_s* pl, const double* x, double* y) {
         ck(cudaEventRecord(pl->ev_x[i], pl->s_in), "event");
         mark(pl->s_in);
     }
+    // y: when the host buffer is pinned and mapped (cudaHostAlloc / registered,
+    // UVA), the kernels store y straight into it over PCIe -- those posted
+    // writes overlap the x upload in the other direction and no D2H pass is
+    // needed.  Otherwise y goes through the device buffer and a D2H copy per
+    // chunk on the third stream.
+    double* y_direct = nullptr;
+    if (rlb::tuning().spmv_plan_zero_copy) {
+        cudaPointerAttributes ay{};
+        if (cudaPointerGetAttributes(&ay, y) == cudaSuccess && ay.type == cudaMemoryTypeHost &&
+            ay.devicePointer != nullptr)
+            y_direct = static_cast<double*>(ay.devicePointer);
+        cudaGetLastError();
+    }
     size_t waited = 0;  // x pieces the compute stream already waits for
     for (size_t c = 0; c + 1 < pl->chunk_row.size(); ++c) {
         while (waited < npc && pl->xpiece[waited] < pl->chunk_xend[c]) {
@@ -483,13 +509,15 @@ void plan_execute_host(rl_spmv_plan_s* pl, const double* x, double* y) {
         }
         const uint64_t r0 = pl->chunk_row[c], r1 = pl->chunk_row[c + 1];
         mark(pl->s_cmp);
-        spmv_csr_rows(pl->unit, Precision::FP64, r0, r1, pl->rp, pl->col, pl->val, pl->x, 0, pl->y,
-                      pl->s_cmp);
-        ck(cudaEventRecord(pl->ev_y[c], pl->s_cmp), "event");
+        spmv_csr_rows(pl->unit, Precision::FP64, r0, r1, pl->rp, pl->col, pl->val, pl->x, 0,
+                      y_direct ? y_direct : pl->y, pl->s_cmp);
         mark(pl->s_cmp);
-        ck(cudaStreamWaitEvent(pl->s_out, pl->ev_y[c], 0), "wait");
-        ck(cudaMemcpyAsync(y + r0, pl->y + r0, (r1 - r0) * 8, cudaMemcpyDeviceToHost, pl->s_out), "D2H y");
-        mark(pl->s_out);
+        if (!y_direct) {
+            ck(cudaEventRecord(pl->ev_y[c], pl->s_cmp), "event");
+            ck(cudaStreamWaitEvent(pl->s_out, pl->ev_y[c], 0), "wait");
+            ck(cudaMemcpyAsync(y + r0, pl->y + r0, (r1 - r0) * 8, cudaMemcpyDeviceToHost, pl->s_out), "D2H y");
+            mark(pl->s_out);
+        }
     }
     ck(cudaStreamSynchronize(pl->s_out), "sync");
     ck(cudaStreamSynchronize(pl->s_cmp), "sync");
@@ -621,6 +649,10 @@ int rl_scale(rl_unit u, rl_precision p, double* a, const double* b, double q, ui
              rl_stream s, rl_kchar* out) {
     return guarded([&] { put(out, rooflens::b200::scale(unit_of(u), prec_of(p), a, b, q, n, s)); });
 }
+int rl_gemv(rl_unit u, rl_precision p, uint64_t m, uint64_t n, const double* A, const double* x, double* y,
+            rl_stream s, rl_kchar* out) {
+    return guarded([&] { put(out, rooflens::b200::gemv(unit_of(u), prec_of(p), m, n, A, x, y, s)); });
+}
 int rl_spmv_csr(rl_unit u, rl_precision p, uint64_t m, uint64_t n, uint64_t nnz, const int32_t* rp,
                 const int32_t* col, const double* val, const double* x, double* y, rl_stream s,
                 rl_kchar* out) {
@@ -747,6 +779,55 @@ int rl_stencil_init(double* u, const uint64_t* dims, int dim, uint64_t o0, uint6
     });
 }
 
+int rl_mtx_stats(const char* path, uint64_t* rows, uint64_t* cols, uint64_t* nnz) {
+    return guarded([&] {
+        require_ptr(path, "path");
+        const SparseMatrixStats s = mtx_stats(path);
+        if (rows) *rows = s.rows;
+        if (cols) *cols = s.cols;
+        if (nnz) *nnz = s.nnz;
+    });
+}
+int rl_mtx_read_csr(const char* path, uint64_t row_cap, uint64_t nnz_cap, int32_t* rp, int32_t* col,
+                    double* val, uint64_t* rows, uint64_t* cols, uint64_t* nnz) {
+    return guarded([&] {
+        require_ptr(path, "path");
+        std::vector<int32_t> vrp, vcol;
+        std::vector<double> vval;
+        const SparseMatrixStats s = mtx_read_csr(path, vrp, vcol, vval);
+        if (row_cap < s.rows + 1 || nnz_cap < s.nnz)
+            throw Error(ErrorKind::InvalidCount, "CSR buffers too small: need " + std::to_string(s.rows + 1) +
+                                                     " row pointers and " + std::to_string(s.nnz) + " entries");
+        require_ptr(rp, "row_ptr");
+        require_ptr(col, "col");
+        require_ptr(val, "val");
+        std::memcpy(rp, vrp.data(), vrp.size() * 4);
+        std::memcpy(col, vcol.data(), vcol.size() * 4);
+        std::memcpy(val, vval.data(), vval.size() * 8);
+        if (rows) *rows = s.rows;
+        if (cols) *cols = s.cols;
+        if (nnz) *nnz = s.nnz;
+    });
+}
+int rl_matrix_analysis_of(uint64_t rows, uint64_t cols, uint64_t nnz, const rl_hw_spec* spec,
+                          rl_precision p, rl_matrix_analysis* out) {
+    return guarded([&] {
+        require_ptr(out, "out");
+        const HardwareSpec h = spec_of(spec);
+        const Precision pr = prec_of(p);
+        const KernelCharacterization k = spmv_csr_model({rows, cols, nnz}, kDefaultIndexBytes, pr);
+        const double I = k.intensity();
+        const double B = machine_balance(h, ExecutionUnit::CudaCore, pr);
+        std::memset(out, 0, sizeof *out);
+        out->work_flops = k.work_flops;
+        out->traffic_bytes = k.traffic_bytes;
+        out->boundedness = static_cast<int>(classify(I, B));
+        out->kernel_ceiling = kernel_speedup_ceiling(tensor_alpha(h, pr), B, I, &out->kernel_ceiling_warnings);
+        out->workload_ceiling = workload_ceiling(I, B);
+        out->csr_bytes = k.traffic_bytes;
+        out->fits_in_l2 = static_cast<double>(k.traffic_bytes) <= h.l2_cache_bytes;
+    });
+}
 int rl_load_spec(const char* text, rl_hw_spec* out) {
     return guarded([&] {
         require_ptr(text, "json_text");
@@ -810,6 +891,7 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         else if (k == "spmv_sched") slot = &t.spmv_sched;
         else if (k == "spmv_threads") slot = &t.spmv_threads;
         else if (k == "spmv_plan_chunks") slot = &t.spmv_plan_chunks;
+        else if (k == "spmv_plan_zero_copy") slot = &t.spmv_plan_zero_copy;
         else if (k == "spmv_tc_blocks_per_sm") slot = &t.spmv_tc_blocks_per_sm;
         else if (k == "spmv_tc_threads") slot = &t.spmv_tc_threads;
         else if (k == "spmv_tc_rows") slot = &t.spmv_tc_rows;

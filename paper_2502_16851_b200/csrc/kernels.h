@@ -18,7 +18,8 @@ struct Tuning {
     int spmv_tc_threads = 1024;
     int spmv_l1_carveout = -1;     // shared-memory carveout % for the CC kernel (-1 = driver default)
     int spmv_tc_rows = 1;          // 8-row blocks per warp iteration (1, 2)
-    int spmv_plan_chunks = 4;      // pipelined row/x chunks of rl_spmv_plan_execute_host
+    int spmv_plan_chunks = 8;      // pipelined row/x chunks of rl_spmv_plan_execute_host
+    int spmv_plan_zero_copy = 0;   // 1: store y straight into pinned host memory (measured slower)
     int spmv_sched = 1;            // 0 grid-stride, 1 contiguous row range per CTA
     int spmv_xhint = 0;            // x gathers: 0 L1 default, 1 L1::evict_last, 2 L1::no_allocate
     int stencil2d_rows = 256;      // rows marched per warp (2D CC)
@@ -68,6 +69,10 @@ cudaError_t launch_stencil_tma(int unit, const StencilDesc& d, uint64_t o0, uint
 // Two fused timesteps of 2d5pt (temporal blocking, CUDA core, TMA-eligible grids).
 cudaError_t launch_stencil_tma_t2(const StencilDesc& d, uint64_t o0, uint64_t o1, const double* u,
                                   double* v, cudaStream_t s);
+
+// Dense GEMV y = A*x, row-major A (m x n).
+cudaError_t launch_gemv(int unit, uint64_t m, uint64_t n, const double* A, const double* x, double* y,
+                        cudaStream_t s);
 
 // Launch accounting (rl_kernel_launches): every <<<>>> site reports itself.
 void note_launch(uint64_t n = 1);

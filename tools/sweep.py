@@ -26,7 +26,7 @@ def timeit(fn, reps=20, warm=3):
 
 def sweep(name, fn, nbytes, grid):
     keys = list(grid)
-    for vals in itertools.product(*[grid[k] for k in keys]):
+    for vals in itertools.product(*[grid[k] for k in keys]) if keys else [()]:
         for k, v in zip(keys, vals):
             P.tuning_set(k, v)
         ms = timeit(fn)
@@ -62,6 +62,18 @@ def main(which):
                "spmv_sched": [0, 1]})
 
 
+def gemv():
+    m, n = 16384, 65536
+    A = torch.empty((m, n), dtype=torch.float64, device="cuda")
+    P.fill_uniform(A.view(-1), 1, 6, 0, 1)
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    P.fill_uniform(x, 1, 4, 0, 1)
+    y = torch.empty(m, dtype=torch.float64, device="cuda")
+    nbytes = P.gemv_model(m, n).traffic_bytes
+    for unit in (0, 1):
+        sweep(f"gemv_{'cc' if unit == 0 else 'tc'}", lambda: P.gemv(A, x, y, unit=unit), nbytes, {})
+
+
 def temporal():
     import math
     u = torch.empty((16384, 16384), dtype=torch.float64, device="cuda")
@@ -95,5 +107,7 @@ if __name__ == "__main__":
             stencils()
         elif w == "temporal":
             temporal()
+        elif w == "gemv":
+            gemv()
         else:
             main(w)
