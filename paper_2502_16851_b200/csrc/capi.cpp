@@ -887,6 +887,8 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         const std::string k(key);
         if (k == "scale_blocks_per_sm") slot = &t.scale_blocks_per_sm;
         else if (k == "spmv_rows") slot = &t.spmv_rows;
+        else if (k == "gemv_rows") slot = &t.gemv_rows;
+        else if (k == "gemv_unroll") slot = &t.gemv_unroll;
         else if (k == "spmv_blocks_per_sm") slot = &t.spmv_blocks_per_sm;
         else if (k == "spmv_sched") slot = &t.spmv_sched;
         else if (k == "spmv_threads") slot = &t.spmv_threads;

@@ -18,7 +18,7 @@
 namespace rlb {
 namespace {
 
-template <int R>
+template <int R, int UK>
 __global__ void __launch_bounds__(256) gemv_cc(uint64_t m, uint64_t n, const double* __restrict__ A,
                                                const double* __restrict__ x, double* __restrict__ y) {
     const int lane = threadIdx.x & 31;
@@ -31,18 +31,27 @@ __global__ void __launch_bounds__(256) gemv_cc(uint64_t m, uint64_t n, const dou
 #pragma unroll
         for (int q = 0; q < R; ++q) acc[q] = 0.0;
         if (vec) {
-            for (uint64_t k = 4 * (uint64_t)lane; k < n; k += 128) {
-                const d4 xv = ld4_cached(x + k);
+            // UK column steps of 128 per iteration: all R*UK loads issued first
+            for (uint64_t kb = 4 * (uint64_t)lane; kb < n; kb += 128 * UK) {
+                d4 xv[UK], a[UK][R];
 #pragma unroll
-                for (int q = 0; q < R; ++q) {
-                    if (r0 + q < m) {
-                        const d4 a = ld4_stream(A + (r0 + q) * n + k, pol);
-                        acc[q] = fma(a.x, xv.x, acc[q]);
-                        acc[q] = fma(a.y, xv.y, acc[q]);
-                        acc[q] = fma(a.z, xv.z, acc[q]);
-                        acc[q] = fma(a.w, xv.w, acc[q]);
-                    }
+                for (int u = 0; u < UK; ++u) {
+                    const uint64_t k = kb + 128 * u;
+                    const bool kin = k < n;
+                    xv[u] = kin ? ld4_cached(x + k) : d4{0, 0, 0, 0};
+#pragma unroll
+                    for (int q = 0; q < R; ++q)
+                        a[u][q] = (kin && r0 + q < m) ? ld4_stream(A + (r0 + q) * n + k, pol) : d4{0, 0, 0, 0};
                 }
+#pragma unroll
+                for (int u = 0; u < UK; ++u)
+#pragma unroll
+                    for (int q = 0; q < R; ++q) {
+                        acc[q] = fma(a[u][q].x, xv[u].x, acc[q]);
+                        acc[q] = fma(a[u][q].y, xv[u].y, acc[q]);
+                        acc[q] = fma(a[u][q].z, xv[u].z, acc[q]);
+                        acc[q] = fma(a[u][q].w, xv[u].w, acc[q]);
+                    }
             }
         } else {
             for (uint64_t k = lane; k < n; k += 32) {
@@ -122,10 +131,14 @@ cudaError_t launch_gemv(int unit, uint64_t m, uint64_t n, const double* A, const
         if (blocks > max_blocks) blocks = max_blocks;
         gemv_tc<<<(unsigned)blocks, 256, 0, s>>>(m, n, A, x, y);
     } else {
-        constexpr int R = 8;
+        const int R = tuning().gemv_rows, UK = tuning().gemv_unroll;
         uint64_t blocks = (m + 8 * R - 1) / (8 * R);
         if (blocks > max_blocks) blocks = max_blocks;
-        gemv_cc<R><<<(unsigned)blocks, 256, 0, s>>>(m, n, A, x, y);
+#define RLB_GEMV(RR, UU) gemv_cc<RR, UU><<<(unsigned)blocks, 256, 0, s>>>(m, n, A, x, y)
+        if (R == 2) { if (UK == 2) RLB_GEMV(2, 2); else if (UK == 4) RLB_GEMV(2, 4); else RLB_GEMV(2, 1); }
+        else if (R == 4) { if (UK == 2) RLB_GEMV(4, 2); else if (UK == 4) RLB_GEMV(4, 4); else RLB_GEMV(4, 1); }
+        else { if (UK == 2) RLB_GEMV(8, 2); else RLB_GEMV(8, 1); }
+#undef RLB_GEMV
     }
     note_launch();
     return cudaGetLastError();

@@ -11,6 +11,8 @@ namespace rlb {
 struct Tuning {
     int scale_blocks_per_sm = 32;  // STREAM grid = 148 * this (swept: tools/sweep.py)
     int scale_unroll = 8;          // 1, 2, 4, 8
+    int gemv_rows = 4;             // rows per warp, CUDA-core GEMV (2, 4, 8)
+    int gemv_unroll = 2;           // 128-column steps in flight per iteration (1, 2, 4)
     int spmv_rows = 2;             // rows per lane group per iteration (1, 2, 4)
     int spmv_blocks_per_sm = 1;    // CUDA-core SpMV grid = 148 * this
     int spmv_threads = 1024;       // CTA size of the CUDA-core kernel (multiple of 32, <= 1024)
