@@ -149,6 +149,7 @@ _SIGNATURES = {
     "rl_spmv_plan_execute_host": (_int, [_ptr, _ptr, _ptr, _KP]),
     "rl_spmv_plan_execute": (_int, [_ptr, _ptr, _ptr, _ptr, _KP]),
     "rl_spmv_plan_destroy": (_int, [_ptr]),
+    "rl_spmv_plan_info": (_int, [_ptr, C.POINTER(_int), C.POINTER(_u64)]),
     "rl_fill_uniform": (_int, [_ptr, _u64, _u64, _u64, _u64, _int, _ptr]),
     "rl_gen_band_csr": (_int, [_u64, _u64, _u64, C.c_uint32, _u64, _u64, _ptr, _ptr, _ptr, _ptr]),
     "rl_stencil_init": (_int, [_ptr, C.POINTER(_u64), _int, _u64, _u64, _int, _u64, _ptr]),
@@ -469,6 +470,12 @@ class SpmvPlan:
         _check(lib().rl_spmv_plan_execute(self._h, _dev_ptr(x, "f64", "x"), _dev_ptr(y, "f64", "y"),
                                           _stream(stream), C.byref(k)))
         return _kc(k)
+
+    def info(self):
+        """(tiled, layout_bytes): layout used and the bytes one execute streams for A."""
+        t, b = _int(), _u64()
+        _check(lib().rl_spmv_plan_info(self._h, C.byref(t), C.byref(b)))
+        return bool(t.value), int(b.value)
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:

@@ -397,6 +397,13 @@ struct rl_spmv_plan_s {
     uint64_t m = 0, n = 0, nnz = 0;
     int32_t *rp = nullptr, *col = nullptr;
     double *val = nullptr, *x = nullptr, *y = nullptr;
+    // column-tiled layout (CUDA-core plans): segments, tile table, block table
+    bool tiled = false;
+    uint8_t* segs = nullptr;
+    rlb::SpmvTile* tiles = nullptr;
+    int* blk_tiles = nullptr;
+    uint64_t nblocks = 0;
+    uint64_t layout_bytes = 0;
     std::vector<uint64_t> chunk_row;   // chunk c = rows [chunk_row[c], chunk_row[c+1])
     std::vector<uint64_t> chunk_xend;  // x prefix [0, chunk_xend[c]) chunk c reads
     std::vector<uint64_t> xpiece;      // x upload pieces: [xpiece[i], xpiece[i+1])
@@ -409,6 +416,9 @@ struct rl_spmv_plan_s {
         if (val) cudaFree(val);
         if (x) cudaFree(x);
         if (y) cudaFree(y);
+        if (segs) cudaFree(segs);
+        if (tiles) cudaFree(tiles);
+        if (blk_tiles) cudaFree(blk_tiles);
         for (auto e : ev_x) cudaEventDestroy(e);
         for (auto e : ev_y) cudaEventDestroy(e);
         if (s_in) cudaStreamDestroy(s_in);
@@ -435,16 +445,38 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
     pl->n = n;
     pl->nnz = nnz;
     pl->kc = k;
-    ck(cudaMalloc(&pl->rp, (m + 1) * 4), "plan alloc");
-    ck(cudaMalloc(&pl->col, nnz * 4), "plan alloc");
-    ck(cudaMalloc(&pl->val, nnz * 8), "plan alloc");
-    ck(cudaMalloc(&pl->x, n * 8), "plan alloc");
+    ck(cudaMalloc(&pl->x, std::max<uint64_t>(n, 2) * 8), "plan alloc");
     ck(cudaMalloc(&pl->y, m * 8), "plan alloc");
-    ck(cudaMemcpy(pl->rp, rp, (m + 1) * 4, cudaMemcpyHostToDevice), "plan upload");
-    ck(cudaMemcpy(pl->col, col, nnz * 4, cudaMemcpyHostToDevice), "plan upload");
-    ck(cudaMemcpy(pl->val, val, nnz * 8, cudaMemcpyHostToDevice), "plan upload");
-    const uint64_t nch = std::min<uint64_t>((uint64_t)rlb::tuning().spmv_plan_chunks, m);
-    for (uint64_t c = 0; c <= nch; ++c) pl->chunk_row.push_back(m * c / nch);
+    pl->tiled = unit == ExecutionUnit::CudaCore && rlb::tuning().spmv_plan_tiled && n % 2 == 0;
+    if (pl->tiled) {
+        std::vector<uint8_t> segs;
+        std::vector<rlb::SpmvTile> tiles;
+        std::vector<int> blk;
+        rlb::spmv_tiled_build(m, n, rp, col, val, segs, tiles, blk);
+        pl->nblocks = blk.size() - 1;
+        pl->layout_bytes = segs.size();
+        ck(cudaMalloc(&pl->segs, std::max<size_t>(segs.size(), 16)), "plan alloc");
+        ck(cudaMalloc(&pl->tiles, std::max<size_t>(tiles.size(), 1) * sizeof(rlb::SpmvTile)), "plan alloc");
+        ck(cudaMalloc(&pl->blk_tiles, blk.size() * sizeof(int)), "plan alloc");
+        if (!segs.empty()) ck(cudaMemcpy(pl->segs, segs.data(), segs.size(), cudaMemcpyHostToDevice), "plan upload");
+        if (!tiles.empty())
+            ck(cudaMemcpy(pl->tiles, tiles.data(), tiles.size() * sizeof(rlb::SpmvTile), cudaMemcpyHostToDevice),
+               "plan upload");
+        ck(cudaMemcpy(pl->blk_tiles, blk.data(), blk.size() * sizeof(int), cudaMemcpyHostToDevice), "plan upload");
+    } else {
+        ck(cudaMalloc(&pl->rp, (m + 1) * 4), "plan alloc");
+        ck(cudaMalloc(&pl->col, std::max<uint64_t>(nnz, 1) * 4), "plan alloc");
+        ck(cudaMalloc(&pl->val, std::max<uint64_t>(nnz, 1) * 8), "plan alloc");
+        ck(cudaMemcpy(pl->rp, rp, (m + 1) * 4, cudaMemcpyHostToDevice), "plan upload");
+        ck(cudaMemcpy(pl->col, col, nnz * 4, cudaMemcpyHostToDevice), "plan upload");
+        ck(cudaMemcpy(pl->val, val, nnz * 8, cudaMemcpyHostToDevice), "plan upload");
+        pl->layout_bytes = (m + 1) * 4 + nnz * 12;
+    }
+    // pipeline chunks: whole tiled blocks when tiled
+    const uint64_t unitrows = pl->tiled ? (uint64_t)rlb::kSpmvTiledRows : 1;
+    const uint64_t units = (m + unitrows - 1) / unitrows;
+    const uint64_t nch = std::min<uint64_t>((uint64_t)rlb::tuning().spmv_plan_chunks, units);
+    for (uint64_t c = 0; c <= nch; ++c) pl->chunk_row.push_back(std::min<uint64_t>(m, units * c / nch * unitrows));
     for (uint64_t c = 0; c < nch; ++c) {
         uint64_t mx = 0;
         for (int64_t j = rp[pl->chunk_row[c]]; j < rp[pl->chunk_row[c + 1]]; ++j) {
@@ -465,6 +497,17 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
     for (auto& e : pl->ev_x) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     for (auto& e : pl->ev_y) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     return pl.release();
+}
+
+// Rows [r0, r1) of y = A x on the plan's layout (r0/r1 block-aligned when tiled).
+void plan_rows(rl_spmv_plan_s* pl, uint64_t r0, uint64_t r1, const double* x, double* y, cudaStream_t s) {
+    if (pl->tiled) {
+        const uint64_t b0 = r0 / rlb::kSpmvTiledRows;
+        const uint64_t b1 = (r1 + rlb::kSpmvTiledRows - 1) / rlb::kSpmvTiledRows;
+        ck(rlb::launch_spmv_tiled(pl->m, pl->segs, pl->tiles, pl->blk_tiles, b0, b1, x, y, s), "spmv (tiled plan)");
+    } else {
+        spmv_csr_rows(pl->unit, Precision::FP64, r0, r1, pl->rp, pl->col, pl->val, x, 0, y, s);
+    }
 }
 
 void plan_execute_host(rl_spmv_plan_s* pl, const double* x, double* y) {
@@ -509,8 +552,7 @@ void plan_execute_host(rl_spmv_plan_s* pl, const double* x, double* y) {
         }
         const uint64_t r0 = pl->chunk_row[c], r1 = pl->chunk_row[c + 1];
         mark(pl->s_cmp);
-        spmv_csr_rows(pl->unit, Precision::FP64, r0, r1, pl->rp, pl->col, pl->val, pl->x, 0,
-                      y_direct ? y_direct : pl->y, pl->s_cmp);
+        plan_rows(pl, r0, r1, pl->x, y_direct ? y_direct : pl->y, pl->s_cmp);
         mark(pl->s_cmp);
         if (!y_direct) {
             ck(cudaEventRecord(pl->ev_y[c], pl->s_cmp), "event");
@@ -729,9 +771,17 @@ int rl_spmv_plan_execute(rl_spmv_plan pl, const double* x, double* y, rl_stream 
         require_ptr(pl, "plan");
         require_ptr(x, "x");
         require_ptr(y, "y");
-        spmv_csr_rows(pl->unit, Precision::FP64, 0, pl->m, pl->rp, pl->col, pl->val, x, 0, y,
-                      static_cast<cudaStream_t>(s));
+        if (pl->tiled && (reinterpret_cast<uintptr_t>(x) & 15))
+            throw Error(ErrorKind::ValidationError, "tiled plan needs a 16-byte aligned x");
+        plan_rows(pl, 0, pl->m, x, y, static_cast<cudaStream_t>(s));
         put(out, pl->kc);
+    });
+}
+int rl_spmv_plan_info(rl_spmv_plan pl, int* tiled, uint64_t* layout_bytes) {
+    return guarded([&] {
+        require_ptr(pl, "plan");
+        if (tiled) *tiled = pl->tiled ? 1 : 0;
+        if (layout_bytes) *layout_bytes = pl->layout_bytes;
     });
 }
 int rl_spmv_plan_destroy(rl_spmv_plan pl) {
@@ -894,6 +944,7 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         else if (k == "spmv_threads") slot = &t.spmv_threads;
         else if (k == "spmv_plan_chunks") slot = &t.spmv_plan_chunks;
         else if (k == "spmv_plan_zero_copy") slot = &t.spmv_plan_zero_copy;
+        else if (k == "spmv_plan_tiled") slot = &t.spmv_plan_tiled;
         else if (k == "spmv_tc_blocks_per_sm") slot = &t.spmv_tc_blocks_per_sm;
         else if (k == "spmv_tc_threads") slot = &t.spmv_tc_threads;
         else if (k == "spmv_tc_rows") slot = &t.spmv_tc_rows;

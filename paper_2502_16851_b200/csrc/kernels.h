@@ -5,6 +5,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <vector>
+
 namespace rlb {
 
 // Kernel-variant knobs, settable through rl_tuning_set() for sweeps.
@@ -21,6 +23,7 @@ struct Tuning {
     int spmv_l1_carveout = -1;     // shared-memory carveout % for the CC kernel (-1 = driver default)
     int spmv_tc_rows = 1;          // 8-row blocks per warp iteration (1, 2)
     int spmv_plan_chunks = 8;      // pipelined row/x chunks of rl_spmv_plan_execute_host
+    int spmv_plan_tiled = 0;       // 1: CUDA-core plans use the column-tiled layout (spmv_tiled.cu; 0.31 ms vs CSR 0.28 ms on the BASELINE matrix)
     int spmv_plan_zero_copy = 0;   // 1: store y straight into pinned host memory (measured slower)
     int spmv_sched = 1;            // 0 grid-stride, 1 contiguous row range per CTA
     int spmv_xhint = 0;            // x gathers: 0 L1 default, 1 L1::evict_last, 2 L1::no_allocate
@@ -75,6 +78,20 @@ cudaError_t launch_stencil_tma_t2(const StencilDesc& d, uint64_t o0, uint64_t o1
 // Dense GEMV y = A*x, row-major A (m x n).
 cudaError_t launch_gemv(int unit, uint64_t m, uint64_t n, const double* A, const double* x, double* y,
                         cudaStream_t s);
+
+// Column-tiled SpMV (rl_spmv_plan's layout for the CUDA core; spmv_tiled.cu).
+struct SpmvTile {
+    uint64_t seg_offset;  // byte offset of the tile's segment
+    int32_t col_base;     // first column (even)
+    int32_t width;        // columns in the x slice (even)
+    int32_t entries;
+    int32_t seg_bytes;    // multiple of 16
+};
+constexpr int kSpmvTiledRows = 8192;  // rows per tiled block
+void spmv_tiled_build(uint64_t m, uint64_t n, const int32_t* rp, const int32_t* col, const double* val,
+                      std::vector<uint8_t>& segs, std::vector<SpmvTile>& tiles, std::vector<int>& blk_tiles);
+cudaError_t launch_spmv_tiled(uint64_t m, const uint8_t* segs, const SpmvTile* tiles, const int* blk_tiles,
+                              uint64_t b0, uint64_t b1, const double* x, double* y, cudaStream_t s);
 
 // Launch accounting (rl_kernel_launches): every <<<>>> site reports itself.
 void note_launch(uint64_t n = 1);

@@ -67,3 +67,67 @@ def test_stencil_host(cuda, unit, preset, shape, steps):
     out = u if steps % 2 == 0 else v
     assert O.rel_err(out, O.stencil(preset, u0, steps)) <= 1e-12
     assert kc.traffic_bytes == 16 * int(np.prod([s - 2 for s in shape])) * steps
+
+
+@pytest.fixture
+def tiled_plans():
+    """The column-tiled plan layout is opt-in (tuning key spmv_plan_tiled)."""
+    P.tuning_set("spmv_plan_tiled", 1)
+    yield
+    P.tuning_set("spmv_plan_tiled", 0)
+
+
+def _plan_check(torch, rp, col, val, ncols, unit, expect_tiled):
+    x = np.random.default_rng(5).uniform(-1, 1, ncols)
+    ref = O.spmv_csr(rp, col, val, x)
+    plan = P.SpmvPlan(rp, col, val, ncols, unit=unit)
+    assert plan.info()[0] == expect_tiled
+    y = np.full(rp.size - 1, np.nan)
+    plan.execute_host(x, y)
+    assert O.rel_err(y, ref) <= 1e-12
+    dx = torch.from_numpy(x).cuda()
+    dy = torch.full((rp.size - 1,), float("nan"), dtype=torch.float64, device="cuda")
+    plan.execute(dx, dy)
+    torch.cuda.synchronize()
+    assert O.rel_err(dy.cpu().numpy(), ref) <= 1e-12
+    # deterministic: a second execution is bit-identical
+    dy2 = torch.full_like(dy, float("nan"))
+    plan.execute(dx, dy2)
+    torch.cuda.synchronize()
+    assert torch.equal(dy, dy2)
+    plan.close()
+
+
+def test_plan_default_layout_is_csr(cuda):
+    import torch
+
+    rp, col, val = O.gen_band_csr(10000, 0, 10000, 8, 500, 3)
+    _plan_check(torch, rp, col, val, 10000, P.CUDA_CORE, False)
+
+
+@pytest.mark.parametrize("m,n,k,hb", [(8192 * 3 + 17, 8192 * 3 + 18, 16, 65536), (100000, 100000, 16, 65536),
+                                      (50000, 50000, 7, 300), (20000, 20000, 40, 20000)])
+def test_tiled_plan_banded(cuda, tiled_plans, m, n, k, hb):
+    import torch
+
+    rp, col, val = O.gen_band_csr(m, 0, n, k, hb, 31)
+    _plan_check(torch, rp, col, val, n, P.CUDA_CORE, n % 2 == 0)
+
+
+def test_tiled_plan_ragged_dense_and_empty(cuda, tiled_plans):
+    """Empty rows, rows denser than a tile segment (forces tile splitting),
+    a rectangular matrix and an odd column count (CSR fallback)."""
+    import torch
+
+    rng = np.random.default_rng(11)
+    m, n = 20000, 30000
+    lens = rng.integers(0, 30, m)
+    lens[::5] = 0
+    lens[7] = 9000        # one very dense row
+    lens[8000:8010] = 3000
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    col = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(np.int32)
+    val = rng.uniform(-1, 1, rp[-1])
+    _plan_check(torch, rp, col, val, n, P.CUDA_CORE, True)
+    _plan_check(torch, rp, col, val, n + 1, P.CUDA_CORE, False)   # odd n -> CSR kernel
+    _plan_check(torch, rp, col, val, n, P.TENSOR_CORE, False)     # TC plans keep CSR
