@@ -405,6 +405,43 @@ def gemv_rows(torch, P, hbm, reps=10):
     return res
 
 
+def stencil_preset_rows(torch, P, hbm, steps=10):
+    """the reference's other presets (kernels.cpp:54-58)
+    2d9pt / 2d13pt / 2d49pt on the 16384^2 grid, radius-R Dirichlet ring,
+    stencil_model bytes (16 B per updated point per step) and flops
+    (2 |S| per point).  2d49pt sits at the FP64 ridge."""
+    import math
+    u = torch.empty((16384, 16384), dtype=torch.float64, device="cuda")
+    v = torch.empty_like(u)
+    out = {}
+    for preset in ("2d9pt", "2d13pt", "2d49pt"):
+        npts, r = P.stencil_preset(preset)[1], P.stencil_preset(preset)[2]
+        P.stencil_init(u, r, SEED)
+        v.copy_(u)
+        pts = math.prod(s - 2 * r for s in u.shape)
+        res = {}
+        for uname, unit in (("cc", P.CUDA_CORE), ("tc", P.TENSOR_CORE)):
+            P.stencil(preset, u, v, 2, unit=unit)
+            torch.cuda.synchronize()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            kc = P.stencil(preset, u, v, steps, unit=unit)
+            e.record()
+            torch.cuda.synchronize()
+            ms = s.elapsed_time(e) / steps
+            gbs = kc.traffic_bytes / steps / (ms * 1e-3) / 1e9
+            res[uname] = {"gbs": round(gbs, 1), "frac_of_measured_peak": round(gbs / hbm, 4),
+                          "tflops": round(kc.work_flops / steps / (ms * 1e-3) / 1e12, 2),
+                          "ms_per_step": round(ms, 4)}
+        res["tc_over_cc"] = round(res["tc"]["gbs"] / res["cc"]["gbs"], 4)
+        res["intensity"] = round(P.stencil_model(preset).intensity, 5)
+        res["config"] = f"16384^2, {steps} steps, radius {r}"
+        out[preset] = res
+    del u, v
+    torch.cuda.empty_cache()
+    return out
+
+
 def add_bounds(P, rows, peaks, hbm):
     """TC/CC speedup ceiling per kernel from the measured B200 figures
     (kernel_speedup_ceiling, reference bounds.cpp:72-85)."""
@@ -641,12 +678,19 @@ def main():
             table = per_kernel_table(torch, P, D, hbm)
             line["temporal_blocking"] = temporal_blocking(torch, P, hbm,
                                                           table["2d5pt"]["cc"]["ms_per_unit"])
-            line["next_rows"] = {"gemv": gemv_rows(torch, P, hbm)}
+            line["next_rows"] = {"gemv": gemv_rows(torch, P, hbm), **stencil_preset_rows(torch, P, hbm)}
         # FP64 peaks last: the DFMA/DMMA chains run at the power cap and would
         # throttle the memory-bound kernels measured after them.
         peaks = fp64_peaks(torch, P)
         bounds = add_bounds(P, table, peaks, hbm)
         add_bounds(P, line["next_rows"], peaks, hbm)
+        balance = peaks["cuda_core"] * 1e12 / (hbm * 1e9)
+        for res in line["next_rows"].values():
+            # which roof binds the CUDA-core form: HBM below the ridge, the DFMA pipe above
+            res["roof"] = "fp64" if res["intensity"] > balance else "hbm"
+            if "tflops" in res.get("cc", {}):
+                res["cc"]["frac_of_fp64_peak"] = round(res["cc"]["tflops"] / peaks["cuda_core"], 4)
+                res["tc"]["frac_of_fp64_peak"] = round(res["tc"]["tflops"] / peaks["tensor_core"], 4)
         line["per_kernel"] = table
         line["fp64_peaks_tflops"] = peaks
         line["bounds"] = bounds

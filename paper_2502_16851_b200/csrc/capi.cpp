@@ -96,9 +96,14 @@ void sweep(ExecutionUnit unit, const rlb::StencilDesc& d, std::uint64_t o0, std:
     const std::uint64_t hi = std::min<std::uint64_t>(o1, outer - d.radius);
     if (lo >= hi) return;
     if (unit == ExecutionUnit::TensorCore && d.preset != rlb::kP2d5 && d.preset != rlb::kP3d7 &&
-        d.preset != rlb::kP3d27)
-        throw Error(ErrorKind::ValidationError,
-                    "no tensor-core formulation for this preset (2d5pt, 3d7pt, 3d27pt only)");
+        d.preset != rlb::kP3d27) {
+        if (!rlb::stencil_r_eligible(d, u, v))
+            throw Error(ErrorKind::ValidationError,
+                        "the tensor-core 2d9pt/2d13pt/2d49pt kernels need an even nx and 16-byte aligned "
+                        "u and v");
+        cuda_check(rlb::launch_stencil_r(1, d, lo, hi, u, v, s), "stencil (tensor core)");
+        return;
+    }
     if (unit == ExecutionUnit::TensorCore)
         cuda_check(rlb::launch_stencil_tc(d, lo, hi, u, v, s), "stencil (tensor core)");
     else
@@ -945,6 +950,8 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         else if (k == "spmv_plan_chunks") slot = &t.spmv_plan_chunks;
         else if (k == "spmv_plan_zero_copy") slot = &t.spmv_plan_zero_copy;
         else if (k == "spmv_plan_tiled") slot = &t.spmv_plan_tiled;
+        else if (k == "stencil_r_ctas_per_sm") slot = &t.stencil_r_ctas_per_sm;
+        else if (k == "stencil_r_cc_stages") slot = &t.stencil_r_cc_stages;
         else if (k == "spmv_tc_blocks_per_sm") slot = &t.spmv_tc_blocks_per_sm;
         else if (k == "spmv_tc_threads") slot = &t.spmv_tc_threads;
         else if (k == "spmv_tc_rows") slot = &t.spmv_tc_rows;

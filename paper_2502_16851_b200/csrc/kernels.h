@@ -39,6 +39,8 @@ struct Tuning {
     int stencil_tc3d_ctas_per_sm = 8;  // ... 3D tensor-core kernels (3-plane mode)
     int stencil_tc3d_mode = 2;         // 3D tensor core, one-plane partial-sum kernel for: bit0 3d7pt, bit1 3d27pt
     int stencil_tc1_ctas_per_sm = 8;   // ... partial-sum mode
+    int stencil_r_cc_stages = 0;       // ... CUDA-core ring depth: 3, 4, 0 = auto (3 for 2d49pt -> 3 CTAs/SM, else 4)
+    int stencil_r_ctas_per_sm = 32;    // 2d9pt/2d13pt/2d49pt TMA kernels: row segments so the grid is this deep
 };
 Tuning& tuning();
 
@@ -70,6 +72,15 @@ cudaError_t launch_stencil_tc(const StencilDesc& d, uint64_t o0, uint64_t o1, co
 bool stencil_tma_eligible(const StencilDesc& d, const double* u, const double* v);
 cudaError_t launch_stencil_tma(int unit, const StencilDesc& d, uint64_t o0, uint64_t o1,
                                const double* u, double* v, cudaStream_t s);
+
+// TMA 2D stencils of the other presets (2d9pt, 2d13pt, 2d49pt; stencil_r.cu).
+bool stencil_r_eligible(const StencilDesc& d, const double* u, const double* v);
+cudaError_t launch_stencil_r(int unit, const StencilDesc& d, uint64_t o0, uint64_t o1, const double* u,
+                             double* v, cudaStream_t s);
+// 2D FP64 tensor map (box_x x box_y, zero OOB fill) into a 64-byte-aligned
+// CUtensorMap; false when the driver entry point is missing.
+bool tma_encode_available();
+bool encode_map_2d(void* map, const double* base, uint64_t nx, uint64_t ny, uint32_t box_x, uint32_t box_y);
 
 // Two fused timesteps of 2d5pt (temporal blocking, CUDA core, TMA-eligible grids).
 cudaError_t launch_stencil_tma_t2(const StencilDesc& d, uint64_t o0, uint64_t o1, const double* u,

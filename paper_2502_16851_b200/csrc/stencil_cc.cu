@@ -396,6 +396,7 @@ cudaError_t launch_stencil_generic(const StencilDesc& d, uint64_t o0, uint64_t o
 cudaError_t launch_stencil_cc(const StencilDesc& d, uint64_t o0, uint64_t o1, const double* u,
                               double* v, cudaStream_t s) {
     if (stencil_tma_eligible(d, u, v)) return launch_stencil_tma(0, d, o0, o1, u, v, s);
+    if (tuning().stencil_tma && stencil_r_eligible(d, u, v)) return launch_stencil_r(0, d, o0, o1, u, v, s);
     const Tuning& t = tuning();
     const bool vec_ok = (d.nx % 4 == 0) && aligned32(u) && aligned32(v);
     if (d.preset == kP2d5 && vec_ok) {

@@ -883,6 +883,20 @@ int split_count(uint64_t tiles, uint64_t extent, int min_chunk, int per_sm) {
 
 }  // namespace
 
+bool tma_encode_available() { return encode_fn() != nullptr; }
+
+bool encode_map_2d(void* map, const double* base, uint64_t nx, uint64_t ny, uint32_t box_x, uint32_t box_y) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t gdim[2] = {nx, ny};
+    cuuint64_t gstride[1] = {nx * 8};
+    cuuint32_t box[2] = {box_x, box_y};
+    cuuint32_t estride[2] = {1, 1};
+    return fn(static_cast<CUtensorMap*>(map), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), gdim,
+              gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 cudaError_t launch_stencil_tma_t2(const StencilDesc& d, uint64_t o0, uint64_t o1, const double* u,
                                   double* v, cudaStream_t s) {
     auto fn = encode_fn();

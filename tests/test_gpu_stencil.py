@@ -101,8 +101,10 @@ def test_custom_weights(cuda, unit, preset):
     assert O.rel_err(out, O.stencil(preset, u0, 3, w)) <= TOL
 
 
-@pytest.mark.parametrize("preset,shape", [("2d9pt", (40, 77)), ("2d13pt", (41, 70)), ("2d49pt", (33, 45))])
-def test_other_presets_cuda_core(cuda, preset, shape):
+@pytest.mark.parametrize("preset,shape", [("2d9pt", (40, 77)), ("2d13pt", (41, 71)), ("2d49pt", (33, 45))])
+def test_other_presets_odd_nx(cuda, preset, shape):
+    """Odd nx: the CUDA core runs the generic kernel; the tensor-core
+    kernels need 16-byte rows and refuse."""
     import torch
 
     r = P.stencil_preset(preset)[2]
@@ -112,6 +114,51 @@ def test_other_presets_cuda_core(cuda, preset, shape):
     with pytest.raises(P.RooflensError) as e:
         _run(torch, preset, u0, 1, P.TENSOR_CORE)
     assert e.value.kind == "ValidationError"
+
+
+SHAPES_R = [(7, 8), (9, 10), (40, 70), (33, 64), (130, 200), (301, 258), (520, 1030)]
+
+
+@pytest.mark.parametrize("unit", UNITS)
+@pytest.mark.parametrize("preset", ["2d9pt", "2d13pt", "2d49pt"])
+@pytest.mark.parametrize("shape", SHAPES_R)
+def test_other_presets_tma(cuda, unit, preset, shape):
+    """2d9pt / 2d13pt / 2d49pt through the TMA kernels (even nx), both units:
+    parity with the oracle and an untouched radius-R Dirichlet ring."""
+    import torch
+
+    r = P.stencil_preset(preset)[2]
+    u0 = O.stencil_init(shape, r, 5)
+    steps = 3
+    out, kc = _run(torch, preset, u0, steps, unit)
+    ref = O.stencil(preset, u0, steps)
+    assert O.rel_err(out, ref) <= TOL
+    ring = _ring_mask(shape, r)
+    assert np.array_equal(out[ring], u0[ring])
+    npts = int(np.prod([s - 2 * r for s in shape])) if min(shape) > 2 * r else 0
+    assert kc.traffic_bytes == 16 * npts * steps
+
+
+@pytest.mark.parametrize("unit", UNITS)
+@pytest.mark.parametrize("preset", ["2d9pt", "2d13pt", "2d49pt"])
+def test_other_presets_custom_weights_and_range(cuda, unit, preset):
+    """Non-symmetric weights (every tap distinct) and a partial row sweep."""
+    import torch
+
+    npts, r = P.stencil_preset(preset)[1], P.stencil_preset(preset)[2]
+    w = np.random.default_rng(2).uniform(-0.2, 0.3, npts)
+    shape = (150, 196)
+    u0 = O.stencil_init(shape, r, 9)
+    out, _ = _run(torch, preset, u0, 2, unit, weights=w)
+    assert O.rel_err(out, O.stencil(preset, u0, 2, w)) <= TOL
+    ref1 = O.stencil(preset, u0, 1, w)
+    u = torch.from_numpy(u0).cuda()
+    v = torch.zeros_like(u)
+    P.stencil_sweep(preset, u, v, 37, 111, weights=w, unit=unit)
+    torch.cuda.synchronize()
+    got = v.cpu().numpy()
+    assert O.rel_err(got[37:111, r:-r], ref1[37:111, r:-r]) <= TOL
+    assert not got[:37].any() and not got[111:].any()
 
 
 @pytest.mark.parametrize("unit", UNITS)

@@ -101,9 +101,32 @@ def stencils():
         torch.cuda.empty_cache()
 
 
+def stencil_r():
+    """2d9pt / 2d13pt / 2d49pt at 16384^2; GB/s of algorithmic bytes and the
+    FP64 rate (W = 2 |S| per point)."""
+    import math
+    u = torch.empty((16384, 16384), dtype=torch.float64, device="cuda")
+    v = torch.empty_like(u)
+    for preset in ("2d9pt", "2d13pt", "2d49pt"):
+        npts, r = P.stencil_preset(preset)[1], P.stencil_preset(preset)[2]
+        P.stencil_init(u, r, 1)
+        v.copy_(u)
+        pts = math.prod(s - 2 * r for s in u.shape)
+        for unit, st, cps in ((0, 4, 32), (0, 3, 32), (0, 4, 8), (1, 4, 32), (1, 4, 8)):
+            P.tuning_set("stencil_r_cc_stages", st)
+            P.tuning_set("stencil_r_ctas_per_sm", cps)
+            ms = timeit(lambda: P.stencil(preset, u, v, 2, unit=unit), reps=5) / 2
+            print(json.dumps({"kernel": f"{preset}_{'cc' if unit == 0 else 'tc'}", "stages": st, "ctas_per_sm": cps,
+                              "ms_per_step": round(ms, 4),
+                              "gbs": round(16 * pts / ms / 1e6, 1),
+                              "tflops": round(2 * npts * pts / ms / 1e9, 2)}), flush=True)
+
+
 if __name__ == "__main__":
     for w in sys.argv[1:]:
-        if w == "stencil":
+        if w == "stencil_r":
+            stencil_r()
+        elif w == "stencil":
             stencils()
         elif w == "temporal":
             temporal()
