@@ -414,6 +414,12 @@ struct rl_spmv_plan_s {
     std::vector<uint64_t> xpiece;      // x upload pieces: [xpiece[i], xpiece[i+1])
     cudaStream_t s_in = nullptr, s_cmp = nullptr, s_out = nullptr;
     std::vector<cudaEvent_t> ev_x, ev_y;
+    cudaEvent_t ev_join[2] = {nullptr, nullptr};
+    // execute_host as a CUDA graph, captured for the last (x, y) host pair
+    cudaGraphExec_t gexec = nullptr;
+    const double* gx = nullptr;
+    double* gy = nullptr;
+    uint64_t graph_launches = 0;
     KernelCharacterization kc;
     ~rl_spmv_plan_s() {
         if (rp) cudaFree(rp);
@@ -424,8 +430,11 @@ struct rl_spmv_plan_s {
         if (segs) cudaFree(segs);
         if (tiles) cudaFree(tiles);
         if (blk_tiles) cudaFree(blk_tiles);
+        if (gexec) cudaGraphExecDestroy(gexec);
         for (auto e : ev_x) cudaEventDestroy(e);
         for (auto e : ev_y) cudaEventDestroy(e);
+        for (auto e : ev_join)
+            if (e) cudaEventDestroy(e);
         if (s_in) cudaStreamDestroy(s_in);
         if (s_cmp) cudaStreamDestroy(s_cmp);
         if (s_out) cudaStreamDestroy(s_out);
@@ -481,7 +490,18 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
     const uint64_t unitrows = pl->tiled ? (uint64_t)rlb::kSpmvTiledRows : 1;
     const uint64_t units = (m + unitrows - 1) / unitrows;
     const uint64_t nch = std::min<uint64_t>((uint64_t)rlb::tuning().spmv_plan_chunks, units);
-    for (uint64_t c = 0; c <= nch; ++c) pl->chunk_row.push_back(std::min<uint64_t>(m, units * c / nch * unitrows));
+    // Chunk c covers weight w_c of the rows: w = 1/2 for the first and last
+    // chunk, 1 otherwise (spmv_plan_taper), so the pipeline's head (the first
+    // x prefix) and tail (the last compute + y copy) are short while the
+    // middle copies stay large.
+    const bool taper = rlb::tuning().spmv_plan_taper && nch >= 3;
+    const uint64_t wsum = taper ? 2 * nch - 2 : 2 * nch;  // in half units
+    uint64_t acc = 0;
+    for (uint64_t c = 0; c <= nch; ++c) {
+        pl->chunk_row.push_back(std::min<uint64_t>(m, units * acc / wsum * unitrows));
+        if (c < nch) acc += (taper && (c == 0 || c == nch - 1)) ? 1 : 2;
+    }
+    pl->chunk_row.back() = m;
     for (uint64_t c = 0; c < nch; ++c) {
         uint64_t mx = 0;
         for (int64_t j = rp[pl->chunk_row[c]]; j < rp[pl->chunk_row[c + 1]]; ++j) {
@@ -492,8 +512,16 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
         }
         pl->chunk_xend.push_back(mx);
     }
-    const uint64_t npc = std::min<uint64_t>((uint64_t)rlb::tuning().spmv_plan_chunks, n);
-    for (uint64_t i = 0; i <= npc; ++i) pl->xpiece.push_back(n * i / npc);
+    // x upload pieces end exactly where a chunk's column prefix ends, so
+    // chunk c waits for no byte of x it does not read
+    pl->xpiece.push_back(0);
+    uint64_t run = 0;
+    for (uint64_t c = 0; c < nch; ++c) {
+        run = std::max(run, pl->chunk_xend[c]);
+        if (run > pl->xpiece.back()) pl->xpiece.push_back(run);
+    }
+    if (pl->xpiece.back() < n) pl->xpiece.push_back(n);
+    const uint64_t npc = pl->xpiece.size() - 1;
     ck(cudaStreamCreateWithFlags(&pl->s_in, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&pl->s_cmp, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&pl->s_out, cudaStreamNonBlocking), "stream");
@@ -501,6 +529,7 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
     pl->ev_y.resize(nch);
     for (auto& e : pl->ev_x) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     for (auto& e : pl->ev_y) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    for (auto& e : pl->ev_join) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     return pl.release();
 }
 
@@ -515,19 +544,11 @@ void plan_rows(rl_spmv_plan_s* pl, uint64_t r0, uint64_t r1, const double* x, do
     }
 }
 
-void plan_execute_host(rl_spmv_plan_s* pl, const double* x, double* y) {
-    require_ptr(pl, "plan");
-    require_ptr(x, "x");
-    require_ptr(y, "y");
-    static const bool trace = getenv("RL_PLAN_TRACE") != nullptr;
-    std::vector<cudaEvent_t> tev;
-    auto mark = [&](cudaStream_t s) {
-        if (!trace) return;
-        cudaEvent_t e;
-        cudaEventCreate(&e);
-        cudaEventRecord(e, s);
-        tev.push_back(e);
-    };
+// Enqueue one pipelined call on the plan's streams (x pieces on s_in, row
+// chunks on s_cmp as their x prefix lands, y chunks on s_out).  `mark`
+// records trace events.
+template <class Mark>
+void plan_enqueue(rl_spmv_plan_s* pl, const double* x, double* y, double* y_direct, Mark&& mark) {
     mark(pl->s_in);
     const size_t npc = pl->ev_x.size();
     for (size_t i = 0; i < npc; ++i) {
@@ -535,19 +556,6 @@ void plan_execute_host(rl_spmv_plan_s* pl, const double* x, double* y) {
         ck(cudaMemcpyAsync(pl->x + a, x + a, (b - a) * 8, cudaMemcpyHostToDevice, pl->s_in), "H2D x");
         ck(cudaEventRecord(pl->ev_x[i], pl->s_in), "event");
         mark(pl->s_in);
-    }
-    // y: when the host buffer is pinned and mapped (cudaHostAlloc / registered,
-    // UVA), the kernels store y straight into it over PCIe -- those posted
-    // writes overlap the x upload in the other direction and no D2H pass is
-    // needed.  Otherwise y goes through the device buffer and a D2H copy per
-    // chunk on the third stream.
-    double* y_direct = nullptr;
-    if (rlb::tuning().spmv_plan_zero_copy) {
-        cudaPointerAttributes ay{};
-        if (cudaPointerGetAttributes(&ay, y) == cudaSuccess && ay.type == cudaMemoryTypeHost &&
-            ay.devicePointer != nullptr)
-            y_direct = static_cast<double*>(ay.devicePointer);
-        cudaGetLastError();
     }
     size_t waited = 0;  // x pieces the compute stream already waits for
     for (size_t c = 0; c + 1 < pl->chunk_row.size(); ++c) {
@@ -566,6 +574,79 @@ void plan_execute_host(rl_spmv_plan_s* pl, const double* x, double* y) {
             mark(pl->s_out);
         }
     }
+}
+
+bool pinned_host(const void* p) {
+    cudaPointerAttributes a{};
+    const bool ok = cudaPointerGetAttributes(&a, p) == cudaSuccess && a.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    return ok;
+}
+
+void plan_execute_host(rl_spmv_plan_s* pl, const double* x, double* y) {
+    require_ptr(pl, "plan");
+    require_ptr(x, "x");
+    require_ptr(y, "y");
+    static const bool trace = getenv("RL_PLAN_TRACE") != nullptr;
+    // y: when the host buffer is pinned and mapped (cudaHostAlloc / registered,
+    // UVA), the kernels can store y straight into it over PCIe (tuning key
+    // spmv_plan_zero_copy; measured slower than the D2H copies).
+    double* y_direct = nullptr;
+    if (rlb::tuning().spmv_plan_zero_copy) {
+        cudaPointerAttributes ay{};
+        if (cudaPointerGetAttributes(&ay, y) == cudaSuccess && ay.type == cudaMemoryTypeHost &&
+            ay.devicePointer != nullptr)
+            y_direct = static_cast<double*>(ay.devicePointer);
+        cudaGetLastError();
+    }
+    // Pinned x and y: the whole call is one CUDA graph (captured once per
+    // (x, y) pair), so the ~60 copies, waits and launches cost one launch of
+    // host time instead of pacing the copy engines.
+    if (!trace && !y_direct && rlb::tuning().spmv_plan_graph) {
+        if (pl->gexec && (pl->gx != x || pl->gy != y)) {
+            cudaGraphExecDestroy(pl->gexec);
+            pl->gexec = nullptr;
+        }
+        if (!pl->gexec && pinned_host(x) && pinned_host(y)) {
+            const uint64_t before = rlb::g_launches.load();
+            ck(cudaStreamBeginCapture(pl->s_in, cudaStreamCaptureModeThreadLocal), "graph capture");
+            cudaGraph_t g = nullptr;
+            try {
+                plan_enqueue(pl, x, y, nullptr, [](cudaStream_t) {});
+                ck(cudaEventRecord(pl->ev_join[0], pl->s_cmp), "event");
+                ck(cudaEventRecord(pl->ev_join[1], pl->s_out), "event");
+                ck(cudaStreamWaitEvent(pl->s_in, pl->ev_join[0], 0), "wait");
+                ck(cudaStreamWaitEvent(pl->s_in, pl->ev_join[1], 0), "wait");
+            } catch (...) {
+                cudaStreamEndCapture(pl->s_in, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            ck(cudaStreamEndCapture(pl->s_in, &g), "graph capture");
+            const cudaError_t e = cudaGraphInstantiate(&pl->gexec, g, 0);
+            cudaGraphDestroy(g);
+            ck(e, "graph instantiate");
+            pl->graph_launches = rlb::g_launches.load() - before;
+            rlb::g_launches.fetch_sub(pl->graph_launches);  // counted per replay below
+            pl->gx = x;
+            pl->gy = y;
+        }
+        if (pl->gexec) {
+            ck(cudaGraphLaunch(pl->gexec, pl->s_in), "graph launch");
+            rlb::note_launch(pl->graph_launches);
+            ck(cudaStreamSynchronize(pl->s_in), "sync");
+            return;
+        }
+    }
+    std::vector<cudaEvent_t> tev;
+    auto mark = [&](cudaStream_t st) {
+        if (!trace) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        tev.push_back(e);
+    };
+    plan_enqueue(pl, x, y, y_direct, mark);
     ck(cudaStreamSynchronize(pl->s_out), "sync");
     ck(cudaStreamSynchronize(pl->s_cmp), "sync");
     ck(cudaStreamSynchronize(pl->s_in), "sync");
@@ -950,8 +1031,12 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         else if (k == "spmv_plan_chunks") slot = &t.spmv_plan_chunks;
         else if (k == "spmv_plan_zero_copy") slot = &t.spmv_plan_zero_copy;
         else if (k == "spmv_plan_tiled") slot = &t.spmv_plan_tiled;
+        else if (k == "spmv_plan_graph") slot = &t.spmv_plan_graph;
+        else if (k == "spmv_plan_taper") slot = &t.spmv_plan_taper;
         else if (k == "stencil_r_ctas_per_sm") slot = &t.stencil_r_ctas_per_sm;
         else if (k == "stencil_r_cc_stages") slot = &t.stencil_r_cc_stages;
+        else if (k == "stencil_r_sym") slot = &t.stencil_r_sym;
+        else if (k == "stencil_r_l2promo") slot = &t.stencil_r_l2promo;
         else if (k == "spmv_tc_blocks_per_sm") slot = &t.spmv_tc_blocks_per_sm;
         else if (k == "spmv_tc_threads") slot = &t.spmv_tc_threads;
         else if (k == "spmv_tc_rows") slot = &t.spmv_tc_rows;

@@ -22,8 +22,10 @@ struct Tuning {
     int spmv_tc_threads = 1024;
     int spmv_l1_carveout = -1;     // shared-memory carveout % for the CC kernel (-1 = driver default)
     int spmv_tc_rows = 1;          // 8-row blocks per warp iteration (1, 2)
-    int spmv_plan_chunks = 8;      // pipelined row/x chunks of rl_spmv_plan_execute_host
+    int spmv_plan_chunks = 16;     // pipelined row/x chunks of rl_spmv_plan_execute_host
     int spmv_plan_tiled = 0;       // 1: CUDA-core plans use the column-tiled layout (spmv_tiled.cu; 0.31 ms vs CSR 0.28 ms on the BASELINE matrix)
+    int spmv_plan_taper = 0;       // 1: half-size first/last pipeline chunks (measured no gain)
+    int spmv_plan_graph = 1;       // execute_host with pinned x/y as one captured CUDA graph
     int spmv_plan_zero_copy = 0;   // 1: store y straight into pinned host memory (measured slower)
     int spmv_sched = 1;            // 0 grid-stride, 1 contiguous row range per CTA
     int spmv_xhint = 0;            // x gathers: 0 L1 default, 1 L1::evict_last, 2 L1::no_allocate
@@ -39,8 +41,10 @@ struct Tuning {
     int stencil_tc3d_ctas_per_sm = 8;  // ... 3D tensor-core kernels (3-plane mode)
     int stencil_tc3d_mode = 2;         // 3D tensor core, one-plane partial-sum kernel for: bit0 3d7pt, bit1 3d27pt
     int stencil_tc1_ctas_per_sm = 8;   // ... partial-sum mode
-    int stencil_r_cc_stages = 0;       // ... CUDA-core ring depth: 3, 4, 0 = auto (3 for 2d49pt -> 3 CTAs/SM, else 4)
-    int stencil_r_ctas_per_sm = 32;    // 2d9pt/2d13pt/2d49pt TMA kernels: row segments so the grid is this deep
+    int stencil_r_cc_stages = 0;       // ... CUDA-core ring depth: 2-4, 0 = auto (2 for 2d49pt -> 4 CTAs/SM, else 4)
+    int stencil_r_ctas_per_sm = 32;
+    int stencil_r_l2promo = 1;         // ... TMA L2 promotion (0 none, 1 64 B, 2 128 B, 3 256 B)
+    int stencil_r_sym = 1;             // 2d49pt CC: pair mirror-symmetric columns (fewer FP64 ops)    // 2d9pt/2d13pt/2d49pt TMA kernels: row segments so the grid is this deep
 };
 Tuning& tuning();
 
@@ -80,7 +84,8 @@ cudaError_t launch_stencil_r(int unit, const StencilDesc& d, uint64_t o0, uint64
 // 2D FP64 tensor map (box_x x box_y, zero OOB fill) into a 64-byte-aligned
 // CUtensorMap; false when the driver entry point is missing.
 bool tma_encode_available();
-bool encode_map_2d(void* map, const double* base, uint64_t nx, uint64_t ny, uint32_t box_x, uint32_t box_y);
+bool encode_map_2d(void* map, const double* base, uint64_t nx, uint64_t ny, uint32_t box_x, uint32_t box_y,
+                   int l2_promotion = 3);  // 0 none, 1 64 B, 2 128 B, 3 256 B
 
 // Two fused timesteps of 2d5pt (temporal blocking, CUDA core, TMA-eligible grids).
 cudaError_t launch_stencil_tma_t2(const StencilDesc& d, uint64_t o0, uint64_t o1, const double* u,

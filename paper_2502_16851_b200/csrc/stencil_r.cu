@@ -16,7 +16,11 @@
 //   every output row within +-R of it, DFMA with the weights straight from
 //   the kernel's parameter bank.  Per stage a warp issues 49*8*2 DFMA per
 //   thread against 14*5 LDS.128 (2d49pt), so the FP64 pipe, not shared
-//   memory, is the limit.
+//   memory, is the limit.  When the box weights are mirror-symmetric in x
+//   (the presets' defaults are), u[x-b] + u[x+b] is formed once per input
+//   row and reused by all 2R+1 output rows: 4 DFMA + 3/8*... DADD per
+//   (input row, output row) instead of 7 DFMA, ~33 FP64 ops per 2d49pt
+//   point instead of 49.
 // Tensor core (DMMA m8n8k4): an 8x8 output tile is a sum of banded products
 //   D += U_dy (8 x K) * B_dy (K x 8) with B_dy[k][n] = w(dy, k - n - R), K =
 //   8 + 2R padded to a multiple of 4 (box: one product per row offset dy;
@@ -159,7 +163,7 @@ __device__ __forceinline__ void store_pair(double* v, uint64_t nx, int R, int64_
 // ===========================================================================
 // One input row (stage row IR of the thread's group) into every output row
 // within +-R of it.
-template <int R, bool BOX, int P, int IR>
+template <int R, bool BOX, bool SYM, int P, int IR>
 __device__ __forceinline__ void cc_row(const double* T, const StencilDesc& d, double (&acc)[kRYr][2]) {
     constexpr int LP = Geo<R>::LP, NP = LP + 1;
     constexpr bool wide = BOX || (IR >= R && IR < R + kRYr);  // star: arms need only the centre
@@ -177,6 +181,30 @@ __device__ __forceinline__ void cc_row(const double* T, const StencilDesc& d, do
         vv[LP] = t.x;
         vv[LP + 1] = t.y;
     }
+    if constexpr (SYM && BOX) {
+        // w(dy, dx) == w(dy, -dx): pair the columns once per input row (R DADD
+        // per column), then R+1 DFMA per (input row, output row) instead of 2R+1
+        double h[2][R + 1];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            h[c][0] = vv[LP + c];
+#pragma unroll
+            for (int b = 1; b <= R; ++b) h[c][b] = vv[LP + c - b] + vv[LP + c + b];
+        }
+#pragma unroll
+        for (int b = 0; b <= R; ++b) {
+#pragma unroll
+            for (int j = 0; j < kRYr; ++j) {
+                const int dy = IR - R - j;
+                if (dy >= -R && dy <= R) {
+                    const double w = d.w[widx<R, BOX>(dy, b)];
+                    acc[j][0] = fma(w, h[0][b], acc[j][0]);
+                    acc[j][1] = fma(w, h[1][b], acc[j][1]);
+                }
+            }
+        }
+        return;
+    }
     // dx outer: consecutive DFMAs go to different accumulators
 #pragma unroll
     for (int dx = -R; dx <= R; ++dx) {
@@ -191,13 +219,13 @@ __device__ __forceinline__ void cc_row(const double* T, const StencilDesc& d, do
         }
     }
 }
-template <int R, bool BOX, int P, int... IR>
+template <int R, bool BOX, bool SYM, int P, int... IR>
 __device__ __forceinline__ void cc_rows(const double* T, const StencilDesc& d, double (&acc)[kRYr][2],
                                         std::integer_sequence<int, IR...>) {
-    (cc_row<R, BOX, P, IR>(T, d, acc), ...);
+    (cc_row<R, BOX, SYM, P, IR>(T, d, acc), ...);
 }
 
-template <int R, bool BOX, int S>
+template <int R, bool BOX, bool SYM, int S>
 __global__ void __launch_bounds__(128) st2dr_tma_cc(const __grid_constant__ CUtensorMap tm, double* __restrict__ v,
                                                     uint64_t nx, uint64_t y_begin, uint64_t y_end, int seg_rows,
                                                     int strips, const __grid_constant__ StencilDesc d) {
@@ -223,7 +251,7 @@ __global__ void __launch_bounds__(128) st2dr_tma_cc(const __grid_constant__ CUte
 #pragma unroll
         for (int j = 0; j < kRYr; ++j) acc[j][0] = acc[j][1] = 0.0;
         // input rows as a compile-time sequence (dy, tap and weight index fold to constants)
-        cc_rows<R, BOX, P>(T, d, acc, std::make_integer_sequence<int, kRYr + 2 * R>{});
+        cc_rows<R, BOX, SYM, P>(T, d, acc, std::make_integer_sequence<int, kRYr + 2 * R>{});
         ring.release(k);
         if (tid == 0 && k + S < nblk) {
             ring.wait_empty(k);
@@ -349,13 +377,23 @@ cudaError_t prep(K kernel, size_t smem) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
+// Box weights mirror-symmetric in x (w(dy, dx) == w(dy, -dx), exactly)?
+template <int R>
+bool x_symmetric(const StencilDesc& d) {
+    for (int dy = -R; dy <= R; ++dy)
+        for (int dx = 1; dx <= R; ++dx)
+            if (d.w[widx<R, true>(dy, dx)] != d.w[widx<R, true>(dy, -dx)]) return false;
+    return true;
+}
+
 template <int R, bool BOX>
 cudaError_t launch_r(int unit, const StencilDesc& d, uint64_t o0, uint64_t o1, const double* u, double* v,
                      cudaStream_t s) {
     constexpr int S = 4;
     CUtensorMap m;
     const uint32_t bx = (uint32_t)(unit == 1 ? pitch<R, true>() : pitch<R, false>());
-    if (!encode_map_2d(&m, u, d.nx, d.ny, bx, (uint32_t)Geo<R>::ROWS)) return cudaErrorInvalidValue;
+    if (!encode_map_2d(&m, u, d.nx, d.ny, bx, (uint32_t)Geo<R>::ROWS, tuning().stencil_r_l2promo))
+        return cudaErrorInvalidValue;
     const uint64_t strips = (d.nx + kTXr - 1) / kTXr;
     // split the rows so the grid is many waves deep (balance across 148 SMs)
     const uint64_t want = (uint64_t)kNumSMs * (uint64_t)(tuning().stencil_r_ctas_per_sm);
@@ -371,14 +409,21 @@ cudaError_t launch_r(int unit, const StencilDesc& d, uint64_t o0, uint64_t o1, c
         const size_t sm = ring_bytes<R, true, S>();
         if ((e = prep(st2dr_tma_tc<R, BOX, S>, sm)) != cudaSuccess) return e;
         st2dr_tma_tc<R, BOX, S><<<grid, 128, sm, s>>>(m, v, d.nx, o0, o1, seg_rows, (int)strips, d);
-    } else if (tuning().stencil_r_cc_stages == 3 || (tuning().stencil_r_cc_stages == 0 && R == 3 && BOX)) {
-        const size_t sm = ring_bytes<R, false, 3>();
-        if ((e = prep(st2dr_tma_cc<R, BOX, 3>, sm)) != cudaSuccess) return e;
-        st2dr_tma_cc<R, BOX, 3><<<grid, 128, sm, s>>>(m, v, d.nx, o0, o1, seg_rows, (int)strips, d);
     } else {
-        const size_t sm = ring_bytes<R, false, S>();
-        if ((e = prep(st2dr_tma_cc<R, BOX, S>, sm)) != cudaSuccess) return e;
-        st2dr_tma_cc<R, BOX, S><<<grid, 128, sm, s>>>(m, v, d.nx, o0, o1, seg_rows, (int)strips, d);
+        int st = tuning().stencil_r_cc_stages;
+        if (st == 0) st = (R == 3 && BOX) ? 2 : 4;  // 2d49pt: compute-bound, more CTAs beat a deeper ring
+#define RLB_RCC(SY, SS)                                                                                     \
+    do {                                                                                                    \
+        const size_t sm = ring_bytes<R, false, SS>();                                                       \
+        if ((e = prep(st2dr_tma_cc<R, BOX, SY, SS>, sm)) != cudaSuccess) return e;                         \
+        st2dr_tma_cc<R, BOX, SY, SS><<<grid, 128, sm, s>>>(m, v, d.nx, o0, o1, seg_rows, (int)strips, d); \
+    } while (0)
+        if (BOX && R == 3 && x_symmetric<R>(d) && tuning().stencil_r_sym) {
+            if (st == 2) RLB_RCC(true, 2); else if (st == 3) RLB_RCC(true, 3); else RLB_RCC(true, 4);
+        } else {
+            if (st == 2) RLB_RCC(false, 2); else if (st == 3) RLB_RCC(false, 3); else RLB_RCC(false, 4);
+        }
+#undef RLB_RCC
     }
     note_launch();
     return cudaGetLastError();

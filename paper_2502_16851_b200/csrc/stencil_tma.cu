@@ -885,7 +885,11 @@ int split_count(uint64_t tiles, uint64_t extent, int min_chunk, int per_sm) {
 
 bool tma_encode_available() { return encode_fn() != nullptr; }
 
-bool encode_map_2d(void* map, const double* base, uint64_t nx, uint64_t ny, uint32_t box_x, uint32_t box_y) {
+bool encode_map_2d(void* map, const double* base, uint64_t nx, uint64_t ny, uint32_t box_x, uint32_t box_y,
+                   int l2_promotion) {
+    static const CUtensorMapL2promotion promo[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
+                                                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
     auto fn = encode_fn();
     if (!fn) return false;
     cuuint64_t gdim[2] = {nx, ny};
@@ -894,7 +898,7 @@ bool encode_map_2d(void* map, const double* base, uint64_t nx, uint64_t ny, uint
     cuuint32_t estride[2] = {1, 1};
     return fn(static_cast<CUtensorMap*>(map), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), gdim,
               gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+              promo[l2_promotion & 3], CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 cudaError_t launch_stencil_tma_t2(const StencilDesc& d, uint64_t o0, uint64_t o1, const double* u,

@@ -131,3 +131,31 @@ def test_tiled_plan_ragged_dense_and_empty(cuda, tiled_plans):
     _plan_check(torch, rp, col, val, n, P.CUDA_CORE, True)
     _plan_check(torch, rp, col, val, n + 1, P.CUDA_CORE, False)   # odd n -> CSR kernel
     _plan_check(torch, rp, col, val, n, P.TENSOR_CORE, False)     # TC plans keep CSR
+
+
+@pytest.mark.parametrize("tiled", [0, 1])
+def test_plan_graph_replay_pinned(cuda, tiled):
+    """Pinned x/y: execute_host runs as a captured CUDA graph.  New x
+    contents are picked up on replay, a new (x, y) pair re-captures, and the
+    launch counter advances per replay."""
+    import torch
+
+    P.tuning_set("spmv_plan_tiled", tiled)
+    try:
+        m = n = 70000
+        rp, col, val = O.gen_band_csr(m, 0, n, 12, 9000, 17)
+        plan = P.SpmvPlan(rp, col, val, n)
+        rng = np.random.default_rng(1)
+        xs = [torch.from_numpy(rng.uniform(-1, 1, n)).pin_memory() for _ in range(2)]
+        ys = [torch.full((m,), float("nan"), dtype=torch.float64).pin_memory() for _ in range(2)]
+        for it in range(3):
+            for j in range(2):
+                xs[j].copy_(torch.from_numpy(rng.uniform(-1, 1, n)))
+                before = P.kernel_launches()
+                plan.execute_host(xs[j], ys[j])
+                assert P.kernel_launches() > before
+                ref = O.spmv_csr(rp, col, val, xs[j].numpy())
+                assert O.rel_err(ys[j].numpy(), ref) <= 1e-12
+        plan.close()
+    finally:
+        P.tuning_set("spmv_plan_tiled", 0)

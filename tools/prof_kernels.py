@@ -1,7 +1,8 @@
 """Run each hot kernel a few times at its BASELINE config (for ncu captures).
 
   python tools/prof_kernels.py [names...]   names: stream_cc stream_tc spmv_cc spmv_tc
-        2d5pt_cc 2d5pt_tc 3d7pt_cc 3d7pt_tc 3d27pt_cc 3d27pt_tc (default: all)
+        2d5pt_cc 2d5pt_tc 3d7pt_cc 3d7pt_tc 3d27pt_cc 3d27pt_tc (default: all);
+        also 2d9pt_* 2d13pt_* 2d49pt_*
 """
 import os
 import sys
@@ -36,9 +37,9 @@ def run(name):
         for _ in range(REPS):
             P.spmv_csr(rp, col, val, x, y, unit=unit)
     else:
-        shape = (16384, 16384) if kern == "2d5pt" else (512, 512, 512)
+        shape = (16384, 16384) if kern.startswith("2d") else (512, 512, 512)
         u = torch.empty(shape, dtype=torch.float64, device="cuda")
-        P.stencil_init(u, 1, 1)
+        P.stencil_init(u, P.stencil_preset(kern)[2], 1)
         v = u.clone()
         P.stencil(kern, u, v, REPS, unit=unit)
     torch.cuda.synchronize()

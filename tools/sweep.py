@@ -112,11 +112,15 @@ def stencil_r():
         P.stencil_init(u, r, 1)
         v.copy_(u)
         pts = math.prod(s - 2 * r for s in u.shape)
-        for unit, st, cps in ((0, 4, 32), (0, 3, 32), (0, 4, 8), (1, 4, 32), (1, 4, 8)):
+        for unit, st, cps, sym in ((0, 0, 32, 0), (0, 0, 32, 1), (0, 0, 32, 2), (0, 0, 32, 3), (0, 0, 64, 0),
+                                   (1, 0, 32, 0), (1, 0, 32, 3)):
             P.tuning_set("stencil_r_cc_stages", st)
+            promo = sym
+            P.tuning_set("stencil_r_l2promo", promo)
+            P.tuning_set("stencil_r_sym", sym)
             P.tuning_set("stencil_r_ctas_per_sm", cps)
             ms = timeit(lambda: P.stencil(preset, u, v, 2, unit=unit), reps=5) / 2
-            print(json.dumps({"kernel": f"{preset}_{'cc' if unit == 0 else 'tc'}", "stages": st, "ctas_per_sm": cps,
+            print(json.dumps({"kernel": f"{preset}_{'cc' if unit == 0 else 'tc'}", "stages": st, "ctas_per_sm": cps, "promo": promo,
                               "ms_per_step": round(ms, 4),
                               "gbs": round(16 * pts / ms / 1e6, 1),
                               "tflops": round(2 * npts * pts / ms / 1e9, 2)}), flush=True)
