@@ -27,11 +27,19 @@ METRICS = {
 
 ALGO = {  # algorithmic bytes per launch (reference models)
     "stream": 2147483648, "spmv": 889192452, "2d5pt": 4293918784, "3d7pt": 2122416000,
-    "3d27pt": 2122416000,
+    "3d27pt": 2122416000, "2d9pt": 16 * 16382 ** 2, "2d13pt": 16 * 16378 ** 2, "2d49pt": 16 * 16378 ** 2,
+    "gemv": (16384 * 65536 + 16384 + 65536) * 8, "spmvtiled": 889192452,
 }
 
 
 def workload(name):
+    m = re.search(r"st2dr_tma_(cc|tc)<(?:\(\w+\))?(\d+), *(?:\(\w+\))?(\w+)", name)
+    if m:
+        r, box = int(m.group(2)), m.group(3) in ("true", "1")
+        return {(1, True): "2d9pt", (3, False): "2d13pt", (3, True): "2d49pt"}[(r, box)] + "_" + m.group(1)
+    if "gemv_cc" in name: return "gemv_cc"
+    if "gemv_tc" in name: return "gemv_tc"
+    if "spmv_tiled" in name: return "spmvtiled_cc"
     if "scale_cc" in name: return "stream_cc"
     if "scale_tc" in name: return "stream_tc"
     if "spmv_cc" in name: return "spmv_cc"
@@ -64,6 +72,8 @@ def main(rep, out_md, out_json=None):
                 except ValueError:
                     rec[k] = float("nan")
         rec["unit_dram"] = units[idx[METRICS["dram_rd"]]]
+        tu = units[idx[METRICS["dur_us"]]]
+        rec["dur_us"] *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}.get(tu, 1.0)
         per.setdefault(w, []).append(rec)
     scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
     lines = ["| kernel | launches | ncu time (µs, cold, serialised) | DRAM read+write per launch (GB) | algorithmic (GB) | traffic / algorithmic | dram % peak | L2 % | L1 % | warps active % | fp64 pipe % | dmma pipe % | regs |",

@@ -2,7 +2,7 @@
 
   python tools/prof_kernels.py [names...]   names: stream_cc stream_tc spmv_cc spmv_tc
         2d5pt_cc 2d5pt_tc 3d7pt_cc 3d7pt_tc 3d27pt_cc 3d27pt_tc (default: all);
-        also 2d9pt_* 2d13pt_* 2d49pt_*
+        also 2d9pt_* 2d13pt_* 2d49pt_* gemv_* spmvtiled_cc
 """
 import os
 import sys
@@ -36,6 +36,29 @@ def run(name):
         P.fill_uniform(x, 1, 4, 0, 1)
         for _ in range(REPS):
             P.spmv_csr(rp, col, val, x, y, unit=unit)
+    elif kern == "gemv":
+        m, n = 16384, 65536
+        A = torch.empty((m, n), dtype=torch.float64, device="cuda")
+        P.fill_uniform(A.view(-1), 1, 6, 0, 1)
+        x = torch.empty(n, dtype=torch.float64, device="cuda")
+        P.fill_uniform(x, 1, 4, 0, 1)
+        y = torch.empty(m, dtype=torch.float64, device="cuda")
+        for _ in range(REPS):
+            P.gemv(A, x, y, unit=unit)
+    elif kern == "spmvtiled":
+        n, k, hb = 1 << 22, 16, 65536
+        rp = torch.empty(n + 1, dtype=torch.int32, device="cuda")
+        col = torch.empty(n * k, dtype=torch.int32, device="cuda")
+        val = torch.empty(n * k, dtype=torch.float64, device="cuda")
+        x = torch.empty(n, dtype=torch.float64, device="cuda")
+        y = torch.empty(n, dtype=torch.float64, device="cuda")
+        P.gen_band_csr(n, 0, n, k, hb, 1, rp, col, val)
+        P.fill_uniform(x, 1, 4, 0, 1)
+        P.tuning_set("spmv_plan_tiled", 1)
+        plan = P.SpmvPlan(rp.cpu(), col.cpu(), val.cpu(), n)
+        for _ in range(REPS):
+            plan.execute(x, y)
+        plan.close()
     else:
         shape = (16384, 16384) if kern.startswith("2d") else (512, 512, 512)
         u = torch.empty(shape, dtype=torch.float64, device="cuda")
