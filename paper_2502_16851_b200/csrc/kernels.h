@@ -23,7 +23,7 @@ struct Tuning {
     int spmv_l1_carveout = -1;     // shared-memory carveout % for the CC kernel (-1 = driver default)
     int spmv_tc_rows = 1;          // 8-row blocks per warp iteration (1, 2)
     int spmv_plan_chunks = 16;     // pipelined row/x chunks of rl_spmv_plan_execute_host
-    int spmv_plan_tiled = 0;       // 1: CUDA-core plans use the column-tiled layout (spmv_tiled.cu; 0.31 ms vs CSR 0.28 ms on the BASELINE matrix)
+    int spmv_plan_tiled = 0;       // 1: CUDA-core plans use the column-tiled layout (spmv_tiled.cu; 0.30 ms vs CSR 0.28 ms on the BASELINE matrix)
     int spmv_plan_taper = 0;       // 1: half-size first/last pipeline chunks (measured no gain)
     int spmv_plan_graph = 1;       // execute_host with pinned x/y as one captured CUDA graph
     int spmv_plan_zero_copy = 0;   // 1: store y straight into pinned host memory (measured slower)

@@ -8,25 +8,27 @@
 // format conversion in the paper) so that every x value a
 // row needs comes from shared memory:
 //
-//   * rows are cut into blocks of RB = 8192 (one CTA of 32 warps; warp w owns
-//     rows 256w .. 256w+255 of the block and their sums in shared memory);
+//   * rows are cut into blocks of RB = 8192 (one CTA of 16 warps; warp w owns
+//     rows 512w .. 512w+511 of the block and their sums in shared memory);
 //   * a block's nonzeros, in column order, are cut into tiles of at most
 //     kEMax entries spanning at most kT = 2048 columns;
-//   * a tile is one contiguous segment in HBM: 33 per-warp entry offsets,
+//   * a tile is one contiguous segment in HBM: 17 per-warp chunk offsets,
 //     the values (f64) and one u32 of metadata per entry (column in tile |
-//     row in warp | segment depth | segment end), entries sorted by row;
+//     row in warp | run start / end | lane carry depth), entries sorted by
+//     row, each warp's chunk padded to a multiple of 4;
 //   * one pipeline thread bulk-copies (cp.async.bulk + mbarrier transaction
 //     count) the x slice and the segment into a 4-stage shared-memory ring;
 //     the last warp to release a stage refills it, so no warp waits on
 //     another except through the data itself;
-//   * each warp walks its entries 32 at a time: lane product val*x (x from
-//     shared memory), a segmented inclusive scan over the lanes (depth from
-//     the metadata, shuffles only as deep as the warp's longest run), and the
-//     run's last lane adds the row's partial sum to shared y.  Rows never
-//     span warps and runs of a row are added in a fixed order, so the result
-//     is deterministic.
+//   * each warp walks its chunk 128 entries at a time, 4 consecutive entries
+//     per lane (128-bit shared loads of values and metadata, x gathered from
+//     the shared slice); runs of a row are summed inside the lane, a run that
+//     crosses lanes takes its carry from one shuffle (a segmented scan only
+//     when a run spans more than two lanes), and the entry that ends a run
+//     adds it to shared y.  Rows never span warps and runs are added in a
+//     fixed order, so the result is deterministic.
 //
-// Traffic per call is the segments (12 B per nonzero + 80 B per tile) plus
+// Traffic per call is the segments (12 B per nonzero + 64 B per tile) plus
 // y; x slices are served from L2.  The algorithmic accounting stays the CSR
 // model's (kernels.cpp:125-136 of the reference).
 #include <algorithm>
@@ -41,25 +43,45 @@
 namespace rlb {
 
 namespace {
-constexpr int kRB = kSpmvTiledRows;  // rows per block
-constexpr int kWarps = 32;
+constexpr int kRB = kSpmvTiledRows;         // rows per block (one CTA)
+constexpr int kWarps = 16;
 constexpr int kThreads = kWarps * 32;
-constexpr int kRowsPerWarp = kRB / kWarps;  // 256 -> 8-bit row field
-constexpr int kT = 2048;                    // max tile width (columns) -> 11-bit column field
-constexpr int kEMax = 2048;                 // max entries per tile
-constexpr int kStages = 4;
+constexpr int kRowsPerWarp = kRB / kWarps;  // 512 -> 9-bit row field
+#ifndef RLB_TILED_T
+#define RLB_TILED_T 2048
+#endif
+#ifndef RLB_TILED_EMAX
+#define RLB_TILED_EMAX 2048
+#endif
+#ifndef RLB_TILED_STAGES
+#define RLB_TILED_STAGES 3
+#endif
+constexpr int kT = RLB_TILED_T;             // max tile width (columns, <= 2048: 11-bit column field)
+constexpr int kEMax = RLB_TILED_EMAX;       // max nonzeros per tile
+constexpr int kPerLane = 4;                 // consecutive entries a lane owns in a round
+constexpr int kRound = 32 * kPerLane;       // entries a warp consumes per round
+constexpr int kEPad = kEMax + (kPerLane - 1) * kWarps;  // warp chunks padded to multiples of 4
+constexpr int kStages = RLB_TILED_STAGES;
 
 __host__ __device__ constexpr size_t pad16(size_t b) { return (b + 15) & ~size_t(15); }
-constexpr size_t kOffBytes = pad16((kWarps + 1) * 2);  // 80
-constexpr size_t kSegMax = kOffBytes + pad16((size_t)kEMax * 12);
+constexpr size_t kOffBytes = 64;  // kWarps + 1 u16 chunk offsets
+constexpr size_t kSegMax = kOffBytes + (size_t)kEPad * 12;
 constexpr size_t kXBytes = (size_t)kT * 8;
 constexpr size_t kStageBytes = kXBytes + kSegMax;
 constexpr size_t kYBytes = (size_t)kRB * 8;
-constexpr size_t kSmem = kStages * kStageBytes + kYBytes + kStages * 8 + kStages * 4;
+constexpr int kDescCache = 512;  // tile descriptors staged in shared memory (later ones read from global)
+constexpr size_t kSmem = kStages * kStageBytes + kYBytes + kDescCache * sizeof(SpmvTile) + kStages * 8 + kStages * 4;
 static_assert(kSmem <= 227 * 1024, "tiled SpMV shared memory");
+static_assert(kStageBytes % 128 == 0 && kSegMax % 16 == 0, "stage alignment");
 
-// metadata word
-constexpr int kColBits = 11, kRowShift = 11, kDepthShift = 19, kEndShift = 24;
+// metadata word of one entry
+constexpr uint32_t kColMask = (1u << 11) - 1;  // bits 0-10: column in the tile
+constexpr int kRowShift = 11;                  // bits 11-19: row in the warp's 512
+constexpr uint32_t kValid = 1u << 20;          // real nonzero (0 = padding)
+constexpr uint32_t kStart = 1u << 21;          // first entry of its row's run in this round
+constexpr uint32_t kEnd = 1u << 22;            // last entry of its row's run in this round
+constexpr int kDepthShift = 23;                // bits 23-27 (lane's first entry): lanes the carry spans
+constexpr uint32_t kLaneStart = 1u << 28;      // (lane's first entry) a run starts in this lane
 
 __device__ __forceinline__ uint32_t sptr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -79,7 +101,9 @@ __global__ void __launch_bounds__(kThreads, 1) spmv_tiled_kernel(uint64_t m, uin
                                                                  double* __restrict__ y) {
     extern __shared__ __align__(128) uint8_t smem[];
     double* ysm = reinterpret_cast<double*>(smem + kStages * kStageBytes);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes + kYBytes);
+    SpmvTile* desc = reinterpret_cast<SpmvTile*>(smem + kStages * kStageBytes + kYBytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes + kYBytes +
+                                                 kDescCache * sizeof(SpmvTile));
     uint32_t* cnt = reinterpret_cast<uint32_t*>(full + kStages);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t b = b_first + blockIdx.x;
@@ -88,6 +112,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmv_tiled_kernel(uint64_t m, uin
     double* yw = ysm + warp * kRowsPerWarp;
 #pragma unroll
     for (int i = 0; i < kRowsPerWarp / 32; ++i) yw[lane + 32 * i] = 0.0;
+    for (int i = tid; i < nt && i < kDescCache; i += kThreads) desc[i] = tiles[t0 + i];
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sptr(full + s)) : "memory");
@@ -97,7 +122,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmv_tiled_kernel(uint64_t m, uin
     }
     __syncthreads();
     auto issue = [&](int k) {
-        const SpmvTile t = tiles[t0 + k];
+        const SpmvTile t = k < kDescCache ? desc[k] : tiles[t0 + k];
         uint8_t* st = smem + (k % kStages) * kStageBytes;
         const uint32_t xb = (uint32_t)(t.width * 8);
         const uint32_t sb = (uint32_t)t.seg_bytes;
@@ -124,26 +149,49 @@ __global__ void __launch_bounds__(kThreads, 1) spmv_tiled_kernel(uint64_t m, uin
         const int E = offs[kWarps], e0 = offs[warp], e1 = offs[warp + 1];
         const double* vals = reinterpret_cast<const double*>(seg + kOffBytes);
         const uint32_t* meta = reinterpret_cast<const uint32_t*>(seg + kOffBytes + (size_t)E * 8);
-        // two 32-entry rounds per pass: both rounds' loads in flight together
-        for (int base = e0; base < e1; base += 64) {
-            const int ea = base + lane, eb = ea + 32;
-            double pa = 0.0, pb = 0.0;
-            uint32_t ma = 0, mb = 0;
-            if (ea < e1) ma = meta[ea];
-            if (eb < e1) mb = meta[eb];
-            if (ea < e1) pa = vals[ea] * xs[ma & ((1u << kColBits) - 1)];
-            if (eb < e1) pb = vals[eb] * xs[mb & ((1u << kColBits) - 1)];
-            const int da = (int)((ma >> kDepthShift) & 31), db = (int)((mb >> kDepthShift) & 31);
-            const int maxd = (int)__reduce_max_sync(0xffffffffu, (unsigned)max(da, db));
-            for (int o = 1; o <= maxd; o <<= 1) {
-                const double qa = __shfl_up_sync(0xffffffffu, pa, o);
-                const double qb = __shfl_up_sync(0xffffffffu, pb, o);
-                if (o <= da) pa += qa;
-                if (o <= db) pb += qb;
+        for (int base = e0; base < e1; base += kRound) {
+            const int e = base + kPerLane * lane;  // chunk lengths are multiples of 4
+            double p[kPerLane] = {0.0, 0.0, 0.0, 0.0};
+            uint32_t mt[kPerLane] = {0u, 0u, 0u, 0u};
+            if (e < e1) {
+                const uint4 m4 = *reinterpret_cast<const uint4*>(meta + e);
+                const double2 va = *reinterpret_cast<const double2*>(vals + e);
+                const double2 vb = *reinterpret_cast<const double2*>(vals + e + 2);
+                mt[0] = m4.x, mt[1] = m4.y, mt[2] = m4.z, mt[3] = m4.w;
+                const double v[kPerLane] = {va.x, va.y, vb.x, vb.y};
+#pragma unroll
+                for (int j = 0; j < kPerLane; ++j)
+                    if (mt[j] & kValid) p[j] = v[j] * xs[mt[j] & kColMask];
             }
-            if ((ma >> kEndShift) & 1) yw[(ma >> kRowShift) & (kRowsPerWarp - 1)] += pa;
-            __syncwarp();
-            if ((mb >> kEndShift) & 1) yw[(mb >> kRowShift) & (kRowsPerWarp - 1)] += pb;
+            // lane tail: the running sum since the lane's last run start
+            double t = 0.0;
+#pragma unroll
+            for (int j = 0; j < kPerLane; ++j) t = (mt[j] & kStart) ? p[j] : t + p[j];
+            const int d = (int)((mt[0] >> kDepthShift) & 31);
+            const int maxd = (int)__reduce_max_sync(0xffffffffu, (unsigned)d);
+            double carry = 0.0;
+            if (maxd > 0) {
+                // segmented inclusive scan of the tails over lanes, only as
+                // deep as the longest run crossing lane boundaries
+                double T = t;
+                bool f = (mt[0] & kLaneStart) || !(mt[0] & kValid);
+                for (int o = 1; o < maxd; o <<= 1) {
+                    const double q = __shfl_up_sync(0xffffffffu, T, o);
+                    const bool fq = __shfl_up_sync(0xffffffffu, (int)f, o) != 0;
+                    if (lane >= o && !f) {
+                        T += q;
+                        f = fq;
+                    }
+                }
+                const double c = __shfl_up_sync(0xffffffffu, T, 1);
+                if (d > 0) carry = c;
+            }
+            double run = carry;
+#pragma unroll
+            for (int j = 0; j < kPerLane; ++j) {
+                run = (mt[j] & kStart) ? p[j] : run + p[j];
+                if (mt[j] & kEnd) yw[(mt[j] >> kRowShift) & (kRowsPerWarp - 1)] += run;
+            }
             __syncwarp();
         }
         // release the stage; the last warp out refills it
@@ -186,6 +234,8 @@ void build_block(uint64_t r0, uint64_t r1, uint64_t n, const int32_t* rp, const 
         for (int64_t k = rp[i]; k < rp[i + 1]; ++k) es.push_back({col[k], (int32_t)(i - r0), val[k]});
     if (es.empty()) return;
     std::stable_sort(es.begin(), es.end(), [](const HostEntry& a, const HostEntry& c) { return a.col < c.col; });
+    std::vector<int> slot_row;       // per padded slot: row (-1 = padding)
+    std::vector<const HostEntry*> slot_src;
     size_t p = 0;
     while (p < es.size()) {
         const int32_t c0 = es[p].col & ~1;
@@ -194,37 +244,74 @@ void build_block(uint64_t r0, uint64_t r1, uint64_t n, const int32_t* rp, const 
         while (q < es.size() && es[q].col < lim && q - p < (size_t)kEMax) ++q;
         int32_t width = ((es[q - 1].col - c0) + 2) & ~1;
         if ((uint64_t)c0 + width > n) width = (int32_t)(n - c0);
-        // entries by (row, column): warps' runs are contiguous, rows sorted
+        // entries by (row, column): each warp's chunk is contiguous, rows sorted
         std::stable_sort(es.begin() + p, es.begin() + q,
                          [](const HostEntry& a, const HostEntry& c) { return a.row < c.row; });
+        const HostEntry* te = es.data() + p;
         const int E = (int)(q - p);
+        // per-warp chunks padded to multiples of kPerLane
+        int off[kWarps + 1];
+        slot_row.clear();
+        slot_src.clear();
+        int cur = 0;
+        for (int w = 0; w < kWarps; ++w) {
+            off[w] = (int)slot_row.size();
+            while (cur < E && te[cur].row / kRowsPerWarp == w) {
+                slot_row.push_back(te[cur].row);
+                slot_src.push_back(te + cur);
+                ++cur;
+            }
+            while (slot_row.size() % kPerLane) {
+                slot_row.push_back(-1);
+                slot_src.push_back(nullptr);
+            }
+        }
+        off[kWarps] = (int)slot_row.size();
+        const int EP = off[kWarps];
         SpmvTile t{};
         t.seg_offset = segs.size();
         t.col_base = c0;
         t.width = width;
         t.entries = E;
-        t.seg_bytes = (int)(kOffBytes + pad16((size_t)E * 12));
+        t.seg_bytes = (int)(kOffBytes + pad16((size_t)EP * 12));
         segs.resize(segs.size() + t.seg_bytes, 0);
         uint8_t* sb = segs.data() + t.seg_offset;
-        uint16_t* off = reinterpret_cast<uint16_t*>(sb);
+        uint16_t* o16 = reinterpret_cast<uint16_t*>(sb);
         double* v = reinterpret_cast<double*>(sb + kOffBytes);
-        uint32_t* mt = reinterpret_cast<uint32_t*>(sb + kOffBytes + (size_t)E * 8);
-        const HostEntry* te = es.data() + p;
-        int cur = 0;
-        for (int w = 0; w <= kWarps; ++w) {
-            while (cur < E && te[cur].row / kRowsPerWarp < w) ++cur;
-            off[w] = (uint16_t)cur;
-        }
-        int seg_start = 0;
-        for (int i = 0; i < E; ++i) {
-            const int w = te[i].row / kRowsPerWarp;
-            if (i == 0 || te[i].row != te[i - 1].row) seg_start = i;
-            const int round_start = off[w] + ((i - off[w]) / 32) * 32;
-            const int depth = i - std::max(seg_start, round_start);
-            const bool end = i + 1 == E || te[i + 1].row != te[i].row || (i + 1 - off[w]) % 32 == 0;
-            v[i] = te[i].val;
-            mt[i] = (uint32_t)(te[i].col - c0) | ((uint32_t)(te[i].row % kRowsPerWarp) << kRowShift) |
-                    ((uint32_t)depth << kDepthShift) | ((end ? 1u : 0u) << kEndShift);
+        uint32_t* mt = reinterpret_cast<uint32_t*>(sb + kOffBytes + (size_t)EP * 8);
+        for (int w = 0; w <= kWarps; ++w) o16[w] = (uint16_t)off[w];
+        for (int w = 0; w < kWarps; ++w) {
+            for (int rs = off[w]; rs < off[w + 1]; rs += kRound) {  // rounds
+                const int re = std::min(rs + kRound, off[w + 1]);
+                auto valid = [&](int i) { return i < re && slot_row[i] >= 0; };
+                bool lane_start[32] = {};
+                for (int i = rs; i < re; ++i) {
+                    const bool st = valid(i) && (i == rs || slot_row[i] != slot_row[i - 1]);
+                    const bool en = valid(i) && (!valid(i + 1) || slot_row[i + 1] != slot_row[i]);
+                    uint32_t word = 0;
+                    if (valid(i)) {
+                        const HostEntry* h = slot_src[i];
+                        v[i] = h->val;
+                        word = (uint32_t)(h->col - c0) | ((uint32_t)(h->row % kRowsPerWarp) << kRowShift) | kValid;
+                    }
+                    if (st) {
+                        word |= kStart;
+                        lane_start[(i - rs) / kPerLane] = true;
+                    }
+                    if (en) word |= kEnd;
+                    mt[i] = word;
+                }
+                // lane's first entry: does a run start in the lane, and how many
+                // lanes back does its carried-in run begin
+                for (int l = 0; l * kPerLane < re - rs; ++l) {
+                    const int i = rs + l * kPerLane;
+                    if (lane_start[l]) mt[i] |= kLaneStart;
+                    if (!valid(i) || (mt[i] & kStart)) continue;
+                    int dd = 1;
+                    while (l - dd >= 0 && !lane_start[l - dd]) ++dd;
+                    mt[i] |= (uint32_t)dd << kDepthShift;
+                }
+            }
         }
         tiles.push_back(t);
         p = q;

@@ -4,12 +4,14 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspa
 import numpy as np, torch
 import oracle as O
 import paper_2502_16851_b200 as P
+P.library_path = os.environ.get("RL_LIB", P.library_path)
 n, k, hb = 1 << 22, 16, 65536
 rp = torch.empty(n + 1, dtype=torch.int32, device="cuda"); col = torch.empty(n * k, dtype=torch.int32, device="cuda")
 val = torch.empty(n * k, dtype=torch.float64, device="cuda"); x = torch.empty(n, dtype=torch.float64, device="cuda")
 y = torch.empty(n, dtype=torch.float64, device="cuda")
 P.gen_band_csr(n, 0, n, k, hb, 1, rp, col, val); P.fill_uniform(x, 1, 4, 0, 1)
 t0 = time.perf_counter()
+P.tuning_set("spmv_plan_tiled", int(os.environ.get("TILED", "1")))
 plan = P.SpmvPlan(rp.cpu(), col.cpu(), val.cpu(), n)
 print("plan build s", round(time.perf_counter() - t0, 2), "info", plan.info())
 def timeit(fn, reps=20):
