@@ -101,6 +101,19 @@ def stencils():
         torch.cuda.empty_cache()
 
 
+def stencil3d_cc():
+    import math
+    for preset in ("3d7pt", "3d27pt"):
+        u = torch.empty((512, 512, 512), dtype=torch.float64, device="cuda")
+        P.stencil_init(u, 1, 1)
+        v = u.clone()
+        nbytes = 4 * 16 * math.prod(s - 2 for s in u.shape)
+        sweep(f"{preset}_cc", lambda: P.stencil(preset, u, v, 4, unit=0), nbytes,
+              {"stencil_ctas_per_sm": [1, 2, 3, 4, 6, 8], "stencil_rows_per_thread": [2, 4]})
+        del u, v
+        torch.cuda.empty_cache()
+
+
 def stencil_r():
     """2d9pt / 2d13pt / 2d49pt at 16384^2; GB/s of algorithmic bytes and the
     FP64 rate (W = 2 |S| per point)."""
@@ -130,6 +143,8 @@ if __name__ == "__main__":
     for w in sys.argv[1:]:
         if w == "stencil_r":
             stencil_r()
+        elif w == "stencil3d_cc":
+            stencil3d_cc()
         elif w == "stencil":
             stencils()
         elif w == "temporal":
