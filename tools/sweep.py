@@ -114,6 +114,17 @@ def stencil3d_cc():
         torch.cuda.empty_cache()
 
 
+def stencil3d_tc():
+    import math
+    u = torch.empty((512, 512, 512), dtype=torch.float64, device="cuda")
+    P.stencil_init(u, 1, 1)
+    v = u.clone()
+    nbytes = 4 * 16 * math.prod(s - 2 for s in u.shape)
+    sweep("3d27pt_tc", lambda: P.stencil("3d27pt", u, v, 4, unit=1), nbytes,
+          {"stencil_tc3d_mode": [0, 2], "stencil_tc1_ctas_per_sm": [4, 8]})
+    sweep("3d27pt_cc", lambda: P.stencil("3d27pt", u, v, 4, unit=0), nbytes, {})
+
+
 def stencil_r():
     """2d9pt / 2d13pt / 2d49pt at 16384^2; GB/s of algorithmic bytes and the
     FP64 rate (W = 2 |S| per point)."""
@@ -145,6 +156,8 @@ if __name__ == "__main__":
             stencil_r()
         elif w == "stencil3d_cc":
             stencil3d_cc()
+        elif w == "stencil3d_tc":
+            stencil3d_tc()
         elif w == "stencil":
             stencils()
         elif w == "temporal":
