@@ -348,6 +348,46 @@ def per_kernel_table(torch, P, D, hbm):
     return rows
 
 
+def cusparse_yardstick(torch, P, hbm, reps=20):
+    """cuSPARSE (the paper's CC SpMV baseline)
+    is in the image; it is timed here on the same BASELINE matrix as a
+    yardstick only (torch's CSR matvec dispatches to cusparseSpMV).  Never
+    on the product path."""
+    n, k, hb = 1 << 22, 16, 65536
+    rp = torch.empty(n + 1, dtype=torch.int32, device="cuda")
+    col = torch.empty(n * k, dtype=torch.int32, device="cuda")
+    val = torch.empty(n * k, dtype=torch.float64, device="cuda")
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    P.gen_band_csr(n, 0, n, k, hb, SEED, rp, col, val)
+    P.fill_uniform(x, SEED, 4, 0, 1)
+    try:
+        A = torch.sparse_csr_tensor(rp, col, val, size=(n, n))
+        xv = x.view(n, 1)
+        y = None
+        for _ in range(3):
+            y = A @ xv
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            y = A @ xv
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / reps
+        ours = torch.empty(n, dtype=torch.float64, device="cuda")
+        P.spmv_csr(rp, col, val, x, ours)
+        torch.cuda.synchronize()
+        rel = float(torch.linalg.norm(y.view(-1) - ours) / torch.linalg.norm(ours))
+        gbs = P.spmv_csr_model(n, n, n * k).traffic_bytes / (ms * 1e-3) / 1e9
+        out = {"gbs": round(gbs, 1), "frac_of_measured_peak": round(gbs / hbm, 4), "ms": round(ms, 4),
+               "rel_diff_vs_ours": rel, "via": f"torch {torch.__version__} sparse CSR matvec (cuSPARSE)"}
+    except Exception as ex:  # yardstick only: never fail the bench on it
+        out = {"unavailable": f"{type(ex).__name__}: {ex}"[:200]}
+    del rp, col, val, x
+    torch.cuda.empty_cache()
+    return out
+
+
 def temporal_blocking(torch, P, hbm, t1_ms_per_step):
     """2d5pt with temporal depth 2 on the BASELINE grid
     (100 timesteps = 50 fused sweeps).  Model bytes are stencil_model(2d5pt,
@@ -676,6 +716,7 @@ def main():
     if world == 1 and not args.no_per_kernel:
         with ClockSampler(dev_index) as clk2:
             table = per_kernel_table(torch, P, D, hbm)
+            table["spmv"]["cusparse_cc_yardstick"] = cusparse_yardstick(torch, P, hbm)
             line["temporal_blocking"] = temporal_blocking(torch, P, hbm,
                                                           table["2d5pt"]["cc"]["ms_per_unit"])
             line["next_rows"] = {"gemv": gemv_rows(torch, P, hbm), **stencil_preset_rows(torch, P, hbm)}
