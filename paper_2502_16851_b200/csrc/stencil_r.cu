@@ -28,7 +28,9 @@
 //   for the vertical arms).  The band fragments are built once per thread;
 //   the U fragments come from the stage, whose row pitch is 4 mod 16 doubles
 //   so each fragment load is two conflict-free wavefronts.  Per 8x8 tile:
-//   2d9pt 9, 2d13pt 8, 2d49pt 28 DMMA.
+//   2d9pt 9, 2d13pt 8, 2d49pt 28 DMMA; with y-mirror-symmetric box weights
+//   (the defaults) the rows y-dy and y+dy are added before one shared
+//   product, so 2d9pt takes 6 and 2d49pt 16.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -69,7 +71,7 @@ __host__ __device__ constexpr int ksteps() { return (8 + 2 * R + 3) / 4; }  // k
 template <int R, bool TC>
 __host__ __device__ constexpr int pitch() {
     int p = kTXr + 2 * Geo<R>::LP;
-    if (TC) {
+    if (TC || R == 1) {  // the CUDA-core 2d9pt stage measured ~2.5 % faster with the wider box too
         const int need = Geo<R>::LP + 56 - R + 4 * ksteps<R>();
         if (p < need) p = need;
         while (p % 16 != 4) ++p;
@@ -203,18 +205,18 @@ __device__ __forceinline__ void cc_row(const double* T, const StencilDesc& d, do
                 }
             }
         }
-        return;
-    }
-    // dx outer: consecutive DFMAs go to different accumulators
+    } else {
+        // dx outer: consecutive DFMAs go to different accumulators
 #pragma unroll
-    for (int dx = -R; dx <= R; ++dx) {
+        for (int dx = -R; dx <= R; ++dx) {
 #pragma unroll
-        for (int j = 0; j < kRYr; ++j) {
-            const int dy = IR - R - j;
-            if (dy >= -R && dy <= R && has_tap<BOX>(dy, dx)) {
-                const double w = d.w[widx<R, BOX>(dy, dx)];
-                acc[j][0] = fma(w, vv[LP + dx], acc[j][0]);
-                acc[j][1] = fma(w, vv[LP + 1 + dx], acc[j][1]);
+            for (int j = 0; j < kRYr; ++j) {
+                const int dy = IR - R - j;
+                if (dy >= -R && dy <= R && has_tap<BOX>(dy, dx)) {
+                    const double w = d.w[widx<R, BOX>(dy, dx)];
+                    acc[j][0] = fma(w, vv[LP + dx], acc[j][0]);
+                    acc[j][1] = fma(w, vv[LP + 1 + dx], acc[j][1]);
+                }
             }
         }
     }
@@ -267,13 +269,15 @@ __global__ void __launch_bounds__(128) st2dr_tma_cc(const __grid_constant__ CUte
 // ===========================================================================
 // Tensor core
 // ===========================================================================
-template <int R, bool BOX, int S>
+template <int R, bool BOX, bool SYMY, int S>
 __global__ void __launch_bounds__(128) st2dr_tma_tc(const __grid_constant__ CUtensorMap tm, double* __restrict__ v,
                                                     uint64_t nx, uint64_t y_begin, uint64_t y_end, int seg_rows,
                                                     int strips, const __grid_constant__ StencilDesc d) {
     constexpr int LP = Geo<R>::LP, P = pitch<R, true>(), STAGE = stage_doubles<R, true>();
     constexpr int KS = ksteps<R>();
-    constexpr int NDY = BOX ? 2 * R + 1 : 1;   // row offsets with an x-band product
+    // x-band products: one per row offset (box), or one per |dy| when the box
+    // weights are mirror-symmetric in y (U[y-dy] + U[y+dy] share a band)
+    constexpr int NDY = BOX ? (SYMY ? R + 1 : 2 * R + 1) : 1;
     extern __shared__ __align__(128) double smem[];
     RingR<S, STAGE> ring(smem);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -287,7 +291,7 @@ __global__ void __launch_bounds__(128) st2dr_tma_tc(const __grid_constant__ CUte
     double bx[NDY][KS];
 #pragma unroll
     for (int i = 0; i < NDY; ++i) {
-        const int dy = BOX ? i - R : 0;
+        const int dy = BOX ? (SYMY ? i : i - R) : 0;
 #pragma unroll
         for (int s = 0; s < KS; ++s) {
             const int dx = 4 * s + fc - fr - R;
@@ -337,12 +341,14 @@ __global__ void __launch_bounds__(128) st2dr_tma_tc(const __grid_constant__ CUte
                 // x-band products: A = U[8ti + R + dy + fr][LP + 8tj - R + 4s + fc]
 #pragma unroll
                 for (int i = 0; i < NDY; ++i) {
-                    const int dy = BOX ? i - R : 0;
+                    const int dy = BOX ? (SYMY ? i : i - R) : 0;
                     const double* ap = T + (8 * ti + R + dy + fr) * P + (LP + 8 * tj - R + fc);
+                    const double* am = T + (8 * ti + R - dy + fr) * P + (LP + 8 * tj - R + fc);
 #pragma unroll
-                    for (int s = 0; s < KS; ++s)
-                        dmma_m8n8k4(acc[ti][c][0], acc[ti][c][1], ap[4 * s], bx[i][s], acc[ti][c][0],
-                                    acc[ti][c][1]);
+                    for (int s = 0; s < KS; ++s) {
+                        const double a = (SYMY && dy > 0) ? ap[4 * s] + am[4 * s] : ap[4 * s];
+                        dmma_m8n8k4(acc[ti][c][0], acc[ti][c][1], a, bx[i][s], acc[ti][c][0], acc[ti][c][1]);
+                    }
                 }
                 if (!BOX) {
                     // vertical arms: D += Band_y (8 x K) * U[8ti + 4s + fc][LP + 8tj + fr]
@@ -386,6 +392,15 @@ bool x_symmetric(const StencilDesc& d) {
     return true;
 }
 
+// Box weights mirror-symmetric in y (w(dy, dx) == w(-dy, dx), exactly)?
+template <int R>
+bool y_symmetric(const StencilDesc& d) {
+    for (int dy = 1; dy <= R; ++dy)
+        for (int dx = -R; dx <= R; ++dx)
+            if (d.w[widx<R, true>(dy, dx)] != d.w[widx<R, true>(-dy, dx)]) return false;
+    return true;
+}
+
 template <int R, bool BOX>
 cudaError_t launch_r(int unit, const StencilDesc& d, uint64_t o0, uint64_t o1, const double* u, double* v,
                      cudaStream_t s) {
@@ -407,8 +422,13 @@ cudaError_t launch_r(int unit, const StencilDesc& d, uint64_t o0, uint64_t o1, c
     cudaError_t e;
     if (unit == 1) {
         const size_t sm = ring_bytes<R, true, S>();
-        if ((e = prep(st2dr_tma_tc<R, BOX, S>, sm)) != cudaSuccess) return e;
-        st2dr_tma_tc<R, BOX, S><<<grid, 128, sm, s>>>(m, v, d.nx, o0, o1, seg_rows, (int)strips, d);
+        if (BOX && y_symmetric<R>(d) && tuning().stencil_r_sym) {
+            if ((e = prep(st2dr_tma_tc<R, BOX, true, S>, sm)) != cudaSuccess) return e;
+            st2dr_tma_tc<R, BOX, true, S><<<grid, 128, sm, s>>>(m, v, d.nx, o0, o1, seg_rows, (int)strips, d);
+        } else {
+            if ((e = prep(st2dr_tma_tc<R, BOX, false, S>, sm)) != cudaSuccess) return e;
+            st2dr_tma_tc<R, BOX, false, S><<<grid, 128, sm, s>>>(m, v, d.nx, o0, o1, seg_rows, (int)strips, d);
+        }
     } else {
         int st = tuning().stencil_r_cc_stages;
         if (st == 0) st = (R == 3 && BOX) ? 2 : 4;  // 2d49pt: compute-bound, more CTAs beat a deeper ring
@@ -418,7 +438,7 @@ cudaError_t launch_r(int unit, const StencilDesc& d, uint64_t o0, uint64_t o1, c
         if ((e = prep(st2dr_tma_cc<R, BOX, SY, SS>, sm)) != cudaSuccess) return e;                         \
         st2dr_tma_cc<R, BOX, SY, SS><<<grid, 128, sm, s>>>(m, v, d.nx, o0, o1, seg_rows, (int)strips, d); \
     } while (0)
-        if (BOX && R == 3 && x_symmetric<R>(d) && tuning().stencil_r_sym) {
+        if (BOX && x_symmetric<R>(d) && tuning().stencil_r_sym) {
             if (st == 2) RLB_RCC(true, 2); else if (st == 3) RLB_RCC(true, 3); else RLB_RCC(true, 4);
         } else {
             if (st == 2) RLB_RCC(false, 2); else if (st == 3) RLB_RCC(false, 3); else RLB_RCC(false, 4);

@@ -10,6 +10,8 @@ import torch  # noqa: E402
 
 import paper_2502_16851_b200 as P  # noqa: E402
 
+P.library_path = os.environ.get("RL_LIB", P.library_path)
+
 
 def timeit(fn, reps=20, warm=3):
     for _ in range(warm):
@@ -136,15 +138,14 @@ def stencil_r():
         P.stencil_init(u, r, 1)
         v.copy_(u)
         pts = math.prod(s - 2 * r for s in u.shape)
-        for unit, st, cps, sym in ((0, 0, 32, 0), (0, 0, 32, 1), (0, 0, 32, 2), (0, 0, 32, 3), (0, 0, 64, 0),
-                                   (1, 0, 32, 0), (1, 0, 32, 3)):
+        for unit, st, cps, sym in ((0, 0, 32, 0), (0, 0, 32, 1), (0, 3, 32, 1), (0, 2, 32, 1), (1, 0, 32, 1)):
             P.tuning_set("stencil_r_cc_stages", st)
-            promo = sym
-            P.tuning_set("stencil_r_l2promo", promo)
+            P.tuning_set("stencil_r_sym", sym)
+            promo = 1
             P.tuning_set("stencil_r_sym", sym)
             P.tuning_set("stencil_r_ctas_per_sm", cps)
             ms = timeit(lambda: P.stencil(preset, u, v, 2, unit=unit), reps=5) / 2
-            print(json.dumps({"kernel": f"{preset}_{'cc' if unit == 0 else 'tc'}", "stages": st, "ctas_per_sm": cps, "promo": promo,
+            print(json.dumps({"kernel": f"{preset}_{'cc' if unit == 0 else 'tc'}", "stages": st, "ctas_per_sm": cps, "sym": sym,
                               "ms_per_step": round(ms, 4),
                               "gbs": round(16 * pts / ms / 1e6, 1),
                               "tflops": round(2 * npts * pts / ms / 1e9, 2)}), flush=True)
