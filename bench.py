@@ -388,29 +388,35 @@ def cusparse_yardstick(torch, P, hbm, reps=20):
     return out
 
 
-def temporal_blocking(torch, P, hbm, t1_ms_per_step):
-    """2d5pt with temporal depth 2 on the BASELINE grid
-    (100 timesteps = 50 fused sweeps).  Model bytes are stencil_model(2d5pt,
-    FP64, 2): 16 B per point per fused sweep (reference kernels.cpp:137-155)."""
+def temporal_blocking(torch, P, hbm, t1_ms_per_step, depths=(2, 4, 5, 7)):
+    """2d5pt with temporal depth t on the BASELINE grid
+    (100 timesteps = floor(100/t) fused sweeps + the remainder as single
+    steps).  Model bytes are stencil_model(2d5pt, FP64, t): 16 B per point per
+    fused sweep (reference kernels.cpp:137-155)."""
     shape = (16384, 16384)
     u = torch.empty(shape, dtype=torch.float64, device="cuda")
     P.stencil_init(u, 1, SEED)
     v = u.clone()
-    P.stencil_temporal("2d5pt", u, v, 4, 2)
-    torch.cuda.synchronize()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    kc, _ = P.stencil_temporal("2d5pt", u, v, 100, 2)
-    e.record()
-    torch.cuda.synchronize()
-    ms = s.elapsed_time(e)
+    out = {}
+    for t in depths:
+        P.stencil_temporal("2d5pt", u, v, 2 * t, t)
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        kc, _ = P.stencil_temporal("2d5pt", u, v, 100, t)
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e)
+        gbs = kc.traffic_bytes / (ms * 1e-3) / 1e9
+        out[f"2d5pt_t{t}"] = {"ms_per_timestep": round(ms / 100, 4), "model_gbs": round(gbs, 1),
+                              "frac_of_measured_peak": round(gbs / hbm, 4),
+                              "timestep_speedup_vs_t1": round(t1_ms_per_step / (ms / 100), 3)}
     del u, v
     torch.cuda.empty_cache()
-    gbs = kc.traffic_bytes / (ms * 1e-3) / 1e9
-    return {"2d5pt_t2": {"ms_per_timestep": round(ms / 100, 4), "model_gbs": round(gbs, 1),
-                         "frac_of_measured_peak": round(gbs / hbm, 4),
-                         "timestep_speedup_vs_t1": round(t1_ms_per_step / (ms / 100), 3),
-                         "note": "50 fused sweeps of 2 timesteps; bytes = stencil_model(t=2)"}}
+    out["note"] = ("register-pipelined kernel (stencil_tb.cu): one HBM read + write per t timesteps; "
+                   "bytes = stencil_model(t) per fused sweep, so model_gbs falls as t rises while the "
+                   "per-timestep time drops")
+    return out
 
 
 def gemv_rows(torch, P, hbm, reps=10):

@@ -209,13 +209,14 @@ KernelCharacterization stencil_temporal(ExecutionUnit unit, Precision p, const S
     require_ptr(u, "u");
     require_ptr(v, "v");
     if (u == v) throw Error(ErrorKind::ValidationError, "u and v must be distinct buffers");
-    if (t > 2) throw Error(ErrorKind::InvalidRange, "temporal depth > 2 is not implemented");
+    if (t > 8) throw Error(ErrorKind::InvalidRange, "temporal depth > 8 is not implemented");
     const rlb::StencilDesc d = make_desc(shape, dims, weights);
-    if (t == 2 && (unit != ExecutionUnit::CudaCore || d.preset != rlb::kP2d5 ||
-                   !rlb::stencil_tma_eligible(d, u, v)))
+    const bool use_tb = t >= 2 && rlb::tuning().stencil_tb && rlb::stencil_tb_supported(d, (int)t, u, v);
+    if (t >= 2 && (unit != ExecutionUnit::CudaCore || d.preset != rlb::kP2d5 ||
+                   (!use_tb && !(t == 2 && rlb::stencil_tma_eligible(d, u, v)))))
         throw Error(ErrorKind::ValidationError,
-                    "temporal depth 2 is implemented for 2d5pt on the CUDA core with even nx and "
-                    "16-byte aligned rows");
+                    "temporal depth >= 2 is implemented for 2d5pt on the CUDA core (even depths need an "
+                    "even nx and 16-byte aligned rows)");
     const std::uint64_t fused = steps / t, rem = steps % t;
     const unsigned __int128 pts = interior_points(d);
     const unsigned __int128 w = pts * ((unsigned __int128)fused * kt.work_flops + (unsigned __int128)rem * k1.work_flops);
@@ -227,9 +228,10 @@ KernelCharacterization stencil_temporal(ExecutionUnit unit, Precision p, const S
     for (std::uint64_t i = 0; i < fused + rem; ++i, ++sweeps) {
         const double* src = (sweeps & 1) ? v : u;
         double* dst = (sweeps & 1) ? u : v;
-        if (i < fused && t == 2) {
-            const std::uint64_t lo = std::max<std::uint64_t>(1, 0), hi = outer - 1;
-            cuda_check(rlb::launch_stencil_tma_t2(d, lo, hi, src, dst, s), "stencil (temporal depth 2)");
+        if (i < fused && use_tb) {
+            cuda_check(rlb::launch_stencil_tb(d, (int)t, 1, outer - 1, src, dst, s), "stencil (temporal blocking)");
+        } else if (i < fused && t == 2) {
+            cuda_check(rlb::launch_stencil_tma_t2(d, 1, outer - 1, src, dst, s), "stencil (temporal depth 2)");
         } else {
             sweep(unit, d, 0, outer, src, dst, s);
         }
@@ -1034,6 +1036,8 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         else if (k == "spmv_plan_graph") slot = &t.spmv_plan_graph;
         else if (k == "spmv_plan_taper") slot = &t.spmv_plan_taper;
         else if (k == "stencil_r_ctas_per_sm") slot = &t.stencil_r_ctas_per_sm;
+        else if (k == "stencil_tb_waves") slot = &t.stencil_tb_waves;
+        else if (k == "stencil_tb") slot = &t.stencil_tb;
         else if (k == "stencil_r_cc_stages") slot = &t.stencil_r_cc_stages;
         else if (k == "stencil_r_sym") slot = &t.stencil_r_sym;
         else if (k == "stencil_r_l2promo") slot = &t.stencil_r_l2promo;

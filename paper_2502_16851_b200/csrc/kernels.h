@@ -43,6 +43,8 @@ struct Tuning {
     int stencil_tc1_ctas_per_sm = 8;   // ... partial-sum mode
     int stencil_r_cc_stages = 0;       // ... CUDA-core ring depth: 2-4, 0 = auto (2 for 2d49pt -> 4 CTAs/SM, else 4)
     int stencil_r_ctas_per_sm = 32;
+    int stencil_tb_waves = 4;          // register temporal blocking: grid = this many waves of resident warps
+    int stencil_tb = 1;                // 1: temporal depth t >= 2 runs the register kernel (0: smem t=2 kernel)
     int stencil_r_l2promo = 1;         // ... TMA L2 promotion (0 none, 1 64 B, 2 128 B, 3 256 B)
     int stencil_r_sym = 1;             // 2d49pt CC: pair mirror-symmetric columns (fewer FP64 ops)    // 2d9pt/2d13pt/2d49pt TMA kernels: row segments so the grid is this deep
 };
@@ -86,6 +88,11 @@ cudaError_t launch_stencil_r(int unit, const StencilDesc& d, uint64_t o0, uint64
 bool tma_encode_available();
 bool encode_map_2d(void* map, const double* base, uint64_t nx, uint64_t ny, uint32_t box_x, uint32_t box_y,
                    int l2_promotion = 3);  // 0 none, 1 64 B, 2 128 B, 3 256 B
+
+// 2d5pt with temporal depth t (2..8) in registers (stencil_tb.cu).
+bool stencil_tb_supported(const StencilDesc& d, int t, const double* u, const double* v);
+cudaError_t launch_stencil_tb(const StencilDesc& d, int t, uint64_t o0, uint64_t o1, const double* u, double* v,
+                              cudaStream_t s);
 
 // Two fused timesteps of 2d5pt (temporal blocking, CUDA core, TMA-eligible grids).
 cudaError_t launch_stencil_tma_t2(const StencilDesc& d, uint64_t o0, uint64_t o1, const double* u,

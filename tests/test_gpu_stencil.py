@@ -243,6 +243,40 @@ def test_2d5pt_temporal_depth2(cuda, shape, steps):
     assert kc.work_flops == pts * (fused * 20 + rem * 10)
 
 
+@pytest.mark.parametrize("t", [2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("shape", [(20, 24), (65, 130), (301, 517), (513, 1026)])
+@pytest.mark.parametrize("kernel", [0, 1])
+def test_2d5pt_temporal_depth_t(cuda, t, shape, kernel):
+    """Temporal depth t (register kernel; kernel 0 = the smem t = 2 kernel
+    where it applies) equals t * k single timesteps, with custom weights,
+    odd and even nx (odd depths only run the scalar-load path), and an
+    untouched Dirichlet ring."""
+    import torch
+
+    if kernel == 0 and (t != 2 or shape[1] % 2):
+        pytest.skip("the shared-memory kernel is t = 2 with even nx only")
+    if t % 2 == 0 and shape[1] % 2:
+        pytest.skip("even depths need 16-byte rows")
+    P.tuning_set("stencil_tb", kernel)
+    try:
+        u0 = O.stencil_init(shape, 1, 23)
+        w = np.array([0.4, 0.2, 0.1, 0.17, 0.13])
+        steps = 2 * t + 1
+        u = torch.from_numpy(u0.copy()).cuda()
+        v = torch.from_numpy(u0.copy()).cuda()
+        kc, out = P.stencil_temporal("2d5pt", u, v, steps, t, weights=w)
+        torch.cuda.synchronize()
+        ref = O.stencil("2d5pt", u0, steps, w)
+        got = out.cpu().numpy()
+        assert O.rel_err(got, ref) <= TOL
+        ring = _ring_mask(shape, 1)
+        assert O.bit_mismatches(got[ring], u0[ring]) == 0
+        pts = (shape[0] - 2) * (shape[1] - 2)
+        assert kc.traffic_bytes == 16 * pts * 3  # 2 fused sweeps + 1 single step
+    finally:
+        P.tuning_set("stencil_tb", 1)
+
+
 def test_temporal_depth_restrictions(cuda):
     import torch
 

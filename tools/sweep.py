@@ -86,6 +86,27 @@ def temporal():
           {"stencil_t2_ctas_per_sm": [8, 12, 16, 24, 32, 48]})
 
 
+def temporal_t():
+    """2d5pt at 16384^2: ms per timestep for temporal depth 1..8 (register
+    kernel), plus the shared-memory t = 2 kernel."""
+    u = torch.empty((16384, 16384), dtype=torch.float64, device="cuda")
+    P.stencil_init(u, 1, 1)
+    v = u.clone()
+    waves_list = [int(x) for x in os.environ.get("TB_WAVES", "1").split(",")]
+    cases = [(1, 1, 1), (2, 0, 1)] + [(t, 1, w) for t in range(2, 9) for w in waves_list]
+    for t, tb, waves in cases:
+        P.tuning_set("stencil_tb", tb)
+        P.tuning_set("stencil_tb_waves", waves)
+        steps = 8 * t
+        fn = (lambda: P.stencil("2d5pt", u, v, steps)) if t == 1 else \
+            (lambda: P.stencil_temporal("2d5pt", u, v, steps, t))
+        ms = timeit(fn, reps=5, warm=2) / steps
+        print(json.dumps({"kernel": "2d5pt_temporal", "t": t, "register_kernel": tb, "waves": waves,
+                          "ms_per_timestep": round(ms, 4),
+                          "timestep_gbs_equiv": round(16 * 16382 ** 2 / ms / 1e6, 1)}), flush=True)
+    P.tuning_set("stencil_tb", 1)
+
+
 def stencils():
     import math
     for preset, shape in (("2d5pt", (16384, 16384)), ("3d7pt", (512, 512, 512)), ("3d27pt", (512, 512, 512))):
@@ -124,6 +145,8 @@ def stencil3d_tc():
     nbytes = 4 * 16 * math.prod(s - 2 for s in u.shape)
     sweep("3d27pt_tc", lambda: P.stencil("3d27pt", u, v, 4, unit=1), nbytes,
           {"stencil_tc3d_mode": [0, 2], "stencil_tc1_ctas_per_sm": [4, 8]})
+    sweep("3d7pt_tc", lambda: P.stencil("3d7pt", u, v, 4, unit=1), nbytes,
+          {"stencil_tc3d_mode": [2], "stencil_tc3d_ctas_per_sm": [6, 8, 12, 16, 24, 8]})
     sweep("3d27pt_cc", lambda: P.stencil("3d27pt", u, v, 4, unit=0), nbytes, {})
 
 
@@ -163,6 +186,8 @@ if __name__ == "__main__":
             stencils()
         elif w == "temporal":
             temporal()
+        elif w == "temporal_t":
+            temporal_t()
         elif w == "gemv":
             gemv()
         else:
