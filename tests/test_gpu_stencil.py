@@ -287,6 +287,12 @@ def test_temporal_depth_restrictions(cuda):
     with pytest.raises(P.RooflensError) as e:
         P.stencil_temporal("2d5pt", u[0], u[1].clone(), 4, 0)
     assert e.value.kind == "InvalidCount"
+    with pytest.raises(P.RooflensError) as e:
+        P.stencil_temporal("2d5pt", u[0], u[1].clone(), 18, 9)
+    assert e.value.kind == "InvalidRange"
+    with pytest.raises(P.RooflensError) as e:
+        P.stencil_temporal("2d5pt", u[0], u[1].clone(), 4, 2, unit=P.TENSOR_CORE)
+    assert e.value.kind == "ValidationError"
 
 
 @pytest.mark.parametrize("mode", [0, 3])
