@@ -8,8 +8,9 @@ report.hpp:19-48, SPEC.md:447-516).
             [--format text|json|csv]
     python -m paper_2502_16851_b200.cli matrix --hw NAME FILE.mtx ...
     python -m paper_2502_16851_b200.cli roofline --hw NAME --out FILE.csv|FILE.svg [--points K]
-    python -m paper_2502_16851_b200.cli measure --kernel scale|spmv-csr|2d5pt|3d7pt|3d27pt
-            [--unit cc|tc] [--reps R]          (runs the sm_100a kernel; needs a GPU)
+    python -m paper_2502_16851_b200.cli measure --kernel scale|gemv|spmv-csr|2d5pt|2d9pt|2d13pt|2d49pt|
+            3d7pt|3d27pt [--unit cc|tc] [--reps R] [--t T (2d5pt)] [--mtx FILE.mtx (spmv-csr)]
+            (runs the sm_100a kernel; needs a GPU)
 
 Exit codes (SPEC.md cli_report): 0 success, 1 usage error, 2 input/parse error,
 3 internal invariant violation.  Every analysis number comes from the C-ABI
@@ -269,12 +270,45 @@ def cmd_measure(args, out):
     and the TC/CC bound of the measured B200 spec."""
     import torch
 
-    from . import fill_uniform, gen_band_csr, scale, spmv_csr, stencil, stencil_init
+    from . import (fill_uniform, gemv, gen_band_csr, mtx_read_csr, scale, spmv_csr, stencil, stencil_init,
+                   stencil_temporal)
 
     unit = CUDA_CORE if args.unit == "cc" else TENSOR_CORE
     spec = measured_b200()
     k = args.kernel
-    if k == "scale":
+    if args.mtx:
+        if k != "spmv-csr":
+            raise UsageError("--mtx goes with --kernel spmv-csr")
+        rp_h, col_h, val_h, ncols = mtx_read_csr(args.mtx)
+        rp, col, val = (torch.from_numpy(a).cuda() for a in (rp_h, col_h, val_h))
+        x = torch.empty(ncols, dtype=torch.float64, device="cuda")
+        y = torch.empty(rp_h.size - 1, dtype=torch.float64, device="cuda")
+        fill_uniform(x, 1, 4, 0, 1)
+        fn = lambda: spmv_csr(rp, col, val, x, y, unit=unit)
+        k = f"spmv-csr:{os.path.basename(args.mtx)}"
+    elif args.t and args.t > 1:
+        if k != "2d5pt":
+            raise UsageError("--t (temporal depth) is implemented for 2d5pt")
+        u = torch.empty((16384, 16384), dtype=torch.float64, device="cuda")
+        stencil_init(u, 1, 1)
+        v = u.clone()
+        fn = lambda: stencil_temporal("2d5pt", u, v, args.t, args.t, unit=unit)[0]
+        k = f"2d5pt:t={args.t}"
+    elif k == "gemv":
+        m, n = args.m or 16384, args.n or 65536
+        A = torch.empty((m, n), dtype=torch.float64, device="cuda")
+        fill_uniform(A.view(-1), 1, 6, 0, 1)
+        x = torch.empty(n, dtype=torch.float64, device="cuda")
+        fill_uniform(x, 1, 4, 0, 1)
+        y = torch.empty(m, dtype=torch.float64, device="cuda")
+        fn = lambda: gemv(A, x, y, unit=unit)
+    elif k in ("2d9pt", "2d13pt", "2d49pt"):
+        u = torch.empty((16384, 16384), dtype=torch.float64, device="cuda")
+        stencil_init(u, stencil_preset(k)[2], 1)
+        v = u.clone()
+        preset = k
+        fn = lambda: stencil(preset, u, v, 1, unit=unit)
+    elif k == "scale":
         n = args.n or (1 << 27)
         b = torch.empty(n, dtype=torch.float64, device="cuda")
         fill_uniform(b, 1, 1, 0, 1)
@@ -352,6 +386,9 @@ def main(argv=None, out=None) -> int:
     me.add_argument("--kernel", required=True)
     me.add_argument("--unit", default="cc", choices=["cc", "tc"])
     me.add_argument("--n", type=int)
+    me.add_argument("--m", type=int)
+    me.add_argument("--t", type=int, help="temporal depth (2d5pt, CUDA core)")
+    me.add_argument("--mtx", help="Matrix Market file for --kernel spmv-csr")
     me.add_argument("--reps", type=int, default=20)
     me.add_argument("--format", dest="format", default=None, choices=["text", "json"])
     try:

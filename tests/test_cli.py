@@ -3,6 +3,8 @@ import csv
 import io
 import json
 
+import numpy as np
+
 import pytest
 
 import paper_2502_16851_b200 as P
@@ -95,3 +97,29 @@ def test_measure_runs_kernel(cuda):
     rc, txt = run("measure", "--kernel", "scale", "--n", str(1 << 24), "--reps", "3", "--format", "json")
     rep = json.loads(txt)
     assert rc == 0 and rep["measured"]["gbs"] > 100
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("argv", [
+    ("--kernel", "gemv", "--m", "2048", "--n", "8192"),
+    ("--kernel", "2d49pt", "--unit", "tc"),
+    ("--kernel", "2d5pt", "--t", "5"),
+])
+def test_measure_next_rows(cuda, argv):
+    rc, txt = run("measure", *argv, "--reps", "2", "--format", "json")
+    rep = json.loads(txt)
+    assert rc == 0 and rep["measured"]["gbs"] > 100 and rep["kernel"]["traffic_bytes"] > 0
+
+
+@pytest.mark.gpu
+def test_measure_mtx_file(cuda, tmp_path):
+    import scipy.io
+    import scipy.sparse as sp
+
+    path = tmp_path / "a.mtx"
+    scipy.io.mmwrite(str(path), sp.random(3000, 3000, density=0.01, format="coo",
+                                          random_state=np.random.default_rng(0)))
+    rc, txt = run("measure", "--kernel", "spmv-csr", "--mtx", str(path), "--reps", "2", "--format", "json")
+    rep = json.loads(txt)
+    assert rc == 0 and rep["kernel"]["name"] == "spmv-csr:a.mtx"
+    assert run("measure", "--kernel", "scale", "--mtx", str(path))[0] == 1
