@@ -212,11 +212,12 @@ KernelCharacterization stencil_temporal(ExecutionUnit unit, Precision p, const S
     if (t > 8) throw Error(ErrorKind::InvalidRange, "temporal depth > 8 is not implemented");
     const rlb::StencilDesc d = make_desc(shape, dims, weights);
     const bool use_tb = t >= 2 && rlb::tuning().stencil_tb && rlb::stencil_tb_supported(d, (int)t, u, v);
-    if (t >= 2 && (unit != ExecutionUnit::CudaCore || d.preset != rlb::kP2d5 ||
-                   (!use_tb && !(t == 2 && rlb::stencil_tma_eligible(d, u, v)))))
+    const bool use_tb3 = t >= 2 && rlb::stencil_tb3_supported(d, (int)t);
+    const bool ok2d = d.preset == rlb::kP2d5 && (use_tb || (t == 2 && rlb::stencil_tma_eligible(d, u, v)));
+    if (t >= 2 && (unit != ExecutionUnit::CudaCore || !(ok2d || use_tb3)))
         throw Error(ErrorKind::ValidationError,
-                    "temporal depth >= 2 is implemented for 2d5pt on the CUDA core (even depths need an "
-                    "even nx and 16-byte aligned rows)");
+                    "temporal depth >= 2 is implemented on the CUDA core for 2d5pt (t <= 8; even depths need "
+                    "an even nx and 16-byte aligned rows) and 3d7pt (t <= 4)");
     const std::uint64_t fused = steps / t, rem = steps % t;
     const unsigned __int128 pts = interior_points(d);
     const unsigned __int128 w = pts * ((unsigned __int128)fused * kt.work_flops + (unsigned __int128)rem * k1.work_flops);
@@ -228,7 +229,9 @@ KernelCharacterization stencil_temporal(ExecutionUnit unit, Precision p, const S
     for (std::uint64_t i = 0; i < fused + rem; ++i, ++sweeps) {
         const double* src = (sweeps & 1) ? v : u;
         double* dst = (sweeps & 1) ? u : v;
-        if (i < fused && use_tb) {
+        if (i < fused && use_tb3) {
+            cuda_check(rlb::launch_stencil_tb3(d, (int)t, 1, outer - 1, src, dst, s), "stencil (3D temporal blocking)");
+        } else if (i < fused && use_tb) {
             cuda_check(rlb::launch_stencil_tb(d, (int)t, 1, outer - 1, src, dst, s), "stencil (temporal blocking)");
         } else if (i < fused && t == 2) {
             cuda_check(rlb::launch_stencil_tma_t2(d, 1, outer - 1, src, dst, s), "stencil (temporal depth 2)");

@@ -94,6 +94,11 @@ bool stencil_tb_supported(const StencilDesc& d, int t, const double* u, const do
 cudaError_t launch_stencil_tb(const StencilDesc& d, int t, uint64_t o0, uint64_t o1, const double* u, double* v,
                               cudaStream_t s);
 
+// 3d7pt with temporal depth t (2..4): z-marching register pipeline (stencil_tb3.cu).
+bool stencil_tb3_supported(const StencilDesc& d, int t);
+cudaError_t launch_stencil_tb3(const StencilDesc& d, int t, uint64_t o0, uint64_t o1, const double* u, double* v,
+                               cudaStream_t s);
+
 // Two fused timesteps of 2d5pt (temporal blocking, CUDA core, TMA-eligible grids).
 cudaError_t launch_stencil_tma_t2(const StencilDesc& d, uint64_t o0, uint64_t o1, const double* u,
                                   double* v, cudaStream_t s);

@@ -277,12 +277,36 @@ def test_2d5pt_temporal_depth_t(cuda, t, shape, kernel):
         P.tuning_set("stencil_tb", 1)
 
 
+@pytest.mark.parametrize("t", [2, 3, 4])
+@pytest.mark.parametrize("shape", [(9, 10, 11), (20, 24, 68), (33, 40, 70), (64, 50, 97)])
+def test_3d7pt_temporal_depth_t(cuda, t, shape):
+    """3d7pt temporal depth t (z-marching register pipeline) equals single
+    timesteps; custom weights; the Dirichlet shell stays bit-exact."""
+    import torch
+
+    u0 = O.stencil_init(shape, 1, 29)
+    w = np.array([0.3, 0.12, 0.08, 0.11, 0.14, 0.1, 0.15])
+    steps = 2 * t + 1
+    u = torch.from_numpy(u0.copy()).cuda()
+    v = torch.from_numpy(u0.copy()).cuda()
+    kc, out = P.stencil_temporal("3d7pt", u, v, steps, t, weights=w)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    assert O.rel_err(got, O.stencil("3d7pt", u0, steps, w)) <= TOL
+    ring = _ring_mask(shape, 1)
+    assert O.bit_mismatches(got[ring], u0[ring]) == 0
+    assert kc.traffic_bytes == 16 * int(np.prod([s - 2 for s in shape])) * 3
+
+
 def test_temporal_depth_restrictions(cuda):
     import torch
 
     u = torch.zeros((20, 24, 64), dtype=torch.float64, device="cuda")
     with pytest.raises(P.RooflensError) as e:
-        P.stencil_temporal("3d7pt", u, u.clone(), 4, 2)
+        P.stencil_temporal("3d27pt", u, u.clone(), 4, 2)
+    assert e.value.kind == "ValidationError"
+    with pytest.raises(P.RooflensError) as e:
+        P.stencil_temporal("3d7pt", u, u.clone(), 10, 5)
     assert e.value.kind == "ValidationError"
     with pytest.raises(P.RooflensError) as e:
         P.stencil_temporal("2d5pt", u[0], u[1].clone(), 4, 0)

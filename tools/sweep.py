@@ -107,6 +107,24 @@ def temporal_t():
     P.tuning_set("stencil_tb", 1)
 
 
+def temporal_3d():
+    """3d7pt at 512^3: ms per timestep for temporal depth 1..4."""
+    u = torch.empty((512, 512, 512), dtype=torch.float64, device="cuda")
+    P.stencil_init(u, 1, 1)
+    v = u.clone()
+    waves_list = [int(x) for x in os.environ.get("TB_WAVES", "4").split(",")]
+    for t in (1, 2, 3, 4):
+        for waves in (waves_list if t > 1 else [1]):
+            P.tuning_set("stencil_tb_waves", waves)
+            steps = 4 * t
+            fn = (lambda: P.stencil("3d7pt", u, v, steps)) if t == 1 else \
+                (lambda: P.stencil_temporal("3d7pt", u, v, steps, t))
+            ms = timeit(fn, reps=5, warm=2) / steps
+            print(json.dumps({"kernel": "3d7pt_temporal", "t": t, "waves": waves, "ms_per_timestep": round(ms, 4),
+                              "timestep_gbs_equiv": round(16 * 510 ** 3 / ms / 1e6, 1)}), flush=True)
+    P.tuning_set("stencil_tb_waves", 4)
+
+
 def stencils():
     import math
     for preset, shape in (("2d5pt", (16384, 16384)), ("3d7pt", (512, 512, 512)), ("3d27pt", (512, 512, 512))):
@@ -188,6 +206,8 @@ if __name__ == "__main__":
             temporal()
         elif w == "temporal_t":
             temporal_t()
+        elif w == "temporal_3d":
+            temporal_3d()
         elif w == "gemv":
             gemv()
         else:
