@@ -360,6 +360,9 @@ def main(argv=None, out=None) -> int:
     out = out or sys.stdout
     ap = argparse.ArgumentParser(prog="rooflens-b200")
     ap.add_argument("--format", default="text", choices=["text", "json", "csv"])
+    # SPEC.md cli_report global flag; this build (like the reference's spec
+    # slice, hardware.hpp:43-58) carries FP64 peaks only
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32", "fp16"])
     sub = ap.add_subparsers(dest="cmd", required=True)
     h = sub.add_parser("hardware")
     h.add_argument("action", choices=["list", "show"])
@@ -397,6 +400,9 @@ def main(argv=None, out=None) -> int:
         return 0 if e.code == 0 else 1
     if getattr(args, "format", None) is None:
         args.format = "text"
+    if args.precision != "fp64":
+        print(f"ValidationError: precision {args.precision} is not supported (FP64 only)", file=sys.stderr)
+        return 2
     try:
         return {"hardware": cmd_hardware, "analyze": cmd_analyze, "matrix": cmd_matrix,
                 "roofline": cmd_roofline, "measure": cmd_measure}[args.cmd](args, out)

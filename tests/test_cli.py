@@ -123,3 +123,8 @@ def test_measure_mtx_file(cuda, tmp_path):
     rep = json.loads(txt)
     assert rc == 0 and rep["kernel"]["name"] == "spmv-csr:a.mtx"
     assert run("measure", "--kernel", "scale", "--mtx", str(path))[0] == 1
+
+
+def test_precision_flag():
+    assert run("--precision", "fp64", "hardware", "list")[0] == 0
+    assert run("--precision", "fp32", "hardware", "list")[0] == 2
