@@ -142,6 +142,18 @@ def stencils():
         torch.cuda.empty_cache()
 
 
+def stencil2d():
+    import math
+    u = torch.empty((16384, 16384), dtype=torch.float64, device="cuda")
+    P.stencil_init(u, 1, 1)
+    v = u.clone()
+    nbytes = 4 * 16 * math.prod(s - 2 for s in u.shape)
+    sweep("2d5pt_tc", lambda: P.stencil("2d5pt", u, v, 4, unit=1), nbytes,
+          {"stencil_tc_ctas_per_sm": [1, 2, 3, 4, 6, 8]})
+    sweep("2d5pt_cc", lambda: P.stencil("2d5pt", u, v, 4, unit=0), nbytes,
+          {"stencil_ctas_per_sm": [1, 2, 4], "stencil2d_rows_per_thread": [2, 4, 8]})
+
+
 def stencil3d_cc():
     import math
     for preset in ("3d7pt", "3d27pt"):
@@ -196,6 +208,8 @@ if __name__ == "__main__":
     for w in sys.argv[1:]:
         if w == "stencil_r":
             stencil_r()
+        elif w == "stencil2d":
+            stencil2d()
         elif w == "stencil3d_cc":
             stencil3d_cc()
         elif w == "stencil3d_tc":
