@@ -1014,18 +1014,21 @@ cudaError_t launch_stencil_tma(int unit, const StencilDesc& d, uint64_t o0, uint
         if (tk == 0) RLB_TC3(0); else if (tk == 1) RLB_TC3(1); else RLB_TC3(2);
 #undef RLB_TC3
     } else {
-        constexpr int S = 4;
-        const size_t sm = ring_bytes<S, kBX>();
         const int ry = tuning().stencil_rows_per_thread;
-#define RLB_CC3(K, R)                                                                                     \
-    do {                                                                                                  \
-        if ((e = prep(st3d_tma_cc<K, S, R>, sm)) != cudaSuccess) return e;                               \
-        st3d_tma_cc<K, S, R><<<grid, 64 * kTY / R, sm, s>>>(m, v, dd, o0, o1, zchunk, tiles_x, tiles_xy); \
+        const int st = tuning().stencil3d_cc_stages;
+#define RLB_CC3(K, R, SS)                                                                                  \
+    do {                                                                                                   \
+        const size_t sm = ring_bytes<SS, kBX>();                                                           \
+        if ((e = prep(st3d_tma_cc<K, SS, R>, sm)) != cudaSuccess) return e;                               \
+        st3d_tma_cc<K, SS, R><<<grid, 64 * kTY / R, sm, s>>>(m, v, dd, o0, o1, zchunk, tiles_x, tiles_xy); \
     } while (0)
+#define RLB_CC3S(K, R) \
+    do { if (st == 6) RLB_CC3(K, R, 6); else if (st == 8) RLB_CC3(K, R, 8); else RLB_CC3(K, R, 4); } while (0)
 #define RLB_CC3K(K) \
-    do { if (ry == 2) RLB_CC3(K, 2); else if (ry == 4) RLB_CC3(K, 4); else RLB_CC3(K, 8); } while (0)
+    do { if (ry == 2) RLB_CC3S(K, 2); else if (ry == 4) RLB_CC3S(K, 4); else RLB_CC3S(K, 8); } while (0)
         if (kind == 0) RLB_CC3K(0); else if (kind == 1) RLB_CC3K(1); else RLB_CC3K(2);
 #undef RLB_CC3K
+#undef RLB_CC3S
 #undef RLB_CC3
     }
     note_launch();
