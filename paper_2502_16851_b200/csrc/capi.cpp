@@ -608,11 +608,15 @@ void plan_execute_host(rl_spmv_plan_s* pl, const double* x, double* y) {
     // (x, y) pair), so the ~60 copies, waits and launches cost one launch of
     // host time instead of pacing the copy engines.
     if (!trace && !y_direct && rlb::tuning().spmv_plan_graph) {
-        if (pl->gexec && (pl->gx != x || pl->gy != y)) {
+        // the cached graph is replayed only for the same pointers, still
+        // page-locked (a buffer freed and re-allocated pageable at the same
+        // address takes the eager path)
+        const bool pinned = pinned_host(x) && pinned_host(y);
+        if (pl->gexec && (pl->gx != x || pl->gy != y || !pinned)) {
             cudaGraphExecDestroy(pl->gexec);
             pl->gexec = nullptr;
         }
-        if (!pl->gexec && pinned_host(x) && pinned_host(y)) {
+        if (!pl->gexec && pinned) {
             const uint64_t before = rlb::g_launches.load();
             ck(cudaStreamBeginCapture(pl->s_in, cudaStreamCaptureModeThreadLocal), "graph capture");
             cudaGraph_t g = nullptr;
