@@ -702,6 +702,18 @@ __global__ void __launch_bounds__(128) st3d_tma_tc1(const __grid_constant__ CUte
             f2[kb] = bandv(kk, r, d.w[3], d.w[2], d.w[3]);  // g3 g2 g3
         }
     }
+    // KIND 3: the class products concatenated along K (K = 10 + 10 -> 5
+    // k-steps): P_0 = [a | b] * [B(g1,g0,g1); B(g2,g1,g2)] and
+    // P_+-1 = [a | b] * [B(g2,g1,g2); B(g3,g2,g3)], 10 DMMA per tile, not 12
+    double h0[KIND == 3 ? 5 : 1], h1[KIND == 3 ? 5 : 1];
+    if (KIND == 3) {
+#pragma unroll
+        for (int s5 = 0; s5 < 5; ++s5) {
+            const int kk = 4 * s5 + c;
+            h0[s5] = kk < 10 ? bandv(kk, r, d.w[1], d.w[0], d.w[1]) : bandv(kk - 10, r, d.w[2], d.w[1], d.w[2]);
+            h1[s5] = kk < 10 ? bandv(kk, r, d.w[2], d.w[1], d.w[2]) : bandv(kk - 10, r, d.w[3], d.w[2], d.w[3]);
+        }
+    }
     double gen[KIND == 2 ? 27 : 1];
     if (KIND == 2) {
 #pragma unroll
@@ -745,6 +757,23 @@ __global__ void __launch_bounds__(128) st3d_tma_tc1(const __grid_constant__ CUte
                 p0[t][0] = d0; p0[t][1] = d1;
                 pm[t][0] = d.w[1] * z0; pm[t][1] = d.w[1] * z1;
                 pp[t][0] = d.w[2] * z0; pp[t][1] = d.w[2] * z1;
+            } else if (KIND == 3) {
+                double e0 = 0.0, e1 = 0.0, g0 = 0.0, g1 = 0.0;
+#pragma unroll
+                for (int s5 = 0; s5 < 5; ++s5) {
+                    const int kk = 4 * s5 + c;
+                    double av;
+                    if (kk < 10) {
+                        av = P[at(8 * rb + r + 1, 8 * cb + kk)];
+                    } else {
+                        const int k2 = kk - 10;
+                        av = P[at(8 * rb + r, 8 * cb + k2)] + P[at(8 * rb + r + 2, 8 * cb + k2)];
+                    }
+                    dmma_m8n8k4(e0, e1, av, h0[s5], e0, e1);  // P_0
+                    dmma_m8n8k4(g0, g1, av, h1[s5], g0, g1);  // P_+-1
+                }
+                p0[t][0] = e0; p0[t][1] = e1;
+                pm[t][0] = pp[t][0] = g0; pm[t][1] = pp[t][1] = g1;
             } else if (KIND == 1) {
                 double e0 = 0.0, e1 = 0.0, g0 = 0.0, g1 = 0.0;
 #pragma unroll
@@ -994,13 +1023,13 @@ cudaError_t launch_stencil_tma(int unit, const StencilDesc& d, uint64_t o0, uint
     if (tc_onepl) {
         constexpr int S = 4;
         const size_t sm = ring_bytes<S, kBX>();
-        const int tk = kind == 0 ? 0 : (kind == 2 ? 1 : 2);
+        const int tk = kind == 0 ? 0 : (kind == 2 ? (tuning().stencil_tc_concat ? 3 : 1) : 2);
 #define RLB_TC1(K)                                                                             \
     do {                                                                                       \
         if ((e = prep(st3d_tma_tc1<K, S>, sm)) != cudaSuccess) return e;                      \
         st3d_tma_tc1<K, S><<<grid, 128, sm, s>>>(m, v, dd, o0, o1, zchunk, tiles_x, tiles_xy); \
     } while (0)
-        if (tk == 0) RLB_TC1(0); else if (tk == 1) RLB_TC1(1); else RLB_TC1(2);
+        if (tk == 0) RLB_TC1(0); else if (tk == 1) RLB_TC1(1); else if (tk == 3) RLB_TC1(3); else RLB_TC1(2);
 #undef RLB_TC1
     } else if (unit == 1) {
         constexpr int S = 5;

@@ -174,7 +174,7 @@ def stencil3d_tc():
     v = u.clone()
     nbytes = 4 * 16 * math.prod(s - 2 for s in u.shape)
     sweep("3d27pt_tc", lambda: P.stencil("3d27pt", u, v, 4, unit=1), nbytes,
-          {"stencil_tc3d_mode": [0, 2], "stencil_tc1_ctas_per_sm": [4, 8]})
+          {"stencil_tc_concat": [0, 1, 0, 1], "stencil_tc1_ctas_per_sm": [4, 8]})
     sweep("3d7pt_tc", lambda: P.stencil("3d7pt", u, v, 4, unit=1), nbytes,
           {"stencil_tc3d_mode": [2], "stencil_tc3d_ctas_per_sm": [6, 8, 12, 16, 24, 8]})
     sweep("3d27pt_cc", lambda: P.stencil("3d27pt", u, v, 4, unit=0), nbytes, {})
