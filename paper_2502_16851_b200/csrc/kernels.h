@@ -37,6 +37,7 @@ struct Tuning {
     int stencil_rows_per_thread = 2;   // 3D TMA CUDA-core kernels: 2, 4 or 8 (CTA = 64*16/this threads)
     int stencil2d_rows_per_thread = 4; // 2D TMA CUDA-core kernel (swept: tools/sweep.py)
     int stencil_t2_ctas_per_sm = 8;    // temporal-depth-2 2d5pt kernel (swept)
+    int stencil_cc27x2 = 1;            // 3d27pt CC class weights: two columns per thread kernel
     int stencil_tc_concat = 1;         // 3d27pt TC one-plane: class products concatenated along K (10 DMMA/tile)
     int stencil3d_cc_stages = 4;       // 3D CUDA-core TMA ring depth (4, 6, 8)
     int stencil_tc_ctas_per_sm = 2;    // ... 2D tensor-core kernel (2: +3 % measured over 1)

@@ -309,6 +309,118 @@ __global__ void __launch_bounds__(64 * kTY / RYT) st3d_tma_cc(const __grid_const
 }
 
 // ===========================================================================
+// CUDA core, 3d27pt with class weights, two columns per thread.  A warp owns
+// the tile's 64 columns (lane: columns 2 lane, 2 lane + 1) and RYT rows; each
+// staged row is read as three 128-bit pairs (columns 2 lane - 1 .. 2 lane + 2
+// of the tile plus alignment), and the vertical sums u[y-1] + u[y+1] of the
+// four columns are shared between the two outputs' face and corner classes:
+// 10 DADD + 12 DFMA/DMUL per two points per plane, half the shared loads of
+// the one-column kernel.  Partial sums across planes as in st3d_tma_cc.
+// ===========================================================================
+template <int S, int RYT>
+__global__ void __launch_bounds__(32 * kTY / RYT) st3d_tma_cc27x2(const __grid_constant__ CUtensorMap tm,
+                                                         double* __restrict__ v, StencilDesc d,
+                                                         uint64_t z_begin, uint64_t z_end, int zchunk,
+                                                         int tiles_x, int tiles_xy) {
+    constexpr int BX = kBX, STAGE = stage_doubles(BX);
+    extern __shared__ __align__(128) double smem[];
+    Ring<S, STAGE> ring(smem);
+    const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
+    const int tile = blockIdx.x % tiles_xy;
+    const uint64_t za = z_begin + (uint64_t)(blockIdx.x / tiles_xy) * zchunk;
+    if (za >= z_end) return;
+    const uint64_t zb = min(za + (uint64_t)zchunk, z_end);
+    const int np = (int)(zb - za) + 2;  // planes za-1 .. zb
+    const int64_t x0 = (int64_t)(tile % tiles_x) * kTX, y0 = (int64_t)(tile / tiles_x) * kTY;
+    const uint64_t nx = d.nx, ny = d.ny;
+    ring.init(kTY / RYT);
+    auto issue = [&](int k) {
+        mbar_expect_tx(ring.full + (k % S), kBY * BX * 8);
+        tma3d(ring.stage(k), &tm, ring.full + (k % S), (int)(x0 - kCofs), (int)(y0 - 1), (int)(za - 1 + k));
+    };
+    if (tid == 0)
+        for (int k = 0; k < S && k < np; ++k) issue(k);
+    const double g0 = d.w[0], g1 = d.w[1], g2 = d.w[2], g3 = d.w[3];
+    const int cb = 2 * lane;            // stage column of the pair (cb, cb+1) = x0 - 2 + cb
+    const int rbase = RYT * wy + 1;     // stage row of this warp's first output row
+    const int64_t x = x0 + 2 * lane;    // output columns x (stage cb + 2) and x + 1
+    const bool in0 = x >= 1 && x <= (int64_t)nx - 2, in1 = x + 1 >= 1 && x + 1 <= (int64_t)nx - 2;
+    const int64_t yr0 = y0 + RYT * wy;
+    double acc_a[RYT][2], acc_b[RYT][2];
+#pragma unroll
+    for (int j = 0; j < RYT; ++j) acc_a[j][0] = acc_a[j][1] = acc_b[j][0] = acc_b[j][1] = 0.0;
+    // row loader: columns cb+1 .. cb+4 of stage row r (x - 1 .. x + 2)
+    auto row4 = [&](const double* T, int r, double (&q)[4]) {
+        const double2 lo = *reinterpret_cast<const double2*>(T + r * BX + cb);
+        const double2 mid = *reinterpret_cast<const double2*>(T + r * BX + cb + 2);
+        const double2 hi = *reinterpret_cast<const double2*>(T + r * BX + cb + 4);
+        q[0] = lo.y;
+        q[1] = mid.x;
+        q[2] = mid.y;
+        q[3] = hi.x;
+    };
+    for (int k = 0; k < np; ++k) {
+        ring.wait_full(k);
+        const double* T = ring.stage(k);
+        double pm[RYT][2], p0[RYT][2];
+        double up[4], md[4];
+        row4(T, rbase - 1, up);
+        row4(T, rbase, md);
+#pragma unroll
+        for (int j = 0; j < RYT; ++j) {
+            double dn[4];
+            row4(T, rbase + j + 1, dn);
+            double vs[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) vs[q] = up[q] + dn[q];
+            // column A = q 1, column B = q 2
+            const double s1a = vs[1] + (md[0] + md[2]), s2a = vs[0] + vs[2];
+            const double s1b = vs[2] + (md[1] + md[3]), s2b = vs[1] + vs[3];
+            p0[j][0] = fma(g2, s2a, fma(g1, s1a, g0 * md[1]));
+            p0[j][1] = fma(g2, s2b, fma(g1, s1b, g0 * md[2]));
+            pm[j][0] = fma(g3, s2a, fma(g2, s1a, g1 * md[1]));
+            pm[j][1] = fma(g3, s2b, fma(g2, s1b, g1 * md[2]));
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                up[q] = md[q];
+                md[q] = dn[q];
+            }
+        }
+        ring.release(k);
+        if (tid == 0 && k + S < np) {
+            ring.wait_empty(k);
+            issue(k + S);
+        }
+        double o[RYT][2];
+#pragma unroll
+        for (int j = 0; j < RYT; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                o[j][h] = acc_a[j][h] + pm[j][h];  // P_+1 of plane p == P_-1 (class symmetry)
+                acc_a[j][h] = acc_b[j][h] + p0[j][h];
+                acc_b[j][h] = pm[j][h];
+            }
+        if (k >= 2) {
+            const uint64_t p = za - 2 + (uint64_t)k;
+#pragma unroll
+            for (int j = 0; j < RYT; ++j) {
+                const int64_t y = yr0 + j;
+                if (y >= 1 && y <= (int64_t)ny - 2) {
+                    double* dst = v + (p * ny + (uint64_t)y) * nx + x;
+                    if (in0 && in1)
+                        asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(dst), "d"(o[j][0]), "d"(o[j][1])
+                                     : "memory");
+                    else {
+                        if (in0) dst[0] = o[j][0];
+                        if (in1) dst[1] = o[j][1];
+                    }
+                }
+            }
+        }
+    }
+}
+
+// ===========================================================================
 // CUDA core, 2d5pt, temporal depth 2 (SURVEY.md §8f "next" #1; PAPER.md:223-236,
 // reference stencil_model(shape, P, t) and min_temporal_depth).  A stage holds
 // rows y0-2 .. y0+17 (box 68 x 20); step 1 is computed into a shared-memory
@@ -1055,7 +1167,17 @@ cudaError_t launch_stencil_tma(int unit, const StencilDesc& d, uint64_t o0, uint
     do { if (st == 6) RLB_CC3(K, R, 6); else if (st == 8) RLB_CC3(K, R, 8); else RLB_CC3(K, R, 4); } while (0)
 #define RLB_CC3K(K) \
     do { if (ry == 2) RLB_CC3S(K, 2); else if (ry == 4) RLB_CC3S(K, 4); else RLB_CC3S(K, 8); } while (0)
-        if (kind == 0) RLB_CC3K(0); else if (kind == 1) RLB_CC3K(1); else RLB_CC3K(2);
+        if (kind == 2 && tuning().stencil_cc27x2) {
+            constexpr int S = 4;
+            const size_t sm = ring_bytes<S, kBX>();
+#define RLB_CC27(R)                                                                                           \
+    do {                                                                                                      \
+        if ((e = prep(st3d_tma_cc27x2<S, R>, sm)) != cudaSuccess) return e;                                  \
+        st3d_tma_cc27x2<S, R><<<grid, 32 * kTY / R, sm, s>>>(m, v, dd, o0, o1, zchunk, tiles_x, tiles_xy); \
+    } while (0)
+            if (ry == 4) RLB_CC27(4); else if (ry == 8) RLB_CC27(8); else RLB_CC27(2);
+#undef RLB_CC27
+        } else if (kind == 0) RLB_CC3K(0); else if (kind == 1) RLB_CC3K(1); else RLB_CC3K(2);
 #undef RLB_CC3K
 #undef RLB_CC3S
 #undef RLB_CC3

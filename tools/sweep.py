@@ -177,7 +177,8 @@ def stencil3d_tc():
           {"stencil_tc_concat": [0, 1, 0, 1], "stencil_tc1_ctas_per_sm": [4, 8]})
     sweep("3d7pt_tc", lambda: P.stencil("3d7pt", u, v, 4, unit=1), nbytes,
           {"stencil_tc3d_mode": [2], "stencil_tc3d_ctas_per_sm": [6, 8, 12, 16, 24, 8]})
-    sweep("3d27pt_cc", lambda: P.stencil("3d27pt", u, v, 4, unit=0), nbytes, {})
+    sweep("3d27pt_cc", lambda: P.stencil("3d27pt", u, v, 4, unit=0), nbytes,
+          {"stencil_cc27x2": [0, 1, 0, 1], "stencil_rows_per_thread": [2, 4]})
 
 
 def stencil_r():
