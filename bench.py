@@ -691,6 +691,18 @@ def main():
     del h
 
     traffic = ncu_traffic().get(f"{args.workload}_{args.unit}")
+    l2_roof = None
+    if args.workload == "spmv" and world == 1:
+        # the binding unit for CSR SpMV on this matrix (profiles/README.md): L2
+        # requests -- one per x gather plus one per 128-byte line of val/col --
+        # against the measured random-gather rate (tools/micro/dsmem_gather.cu:
+        # 1.0 per SM per cycle, 290 G/s at 1.965 GHz)
+        m = Spmv.n_local
+        reqs = m * Spmv.k + (m * Spmv.k * 12) // 128
+        rate = reqs / (launch_ms * 1e-3) / 1e9
+        l2_roof = {"bound": "l2_requests", "requests_per_step": reqs, "achieved": round(rate, 1),
+                   "peak": 290.0, "unit": "G requests/s", "frac": round(rate / 290.0, 4),
+                   "peak_source": "measured random 8-byte L2 gather rate (tools/micro/dsmem_gather.cu)"}
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
@@ -706,6 +718,7 @@ def main():
                      "frac": round(achieved / hbm, 4), "traffic": traffic,
                      "launch_ms_mean": round(launch_ms, 5),
                      "launch_ms_p50": round(per_sorted[len(per_sorted) // 2], 5)},
+        "roofline_l2_requests": l2_roof,
         "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
                 "api": ("rl_spmv_plan_execute_host: A resident (uploaded once by rl_spmv_plan_create), "
