@@ -97,10 +97,13 @@ KernelCharacterization spmv_csr(ExecutionUnit unit, Precision precision,
                                 const SparseMatrixStats& stats, const std::int32_t* row_ptr,
                                 const std::int32_t* col, const double* val, const double* x,
                                 double* y, Stream stream);
+// long_rows: -1 = unknown (rows longer than the tuning key spmv_long_min are
+// diverted on the device to a load-balanced second kernel), 0 = the caller
+// knows there are none, 1 = present.
 void spmv_csr_rows(ExecutionUnit unit, Precision precision, std::uint64_t row_begin,
                    std::uint64_t row_end, const std::int32_t* row_ptr, const std::int32_t* col,
                    const double* val, const double* x, std::int64_t col_base, double* y,
-                   Stream stream);
+                   Stream stream, int long_rows = -1);
 KernelCharacterization stencil(ExecutionUnit unit, Precision precision, const StencilShape& shape,
                                const std::uint64_t dims[3], const double* weights,
                                std::uint64_t steps, double* u, double* v, Stream stream);

@@ -139,14 +139,14 @@ KernelCharacterization gemv(ExecutionUnit unit, Precision p, std::uint64_t m, st
 
 void spmv_csr_rows(ExecutionUnit unit, Precision p, std::uint64_t r0, std::uint64_t r1,
                    const std::int32_t* rp, const std::int32_t* col, const double* val,
-                   const double* x, std::int64_t col_base, double* y, Stream stream) {
+                   const double* x, std::int64_t col_base, double* y, Stream stream, int long_rows) {
     require_fp64(p);
     if (r1 < r0) throw Error(ErrorKind::InvalidRange, "row_end < row_begin");
     if (r1 == r0) return;
     require_ptr(rp, "row_ptr");
     require_ptr(y, "y");
     cuda_check(rlb::launch_spmv(unit == ExecutionUnit::TensorCore, r0, r1, rp, col, val, x, col_base,
-                                y, 0.0, static_cast<cudaStream_t>(stream)),
+                                y, long_rows, static_cast<cudaStream_t>(stream)),
                "spmv_csr");
 }
 
@@ -418,6 +418,7 @@ struct rl_spmv_plan_s {
     std::vector<uint64_t> chunk_xend;  // x prefix [0, chunk_xend[c]) chunk c reads
     std::vector<uint64_t> xpiece;      // x upload pieces: [xpiece[i], xpiece[i+1])
     cudaStream_t s_in = nullptr, s_cmp = nullptr, s_out = nullptr;
+    int long_rows = 0;  // the CSR has rows the per-row kernels divert (spmv.cu)
     std::vector<cudaEvent_t> ev_x, ev_y;
     cudaEvent_t ev_join[2] = {nullptr, nullptr};
     // execute_host as a CUDA graph, captured for the last (x, y) host pair
@@ -494,6 +495,11 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
     // pipeline chunks: whole tiled blocks when tiled
     const uint64_t unitrows = pl->tiled ? (uint64_t)rlb::kSpmvTiledRows : 1;
     const uint64_t units = (m + unitrows - 1) / unitrows;
+    {
+        int64_t maxlen = 0;
+        for (uint64_t i = 0; i < m; ++i) maxlen = std::max<int64_t>(maxlen, (int64_t)rp[i + 1] - rp[i]);
+        pl->long_rows = (maxlen > rlb::tuning().spmv_long_min && rlb::tuning().spmv_long_rows) ? 1 : 0;
+    }
     const uint64_t nch = std::min<uint64_t>((uint64_t)rlb::tuning().spmv_plan_chunks, units);
     // Chunk c covers weight w_c of the rows: w = 1/2 for the first and last
     // chunk, 1 otherwise (spmv_plan_taper), so the pipeline's head (the first
@@ -535,6 +541,10 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
     for (auto& e : pl->ev_x) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     for (auto& e : pl->ev_y) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     for (auto& e : pl->ev_join) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    if (pl->long_rows) {  // reserve the diversion buffers now: execute_host runs under graph capture
+        rlb::LongRows lr{};
+        ck(rlb::spmv_long_workspace(pl->s_cmp, m, lr), "plan long-row workspace");
+    }
     return pl.release();
 }
 
@@ -545,7 +555,7 @@ void plan_rows(rl_spmv_plan_s* pl, uint64_t r0, uint64_t r1, const double* x, do
         const uint64_t b1 = (r1 + rlb::kSpmvTiledRows - 1) / rlb::kSpmvTiledRows;
         ck(rlb::launch_spmv_tiled(pl->m, pl->segs, pl->tiles, pl->blk_tiles, b0, b1, x, y, s), "spmv (tiled plan)");
     } else {
-        spmv_csr_rows(pl->unit, Precision::FP64, r0, r1, pl->rp, pl->col, pl->val, x, 0, y, s);
+        spmv_csr_rows(pl->unit, Precision::FP64, r0, r1, pl->rp, pl->col, pl->val, x, 0, y, s, pl->long_rows);
     }
 }
 
@@ -1040,6 +1050,9 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         else if (k == "spmv_plan_chunks") slot = &t.spmv_plan_chunks;
         else if (k == "spmv_plan_zero_copy") slot = &t.spmv_plan_zero_copy;
         else if (k == "spmv_plan_tiled") slot = &t.spmv_plan_tiled;
+        else if (k == "spmv_long_rows") slot = &t.spmv_long_rows;
+        else if (k == "spmv_long_min") slot = &t.spmv_long_min;
+        else if (k == "spmv_long_huge") slot = &t.spmv_long_huge;
         else if (k == "spmv_plan_graph") slot = &t.spmv_plan_graph;
         else if (k == "spmv_plan_taper") slot = &t.spmv_plan_taper;
         else if (k == "stencil_r_ctas_per_sm") slot = &t.stencil_r_ctas_per_sm;

@@ -22,6 +22,9 @@ struct Tuning {
     int spmv_tc_threads = 1024;
     int spmv_l1_carveout = -1;     // shared-memory carveout % for the CC kernel (-1 = driver default)
     int spmv_tc_rows = 1;          // 8-row blocks per warp iteration (1, 2)
+    int spmv_long_rows = 1;        // divert long rows of the CSR kernels to a load-balanced second kernel
+    int spmv_long_min = 64;        // ... rows longer than this many nonzeros
+    int spmv_long_huge = 8192;     // ... and a CTA (not a warp) per row past this length
     int spmv_plan_chunks = 16;     // pipelined row/x chunks of rl_spmv_plan_execute_host
     int spmv_plan_tiled = 0;       // 1: CUDA-core plans use the column-tiled layout (spmv_tiled.cu; 0.30 ms vs CSR 0.28 ms on the BASELINE matrix)
     int spmv_plan_taper = 0;       // 1: half-size first/last pipeline chunks (measured no gain)
@@ -68,9 +71,28 @@ enum StencilPreset : int {
 
 cudaError_t launch_scale(int unit, double* a, const double* b, double q, uint64_t n,
                          cudaStream_t s);
+// Long-row diversion state of one SpMV launch (spmv.cu): rows longer than
+// lmax go to the medium list (warp per row), past lhuge to the huge list
+// (CTA per row), computed by spmv_long after the per-row kernel;
+// ctr = {n_med, n_huge, exited}.  ctr == nullptr: off.
+struct LongRows {
+    unsigned* ctr;
+    int* med;
+    int* huge;
+    int64_t lmax;
+    int64_t lhuge;
+};
+// long_rows: -1 unknown (divert on the device), 0 known absent (no
+// diversion), 1 known present.
 cudaError_t launch_spmv(int unit, uint64_t r0, uint64_t r1, const int* rp, const int* col,
                         const double* val, const double* x, int64_t col_base, double* y,
-                        double avg_nnz_per_row, cudaStream_t s);
+                        int long_rows, cudaStream_t s);
+cudaError_t launch_spmv_rows(int unit, uint64_t r0, uint64_t r1, const int* rp, const int* col,
+                             const double* val, const double* x, int64_t col_base, double* y,
+                             const LongRows& lr, cudaStream_t s);
+// Per-(device, stream) diversion buffers for `rows` rows; allocates (outside
+// stream capture) on first use or growth.
+cudaError_t spmv_long_workspace(cudaStream_t s, uint64_t rows, LongRows& lr);
 // One sweep over outer indices [o0, o1) (already clipped to the interior).
 cudaError_t launch_stencil_cc(const StencilDesc& d, uint64_t o0, uint64_t o1, const double* u,
                               double* v, cudaStream_t s);

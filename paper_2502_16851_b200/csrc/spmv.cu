@@ -18,6 +18,11 @@
 //      ceil(maxlen/16) x 4 DMMA m8n8k4 steps (rows shorter than the block's
 //      longest row are zero-padded).  Off-diagonal products are discarded:
 //      1/8 utilisation, as the paper's bound assumes.
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <utility>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -78,6 +83,164 @@ __device__ __forceinline__ void gather4(double (&xv)[4], const Nz4& z,
         xv[k] = k < z.n ? ld_x(x + ((int64_t)z.c[k] - col_base), polx, XH) : 0.0;
 }
 
+// Rows longer than lr.lmax nonzeros leave the per-row kernels (they would
+// hold a warp for ~len/16 steps while its other rows finish in one): the
+// lane that owns the row's start appends it to the medium list (a warp per
+// row) or, past lr.lhuge, the huge list (a CTA per row), and spmv_long then
+// computes them load-balanced.  lr.ctr == nullptr disables the diversion.
+__device__ __forceinline__ bool divert_long(const LongRows& lr, uint64_t row, int64_t& s, int64_t& e,
+                                            bool leader) {
+    if (lr.ctr == nullptr || e - s <= lr.lmax) return false;
+    if (leader) {
+        const bool huge = e - s > lr.lhuge;
+        const unsigned i = atomicAdd(lr.ctr + (huge ? 1 : 0), 1u);
+        (huge ? lr.huge : lr.med)[i] = (int)row;
+    }
+    e = s;
+    return true;
+}
+
+// Nonzeros [j, j+4) clipped to [lo, hi): vector loads when aligned and whole.
+struct Nz4m {
+    double v[4];
+    int c[4];
+    bool ok[4];
+};
+__device__ __forceinline__ Nz4m load_nz4_rng(const int* __restrict__ col, const double* __restrict__ val,
+                                             int64_t j, int64_t lo, int64_t hi, uint64_t pol) {
+    Nz4m z;
+    if (((j & 3) == 0) && j >= lo && j + 4 <= hi) {
+        const d4 v = ld4_stream(val + j, pol);
+        int4 ci;
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+            : "=r"(ci.x), "=r"(ci.y), "=r"(ci.z), "=r"(ci.w)
+            : "l"(col + j), "l"(pol));
+        z.v[0] = v.x; z.v[1] = v.y; z.v[2] = v.z; z.v[3] = v.w;
+        z.c[0] = ci.x; z.c[1] = ci.y; z.c[2] = ci.z; z.c[3] = ci.w;
+        z.ok[0] = z.ok[1] = z.ok[2] = z.ok[3] = true;
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            z.ok[k] = j + k >= lo && j + k < hi;
+            z.v[k] = z.ok[k] ? ld_stream(val + j + k, pol) : 0.0;
+            z.c[k] = z.ok[k] ? ld_stream_i32(col + j + k, pol) : 0;
+        }
+    }
+    return z;
+}
+__device__ __forceinline__ void gather4m(double (&xv)[4], const Nz4m& z, const double* __restrict__ x,
+                                         int64_t col_base, uint64_t polx) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) xv[k] = z.ok[k] ? ld_x(x + ((int64_t)z.c[k] - col_base), polx, 0) : 0.0;
+}
+
+// Sum of nonzeros [lo, hi) of one row by one warp, valid in every lane.
+// CUDA core: lanes stride 4-wide aligned groups; fixed-order xor reduction.
+__device__ __forceinline__ double warp_segment_cc(const int* __restrict__ col, const double* __restrict__ val,
+                                                  const double* __restrict__ x, int64_t col_base, int64_t lo,
+                                                  int64_t hi, uint64_t pol, uint64_t polx) {
+    const int lane = threadIdx.x & 31;
+    double acc = 0.0;
+    for (int64_t j = (lo & ~int64_t(3)) + 4 * lane; j < hi; j += 128) {
+        const Nz4m z = load_nz4_rng(col, val, j, lo, hi, pol);
+        double xv[4];
+        gather4m(xv, z, x, col_base, polx);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc = fma(z.v[k], xv[k], acc);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    return acc;
+}
+
+// Tensor core: the segment is cut into 8 virtual rows of C nonzeros (C a
+// multiple of 4, starts aligned) and run as the DASP-style 8-row block of
+// K4: D[r][r] accumulates virtual row r; the 8 diagonal values are summed in
+// a fixed order.
+__device__ __forceinline__ double warp_segment_tc(const int* __restrict__ col, const double* __restrict__ val,
+                                                  const double* __restrict__ x, int64_t col_base, int64_t lo,
+                                                  int64_t hi, uint64_t pol, uint64_t polx) {
+    const int lane = threadIdx.x & 31, r = lane >> 2, c = lane & 3;
+    const int64_t base = lo & ~int64_t(3);
+    const int64_t C = (((hi - base) + 7) / 8 + 3) & ~int64_t(3);
+    const int64_t vlo = max(lo, base + r * C), vhi = min(hi, base + (r + 1) * C);
+    double d0 = 0.0, d1 = 0.0;
+    for (int64_t off = 0; off < C; off += 16) {
+        const Nz4m z = load_nz4_rng(col, val, base + r * C + off + 4 * c, vlo, vhi, pol);
+        double xv[4];
+        gather4m(xv, z, x, col_base, polx);
+        dmma_m8n8k4(d0, d1, z.v[0], xv[0], d0, d1);
+        dmma_m8n8k4(d0, d1, z.v[1], xv[1], d0, d1);
+        dmma_m8n8k4(d0, d1, z.v[2], xv[2], d0, d1);
+        dmma_m8n8k4(d0, d1, z.v[3], xv[3], d0, d1);
+    }
+    const double dv = (r & 1) ? d1 : d0;  // D[r][r] in lane 4r + r/2
+    double sum = 0.0;
+#pragma unroll
+    for (int rr = 0; rr < 8; ++rr) sum += __shfl_sync(0xffffffffu, dv, 4 * rr + (rr >> 1));
+    return sum;
+}
+
+// Longest row of [r0, r1): the one-time probe behind row_profile().
+__global__ void __launch_bounds__(256) spmv_maxlen(uint64_t r0, uint64_t r1, const int* __restrict__ rp,
+                                                   int* __restrict__ out) {
+    int m = 0;
+    for (uint64_t i = r0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < r1;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        m = max(m, __ldg(rp + i + 1) - __ldg(rp + i));
+    m = (int)__reduce_max_sync(0xffffffffu, (unsigned)m);
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// The diverted rows, after the per-row kernel (stream order): huge rows a
+// CTA each (the warps take contiguous slices, fixed-order block sum), medium
+// rows a warp each.  The last CTA out zeroes the counters for the next call
+// on this stream, so no memset node is needed.
+// ctr: 0 n_med, 1 n_huge, 2 exited.
+template <int TC>
+__global__ void __launch_bounds__(1024) spmv_long(const int* __restrict__ rp, const int* __restrict__ col,
+                                                  const double* __restrict__ val, const double* __restrict__ x,
+                                                  int64_t col_base, double* __restrict__ y, LongRows lr) {
+    __shared__ double red[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+    const uint64_t pol = policy_evict_first(), polx = policy_evict_last();
+    const unsigned nmed = *reinterpret_cast<volatile unsigned*>(lr.ctr);
+    const unsigned nhuge = *reinterpret_cast<volatile unsigned*>(lr.ctr + 1);
+    for (unsigned i = blockIdx.x; i < nhuge; i += gridDim.x) {
+        const int row = lr.huge[i];
+        const int64_t s = __ldg(rp + row), e = __ldg(rp + row + 1);
+        const int64_t part = (((e - s) + nwarp - 1) / nwarp + 3) & ~int64_t(3);
+        const int64_t lo = min(e, s + warp * part), hi = min(e, s + (warp + 1) * part);
+        const double v = TC ? warp_segment_tc(col, val, x, col_base, lo, hi, pol, polx)
+                            : warp_segment_cc(col, val, x, col_base, lo, hi, pol, polx);
+        if (lane == 0) red[warp] = v;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int w = 0; w < nwarp; ++w) t += red[w];
+            y[row] = t;
+        }
+        __syncthreads();
+    }
+    const unsigned gw = blockIdx.x * (unsigned)nwarp + (unsigned)warp, nw = gridDim.x * (unsigned)nwarp;
+    for (unsigned i = gw; i < nmed; i += nw) {
+        const int row = lr.med[i];
+        const int64_t s = __ldg(rp + row), e = __ldg(rp + row + 1);
+        const double v = TC ? warp_segment_tc(col, val, x, col_base, s, e, pol, polx)
+                            : warp_segment_cc(col, val, x, col_base, s, e, pol, polx);
+        if (lane == 0) y[row] = v;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(lr.ctr + 2, 1u) == gridDim.x - 1) {
+            lr.ctr[0] = 0;
+            lr.ctr[1] = 0;
+            lr.ctr[2] = 0;
+        }
+    }
+}
+
 // K3: CUDA core.  Row of warp-step u for group q: wbase + 8u + q.
 // SCHED 0: warps stride over the whole row range (grid-stride);
 // SCHED 1: each CTA owns one contiguous row range (x-window locality in L1).
@@ -87,7 +250,7 @@ __global__ void __launch_bounds__(1024) spmv_cc_v4(uint64_t r0, uint64_t r1,
                                                   const int* __restrict__ col,
                                                   const double* __restrict__ val,
                                                   const double* __restrict__ x, int64_t col_base,
-                                                  double* __restrict__ y) {
+                                                  double* __restrict__ y, LongRows lr) {
     const int lane = threadIdx.x & 31;
     const int c = lane & 3, q = lane >> 2;
     const uint64_t pol = policy_evict_first(), polx = policy_evict_last();
@@ -116,6 +279,12 @@ __global__ void __launch_bounds__(1024) spmv_cc_v4(uint64_t r0, uint64_t r1,
             s[u] = ok ? __ldg(rp + row) : 0;
             e[u] = ok ? __ldg(rp + row + 1) : 0;
         }
+        // rows past 16 nonzeros only: the diversion check stays off the
+        // BASELINE path (16 per row), whose first 16 are loaded regardless
+        bool skip[R];
+#pragma unroll
+        for (int u = 0; u < R; ++u)
+            skip[u] = e[u] - s[u] > 16 && divert_long(lr, wbase + 8 * u + q, s[u], e[u], c == 0);
         Nz4 z[R];
 #pragma unroll
         for (int u = 0; u < R; ++u) z[u] = load_nz4(col, val, s[u] + 4 * c, e[u], col_pad, pol);
@@ -147,7 +316,7 @@ __global__ void __launch_bounds__(1024) spmv_cc_v4(uint64_t r0, uint64_t r1,
             a += __shfl_xor_sync(0xffffffffu, a, 1);
             a += __shfl_xor_sync(0xffffffffu, a, 2);
             const uint64_t row = wbase + 8 * u + q;
-            if (c == 0 && row < rend) y[row] = a;
+            if (c == 0 && row < rend && !skip[u]) y[row] = a;
         }
     }
 }
@@ -160,7 +329,7 @@ __global__ void __launch_bounds__(1024) spmv_tc(uint64_t r0, uint64_t r1,
                                                 const int* __restrict__ col,
                                                 const double* __restrict__ val,
                                                 const double* __restrict__ x, int64_t col_base,
-                                                double* __restrict__ y) {
+                                                double* __restrict__ y, LongRows lr) {
     const int lane = threadIdx.x & 31;
     const int r = lane >> 2, c = lane & 3;
     const uint64_t pol = policy_evict_first(), polx = policy_evict_last();
@@ -181,6 +350,7 @@ __global__ void __launch_bounds__(1024) spmv_tc(uint64_t r0, uint64_t r1,
     }
     for (uint64_t base = first; base < last; base += stride) {
         int64_t s[RB], e[RB];
+        bool skip[RB];
         int len = 0;
 #pragma unroll
         for (int q = 0; q < RB; ++q) {
@@ -188,6 +358,7 @@ __global__ void __launch_bounds__(1024) spmv_tc(uint64_t r0, uint64_t r1,
             const bool ok = row < last;
             s[q] = ok ? __ldg(rp + row) : 0;
             e[q] = ok ? __ldg(rp + row + 1) : 0;
+            skip[q] = divert_long(lr, row, s[q], e[q], c == 0);  // long rows leave the 8-row block
             len = max(len, (int)(e[q] - s[q]));
         }
         const int maxlen = __reduce_max_sync(0xffffffffu, len);
@@ -213,18 +384,88 @@ __global__ void __launch_bounds__(1024) spmv_tc(uint64_t r0, uint64_t r1,
 #pragma unroll
         for (int q = 0; q < RB; ++q) {
             const uint64_t row = base + 8 * q + r;
-            if (c == (r >> 1) && row < last) y[row] = (r & 1) ? d1[q] : d0[q];
+            if (c == (r >> 1) && row < last && !skip[q]) y[row] = (r & 1) ? d1[q] : d0[q];
         }
     }
 }
 
 }  // namespace
 
+// Has the CSR row range rows the per-row kernels divert?  Probed once per
+// (device, row_ptr, col, val, range): one small kernel and one stream
+// synchronisation on the first call, then cached, so later calls stay fully
+// asynchronous and pay nothing when there are none.  A stale entry (arrays
+// rewritten in place at the same addresses) costs speed only: undiverted
+// long rows are still computed by the per-row kernels, and a needless
+// diversion pass finds empty lists.  Under stream capture the probe is
+// skipped (-1: divert on the device).
+static int row_profile(const int* rp, const int* col, const double* val, uint64_t r0, uint64_t r1,
+                       cudaStream_t s) {
+    struct Key {
+        int dev;
+        const void *rp, *col, *val;
+        uint64_t r0, r1;
+        bool operator<(const Key& o) const {
+            return std::tie(dev, rp, col, val, r0, r1) < std::tie(o.dev, o.rp, o.col, o.val, o.r0, o.r1);
+        }
+    };
+    static std::mutex mu;
+    static std::map<Key, int> cache;
+    static std::map<int, int*> slots;  // per-device probe result
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+    const Key key{dev, rp, col, val, r0, r1};
+    std::lock_guard<std::mutex> lock(mu);
+    const auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return -1;
+    int*& slot = slots[dev];
+    if (!slot && cudaMalloc(&slot, sizeof(int)) != cudaSuccess) {
+        slot = nullptr;
+        cudaGetLastError();
+        return -1;
+    }
+    int h = 0;
+    if (cudaMemsetAsync(slot, 0, sizeof(int), s) != cudaSuccess) return -1;
+    spmv_maxlen<<<kNumSMs * 4, 256, 0, s>>>(r0, r1, rp, slot);
+    note_launch();
+    if (cudaMemcpyAsync(&h, slot, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return -1;
+    const int v = h > tuning().spmv_long_min ? 1 : 0;
+    if (cache.size() >= 1024) cache.clear();
+    cache[key] = v;
+    return v;
+}
+
 cudaError_t launch_spmv(int unit, uint64_t r0, uint64_t r1, const int* rp, const int* col,
                         const double* val, const double* x, int64_t col_base, double* y,
-                        double avg_nnz_per_row, cudaStream_t s) {
-    (void)avg_nnz_per_row;
+                        int long_rows, cudaStream_t s) {
     if (r1 <= r0) return cudaSuccess;
+    const Tuning& t = tuning();
+    if (long_rows < 0 && t.spmv_long_rows) long_rows = row_profile(rp, col, val, r0, r1, s);
+    // long-row diversion (long_rows: -1 unknown, 0 none, 1 present)
+    LongRows lr{};
+    if (long_rows != 0 && t.spmv_long_rows) {
+        cudaError_t e = spmv_long_workspace(s, r1 - r0, lr);
+        if (e != cudaSuccess) return e;
+        lr.lmax = t.spmv_long_min;
+        lr.lhuge = t.spmv_long_huge;
+    }
+    cudaError_t err = launch_spmv_rows(unit, r0, r1, rp, col, val, x, col_base, y, lr, s);
+    if (err != cudaSuccess || lr.ctr == nullptr) return err;
+    if (unit == 1)
+        spmv_long<1><<<kNumSMs, 1024, 0, s>>>(rp, col, val, x, col_base, y, lr);
+    else
+        spmv_long<0><<<kNumSMs, 1024, 0, s>>>(rp, col, val, x, col_base, y, lr);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_spmv_rows(int unit, uint64_t r0, uint64_t r1, const int* rp, const int* col,
+                             const double* val, const double* x, int64_t col_base, double* y,
+                             const LongRows& lr, cudaStream_t s) {
     const Tuning& t = tuning();
     const int threads = 256;
     const uint64_t rows = r1 - r0;
@@ -234,7 +475,7 @@ cudaError_t launch_spmv(int unit, uint64_t r0, uint64_t r1, const int* rp, const
         uint64_t blocks = (rows + (uint64_t)(tthreads / 32) * 8 * RB - 1) / ((uint64_t)(tthreads / 32) * 8 * RB);
         const uint64_t cap = (uint64_t)kNumSMs * (uint64_t)t.spmv_tc_blocks_per_sm;
         if (blocks > cap) blocks = cap;
-#define RLB_TC(R, S) spmv_tc<R, S><<<(unsigned)blocks, tthreads, 0, s>>>(r0, r1, rp, col, val, x, col_base, y)
+#define RLB_TC(R, S) spmv_tc<R, S><<<(unsigned)blocks, tthreads, 0, s>>>(r0, r1, rp, col, val, x, col_base, y, lr)
         if (t.spmv_sched == 0) { if (RB == 2) RLB_TC(2, 0); else RLB_TC(1, 0); }
         else { if (RB == 2) RLB_TC(2, 1); else RLB_TC(1, 1); }
 #undef RLB_TC
@@ -253,7 +494,7 @@ cudaError_t launch_spmv(int unit, uint64_t r0, uint64_t r1, const int* rp, const
         if (t.spmv_l1_carveout >= 0)                                                              \
             cudaFuncSetAttribute(spmv_cc_v4<RR, SS, XX>,                                          \
                                  cudaFuncAttributePreferredSharedMemoryCarveout, t.spmv_l1_carveout); \
-        spmv_cc_v4<RR, SS, XX><<<(unsigned)blocks, cthreads, 0, s>>>(r0, r1, rp, col, val, x, col_base, y); \
+        spmv_cc_v4<RR, SS, XX><<<(unsigned)blocks, cthreads, 0, s>>>(r0, r1, rp, col, val, x, col_base, y, lr); \
     } while (0)
 #define RLB_SPMV_R(SS, XX)                        \
     do {                                          \
@@ -270,6 +511,45 @@ cudaError_t launch_spmv(int unit, uint64_t r0, uint64_t r1, const int* rp, const
 #undef RLB_SPMV
     note_launch();
     return cudaGetLastError();
+}
+
+namespace {
+struct LongWs {
+    unsigned* ctr = nullptr;
+    int* med = nullptr;
+    int* huge = nullptr;
+    uint64_t cap = 0;
+};
+}  // namespace
+
+cudaError_t spmv_long_workspace(cudaStream_t s, uint64_t rows, LongRows& lr) {
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, LongWs> table;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    LongWs& w = table[{dev, s}];
+    if (w.cap < rows) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if ((e = cudaStreamIsCapturing(s, &cs)) != cudaSuccess) return e;
+        if (cs != cudaStreamCaptureStatusNone) return cudaErrorStreamCaptureUnsupported;  // reserve first
+        if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;  // old buffers may be in flight
+        if (w.ctr) cudaFree(w.ctr);
+        if (w.med) cudaFree(w.med);
+        if (w.huge) cudaFree(w.huge);
+        w = LongWs{};
+        const uint64_t cap = rows < 1024 ? 1024 : rows;
+        if ((e = cudaMalloc(&w.ctr, 8 * sizeof(unsigned))) != cudaSuccess) return e;
+        if ((e = cudaMemset(w.ctr, 0, 8 * sizeof(unsigned))) != cudaSuccess) return e;
+        if ((e = cudaMalloc(&w.med, cap * sizeof(int))) != cudaSuccess) return e;
+        if ((e = cudaMalloc(&w.huge, cap * sizeof(int))) != cudaSuccess) return e;
+        w.cap = cap;
+    }
+    lr.ctr = w.ctr;
+    lr.med = w.med;
+    lr.huge = w.huge;
+    return cudaSuccess;
 }
 
 }  // namespace rlb

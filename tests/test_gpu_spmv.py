@@ -154,3 +154,58 @@ def test_spmv_errors(cuda):
     with pytest.raises(P.RooflensError) as e:  # nnz = 0: the model rejects it
         P.spmv_csr(rp, rp[:0], z[:0], z, z)
     assert e.value.kind == "ValidationError"
+
+
+def _skewed_csr(m, n, seed, huge=(3, 20000)):
+    """Power-law row lengths plus a few huge rows (past spmv_long_huge)."""
+    rng = np.random.default_rng(seed)
+    lens = np.minimum(rng.zipf(1.6, m), 3000).astype(np.int64)
+    for r in rng.choice(m, huge[0], replace=False):
+        lens[r] = huge[1]
+    lens = np.minimum(lens, n)
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    col = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(np.int32)
+    return rp, col, rng.uniform(-1, 1, rp[-1])
+
+
+@pytest.mark.parametrize("unit", UNITS)
+def test_spmv_long_rows_diverted(cuda, unit):
+    """Rows past spmv_long_min go to the load-balanced second kernel (a warp
+    per row, a CTA per row past spmv_long_huge); results equal the oracle."""
+    import torch
+
+    m, n = 20000, 30000
+    rp, col, val = _skewed_csr(m, n, 3)
+    assert np.diff(rp).max() > 8192 and (np.diff(rp) > 64).sum() > 50
+    x = np.random.default_rng(4).uniform(-1, 1, n)
+    d = [torch.from_numpy(t).cuda() for t in (rp, col, val, x)]
+    y = torch.full((m,), float("nan"), dtype=torch.float64, device="cuda")
+    for _ in range(3):  # the counters reset themselves between calls
+        P.spmv_csr(d[0], d[1], d[2], d[3], y, unit=unit)
+        torch.cuda.synchronize()
+        assert O.rel_err(y.cpu().numpy(), O.spmv_csr(rp, col, val, x)) <= TOL
+
+
+@pytest.mark.parametrize("unit", UNITS)
+def test_spmv_profile_cache_stale_is_still_correct(cuda, unit):
+    """The long-row profile is cached per buffer triple: rewriting the same
+    buffers with a different structure must still give exact results."""
+    import torch
+
+    m, n = 4000, 4000
+    rp1, col1, val1 = O.gen_band_csr(m, 0, n, 8, 100, 1)           # short rows only
+    rp2, col2, val2 = _skewed_csr(m, n, 5, huge=(2, 3500))          # long rows
+    nnz = max(rp1[-1], rp2[-1])
+    drp = torch.empty(m + 1, dtype=torch.int32, device="cuda")
+    dcol = torch.empty(nnz, dtype=torch.int32, device="cuda")
+    dval = torch.empty(nnz, dtype=torch.float64, device="cuda")
+    x = np.random.default_rng(6).uniform(-1, 1, n)
+    dx = torch.from_numpy(x).cuda()
+    y = torch.empty(m, dtype=torch.float64, device="cuda")
+    for rp, col, val in ((rp1, col1, val1), (rp2, col2, val2), (rp1, col1, val1)):
+        drp.copy_(torch.from_numpy(rp))
+        dcol[:rp[-1]].copy_(torch.from_numpy(col))
+        dval[:rp[-1]].copy_(torch.from_numpy(val))
+        P.spmv_csr(drp, dcol, dval, dx, y, unit=unit)
+        torch.cuda.synchronize()
+        assert O.rel_err(y.cpu().numpy(), O.spmv_csr(rp, col, val, x)) <= TOL

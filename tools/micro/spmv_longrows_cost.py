@@ -1,0 +1,19 @@
+import os, sys
+sys.path.insert(0, "/root/repo")
+import torch, paper_2502_16851_b200 as P
+n, k, hb = 1 << 22, 16, 65536
+rp = torch.empty(n + 1, dtype=torch.int32, device="cuda"); col = torch.empty(n * k, dtype=torch.int32, device="cuda")
+val = torch.empty(n * k, dtype=torch.float64, device="cuda"); x = torch.empty(n, dtype=torch.float64, device="cuda")
+y = torch.empty(n, dtype=torch.float64, device="cuda")
+P.gen_band_csr(n, 0, n, k, hb, 1, rp, col, val); P.fill_uniform(x, 1, 4, 0, 1)
+def t(fn, reps=200):
+    for _ in range(5): fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps): fn()
+    e.record(); torch.cuda.synchronize()
+    return s.elapsed_time(e) / reps
+for lr in (0, 1, 0, 1):
+    P.tuning_set("spmv_long_rows", lr)
+    print("long_rows", lr, round(t(lambda: P.spmv_csr(rp, col, val, x, y)), 4), "ms", flush=True)
