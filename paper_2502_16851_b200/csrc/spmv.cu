@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(1024) spmv_long(const int* __restrict__ rp, co
 // K3: CUDA core.  Row of warp-step u for group q: wbase + 8u + q.
 // SCHED 0: warps stride over the whole row range (grid-stride);
 // SCHED 1: each CTA owns one contiguous row range (x-window locality in L1).
-template <int R, int SCHED, int XH>
+template <int R, int SCHED, int XH, bool DIV>
 __global__ void __launch_bounds__(1024) spmv_cc_v4(uint64_t r0, uint64_t r1,
                                                   const int* __restrict__ rp,
                                                   const int* __restrict__ col,
@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(1024) spmv_cc_v4(uint64_t r0, uint64_t r1,
         bool skip[R];
 #pragma unroll
         for (int u = 0; u < R; ++u)
-            skip[u] = e[u] - s[u] > 16 && divert_long(lr, wbase + 8 * u + q, s[u], e[u], c == 0);
+            skip[u] = DIV && e[u] - s[u] > 16 && divert_long(lr, wbase + 8 * u + q, s[u], e[u], c == 0);
         Nz4 z[R];
 #pragma unroll
         for (int u = 0; u < R; ++u) z[u] = load_nz4(col, val, s[u] + 4 * c, e[u], col_pad, pol);
@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(1024) spmv_cc_v4(uint64_t r0, uint64_t r1,
 
 // K4: tensor core.  A warp owns RB 8-row blocks per iteration (independent
 // DMMA accumulator chains); SCHED as in K3.
-template <int RB, int SCHED>
+template <int RB, int SCHED, bool DIV>
 __global__ void __launch_bounds__(1024) spmv_tc(uint64_t r0, uint64_t r1,
                                                 const int* __restrict__ rp,
                                                 const int* __restrict__ col,
@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(1024) spmv_tc(uint64_t r0, uint64_t r1,
             const bool ok = row < last;
             s[q] = ok ? __ldg(rp + row) : 0;
             e[q] = ok ? __ldg(rp + row + 1) : 0;
-            skip[q] = divert_long(lr, row, s[q], e[q], c == 0);  // long rows leave the 8-row block
+            skip[q] = DIV && divert_long(lr, row, s[q], e[q], c == 0);  // long rows leave the 8-row block
             len = max(len, (int)(e[q] - s[q]));
         }
         const int maxlen = __reduce_max_sync(0xffffffffu, len);
@@ -475,7 +475,11 @@ cudaError_t launch_spmv_rows(int unit, uint64_t r0, uint64_t r1, const int* rp, 
         uint64_t blocks = (rows + (uint64_t)(tthreads / 32) * 8 * RB - 1) / ((uint64_t)(tthreads / 32) * 8 * RB);
         const uint64_t cap = (uint64_t)kNumSMs * (uint64_t)t.spmv_tc_blocks_per_sm;
         if (blocks > cap) blocks = cap;
-#define RLB_TC(R, S) spmv_tc<R, S><<<(unsigned)blocks, tthreads, 0, s>>>(r0, r1, rp, col, val, x, col_base, y, lr)
+#define RLB_TC(R, S)                                                                                        \
+    do {                                                                                                    \
+        if (lr.ctr) spmv_tc<R, S, true><<<(unsigned)blocks, tthreads, 0, s>>>(r0, r1, rp, col, val, x, col_base, y, lr); \
+        else spmv_tc<R, S, false><<<(unsigned)blocks, tthreads, 0, s>>>(r0, r1, rp, col, val, x, col_base, y, lr); \
+    } while (0)
         if (t.spmv_sched == 0) { if (RB == 2) RLB_TC(2, 0); else RLB_TC(1, 0); }
         else { if (RB == 2) RLB_TC(2, 1); else RLB_TC(1, 1); }
 #undef RLB_TC
@@ -489,13 +493,15 @@ cudaError_t launch_spmv_rows(int unit, uint64_t r0, uint64_t r1, const int* rp, 
     const uint64_t cap = (uint64_t)kNumSMs * (uint64_t)t.spmv_blocks_per_sm;
     if (blocks > cap) blocks = cap;
     const int sched = t.spmv_sched, xh = t.spmv_xhint;
-#define RLB_SPMV(RR, SS, XX)                                                                      \
-    do {                                                                                          \
-        if (t.spmv_l1_carveout >= 0)                                                              \
-            cudaFuncSetAttribute(spmv_cc_v4<RR, SS, XX>,                                          \
-                                 cudaFuncAttributePreferredSharedMemoryCarveout, t.spmv_l1_carveout); \
-        spmv_cc_v4<RR, SS, XX><<<(unsigned)blocks, cthreads, 0, s>>>(r0, r1, rp, col, val, x, col_base, y, lr); \
+#define RLB_SPMV2(RR, SS, XX, DV)                                                                      \
+    do {                                                                                                \
+        if (t.spmv_l1_carveout >= 0)                                                                    \
+            cudaFuncSetAttribute(spmv_cc_v4<RR, SS, XX, DV>,                                            \
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, t.spmv_l1_carveout);   \
+        spmv_cc_v4<RR, SS, XX, DV><<<(unsigned)blocks, cthreads, 0, s>>>(r0, r1, rp, col, val, x, col_base, y, lr); \
     } while (0)
+#define RLB_SPMV(RR, SS, XX) \
+    do { if (lr.ctr) RLB_SPMV2(RR, SS, XX, true); else RLB_SPMV2(RR, SS, XX, false); } while (0)
 #define RLB_SPMV_R(SS, XX)                        \
     do {                                          \
         if (R == 1) RLB_SPMV(1, SS, XX);          \
@@ -509,6 +515,7 @@ cudaError_t launch_spmv_rows(int unit, uint64_t r0, uint64_t r1, const int* rp, 
     }
 #undef RLB_SPMV_R
 #undef RLB_SPMV
+#undef RLB_SPMV2
     note_launch();
     return cudaGetLastError();
 }
