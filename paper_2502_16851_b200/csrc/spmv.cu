@@ -140,17 +140,24 @@ __device__ __forceinline__ double warp_segment_cc(const int* __restrict__ col, c
                                                   const double* __restrict__ x, int64_t col_base, int64_t lo,
                                                   int64_t hi, uint64_t pol, uint64_t polx) {
     const int lane = threadIdx.x & 31;
-    double acc = 0.0;
-    for (int64_t j = (lo & ~int64_t(3)) + 4 * lane; j < hi; j += 128) {
-        const Nz4m z = load_nz4_rng(col, val, j, lo, hi, pol);
-        double xv[4];
-        gather4m(xv, z, x, col_base, polx);
+    constexpr int U = 4;  // 4 x 128 nonzeros in flight per warp step (loads first, then gathers)
+    double acc[U] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t j0 = (lo & ~int64_t(3)) + 4 * lane; j0 < hi; j0 += 128 * U) {
+        Nz4m z[U];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) acc = fma(z.v[k], xv[k], acc);
+        for (int u = 0; u < U; ++u) z[u] = load_nz4_rng(col, val, j0 + 128 * u, lo, hi, pol);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            double xv[4];
+            gather4m(xv, z[u], x, col_base, polx);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc[u] = fma(z[u].v[k], xv[k], acc[u]);
+        }
     }
+    double a = (acc[0] + acc[1]) + (acc[2] + acc[3]);
 #pragma unroll
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    return acc;
+    for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    return a;
 }
 
 // Tensor core: the segment is cut into 8 virtual rows of C nonzeros (C a
@@ -164,17 +171,25 @@ __device__ __forceinline__ double warp_segment_tc(const int* __restrict__ col, c
     const int64_t base = lo & ~int64_t(3);
     const int64_t C = (((hi - base) + 7) / 8 + 3) & ~int64_t(3);
     const int64_t vlo = max(lo, base + r * C), vhi = min(hi, base + (r + 1) * C);
-    double d0 = 0.0, d1 = 0.0;
-    for (int64_t off = 0; off < C; off += 16) {
-        const Nz4m z = load_nz4_rng(col, val, base + r * C + off + 4 * c, vlo, vhi, pol);
-        double xv[4];
-        gather4m(xv, z, x, col_base, polx);
-        dmma_m8n8k4(d0, d1, z.v[0], xv[0], d0, d1);
-        dmma_m8n8k4(d0, d1, z.v[1], xv[1], d0, d1);
-        dmma_m8n8k4(d0, d1, z.v[2], xv[2], d0, d1);
-        dmma_m8n8k4(d0, d1, z.v[3], xv[3], d0, d1);
+    constexpr int U = 4;  // 4 steps of 16 in flight: loads first, then gathers and DMMA chains
+    double d0[U] = {0.0, 0.0, 0.0, 0.0}, d1[U] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t off0 = 0; off0 < C; off0 += 16 * U) {
+        Nz4m z[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            z[u] = load_nz4_rng(col, val, base + r * C + off0 + 16 * u + 4 * c, vlo, vhi, pol);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            double xv[4];
+            gather4m(xv, z[u], x, col_base, polx);
+            dmma_m8n8k4(d0[u], d1[u], z[u].v[0], xv[0], d0[u], d1[u]);
+            dmma_m8n8k4(d0[u], d1[u], z[u].v[1], xv[1], d0[u], d1[u]);
+            dmma_m8n8k4(d0[u], d1[u], z[u].v[2], xv[2], d0[u], d1[u]);
+            dmma_m8n8k4(d0[u], d1[u], z[u].v[3], xv[3], d0[u], d1[u]);
+        }
     }
-    const double dv = (r & 1) ? d1 : d0;  // D[r][r] in lane 4r + r/2
+    const double e0 = (d0[0] + d0[1]) + (d0[2] + d0[3]), e1 = (d1[0] + d1[1]) + (d1[2] + d1[3]);
+    const double dv = (r & 1) ? e1 : e0;  // D[r][r] in lane 4r + r/2
     double sum = 0.0;
 #pragma unroll
     for (int rr = 0; rr < 8; ++rr) sum += __shfl_sync(0xffffffffu, dv, 4 * rr + (rr >> 1));
@@ -198,7 +213,7 @@ __global__ void __launch_bounds__(256) spmv_maxlen(uint64_t r0, uint64_t r1, con
 // on this stream, so no memset node is needed.
 // ctr: 0 n_med, 1 n_huge, 2 exited.
 template <int TC>
-__global__ void __launch_bounds__(1024) spmv_long(const int* __restrict__ rp, const int* __restrict__ col,
+__global__ void __launch_bounds__(256) spmv_long(const int* __restrict__ rp, const int* __restrict__ col,
                                                   const double* __restrict__ val, const double* __restrict__ x,
                                                   int64_t col_base, double* __restrict__ y, LongRows lr) {
     __shared__ double red[32];
@@ -456,9 +471,9 @@ cudaError_t launch_spmv(int unit, uint64_t r0, uint64_t r1, const int* rp, const
     cudaError_t err = launch_spmv_rows(unit, r0, r1, rp, col, val, x, col_base, y, lr, s);
     if (err != cudaSuccess || lr.ctr == nullptr) return err;
     if (unit == 1)
-        spmv_long<1><<<kNumSMs, 1024, 0, s>>>(rp, col, val, x, col_base, y, lr);
+        spmv_long<1><<<kNumSMs * 8, 256, 0, s>>>(rp, col, val, x, col_base, y, lr);
     else
-        spmv_long<0><<<kNumSMs, 1024, 0, s>>>(rp, col, val, x, col_base, y, lr);
+        spmv_long<0><<<kNumSMs * 8, 256, 0, s>>>(rp, col, val, x, col_base, y, lr);
     note_launch();
     return cudaGetLastError();
 }
