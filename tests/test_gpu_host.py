@@ -159,3 +159,28 @@ def test_plan_graph_replay_pinned(cuda, tiled):
         plan.close()
     finally:
         P.tuning_set("spmv_plan_tiled", 0)
+
+
+def test_plan_with_long_rows_pinned(cuda):
+    """A skewed matrix through the plan: the long-row kernel runs inside the
+    captured graph (its workspace is reserved at plan creation)."""
+    import torch
+
+    rng = np.random.default_rng(8)
+    m = n = 30000
+    lens = np.minimum(rng.zipf(1.6, m), 2500)
+    lens[[5, 7000, 29000]] = 12000
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    col = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(np.int32)
+    val = rng.uniform(-1, 1, rp[-1])
+    plan = P.SpmvPlan(rp, col, val, n)
+    hx = torch.from_numpy(rng.uniform(-1, 1, n)).pin_memory()
+    hy = torch.empty(m, dtype=torch.float64).pin_memory()
+    for _ in range(3):
+        plan.execute_host(hx, hy)
+        assert O.rel_err(hy.numpy(), O.spmv_csr(rp, col, val, hx.numpy())) <= 1e-12
+    dy = torch.empty(m, dtype=torch.float64, device="cuda")
+    plan.execute(hx.cuda(), dy)
+    torch.cuda.synchronize()
+    assert O.rel_err(dy.cpu().numpy(), O.spmv_csr(rp, col, val, hx.numpy())) <= 1e-12
+    plan.close()
