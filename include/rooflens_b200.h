@@ -269,6 +269,14 @@ RL_API int rl_tensor_alpha(const rl_hw_spec* spec, rl_precision precision, doubl
 RL_API int rl_attainable(const rl_hw_spec* spec, rl_unit unit, rl_precision precision,
                   double intensity, double* out);
 RL_API int rl_classify(double intensity, double balance);
+/* ridge_point (roofline.cpp:36-38) and sample_curve (roofline.cpp:40-79):
+ * n_points log-spaced intensities in [i_min, i_max] plus the ridge when it
+ * falls inside; writes *count (<= n_points + 1) pairs into intensity[] and
+ * attainable[] (capacity entries each; InvalidRange if too small). */
+RL_API int rl_ridge_point(const rl_hw_spec* spec, rl_unit unit, rl_precision precision, double* out);
+RL_API int rl_sample_curve(const rl_hw_spec* spec, rl_unit unit, rl_precision precision, double i_min,
+                           double i_max, uint64_t n_points, double* intensity, double* attainable,
+                           uint64_t capacity, uint64_t* count);
 /* bounds.cpp:56-62, 72-135. */
 RL_API int rl_unoverlapped_speedup(double t_cmp, double t_mem, double t_others, double alpha,
                             double* out);

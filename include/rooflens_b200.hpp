@@ -136,6 +136,11 @@ enum class Boundedness { MemoryBound, ComputeBound, Balanced };
 double attainable(const HardwareSpec& spec, ExecutionUnit unit, Precision precision,
                   double intensity);
 Boundedness classify(double intensity, double balance);
+// ridge_point / sample_curve (roofline.cpp:36-79): (intensity, attainable) pairs.
+double ridge_point(const HardwareSpec& spec, ExecutionUnit unit, Precision precision);
+std::vector<std::pair<double, double>> sample_curve(const HardwareSpec& spec, ExecutionUnit unit,
+                                                    Precision precision, double i_min, double i_max,
+                                                    std::size_t n_points);
 
 // Bounds (bounds.cpp:56-135).
 double unoverlapped_speedup(double t_cmp, double t_mem, double t_others, double alpha);

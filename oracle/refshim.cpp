@@ -150,6 +150,21 @@ int ref_classify(double intensity, double balance) {
     return static_cast<int>(classify(intensity, balance));
 }
 
+// sample_curve (roofline.cpp:40-79) into caller arrays of `cap` entries.
+int ref_sample_curve(double bw, double p_cc, double p_tc, int unit, double i_min, double i_max,
+                     uint64_t n, double* xs, double* ys, uint64_t cap, uint64_t* count) {
+    return guarded([&] {
+        const auto pts = sample_curve(mk(bw, p_cc, p_tc), unit_of(unit), Precision::FP64, i_min, i_max,
+                                      (std::size_t)n);
+        if (pts.size() > cap) throw Error(ErrorKind::InvalidRange, "capacity");
+        for (std::size_t k = 0; k < pts.size(); ++k) {
+            xs[k] = pts[k].intensity;
+            ys[k] = pts[k].attainable;
+        }
+        *count = pts.size();
+    });
+}
+
 int ref_kernel_speedup_ceiling(double alpha, double balance, double intensity, double* out,
                                int* n_warnings) {
     return guarded([&] {

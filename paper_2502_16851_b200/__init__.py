@@ -33,7 +33,7 @@ __all__ = [
     "spmv_csr_model", "stencil_model", "stencil_preset", "stencil_default_weights", "scale",
     "gemv", "spmv_csr", "spmv_csr_rows", "stencil", "stencil_temporal", "stencil_sweep", "scale_host", "spmv_csr_host",
     "stencil_host", "SpmvPlan", "mtx_stats", "mtx_read_csr", "matrix_analysis", "fill_uniform", "gen_band_csr", "stencil_init", "load_spec", "builtin_spec",
-    "machine_balance", "tensor_alpha", "attainable", "classify", "unoverlapped_speedup",
+    "machine_balance", "tensor_alpha", "attainable", "classify", "ridge_point", "sample_curve", "unoverlapped_speedup",
     "kernel_speedup_ceiling", "tensor_core_ceiling", "workload_ceiling", "min_temporal_depth",
     "tc_scale_trick_throughput", "fp64_peak_launch", "tuning_set", "kernel_launches",
     "ERROR_KINDS", "EXPORTED_SYMBOLS",
@@ -163,6 +163,8 @@ _SIGNATURES = {
     "rl_tensor_alpha": (_int, [_HP, _int, C.POINTER(_dbl)]),
     "rl_attainable": (_int, [_HP, _int, _int, _dbl, C.POINTER(_dbl)]),
     "rl_classify": (_int, [_dbl, _dbl]),
+    "rl_ridge_point": (_int, [_HP, _int, _int, C.POINTER(_dbl)]),
+    "rl_sample_curve": (_int, [_HP, _int, _int, _dbl, _dbl, _u64, _ptr, _ptr, _u64, C.POINTER(_u64)]),
     "rl_unoverlapped_speedup": (_int, [_dbl, _dbl, _dbl, _dbl, C.POINTER(_dbl)]),
     "rl_kernel_speedup_ceiling": (_int, [_dbl, _dbl, _dbl, C.POINTER(_dbl), C.POINTER(_int)]),
     "rl_tensor_core_ceiling": (_int, [_dbl, C.POINTER(_dbl)]),
@@ -593,6 +595,26 @@ def attainable(spec: HardwareSpec, intensity: float, unit: int = CUDA_CORE,
 
 def classify(intensity: float, balance: float) -> int:
     return lib().rl_classify(float(intensity), float(balance))
+
+
+def ridge_point(spec: HardwareSpec, unit: int = CUDA_CORE, precision: int = FP64) -> float:
+    s = spec._c()
+    return _d1(lib().rl_ridge_point, C.byref(s), unit, precision)
+
+
+def sample_curve(spec: HardwareSpec, i_min: float, i_max: float, n_points: int, unit: int = CUDA_CORE,
+                 precision: int = FP64):
+    """[(intensity, attainable)] as the reference's sample_curve (roofline.cpp:40-79)."""
+    import numpy as np
+
+    s = spec._c()
+    cap = int(n_points) + 1
+    xs = np.empty(cap, np.float64)
+    ys = np.empty(cap, np.float64)
+    cnt = _u64()
+    _check(lib().rl_sample_curve(C.byref(s), unit, precision, float(i_min), float(i_max), int(n_points),
+                                 xs.ctypes.data, ys.ctypes.data, cap, C.byref(cnt)))
+    return list(zip(xs[:cnt.value].tolist(), ys[:cnt.value].tolist()))
 
 
 def unoverlapped_speedup(t_cmp, t_mem, t_others, alpha) -> float:

@@ -28,7 +28,7 @@ import os
 import sys
 
 from . import (CUDA_CORE, FP64, TENSOR_CORE, HardwareSpec, RooflensError, attainable, builtin_spec,
-               classify, gemv_model, kernel_speedup_ceiling, load_spec, machine_balance, matrix_analysis,
+               classify, gemv_model, sample_curve as _sample_curve, kernel_speedup_ceiling, load_spec, machine_balance, matrix_analysis,
                min_temporal_depth, mtx_stats, scale_model, spmv_csr_model, stencil_model, stencil_preset,
                tensor_alpha, tensor_core_ceiling, workload_ceiling)
 
@@ -208,24 +208,11 @@ def cmd_matrix(args, out):
 
 
 def sample_curve(spec: HardwareSpec, unit: int, i_min: float, i_max: float, n: int):
-    """reference roofline.cpp:40-79: n log-spaced intensities plus the ridge."""
+    """reference roofline.cpp:40-79 through the C-ABI (rl_sample_curve)."""
     if not (i_min > 0 and i_min < i_max) or n < 2:
         raise UsageError("need 0 < i_min < i_max and points >= 2")
-    xs = []
-    for k in range(n):
-        if k == 0:
-            xs.append(i_min)
-        elif k == n - 1:
-            xs.append(i_max)
-        else:
-            f = k / (n - 1)
-            xs.append(math.exp(math.log(i_min) + f * (math.log(i_max) - math.log(i_min))))
-    ridge = machine_balance(spec, unit)
-    if i_min <= ridge <= i_max and ridge not in xs:
-        xs.append(ridge)
-        xs.sort()
     name = "FP64 " + ("CudaCore" if unit == CUDA_CORE else "TensorCore")
-    return [(x, attainable(spec, x, unit), name) for x in xs]
+    return [(x, y, name) for x, y in _sample_curve(spec, i_min, i_max, n, unit=unit)]
 
 
 def cmd_roofline(args, out):

@@ -1005,6 +1005,29 @@ int rl_attainable(const rl_hw_spec* s, rl_unit u, rl_precision p, double i, doub
     return guarded([&] { *out = attainable(spec_of(s), unit_of(u), prec_of(p), i); });
 }
 int rl_classify(double i, double b) { return static_cast<int>(classify(i, b)); }
+int rl_ridge_point(const rl_hw_spec* s, rl_unit u, rl_precision p, double* out) {
+    return guarded([&] {
+        require_ptr(s, "spec");
+        require_ptr(out, "out");
+        *out = ridge_point(spec_of(s), unit_of(u), prec_of(p));
+    });
+}
+int rl_sample_curve(const rl_hw_spec* s, rl_unit u, rl_precision p, double i_min, double i_max, uint64_t n,
+                    double* xs, double* ys, uint64_t capacity, uint64_t* count) {
+    return guarded([&] {
+        require_ptr(s, "spec");
+        require_ptr(count, "count");
+        const auto pts = sample_curve(spec_of(s), unit_of(u), prec_of(p), i_min, i_max, (std::size_t)n);
+        if (pts.size() > capacity) throw Error(ErrorKind::InvalidRange, "output capacity too small");
+        require_ptr(xs, "intensity");
+        require_ptr(ys, "attainable");
+        for (std::size_t k = 0; k < pts.size(); ++k) {
+            xs[k] = pts[k].first;
+            ys[k] = pts[k].second;
+        }
+        *count = pts.size();
+    });
+}
 int rl_unoverlapped_speedup(double tc, double tm, double to, double a, double* out) {
     return guarded([&] { *out = unoverlapped_speedup(tc, tm, to, a); });
 }

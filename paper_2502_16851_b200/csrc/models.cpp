@@ -286,6 +286,35 @@ Boundedness classify(double intensity, double balance) {
                                  : Boundedness::Balanced;
 }
 
+// ridge_point / sample_curve (reference roofline.cpp:36-79): n log-spaced
+// intensities from i_min to i_max (endpoints exact), the ridge inserted in
+// order when it lies inside and is not already a sample.
+double ridge_point(const HardwareSpec& s, ExecutionUnit u, Precision p) { return machine_balance(s, u, p); }
+
+std::vector<std::pair<double, double>> sample_curve(const HardwareSpec& s, ExecutionUnit u, Precision p,
+                                                    double i_min, double i_max, std::size_t n_points) {
+    if (!(i_min > 0.0) || !(i_min < i_max)) throw Error(ErrorKind::InvalidRange, "need 0 < i_min < i_max");
+    if (n_points < 2) throw Error(ErrorKind::InvalidRange, "need n_points >= 2");
+    std::vector<double> xs;
+    xs.reserve(n_points + 1);
+    const double lo = std::log(i_min), hi = std::log(i_max);
+    for (std::size_t k = 0; k < n_points; ++k) {
+        if (k == 0)
+            xs.push_back(i_min);
+        else if (k == n_points - 1)
+            xs.push_back(i_max);
+        else
+            xs.push_back(std::exp(lo + (static_cast<double>(k) / static_cast<double>(n_points - 1)) * (hi - lo)));
+    }
+    const double ridge = ridge_point(s, u, p);
+    if (ridge >= i_min && ridge <= i_max && std::find(xs.begin(), xs.end(), ridge) == xs.end())
+        xs.insert(std::upper_bound(xs.begin(), xs.end(), ridge), ridge);
+    std::vector<std::pair<double, double>> out;
+    out.reserve(xs.size());
+    for (double i : xs) out.emplace_back(i, attainable(s, u, p, i));
+    return out;
+}
+
 // ---------------------------------------------------------------------------
 // Bounds
 // ---------------------------------------------------------------------------

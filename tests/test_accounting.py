@@ -173,3 +173,35 @@ def test_baseline_known_answers():
     assert P.stencil_model("3d7pt") == P.KernelCharacterization(14, 16)
     assert P.stencil_model("3d27pt") == P.KernelCharacterization(54, 16)
     assert P.tensor_core_ceiling(2.0) == 4.0 / 3.0
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref absent")
+@pytest.mark.parametrize("unit", [P.CUDA_CORE, P.TENSOR_CORE])
+@pytest.mark.parametrize("lims", [(1e-3, 1e3, 2), (0.01, 100.0, 7), (1.0, 2.0, 33), (1e-2, 1e4, 128)])
+def test_sample_curve_matches_reference(unit, lims):
+    """ridge_point / sample_curve (roofline.cpp:36-79): identical samples,
+    the ridge inserted in order, bit-exact doubles."""
+    import ctypes as C
+
+    import numpy as np
+
+    spec = P.HardwareSpec("B200", 6.5431e12, 126e6, 36.43e12, 37.15e12)
+    i_min, i_max, n = lims
+    got = P.sample_curve(spec, i_min, i_max, n, unit=unit)
+    xs = np.empty(n + 1)
+    ys = np.empty(n + 1)
+    cnt = C.c_uint64()
+    rc = O.ref().ref_sample_curve(spec.memory_bandwidth, spec.peak_cuda_core, spec.peak_tensor_core, unit,
+                                  i_min, i_max, n, xs.ctypes.data, ys.ctypes.data, n + 1, C.byref(cnt))
+    assert rc == 0
+    want = list(zip(xs[:cnt.value].tolist(), ys[:cnt.value].tolist()))
+    assert got == want
+    assert P.ridge_point(spec, unit) == P.machine_balance(spec, unit)
+
+
+def test_sample_curve_errors():
+    spec = P.HardwareSpec("B200", 6.5431e12, 126e6, 36.43e12, 37.15e12)
+    for args in ((0.0, 1.0, 4), (2.0, 1.0, 4), (1.0, 2.0, 1)):
+        with pytest.raises(P.RooflensError) as e:
+            P.sample_curve(spec, *args)
+        assert e.value.kind == "InvalidRange"
