@@ -280,6 +280,10 @@ RL_API int rl_sample_curve(const rl_hw_spec* spec, rl_unit unit, rl_precision pr
 /* bounds.cpp:56-62, 72-135. */
 RL_API int rl_unoverlapped_speedup(double t_cmp, double t_mem, double t_others, double alpha,
                             double* out);
+/* mem_cmp_ratio = B / I (bounds.cpp:45-48); overlapped_total = max of the
+ * time components (bounds.cpp:50-53). */
+RL_API int rl_mem_cmp_ratio(double balance, double intensity, double* out);
+RL_API int rl_overlapped_total(double t_cmp, double t_mem, double t_others, double* out);
 RL_API int rl_kernel_speedup_ceiling(double alpha, double balance, double intensity, double* out,
                               int* n_warnings);
 RL_API int rl_tensor_core_ceiling(double alpha, double* out);

@@ -143,6 +143,8 @@ std::vector<std::pair<double, double>> sample_curve(const HardwareSpec& spec, Ex
                                                     std::size_t n_points);
 
 // Bounds (bounds.cpp:56-135).
+double mem_cmp_ratio(double balance, double intensity);
+double overlapped_total(double t_cmp, double t_mem, double t_others);
 double unoverlapped_speedup(double t_cmp, double t_mem, double t_others, double alpha);
 double kernel_speedup_ceiling(double alpha, double balance, double intensity, int* n_warnings);
 double tensor_core_ceiling(double alpha);

@@ -57,6 +57,8 @@ _REF_SIGS = {
     "ref_tensor_alpha": (_int, [_dbl, _dbl, _dbl, _DP]),
     "ref_attainable": (_int, [_dbl, _dbl, _dbl, _int, _dbl, _DP]),
     "ref_classify": (_int, [_dbl, _dbl]),
+    "ref_mem_cmp_ratio": (_int, [_dbl, _dbl, _DP]),
+    "ref_overlapped_total": (_int, [_dbl, _dbl, _dbl, _DP]),
     "ref_sample_curve": (_int, [_dbl, _dbl, _dbl, _int, _dbl, _dbl, _u64, _ptr, _ptr, _u64, _U64P]),
     "ref_kernel_speedup_ceiling": (_int, [_dbl, _dbl, _dbl, _DP, C.POINTER(_int)]),
     "ref_tensor_core_ceiling": (_int, [_dbl, _DP]),

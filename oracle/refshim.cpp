@@ -187,6 +187,14 @@ int ref_unoverlapped_speedup(double t_cmp, double t_mem, double t_others, double
     return guarded([&] { *out = unoverlapped_speedup(TimeBreakdown{t_cmp, t_mem, t_others}, alpha); });
 }
 
+int ref_mem_cmp_ratio(double balance, double intensity, double* out) {
+    return guarded([&] { *out = mem_cmp_ratio(balance, intensity); });
+}
+
+int ref_overlapped_total(double t_cmp, double t_mem, double t_others, double* out) {
+    return guarded([&] { *out = overlapped_total(TimeBreakdown{t_cmp, t_mem, t_others}); });
+}
+
 int ref_min_temporal_depth(double balance, double intensity, uint64_t* out) {
     return guarded([&] { *out = min_temporal_depth(balance, intensity); });
 }

@@ -33,7 +33,7 @@ __all__ = [
     "spmv_csr_model", "stencil_model", "stencil_preset", "stencil_default_weights", "scale",
     "gemv", "spmv_csr", "spmv_csr_rows", "stencil", "stencil_temporal", "stencil_sweep", "scale_host", "spmv_csr_host",
     "stencil_host", "SpmvPlan", "mtx_stats", "mtx_read_csr", "matrix_analysis", "fill_uniform", "gen_band_csr", "stencil_init", "load_spec", "builtin_spec",
-    "machine_balance", "tensor_alpha", "attainable", "classify", "ridge_point", "sample_curve", "unoverlapped_speedup",
+    "machine_balance", "tensor_alpha", "attainable", "classify", "ridge_point", "sample_curve", "mem_cmp_ratio", "overlapped_total", "unoverlapped_speedup",
     "kernel_speedup_ceiling", "tensor_core_ceiling", "workload_ceiling", "min_temporal_depth",
     "tc_scale_trick_throughput", "fp64_peak_launch", "tuning_set", "kernel_launches",
     "ERROR_KINDS", "EXPORTED_SYMBOLS",
@@ -164,6 +164,8 @@ _SIGNATURES = {
     "rl_attainable": (_int, [_HP, _int, _int, _dbl, C.POINTER(_dbl)]),
     "rl_classify": (_int, [_dbl, _dbl]),
     "rl_ridge_point": (_int, [_HP, _int, _int, C.POINTER(_dbl)]),
+    "rl_mem_cmp_ratio": (_int, [_dbl, _dbl, C.POINTER(_dbl)]),
+    "rl_overlapped_total": (_int, [_dbl, _dbl, _dbl, C.POINTER(_dbl)]),
     "rl_sample_curve": (_int, [_HP, _int, _int, _dbl, _dbl, _u64, _ptr, _ptr, _u64, C.POINTER(_u64)]),
     "rl_unoverlapped_speedup": (_int, [_dbl, _dbl, _dbl, _dbl, C.POINTER(_dbl)]),
     "rl_kernel_speedup_ceiling": (_int, [_dbl, _dbl, _dbl, C.POINTER(_dbl), C.POINTER(_int)]),
@@ -615,6 +617,14 @@ def sample_curve(spec: HardwareSpec, i_min: float, i_max: float, n_points: int, 
     _check(lib().rl_sample_curve(C.byref(s), unit, precision, float(i_min), float(i_max), int(n_points),
                                  xs.ctypes.data, ys.ctypes.data, cap, C.byref(cnt)))
     return list(zip(xs[:cnt.value].tolist(), ys[:cnt.value].tolist()))
+
+
+def mem_cmp_ratio(balance, intensity) -> float:
+    return _d1(lib().rl_mem_cmp_ratio, float(balance), float(intensity))
+
+
+def overlapped_total(t_cmp, t_mem, t_others) -> float:
+    return _d1(lib().rl_overlapped_total, float(t_cmp), float(t_mem), float(t_others))
 
 
 def unoverlapped_speedup(t_cmp, t_mem, t_others, alpha) -> float:

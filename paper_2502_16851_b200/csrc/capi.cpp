@@ -1028,6 +1028,18 @@ int rl_sample_curve(const rl_hw_spec* s, rl_unit u, rl_precision p, double i_min
         *count = pts.size();
     });
 }
+int rl_mem_cmp_ratio(double b, double i, double* out) {
+    return guarded([&] {
+        require_ptr(out, "out");
+        *out = mem_cmp_ratio(b, i);
+    });
+}
+int rl_overlapped_total(double tc, double tm, double to, double* out) {
+    return guarded([&] {
+        require_ptr(out, "out");
+        *out = overlapped_total(tc, tm, to);
+    });
+}
 int rl_unoverlapped_speedup(double tc, double tm, double to, double a, double* out) {
     return guarded([&] { *out = unoverlapped_speedup(tc, tm, to, a); });
 }

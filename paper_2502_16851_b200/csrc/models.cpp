@@ -327,11 +327,27 @@ void need_intensity(double i) {
 }
 }  // namespace
 
-double unoverlapped_speedup(double t_cmp, double t_mem, double t_others, double alpha) {
+static void need_breakdown(double t_cmp, double t_mem, double t_others) {
     if (t_cmp < 0.0 || t_mem < 0.0 || t_others < 0.0)
         throw Error(ErrorKind::ValidationError, "time components must be >= 0");
     if (t_cmp == 0.0 && t_mem == 0.0 && t_others == 0.0)
         throw Error(ErrorKind::ValidationError, "time breakdown is all zero");
+}
+
+// mem_cmp_ratio (bounds.cpp:45-48): T_mem / T_cmp = B / I.
+double mem_cmp_ratio(double balance, double intensity) {
+    need_intensity(intensity);
+    return balance / intensity;
+}
+
+// overlapped_total (bounds.cpp:50-53): the fully overlapped time.
+double overlapped_total(double t_cmp, double t_mem, double t_others) {
+    need_breakdown(t_cmp, t_mem, t_others);
+    return std::max({t_cmp, t_mem, t_others});
+}
+
+double unoverlapped_speedup(double t_cmp, double t_mem, double t_others, double alpha) {
+    need_breakdown(t_cmp, t_mem, t_others);
     need_alpha(alpha);
     if (t_cmp == 0.0) return 1.0;
     return (t_cmp + t_mem + t_others) / (t_cmp / alpha + t_mem + t_others);

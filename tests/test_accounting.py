@@ -205,3 +205,28 @@ def test_sample_curve_errors():
         with pytest.raises(P.RooflensError) as e:
             P.sample_curve(spec, *args)
         assert e.value.kind == "InvalidRange"
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref absent")
+def test_mem_cmp_ratio_and_overlapped_total_match_reference():
+    import ctypes as C
+
+    rng = random.Random(7)
+    for _ in range(200):
+        b, i = rng.choice([0.0, 1.0, rng.uniform(0.1, 50)]), rng.choice([0.0, -1.0, rng.uniform(1e-3, 100)])
+        out = C.c_double()
+        rc = O.ref().ref_mem_cmp_ratio(b, i, C.byref(out))
+        if rc == 0:
+            assert P.mem_cmp_ratio(b, i) == out.value
+        else:
+            with pytest.raises(P.RooflensError) as e:
+                P.mem_cmp_ratio(b, i)
+            assert e.value.code == rc
+        t = [rng.choice([0.0, -1.0, rng.uniform(0, 10)]) for _ in range(3)]
+        rc = O.ref().ref_overlapped_total(*t, C.byref(out))
+        if rc == 0:
+            assert P.overlapped_total(*t) == out.value
+        else:
+            with pytest.raises(P.RooflensError) as e:
+                P.overlapped_total(*t)
+            assert e.value.code == rc
