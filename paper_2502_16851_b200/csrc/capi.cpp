@@ -212,7 +212,8 @@ KernelCharacterization stencil_temporal(ExecutionUnit unit, Precision p, const S
     if (t > 8) throw Error(ErrorKind::InvalidRange, "temporal depth > 8 is not implemented");
     const rlb::StencilDesc d = make_desc(shape, dims, weights);
     const bool use_tb = t >= 2 && rlb::tuning().stencil_tb && rlb::stencil_tb_supported(d, (int)t, u, v);
-    const bool use_tb3 = t >= 2 && rlb::stencil_tb3_supported(d, (int)t);
+    const bool use_tb3r = t >= 2 && rlb::tuning().stencil_tb3_mode && rlb::stencil_tb3r_supported(d, (int)t, u, v);
+    const bool use_tb3 = t >= 2 && (use_tb3r || rlb::stencil_tb3_supported(d, (int)t));
     const bool ok2d = d.preset == rlb::kP2d5 && (use_tb || (t == 2 && rlb::stencil_tma_eligible(d, u, v)));
     if (t >= 2 && (unit != ExecutionUnit::CudaCore || !(ok2d || use_tb3)))
         throw Error(ErrorKind::ValidationError,
@@ -229,7 +230,9 @@ KernelCharacterization stencil_temporal(ExecutionUnit unit, Precision p, const S
     for (std::uint64_t i = 0; i < fused + rem; ++i, ++sweeps) {
         const double* src = (sweeps & 1) ? v : u;
         double* dst = (sweeps & 1) ? u : v;
-        if (i < fused && use_tb3) {
+        if (i < fused && use_tb3r) {
+            cuda_check(rlb::launch_stencil_tb3r(d, (int)t, 1, outer - 1, src, dst, s), "stencil (3D temporal blocking)");
+        } else if (i < fused && use_tb3) {
             cuda_check(rlb::launch_stencil_tb3(d, (int)t, 1, outer - 1, src, dst, s), "stencil (3D temporal blocking)");
         } else if (i < fused && use_tb) {
             cuda_check(rlb::launch_stencil_tb(d, (int)t, 1, outer - 1, src, dst, s), "stencil (temporal blocking)");
@@ -1093,6 +1096,10 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         else if (k == "stencil_r_ctas_per_sm") slot = &t.stencil_r_ctas_per_sm;
         else if (k == "stencil_tb_waves") slot = &t.stencil_tb_waves;
         else if (k == "stencil_tb") slot = &t.stencil_tb;
+        else if (k == "stencil_tb3_mode") slot = &t.stencil_tb3_mode;
+        else if (k == "stencil_tb3_chunks") slot = &t.stencil_tb3_chunks;
+        else if (k == "stencil_tb3_shape") slot = &t.stencil_tb3_shape;
+        else if (k == "stencil_tb3_l2promo") slot = &t.stencil_tb3_l2promo;
         else if (k == "stencil3d_cc_stages") slot = &t.stencil3d_cc_stages;
         else if (k == "stencil_tc_concat") slot = &t.stencil_tc_concat;
         else if (k == "stencil_cc27x2") slot = &t.stencil_cc27x2;

@@ -51,6 +51,10 @@ struct Tuning {
     int stencil_r_ctas_per_sm = 32;
     int stencil_tb_waves = 4;          // register temporal blocking: grid = this many waves of resident warps
     int stencil_tb = 1;                // 1: temporal depth t >= 2 runs the register kernel (0: smem t=2 kernel)
+    int stencil_tb3_mode = 1;          // 3d7pt t >= 2: 1 register-blocked TMA kernel (stencil_tb3r.cu), 0 the z-column kernel
+    int stencil_tb3_shape = 0;         // stencil_tb3r rows per warp x warps: 0 default, 1 4x8, 2 2x16
+    int stencil_tb3_chunks = 0;        // z chunks per tile for stencil_tb3r (0: auto)
+    int stencil_tb3_l2promo = 3;       // TMA L2 promotion of the stencil_tb3r boxes (0 none .. 3 256 B)
     int stencil_r_l2promo = 1;         // ... TMA L2 promotion (0 none, 1 64 B, 2 128 B, 3 256 B)
     int stencil_r_sym = 1;             // 2d49pt CC: pair mirror-symmetric columns (fewer FP64 ops)    // 2d9pt/2d13pt/2d49pt TMA kernels: row segments so the grid is this deep
 };
@@ -113,6 +117,9 @@ cudaError_t launch_stencil_r(int unit, const StencilDesc& d, uint64_t o0, uint64
 bool tma_encode_available();
 bool encode_map_2d(void* map, const double* base, uint64_t nx, uint64_t ny, uint32_t box_x, uint32_t box_y,
                    int l2_promotion = 3);  // 0 none, 1 64 B, 2 128 B, 3 256 B
+// 3D FP64 tensor map (box_x x box_y x 1), same conventions.
+bool encode_map_3d(void* map, const double* base, uint64_t nx, uint64_t ny, uint64_t nz, uint32_t box_x,
+                   uint32_t box_y, int l2_promotion = 3);
 
 // 2d5pt with temporal depth t (2..8) in registers (stencil_tb.cu).
 bool stencil_tb_supported(const StencilDesc& d, int t, const double* u, const double* v);
@@ -123,6 +130,12 @@ cudaError_t launch_stencil_tb(const StencilDesc& d, int t, uint64_t o0, uint64_t
 bool stencil_tb3_supported(const StencilDesc& d, int t);
 cudaError_t launch_stencil_tb3(const StencilDesc& d, int t, uint64_t o0, uint64_t o1, const double* u, double* v,
                                cudaStream_t s);
+// 3d7pt with temporal depth t (2..4), register-blocked and skewed: TMA plane
+// tiles, one barrier per input plane (stencil_tb3r.cu).  Needs an even nx
+// and 16-byte aligned u / v.
+bool stencil_tb3r_supported(const StencilDesc& d, int t, const double* u, const double* v);
+cudaError_t launch_stencil_tb3r(const StencilDesc& d, int t, uint64_t o0, uint64_t o1, const double* u, double* v,
+                                cudaStream_t s);
 
 // Two fused timesteps of 2d5pt (temporal blocking, CUDA core, TMA-eligible grids).
 cudaError_t launch_stencil_tma_t2(const StencilDesc& d, uint64_t o0, uint64_t o1, const double* u,

@@ -1042,6 +1042,22 @@ bool encode_map_2d(void* map, const double* base, uint64_t nx, uint64_t ny, uint
               promo[l2_promotion & 3], CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+bool encode_map_3d(void* map, const double* base, uint64_t nx, uint64_t ny, uint64_t nz, uint32_t box_x,
+                   uint32_t box_y, int l2_promotion) {
+    static const CUtensorMapL2promotion promo[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
+                                                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t gdim[3] = {nx, ny, nz};
+    cuuint64_t gstride[2] = {nx * 8, nx * ny * 8};
+    cuuint32_t box[3] = {box_x, box_y, 1};
+    cuuint32_t estride[3] = {1, 1, 1};
+    return fn(static_cast<CUtensorMap*>(map), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), gdim,
+              gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+              promo[l2_promotion & 3], CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 cudaError_t launch_stencil_tma_t2(const StencilDesc& d, uint64_t o0, uint64_t o1, const double* u,
                                   double* v, cudaStream_t s) {
     auto fn = encode_fn();

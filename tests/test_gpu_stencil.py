@@ -277,11 +277,14 @@ def test_2d5pt_temporal_depth_t(cuda, t, shape, kernel):
         P.tuning_set("stencil_tb", 1)
 
 
+@pytest.mark.parametrize("mode", [1, 0])
 @pytest.mark.parametrize("t", [2, 3, 4])
-@pytest.mark.parametrize("shape", [(9, 10, 11), (20, 24, 68), (33, 40, 70), (64, 50, 97)])
-def test_3d7pt_temporal_depth_t(cuda, t, shape):
-    """3d7pt temporal depth t (z-marching register pipeline) equals single
-    timesteps; custom weights; the Dirichlet shell stays bit-exact."""
+@pytest.mark.parametrize("shape", [(9, 10, 11), (20, 24, 68), (33, 40, 70), (64, 50, 97), (37, 130, 126),
+                                   (70, 29, 200)])
+def test_3d7pt_temporal_depth_t(cuda, mode, t, shape):
+    """3d7pt temporal depth t equals single timesteps; custom weights; the
+    Dirichlet shell stays bit-exact.  mode 1: the register-blocked TMA kernel
+    (stencil_tb3r.cu; odd nx falls back), mode 0: the z-column kernel."""
     import torch
 
     u0 = O.stencil_init(shape, 1, 29)
@@ -289,8 +292,12 @@ def test_3d7pt_temporal_depth_t(cuda, t, shape):
     steps = 2 * t + 1
     u = torch.from_numpy(u0.copy()).cuda()
     v = torch.from_numpy(u0.copy()).cuda()
-    kc, out = P.stencil_temporal("3d7pt", u, v, steps, t, weights=w)
-    torch.cuda.synchronize()
+    P.tuning_set("stencil_tb3_mode", mode)
+    try:
+        kc, out = P.stencil_temporal("3d7pt", u, v, steps, t, weights=w)
+        torch.cuda.synchronize()
+    finally:
+        P.tuning_set("stencil_tb3_mode", 1)
     got = out.cpu().numpy()
     assert O.rel_err(got, O.stencil("3d7pt", u0, steps, w)) <= TOL
     ring = _ring_mask(shape, 1)
@@ -339,3 +346,29 @@ def test_3d_tensor_core_formulations(cuda, mode, preset, shape):
             assert O.rel_err(out, O.stencil(preset, u0, 2, w)) <= TOL
     finally:
         P.tuning_set("stencil_tc3d_mode", prev)
+
+
+@pytest.mark.parametrize("shape_knob", [0, 1, 2])
+@pytest.mark.parametrize("t", [2, 3, 4])
+@pytest.mark.parametrize("chunks", [1, 3, 7])
+def test_3d7pt_temporal_z_chunks(cuda, t, chunks, shape_knob):
+    """The register-blocked 3D kernel split into z chunks (each chunk
+    re-loads its 2t-plane cone) gives the same result as single steps."""
+    import torch
+
+    shape = (45, 66, 134)
+    u0 = O.stencil_init(shape, 1, 31)
+    u = torch.from_numpy(u0.copy()).cuda()
+    v = torch.from_numpy(u0.copy()).cuda()
+    P.tuning_set("stencil_tb3_chunks", chunks)
+    P.tuning_set("stencil_tb3_shape", shape_knob)
+    try:
+        _, out = P.stencil_temporal("3d7pt", u, v, 2 * t, t)
+        torch.cuda.synchronize()
+    finally:
+        P.tuning_set("stencil_tb3_chunks", 0)
+        P.tuning_set("stencil_tb3_shape", 0)
+    got = out.cpu().numpy()
+    assert O.rel_err(got, O.stencil("3d7pt", u0, 2 * t)) <= TOL
+    ring = _ring_mask(shape, 1)
+    assert O.bit_mismatches(got[ring], u0[ring]) == 0

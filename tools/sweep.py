@@ -108,21 +108,31 @@ def temporal_t():
 
 
 def temporal_3d():
-    """3d7pt at 512^3: ms per timestep for temporal depth 1..4."""
+    """3d7pt at 512^3: ms per timestep for temporal depth 1..4, both 3D
+    temporal kernels (TB3_MODES), z-chunk counts from TB3_CHUNKS (0 = auto)."""
     u = torch.empty((512, 512, 512), dtype=torch.float64, device="cuda")
     P.stencil_init(u, 1, 1)
     v = u.clone()
-    waves_list = [int(x) for x in os.environ.get("TB_WAVES", "4").split(",")]
+    modes = [int(x) for x in os.environ.get("TB3_MODES", "1,0").split(",")]
+    chunks = [int(x) for x in os.environ.get("TB3_CHUNKS", "0").split(",")]
+    shapes = [int(x) for x in os.environ.get("TB3_SHAPES", "0").split(",")]
     for t in (1, 2, 3, 4):
-        for waves in (waves_list if t > 1 else [1]):
-            P.tuning_set("stencil_tb_waves", waves)
-            steps = 4 * t
-            fn = (lambda: P.stencil("3d7pt", u, v, steps)) if t == 1 else \
-                (lambda: P.stencil_temporal("3d7pt", u, v, steps, t))
-            ms = timeit(fn, reps=5, warm=2) / steps
-            print(json.dumps({"kernel": "3d7pt_temporal", "t": t, "waves": waves, "ms_per_timestep": round(ms, 4),
-                              "timestep_gbs_equiv": round(16 * 510 ** 3 / ms / 1e6, 1)}), flush=True)
-    P.tuning_set("stencil_tb_waves", 4)
+        for mode in (modes if t > 1 else [1]):
+          for shp in (shapes if t > 1 and mode == 1 else [0]):
+            for ch in (chunks if t > 1 and mode == 1 else [0]):
+                P.tuning_set("stencil_tb3_shape", shp)
+                P.tuning_set("stencil_tb3_mode", mode)
+                P.tuning_set("stencil_tb3_chunks", ch)
+                steps = 4 * t
+                fn = (lambda: P.stencil("3d7pt", u, v, steps)) if t == 1 else \
+                    (lambda: P.stencil_temporal("3d7pt", u, v, steps, t))
+                ms = timeit(fn, reps=5, warm=2) / steps
+                print(json.dumps({"kernel": "3d7pt_temporal", "t": t, "mode": mode, "shape": shp, "chunks": ch,
+                                  "ms_per_timestep": round(ms, 4),
+                                  "timestep_gbs_equiv": round(16 * 510 ** 3 / ms / 1e6, 1)}), flush=True)
+    P.tuning_set("stencil_tb3_mode", 1)
+    P.tuning_set("stencil_tb3_chunks", 0)
+    P.tuning_set("stencil_tb3_shape", 0)
 
 
 def stencils():
