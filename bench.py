@@ -388,34 +388,40 @@ def cusparse_yardstick(torch, P, hbm, reps=20):
     return out
 
 
-def temporal_blocking(torch, P, hbm, t1_ms_per_step, depths=(2, 4, 5, 7)):
-    """2d5pt with temporal depth t on the BASELINE grid
-    (100 timesteps = floor(100/t) fused sweeps + the remainder as single
-    steps).  Model bytes are stencil_model(2d5pt, FP64, t): 16 B per point per
-    fused sweep (reference kernels.cpp:137-155)."""
-    shape = (16384, 16384)
-    u = torch.empty(shape, dtype=torch.float64, device="cuda")
-    P.stencil_init(u, 1, SEED)
-    v = u.clone()
+def temporal_blocking(torch, P, hbm, t1_ms_per_step, t1_ms_per_step_3d=None, depths=(2, 4, 5, 7),
+                      depths_3d=(2, 3, 4)):
+    """2d5pt (16384^2, 100 timesteps) and 3d7pt (512^3, 50
+    timesteps) with temporal depth t on the BASELINE grids: floor(steps/t)
+    fused sweeps + the remainder as single steps.  Model bytes are
+    stencil_model(preset, FP64, t): 16 B per point per fused sweep (reference
+    kernels.cpp:137-155)."""
     out = {}
-    for t in depths:
-        P.stencil_temporal("2d5pt", u, v, 2 * t, t)
-        torch.cuda.synchronize()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        kc, _ = P.stencil_temporal("2d5pt", u, v, 100, t)
-        e.record()
-        torch.cuda.synchronize()
-        ms = s.elapsed_time(e)
-        gbs = kc.traffic_bytes / (ms * 1e-3) / 1e9
-        out[f"2d5pt_t{t}"] = {"ms_per_timestep": round(ms / 100, 4), "model_gbs": round(gbs, 1),
-                              "frac_of_measured_peak": round(gbs / hbm, 4),
-                              "timestep_speedup_vs_t1": round(t1_ms_per_step / (ms / 100), 3)}
-    del u, v
-    torch.cuda.empty_cache()
-    out["note"] = ("register-pipelined kernel (stencil_tb.cu): one HBM read + write per t timesteps; "
-                   "bytes = stencil_model(t) per fused sweep, so model_gbs falls as t rises while the "
-                   "per-timestep time drops")
+    for preset, shape, steps, ds, t1 in (("2d5pt", (16384, 16384), 100, depths, t1_ms_per_step),
+                                          ("3d7pt", (512, 512, 512), 50, depths_3d, t1_ms_per_step_3d)):
+        u = torch.empty(shape, dtype=torch.float64, device="cuda")
+        P.stencil_init(u, 1, SEED)
+        v = u.clone()
+        for t in ds:
+            P.stencil_temporal(preset, u, v, 2 * t, t)
+            torch.cuda.synchronize()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            kc, _ = P.stencil_temporal(preset, u, v, steps, t)
+            e.record()
+            torch.cuda.synchronize()
+            ms = s.elapsed_time(e)
+            gbs = kc.traffic_bytes / (ms * 1e-3) / 1e9
+            row = {"ms_per_timestep": round(ms / steps, 4), "model_gbs": round(gbs, 1),
+                   "frac_of_measured_peak": round(gbs / hbm, 4)}
+            if t1:
+                row["timestep_speedup_vs_t1"] = round(t1 / (ms / steps), 3)
+            out[f"{preset}_t{t}"] = row
+        del u, v
+        torch.cuda.empty_cache()
+    out["note"] = ("2d5pt: register-pipelined strips (stencil_tb.cu); 3d7pt: register-blocked TMA tiles, one "
+                   "barrier per plane (stencil_tb3r.cu).  One HBM read + write per t timesteps; bytes = "
+                   "stencil_model(t) per fused sweep, so model_gbs falls as t rises while the per-timestep "
+                   "time drops")
     return out
 
 
@@ -737,7 +743,8 @@ def main():
             table = per_kernel_table(torch, P, D, hbm)
             table["spmv"]["cusparse_cc_yardstick"] = cusparse_yardstick(torch, P, hbm)
             line["temporal_blocking"] = temporal_blocking(torch, P, hbm,
-                                                          table["2d5pt"]["cc"]["ms_per_unit"])
+                                                          table["2d5pt"]["cc"]["ms_per_unit"],
+                                                          table["3d7pt"]["cc"]["ms_per_unit"])
             line["next_rows"] = {"gemv": gemv_rows(torch, P, hbm), **stencil_preset_rows(torch, P, hbm)}
         # FP64 peaks last: the DFMA/DMMA chains run at the power cap and would
         # throttle the memory-bound kernels measured after them.
