@@ -39,6 +39,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tma.cuh"
 
 namespace rlb {
 
@@ -83,15 +84,7 @@ constexpr uint32_t kEnd = 1u << 22;            // last entry of its row's run in
 constexpr int kDepthShift = 23;                // bits 23-27 (lane's first entry): lanes the carry spans
 constexpr uint32_t kLaneStart = 1u << 28;      // (lane's first entry) a run starts in this lane
 
-__device__ __forceinline__ uint32_t sptr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
-            "r"(sptr(dst)),
-        "l"(src), "r"(bytes), "r"(sptr(bar)), "l"(pol)
-        : "memory");
-}
+using namespace tmaop;  // mbarrier / bulk-copy primitives (tma.cuh)
 
 __global__ void __launch_bounds__(kThreads, 1) spmv_tiled_kernel(uint64_t m, uint64_t b_first,
                                                                  const uint8_t* __restrict__ segs,
@@ -115,10 +108,10 @@ __global__ void __launch_bounds__(kThreads, 1) spmv_tiled_kernel(uint64_t m, uin
     for (int i = tid; i < nt && i < kDescCache; i += kThreads) desc[i] = tiles[t0 + i];
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sptr(full + s)) : "memory");
+            mbar_init(full + s, 1);
             cnt[s] = 0;
         }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_fence_init();
     }
     __syncthreads();
     auto issue = [&](int k) {
@@ -127,8 +120,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmv_tiled_kernel(uint64_t m, uin
         const uint32_t xb = (uint32_t)(t.width * 8);
         const uint32_t sb = (uint32_t)t.seg_bytes;
         uint64_t* bar = full + (k % kStages);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sptr(bar)), "r"(xb + sb)
-                     : "memory");
+        mbar_expect_tx(bar, xb + sb);
         bulk_g2s(st, x + t.col_base, xb, bar, policy_evict_last());
         bulk_g2s(st + kXBytes, segs + t.seg_offset, sb, bar, policy_evict_first());
     };
@@ -137,11 +129,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmv_tiled_kernel(uint64_t m, uin
     for (int k = 0; k < nt; ++k) {
         const int s = k % kStages;
         const uint32_t parity = (uint32_t)((k / kStages) & 1);
-        asm volatile(
-            "{\n .reg .pred P;\nRLB_TW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2;\n"
-            " @!P bra RLB_TW_%=;\n}" ::"r"(sptr(full + s)),
-            "r"(parity), "r"(1000000u)
-            : "memory");
+        mbar_wait_hint(full + s, parity, 1000000u);
         const uint8_t* st = smem + s * kStageBytes;
         const double* xs = reinterpret_cast<const double*>(st);
         const uint8_t* seg = st + kXBytes;

@@ -38,6 +38,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tma.cuh"
 
 namespace rlb {
 namespace {
@@ -46,17 +47,7 @@ constexpr int kTXr = 64;   // columns per strip
 constexpr int kTYr = 32;   // output rows per stage
 constexpr int kRYr = 8;    // output rows per thread (CC) / per DMMA tile
 
-__device__ __forceinline__ uint32_t sptr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sptr(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-    asm volatile(
-        "{\n .reg .pred P;\nRLB_RW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
-        " @!P bra RLB_RW_%=;\n}" ::"r"(sptr(b)),
-        "r"(parity)
-        : "memory");
-}
+using namespace tmaop;  // mbarrier / TMA primitives and the stage Ring (tma.cuh)
 
 template <int R>
 struct Geo {
@@ -107,44 +98,6 @@ __host__ __device__ constexpr bool has_tap(int dy, int dx) {
 }
 
 // Shared ring + producer for both units.
-template <int S, int STAGE>
-struct RingR {
-    double* base;
-    uint64_t* full;
-    uint64_t* empty;
-    __device__ RingR(double* smem) : base(smem) {
-        full = reinterpret_cast<uint64_t*>(smem + S * STAGE);
-        empty = full + S;
-    }
-    __device__ double* stage(int k) const { return base + (k % S) * STAGE; }
-    __device__ void init(int consumers) {
-        if (threadIdx.x == 0) {
-            for (int s = 0; s < S; ++s) {
-                mbar_init(full + s, 1);
-                mbar_init(empty + s, consumers);
-            }
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
-        __syncthreads();
-    }
-    __device__ void wait_full(int k) { mbar_wait(full + (k % S), (uint32_t)((k / S) & 1)); }
-    __device__ void release(int k) {
-        __syncwarp();
-        if ((threadIdx.x & 31) == 0)
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sptr(empty + (k % S))) : "memory");
-    }
-    __device__ void wait_empty(int k) { mbar_wait(empty + (k % S), (uint32_t)((k / S) & 1)); }
-    __device__ void issue(int k, const CUtensorMap* tm, int x, int y, uint32_t bytes) {
-        uint64_t* bar = full + (k % S);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sptr(bar)), "r"(bytes)
-                     : "memory");
-        asm volatile(
-            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
-                "r"(sptr(stage(k))),
-            "l"(tm), "r"(sptr(bar)), "r"(x), "r"(y)
-            : "memory");
-    }
-};
 
 // Store two adjacent outputs (x, x+1) of row y when interior.
 __device__ __forceinline__ void store_pair(double* v, uint64_t nx, int R, int64_t x, uint64_t y, double a,
@@ -233,7 +186,7 @@ __global__ void __launch_bounds__(128) st2dr_tma_cc(const __grid_constant__ CUte
                                                     int strips, const __grid_constant__ StencilDesc d) {
     constexpr int LP = Geo<R>::LP, P = pitch<R, false>(), STAGE = stage_doubles<R, false>();
     extern __shared__ __align__(128) double smem[];
-    RingR<S, STAGE> ring(smem);
+    Ring<S, STAGE> ring(smem);
     const int tid = threadIdx.x, lane = tid & 31, g = tid >> 5;
     const int64_t x0 = (int64_t)(blockIdx.x % strips) * kTXr;
     const uint64_t ya = y_begin + (uint64_t)(blockIdx.x / strips) * seg_rows;
@@ -244,7 +197,7 @@ __global__ void __launch_bounds__(128) st2dr_tma_cc(const __grid_constant__ CUte
     constexpr uint32_t kBytes = Geo<R>::ROWS * P * 8;
     if (tid == 0)
         for (int k = 0; k < S && k < nblk; ++k)
-            ring.issue(k, &tm, (int)(x0 - LP), (int)(ya + (uint64_t)k * kTYr) - R, kBytes);
+            ring.issue2d(k, &tm, (int)(x0 - LP), (int)(ya + (uint64_t)k * kTYr) - R, kBytes);
     const int64_t x = x0 + 2 * lane;
     for (int k = 0; k < nblk; ++k) {
         ring.wait_full(k);
@@ -257,7 +210,7 @@ __global__ void __launch_bounds__(128) st2dr_tma_cc(const __grid_constant__ CUte
         ring.release(k);
         if (tid == 0 && k + S < nblk) {
             ring.wait_empty(k);
-            ring.issue(k + S, &tm, (int)(x0 - LP), (int)(ya + (uint64_t)(k + S) * kTYr) - R, kBytes);
+            ring.issue2d(k + S, &tm, (int)(x0 - LP), (int)(ya + (uint64_t)(k + S) * kTYr) - R, kBytes);
         }
         const uint64_t yr = ya + (uint64_t)k * kTYr + kRYr * g;
 #pragma unroll
@@ -279,7 +232,7 @@ __global__ void __launch_bounds__(128) st2dr_tma_tc(const __grid_constant__ CUte
     // weights are mirror-symmetric in y (U[y-dy] + U[y+dy] share a band)
     constexpr int NDY = BOX ? (SYMY ? R + 1 : 2 * R + 1) : 1;
     extern __shared__ __align__(128) double smem[];
-    RingR<S, STAGE> ring(smem);
+    Ring<S, STAGE> ring(smem);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int fr = lane >> 2, fc = lane & 3;   // fragment row / column
     const int64_t x0 = (int64_t)(blockIdx.x % strips) * kTXr;
@@ -323,7 +276,7 @@ __global__ void __launch_bounds__(128) st2dr_tma_tc(const __grid_constant__ CUte
     constexpr uint32_t kBytes = Geo<R>::ROWS * P * 8;
     if (tid == 0)
         for (int k = 0; k < S && k < nblk; ++k)
-            ring.issue(k, &tm, (int)(x0 - LP), (int)(ya + (uint64_t)k * kTYr) - R, kBytes);
+            ring.issue2d(k, &tm, (int)(x0 - LP), (int)(ya + (uint64_t)k * kTYr) - R, kBytes);
     for (int k = 0; k < nblk; ++k) {
         ring.wait_full(k);
         const double* T = ring.stage(k);
@@ -363,7 +316,7 @@ __global__ void __launch_bounds__(128) st2dr_tma_tc(const __grid_constant__ CUte
         ring.release(k);
         if (tid == 0 && k + S < nblk) {
             ring.wait_empty(k);
-            ring.issue(k + S, &tm, (int)(x0 - LP), (int)(ya + (uint64_t)(k + S) * kTYr) - R, kBytes);
+            ring.issue2d(k + S, &tm, (int)(x0 - LP), (int)(ya + (uint64_t)(k + S) * kTYr) - R, kBytes);
         }
         const uint64_t ys = ya + (uint64_t)k * kTYr;
 #pragma unroll

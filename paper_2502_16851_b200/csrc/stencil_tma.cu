@@ -34,6 +34,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tma.cuh"
 
 namespace rlb {
 namespace {
@@ -42,78 +43,7 @@ constexpr int kTX = 64, kTY = 16, kRY = 8, kBY = kTY + 2;
 constexpr int kBX = 68;   // box / stage row width (doubles)
 constexpr int kCofs = 2;  // stage column of the tile's first x
 
-// ---------------------------------------------------------------------------
-// mbarrier / TMA primitives
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t sptr(const void* p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sptr(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sptr(b)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sptr(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-    asm volatile(
-        "{\n .reg .pred P;\n"
-        "RLB_WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
-        " @!P bra RLB_WAIT_%=;\n}" ::"r"(sptr(b)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* m, uint64_t* bar, int x, int y) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-            sptr(dst)),
-        "l"(m), "r"(sptr(bar)), "r"(x), "r"(y)
-        : "memory");
-}
-__device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* m, uint64_t* bar, int x, int y, int z) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
-            sptr(dst)),
-        "l"(m), "r"(sptr(bar)), "r"(x), "r"(y), "r"(z)
-        : "memory");
-}
-
-// Ring bookkeeping shared by all kernels: S stages of STAGE doubles, then
-// S full + S empty barriers.
-template <int S, int STAGE>
-struct Ring {
-    double* base;
-    uint64_t* full;
-    uint64_t* empty;
-    __device__ Ring(double* smem) : base(smem) {
-        full = reinterpret_cast<uint64_t*>(smem + S * STAGE);
-        empty = full + S;
-    }
-    __device__ double* stage(int k) const { return base + (k % S) * STAGE; }
-    __device__ void init(int consumers) {
-        if (threadIdx.x == 0) {
-            for (int s = 0; s < S; ++s) {
-                mbar_init(full + s, 1);
-                mbar_init(empty + s, consumers);
-            }
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
-        __syncthreads();
-    }
-    __device__ void wait_full(int k) { mbar_wait(full + (k % S), (uint32_t)((k / S) & 1)); }
-    // One arrive per warp once the whole warp has finished reading stage k.
-    __device__ void release(int k) {
-        __syncwarp();
-        if ((threadIdx.x & 31) == 0) mbar_arrive(empty + (k % S));
-    }
-    // Producer: before refilling the stage that held item k, wait until every
-    // consumer warp released item k.
-    __device__ void wait_empty(int k) { mbar_wait(empty + (k % S), (uint32_t)((k / S) & 1)); }
-};
+using namespace tmaop;  // mbarrier / TMA primitives and the stage Ring (tma.cuh)
 
 __host__ __device__ constexpr int stage_doubles(int bx) { return ((kBY * bx * 8 + 127) / 128) * 128 / 8; }
 template <int S, int BX>
