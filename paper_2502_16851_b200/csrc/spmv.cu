@@ -29,6 +29,42 @@
 namespace rlb {
 namespace {
 
+// val / col streaming loads.  RLB_SPMV_STREAM_L1 = 1 lets them allocate in
+// L1 (an experiment: L1::no_allocate scattered loads measured 2.4x slower
+// than allocating ones, tools/micro/tma_gather.cu).
+#ifndef RLB_SPMV_STREAM_L1
+#define RLB_SPMV_STREAM_L1 0
+#endif
+#if RLB_SPMV_STREAM_L1
+#define RLB_SP_NOALLOC ""
+#else
+#define RLB_SP_NOALLOC ".L1::no_allocate"
+#endif
+__device__ __forceinline__ d4 sp_ld4(const double* p, uint64_t pol) {
+    d4 v;
+    asm("ld.global.nc" RLB_SP_NOALLOC ".L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+        : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+        : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ int4 sp_ld4_i32(const int* p, uint64_t pol) {
+    int4 ci;
+    asm("ld.global.nc" RLB_SP_NOALLOC ".L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+        : "=r"(ci.x), "=r"(ci.y), "=r"(ci.z), "=r"(ci.w)
+        : "l"(p), "l"(pol));
+    return ci;
+}
+__device__ __forceinline__ double sp_ld(const double* p, uint64_t pol) {
+    double v;
+    asm("ld.global.nc" RLB_SP_NOALLOC ".L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ int sp_ld_i32(const int* p, uint64_t pol) {
+    int v;
+    asm("ld.global.nc" RLB_SP_NOALLOC ".L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
 struct Nz4 {
     double v[4];
     int c[4];
@@ -41,11 +77,8 @@ __device__ __forceinline__ Nz4 load_nz4(const int* __restrict__ col,
                                         int col_pad, uint64_t pol) {
     Nz4 z;
     if (((j & 3) == 0) && j + 4 <= e) {
-        const d4 v = ld4_stream(val + j, pol);
-        int4 ci;
-        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
-            : "=r"(ci.x), "=r"(ci.y), "=r"(ci.z), "=r"(ci.w)
-            : "l"(col + j), "l"(pol));
+        const d4 v = sp_ld4(val + j, pol);
+        const int4 ci = sp_ld4_i32(col + j, pol);
         z.v[0] = v.x; z.v[1] = v.y; z.v[2] = v.z; z.v[3] = v.w;
         z.c[0] = ci.x; z.c[1] = ci.y; z.c[2] = ci.z; z.c[3] = ci.w;
         z.n = 4;
@@ -55,8 +88,8 @@ __device__ __forceinline__ Nz4 load_nz4(const int* __restrict__ col,
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const bool ok = j + k < e;
-            z.v[k] = ok ? ld_stream(val + j + k, pol) : 0.0;
-            z.c[k] = ok ? ld_stream_i32(col + j + k, pol) : col_pad;
+            z.v[k] = ok ? sp_ld(val + j + k, pol) : 0.0;
+            z.c[k] = ok ? sp_ld_i32(col + j + k, pol) : col_pad;
         }
     }
     return z;
@@ -110,11 +143,8 @@ __device__ __forceinline__ Nz4m load_nz4_rng(const int* __restrict__ col, const 
                                              int64_t j, int64_t lo, int64_t hi, uint64_t pol) {
     Nz4m z;
     if (((j & 3) == 0) && j >= lo && j + 4 <= hi) {
-        const d4 v = ld4_stream(val + j, pol);
-        int4 ci;
-        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
-            : "=r"(ci.x), "=r"(ci.y), "=r"(ci.z), "=r"(ci.w)
-            : "l"(col + j), "l"(pol));
+        const d4 v = sp_ld4(val + j, pol);
+        const int4 ci = sp_ld4_i32(col + j, pol);
         z.v[0] = v.x; z.v[1] = v.y; z.v[2] = v.z; z.v[3] = v.w;
         z.c[0] = ci.x; z.c[1] = ci.y; z.c[2] = ci.z; z.c[3] = ci.w;
         z.ok[0] = z.ok[1] = z.ok[2] = z.ok[3] = true;
@@ -122,8 +152,8 @@ __device__ __forceinline__ Nz4m load_nz4_rng(const int* __restrict__ col, const 
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             z.ok[k] = j + k >= lo && j + k < hi;
-            z.v[k] = z.ok[k] ? ld_stream(val + j + k, pol) : 0.0;
-            z.c[k] = z.ok[k] ? ld_stream_i32(col + j + k, pol) : 0;
+            z.v[k] = z.ok[k] ? sp_ld(val + j + k, pol) : 0.0;
+            z.c[k] = z.ok[k] ? sp_ld_i32(col + j + k, pol) : 0;
         }
     }
     return z;
@@ -482,9 +512,7 @@ cudaError_t launch_spmv_rows(int unit, uint64_t r0, uint64_t r1, const int* rp, 
                              const double* val, const double* x, int64_t col_base, double* y,
                              const LongRows& lr, cudaStream_t s) {
     const Tuning& t = tuning();
-    const int threads = 256;
     const uint64_t rows = r1 - r0;
-    const uint64_t max_blocks = (uint64_t)kNumSMs * (uint64_t)t.spmv_blocks_per_sm;
     if (unit == 1) {
         const int tthreads = t.spmv_tc_threads, RB = t.spmv_tc_rows;
         uint64_t blocks = (rows + (uint64_t)(tthreads / 32) * 8 * RB - 1) / ((uint64_t)(tthreads / 32) * 8 * RB);
