@@ -1090,7 +1090,8 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         else if (k == "spmv_plan_tiled") slot = &t.spmv_plan_tiled;
         else if (k == "spmv_long_rows") slot = &t.spmv_long_rows;
         else if (k == "spmv_long_min") slot = &t.spmv_long_min;
-        else if (k == "spmv_long_huge") slot = &t.spmv_long_huge;
+        else if (k == "spmv_long_piece") slot = &t.spmv_long_piece;
+        else if (k == "spmv_long_group") slot = &t.spmv_long_group;
         else if (k == "spmv_plan_graph") slot = &t.spmv_plan_graph;
         else if (k == "spmv_plan_taper") slot = &t.spmv_plan_taper;
         else if (k == "stencil_r_ctas_per_sm") slot = &t.stencil_r_ctas_per_sm;

@@ -24,7 +24,8 @@ struct Tuning {
     int spmv_tc_rows = 1;          // 8-row blocks per warp iteration (1, 2)
     int spmv_long_rows = 1;        // divert long rows of the CSR kernels to a load-balanced second kernel
     int spmv_long_min = 64;        // ... rows longer than this many nonzeros
-    int spmv_long_huge = 8192;     // ... and a CTA (not a warp) per row past this length
+    int spmv_long_piece = 512;     // ... cut into pieces of this many nonzeros, balanced over the warps
+    int spmv_long_group = 8;       // lanes per piece of the CUDA-core long-row kernel (8, 16, 32)
     int spmv_plan_chunks = 16;     // pipelined row/x chunks of rl_spmv_plan_execute_host
     int spmv_plan_tiled = 0;       // 1: CUDA-core plans use the column-tiled layout (spmv_tiled.cu; 0.30 ms vs CSR 0.28 ms on the BASELINE matrix)
     int spmv_plan_taper = 0;       // 1: half-size first/last pipeline chunks (measured no gain)
@@ -76,16 +77,23 @@ enum StencilPreset : int {
 cudaError_t launch_scale(int unit, double* a, const double* b, double q, uint64_t n,
                          cudaStream_t s);
 // Long-row diversion state of one SpMV launch (spmv.cu): rows longer than
-// lmax go to the medium list (warp per row), past lhuge to the huge list
-// (CTA per row), computed by spmv_long after the per-row kernel;
-// ctr = {n_med, n_huge, exited}.  ctr == nullptr: off.
+// lmax leave the per-row kernel; each is cut into ceil(len / piece) pieces of
+// at most `piece` nonzeros and appended to the list with its first global
+// piece number (one 64-bit atomic: list index << 38 | pieces so far, so
+// base[] ascends with the index).  spmv_long then hands every warp an equal
+// run of pieces.  ctr[0..1] is that 64-bit counter, ctr[2] the exit count.
+// ctr == nullptr: off.
 struct LongRows {
     unsigned* ctr;
-    int* med;
-    int* huge;
+    int* rows;       // diverted rows (list order)
+    unsigned* base;  // first global piece of each listed row (ascending)
+    double* part;    // partial sums of split rows, by global piece (pcap)
+    unsigned* done;  // per listed row: pieces finished
     int64_t lmax;
-    int64_t lhuge;
+    int64_t piece;
+    uint64_t pcap;
 };
+constexpr int kLongIndexShift = 38;
 // long_rows: -1 unknown (divert on the device), 0 known absent (no
 // diversion), 1 known present.
 cudaError_t launch_spmv(int unit, uint64_t r0, uint64_t r1, const int* rp, const int* col,

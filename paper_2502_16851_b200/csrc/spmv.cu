@@ -118,16 +118,19 @@ __device__ __forceinline__ void gather4(double (&xv)[4], const Nz4& z,
 
 // Rows longer than lr.lmax nonzeros leave the per-row kernels (they would
 // hold a warp for ~len/16 steps while its other rows finish in one): the
-// lane that owns the row's start appends it to the medium list (a warp per
-// row) or, past lr.lhuge, the huge list (a CTA per row), and spmv_long then
-// computes them load-balanced.  lr.ctr == nullptr disables the diversion.
+// lane that owns the row's start appends it, with its piece count, to the
+// list (see LongRows), and spmv_long computes the pieces load-balanced.
+// lr.ctr == nullptr disables the diversion.
 __device__ __forceinline__ bool divert_long(const LongRows& lr, uint64_t row, int64_t& s, int64_t& e,
                                             bool leader) {
     if (lr.ctr == nullptr || e - s <= lr.lmax) return false;
     if (leader) {
-        const bool huge = e - s > lr.lhuge;
-        const unsigned i = atomicAdd(lr.ctr + (huge ? 1 : 0), 1u);
-        (huge ? lr.huge : lr.med)[i] = (int)row;
+        const unsigned long long np = (unsigned long long)((e - s + lr.piece - 1) / lr.piece);
+        const unsigned long long old =
+            atomicAdd(reinterpret_cast<unsigned long long*>(lr.ctr), (1ull << kLongIndexShift) | np);
+        const unsigned i = (unsigned)(old >> kLongIndexShift);
+        lr.rows[i] = (int)row;
+        lr.base[i] = (unsigned)(old & ((1ull << kLongIndexShift) - 1));
     }
     e = s;
     return true;
@@ -164,18 +167,21 @@ __device__ __forceinline__ void gather4m(double (&xv)[4], const Nz4m& z, const d
     for (int k = 0; k < 4; ++k) xv[k] = z.ok[k] ? ld_x(x + ((int64_t)z.c[k] - col_base), polx, 0) : 0.0;
 }
 
-// Sum of nonzeros [lo, hi) of one row by one warp, valid in every lane.
-// CUDA core: lanes stride 4-wide aligned groups; fixed-order xor reduction.
-__device__ __forceinline__ double warp_segment_cc(const int* __restrict__ col, const double* __restrict__ val,
-                                                  const double* __restrict__ x, int64_t col_base, int64_t lo,
-                                                  int64_t hi, uint64_t pol, uint64_t polx) {
-    const int lane = threadIdx.x & 31;
-    constexpr int U = 4;  // 4 x 128 nonzeros in flight per warp step (loads first, then gathers)
+// Sum of nonzeros [lo, hi) of one row by a group of GL lanes (GL = 32: the
+// whole warp), valid in every lane of the group.  CUDA core: lanes stride
+// 4-wide aligned groups; fixed-order xor reduction within the group.
+template <int GL = 32>
+__device__ __forceinline__ double group_segment_cc(const int* __restrict__ col, const double* __restrict__ val,
+                                                   const double* __restrict__ x, int64_t col_base, int64_t lo,
+                                                   int64_t hi, uint64_t pol, uint64_t polx) {
+    const int lane = threadIdx.x & 31, gl = lane & (GL - 1);
+    const unsigned gmask = GL == 32 ? 0xffffffffu : (((1u << GL) - 1u) << (lane & ~(GL - 1)));
+    constexpr int U = 4;  // 4 x 4 GL nonzeros in flight per group step (loads first, then gathers)
     double acc[U] = {0.0, 0.0, 0.0, 0.0};
-    for (int64_t j0 = (lo & ~int64_t(3)) + 4 * lane; j0 < hi; j0 += 128 * U) {
+    for (int64_t j0 = (lo & ~int64_t(3)) + 4 * gl; j0 < hi; j0 += 4 * GL * U) {
         Nz4m z[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) z[u] = load_nz4_rng(col, val, j0 + 128 * u, lo, hi, pol);
+        for (int u = 0; u < U; ++u) z[u] = load_nz4_rng(col, val, j0 + 4 * GL * u, lo, hi, pol);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             double xv[4];
@@ -186,8 +192,13 @@ __device__ __forceinline__ double warp_segment_cc(const int* __restrict__ col, c
     }
     double a = (acc[0] + acc[1]) + (acc[2] + acc[3]);
 #pragma unroll
-    for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    for (int o = GL / 2; o; o >>= 1) a += __shfl_xor_sync(gmask, a, o);
     return a;
+}
+__device__ __forceinline__ double warp_segment_cc(const int* __restrict__ col, const double* __restrict__ val,
+                                                  const double* __restrict__ x, int64_t col_base, int64_t lo,
+                                                  int64_t hi, uint64_t pol, uint64_t polx) {
+    return group_segment_cc<32>(col, val, x, col_base, lo, hi, pol, polx);
 }
 
 // Tensor core: the segment is cut into 8 virtual rows of C nonzeros (C a
@@ -226,6 +237,35 @@ __device__ __forceinline__ double warp_segment_tc(const int* __restrict__ col, c
     return sum;
 }
 
+// Tensor core, eight independent segments at once: virtual row r of the
+// DASP-style block (lanes 4r..4r+3) walks its own [lo, hi) (the lanes of a
+// virtual row pass the same range; empty ranges are allowed).  Returns
+// virtual row r's sum, valid in lane 4r + r/2 (where D[r][r] lives).
+__device__ __forceinline__ double warp_multi_tc(const int* __restrict__ col, const double* __restrict__ val,
+                                                const double* __restrict__ x, int64_t col_base, int64_t lo,
+                                                int64_t hi, uint64_t pol, uint64_t polx) {
+    const int lane = threadIdx.x & 31, r = lane >> 2, c = lane & 3;
+    const int64_t base = lo & ~int64_t(3);
+    constexpr int U = 4;  // 4 steps of 16 per virtual row in flight
+    double d0[U] = {0.0, 0.0, 0.0, 0.0}, d1[U] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t off0 = 0; __any_sync(0xffffffffu, base + off0 < hi); off0 += 16 * U) {
+        Nz4m z[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) z[u] = load_nz4_rng(col, val, base + off0 + 16 * u + 4 * c, lo, hi, pol);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            double xv[4];
+            gather4m(xv, z[u], x, col_base, polx);
+            dmma_m8n8k4(d0[u], d1[u], z[u].v[0], xv[0], d0[u], d1[u]);
+            dmma_m8n8k4(d0[u], d1[u], z[u].v[1], xv[1], d0[u], d1[u]);
+            dmma_m8n8k4(d0[u], d1[u], z[u].v[2], xv[2], d0[u], d1[u]);
+            dmma_m8n8k4(d0[u], d1[u], z[u].v[3], xv[3], d0[u], d1[u]);
+        }
+    }
+    const double e0 = (d0[0] + d0[1]) + (d0[2] + d0[3]), e1 = (d1[0] + d1[1]) + (d1[2] + d1[3]);
+    return (r & 1) ? e1 : e0;
+}
+
 // Longest row of [r0, r1): the one-time probe behind row_profile().
 __global__ void __launch_bounds__(256) spmv_maxlen(uint64_t r0, uint64_t r1, const int* __restrict__ rp,
                                                    int* __restrict__ out) {
@@ -237,50 +277,111 @@ __global__ void __launch_bounds__(256) spmv_maxlen(uint64_t r0, uint64_t r1, con
     if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
 
-// The diverted rows, after the per-row kernel (stream order): huge rows a
-// CTA each (the warps take contiguous slices, fixed-order block sum), medium
-// rows a warp each.  The last CTA out zeroes the counters for the next call
-// on this stream, so no memset node is needed.
-// ctr: 0 n_med, 1 n_huge, 2 exited.
-template <int TC>
-__global__ void __launch_bounds__(256) spmv_long(const int* __restrict__ rp, const int* __restrict__ col,
-                                                  const double* __restrict__ val, const double* __restrict__ x,
-                                                  int64_t col_base, double* __restrict__ y, LongRows lr) {
-    __shared__ double red[32];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+// The diverted rows, after the per-row kernel (stream order).  Warp w of W
+// takes the contiguous run of pieces [w P/W, (w+1) P/W) -- pieces are at
+// most lr.piece nonzeros, so the runs balance whatever the row lengths.  It
+// finds its first row with a 32-ary search over base[] (3 round trips for
+// 32 K rows), then its groups of GL lanes (CUDA core: 8, so four pieces --
+// e.g. four short rows -- are in flight per warp; tensor core: the whole
+// warp) walk the run, group j taking every (32/GL)-th piece.  A row of one
+// piece is stored directly; a split row's pieces go to part[] and the group
+// that finishes the row's last piece adds them in piece order, so the result
+// does not depend on timing.  (A split row past the part[] capacity is done
+// whole by its first piece's group.)  The last CTA out zeroes the counters
+// for the next call on this stream, so no memset node is needed.
+template <int TC, int GL>
+__global__ void __launch_bounds__(256, 2) spmv_long(const int* __restrict__ rp, const int* __restrict__ col,
+                                                     const double* __restrict__ val, const double* __restrict__ x,
+                                                     int64_t col_base, double* __restrict__ y, LongRows lr) {
+    static_assert(!TC || GL == 32, "the tensor-core block spans the whole warp (eight pieces, one per virtual row)");
+    constexpr int NG = 32 / GL;
+    const int tid = threadIdx.x, lane = tid & 31, grp = lane / GL, gl = lane & (GL - 1);
     const uint64_t pol = policy_evict_first(), polx = policy_evict_last();
-    const unsigned nmed = *reinterpret_cast<volatile unsigned*>(lr.ctr);
-    const unsigned nhuge = *reinterpret_cast<volatile unsigned*>(lr.ctr + 1);
-    for (unsigned i = blockIdx.x; i < nhuge; i += gridDim.x) {
-        const int row = lr.huge[i];
-        const int64_t s = __ldg(rp + row), e = __ldg(rp + row + 1);
-        const int64_t part = (((e - s) + nwarp - 1) / nwarp + 3) & ~int64_t(3);
-        const int64_t lo = min(e, s + warp * part), hi = min(e, s + (warp + 1) * part);
-        const double v = TC ? warp_segment_tc(col, val, x, col_base, lo, hi, pol, polx)
-                            : warp_segment_cc(col, val, x, col_base, lo, hi, pol, polx);
-        if (lane == 0) red[warp] = v;
-        __syncthreads();
-        if (tid == 0) {
-            double t = 0.0;
-            for (int w = 0; w < nwarp; ++w) t += red[w];
-            y[row] = t;
+    const unsigned long long c = *reinterpret_cast<volatile unsigned long long*>(lr.ctr);
+    const unsigned nlong = (unsigned)(c >> kLongIndexShift);
+    const uint64_t npieces = c & ((1ull << kLongIndexShift) - 1);
+    const uint64_t W = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    const uint64_t w = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
+    const uint64_t g0 = npieces * w / W, g1 = npieces * (w + 1) / W;
+    if (g0 < g1) {
+        // last list index i with base[i] <= g0: 32-ary search
+        unsigned lo = 0, hi = nlong;  // answer in [lo, hi)
+        while (hi - lo > 1) {
+            const unsigned span = hi - lo, step = (span + 31) / 32;
+            const unsigned probe = lo + lane * step;
+            const bool le = probe < hi && __ldg(lr.base + probe) <= g0;
+            const unsigned ball = __ballot_sync(0xffffffffu, le);
+            const int k = 31 - __clz(ball);  // lane 0 always qualifies (base[lo] <= g0)
+            lo = lo + (unsigned)k * step;
+            hi = min(hi, lo + step);
         }
-        __syncthreads();
-    }
-    const unsigned gw = blockIdx.x * (unsigned)nwarp + (unsigned)warp, nw = gridDim.x * (unsigned)nwarp;
-    for (unsigned i = gw; i < nmed; i += nw) {
-        const int row = lr.med[i];
-        const int64_t s = __ldg(rp + row), e = __ldg(rp + row + 1);
-        const double v = TC ? warp_segment_tc(col, val, x, col_base, s, e, pol, polx)
-                            : warp_segment_cc(col, val, x, col_base, s, e, pol, polx);
-        if (lane == 0) y[row] = v;
+        unsigned i = lo;
+        uint64_t b_i = __ldg(lr.base + i);
+        uint64_t b_n = i + 1 < nlong ? __ldg(lr.base + i + 1) : npieces;
+        // TC: virtual row r (lanes 4r..4r+3) takes piece gb + r of each batch
+        // of 8; CC: group grp takes every NG-th piece.
+        constexpr int STRIDE = TC ? 8 : NG;
+        const int slot = TC ? (lane >> 2) : grp;
+        const uint64_t gend = TC ? g0 + (g1 - g0 + 7) / 8 * 8 : g1;  // TC: whole batches (the warp stays converged)
+        for (uint64_t g = g0 + slot; g < gend; g += STRIDE) {
+            const bool live = g < g1;
+            int row = 0;
+            int64_t a = 0, bnd = 0;
+            uint64_t np = 0;
+            bool whole = true;
+            if (live) {
+                while (g >= b_n) {
+                    ++i;
+                    b_i = b_n;
+                    b_n = i + 1 < nlong ? __ldg(lr.base + i + 1) : npieces;
+                }
+                row = lr.rows[i];
+                const int64_t s = __ldg(rp + row), e = __ldg(rp + row + 1);
+                np = b_n - b_i;
+                const uint64_t q = g - b_i;
+                whole = np == 1 || b_n > lr.pcap;  // unsplit, or past capacity: done by piece 0's lanes
+                if (!whole || q == 0) {
+                    a = whole ? s : s + (int64_t)q * lr.piece;
+                    bnd = whole ? e : min(e, a + lr.piece);
+                } else {
+                    row = -1;  // a later piece of a row done whole: nothing to do
+                }
+            } else {
+                row = -1;
+            }
+            if constexpr (!TC) {
+                if (row < 0) continue;
+            }
+            double v;
+            bool leader;
+            if constexpr (TC) {
+                v = warp_multi_tc(col, val, x, col_base, a, bnd, pol, polx);
+                leader = lane == 4 * slot + (slot >> 1);
+            } else {
+                v = group_segment_cc<GL>(col, val, x, col_base, a, bnd, pol, polx);
+                leader = gl == 0;
+            }
+            if (!leader || row < 0) continue;
+            if (whole) {
+                y[row] = v;
+                continue;
+            }
+            lr.part[g] = v;
+            __threadfence();
+            if (atomicAdd(lr.done + i, 1u) == (unsigned)np - 1) {  // the row's last piece: sum in order
+                __threadfence();
+                double r = 0.0;
+                for (uint64_t p = b_i; p < b_n; ++p) r += *reinterpret_cast<volatile double*>(lr.part + p);
+                y[row] = r;
+                lr.done[i] = 0;
+            }
+        }
     }
     __syncthreads();
     if (tid == 0) {
         __threadfence();
         if (atomicAdd(lr.ctr + 2, 1u) == gridDim.x - 1) {
-            lr.ctr[0] = 0;
-            lr.ctr[1] = 0;
+            *reinterpret_cast<unsigned long long*>(lr.ctr) = 0ull;
             lr.ctr[2] = 0;
         }
     }
@@ -438,11 +539,12 @@ __global__ void __launch_bounds__(1024) spmv_tc(uint64_t r0, uint64_t r1,
 
 // Has the CSR row range rows the per-row kernels divert?  Probed once per
 // (device, row_ptr, col, val, range): one small kernel and one stream
-// synchronisation on the first call, then cached, so later calls stay fully
+// synchronisation on the first call, then cached (the longest row; the
+// answer follows the current spmv_long_min), so later calls stay fully
 // asynchronous and pay nothing when there are none.  A stale entry (arrays
 // rewritten in place at the same addresses) costs speed only: undiverted
 // long rows are still computed by the per-row kernels, and a needless
-// diversion pass finds empty lists.  Under stream capture the probe is
+// diversion pass finds an empty list.  Under stream capture the probe is
 // skipped (-1: divert on the device).
 static int row_profile(const int* rp, const int* col, const double* val, uint64_t r0, uint64_t r1,
                        cudaStream_t s) {
@@ -455,14 +557,14 @@ static int row_profile(const int* rp, const int* col, const double* val, uint64_
         }
     };
     static std::mutex mu;
-    static std::map<Key, int> cache;
+    static std::map<Key, int> cache;   // longest row
     static std::map<int, int*> slots;  // per-device probe result
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return -1;
     const Key key{dev, rp, col, val, r0, r1};
     std::lock_guard<std::mutex> lock(mu);
     const auto it = cache.find(key);
-    if (it != cache.end()) return it->second;
+    if (it != cache.end()) return it->second > tuning().spmv_long_min ? 1 : 0;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return -1;
     int*& slot = slots[dev];
@@ -478,10 +580,9 @@ static int row_profile(const int* rp, const int* col, const double* val, uint64_
     if (cudaMemcpyAsync(&h, slot, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
         cudaStreamSynchronize(s) != cudaSuccess)
         return -1;
-    const int v = h > tuning().spmv_long_min ? 1 : 0;
     if (cache.size() >= 1024) cache.clear();
-    cache[key] = v;
-    return v;
+    cache[key] = h;
+    return h > tuning().spmv_long_min ? 1 : 0;
 }
 
 cudaError_t launch_spmv(int unit, uint64_t r0, uint64_t r1, const int* rp, const int* col,
@@ -496,14 +597,18 @@ cudaError_t launch_spmv(int unit, uint64_t r0, uint64_t r1, const int* rp, const
         cudaError_t e = spmv_long_workspace(s, r1 - r0, lr);
         if (e != cudaSuccess) return e;
         lr.lmax = t.spmv_long_min;
-        lr.lhuge = t.spmv_long_huge;
+        lr.piece = t.spmv_long_piece > 64 ? t.spmv_long_piece : 64;
     }
     cudaError_t err = launch_spmv_rows(unit, r0, r1, rp, col, val, x, col_base, y, lr, s);
     if (err != cudaSuccess || lr.ctr == nullptr) return err;
     if (unit == 1)
-        spmv_long<1><<<kNumSMs * 8, 256, 0, s>>>(rp, col, val, x, col_base, y, lr);
+        spmv_long<1, 32><<<kNumSMs * 2, 256, 0, s>>>(rp, col, val, x, col_base, y, lr);
+    else if (t.spmv_long_group == 32)
+        spmv_long<0, 32><<<kNumSMs * 2, 256, 0, s>>>(rp, col, val, x, col_base, y, lr);
+    else if (t.spmv_long_group == 16)
+        spmv_long<0, 16><<<kNumSMs * 2, 256, 0, s>>>(rp, col, val, x, col_base, y, lr);
     else
-        spmv_long<0><<<kNumSMs * 8, 256, 0, s>>>(rp, col, val, x, col_base, y, lr);
+        spmv_long<0, 8><<<kNumSMs * 2, 256, 0, s>>>(rp, col, val, x, col_base, y, lr);
     note_launch();
     return cudaGetLastError();
 }
@@ -566,8 +671,10 @@ cudaError_t launch_spmv_rows(int unit, uint64_t r0, uint64_t r1, const int* rp, 
 namespace {
 struct LongWs {
     unsigned* ctr = nullptr;
-    int* med = nullptr;
-    int* huge = nullptr;
+    int* rows = nullptr;
+    unsigned* base = nullptr;
+    double* part = nullptr;
+    unsigned* done = nullptr;
     uint64_t cap = 0;
 };
 }  // namespace
@@ -586,19 +693,27 @@ cudaError_t spmv_long_workspace(cudaStream_t s, uint64_t rows, LongRows& lr) {
         if (cs != cudaStreamCaptureStatusNone) return cudaErrorStreamCaptureUnsupported;  // reserve first
         if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;  // old buffers may be in flight
         if (w.ctr) cudaFree(w.ctr);
-        if (w.med) cudaFree(w.med);
-        if (w.huge) cudaFree(w.huge);
+        if (w.rows) cudaFree(w.rows);
+        if (w.base) cudaFree(w.base);
+        if (w.part) cudaFree(w.part);
+        if (w.done) cudaFree(w.done);
         w = LongWs{};
-        const uint64_t cap = rows < 1024 ? 1024 : rows;
+        const uint64_t cap = rows < 65536 ? 65536 : rows;  // list entries and split pieces
         if ((e = cudaMalloc(&w.ctr, 8 * sizeof(unsigned))) != cudaSuccess) return e;
         if ((e = cudaMemset(w.ctr, 0, 8 * sizeof(unsigned))) != cudaSuccess) return e;
-        if ((e = cudaMalloc(&w.med, cap * sizeof(int))) != cudaSuccess) return e;
-        if ((e = cudaMalloc(&w.huge, cap * sizeof(int))) != cudaSuccess) return e;
+        if ((e = cudaMalloc(&w.rows, cap * sizeof(int))) != cudaSuccess) return e;
+        if ((e = cudaMalloc(&w.base, cap * sizeof(unsigned))) != cudaSuccess) return e;
+        if ((e = cudaMalloc(&w.part, cap * sizeof(double))) != cudaSuccess) return e;
+        if ((e = cudaMalloc(&w.done, cap * sizeof(unsigned))) != cudaSuccess) return e;
+        if ((e = cudaMemset(w.done, 0, cap * sizeof(unsigned))) != cudaSuccess) return e;
         w.cap = cap;
     }
     lr.ctr = w.ctr;
-    lr.med = w.med;
-    lr.huge = w.huge;
+    lr.rows = w.rows;
+    lr.base = w.base;
+    lr.part = w.part;
+    lr.done = w.done;
+    lr.pcap = w.cap;
     return cudaSuccess;
 }
 

@@ -184,3 +184,18 @@ def test_plan_with_long_rows_pinned(cuda):
     torch.cuda.synchronize()
     assert O.rel_err(dy.cpu().numpy(), O.spmv_csr(rp, col, val, hx.numpy())) <= 1e-12
     plan.close()
+
+
+def test_plan_short_rows(cuda):
+    """A short-row CSR (mean < 4 nonzeros, a few long rows): the plan picks the
+    lane-per-row kernel from its host profile; pinned and pageable paths."""
+    import torch
+
+    rng = np.random.default_rng(21)
+    m, n = 50000, 20000
+    lens = rng.integers(0, 5, m)
+    lens[rng.choice(m, 12, replace=False)] = 2500
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    col = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(np.int32)
+    val = rng.uniform(-1, 1, rp[-1])
+    _plan_check(torch, rp, col, val, n, P.CUDA_CORE, False)

@@ -157,7 +157,7 @@ def test_spmv_errors(cuda):
 
 
 def _skewed_csr(m, n, seed, huge=(3, 20000)):
-    """Power-law row lengths plus a few huge rows (past spmv_long_huge)."""
+    """Power-law row lengths plus a few huge rows (many pieces each)."""
     rng = np.random.default_rng(seed)
     lens = np.minimum(rng.zipf(1.6, m), 3000).astype(np.int64)
     for r in rng.choice(m, huge[0], replace=False):
@@ -170,8 +170,9 @@ def _skewed_csr(m, n, seed, huge=(3, 20000)):
 
 @pytest.mark.parametrize("unit", UNITS)
 def test_spmv_long_rows_diverted(cuda, unit):
-    """Rows past spmv_long_min go to the load-balanced second kernel (a warp
-    per row, a CTA per row past spmv_long_huge); results equal the oracle."""
+    """Rows past spmv_long_min go to the load-balanced second kernel (rows cut
+    into spmv_long_piece-nonzero pieces, equal runs of pieces per warp);
+    results equal the oracle."""
     import torch
 
     m, n = 20000, 30000
@@ -184,6 +185,90 @@ def test_spmv_long_rows_diverted(cuda, unit):
         P.spmv_csr(d[0], d[1], d[2], d[3], y, unit=unit)
         torch.cuda.synchronize()
         assert O.rel_err(y.cpu().numpy(), O.spmv_csr(rp, col, val, x)) <= TOL
+
+
+@pytest.mark.parametrize("unit", UNITS)
+@pytest.mark.parametrize("piece", [64, 100, 777, 2048, 1 << 20])
+@pytest.mark.parametrize("group", [8, 16, 32])
+def test_spmv_long_row_pieces(cuda, unit, piece, group):
+    """Any piece size (not a multiple of 4, or larger than every row) gives
+    the oracle's result, bit-identical from call to call (split rows are
+    summed in piece order by whichever warp finishes last)."""
+    import torch
+
+    m, n = 6000, 30000
+    rp, col, val = _skewed_csr(m, n, 8, huge=(5, 25000))
+    x = np.random.default_rng(9).uniform(-1, 1, n)
+    d = [torch.from_numpy(t).cuda() for t in (rp, col, val, x)]
+    y = torch.full((m,), float("nan"), dtype=torch.float64, device="cuda")
+    P.tuning_set("spmv_long_piece", piece)
+    P.tuning_set("spmv_long_group", group)
+    try:
+        outs = []
+        for _ in range(3):
+            P.spmv_csr(d[0], d[1], d[2], d[3], y, unit=unit)
+            torch.cuda.synchronize()
+            outs.append(y.cpu().numpy().copy())
+    finally:
+        P.tuning_set("spmv_long_piece", 512)
+        P.tuning_set("spmv_long_group", 8)
+    assert O.rel_err(outs[0], O.spmv_csr(rp, col, val, x)) <= TOL
+    assert O.bit_mismatches(outs[0], outs[1]) == 0 and O.bit_mismatches(outs[0], outs[2]) == 0
+
+
+@pytest.mark.parametrize("unit", UNITS)
+def test_spmv_long_row_piece_capacity(cuda, unit):
+    """More split pieces than the workspace holds (65536 at this size): the
+    rows past capacity are computed whole by one warp, still exact."""
+    import torch
+
+    m, n = 3000, 8000
+    rng = np.random.default_rng(12)
+    lens = rng.integers(2000, 4000, m)
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    col = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(np.int32)
+    val = rng.uniform(-1, 1, rp[-1])
+    assert rp[-1] // 64 > 65536
+    x = rng.uniform(-1, 1, n)
+    d = [torch.from_numpy(t).cuda() for t in (rp, col, val, x)]
+    y = torch.full((m,), float("nan"), dtype=torch.float64, device="cuda")
+    P.tuning_set("spmv_long_piece", 64)
+    try:
+        P.spmv_csr(d[0], d[1], d[2], d[3], y, unit=unit)
+        torch.cuda.synchronize()
+    finally:
+        P.tuning_set("spmv_long_piece", 512)
+    assert O.rel_err(y.cpu().numpy(), O.spmv_csr(rp, col, val, x)) <= TOL
+
+
+@pytest.mark.parametrize("unit", UNITS)
+@pytest.mark.parametrize("long_rows", [False, True])
+@pytest.mark.parametrize("m", [1, 31, 33, 5000, 70001])
+def test_spmv_short_rows(cuda, unit, long_rows, m):
+    """Rows of 0-5 nonzeros (power-law graphs' many tiny rows), with and
+    without diverted long rows; empty rows give 0."""
+    import torch
+
+    n = 4000
+    rng = np.random.default_rng(m + 7 * long_rows)
+    lens = rng.integers(0, 6, m)
+    if long_rows and m > 40:
+        lens[rng.choice(m, 20, replace=False)] = rng.integers(65, 3000, 20)
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    if rp[-1] == 0:
+        lens[0] = 1
+        rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    col = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(np.int32)
+    val = rng.uniform(-1, 1, rp[-1])
+    x = rng.uniform(-1, 1, n)
+    d = [torch.from_numpy(t).cuda() for t in (rp, col, val, x)]
+    y = torch.full((m,), float("nan"), dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        P.spmv_csr(d[0], d[1], d[2], d[3], y, unit=unit)
+        torch.cuda.synchronize()
+        got = y.cpu().numpy()
+        assert O.rel_err(got, O.spmv_csr(rp, col, val, x)) <= TOL
+        assert np.all(got[lens == 0] == 0.0)
 
 
 @pytest.mark.parametrize("unit", UNITS)

@@ -43,9 +43,9 @@ cases["zipf1.7"] = (z * (16 * m / z.sum())).astype(np.int64).clip(0, n)
 d = np.full(m, 12)
 d[rng.choice(m, 16, replace=False)] = 200000
 cases["dense_rows"] = d
-for key in ("spmv_long_min", "spmv_long_huge"):
-    if os.environ.get(key.upper()):
-        P.tuning_set(key, int(os.environ[key.upper()]))
+for k, v in os.environ.items():  # RLT_<tuning key>=<int>, e.g. RLT_SPMV_LONG_HUGE=2048
+    if k.startswith("RLT_"):
+        P.tuning_set(k[4:].lower(), int(v))
 for name, lens in cases.items():
     rp, col, val = build(lens, n, rng)
     x = torch.from_numpy(rng.uniform(-1, 1, n)).cuda()
