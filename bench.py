@@ -388,7 +388,7 @@ def cusparse_yardstick(torch, P, hbm, reps=20):
     return out
 
 
-def temporal_blocking(torch, P, hbm, t1_ms_per_step, t1_ms_per_step_3d=None, depths=(2, 4, 5, 7),
+def temporal_blocking(torch, P, hbm, t1_ms_per_step, t1_ms_per_step_3d=None, depths=(2, 3, 4, 5, 7),
                       depths_3d=(2, 3, 4)):
     """2d5pt (16384^2, 100 timesteps) and 3d7pt (512^3, 50
     timesteps) with temporal depth t on the BASELINE grids: floor(steps/t)

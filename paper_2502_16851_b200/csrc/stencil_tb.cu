@@ -157,10 +157,18 @@ __global__ void __launch_bounds__(256, 2) st2d_cc_tb(const double* __restrict__ 
         tb_march<T, PF, false>(u, v, nx, ny, ya, yb, strip, lane, d);
 }
 
-#ifndef RLB_TB_PF
-#define RLB_TB_PF 3
-#endif
-constexpr int kTbPF = RLB_TB_PF;  // rows in flight per warp (a multiple of 3)
+// Rows in flight per warp (a multiple of 3, so the unrolled body returns
+// every level window to the same registers).  The kernel is occupancy-bound
+// by registers (2 CTAs/SM), so its HBM parallelism is this prefetch queue.
+// Per timestep at 16384^2 (tools/sweep.py temporal_t, 3 / 6 / 9 rows):
+// t = 2 0.53 / 0.42 / 0.38 ms, t = 3 0.30 / 0.26 / -, t = 4 0.29 / 0.27 / -,
+// t = 5 0.21 / 0.24 / -; deeper t sit at the 128-register cap, where longer
+// queues spill and lose.  (A two-row partial-sum window per level measured
+// slower: t = 2 0.72 ms at 9 rows.)
+template <int T>
+constexpr int tb_pf() {
+    return T == 2 ? 9 : (T <= 4 ? 6 : 3);
+}
 
 template <int T>
 cudaError_t launch_tb(const StencilDesc& d, uint64_t o0, uint64_t o1, const double* u, double* v, cudaStream_t s) {
@@ -171,7 +179,7 @@ cudaError_t launch_tb(const StencilDesc& d, uint64_t o0, uint64_t o1, const doub
     // below (halo), so keep it >= 16 T rows
     static int bps = 0;
     if (!bps) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, st2d_cc_tb<T, kTbPF>, 256, 0) != cudaSuccess ||
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, st2d_cc_tb<T, tb_pf<T>()>, 256, 0) != cudaSuccess ||
             bps < 1)
             bps = 1;
     }
@@ -185,9 +193,7 @@ cudaError_t launch_tb(const StencilDesc& d, uint64_t o0, uint64_t o1, const doub
     const uint64_t segs = (rows + seg_rows - 1) / seg_rows;
     const uint64_t warps = (uint64_t)strips * segs;
     const unsigned blocks = (unsigned)((warps + 7) / 8);
-    // kTbPF rows in flight, a multiple of 3, so the unrolled body returns
-    // every level window to the same registers (no window-shift moves)
-    st2d_cc_tb<T, kTbPF><<<blocks, 256, 0, s>>>(u, v, (int)d.nx, (int)d.ny, (int)o0, (int)o1, seg_rows, strips, d);
+    st2d_cc_tb<T, tb_pf<T>()><<<blocks, 256, 0, s>>>(u, v, (int)d.nx, (int)d.ny, (int)o0, (int)o1, seg_rows, strips, d);
     note_launch();
     return cudaGetLastError();
 }
