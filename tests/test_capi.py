@@ -77,3 +77,18 @@ def test_no_cpu_fallback_without_gpu():
     rc = P.lib().rl_scale(P.CUDA_CORE, P.FP64, C.addressof(buf), C.addressof(buf), 2.0, 8, None, None)
     assert rc >= 100, rc
     assert b"CudaError" in P.lib().rl_last_error()
+
+
+def test_every_documented_tuning_key_is_settable():
+    """INTEGRATION.md's tuning table lists exactly the keys rl_tuning_set
+    accepts; setting one returns the previous value (restored here)."""
+    import re
+
+    text = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "INTEGRATION.md")).read()
+    table = text[text.index("| family | keys |"):]
+    table = table[:table.index("\n\n")]
+    keys = re.findall(r"`([a-z0-9_]+)`", table)
+    assert len(keys) >= 40
+    for k in keys:
+        prev = P.tuning_set(k, 1)
+        assert P.tuning_set(k, prev) == 1, k
