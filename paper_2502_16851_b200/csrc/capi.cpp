@@ -1097,6 +1097,7 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         else if (k == "stencil_r_ctas_per_sm") slot = &t.stencil_r_ctas_per_sm;
         else if (k == "stencil_tb_waves") slot = &t.stencil_tb_waves;
         else if (k == "stencil_tb") slot = &t.stencil_tb;
+        else if (k == "stencil_tb_tma") slot = &t.stencil_tb_tma;
         else if (k == "stencil_tb3_mode") slot = &t.stencil_tb3_mode;
         else if (k == "stencil_tb3_chunks") slot = &t.stencil_tb3_chunks;
         else if (k == "stencil_tb3_shape") slot = &t.stencil_tb3_shape;

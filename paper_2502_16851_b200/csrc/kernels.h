@@ -51,11 +51,12 @@ struct Tuning {
     int stencil_r_cc_stages = 0;       // ... CUDA-core ring depth: 2-4, 0 = auto (2 for 2d49pt -> 4 CTAs/SM, else 4)
     int stencil_r_ctas_per_sm = 32;
     int stencil_tb_waves = 4;          // register temporal blocking: grid = this many waves of resident warps
+    int stencil_tb_tma = 4;            // 2d5pt depth >= this streams rows through a per-warp TMA ring (0: never; register queue)
     int stencil_tb = 1;                // 1: temporal depth t >= 2 runs the register kernel (0: smem t=2 kernel)
     int stencil_tb3_mode = 1;          // 3d7pt t >= 2: 1 register-blocked TMA kernel (stencil_tb3r.cu), 0 the z-column kernel
     int stencil_tb3_shape = 0;         // stencil_tb3r rows per warp x warps: 0/1 4x8, 2 2x16, 3 4x16 (t=2)
     int stencil_tb3_chunks = 0;        // z chunks per tile for stencil_tb3r (0: auto)
-    int stencil_tb3_l2promo = 3;       // TMA L2 promotion of the stencil_tb3r boxes (0 none .. 3 256 B)
+    int stencil_tb3_l2promo = 2;       // TMA L2 promotion of the stencil_tb3r boxes (0 none .. 3 256 B)
     int stencil_r_l2promo = 1;         // ... TMA L2 promotion (0 none, 1 64 B, 2 128 B, 3 256 B)
     int stencil_r_sym = 1;             // 2d49pt CC: pair mirror-symmetric columns (fewer FP64 ops)    // 2d9pt/2d13pt/2d49pt TMA kernels: row segments so the grid is this deep
 };

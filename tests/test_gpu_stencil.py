@@ -372,3 +372,26 @@ def test_3d7pt_temporal_z_chunks(cuda, t, chunks, shape_knob):
     assert O.rel_err(got, O.stencil("3d7pt", u0, 2 * t)) <= TOL
     ring = _ring_mask(shape, 1)
     assert O.bit_mismatches(got[ring], u0[ring]) == 0
+
+
+@pytest.mark.parametrize("tma_from", [2, 0])
+@pytest.mark.parametrize("t", [2, 3, 4, 5, 8])
+@pytest.mark.parametrize("shape", [(70, 134), (131, 258), (45, 64)])
+def test_2d5pt_temporal_tma_ring(cuda, tma_from, t, shape):
+    """2d5pt temporal depth t with the rows streamed through the per-warp TMA
+    ring (odd t reads the unaligned column pair) or the register queue."""
+    import torch
+
+    u0 = O.stencil_init(shape, 1, 41)
+    u = torch.from_numpy(u0.copy()).cuda()
+    v = torch.from_numpy(u0.copy()).cuda()
+    P.tuning_set("stencil_tb_tma", tma_from)
+    try:
+        _, out = P.stencil_temporal("2d5pt", u, v, 2 * t + 1, t)
+        torch.cuda.synchronize()
+    finally:
+        P.tuning_set("stencil_tb_tma", 4)
+    got = out.cpu().numpy()
+    assert O.rel_err(got, O.stencil("2d5pt", u0, 2 * t + 1)) <= TOL
+    ring = _ring_mask(shape, 1)
+    assert O.bit_mismatches(got[ring], u0[ring]) == 0
