@@ -38,7 +38,7 @@ struct Tuning {
     int tc_stencil_zchunk = 32;
     int stencil_tma = 1;           // 1: TMA-pipelined kernels when eligible
     int stencil_ctas_per_sm = 1;   // grid sizing target, TMA CUDA-core kernels
-    int stencil_rows_per_thread = 2;   // 3D TMA CUDA-core kernels: 2, 4 or 8 (CTA = 64*16/this threads)
+    int stencil_rows_per_thread = 0;   // 3D TMA CUDA-core kernels: 2, 4 or 8 (CTA = 64*16/this threads); 0 = per preset
     int stencil2d_rows_per_thread = 4; // 2D TMA CUDA-core kernel (swept: tools/sweep.py)
     int stencil_t2_ctas_per_sm = 8;    // temporal-depth-2 2d5pt kernel (swept)
     int stencil_cc27x2 = 1;            // 3d27pt CC class weights: two columns per thread kernel

@@ -1101,7 +1101,9 @@ cudaError_t launch_stencil_tma(int unit, const StencilDesc& d, uint64_t o0, uint
         if (tk == 0) RLB_TC3(0); else if (tk == 1) RLB_TC3(1); else RLB_TC3(2);
 #undef RLB_TC3
     } else {
-        const int ry = tuning().stencil_rows_per_thread;
+        // rows per thread: 0 = the measured default per preset (3d7pt 4: 6.18 vs
+        // 5.80-6.01 TB/s at 2; 27pt 2: 5.86 vs 4.79 at 4, tools/sweep.py stencil3d_cc)
+        const int ry = tuning().stencil_rows_per_thread ? tuning().stencil_rows_per_thread : (kind == 0 ? 4 : 2);
         const int st = tuning().stencil3d_cc_stages;
 #define RLB_CC3(K, R, SS)                                                                                  \
     do {                                                                                                   \

@@ -172,7 +172,9 @@ def stencil3d_cc():
         v = u.clone()
         nbytes = 4 * 16 * math.prod(s - 2 for s in u.shape)
         sweep(f"{preset}_cc", lambda: P.stencil(preset, u, v, 4, unit=0), nbytes,
-              {"stencil3d_cc_stages": [4, 6, 8, 4], "stencil_rows_per_thread": [2, 4]})
+              {"stencil3d_cc_stages": [4, 6, 8, 4], "stencil_rows_per_thread": [4, 2, 0]})
+        sweep(f"{preset}_cc", lambda: P.stencil(preset, u, v, 4, unit=0), nbytes,
+              {"stencil_ctas_per_sm": [1, 2, 3, 4, 6, 8, 1]})
         del u, v
         torch.cuda.empty_cache()
 
