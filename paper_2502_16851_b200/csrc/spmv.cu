@@ -195,47 +195,6 @@ __device__ __forceinline__ double group_segment_cc(const int* __restrict__ col, 
     for (int o = GL / 2; o; o >>= 1) a += __shfl_xor_sync(gmask, a, o);
     return a;
 }
-__device__ __forceinline__ double warp_segment_cc(const int* __restrict__ col, const double* __restrict__ val,
-                                                  const double* __restrict__ x, int64_t col_base, int64_t lo,
-                                                  int64_t hi, uint64_t pol, uint64_t polx) {
-    return group_segment_cc<32>(col, val, x, col_base, lo, hi, pol, polx);
-}
-
-// Tensor core: the segment is cut into 8 virtual rows of C nonzeros (C a
-// multiple of 4, starts aligned) and run as the DASP-style 8-row block of
-// K4: D[r][r] accumulates virtual row r; the 8 diagonal values are summed in
-// a fixed order.
-__device__ __forceinline__ double warp_segment_tc(const int* __restrict__ col, const double* __restrict__ val,
-                                                  const double* __restrict__ x, int64_t col_base, int64_t lo,
-                                                  int64_t hi, uint64_t pol, uint64_t polx) {
-    const int lane = threadIdx.x & 31, r = lane >> 2, c = lane & 3;
-    const int64_t base = lo & ~int64_t(3);
-    const int64_t C = (((hi - base) + 7) / 8 + 3) & ~int64_t(3);
-    const int64_t vlo = max(lo, base + r * C), vhi = min(hi, base + (r + 1) * C);
-    constexpr int U = 4;  // 4 steps of 16 in flight: loads first, then gathers and DMMA chains
-    double d0[U] = {0.0, 0.0, 0.0, 0.0}, d1[U] = {0.0, 0.0, 0.0, 0.0};
-    for (int64_t off0 = 0; off0 < C; off0 += 16 * U) {
-        Nz4m z[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-            z[u] = load_nz4_rng(col, val, base + r * C + off0 + 16 * u + 4 * c, vlo, vhi, pol);
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            double xv[4];
-            gather4m(xv, z[u], x, col_base, polx);
-            dmma_m8n8k4(d0[u], d1[u], z[u].v[0], xv[0], d0[u], d1[u]);
-            dmma_m8n8k4(d0[u], d1[u], z[u].v[1], xv[1], d0[u], d1[u]);
-            dmma_m8n8k4(d0[u], d1[u], z[u].v[2], xv[2], d0[u], d1[u]);
-            dmma_m8n8k4(d0[u], d1[u], z[u].v[3], xv[3], d0[u], d1[u]);
-        }
-    }
-    const double e0 = (d0[0] + d0[1]) + (d0[2] + d0[3]), e1 = (d1[0] + d1[1]) + (d1[2] + d1[3]);
-    const double dv = (r & 1) ? e1 : e0;  // D[r][r] in lane 4r + r/2
-    double sum = 0.0;
-#pragma unroll
-    for (int rr = 0; rr < 8; ++rr) sum += __shfl_sync(0xffffffffu, dv, 4 * rr + (rr >> 1));
-    return sum;
-}
 
 // Tensor core, eight independent segments at once: virtual row r of the
 // DASP-style block (lanes 4r..4r+3) walks its own [lo, hi) (the lanes of a

@@ -313,7 +313,6 @@ __global__ void __launch_bounds__(32 * TY) st3d_cc(const double* __restrict__ u,
                     // We hold the in-plane sum of plane p-1 in acc_a (computed last
                     // iteration), prev = u(p-2), cur = u(p-1).
                     double o[4];
-                    const double cu[4] = {cur.x, cur.y, cur.z, cur.w};
                     const double pv[4] = {prev.x, prev.y, prev.z, prev.w};
                     const double nx4[4] = {pl.own.x, pl.own.y, pl.own.z, pl.own.w};
 #pragma unroll

@@ -39,7 +39,7 @@
 namespace rlb {
 namespace {
 
-constexpr int kTX = 64, kTY = 16, kRY = 8, kBY = kTY + 2;
+constexpr int kTX = 64, kTY = 16, kBY = kTY + 2;
 constexpr int kBX = 68;   // box / stage row width (doubles)
 constexpr int kCofs = 2;  // stage column of the tile's first x
 
