@@ -1106,6 +1106,7 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         else if (k == "stencil_tc_concat") slot = &t.stencil_tc_concat;
         else if (k == "stencil_cc27x2") slot = &t.stencil_cc27x2;
         else if (k == "stencil_r_cc_stages") slot = &t.stencil_r_cc_stages;
+        else if (k == "stencil_r_tc_stages") slot = &t.stencil_r_tc_stages;
         else if (k == "stencil_r_sym") slot = &t.stencil_r_sym;
         else if (k == "stencil_r_l2promo") slot = &t.stencil_r_l2promo;
         else if (k == "spmv_tc_blocks_per_sm") slot = &t.spmv_tc_blocks_per_sm;

@@ -49,6 +49,7 @@ struct Tuning {
     int stencil_tc3d_mode = 2;         // 3D tensor core, one-plane partial-sum kernel for: bit0 3d7pt, bit1 3d27pt
     int stencil_tc1_ctas_per_sm = 8;   // ... partial-sum mode
     int stencil_r_cc_stages = 0;       // ... CUDA-core ring depth: 2-4, 0 = auto (2 for 2d49pt -> 4 CTAs/SM, else 4)
+    int stencil_r_tc_stages = 0;       // TMA ring stages of the radius-R tensor-core kernels (0: 2 at radius 3, else 4)
     int stencil_r_ctas_per_sm = 32;
     int stencil_tb_waves = 4;          // register temporal blocking: grid = this many waves of resident warps
     int stencil_tb_tma = 4;            // 2d5pt depth >= this streams rows through a per-warp TMA ring (0: never; register queue)

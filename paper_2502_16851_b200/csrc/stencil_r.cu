@@ -374,14 +374,24 @@ cudaError_t launch_r(int unit, const StencilDesc& d, uint64_t o0, uint64_t o1, c
     const unsigned grid = (unsigned)(strips * segs);
     cudaError_t e;
     if (unit == 1) {
-        const size_t sm = ring_bytes<R, true, S>();
+        // stages: radius 3's DMMA chains need warps more than ring depth (4
+        // stages leave 2 CTAs = 8 warps per SM, `wait`-stalled).  Measured
+        // 16384^2 GB/s at 2 / 4 stages: 2d49pt 3650 / 3105, 2d13pt 5950 / 5690,
+        // 2d9pt 5870 / 6220.
+        int st = tuning().stencil_r_tc_stages;
+        if (st == 0) st = R == 3 ? 2 : S;
+#define RLB_RTC(SY, SS)                                                                                     \
+    do {                                                                                                    \
+        const size_t sm = ring_bytes<R, true, SS>();                                                        \
+        if ((e = prep(st2dr_tma_tc<R, BOX, SY, SS>, sm)) != cudaSuccess) return e;                         \
+        st2dr_tma_tc<R, BOX, SY, SS><<<grid, 128, sm, s>>>(m, v, d.nx, o0, o1, seg_rows, (int)strips, d); \
+    } while (0)
         if (BOX && y_symmetric<R>(d) && tuning().stencil_r_sym) {
-            if ((e = prep(st2dr_tma_tc<R, BOX, true, S>, sm)) != cudaSuccess) return e;
-            st2dr_tma_tc<R, BOX, true, S><<<grid, 128, sm, s>>>(m, v, d.nx, o0, o1, seg_rows, (int)strips, d);
+            if (st == 2) RLB_RTC(true, 2); else if (st == 3) RLB_RTC(true, 3); else RLB_RTC(true, 4);
         } else {
-            if ((e = prep(st2dr_tma_tc<R, BOX, false, S>, sm)) != cudaSuccess) return e;
-            st2dr_tma_tc<R, BOX, false, S><<<grid, 128, sm, s>>>(m, v, d.nx, o0, o1, seg_rows, (int)strips, d);
+            if (st == 2) RLB_RTC(false, 2); else if (st == 3) RLB_RTC(false, 3); else RLB_RTC(false, 4);
         }
+#undef RLB_RTC
     } else {
         int st = tuning().stencil_r_cc_stages;
         if (st == 0) st = (R == 3 && BOX) ? 2 : 4;  // 2d49pt: compute-bound, more CTAs beat a deeper ring
