@@ -1127,6 +1127,10 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         else if (k == "stencil_tc3d_ctas_per_sm") slot = &t.stencil_tc3d_ctas_per_sm;
         else if (k == "stencil_tc3d_mode") slot = &t.stencil_tc3d_mode;
         else if (k == "stencil_tc1_ctas_per_sm") slot = &t.stencil_tc1_ctas_per_sm;
+        else if (k == "stencil_tc3d_hybrid") slot = &t.stencil_tc3d_hybrid;
+        else if (k == "stencil_tch_ctas_per_sm") slot = &t.stencil_tch_ctas_per_sm;
+        else if (k == "stencil_tch_k8") slot = &t.stencil_tch_k8;
+        else if (k == "stencil_tch_tpw") slot = &t.stencil_tch_tpw;
         else throw Error(ErrorKind::ValidationError, "unknown tuning key '" + k + "'");
         if (previous) *previous = *slot;
         if (value < -1) throw Error(ErrorKind::InvalidRange, "tuning values must be >= -1");

@@ -893,6 +893,185 @@ __global__ void __launch_bounds__(128) st3d_tma_tc1(const __grid_constant__ CUte
     }
 }
 
+// ===========================================================================
+// Tensor core, 3D, x-band on DMMA with the rest on DFMA (the default 3D TC
+// kernel).  DMMA and DFMA share one FP64 datapath on B200 (tools/micro/
+// fp64_pipes.cu: 36.3 TF/s DFMA alone, 37.1 DMMA alone, <= 34.5 combined),
+// and a banded 8x8 product spends 12 k-slots on 3 taps, so every tap moved to
+// the DMMA costs 4 slots of the shared datapath; sustained runs also hit
+// sw_power_cap sooner the more DMMA they issue.  This kernel keeps exactly
+// one banded contraction per output tile on the tensor core -- the x
+// direction, 3 DMMA per 8x8 tile -- and feeds everything else in through the
+// accumulator C:
+//   KIND 0 (3d7pt):  D = U_z . band(w_x-, 0, w_x+) + C,
+//                    C = w_c u + w_y- u[y-1] + w_y+ u[y+1] + w_z- u[z-1] + w_z+ u[z+1]
+//   KIND 1 (3d27pt, class weights g0..g3): every x-band of the box is
+//     band(g(a+1), g(a), g(a+1)) = g(a+1) E + g(a) I with E = band(1, 0, 1),
+//     a = |dy| + |dz|, so  out = alpha . E + beta  with the y-z class sums
+//     S_a:  alpha = g1 S0 + g2 S1 + g3 S2 (A-fragment positions, one DMMA
+//     operand per k-slot) and beta = g0 S0 + g1 S1 + g2 S2 (accumulator
+//     positions).  Both are accumulated across planes like the CUDA-core
+//     partial sums: plane q adds (g1 a + g2 b) to alpha(q) and (g2 a + g3 b)
+//     to alpha(q +- 1), a = u[y], b = u[y-1] + u[y+1].
+// 12 DMMA-FMA + ~5 (7pt) / ~15 (27pt) DFMA per point, against 24 / 40 DMMA-FMA
+// in the full banded formulations (st3d_tma_tc / st3d_tma_tc1).
+//
+// KS = 2 shortens the band product to K = 8 (window columns x0-1 .. x0+6 of
+// each 8-column tile): 2 DMMA per tile instead of 3.  The two taps that fall
+// outside -- the x+1 taps of output columns 6 and 7 -- are the next tile's
+// first two window columns, i.e. A-fragment elements already held by lanes
+// c = 0 and 1 of the same row; two shuffles bring them to lane c = 3, whose
+// accumulator holds columns 6 and 7, for one DFMA each.
+//
+// Fragment rows are permuted, MMA row m <-> tile row pi(m) (bits 0 and 1
+// swapped), so the accumulator-position 128-bit loads (lane r, c reads
+// columns 2c, 2c+1 of row pi(r)) are conflict-free with the 68-double stage
+// pitch: a quarter-warp's rows pi(0), pi(1) = 0, 2 land 8 banks apart.
+// ===========================================================================
+__device__ __forceinline__ int frag_row(int m) { return (m & 4) | ((m & 1) << 1) | ((m >> 1) & 1); }
+
+template <int KIND, int S, int KS, int TPW>
+__global__ void __launch_bounds__(512 / TPW) st3d_tma_tch(const __grid_constant__ CUtensorMap tm,
+                                                    double* __restrict__ v, StencilDesc d, uint64_t z_begin,
+                                                    uint64_t z_end, int zchunk, int tiles_x, int tiles_xy) {
+    constexpr int BX = kBX, STAGE = stage_doubles(BX);
+    extern __shared__ __align__(128) double smem[];
+    Ring<S, STAGE> ring(smem);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int r = lane >> 2, c = lane & 3;
+    constexpr int NE = 2 * TPW + 1;         // A-fragment elements per lane (tiles share one)
+    const int rb = warp / (8 / TPW), cb0 = TPW * (warp % (8 / TPW));
+    const uint64_t nx = d.nx, ny = d.ny;
+    const int tile = blockIdx.x % tiles_xy;
+    const uint64_t za = z_begin + (uint64_t)(blockIdx.x / tiles_xy) * zchunk;
+    if (za >= z_end) return;
+    const uint64_t zb = min(za + (uint64_t)zchunk, z_end);
+    const int np = (int)(zb - za) + 2;
+    const int64_t x0 = (int64_t)(tile % tiles_x) * kTX, y0 = (int64_t)(tile / tiles_x) * kTY;
+    ring.init(16 / TPW);
+    auto issue = [&](int k) {
+        mbar_expect_tx(ring.full + (k % S), kBY * BX * 8);
+        tma3d(ring.stage(k), &tm, ring.full + (k % S), (int)(x0 - kCofs), (int)(y0 - 1), (int)(za - 1 + k));
+    };
+    if (tid == 0)
+        for (int k = 0; k < S && k < np; ++k) issue(k);
+
+    const int pr = 8 * rb + frag_row(r) + 1;  // stage row of this lane's fragment row
+    // A-fragment element i (tile t = cb0 + i/2 .. k-step): window column 8 cb0 + 4 i + c,
+    // stage column + 1 (window column 0 = x0 - 1 = stage column 1); columns past
+    // the box only meet zero band rows (k = 10, 11), so they are clamped.
+    auto acol = [&](int i) { return min(8 * cb0 + 4 * i + c + 1, BX - 1); };
+    // accumulator pair of tile t: columns x0 + 8 (cb0 + t) + 2c (+1) -> stage column + 2
+    auto dcol = [&](int t) { return 8 * (cb0 + t) + 2 * c + kCofs; };
+
+    double bx[3];
+#pragma unroll
+    for (int kb = 0; kb < 3; ++kb)
+        bx[kb] = KIND == 0 ? bandv(4 * kb + c, r, d.w[5], 0.0, d.w[6]) : bandv(4 * kb + c, r, 1.0, 0.0, 1.0);
+    // KS = 2: weight of the two x+1 taps past the K = 8 window (lane c = 3 only)
+    const double wfix = c == 3 ? (KIND == 0 ? d.w[6] : 1.0) : 0.0;
+    const int src8 = lane & ~3, src9 = src8 | 1;
+
+    double acc_a[TPW][2], acc_b[TPW][2];  // accumulator-position partial sums (C operand)
+    double al_a[NE], al_b[NE];            // KIND 1: alpha partial sums at the A-fragment positions
+#pragma unroll
+    for (int t = 0; t < TPW; ++t) acc_a[t][0] = acc_a[t][1] = acc_b[t][0] = acc_b[t][1] = 0.0;
+#pragma unroll
+    for (int i = 0; i < NE; ++i) al_a[i] = al_b[i] = 0.0;
+    const double w0 = d.w[0], w1 = d.w[1], w2 = d.w[2], w3 = d.w[3], w4 = d.w[4];
+    const int64_t yo = y0 + 8 * rb + frag_row(r);
+    const bool row_ok = yo >= 1 && yo <= (int64_t)ny - 2;
+
+    for (int k = 0; k < np; ++k) {
+        ring.wait_full(k);
+        const double* P = ring.stage(k);
+        const double* Pc = P + pr * BX;
+        double o[TPW][2];
+        if (KIND == 0) {
+            // plane k: finishes output k-1 (its z+1 term), forms output k = U.Bx + C,
+            // starts output k+1 (its z-1 term)
+            double a[NE];
+#pragma unroll
+            for (int i = 0; i < NE; ++i) a[i] = Pc[acol(i)];
+#pragma unroll
+            for (int t = 0; t < TPW; ++t) {
+                const double2 ct = *reinterpret_cast<const double2*>(Pc + dcol(t));
+                const double2 up = *reinterpret_cast<const double2*>(Pc - BX + dcol(t));
+                const double2 dn = *reinterpret_cast<const double2*>(Pc + BX + dcol(t));
+                o[t][0] = fma(w2, ct.x, acc_a[t][0]);
+                o[t][1] = fma(w2, ct.y, acc_a[t][1]);
+                double d0 = fma(w4, dn.x, fma(w3, up.x, fma(w0, ct.x, acc_b[t][0])));
+                double d1 = fma(w4, dn.y, fma(w3, up.y, fma(w0, ct.y, acc_b[t][1])));
+                if (KS == 2) {
+                    d0 = fma(wfix, __shfl_sync(0xffffffffu, a[2 * t + 2], src8), d0);
+                    d1 = fma(wfix, __shfl_sync(0xffffffffu, a[2 * t + 2], src9), d1);
+                }
+#pragma unroll
+                for (int kb = 0; kb < KS; ++kb) dmma_m8n8k4(d0, d1, a[2 * t + kb], bx[kb], d0, d1);
+                acc_a[t][0] = d0;
+                acc_a[t][1] = d1;
+                acc_b[t][0] = w1 * ct.x;
+                acc_b[t][1] = w1 * ct.y;
+            }
+        } else {
+            const double g0 = d.w[0], g1 = d.w[1], g2 = d.w[2], g3 = d.w[3];
+            double aout[NE];
+#pragma unroll
+            for (int i = 0; i < NE; ++i) {
+                const int cc = acol(i);
+                const double a = Pc[cc], b = Pc[cc - BX] + Pc[cc + BX];
+                const double c1 = fma(g3, b, g2 * a);
+                aout[i] = al_a[i] + c1;
+                al_a[i] = al_b[i] + fma(g2, b, g1 * a);
+                al_b[i] = c1;
+            }
+#pragma unroll
+            for (int t = 0; t < TPW; ++t) {
+                const double2 ct = *reinterpret_cast<const double2*>(Pc + dcol(t));
+                const double2 up = *reinterpret_cast<const double2*>(Pc - BX + dcol(t));
+                const double2 dn = *reinterpret_cast<const double2*>(Pc + BX + dcol(t));
+                const double b0 = up.x + dn.x, b1 = up.y + dn.y;
+                const double e0 = fma(g2, b0, g1 * ct.x), e1 = fma(g2, b1, g1 * ct.y);
+                double d0 = acc_a[t][0] + e0, d1 = acc_a[t][1] + e1;
+                acc_a[t][0] = acc_b[t][0] + fma(g1, b0, g0 * ct.x);
+                acc_a[t][1] = acc_b[t][1] + fma(g1, b1, g0 * ct.y);
+                acc_b[t][0] = e0;
+                acc_b[t][1] = e1;
+                if (k >= 2) {
+                    if (KS == 2) {
+                        d0 = fma(wfix, __shfl_sync(0xffffffffu, aout[2 * t + 2], src8), d0);
+                        d1 = fma(wfix, __shfl_sync(0xffffffffu, aout[2 * t + 2], src9), d1);
+                    }
+#pragma unroll
+                    for (int kb = 0; kb < KS; ++kb) dmma_m8n8k4(d0, d1, aout[2 * t + kb], bx[kb], d0, d1);
+                }
+                o[t][0] = d0;
+                o[t][1] = d1;
+            }
+        }
+        ring.release(k);
+        if (tid == 0 && k + S < np) {
+            ring.wait_empty(k);
+            issue(k + S);
+        }
+        if (k >= 2 && row_ok) {
+            const uint64_t z = za - 2 + (uint64_t)k;
+            double* vr = v + (z * ny + (uint64_t)yo) * nx;
+#pragma unroll
+            for (int t = 0; t < TPW; ++t) {
+                const int64_t xx = x0 + 8 * (cb0 + t) + 2 * c;
+                const bool i0 = xx >= 1 && xx <= (int64_t)nx - 2, i1 = xx + 1 <= (int64_t)nx - 2;
+                if (i0 && i1)
+                    asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(vr + xx), "d"(o[t][0]), "d"(o[t][1]) : "memory");
+                else {
+                    if (i0) vr[xx] = o[t][0];
+                    if (i1) vr[xx + 1] = o[t][1];
+                }
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // host: tensor maps
 // ---------------------------------------------------------------------------
@@ -1058,14 +1237,6 @@ cudaError_t launch_stencil_tma(int unit, const StencilDesc& d, uint64_t o0, uint
     }
     const int tiles_x = (int)((d.nx + kTX - 1) / kTX);
     const int tiles_xy = tiles_x * (int)((d.ny + kTY - 1) / kTY);
-    const int nch = split_count(tiles_xy, o1 - o0, 8,
-                                unit == 1 ? (((tuning().stencil_tc3d_mode >> (d.preset == kP3d7 ? 0 : 1)) & 1)
-                                                 ? tuning().stencil_tc1_ctas_per_sm
-                                                 : tuning().stencil_tc3d_ctas_per_sm)
-                                          : tuning().stencil_ctas_per_sm);
-    const int zchunk = (int)((o1 - o0 + nch - 1) / nch);
-    const int zch = (int)((o1 - o0 + zchunk - 1) / zchunk);
-    const unsigned grid = (unsigned)(tiles_xy * zch);
     StencilDesc dd = d;
     int kind = 0;
     if (d.preset == kP3d27) {
@@ -1077,8 +1248,35 @@ cudaError_t launch_stencil_tma(int unit, const StencilDesc& d, uint64_t o0, uint
             kind = 1;
         }
     }
+    const bool tc_hybrid = unit == 1 && kind != 1 && tuning().stencil_tc3d_hybrid;
     const bool tc_onepl = unit == 1 && ((tuning().stencil_tc3d_mode >> (kind == 0 ? 0 : 1)) & 1);
-    if (tc_onepl) {
+    const int nch = split_count(tiles_xy, o1 - o0, 8,
+                                unit == 1 ? (tc_hybrid ? (tuning().stencil_tch_ctas_per_sm
+                                                              ? tuning().stencil_tch_ctas_per_sm
+                                                              : (kind == 0 ? 1 : 8))
+                                             : tc_onepl ? tuning().stencil_tc1_ctas_per_sm
+                                                        : tuning().stencil_tc3d_ctas_per_sm)
+                                          : tuning().stencil_ctas_per_sm);
+    const int zchunk = (int)((o1 - o0 + nch - 1) / nch);
+    const int zch = (int)((o1 - o0 + zchunk - 1) / zchunk);
+    const unsigned grid = (unsigned)(tiles_xy * zch);
+    if (tc_hybrid) {
+        constexpr int S = 4;
+        const size_t sm = ring_bytes<S, kBX>();
+#define RLB_TCH(K, KS, TPW)                                                                                \
+    do {                                                                                                   \
+        if ((e = prep(st3d_tma_tch<K, S, KS, TPW>, sm)) != cudaSuccess) return e;                         \
+        st3d_tma_tch<K, S, KS, TPW><<<grid, 512 / TPW, sm, s>>>(m, v, dd, o0, o1, zchunk, tiles_x, tiles_xy); \
+    } while (0)
+#define RLB_TCH2(K, TPW) \
+    do { if (tuning().stencil_tch_k8) RLB_TCH(K, 2, TPW); else RLB_TCH(K, 3, TPW); } while (0)
+#define RLB_TCH3(K) \
+    do { const int tp = tuning().stencil_tch_tpw ? tuning().stencil_tch_tpw : (K == 0 ? 2 : 4); if (tp == 4) RLB_TCH2(K, 4); else if (tp == 1) RLB_TCH2(K, 1); else RLB_TCH2(K, 2); } while (0)
+        if (kind == 0) RLB_TCH3(0); else RLB_TCH3(1);
+#undef RLB_TCH3
+#undef RLB_TCH2
+#undef RLB_TCH
+    } else if (tc_onepl) {
         constexpr int S = 4;
         const size_t sm = ring_bytes<S, kBX>();
         const int tk = kind == 0 ? 0 : (kind == 2 ? (tuning().stencil_tc_concat ? 3 : 1) : 2);

@@ -15,6 +15,11 @@ METRICS = [
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %", 1, "{:.1f}"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue %", 1, "{:.1f}"),
     ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "fp64 pipe %", 1, "{:.1f}"),
+    ("sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active", "dmma pipe %", 1, "{:.1f}"),
+    ("smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio", "stall mio", 1, "{:.2f}"),
+    ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "stall long sb", 1, "{:.2f}"),
+    ("smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio", "stall math", 1, "{:.2f}"),
+    ("smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio", "stall barrier", 1, "{:.2f}"),
     ("launch__registers_per_thread", "regs", 1, "{:.0f}"),
 ]
 UNITS = {"ns": 1, "us": 1e3, "usecond": 1e3, "ms": 1e6, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9,

@@ -71,6 +71,10 @@ def run(name):
 if __name__ == "__main__":
     names = sys.argv[1:] or ["stream_cc", "stream_tc", "spmv_cc", "spmv_tc", "2d5pt_cc", "2d5pt_tc",
                              "3d7pt_cc", "3d7pt_tc", "3d27pt_cc", "3d27pt_tc"]
+    # PROF_TUNE="key=val,key=val": rl_tuning_set before the runs
+    for kv in filter(None, os.environ.get("PROF_TUNE", "").split(",")):
+        k, v = kv.split("=")
+        P.tuning_set(k, int(v))
     for nm in names:
         run(nm)
         torch.cuda.empty_cache()

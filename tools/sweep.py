@@ -193,6 +193,24 @@ def stencil3d_tc():
           {"stencil_cc27x2": [0, 1, 0, 1], "stencil_rows_per_thread": [2, 4]})
 
 
+def stencil3d_tch():
+    """3D tensor core: x-band hybrid (st3d_tma_tch) vs the full banded kernels, 50 timesteps."""
+    import math
+    for preset in ("3d7pt", "3d27pt"):
+        u = torch.empty((512, 512, 512), dtype=torch.float64, device="cuda")
+        P.stencil_init(u, 1, 1)
+        v = u.clone()
+        nbytes = 50 * 16 * math.prod(s - 2 for s in u.shape)
+        for hy in (1, 0):
+            P.tuning_set("stencil_tc3d_hybrid", hy)
+            grid = {"stencil_tch_ctas_per_sm": [2, 3, 4, 8]} if hy else {}
+            sweep(f"{preset}_tc_hybrid{hy}", lambda: P.stencil(preset, u, v, 50, unit=1), nbytes, grid)
+        P.tuning_set("stencil_tc3d_hybrid", 1)
+        sweep(f"{preset}_cc", lambda: P.stencil(preset, u, v, 50, unit=0), nbytes, {})
+        del u, v
+        torch.cuda.empty_cache()
+
+
 def stencil_r():
     """2d9pt / 2d13pt / 2d49pt at 16384^2; GB/s of algorithmic bytes and the
     FP64 rate (W = 2 |S| per point)."""
@@ -225,6 +243,8 @@ if __name__ == "__main__":
             stencil2d()
         elif w == "stencil3d_cc":
             stencil3d_cc()
+        elif w == "stencil3d_tch":
+            stencil3d_tch()
         elif w == "stencil3d_tc":
             stencil3d_tc()
         elif w == "stencil":
