@@ -329,9 +329,11 @@ def per_kernel_table(torch, P, D, hbm):
         wl = make(name, torch, P, D, 0, 1)
         res = {}
         for uname, unit in (("cc", P.CUDA_CORE), ("tc", P.TENSOR_CORE)):
-            reps = spec["reps"] if name in ("stream", "spmv") else 1
+            # stencils: 5 runs of the full timestep count, median run (one run is
+            # +-5 % noisy on this box; the spread is reported)
+            reps = spec["reps"] if name in ("stream", "spmv") else 5
             total, per = time_steps(torch, wl, unit, reps, 2, 1)
-            ms = total / reps
+            ms = total / reps if name in ("stream", "spmv") else sorted(per)[len(per) // 2]
             if name in ("stream", "spmv"):
                 gbs = wl.bytes / (ms * 1e-3) / 1e9
                 unit_ms = ms
@@ -340,6 +342,10 @@ def per_kernel_table(torch, P, D, hbm):
                 unit_ms = ms / wl.tsteps
             res[uname] = {"gbs": round(gbs, 1), "frac_of_measured_peak": round(gbs / hbm, 4),
                           "ms_per_unit": round(unit_ms, 4)}
+            if name not in ("stream", "spmv"):
+                res[uname]["runs"] = reps
+                res[uname]["gbs_min_max"] = [round(wl.bytes / (max(per) * 1e-3) / 1e9, 1),
+                                             round(wl.bytes / (min(per) * 1e-3) / 1e9, 1)]
         res["tc_over_cc"] = round(res["tc"]["gbs"] / res["cc"]["gbs"], 4)
         res["intensity"] = round(intensity[name], 5)
         rows[name] = res

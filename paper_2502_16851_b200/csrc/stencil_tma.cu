@@ -137,7 +137,9 @@ __global__ void __launch_bounds__(64 * kTY / RYT) st3d_tma_cc(const __grid_const
     if (za >= z_end) return;
     const uint64_t zb = min(za + (uint64_t)zchunk, z_end);
     const int np = (int)(zb - za) + 2;  // planes za-1 .. zb
-    const int64_t x0 = (int64_t)(tile % tiles_x) * kTX, y0 = (int64_t)(tile / tiles_x) * kTY;
+    const int64_t x0 = (int64_t)(tile % tiles_x) * kTX;
+    const uint64_t nty = (uint64_t)(tiles_xy / tiles_x), ty = (uint64_t)(tile / tiles_x);
+    const int64_t y0 = (int64_t)(ty * d.ny / nty), yhi = (int64_t)((ty + 1) * d.ny / nty);  // rows [y0, yhi)
     const uint64_t nx = d.nx, ny = d.ny;
     const int64_t xs = x0 - kCofs;
     const int cofs = kCofs, rofs = 1;  // stage column/row of (x0, y0); boxes may start OOB
@@ -232,7 +234,7 @@ __global__ void __launch_bounds__(64 * kTY / RYT) st3d_tma_cc(const __grid_const
 #pragma unroll
             for (int j = 0; j < RYT; ++j) {
                 const int64_t y = yr0 + j;
-                if (y >= 1 && y <= (int64_t)ny - 2) v[(p * ny + (uint64_t)y) * nx + x] = o[j];
+                if (y >= 1 && y <= (int64_t)ny - 2 && y < yhi) v[(p * ny + (uint64_t)y) * nx + x] = o[j];
             }
         }
     }
@@ -261,7 +263,9 @@ __global__ void __launch_bounds__(32 * kTY / RYT) st3d_tma_cc27x2(const __grid_c
     if (za >= z_end) return;
     const uint64_t zb = min(za + (uint64_t)zchunk, z_end);
     const int np = (int)(zb - za) + 2;  // planes za-1 .. zb
-    const int64_t x0 = (int64_t)(tile % tiles_x) * kTX, y0 = (int64_t)(tile / tiles_x) * kTY;
+    const int64_t x0 = (int64_t)(tile % tiles_x) * kTX;
+    const uint64_t nty = (uint64_t)(tiles_xy / tiles_x), ty = (uint64_t)(tile / tiles_x);
+    const int64_t y0 = (int64_t)(ty * d.ny / nty), yhi = (int64_t)((ty + 1) * d.ny / nty);  // rows [y0, yhi)
     const uint64_t nx = d.nx, ny = d.ny;
     ring.init(kTY / RYT);
     auto issue = [&](int k) {
@@ -289,8 +293,15 @@ __global__ void __launch_bounds__(32 * kTY / RYT) st3d_tma_cc27x2(const __grid_c
         q[2] = mid.y;
         q[3] = hi.x;
     };
+    // warps whose rows all lie past the tile (13-14-row balanced tiles) only
+    // keep the ring protocol (warp 0, the producer's, always has rows)
+    const bool live = yr0 < yhi;
     for (int k = 0; k < np; ++k) {
         ring.wait_full(k);
+        if (!live) {
+            ring.release(k);
+            continue;
+        }
         const double* T = ring.stage(k);
         double pm[RYT][2], p0[RYT][2];
         double up[4], md[4];
@@ -335,7 +346,7 @@ __global__ void __launch_bounds__(32 * kTY / RYT) st3d_tma_cc27x2(const __grid_c
 #pragma unroll
             for (int j = 0; j < RYT; ++j) {
                 const int64_t y = yr0 + j;
-                if (y >= 1 && y <= (int64_t)ny - 2) {
+                if (y >= 1 && y <= (int64_t)ny - 2 && y < yhi) {
                     double* dst = v + (p * ny + (uint64_t)y) * nx + x;
                     if (in0 && in1)
                         asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(dst), "d"(o[j][0]), "d"(o[j][1])
@@ -947,7 +958,9 @@ __global__ void __launch_bounds__(512 / TPW) st3d_tma_tch(const __grid_constant_
     if (za >= z_end) return;
     const uint64_t zb = min(za + (uint64_t)zchunk, z_end);
     const int np = (int)(zb - za) + 2;
-    const int64_t x0 = (int64_t)(tile % tiles_x) * kTX, y0 = (int64_t)(tile / tiles_x) * kTY;
+    const int64_t x0 = (int64_t)(tile % tiles_x) * kTX;
+    const uint64_t nty = (uint64_t)(tiles_xy / tiles_x), ty = (uint64_t)(tile / tiles_x);
+    const int64_t y0 = (int64_t)(ty * d.ny / nty), yhi = (int64_t)((ty + 1) * d.ny / nty);  // rows [y0, yhi)
     ring.init(16 / TPW);
     auto issue = [&](int k) {
         mbar_expect_tx(ring.full + (k % S), kBY * BX * 8);
@@ -980,7 +993,7 @@ __global__ void __launch_bounds__(512 / TPW) st3d_tma_tch(const __grid_constant_
     for (int i = 0; i < NE; ++i) al_a[i] = al_b[i] = 0.0;
     const double w0 = d.w[0], w1 = d.w[1], w2 = d.w[2], w3 = d.w[3], w4 = d.w[4];
     const int64_t yo = y0 + 8 * rb + frag_row(r);
-    const bool row_ok = yo >= 1 && yo <= (int64_t)ny - 2;
+    const bool row_ok = yo >= 1 && yo <= (int64_t)ny - 2 && yo < yhi;
 
     for (int k = 0; k < np; ++k) {
         ring.wait_full(k);
@@ -1236,7 +1249,7 @@ cudaError_t launch_stencil_tma(int unit, const StencilDesc& d, uint64_t o0, uint
         return cudaGetLastError();
     }
     const int tiles_x = (int)((d.nx + kTX - 1) / kTX);
-    const int tiles_xy = tiles_x * (int)((d.ny + kTY - 1) / kTY);
+    int tiles_xy = tiles_x * (int)((d.ny + kTY - 1) / kTY);
     StencilDesc dd = d;
     int kind = 0;
     if (d.preset == kP3d27) {
@@ -1253,10 +1266,26 @@ cudaError_t launch_stencil_tma(int unit, const StencilDesc& d, uint64_t o0, uint
     const int nch = split_count(tiles_xy, o1 - o0, 8,
                                 unit == 1 ? (tc_hybrid ? (tuning().stencil_tch_ctas_per_sm
                                                               ? tuning().stencil_tch_ctas_per_sm
-                                                              : (kind == 0 ? 1 : 8))
+                                                              : (kind == 0 ? 1 : 16))
                                              : tc_onepl ? tuning().stencil_tc1_ctas_per_sm
                                                         : tuning().stencil_tc3d_ctas_per_sm)
                                           : tuning().stencil_ctas_per_sm);
+    // Row balance (one z-front, nch == 1): 256 tiles of 16 rows on 148 SMs put
+    // two tiles on most SMs and one on the rest; instead cut the rows into nty
+    // tiles of <= 16 rows (row y0 = ty * ny / nty) so the busiest SM holds the
+    // fewest rows -- 512 rows: 37 tiles of 13-14 rows, 296 CTAs = 2 per SM.
+    // Kernels that take it: st3d_tma_cc, st3d_tma_cc27x2, st3d_tma_tch.
+    const bool balanced_kernel = unit == 0 || tc_hybrid;
+    if (balanced_kernel && nch == 1 && tuning().stencil3d_balance) {
+        const uint64_t nty0 = (d.ny + kTY - 1) / kTY;
+        uint64_t best = nty0, bcost = ~0ull;
+        for (uint64_t nty = nty0; nty <= 2 * nty0; ++nty) {
+            const uint64_t per_sm = ((uint64_t)tiles_x * nty + kNumSMs - 1) / kNumSMs;
+            const uint64_t cost = per_sm * ((d.ny + nty - 1) / nty);
+            if (cost < bcost) { bcost = cost; best = nty; }
+        }
+        tiles_xy = tiles_x * (int)best;
+    }
     const int zchunk = (int)((o1 - o0 + nch - 1) / nch);
     const int zch = (int)((o1 - o0 + zchunk - 1) / zchunk);
     const unsigned grid = (unsigned)(tiles_xy * zch);
