@@ -51,6 +51,7 @@ struct Tuning {
     int stencil_tc3d_hybrid = 1;       // 3D tensor core: x-band on DMMA, centre/y/z on DFMA (st3d_tma_tch, 3 DMMA/tile); 3d7pt and class-weight 3d27pt
     int stencil_tch_ctas_per_sm = 0;   // ... grid sizing of that kernel (0: per preset, 3d7pt 1 = one z-front, 3d27pt 16)
     int stencil_tch_tpw = 0;           // ... 8x8 tiles per warp: 4 (128-thread CTAs), 2 (256), 1 (512); 0: per preset (3d7pt 2, 3d27pt 4)
+    int stencil_tc2d_hybrid = 1;       // 2d5pt tensor core: x-band on DMMA, centre/y on DFMA (st2d_tma_tch, 3 DMMA/tile); 0: 6 DMMA/tile
     int stencil3d_balance = 1;         // 3D TMA kernels with one z-front: rows cut into tiles of <= 16 so the SMs hold equal rows
     int stencil_tch_k8 = 0;            // ... 1: K = 8 band window (2 DMMA/tile, two x+1 taps by shuffle + DFMA; measured no faster); 0: K = 12, 3 DMMA
     int stencil_r_cc_stages = 0;       // ... CUDA-core ring depth: 2-4, 0 = auto (2 for 2d49pt -> 4 CTAs/SM, else 4)

@@ -536,6 +536,85 @@ __global__ void __launch_bounds__(128) st2d_tma_tc(const __grid_constant__ CUten
 }
 
 // ===========================================================================
+// Tensor core, 2d5pt, x-band on DMMA (the default 2D TC kernel): the 3D
+// st3d_tma_tch scheme in 2D -- D = U . band(w_x-, 0, w_x+) + C with
+// C = w_c u + w_y- u[y-1] + w_y+ u[y+1] formed by DFMA at the accumulator
+// positions: 3 DMMA per 8x8 tile instead of the 6 of st2d_tma_tc, fragment
+// rows permuted (frag_row) for conflict-free 128-bit accumulator loads.
+// ===========================================================================
+__device__ __forceinline__ int frag_row2(int m) { return (m & 4) | ((m & 1) << 1) | ((m >> 1) & 1); }
+
+template <int S>
+__global__ void __launch_bounds__(128) st2d_tma_tch(const __grid_constant__ CUtensorMap tm,
+                                                    double* __restrict__ v, uint64_t nx, uint64_t y_begin,
+                                                    uint64_t y_end, int seg_rows, int strips, StencilDesc d) {
+    constexpr int BX = kBX, STAGE = stage_doubles(BX);
+    extern __shared__ __align__(128) double smem[];
+    Ring<S, STAGE> ring(smem);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int r = lane >> 2, c = lane & 3;
+    const int rb = warp >> 1, cb0 = 4 * (warp & 1);
+    const int64_t x0 = (int64_t)(blockIdx.x % strips) * kTX;
+    const uint64_t ya = y_begin + (uint64_t)(blockIdx.x / strips) * seg_rows;
+    if (ya >= y_end) return;
+    const uint64_t yb = min(ya + (uint64_t)seg_rows, y_end);
+    const int nblk = (int)((yb - ya + kTY - 1) / kTY);
+    ring.init(4);
+    auto issue = [&](int k) {
+        mbar_expect_tx(ring.full + (k % S), kBY * BX * 8);
+        tma2d(ring.stage(k), &tm, ring.full + (k % S), (int)(x0 - kCofs), (int)(ya + (uint64_t)k * kTY) - 1);
+    };
+    if (tid == 0)
+        for (int k = 0; k < S && k < nblk; ++k) issue(k);
+    double bx[3];
+#pragma unroll
+    for (int kb = 0; kb < 3; ++kb) bx[kb] = bandv(4 * kb + c, r, d.w[3], 0.0, d.w[4]);
+    const double w0 = d.w[0], w1 = d.w[1], w2 = d.w[2];
+    const int fr = frag_row2(r), pr = 8 * rb + fr + 1;
+    for (int k = 0; k < nblk; ++k) {
+        ring.wait_full(k);
+        const double* Pc = ring.stage(k) + pr * BX;
+        double a[9];
+#pragma unroll
+        for (int i = 0; i < 9; ++i) a[i] = Pc[min(8 * cb0 + 4 * i + c + 1, BX - 1)];
+        double D0[4], D1[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int dc = 8 * (cb0 + t) + 2 * c + kCofs;
+            const double2 ct = *reinterpret_cast<const double2*>(Pc + dc);
+            const double2 up = *reinterpret_cast<const double2*>(Pc - BX + dc);
+            const double2 dn = *reinterpret_cast<const double2*>(Pc + BX + dc);
+            double d0 = fma(w2, dn.x, fma(w1, up.x, w0 * ct.x));
+            double d1 = fma(w2, dn.y, fma(w1, up.y, w0 * ct.y));
+#pragma unroll
+            for (int kb = 0; kb < 3; ++kb) dmma_m8n8k4(d0, d1, a[2 * t + kb], bx[kb], d0, d1);
+            D0[t] = d0;
+            D1[t] = d1;
+        }
+        ring.release(k);
+        if (tid == 0 && k + S < nblk) {
+            ring.wait_empty(k);
+            issue(k + S);
+        }
+        const uint64_t y = ya + (uint64_t)k * kTY + 8 * rb + fr;
+        if (y < yb) {
+            double* vr = v + y * nx;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const int64_t xx = x0 + 8 * (cb0 + t) + 2 * c;
+                const bool i0 = xx >= 1 && xx <= (int64_t)nx - 2, i1 = xx + 1 <= (int64_t)nx - 2;
+                if (i0 && i1)
+                    asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(vr + xx), "d"(D0[t]), "d"(D1[t]) : "memory");
+                else {
+                    if (i0) vr[xx] = D0[t];
+                    if (i1) vr[xx + 1] = D1[t];
+                }
+            }
+        }
+    }
+}
+
+// ===========================================================================
 // Tensor core, 3D: planes z-1, z, z+1 resident (S >= 5).
 // KIND 0: 3d7pt, 1: 3d27pt class weights, 2: 3d27pt general.
 // ===========================================================================
@@ -1231,8 +1310,13 @@ cudaError_t launch_stencil_tma(int unit, const StencilDesc& d, uint64_t o0, uint
         if (unit == 1) {
             constexpr int S = 4;
             const size_t sm = ring_bytes<S, kBX>();
-            if ((e = prep(st2d_tma_tc<S>, sm)) != cudaSuccess) return e;
-            st2d_tma_tc<S><<<grid, 128, sm, s>>>(m, v, d.nx, o0, o1, seg_rows, strips, d);
+            if (tuning().stencil_tc2d_hybrid) {
+                if ((e = prep(st2d_tma_tch<S>, sm)) != cudaSuccess) return e;
+                st2d_tma_tch<S><<<grid, 128, sm, s>>>(m, v, d.nx, o0, o1, seg_rows, strips, d);
+            } else {
+                if ((e = prep(st2d_tma_tc<S>, sm)) != cudaSuccess) return e;
+                st2d_tma_tc<S><<<grid, 128, sm, s>>>(m, v, d.nx, o0, o1, seg_rows, strips, d);
+            }
         } else {
             constexpr int S = 4;
             const size_t sm = ring_bytes<S, kBX>();
