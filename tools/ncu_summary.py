@@ -1,5 +1,5 @@
 """Markdown table of the key metrics of ncu --set full captures:
-python tools/ncu_summary.py "label::path.ncu-rep[@algorithmic GB per launch]" ..."""
+python tools/ncu_summary.py "label::path.ncu-rep[#kernel regex][@algorithmic GB per launch]" ..."""
 import csv
 import io
 import subprocess
@@ -27,9 +27,13 @@ UNITS = {"ns": 1, "us": 1e3, "usecond": 1e3, "ms": 1e6, "byte": 1, "Kbyte": 1e3,
 
 
 def read(path):
+    import re
+    path, _, pat = path.partition("#")  # "file.ncu-rep#kernel-name regex": first matching launch
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    head, units, vals = rows[0], rows[1], rows[2]
+    head, units = rows[0], rows[1]
+    ki = head.index("Kernel Name")
+    vals = next(r for r in rows[2:] if not pat or re.search(pat, r[ki]))
     res = {"kernel": vals[head.index("Kernel Name")]}
     for m, *_ in METRICS:
         if m in head:
