@@ -326,15 +326,24 @@ def test_temporal_depth_restrictions(cuda):
     assert e.value.kind == "ValidationError"
 
 
-@pytest.mark.parametrize("mode", [0, 3])
+@pytest.mark.parametrize("knobs", [
+    {"stencil_tc3d_hybrid": 0, "stencil_tc3d_mode": 0},
+    {"stencil_tc3d_hybrid": 0, "stencil_tc3d_mode": 3},
+    {"stencil_tc3d_hybrid": 1},
+    {"stencil_tc3d_hybrid": 1, "stencil_tch_tpw": 4, "stencil_tch_ctas_per_sm": 8},
+    {"stencil_tc3d_hybrid": 1, "stencil_tch_tpw": 1, "stencil_tch_k8": 1},
+    {"stencil_tc3d_hybrid": 1, "stencil_tch_tpw": 2, "stencil_tch_k8": 1, "stencil3d_balance": 0},
+])
 @pytest.mark.parametrize("preset", ["3d7pt", "3d27pt"])
-@pytest.mark.parametrize("shape", [(10, 17, 66), (34, 20, 130), (40, 40, 64)])
-def test_3d_tensor_core_formulations(cuda, mode, preset, shape):
-    """Both 3D tensor-core formulations (3 planes resident / one plane with
-    partial sums) match the oracle, for class and general 27pt weights."""
+@pytest.mark.parametrize("shape", [(10, 17, 66), (34, 20, 130), (40, 40, 64), (12, 70, 200)])
+def test_3d_tensor_core_formulations(cuda, knobs, preset, shape):
+    """Every 3D tensor-core formulation (full banded with 3 planes resident or
+    one plane with partial sums; the x-band kernel st3d_tma_tch with its
+    tiles-per-warp / K-window / row-balance knobs) matches the oracle, for
+    class and general 27pt weights."""
     import torch
 
-    prev = P.tuning_set("stencil_tc3d_mode", mode)
+    prev = {k: P.tuning_set(k, v) for k, v in knobs.items()}
     try:
         u0 = O.stencil_init(shape, 1, 23)
         out, _ = _run(torch, preset, u0, 3, P.TENSOR_CORE)
@@ -345,7 +354,41 @@ def test_3d_tensor_core_formulations(cuda, mode, preset, shape):
             out, _ = _run(torch, preset, u0, 2, P.TENSOR_CORE, weights=w)
             assert O.rel_err(out, O.stencil(preset, u0, 2, w)) <= TOL
     finally:
-        P.tuning_set("stencil_tc3d_mode", prev)
+        for k, v in prev.items():
+            P.tuning_set(k, v)
+
+
+@pytest.mark.parametrize("hybrid", [0, 1])
+@pytest.mark.parametrize("shape", [(70, 132), (130, 260), (33, 1030)])
+def test_2d_tensor_core_formulations(cuda, hybrid, shape):
+    """2d5pt tensor core: the x-band kernel (st2d_tma_tch) and the full banded
+    kernel match the oracle."""
+    import torch
+
+    prev = P.tuning_set("stencil_tc2d_hybrid", hybrid)
+    try:
+        u0 = O.stencil_init(shape, 1, 29)
+        out, _ = _run(torch, "2d5pt", u0, 3, P.TENSOR_CORE)
+        assert O.rel_err(out, O.stencil("2d5pt", u0, 3)) <= TOL
+    finally:
+        P.tuning_set("stencil_tc2d_hybrid", prev)
+
+
+@pytest.mark.parametrize("balance", [0, 1])
+@pytest.mark.parametrize("preset", ["3d7pt", "3d27pt"])
+def test_3d_row_balanced_tiles(cuda, balance, preset):
+    """Row-balanced tiles (rows cut into nty tiles of 13-14 rows at 512 rows;
+    here 200 rows -> tiles of <= 16) match the oracle on both units."""
+    import torch
+
+    prev = P.tuning_set("stencil3d_balance", balance)
+    try:
+        u0 = O.stencil_init((6, 200, 256), 1, 31)
+        for unit in (P.CUDA_CORE, P.TENSOR_CORE):
+            out, _ = _run(torch, preset, u0, 2, unit)
+            assert O.rel_err(out, O.stencil(preset, u0, 2)) <= TOL
+    finally:
+        P.tuning_set("stencil3d_balance", prev)
 
 
 @pytest.mark.parametrize("shape_knob", [0, 1, 2])
