@@ -420,6 +420,7 @@ struct rl_spmv_plan_s {
     std::vector<uint64_t> chunk_row;   // chunk c = rows [chunk_row[c], chunk_row[c+1])
     std::vector<uint64_t> chunk_xend;  // x prefix [0, chunk_xend[c]) chunk c reads
     std::vector<uint64_t> xpiece;      // x upload pieces: [xpiece[i], xpiece[i+1])
+    std::vector<char> ycut;            // chunk c ends a y copy group
     cudaStream_t s_in = nullptr, s_cmp = nullptr, s_out = nullptr;
     int long_rows = 0;  // the CSR has rows the per-row kernels divert (spmv.cu)
     std::vector<cudaEvent_t> ev_x, ev_y;
@@ -535,6 +536,32 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
         if (run > pl->xpiece.back()) pl->xpiece.push_back(run);
     }
     if (pl->xpiece.back() < n) pl->xpiece.push_back(n);
+    // Fewer, larger copies (spmv_plan_xpieces / spmv_plan_ygroups): with both
+    // PCIe directions busy every extra copy pair costs ~8-17 us
+    // (tools/micro/pcie_multi.cu: 64 MiB moves in 0.675 ms as 1+1 copies,
+    // 0.925 ms as 16+16).  The first x piece stays the first chunk's prefix so
+    // compute and the y stream start early; the later boundaries are thinned
+    // to at most `xpieces` pieces.
+    if (const int xp = rlb::tuning().spmv_plan_xpieces; xp >= 2 && pl->xpiece.size() - 1 > (size_t)xp) {
+        std::vector<uint64_t> b(pl->xpiece.begin() + 1, pl->xpiece.end());  // piece ends, last == n
+        std::vector<uint64_t> keep{0, b[0]};
+        const size_t rest = b.size() - 1;  // ends after the first piece
+        for (int j = 1; j < xp; ++j) {
+            const uint64_t e = b[std::min(rest, (size_t)((uint64_t)rest * j / (xp - 1)))];
+            if (e > keep.back()) keep.push_back(e);
+        }
+        if (keep.back() < n) keep.push_back(n);
+        pl->xpiece = keep;
+    }
+    // y copies: one per group of consecutive chunks (0: one per chunk)
+    {
+        const int yg = rlb::tuning().spmv_plan_ygroups;
+        for (uint64_t c = 0; c < nch; ++c) {
+            const bool last = c + 1 == nch;
+            const bool cut = yg <= 0 || last || (uint64_t)((c + 1) * (uint64_t)yg / nch) != (uint64_t)(c * (uint64_t)yg / nch);
+            pl->ycut.push_back(cut ? 1 : 0);
+        }
+    }
     const uint64_t npc = pl->xpiece.size() - 1;
     ck(cudaStreamCreateWithFlags(&pl->s_in, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&pl->s_cmp, cudaStreamNonBlocking), "stream");
@@ -576,6 +603,7 @@ void plan_enqueue(rl_spmv_plan_s* pl, const double* x, double* y, double* y_dire
         mark(pl->s_in);
     }
     size_t waited = 0;  // x pieces the compute stream already waits for
+    uint64_t ystart = 0;   // first row of the pending y group
     for (size_t c = 0; c + 1 < pl->chunk_row.size(); ++c) {
         while (waited < npc && pl->xpiece[waited] < pl->chunk_xend[c]) {
             ck(cudaStreamWaitEvent(pl->s_cmp, pl->ev_x[waited], 0), "wait");
@@ -585,11 +613,13 @@ void plan_enqueue(rl_spmv_plan_s* pl, const double* x, double* y, double* y_dire
         mark(pl->s_cmp);
         plan_rows(pl, r0, r1, pl->x, y_direct ? y_direct : pl->y, pl->s_cmp);
         mark(pl->s_cmp);
-        if (!y_direct) {
+        if (!y_direct && pl->ycut[c]) {
             ck(cudaEventRecord(pl->ev_y[c], pl->s_cmp), "event");
             ck(cudaStreamWaitEvent(pl->s_out, pl->ev_y[c], 0), "wait");
-            ck(cudaMemcpyAsync(y + r0, pl->y + r0, (r1 - r0) * 8, cudaMemcpyDeviceToHost, pl->s_out), "D2H y");
+            ck(cudaMemcpyAsync(y + ystart, pl->y + ystart, (r1 - ystart) * 8, cudaMemcpyDeviceToHost, pl->s_out),
+               "D2H y");
             mark(pl->s_out);
+            ystart = r1;
         }
     }
 }
@@ -1094,6 +1124,8 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         else if (k == "spmv_long_group") slot = &t.spmv_long_group;
         else if (k == "spmv_plan_graph") slot = &t.spmv_plan_graph;
         else if (k == "spmv_plan_taper") slot = &t.spmv_plan_taper;
+        else if (k == "spmv_plan_xpieces") slot = &t.spmv_plan_xpieces;
+        else if (k == "spmv_plan_ygroups") slot = &t.spmv_plan_ygroups;
         else if (k == "stencil_r_ctas_per_sm") slot = &t.stencil_r_ctas_per_sm;
         else if (k == "stencil_tb_waves") slot = &t.stencil_tb_waves;
         else if (k == "stencil_tb") slot = &t.stencil_tb;

@@ -28,6 +28,8 @@ struct Tuning {
     int spmv_long_group = 8;       // lanes per piece of the CUDA-core long-row kernel (8, 16, 32)
     int spmv_plan_chunks = 16;     // pipelined row/x chunks of rl_spmv_plan_execute_host
     int spmv_plan_tiled = 0;       // 1: CUDA-core plans use the column-tiled layout (spmv_tiled.cu; 0.30 ms vs CSR 0.28 ms on the BASELINE matrix)
+    int spmv_plan_xpieces = 0;     // max x upload pieces (first = chunk 0's prefix); 0: one per chunk
+    int spmv_plan_ygroups = 0;     // y download copies (groups of consecutive chunks); 0: one per chunk
     int spmv_plan_taper = 0;       // 1: half-size first/last pipeline chunks (measured no gain)
     int spmv_plan_graph = 1;       // execute_host with pinned x/y as one captured CUDA graph
     int spmv_plan_zero_copy = 0;   // 1: store y straight into pinned host memory (measured slower)
