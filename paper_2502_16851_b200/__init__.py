@@ -476,10 +476,17 @@ class SpmvPlan:
         return _kc(k)
 
     def info(self):
-        """(tiled, layout_bytes): layout used and the bytes one execute streams for A."""
+        """(tiled, layout_bytes): whether the column-tiled layout is used and the
+        bytes one execute streams for A."""
         t, b = _int(), _u64()
         _check(lib().rl_spmv_plan_info(self._h, C.byref(t), C.byref(b)))
-        return bool(t.value), int(b.value)
+        return t.value == 1, int(b.value)
+
+    def layout(self) -> str:
+        """"csr", "tiled" (spmv_tiled.cu) or "sorted" (column-sorted blocks, spmv_sorted.cu)."""
+        t = _int()
+        _check(lib().rl_spmv_plan_info(self._h, C.byref(t), None))
+        return {0: "csr", 1: "tiled", 2: "sorted"}[t.value]
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:

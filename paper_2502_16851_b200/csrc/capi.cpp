@@ -6,6 +6,7 @@
 // kernel(s) on the caller's stream, and returns the reference model's W/Q for
 // the call.  There is no CPU path: a missing/unusable device surfaces as a
 // CUDA error code (RL_ERR_CUDA_BASE + cudaError_t).
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -412,6 +413,13 @@ struct rl_spmv_plan_s {
     double *val = nullptr, *x = nullptr, *y = nullptr;
     // column-tiled layout (CUDA-core plans): segments, tile table, block table
     bool tiled = false;
+    // column-sorted block layout (spmv_sorted.cu)
+    bool sorted = false;
+    int scap = 0;
+    rlb::SpmvSBlock* sblk = nullptr;
+    uint32_t* spk = nullptr;
+    double* ssv = nullptr;
+    std::vector<uint32_t> sblk_r0;
     uint8_t* segs = nullptr;
     rlb::SpmvTile* tiles = nullptr;
     int* blk_tiles = nullptr;
@@ -437,6 +445,9 @@ struct rl_spmv_plan_s {
         if (val) cudaFree(val);
         if (x) cudaFree(x);
         if (y) cudaFree(y);
+        if (sblk) cudaFree(sblk);
+        if (spk) cudaFree(spk);
+        if (ssv) cudaFree(ssv);
         if (segs) cudaFree(segs);
         if (tiles) cudaFree(tiles);
         if (blk_tiles) cudaFree(blk_tiles);
@@ -488,13 +499,39 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
                "plan upload");
         ck(cudaMemcpy(pl->blk_tiles, blk.data(), blk.size() * sizeof(int), cudaMemcpyHostToDevice), "plan upload");
     } else {
+        // column-sorted blocks (spmv_sorted.cu) for CUDA-core plans whose rows
+        // all fit (<= 64 nonzeros, block column span < 2^18); else the CSR
+        std::vector<rlb::SpmvSBlock> sb;
+        std::vector<uint32_t> spk;
+        std::vector<double> ssv;
+        if (unit == ExecutionUnit::CudaCore && rlb::tuning().spmv_plan_sorted && nnz > 0) {
+            for (uint64_t i = 0; i < m; ++i)
+                for (int32_t k = rp[i]; k < rp[i + 1]; ++k)
+                    if (col[k] < 0 || (uint64_t)col[k] >= n)
+                        throw Error(ErrorKind::IndexOutOfRange, "column index " + std::to_string(col[k]) +
+                                                                    " outside [0, " + std::to_string(n) + ")");
+            pl->scap = rlb::spmv_sorted_cap();
+            pl->sorted = rlb::spmv_sorted_build(m, rp, col, val, pl->scap, sb, spk, ssv);
+        }
         ck(cudaMalloc(&pl->rp, (m + 1) * 4), "plan alloc");
-        ck(cudaMalloc(&pl->col, std::max<uint64_t>(nnz, 1) * 4), "plan alloc");
-        ck(cudaMalloc(&pl->val, std::max<uint64_t>(nnz, 1) * 8), "plan alloc");
         ck(cudaMemcpy(pl->rp, rp, (m + 1) * 4, cudaMemcpyHostToDevice), "plan upload");
-        ck(cudaMemcpy(pl->col, col, nnz * 4, cudaMemcpyHostToDevice), "plan upload");
-        ck(cudaMemcpy(pl->val, val, nnz * 8, cudaMemcpyHostToDevice), "plan upload");
-        pl->layout_bytes = (m + 1) * 4 + nnz * 12;
+        if (pl->sorted) {
+            ck(cudaMalloc(&pl->sblk, sb.size() * sizeof(rlb::SpmvSBlock)), "plan alloc");
+            ck(cudaMalloc(&pl->spk, nnz * 4), "plan alloc");
+            ck(cudaMalloc(&pl->ssv, nnz * 8), "plan alloc");
+            ck(cudaMemcpy(pl->sblk, sb.data(), sb.size() * sizeof(rlb::SpmvSBlock), cudaMemcpyHostToDevice),
+               "plan upload");
+            ck(cudaMemcpy(pl->spk, spk.data(), nnz * 4, cudaMemcpyHostToDevice), "plan upload");
+            ck(cudaMemcpy(pl->ssv, ssv.data(), nnz * 8, cudaMemcpyHostToDevice), "plan upload");
+            for (const auto& b : sb) pl->sblk_r0.push_back(b.r0);
+            pl->layout_bytes = (m + 1) * 4 + nnz * 12 + sb.size() * sizeof(rlb::SpmvSBlock);
+        } else {
+            ck(cudaMalloc(&pl->col, std::max<uint64_t>(nnz, 1) * 4), "plan alloc");
+            ck(cudaMalloc(&pl->val, std::max<uint64_t>(nnz, 1) * 8), "plan alloc");
+            ck(cudaMemcpy(pl->col, col, nnz * 4, cudaMemcpyHostToDevice), "plan upload");
+            ck(cudaMemcpy(pl->val, val, nnz * 8, cudaMemcpyHostToDevice), "plan upload");
+            pl->layout_bytes = (m + 1) * 4 + nnz * 12;
+        }
     }
     // pipeline chunks: whole tiled blocks when tiled
     const uint64_t unitrows = pl->tiled ? (uint64_t)rlb::kSpmvTiledRows : 1;
@@ -504,7 +541,7 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
         for (uint64_t i = 0; i < m; ++i) maxlen = std::max<int64_t>(maxlen, (int64_t)rp[i + 1] - rp[i]);
         pl->long_rows = (maxlen > rlb::tuning().spmv_long_min && rlb::tuning().spmv_long_rows) ? 1 : 0;
     }
-    const uint64_t nch = std::min<uint64_t>((uint64_t)rlb::tuning().spmv_plan_chunks, units);
+    uint64_t nch = std::min<uint64_t>((uint64_t)rlb::tuning().spmv_plan_chunks, units);
     // Chunk c covers weight w_c of the rows: w = 1/2 for the first and last
     // chunk, 1 otherwise (spmv_plan_taper), so the pipeline's head (the first
     // x prefix) and tail (the last compute + y copy) are short while the
@@ -517,6 +554,14 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
         if (c < nch) acc += (taper && (c == 0 || c == nch - 1)) ? 1 : 2;
     }
     pl->chunk_row.back() = m;
+    if (pl->sorted) {  // chunk boundaries on block starts
+        for (size_t c = 1; c + 1 < pl->chunk_row.size(); ++c) {
+            auto it = std::lower_bound(pl->sblk_r0.begin(), pl->sblk_r0.end(), (uint32_t)pl->chunk_row[c]);
+            pl->chunk_row[c] = it == pl->sblk_r0.end() ? m : *it;
+        }
+        pl->chunk_row.erase(std::unique(pl->chunk_row.begin(), pl->chunk_row.end()), pl->chunk_row.end());
+        nch = pl->chunk_row.size() - 1;
+    }
     for (uint64_t c = 0; c < nch; ++c) {
         uint64_t mx = 0;
         for (int64_t j = rp[pl->chunk_row[c]]; j < rp[pl->chunk_row[c + 1]]; ++j) {
@@ -580,6 +625,13 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
 
 // Rows [r0, r1) of y = A x on the plan's layout (r0/r1 block-aligned when tiled).
 void plan_rows(rl_spmv_plan_s* pl, uint64_t r0, uint64_t r1, const double* x, double* y, cudaStream_t s) {
+    if (pl->sorted) {
+        const auto& v = pl->sblk_r0;
+        const int b0 = (int)(std::lower_bound(v.begin(), v.end(), (uint32_t)r0) - v.begin());
+        const int b1 = r1 >= pl->m ? (int)v.size() : (int)(std::lower_bound(v.begin(), v.end(), (uint32_t)r1) - v.begin());
+        ck(rlb::launch_spmv_sorted(pl->sblk, b0, b1, pl->spk, pl->ssv, pl->rp, x, y, pl->scap, s), "spmv (sorted plan)");
+        return;
+    }
     if (pl->tiled) {
         const uint64_t b0 = r0 / rlb::kSpmvTiledRows;
         const uint64_t b1 = (r1 + rlb::kSpmvTiledRows - 1) / rlb::kSpmvTiledRows;
@@ -918,7 +970,7 @@ int rl_spmv_plan_execute(rl_spmv_plan pl, const double* x, double* y, rl_stream 
 int rl_spmv_plan_info(rl_spmv_plan pl, int* tiled, uint64_t* layout_bytes) {
     return guarded([&] {
         require_ptr(pl, "plan");
-        if (tiled) *tiled = pl->tiled ? 1 : 0;
+        if (tiled) *tiled = pl->tiled ? 1 : (pl->sorted ? 2 : 0);
         if (layout_bytes) *layout_bytes = pl->layout_bytes;
     });
 }
@@ -1125,6 +1177,9 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         else if (k == "spmv_plan_graph") slot = &t.spmv_plan_graph;
         else if (k == "spmv_plan_taper") slot = &t.spmv_plan_taper;
         else if (k == "spmv_plan_xpieces") slot = &t.spmv_plan_xpieces;
+        else if (k == "spmv_plan_sorted") slot = &t.spmv_plan_sorted;
+        else if (k == "spmv_sorted_cap") slot = &t.spmv_sorted_cap;
+        else if (k == "spmv_sorted_pipe") slot = &t.spmv_sorted_pipe;
         else if (k == "spmv_plan_ygroups") slot = &t.spmv_plan_ygroups;
         else if (k == "stencil_r_ctas_per_sm") slot = &t.stencil_r_ctas_per_sm;
         else if (k == "stencil_tb_waves") slot = &t.stencil_tb_waves;

@@ -27,6 +27,9 @@ struct Tuning {
     int spmv_long_piece = 512;     // ... cut into pieces of this many nonzeros, balanced over the warps
     int spmv_long_group = 8;       // lanes per piece of the CUDA-core long-row kernel (8, 16, 32)
     int spmv_plan_chunks = 16;     // pipelined row/x chunks of rl_spmv_plan_execute_host
+    int spmv_plan_sorted = 0;      // 1: CUDA-core plans use the column-sorted block layout when eligible (spmv_sorted.cu; halves the L2 requests but measured 0.287 vs 0.274 ms: latency-bound)
+    int spmv_sorted_cap = 16384;   // ... slot grid per block (16384: 1024 threads, 1 CTA/SM; 8192: 512 threads, 3 CTAs/SM)
+    int spmv_sorted_pipe = 0;      // ... cap 12288: software-pipelined kernel (two product buffers, 1 CTA/SM)
     int spmv_plan_tiled = 0;       // 1: CUDA-core plans use the column-tiled layout (spmv_tiled.cu; 0.30 ms vs CSR 0.28 ms on the BASELINE matrix)
     int spmv_plan_xpieces = 0;     // max x upload pieces (first = chunk 0's prefix); 0: one per chunk
     int spmv_plan_ygroups = 0;     // y download copies (groups of consecutive chunks); 0: one per chunk
@@ -176,6 +179,21 @@ void spmv_tiled_build(uint64_t m, uint64_t n, const int32_t* rp, const int32_t* 
                       std::vector<uint8_t>& segs, std::vector<SpmvTile>& tiles, std::vector<int>& blk_tiles);
 cudaError_t launch_spmv_tiled(uint64_t m, const uint8_t* segs, const SpmvTile* tiles, const int* blk_tiles,
                               uint64_t b0, uint64_t b1, const double* x, double* y, cudaStream_t s);
+
+// Column-sorted block layout (rl_spmv_plan's default CUDA-core layout when
+// eligible; spmv_sorted.cu).
+struct SpmvSBlock {
+    uint32_t r0;       // first row
+    uint32_t rows;     // rows (<= 1024)
+    uint64_t k0;       // first nonzero (CSR offset; the block's entries are [k0, k0 + nent))
+    int32_t colbase;   // smallest column of the block
+    int32_t nent;      // nonzeros
+};
+int spmv_sorted_cap();
+bool spmv_sorted_build(uint64_t m, const int32_t* rp, const int32_t* col, const double* val, int cap,
+                       std::vector<SpmvSBlock>& blks, std::vector<uint32_t>& pk, std::vector<double>& sv);
+cudaError_t launch_spmv_sorted(const SpmvSBlock* blks, int b0, int b1, const uint32_t* pk, const double* sv,
+                               const int32_t* rp, const double* x, double* y, int cap, cudaStream_t s);
 
 // Launch accounting (rl_kernel_launches): every <<<>>> site reports itself.
 void note_launch(uint64_t n = 1);

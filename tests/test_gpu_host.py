@@ -78,10 +78,14 @@ def tiled_plans():
 
 
 def _plan_check(torch, rp, col, val, ncols, unit, expect_tiled):
+    """expect_tiled: True / False (tiled or not), or a layout name."""
     x = np.random.default_rng(5).uniform(-1, 1, ncols)
     ref = O.spmv_csr(rp, col, val, x)
     plan = P.SpmvPlan(rp, col, val, ncols, unit=unit)
-    assert plan.info()[0] == expect_tiled
+    if isinstance(expect_tiled, str):
+        assert plan.layout() == expect_tiled
+    else:
+        assert plan.info()[0] == expect_tiled
     y = np.full(rp.size - 1, np.nan)
     plan.execute_host(x, y)
     assert O.rel_err(y, ref) <= 1e-12
@@ -98,11 +102,78 @@ def _plan_check(torch, rp, col, val, ncols, unit, expect_tiled):
     plan.close()
 
 
-def test_plan_default_layout_is_csr(cuda):
+@pytest.fixture
+def sorted_plans():
+    """The column-sorted block layout is opt-in (tuning key spmv_plan_sorted)."""
+    P.tuning_set("spmv_plan_sorted", 1)
+    yield
+    P.tuning_set("spmv_plan_sorted", 0)
+
+
+def test_plan_default_layout(cuda):
+    """Plans keep the caller's CSR by default; with spmv_plan_sorted = 1,
+    CUDA-core plans whose rows all fit (<= 64 nonzeros) take the
+    column-sorted block layout, tensor-core plans keep CSR."""
     import torch
 
     rp, col, val = O.gen_band_csr(10000, 0, 10000, 8, 500, 3)
-    _plan_check(torch, rp, col, val, 10000, P.CUDA_CORE, False)
+    _plan_check(torch, rp, col, val, 10000, P.CUDA_CORE, "csr")
+    P.tuning_set("spmv_plan_sorted", 1)
+    try:
+        _plan_check(torch, rp, col, val, 10000, P.CUDA_CORE, "sorted")
+        _plan_check(torch, rp, col, val, 10000, P.TENSOR_CORE, "csr")
+    finally:
+        P.tuning_set("spmv_plan_sorted", 0)
+
+
+@pytest.mark.parametrize("cap,pipe", [(16384, 0), (12288, 0), (12288, 1), (8192, 0)])
+@pytest.mark.parametrize("m,n,k,hb", [(1024 * 5 + 3, 1024 * 5 + 3, 16, 65536), (100000, 100000, 16, 65536),
+                                      (50000, 60000, 7, 300), (20000, 20000, 64, 20000),
+                                      (30000, 30000, 5, 200000)])
+def test_sorted_plan_banded(cuda, sorted_plans, cap, pipe, m, n, k, hb):
+    """Column-sorted blocks (spmv_sorted.cu): banded matrices up to 64
+    nonzeros per row, rectangular, and bands wider than a block's 2^18-column
+    span (blocks then break on the span); deterministic across executions."""
+    import torch
+
+    P.tuning_set("spmv_sorted_cap", cap)
+    P.tuning_set("spmv_sorted_pipe", pipe)
+    try:
+        rp, col, val = O.gen_band_csr(m, 0, n, k, hb, 37)
+        _plan_check(torch, rp, col, val, n, P.CUDA_CORE, "sorted")
+    finally:
+        P.tuning_set("spmv_sorted_cap", 16384)
+        P.tuning_set("spmv_sorted_pipe", 0)
+
+
+def test_sorted_plan_ragged_and_fallbacks(cuda, sorted_plans):
+    """Empty rows, ragged lengths and a full 64-nonzero row stay sorted; a
+    65-nonzero row, or one row spanning 2^18+ columns, falls back to CSR."""
+    import torch
+
+    rng = np.random.default_rng(12)
+    m, n = 20000, 400000
+    lens = rng.integers(0, 30, m)
+    lens[::7] = 0
+    lens[100] = 64
+
+    def build(lens, spread):
+        rows = []
+        for i, l in enumerate(lens):
+            c0 = min(i * (n // m), n - spread)
+            rows.append(np.sort(rng.choice(spread, l, replace=False)) + c0)
+        rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+        return rp, np.concatenate(rows).astype(np.int32), rng.uniform(-1, 1, rp[-1])
+
+    rp, col, val = build(lens, 5000)
+    _plan_check(torch, rp, col, val, n, P.CUDA_CORE, "sorted")
+    lens2 = lens.copy()
+    lens2[200] = 65
+    rp, col, val = build(lens2, 5000)
+    _plan_check(torch, rp, col, val, n, P.CUDA_CORE, "csr")
+    rp, col, val = build(lens, 300000)  # rows spanning up to 300000 columns
+    span = max(int(col[a:b].max() - col[a:b].min()) for a, b in zip(rp[:-1], rp[1:]) if b > a)
+    _plan_check(torch, rp, col, val, n, P.CUDA_CORE, "csr" if span >= 1 << 18 else "sorted")
 
 
 @pytest.mark.parametrize("m,n,k,hb", [(8192 * 3 + 17, 8192 * 3 + 18, 16, 65536), (100000, 100000, 16, 65536),
