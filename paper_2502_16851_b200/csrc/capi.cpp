@@ -517,14 +517,15 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
         ck(cudaMemcpy(pl->rp, rp, (m + 1) * 4, cudaMemcpyHostToDevice), "plan upload");
         if (pl->sorted) {
             ck(cudaMalloc(&pl->sblk, sb.size() * sizeof(rlb::SpmvSBlock)), "plan alloc");
-            ck(cudaMalloc(&pl->spk, nnz * 4), "plan alloc");
-            ck(cudaMalloc(&pl->ssv, nnz * 8), "plan alloc");
+            const uint64_t ne = spk.size();  // entries incl. 4-alignment padding
+            ck(cudaMalloc(&pl->spk, ne * 4), "plan alloc");
+            ck(cudaMalloc(&pl->ssv, ne * 8), "plan alloc");
             ck(cudaMemcpy(pl->sblk, sb.data(), sb.size() * sizeof(rlb::SpmvSBlock), cudaMemcpyHostToDevice),
                "plan upload");
-            ck(cudaMemcpy(pl->spk, spk.data(), nnz * 4, cudaMemcpyHostToDevice), "plan upload");
-            ck(cudaMemcpy(pl->ssv, ssv.data(), nnz * 8, cudaMemcpyHostToDevice), "plan upload");
+            ck(cudaMemcpy(pl->spk, spk.data(), ne * 4, cudaMemcpyHostToDevice), "plan upload");
+            ck(cudaMemcpy(pl->ssv, ssv.data(), ne * 8, cudaMemcpyHostToDevice), "plan upload");
             for (const auto& b : sb) pl->sblk_r0.push_back(b.r0);
-            pl->layout_bytes = (m + 1) * 4 + nnz * 12 + sb.size() * sizeof(rlb::SpmvSBlock);
+            pl->layout_bytes = (m + 1) * 4 + ne * 12 + sb.size() * sizeof(rlb::SpmvSBlock);
         } else {
             ck(cudaMalloc(&pl->col, std::max<uint64_t>(nnz, 1) * 4), "plan alloc");
             ck(cudaMalloc(&pl->val, std::max<uint64_t>(nnz, 1) * 8), "plan alloc");

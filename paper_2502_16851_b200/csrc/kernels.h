@@ -185,9 +185,10 @@ cudaError_t launch_spmv_tiled(uint64_t m, const uint8_t* segs, const SpmvTile* t
 struct SpmvSBlock {
     uint32_t r0;       // first row
     uint32_t rows;     // rows (<= 1024)
-    uint64_t k0;       // first nonzero (CSR offset; the block's entries are [k0, k0 + nent))
+    uint64_t k0;       // first nonzero (CSR offset)
+    uint64_t kp;       // first entry in the padded sorted arrays (multiple of 32)
     int32_t colbase;   // smallest column of the block
-    int32_t nent;      // nonzeros
+    int32_t nent;      // entries, padded to a multiple of 32 (padding: value 0, slot = cap - 1)
 };
 int spmv_sorted_cap();
 bool spmv_sorted_build(uint64_t m, const int32_t* rp, const int32_t* col, const double* val, int cap,

@@ -52,8 +52,8 @@ __global__ void __launch_bounds__(T) spmv_sorted_kernel(const SpmvSBlock* __rest
             rlo = __ldg(rp + blk.r0 + tid);
             rhi = __ldg(rp + blk.r0 + tid + 1);
         }
-        const uint32_t* p = pk + blk.k0;
-        const double* v = sv + blk.k0;
+        const uint32_t* p = pk + blk.kp;
+        const double* v = sv + blk.kp;
         const double* xb = x + blk.colbase;
         constexpr int U = 8;
         int e = tid;
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(T, 1) spmv_sorted_pipe(const SpmvSBlock* __res
                                                          const int32_t* __restrict__ rp,
                                                          const double* __restrict__ x, double* __restrict__ y) {
     constexpr int EPT = CAP / T;
-    extern __shared__ __align__(16) double prod[];  // 2 x CAP
+    extern __shared__ __align__(16) double prod[];  // 2 x (CAP + 2)
     const int tid = threadIdx.x;
     const uint64_t pol = policy_evict_first(), polx = policy_evict_last();
     SpmvSBlock prev{};
@@ -128,14 +128,14 @@ __global__ void __launch_bounds__(T, 1) spmv_sorted_pipe(const SpmvSBlock* __res
                 a[u] = 0.0;
                 if (e < blk.nent) {
                     asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
-                        : "=r"(q[u]) : "l"(pk + blk.k0 + e), "l"(pol));
+                        : "=r"(q[u]) : "l"(pk + blk.kp + e), "l"(pol));
                     asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
-                        : "=d"(a[u]) : "l"(sv + blk.k0 + e), "l"(pol));
+                        : "=d"(a[u]) : "l"(sv + blk.kp + e), "l"(pol));
                 }
             }
         }
         if (have_prev) {  // phase 2 of the previous block (other buffer)
-            const double* pb = prod + ((it - 1) & 1) * CAP;
+            const double* pb = prod + ((it - 1) & 1) * (CAP + 2);
             if (tid < (int)prev.rows) {
                 const int len = phi - plo;
                 double sacc = 0.0;
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(T, 1) spmv_sorted_pipe(const SpmvSBlock* __res
             }
         }
         if (have) {
-            double* pb = prod + (it & 1) * CAP;
+            double* pb = prod + (it & 1) * (CAP + 2);
             const double* xb = x + blk.colbase;
             double g[EPT];
 #pragma unroll
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(T, 1) spmv_sorted_pipe(const SpmvSBlock* __res
 template <int CAP, int T>
 cudaError_t launch_pipe(const SpmvSBlock* blks, int b0, int b1, const uint32_t* pk, const double* sv,
                         const int32_t* rp, const double* x, double* y, cudaStream_t s) {
-    const size_t smem = (size_t)CAP * 16;
+    const size_t smem = (size_t)(CAP + 2) * 16;
     cudaError_t e = cudaFuncSetAttribute(spmv_sorted_pipe<CAP, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
@@ -179,7 +179,7 @@ cudaError_t launch_pipe(const SpmvSBlock* blks, int b0, int b1, const uint32_t* 
 template <int CAP, int T>
 cudaError_t launch_cfg(const SpmvSBlock* blks, int b0, int b1, const uint32_t* pk, const double* sv,
                        const int32_t* rp, const double* x, double* y, int ctas_per_sm, cudaStream_t s) {
-    const size_t smem = (size_t)CAP * 8;
+    const size_t smem = (size_t)(CAP + 2) * 8;
     cudaError_t e = cudaFuncSetAttribute(spmv_sorted_kernel<CAP, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
@@ -229,16 +229,29 @@ bool spmv_sorted_build(uint64_t m, const int32_t* rp, const int32_t* col, const 
             ++rows;
         }
         if (rows == 0) return false;  // a single row that cannot fit (span >= 2^18)
+        // a block padded to 32 entries needs the dummy slot cap - 1 outside its grid
+        if (((rp[r + rows] - rp[r]) & 31) && rows * (uint64_t)maxlen >= (uint64_t)cap) {
+            if (rows == 1) return false;
+            --rows;
+        }
         b.rows = (uint32_t)rows;
         b.colbase = hi >= lo ? lo : 0;
         b.nent = rp[r + rows] - rp[r];
         blks.push_back(b);
         r += rows;
     }
-    // 2. per-block column sort (parallel over blocks)
-    const uint64_t nnz = (uint64_t)rp[m];
-    pk.assign(nnz, 0);
-    sv.assign(nnz, 0.0);
+    // 2. padded offsets: every block starts on a 32-entry boundary (128-byte
+    //    aligned packed columns, 256-byte aligned values);
+    //    padding entries carry value 0 and the dummy slot cap - 1 (outside every slot grid)
+    uint64_t kp = 0;
+    for (auto& b : blks) {
+        b.kp = kp;
+        b.nent = (b.nent + 31) & ~31;
+        kp += (uint64_t)b.nent;
+    }
+    // 3. per-block column sort (parallel over blocks)
+    pk.assign(kp, (uint32_t)(cap - 1));
+    sv.assign(kp, 0.0);
     const unsigned nth = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 64));
     std::vector<std::thread> pool;
     for (unsigned t = 0; t < nth; ++t)
@@ -259,8 +272,8 @@ bool spmv_sorted_build(uint64_t m, const int32_t* rp, const int32_t* col, const 
                 std::sort(key.begin(), key.end());
                 for (size_t e = 0; e < key.size(); ++e) {
                     const uint64_t c = key[e] >> 46, slot = (key[e] >> 32) & 0x3fff, kk = key[e] & 0xffffffffu;
-                    pk[b.k0 + e] = (uint32_t)((c << 14) | slot);
-                    sv[b.k0 + e] = val[b.k0 + kk];
+                    pk[b.kp + e] = (uint32_t)((c << 14) | slot);
+                    sv[b.kp + e] = val[b.k0 + kk];
                 }
             }
         });

@@ -19,6 +19,7 @@ y0 = torch.empty(n, dtype=torch.float64, device="cuda")
 P.spmv_csr(rp, col, val, x, y0)
 hrp, hcol, hval = rp.cpu(), col.cpu(), val.cpu()
 plans = {}
+P.tuning_set("spmv_plan_sorted", 1)
 if os.environ.get("ONLY"):  # one plan, three executes (for ncu)
     P.tuning_set("spmv_sorted_cap", int(os.environ["ONLY"]))
     pl = P.SpmvPlan(hrp, hcol, hval, n)
