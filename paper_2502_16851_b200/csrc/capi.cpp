@@ -1218,6 +1218,7 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         else if (k == "stencil_tc3d_hybrid") slot = &t.stencil_tc3d_hybrid;
         else if (k == "stencil_tch_ctas_per_sm") slot = &t.stencil_tch_ctas_per_sm;
         else if (k == "stencil_tch_k8") slot = &t.stencil_tch_k8;
+        else if (k == "stencil_tch_stages") slot = &t.stencil_tch_stages;
         else if (k == "stencil3d_balance") slot = &t.stencil3d_balance;
         else if (k == "stencil_tc2d_hybrid") slot = &t.stencil_tc2d_hybrid;
         else if (k == "stencil_tch_tpw") slot = &t.stencil_tch_tpw;

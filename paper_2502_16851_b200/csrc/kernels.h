@@ -58,6 +58,7 @@ struct Tuning {
     int stencil_tch_tpw = 0;           // ... 8x8 tiles per warp: 4 (128-thread CTAs), 2 (256), 1 (512); 0: per preset (3d7pt 2, 3d27pt 4)
     int stencil_tc2d_hybrid = 1;       // 2d5pt tensor core: x-band on DMMA, centre/y on DFMA (st2d_tma_tch, 3 DMMA/tile); 0: 6 DMMA/tile
     int stencil3d_balance = 1;         // 3D TMA kernels with one z-front: rows cut into tiles of <= 16 so the SMs hold equal rows
+    int stencil_tch_stages = 4;        // ... TMA ring depth (4 or 6; 6 measured 7-9 % slower)
     int stencil_tch_k8 = 0;            // ... 1: K = 8 band window (2 DMMA/tile, two x+1 taps by shuffle + DFMA; measured no faster); 0: K = 12, 3 DMMA
     int stencil_r_cc_stages = 0;       // ... CUDA-core ring depth: 2-4, 0 = auto (2 for 2d49pt -> 4 CTAs/SM, else 4)
     int stencil_r_tc_stages = 0;       // TMA ring stages of the radius-R tensor-core kernels (0: 2 at radius 3, else 4)

@@ -1374,13 +1374,14 @@ cudaError_t launch_stencil_tma(int unit, const StencilDesc& d, uint64_t o0, uint
     const int zch = (int)((o1 - o0 + zchunk - 1) / zchunk);
     const unsigned grid = (unsigned)(tiles_xy * zch);
     if (tc_hybrid) {
-        constexpr int S = 4;
-        const size_t sm = ring_bytes<S, kBX>();
-#define RLB_TCH(K, KS, TPW)                                                                                \
+#define RLB_TCHS(K, KS, TPW, S)                                                                            \
     do {                                                                                                   \
+        const size_t sm = ring_bytes<S, kBX>();                                                            \
         if ((e = prep(st3d_tma_tch<K, S, KS, TPW>, sm)) != cudaSuccess) return e;                         \
         st3d_tma_tch<K, S, KS, TPW><<<grid, 512 / TPW, sm, s>>>(m, v, dd, o0, o1, zchunk, tiles_x, tiles_xy); \
     } while (0)
+#define RLB_TCH(K, KS, TPW) \
+    do { if (KS == 3 && tuning().stencil_tch_stages == 6) RLB_TCHS(K, 3, TPW, 6); else RLB_TCHS(K, KS, TPW, 4); } while (0)
 #define RLB_TCH2(K, TPW) \
     do { if (tuning().stencil_tch_k8) RLB_TCH(K, 2, TPW); else RLB_TCH(K, 3, TPW); } while (0)
 #define RLB_TCH3(K) \
@@ -1389,6 +1390,7 @@ cudaError_t launch_stencil_tma(int unit, const StencilDesc& d, uint64_t o0, uint
 #undef RLB_TCH3
 #undef RLB_TCH2
 #undef RLB_TCH
+#undef RLB_TCHS
     } else if (tc_onepl) {
         constexpr int S = 4;
         const size_t sm = ring_bytes<S, kBX>();
