@@ -135,7 +135,7 @@ class Spmv:
     k = 16
     hb = 65536
 
-    def __init__(self, torch, P, D, rank, world):
+    def __init__(self, torch, P, D, rank, world, comm=None, unit=None):
         self.torch, self.P, self.D, self.world = torch, P, D, world
         n_glob = self.n_local * world
         self.part = pt = D.SpmvPartition(n_glob, self.hb, world, rank)
@@ -152,14 +152,24 @@ class Spmv:
         # per-rank: the model on the local row block with its own x slice.
         self.job_bytes = P.spmv_csr_model(n_glob, n_glob, n_glob * self.k).traffic_bytes
         self.bytes = P.spmv_csr_model(m, m, m * self.k).traffic_bytes
+        self.plans = {}
+        self.comm = comm
 
     def step(self, unit):
-        P, pt = self.P, self.part
+        P = self.P
         if self.world == 1:
             P.spmv_csr(self.rp, self.col, self.val, self.x, self.y, unit=unit)
         else:
-            self.D.dist_spmv_step(pt, self.x, lambda lo, hi: P.spmv_csr_rows(
-                lo, hi, self.rp, self.col, self.val, self.x, self.y, col_base=pt.col_base, unit=unit))
+            # rl_dist_spmv: NCCL halo exchange overlapped with the interior rows
+            if unit not in self.plans:
+                self.plans[unit] = self.D.DistSpmv(self.comm, self.n_local * self.world, self.hb,
+                                                   [(self.rp, self.col, self.val, self.x, self.y)], unit=unit)
+            self.plans[unit].execute()
+
+    def close(self):
+        for pl in self.plans.values():
+            pl.close()
+        self.plans = {}
 
     def host_buffers(self):
         t = self.torch
@@ -174,7 +184,15 @@ class Spmv:
     def e2e_step(self, h, unit):
         """The iterative-solver call pattern: A was uploaded once into a plan
         (rl_spmv_plan_create, outside the timed region); each step moves x in
-        and y out through pinned host memory (rl_spmv_plan_execute_host)."""
+        and y out through pinned host memory (rl_spmv_plan_execute_host).
+        N > 1: the owned x goes into the rank's window, rl_dist_spmv_execute,
+        y comes back."""
+        if self.world > 1:
+            self.x[self.part.own_slice()].copy_(h["x"][self.part.own_slice()], non_blocking=True)
+            self.step(unit)
+            h["y"].copy_(self.y, non_blocking=True)
+            self.torch.cuda.current_stream().synchronize()
+            return
         if "plan" not in h:
             h["plan"] = self.P.SpmvPlan(h["rp"], h["col"], h["val"], h["x"].numel(), unit=unit)
         h["plan"].execute_host(h["x"], h["y"])
@@ -184,6 +202,8 @@ class Spmv:
         self.P.spmv_csr_host(h["rp"], h["col"], h["val"], h["x"], h["y"], unit=unit)
 
     def h2d_d2h(self, h):
+        if self.world > 1:
+            return self.part.rows * 8, h["y"].numel() * 8
         return h["x"].numel() * 8, h["y"].numel() * 8
 
     def full_copy_bytes(self, h):
@@ -194,8 +214,8 @@ class Spmv:
 class Stream:
     n = 1 << 27
 
-    def __init__(self, torch, P, D, rank, world):
-        self.torch, self.P = torch, P
+    def __init__(self, torch, P, D, rank, world, comm=None, unit=None):
+        self.torch, self.P, self.D, self.comm, self.world = torch, P, D, comm, world
         lo, hi = D.scale_chunk(self.n * world, world, rank)
         self.b = torch.empty(hi - lo, dtype=torch.float64, device="cuda")
         self.a = torch.empty_like(self.b)
@@ -204,7 +224,13 @@ class Stream:
         self.job_bytes = P.scale_model(self.n * world).traffic_bytes
 
     def step(self, unit):
-        self.P.scale(self.a, self.b, 3.0, unit=unit)
+        if self.world == 1:
+            self.P.scale(self.a, self.b, 3.0, unit=unit)
+        else:
+            self.D.dist_scale(self.comm, self.a, self.b, 3.0, self.n * self.world, unit=unit)
+
+    def close(self):
+        pass
 
     def host_buffers(self):
         t = self.torch
@@ -212,6 +238,12 @@ class Stream:
                 "a": t.empty(self.b.shape, dtype=t.float64, pin_memory=True)}
 
     def e2e_step(self, h, unit):
+        if self.world > 1:
+            self.b.copy_(h["b"], non_blocking=True)
+            self.step(unit)
+            h["a"].copy_(self.a, non_blocking=True)
+            self.torch.cuda.current_stream().synchronize()
+            return
         self.P.scale_host(h["a"], h["b"], 3.0, unit=unit)
 
     def h2d_d2h(self, h):
@@ -222,30 +254,38 @@ class Stencil:
     """One step = one full BASELINE run (100 / 50 double-buffered timesteps).
     At N > 1 the global grid grows along the slab axis (weak scaling)."""
 
-    def __init__(self, torch, P, D, rank, world, preset):
+    def __init__(self, torch, P, D, rank, world, preset, comm=None, unit=None):
         self.torch, self.P, self.D, self.preset, self.world = torch, P, D, preset, world
         base = (16384, 16384) if preset == "2d5pt" else (512, 512, 512)
         self.tsteps = 100 if preset == "2d5pt" else 50
-        gshape = (base[0] * world,) + base[1:]
-        self.part = pt = D.SlabPartition(gshape[0], world, rank, 1)
-        local = (pt.local_outer,) + base[1:]
-        self.u = torch.empty(local, dtype=torch.float64, device="cuda")
+        self.gshape = gshape = (base[0] * world,) + base[1:]
+        self.part = pt = D.SlabPartition(preset, gshape, world, rank)
+        self.u = torch.empty(pt.local_shape, dtype=torch.float64, device="cuda")
         P.stencil_init(self.u, 1, SEED, outer_begin=pt.g_lo, global_shape=gshape)
         self.v = self.u.clone()
         inner = lambda shp: __import__("math").prod(s - 2 for s in shp)
         self.job_bytes = 16 * inner(gshape) * self.tsteps
-        a, b = pt.own_local()
         own_inner = (min(pt.o1, gshape[0] - 1) - max(pt.o0, 1)) * inner((3,) + base[1:])
         self.bytes = 16 * own_inner * self.tsteps
+        self.plans = {}
+        self.comm = comm
 
     def step(self, unit):
         P = self.P
         if self.world == 1:
             P.stencil(self.preset, self.u, self.v, self.tsteps, unit=unit)
         else:
-            self.D.dist_stencil(self.part, self.u, self.v, self.tsteps,
-                                lambda s, d, lo, hi: P.stencil_sweep(self.preset, s, d, lo, hi,
-                                                                     unit=unit))
+            # rl_dist_stencil: per timestep the ghost planes/rows go over NCCL
+            # while the slab interior is swept; timestep pairs replay a CUDA graph
+            if unit not in self.plans:
+                self.plans[unit] = self.D.DistStencil(self.comm, self.preset, self.gshape, [self.u], [self.v],
+                                                      unit=unit)
+            self.plans[unit].run(self.tsteps)
+
+    def close(self):
+        for pl in self.plans.values():
+            pl.close()
+        self.plans = {}
 
     def host_buffers(self):
         t = self.torch
@@ -253,18 +293,25 @@ class Stencil:
                 "v": t.empty(self.u.shape, dtype=t.float64, pin_memory=True).copy_(self.u)}
 
     def e2e_step(self, h, unit):
+        if self.world > 1:
+            self.u.copy_(h["u"], non_blocking=True)
+            self.v.copy_(self.u)
+            self.step(unit)
+            h["v"].copy_(self.u if self.tsteps % 2 == 0 else self.v, non_blocking=True)
+            self.torch.cuda.current_stream().synchronize()
+            return
         self.P.stencil_host(self.preset, h["u"], h["v"], self.tsteps, unit=unit)
 
     def h2d_d2h(self, h):
         return h["u"].numel() * 8, h["u"].numel() * 8
 
 
-def make(name, torch, P, D, rank, world):
+def make(name, torch, P, D, rank, world, comm=None):
     if name == "spmv":
-        return Spmv(torch, P, D, rank, world)
+        return Spmv(torch, P, D, rank, world, comm)
     if name == "stream":
-        return Stream(torch, P, D, rank, world)
-    return Stencil(torch, P, D, rank, world, name)
+        return Stream(torch, P, D, rank, world, comm)
+    return Stencil(torch, P, D, rank, world, name, comm)
 
 
 def time_steps(torch, wl, unit, steps, warmup, world):
@@ -316,6 +363,36 @@ def fp64_peaks(torch, P):
     return out
 
 
+def _tc_pure_keys(name):
+    """Tuning keys that select the paper's full banded tensor-core form (every
+    tap on DMMA) instead of the default x-band hybrid."""
+    return {"2d5pt": {"stencil_tc2d_hybrid": 0}, "3d7pt": {"stencil_tc3d_hybrid": 0},
+            "3d27pt": {"stencil_tc3d_hybrid": 0}}.get(name, {})
+
+
+def _with_keys(P, keys, fn):
+    prev = {k: P.tuning_set(k, v) for k, v in keys.items()}
+    try:
+        return fn()
+    finally:
+        for k, v in prev.items():
+            P.tuning_set(k, v)
+
+
+def _time_e2e(torch, wl, unit, reps):
+    h = wl.host_buffers()
+    bi, bo = wl.h2d_d2h(h)
+    wl.e2e_step(h, unit)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        wl.e2e_step(h, unit)
+    el = time.perf_counter() - t0
+    if "plan" in h:
+        h["plan"].close()
+    return {"value": round(wl.job_bytes * reps / el / 1e9, 1), "unit": "GB/s", "h2d_bytes_per_step": bi,
+            "d2h_bytes_per_step": bo, "steps": reps}
+
+
 def per_kernel_table(torch, P, D, hbm):
     rows = {}
     intensity = {
@@ -328,27 +405,37 @@ def per_kernel_table(torch, P, D, hbm):
     for name, spec in WORKLOADS.items():
         wl = make(name, torch, P, D, 0, 1)
         res = {}
-        for uname, unit in (("cc", P.CUDA_CORE), ("tc", P.TENSOR_CORE)):
+        variants = [("cc", P.CUDA_CORE, {}), ("tc", P.TENSOR_CORE, {})]
+        if _tc_pure_keys(name):
+            variants.append(("tc_pure", P.TENSOR_CORE, _tc_pure_keys(name)))
+        for uname, unit, keys in variants:
             # stencils: 5 runs of the full timestep count, median run (one run is
             # +-5 % noisy on this box; the spread is reported)
             reps = spec["reps"] if name in ("stream", "spmv") else 5
-            total, per = time_steps(torch, wl, unit, reps, 2, 1)
+            total, per = _with_keys(P, keys, lambda: time_steps(torch, wl, unit, reps, 2, 1))
             ms = total / reps if name in ("stream", "spmv") else sorted(per)[len(per) // 2]
-            if name in ("stream", "spmv"):
-                gbs = wl.bytes / (ms * 1e-3) / 1e9
-                unit_ms = ms
-            else:
-                gbs = wl.bytes / (ms * 1e-3) / 1e9
-                unit_ms = ms / wl.tsteps
+            gbs = wl.bytes / (ms * 1e-3) / 1e9
+            unit_ms = ms if name in ("stream", "spmv") else ms / wl.tsteps
             res[uname] = {"gbs": round(gbs, 1), "frac_of_measured_peak": round(gbs / hbm, 4),
                           "ms_per_unit": round(unit_ms, 4)}
             if name not in ("stream", "spmv"):
                 res[uname]["runs"] = reps
                 res[uname]["gbs_min_max"] = [round(wl.bytes / (max(per) * 1e-3) / 1e9, 1),
                                              round(wl.bytes / (min(per) * 1e-3) / 1e9, 1)]
+            if keys:
+                res[uname]["kernel"] = "full banded DMMA form (every tap on the tensor core), tuning " + \
+                    ", ".join(f"{k}={v}" for k, v in keys.items())
         res["tc_over_cc"] = round(res["tc"]["gbs"] / res["cc"]["gbs"], 4)
+        if "tc_pure" in res:
+            res["tc_pure_over_cc"] = round(res["tc_pure"]["gbs"] / res["cc"]["gbs"], 4)
+            res["tc"]["kernel"] = "x-band hybrid (x taps on DMMA, centre/y/z taps on DFMA)"
         res["intensity"] = round(intensity[name], 5)
+        if name != "spmv":
+            # end to end through the host-buffer C-ABI call (rl_scale_host /
+            # rl_stencil_host): H2D of the input and D2H of the result inside
+            res["e2e_cc"] = _time_e2e(torch, wl, P.CUDA_CORE, 3 if name == "stream" else 1)
         rows[name] = res
+        wl.close()
         del wl
         torch.cuda.empty_cache()
     return rows
@@ -543,19 +630,26 @@ def stencil_preset_rows(torch, P, hbm, steps=10):
     return out
 
 
-def add_bounds(P, rows, peaks, hbm):
+def add_bounds(P, rows, peaks_runs, hbm):
     """TC/CC speedup ceiling per kernel from the measured B200 figures
-    (kernel_speedup_ceiling, reference bounds.cpp:72-85)."""
-    alpha = peaks["tensor_core"] / peaks["cuda_core"]
-    balance = peaks["cuda_core"] * 1e12 / (hbm * 1e9)
+    (kernel_speedup_ceiling, reference bounds.cpp:72-85).  K11 runs before and
+    after the kernel table; alpha moves with the power state, so every bound is
+    reported as the range over those runs and `within_bound` uses its top."""
+    alphas = [pk["tensor_core"] / pk["cuda_core"] for pk in peaks_runs]
+    balances = [pk["cuda_core"] * 1e12 / (hbm * 1e9) for pk in peaks_runs]
     for name, res in rows.items():
-        ceil, _ = P.kernel_speedup_ceiling(max(alpha, 1.0), balance, res["intensity"])
-        res["bound"] = round(ceil, 4)
-        res["within_bound"] = bool(res["tc_over_cc"] <= ceil * 1.02)
-    return {"alpha": round(alpha, 4), "balance_flop_per_byte": round(balance, 4),
-                  "tensor_core_ceiling": round(P.tensor_core_ceiling(max(alpha, 1.0)), 4),
-                  "note": "alpha = measured DMMA/DFMA FP64 peak; ceilings from "
-                          "kernel_speedup_ceiling (bounds.cpp:72-85) with alpha clamped to >= 1"}
+        ceils = [P.kernel_speedup_ceiling(max(a, 1.0), bl, res["intensity"])[0] for a, bl in zip(alphas, balances)]
+        res["bound"] = round(max(ceils), 4)
+        res["bound_range"] = [round(min(ceils), 4), round(max(ceils), 4)]
+        res["within_bound"] = bool(res["tc_over_cc"] <= max(ceils) * 1.02)
+        if "tc_pure_over_cc" in res:
+            res["tc_pure_within_bound"] = bool(res["tc_pure_over_cc"] <= max(ceils) * 1.02)
+    return {"alpha": round(alphas[0], 4), "alpha_range": [round(min(alphas), 4), round(max(alphas), 4)],
+            "balance_flop_per_byte": round(balances[0], 4),
+            "balance_range": [round(min(balances), 4), round(max(balances), 4)],
+            "tensor_core_ceiling": round(P.tensor_core_ceiling(max(max(alphas), 1.0)), 4),
+            "note": "alpha = measured DMMA/DFMA FP64 peak (K11 before and after the kernel table); ceilings "
+                    "from kernel_speedup_ceiling (bounds.cpp:72-85) with alpha clamped to >= 1"}
 
 
 def cpu_baseline(name, seconds=10.0):
@@ -579,14 +673,14 @@ def cpu_baseline(name, seconds=10.0):
         fn = lambda: O.scale(b, 3.0)
         sample = "full 2^27-element Scale, repeated"
     else:
-        shape = (4096, 4096) if name == "2d5pt" else (256, 256, 256)
+        shape = (16384, 16384) if name == "2d5pt" else (512, 512, 512)
         u0 = O.stencil_init(shape, 1, SEED)
         inner = 1
         for s in shape:
             inner *= s - 2
         nbytes = 16 * inner
         fn = lambda: O.stencil(name, u0, 1)
-        sample = f"{shape} grid (scaled-down BASELINE grid), 1 timestep per call"
+        sample = f"full BASELINE {shape} grid, 1 timestep per call"
     fn()
     t0 = time.perf_counter()
     calls = 0
@@ -601,11 +695,40 @@ def cpu_baseline(name, seconds=10.0):
             "sample": f"{sample}; {calls} calls in {el:.1f} s"}
 
 
+def workload_bytes(name, world):
+    """Per-GPU algorithmic bytes per step: the reference model of the rank's
+    share (spmv_csr_model / scale_model / stencil_model, kernels.cpp:74-155)."""
+    import math
+
+    import paper_2502_16851_b200 as P
+
+    if name == "spmv":
+        m = Spmv.n_local
+        return P.spmv_csr_model(m, m, m * Spmv.k).traffic_bytes
+    if name == "stream":
+        return P.scale_model(Stream.n).traffic_bytes
+    shape = (16384, 16384) if name == "2d5pt" else (512, 512, 512)
+    return 16 * math.prod(s - 2 for s in shape) * WORKLOADS[name]["reps"]
+
+
+def make_config(args, world):
+    """The `config` object both arms print (identical keys and values)."""
+    return {"workload": WORKLOADS[args.workload]["desc"],
+            "unit": "cuda_core" if args.unit == "cc" else "tensor_core",
+            "parallelism": f"rows/slabs x{world} (NCCL halo exchange)" if world > 1 else "single GPU",
+            "l2": "inputs larger than L2 (no flush needed)",
+            "algorithmic_bytes_per_step_per_gpu": workload_bytes(args.workload, world),
+            "peak_source": hbm_peak()[1]}
+
+
 def run_reference(args, rank, world):
     """--impl reference: the reference path on the host cores (the reference
     has no executing kernel, so its CPU path is the oracle port)."""
     if rank != 0:
         return
+    # all the host threads this process may use (torchrun exports
+    # OMP_NUM_THREADS=1 to every rank; the other ranks do no work here)
+    os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
     import oracle as O
 
     name = args.workload
@@ -633,6 +756,8 @@ def run_reference(args, rank, world):
         nbytes = 16 * inner
         fn = lambda: O.stencil(name, u0, 1)
         sample = f"full {shape} grid, one timestep per step (of {spec['reps']})"
+    if world > 1:
+        sample += f"; one rank's share of the {world}-GPU weak-scaled job, on rank 0's host cores"
     for _ in range(args.warmup):
         fn()
     t0 = time.perf_counter()
@@ -650,7 +775,7 @@ def run_reference(args, rank, world):
         "n_gpus": world, "steps": steps, "warmup": args.warmup,
         "ms_per_step": round(el / steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded splitmix64, BASELINE shapes)",
-        "config": {"workload": spec["desc"], "unit": "cpu"},
+        "config": make_config(args, world),
         "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": thr, "kind": "port",
                          "sample": sample + (f"; stopped after {steps} of {args.steps} steps "
                                              f"({budget:.0f} s budget)" if steps < args.steps else "")},
@@ -658,6 +783,122 @@ def run_reference(args, rank, world):
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def dist_table(torch, P, D, comm, world, hbm, reps=10):
+    """N > 1: every BASELINE config on both units through rl_dist_* (whole-job
+    GB/s = global model bytes / max-over-ranks time)."""
+    out = {}
+    for name in ("stream", "spmv", "2d5pt", "3d7pt", "3d27pt"):
+        wl = make(name, torch, P, D, comm.rank, world, comm)
+        res = {}
+        for uname, unit in (("cc", P.CUDA_CORE), ("tc", P.TENSOR_CORE)):
+            r = reps if name in ("stream", "spmv") else 3
+            total, _ = time_steps(torch, wl, unit, r, 2, world)
+            gbs = wl.job_bytes * r / (total * 1e-3) / 1e9
+            res[uname] = {"gbs": round(gbs, 1), "gbs_per_gpu": round(gbs / world, 1),
+                          "frac_of_measured_peak_per_gpu": round(gbs / world / hbm, 4),
+                          "ms_per_step": round(total / r, 4)}
+        res["tc_over_cc"] = round(res["tc"]["gbs"] / res["cc"]["gbs"], 4)
+        out[name] = res
+        wl.close()
+        del wl
+        torch.cuda.empty_cache()
+    return out
+
+
+def dist_one_gpu(torch, P, D, hbm):
+    """The sharded path on ONE GPU: two parts per rank on a world-1 NCCL
+    communicator, halos through NCCL self send/recv inside the same group a
+    multi-GPU run posts.  Measures what the C++ step adds over the
+    single-launch kernels and its host cost per step (enqueue time of a
+    graph-replayed call, no synchronisation)."""
+    import math
+
+    comm = D.Comm.single()
+    out = {"nccl": comm.info()}
+    # SpMV: BASELINE matrix, 2 parts
+    n, k, hb, L = 1 << 22, 16, 65536, 2
+    tens = []
+    for i in range(L):
+        p = D.SpmvPartition(n, hb, L, i)
+        rp = torch.empty(p.rows + 1, dtype=torch.int32, device="cuda")
+        col = torch.empty(p.rows * k, dtype=torch.int32, device="cuda")
+        val = torch.empty(p.rows * k, dtype=torch.float64, device="cuda")
+        P.gen_band_csr(p.rows, p.r0, n, k, hb, SEED, rp, col, val)
+        x = torch.empty(p.window, dtype=torch.float64, device="cuda")
+        P.fill_uniform(x, SEED, 4, p.col_base, 1)
+        tens.append((rp, col, val, x, torch.empty(p.rows, dtype=torch.float64, device="cuda")))
+    plan = D.DistSpmv(comm, n, hb, tens)
+    reps = 20
+    for _ in range(3):
+        plan.execute()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        plan.execute()
+    host = (time.perf_counter() - t0) / reps
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / reps
+    gbs = P.spmv_csr_model(n, n, n * k).traffic_bytes / (ms * 1e-3) / 1e9
+    out["spmv_2parts"] = {"gbs": round(gbs, 1), "frac_of_measured_peak": round(gbs / hbm, 4),
+                          "ms_per_call": round(ms, 4), "host_us_per_call": round(host * 1e6, 2),
+                          "halo_bytes_per_call": 2 * 2 * hb * 8}
+    plan.close()
+    del tens
+    torch.cuda.empty_cache()
+    # stencils: 2 slabs per GPU, BASELINE grids and timestep counts
+    for preset, shape, steps in (("2d5pt", (16384, 16384), 100), ("3d7pt", (512, 512, 512), 50),
+                                 ("3d27pt", (512, 512, 512), 50)):
+        parts = [D.SlabPartition(preset, shape, L, i) for i in range(L)]
+        us = []
+        for p in parts:
+            u = torch.empty(p.local_shape, dtype=torch.float64, device="cuda")
+            P.stencil_init(u, 1, SEED, outer_begin=p.g_lo, global_shape=shape)
+            us.append(u)
+        vs = [u.clone() for u in us]
+        plan = D.DistStencil(comm, preset, shape, us, vs)
+        plan.run(2)
+        plan.run(steps)
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        t0 = time.perf_counter()
+        kc, _ = plan.run(steps)
+        host = (time.perf_counter() - t0) / steps
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e)
+        gbs = kc.traffic_bytes / (ms * 1e-3) / 1e9
+        layer = math.prod(shape[1:])
+        out[f"{preset}_2parts"] = {"gbs": round(gbs, 1), "frac_of_measured_peak": round(gbs / hbm, 4),
+                                   "ms_per_timestep": round(ms / steps, 4),
+                                   "host_us_per_timestep": round(host * 1e6, 2),
+                                   "halo_bytes_per_timestep": 2 * 2 * layer * 8}
+        plan.close()
+        del us, vs
+        torch.cuda.empty_cache()
+    comm.close()
+    out["note"] = ("rl_dist_* with 2 parts on one GPU (world-1 NCCL, self send/recv); steady-state calls "
+                   "replay a captured CUDA graph, host_us = enqueue time per call / timestep")
+    return out
+
+
+def relaunch(args):
+    """--gpus N without a torchrun environment: re-exec this command under
+    torch.distributed.run with N ranks on 127.0.0.1."""
+    import socket
+
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
 
 
 def main():
@@ -674,8 +915,14 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        relaunch(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU "
+              f"(torchrun --nproc-per-node {args.gpus}) or drop WORLD_SIZE", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -686,17 +933,29 @@ def main():
     import paper_2502_16851_b200 as P
     from paper_2502_16851_b200 import dist as D
 
+    comm = None
     if world > 1:
+        # NCCL's init lines (rank, nranks, transport) go to stderr so the
+        # JSON line stays alone on stdout
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
         dist.init_process_group("nccl")
+        P.lib()
+        comm = D.Comm.from_env()
     else:
         torch.cuda.set_device(0)
     P.lib()
     hbm, hbm_src = hbm_peak()
     unit = P.CUDA_CORE if args.unit == "cc" else P.TENSOR_CORE
 
-    wl = make(args.workload, torch, P, D, rank, world)
+    wl = make(args.workload, torch, P, D, rank, world, comm)
     dev_index = torch.cuda.current_device()
+    peaks_runs = []
+    if world == 1 and not args.no_per_kernel:
+        peaks_runs.append(fp64_peaks(torch, P))   # K11, first of two (alpha range)
+        time.sleep(1.0)
     launches0 = P.kernel_launches()
     with ClockSampler(dev_index) as clk:
         # warm-up inside so the sampler sees the GPU under load before timing
@@ -711,7 +970,7 @@ def main():
     launch_ms = statistics.mean(per)  # one kernel launch per step at N=1
     achieved = bytes_per_step_rank / (launch_ms * 1e-3) / 1e9
 
-    # end to end through the host-buffer C-ABI call
+    # end to end through the public API with host buffers
     h = wl.host_buffers()
     h2d, d2h = wl.h2d_d2h(h)
     wl.e2e_step(h, unit)
@@ -727,16 +986,12 @@ def main():
         e2e_s = float(t.item())
     e2e_val = wl.job_bytes * args.e2e_steps / e2e_s / 1e9
     full_copy = None
-    if hasattr(wl, "full_copy_step"):
+    if hasattr(wl, "full_copy_step") and world == 1:
         wl.full_copy_step(h, unit)
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             wl.full_copy_step(h, unit)
         fc_s = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([fc_s], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            fc_s = float(t.item())
         fi, fo = wl.full_copy_bytes(h)
         full_copy = {"value": round(wl.job_bytes * args.e2e_steps / fc_s / 1e9, 3), "unit": "GB/s",
                      "h2d_bytes_per_step": fi, "d2h_bytes_per_step": fo,
@@ -758,35 +1013,38 @@ def main():
         l2_roof = {"bound": "l2_requests", "requests_per_step": reqs, "achieved": round(rate, 1),
                    "peak": 290.0, "unit": "G requests/s", "frac": round(rate / 290.0, 4),
                    "peak_source": "measured random 8-byte L2 gather rate (tools/micro/dsmem_gather.cu)"}
+    api = {"spmv": ("rl_spmv_plan_execute_host: A resident (uploaded once by rl_spmv_plan_create), "
+                    "x H2D and y D2H from pinned host memory inside every timed call"),
+           }.get(args.workload, "rl_*_host C-ABI (pinned host buffers, copies inside the timed call)")
+    if world > 1:
+        api = ("rl_dist_* plan: the rank's owned input H2D from pinned host memory, the distributed call "
+               "(NCCL halo exchange + kernels), the rank's result D2H; max over ranks")
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded splitmix64 inputs generated in HBM; BASELINE.json shapes)",
-        "config": {"workload": WORKLOADS[args.workload]["desc"],
-                   "unit": "cuda_core" if unit == P.CUDA_CORE else "tensor_core",
-                   "parallelism": f"rows/slabs x{world}" if world > 1 else "single GPU",
-                   "l2": "inputs larger than L2 (no flush needed)",
-                   "algorithmic_bytes_per_step_per_gpu": bytes_per_step_rank,
-                   "peak_source": hbm_src},
+        "config": make_config(args, world),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
                      "frac": round(achieved / hbm, 4), "traffic": traffic,
                      "launch_ms_mean": round(launch_ms, 5),
                      "launch_ms_p50": round(per_sorted[len(per_sorted) // 2], 5)},
         "roofline_l2_requests": l2_roof,
         "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
-                "api": ("rl_spmv_plan_execute_host: A resident (uploaded once by rl_spmv_plan_create), "
-                        "x H2D and y D2H from pinned host memory inside every timed call"
-                        if args.workload == "spmv" else
-                        "rl_*_host C-ABI (pinned host buffers, copies inside the timed call)")},
+                "d2h_bytes_per_step": d2h, "steps": args.e2e_steps, "api": api},
         "e2e_full_copy": full_copy,
         "gpu_launches": timed_launches,
         "clocks": clk.summary(),
     }
+    wl.close()
     del wl
     torch.cuda.empty_cache()
 
+    if world > 1:
+        line["dist"] = {"comm": comm.info(), "per_kernel": dist_table(torch, P, D, comm, world, hbm),
+                        "halo": {"spmv_bytes_per_call_per_inner_rank": 2 * 2 * Spmv.hb * 8,
+                                 "2d_bytes_per_timestep_per_inner_rank": 2 * 2 * 16384 * 8,
+                                 "3d_bytes_per_timestep_per_inner_rank": 2 * 2 * 512 * 512 * 8}}
     if world == 1 and not args.no_per_kernel:
         with ClockSampler(dev_index) as clk2:
             table = per_kernel_table(torch, P, D, hbm)
@@ -796,11 +1054,12 @@ def main():
                                                           table["2d5pt"]["cc"]["ms_per_unit"],
                                                           table["3d7pt"]["cc"]["ms_per_unit"])
             line["next_rows"] = {"gemv": gemv_rows(torch, P, hbm), **stencil_preset_rows(torch, P, hbm)}
-        # FP64 peaks last: the DFMA/DMMA chains run at the power cap and would
-        # throttle the memory-bound kernels measured after them.
-        peaks = fp64_peaks(torch, P)
-        bounds = add_bounds(P, table, peaks, hbm)
-        add_bounds(P, line["next_rows"], peaks, hbm)
+            line["dist_one_gpu"] = dist_one_gpu(torch, P, D, hbm)
+        # K11 again at the end (after the power-capped stretch): alpha range
+        peaks_runs.append(fp64_peaks(torch, P))
+        bounds = add_bounds(P, table, peaks_runs, hbm)
+        add_bounds(P, line["next_rows"], peaks_runs, hbm)
+        peaks = peaks_runs[0]
         balance = peaks["cuda_core"] * 1e12 / (hbm * 1e9)
         for res in line["next_rows"].values():
             # which roof binds the CUDA-core form: HBM below the ridge, the DFMA pipe above
@@ -810,12 +1069,15 @@ def main():
                 res["tc"]["frac_of_fp64_peak"] = round(res["tc"]["tflops"] / peaks["tensor_core"], 4)
         line["per_kernel"] = table
         line["fp64_peaks_tflops"] = peaks
+        line["fp64_peaks_tflops_runs"] = peaks_runs
         line["bounds"] = bounds
         line["per_kernel_clocks"] = clk2.summary()
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.workload)
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -15,7 +15,7 @@
  *     pure host functions.  No allocation happens in the device entry points.
  *   - Return codes: RL_OK (0); 1 + ErrorKind ordinal of the reference
  *     (error.hpp:10-32: MissingPeak=0 ... IoError=16); RL_ERR_CUDA_BASE +
- *     cudaError_t.  rl_last_error() returns a thread-local copy of the
+ *     cudaError_t; RL_ERR_NCCL_BASE + ncclResult_t (rl_dist_* only).  rl_last_error() returns a thread-local copy of the
  *     message, formatted like the reference's exceptions ("<Kind>: <msg>",
  *     error.hpp:38-40).  No exception crosses the boundary.
  *   - Precision is FP64 only in this build (ValidationError otherwise).
@@ -52,18 +52,20 @@ typedef struct {
     uint64_t traffic_bytes;
 } rl_kchar;
 
-/* FP64 slice of HardwareSpec (hardware.hpp:43-58), SI units. */
+/* HardwareSpec (hardware.hpp:43-58), SI units.  The reference's
+ * map<(ExecutionUnit, Precision), peak> is the fixed table peaks[unit][precision]
+ * (rl_unit x rl_precision ordinals); 0 = no entry (MissingPeak on use). */
 typedef struct {
     char name[64];
     double memory_bandwidth; /* bytes/s */
     double l2_cache_bytes;
-    double peak_cuda_core;   /* flops/s, FP64 */
-    double peak_tensor_core; /* flops/s, FP64; 0 = absent */
+    double peaks[2][3];      /* flops/s */
 } rl_hw_spec;
 
 #define RL_OK 0
 #define RL_ERR_KIND_BASE 1
 #define RL_ERR_CUDA_BASE 100
+#define RL_ERR_NCCL_BASE 200
 
 /* ErrorKind ordinals (error.hpp:10-32). */
 enum {
@@ -259,6 +261,14 @@ RL_API int rl_matrix_analysis_of(uint64_t rows, uint64_t cols, uint64_t nnz, con
 /* replaces rooflens::load_spec (hardware.cpp:183-237): same JSON schema
  * (hardware.hpp:75-81), unknown keys -> ParseError, SI conversion. */
 RL_API int rl_load_spec(const char* json_text, rl_hw_spec* out);
+/* replaces rooflens::load_spec_file (hardware.cpp:239-247): IoError when the
+ * file cannot be opened, else load_spec of its contents. */
+RL_API int rl_load_spec_file(const char* path, rl_hw_spec* out);
+/* replaces rooflens::serialize_spec (hardware.cpp:249-264): the same 2-space
+ * JSON document, byte for byte.  Writes at most `capacity` bytes including
+ * the terminating NUL; *length (optional) gets the full length without it
+ * (InvalidRange when it does not fit). */
+RL_API int rl_serialize_spec(const rl_hw_spec* spec, char* buffer, uint64_t capacity, uint64_t* length);
 /* replaces rooflens::builtin_spec (hardware.cpp:121-150): "A100-80GB", "GH200". */
 RL_API int rl_builtin_spec(const char* name, rl_hw_spec* out);
 /* machine_balance (hardware.cpp:112-114) / tensor_alpha (hardware.cpp:116-119). */
@@ -290,6 +300,110 @@ RL_API int rl_tensor_core_ceiling(double alpha, double* out);
 RL_API int rl_workload_ceiling(double intensity, double balance, double* out);
 RL_API int rl_min_temporal_depth(double balance, double single_step_intensity, uint64_t* out);
 RL_API int rl_tc_scale_trick_throughput(double peak_tc, uint64_t m, uint64_t n, double* out);
+
+/* ---------------------------------------------------------------------------
+ * Multi-GPU (north_star): one process per GPU, NCCL
+ * point-to-point over NVLink/NVSwitch, the kernels above as per-part compute.
+ * The reference has no multi-GPU form; these entry points are
+ * the sharded counterparts of rl_scale / rl_spmv_csr / rl_stencil and return
+ * the reference model's W/Q of the WHOLE (global) problem.
+ *
+ * A job is split into P = world * parts_local contiguous parts; process
+ * `rank` owns parts [rank*parts_local, (rank+1)*parts_local).  Production
+ * runs use parts_local = 1 (one part per GPU); parts_local > 1 runs several
+ * parts on one GPU through the same NCCL schedule (self send/recv), which is
+ * how the exchange is tested on a single device.  NCCL is loaded at
+ * rl_dist_init (the copy already in the process, e.g. torch's, else
+ * $RL_NCCL_LIBRARY, else libnccl.so.2); failures return RL_ERR_NCCL_BASE +
+ * ncclResult_t.  Buffers are caller-owned device memory on the communicator's
+ * device; plans keep pointers, streams, events and CUDA graphs.
+ * ------------------------------------------------------------------------- */
+typedef struct rl_dist_s* rl_dist;
+#define RL_DIST_UNIQUE_ID_BYTES 128
+/* ncclGetUniqueId on one process (rank 0); share the bytes out of band. */
+RL_API int rl_dist_unique_id(uint8_t* id /* RL_DIST_UNIQUE_ID_BYTES */);
+/* ncclCommInitRank on the current CUDA device. */
+RL_API int rl_dist_init(int world, int rank, const uint8_t* id, rl_dist* out);
+RL_API int rl_dist_destroy(rl_dist comm);
+RL_API int rl_dist_info(rl_dist comm, int* world, int* rank, int* device, int* nccl_version);
+/* Sum of one uint64 over all ranks (NCCL all-reduce; synchronous). */
+RL_API int rl_dist_allreduce_u64(rl_dist comm, uint64_t* value);
+/* Max of one double over all ranks (NCCL all-reduce; synchronous) -- the
+ * max-over-ranks of a device-timed interval. */
+RL_API int rl_dist_allreduce_max(rl_dist comm, double* value);
+
+/* Partitions (pure host).  Part `part` of `parts`: contiguous block of n,
+ * sizes differing by <= 1, larger blocks first. */
+RL_API int rl_dist_block(uint64_t n, uint64_t parts, uint64_t part, uint64_t* begin, uint64_t* end);
+/* SpMV rows [row_begin, row_end) and x window [col_begin, col_end) =
+ * [max(0, row_begin - hb), min(n, row_end + hb)) of a part of an n x n
+ * matrix with half-bandwidth hb.  ValidationError when a part holds fewer
+ * than hb rows (the halo would span more than the neighbour). */
+RL_API int rl_dist_spmv_part(uint64_t n, uint64_t hb, uint64_t parts, uint64_t part, uint64_t* row_begin,
+                             uint64_t* row_end, uint64_t* col_begin, uint64_t* col_end);
+/* Stencil slab of the outer axis (rows in 2D, planes in 3D; dims global):
+ * owned [own_begin, own_end) and buffer [buf_begin, buf_end) = the owned
+ * layers plus `radius` ghost layers per side where a neighbour exists.  The
+ * part's u and v hold buf_end - buf_begin layers of the global layer size. */
+RL_API int rl_dist_stencil_part(const char* preset, const uint64_t* dims, uint64_t parts, uint64_t part,
+                                uint64_t* own_begin, uint64_t* own_end, uint64_t* buf_begin,
+                                uint64_t* buf_end);
+
+/* One halo transfer of the per-call / per-timestep exchange, in the order a
+ * rank posts it inside one NCCL group: kind 0 = send, 1 = recv; `peer` =
+ * the other rank; `part` = local part index; offset / count in doubles of
+ * that part's x window (SpMV) or field buffer (stencil). */
+typedef struct {
+    int32_t kind;
+    int32_t peer;
+    int32_t part;
+    int32_t reserved;
+    uint64_t offset;
+    uint64_t count;
+} rl_dist_op;
+RL_API int rl_dist_spmv_schedule(uint64_t n, uint64_t hb, int world, int parts_local, int rank,
+                                 rl_dist_op* ops, uint64_t capacity, uint64_t* count);
+RL_API int rl_dist_stencil_schedule(const char* preset, const uint64_t* dims, int world, int parts_local,
+                                    int rank, rl_dist_op* ops, uint64_t capacity, uint64_t* count);
+
+/* STREAM Scale on this rank's chunk rl_dist_block(n_global, world, rank):
+ * a / b hold that chunk.  No communication.  kchar = scale_model(n_global). */
+RL_API int rl_dist_scale(rl_dist comm, rl_unit unit, rl_precision precision, double* a, const double* b,
+                         double q, uint64_t n_global, rl_stream stream, rl_kchar* out);
+
+/* Row-partitioned CSR SpMV of an n x n matrix with half-bandwidth hb.  For
+ * local part i: row_ptr[i] (rows+1, starting at 0), col[i] (GLOBAL columns),
+ * val[i], x[i] = the part's x window (col_end - col_begin doubles; the
+ * caller writes the owned x at offset row_begin - col_begin before each
+ * execute), y[i] (rows).  create checks every column against [0, n) and the
+ * band (ValidationError otherwise), sums nnz over the ranks, and reserves the
+ * plan's streams, events and long-row workspace. */
+typedef struct rl_dist_spmv_s* rl_dist_spmv;
+RL_API int rl_dist_spmv_create(rl_dist comm, rl_unit unit, rl_precision precision, uint64_t n, uint64_t hb,
+                               int parts_local, const int32_t* const* row_ptr, const int32_t* const* col,
+                               const double* const* val, double* const* x, double* const* y,
+                               rl_dist_spmv* out);
+/* One y = A x: the halo exchange (NCCL group on a high-priority stream)
+ * overlaps the interior rows; the edge rows follow.  Ordered after prior work
+ * on `stream`; later work on `stream` sees y.  kchar = spmv_csr_model of the
+ * global matrix.  Replayed as a CUDA graph after the first call. */
+RL_API int rl_dist_spmv_execute(rl_dist_spmv plan, rl_stream stream, rl_kchar* out);
+RL_API int rl_dist_spmv_destroy(rl_dist_spmv plan);
+
+/* Slab-decomposed Jacobi stencil on the global grid `dims`.  u[i] / v[i]:
+ * local part i's buffers (rl_dist_stencil_part layers; the Dirichlet ring
+ * identical in both).  run performs `steps` timesteps starting from u: per
+ * timestep the ghost layers go out on the NCCL stream while the slab interior
+ * is swept, then the edge layers are swept.  Result in u for even steps, in v
+ * for odd (*result_in_v).  Timestep pairs replay as one CUDA graph.  kchar =
+ * stencil_model(preset, FP64, 1) x global interior points x steps. */
+typedef struct rl_dist_stencil_s* rl_dist_stencil;
+RL_API int rl_dist_stencil_create(rl_dist comm, rl_unit unit, rl_precision precision, const char* preset,
+                                  const uint64_t* dims, const double* weights, int parts_local,
+                                  double* const* u, double* const* v, rl_dist_stencil* out);
+RL_API int rl_dist_stencil_run(rl_dist_stencil plan, uint64_t steps, rl_stream stream, int* result_in_v,
+                               rl_kchar* out);
+RL_API int rl_dist_stencil_destroy(rl_dist_stencil plan);
 
 /* ---------------------------------------------------------------------------
  * K11: FP64 peak microbenchmarks (DFMA chains on the fp64 pipe, DMMA chains on

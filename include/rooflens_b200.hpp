@@ -116,17 +116,20 @@ SparseMatrixStats mtx_stats(const std::string& path);
 SparseMatrixStats mtx_read_csr(const std::string& path, std::vector<std::int32_t>& row_ptr,
                                std::vector<std::int32_t>& col, std::vector<double>& val);
 
-// Hardware spec (hardware.hpp:43-89), FP64 slice.
+// Hardware spec (hardware.hpp:43-89).  The reference's map<(unit,
+// precision), peak> is a fixed [unit][precision] table here (0 = absent).
 struct HardwareSpec {
     std::string name;
     double memory_bandwidth = 0.0;  // B/s
     double l2_cache_bytes = 0.0;
-    double peak_cuda_core = 0.0;    // flops/s
-    double peak_tensor_core = 0.0;  // flops/s, 0 = absent
+    double peaks[2][3] = {};        // flops/s by [ExecutionUnit][Precision], 0 = absent
+    bool has_peak(ExecutionUnit u, Precision p) const;
     double peak(ExecutionUnit u, Precision p) const;  // throws MissingPeak
-    void validate() const;
+    void validate() const;  // hardware.cpp:91-110, including the peak table
 };
 HardwareSpec load_spec(const std::string& json_text);
+HardwareSpec load_spec_file(const std::string& path);    // hardware.cpp:239-247
+std::string serialize_spec(const HardwareSpec& spec);    // hardware.cpp:249-264
 const HardwareSpec& builtin_spec(std::string_view name);
 double machine_balance(const HardwareSpec& spec, ExecutionUnit unit, Precision precision);
 double tensor_alpha(const HardwareSpec& spec, Precision precision);

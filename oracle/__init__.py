@@ -57,6 +57,9 @@ _REF_SIGS = {
     "ref_tensor_alpha": (_int, [_dbl, _dbl, _dbl, _DP]),
     "ref_attainable": (_int, [_dbl, _dbl, _dbl, _int, _dbl, _DP]),
     "ref_classify": (_int, [_dbl, _dbl]),
+    "ref_spec_eval": (_int, [C.c_char_p, _int, _int, _int, _dbl, _DP]),
+    "ref_serialize_spec": (_int, [C.c_char_p, C.c_char_p, _u64]),
+    "ref_load_spec_file": (_int, [C.c_char_p, _DP]),
     "ref_mem_cmp_ratio": (_int, [_dbl, _dbl, _DP]),
     "ref_overlapped_total": (_int, [_dbl, _dbl, _dbl, _DP]),
     "ref_sample_curve": (_int, [_dbl, _dbl, _dbl, _int, _dbl, _dbl, _u64, _ptr, _ptr, _u64, _U64P]),

@@ -146,6 +146,32 @@ int ref_attainable(double bw, double p_cc, double p_tc, int unit, double intensi
     });
 }
 
+// Any (unit, precision) on a spec loaded from a JSON document (the full
+// reference peak table): what 0 machine_balance, 1 tensor_alpha, 2 attainable
+// at `intensity`, 3 ridge_point.
+int ref_spec_eval(const char* doc, int what, int unit, int prec, double intensity, double* out) {
+    return guarded([&] {
+        const HardwareSpec s = load_spec(doc);
+        if (what == 0) *out = machine_balance(s, unit_of(unit), prec_of(prec));
+        else if (what == 1) *out = tensor_alpha(s, prec_of(prec));
+        else if (what == 2) *out = attainable(s, unit_of(unit), prec_of(prec), intensity);
+        else *out = ridge_point(s, unit_of(unit), prec_of(prec));
+    });
+}
+
+// serialize_spec(load_spec(doc)) into buf (cap bytes incl. NUL).
+int ref_serialize_spec(const char* doc, char* buf, uint64_t cap) {
+    return guarded([&] {
+        const std::string t = serialize_spec(load_spec(doc));
+        if (t.size() + 1 > cap) throw Error(ErrorKind::InvalidRange, "capacity");
+        std::memcpy(buf, t.c_str(), t.size() + 1);
+    });
+}
+
+int ref_load_spec_file(const char* path, double* bw) {
+    return guarded([&] { *bw = load_spec_file(path).memory_bandwidth; });
+}
+
 int ref_classify(double intensity, double balance) {
     return static_cast<int>(classify(intensity, balance));
 }

@@ -32,7 +32,7 @@ __all__ = [
     "HardwareSpec", "lib", "library_path", "scale_model", "gemv_model", "spmv_generic_model",
     "spmv_csr_model", "stencil_model", "stencil_preset", "stencil_default_weights", "scale",
     "gemv", "spmv_csr", "spmv_csr_rows", "stencil", "stencil_temporal", "stencil_sweep", "scale_host", "spmv_csr_host",
-    "stencil_host", "SpmvPlan", "mtx_stats", "mtx_read_csr", "matrix_analysis", "fill_uniform", "gen_band_csr", "stencil_init", "load_spec", "builtin_spec",
+    "stencil_host", "SpmvPlan", "mtx_stats", "mtx_read_csr", "matrix_analysis", "fill_uniform", "gen_band_csr", "stencil_init", "load_spec", "load_spec_file", "serialize_spec", "builtin_spec",
     "machine_balance", "tensor_alpha", "attainable", "classify", "ridge_point", "sample_curve", "mem_cmp_ratio", "overlapped_total", "unoverlapped_speedup",
     "kernel_speedup_ceiling", "tensor_core_ceiling", "workload_ceiling", "min_temporal_depth",
     "tc_scale_trick_throughput", "fp64_peak_launch", "tuning_set", "kernel_launches",
@@ -75,8 +75,7 @@ class _KChar(C.Structure):
 
 class _HwSpec(C.Structure):
     _fields_ = [("name", C.c_char * 64), ("memory_bandwidth", C.c_double),
-                ("l2_cache_bytes", C.c_double), ("peak_cuda_core", C.c_double),
-                ("peak_tensor_core", C.c_double)]
+                ("l2_cache_bytes", C.c_double), ("peaks", (C.c_double * 3) * 2)]
 
 
 @dataclass(frozen=True)
@@ -93,27 +92,38 @@ class KernelCharacterization:
 
 @dataclass(frozen=True)
 class HardwareSpec:
-    """FP64 slice of ``rooflens::HardwareSpec`` (hardware.hpp:43-58), SI units."""
+    """``rooflens::HardwareSpec`` (hardware.hpp:43-58), SI units.  The FP64
+    peaks are the positional fields; ``fp32`` / ``fp16`` hold (cuda_core,
+    tensor_core) pairs; 0 = no entry (MissingPeak on use)."""
 
     name: str
     memory_bandwidth: float
     l2_cache_bytes: float
     peak_cuda_core: float
     peak_tensor_core: float = 0.0
+    fp32: tuple = (0.0, 0.0)
+    fp16: tuple = (0.0, 0.0)
+
+    def peak_table(self):
+        """[unit][precision] (rl_unit x rl_precision ordinals)."""
+        return ((self.peak_cuda_core, self.fp32[0], self.fp16[0]),
+                (self.peak_tensor_core, self.fp32[1], self.fp16[1]))
 
     def _c(self) -> _HwSpec:
         s = _HwSpec()
         s.name = self.name.encode()[:63]
         s.memory_bandwidth = self.memory_bandwidth
         s.l2_cache_bytes = self.l2_cache_bytes
-        s.peak_cuda_core = self.peak_cuda_core
-        s.peak_tensor_core = self.peak_tensor_core
+        for u, row in enumerate(self.peak_table()):
+            for p, v in enumerate(row):
+                s.peaks[u][p] = v
         return s
 
     @staticmethod
     def _from(s: _HwSpec) -> "HardwareSpec":
-        return HardwareSpec(s.name.decode(), s.memory_bandwidth, s.l2_cache_bytes,
-                            s.peak_cuda_core, s.peak_tensor_core)
+        t = [[s.peaks[u][p] for p in range(3)] for u in range(2)]
+        return HardwareSpec(s.name.decode(), s.memory_bandwidth, s.l2_cache_bytes, t[0][0], t[1][0],
+                            (t[0][1], t[1][1]), (t[0][2], t[1][2]))
 
 
 _u64, _i64, _dbl, _int, _ptr = C.c_uint64, C.c_int64, C.c_double, C.c_int, C.c_void_p
@@ -159,6 +169,8 @@ _SIGNATURES = {
     "rl_matrix_analysis_of": (_int, [_u64, _u64, _u64, _HP, _int, _ptr]),
     "rl_load_spec": (_int, [C.c_char_p, _HP]),
     "rl_builtin_spec": (_int, [C.c_char_p, _HP]),
+    "rl_load_spec_file": (_int, [C.c_char_p, _HP]),
+    "rl_serialize_spec": (_int, [_HP, C.c_char_p, _u64, C.POINTER(_u64)]),
     "rl_machine_balance": (_int, [_HP, _int, _int, C.POINTER(_dbl)]),
     "rl_tensor_alpha": (_int, [_HP, _int, C.POINTER(_dbl)]),
     "rl_attainable": (_int, [_HP, _int, _int, _dbl, C.POINTER(_dbl)]),
@@ -175,6 +187,30 @@ _SIGNATURES = {
     "rl_tc_scale_trick_throughput": (_int, [_dbl, _u64, _u64, C.POINTER(_dbl)]),
     "rl_fp64_peak_launch": (_int, [_int, _u64, _ptr, _ptr, C.POINTER(_dbl)]),
     "rl_tuning_set": (_int, [C.c_char_p, _i64, C.POINTER(_i64)]),
+    # multi-GPU (dist.py wraps these)
+    "rl_dist_unique_id": (_int, [_ptr]),
+    "rl_dist_init": (_int, [_int, _int, _ptr, C.POINTER(_ptr)]),
+    "rl_dist_destroy": (_int, [_ptr]),
+    "rl_dist_info": (_int, [_ptr, C.POINTER(_int), C.POINTER(_int), C.POINTER(_int), C.POINTER(_int)]),
+    "rl_dist_allreduce_u64": (_int, [_ptr, C.POINTER(_u64)]),
+    "rl_dist_allreduce_max": (_int, [_ptr, C.POINTER(_dbl)]),
+    "rl_dist_block": (_int, [_u64, _u64, _u64, C.POINTER(_u64), C.POINTER(_u64)]),
+    "rl_dist_spmv_part": (_int, [_u64, _u64, _u64, _u64, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64),
+                                 C.POINTER(_u64)]),
+    "rl_dist_stencil_part": (_int, [C.c_char_p, C.POINTER(_u64), _u64, _u64, C.POINTER(_u64), C.POINTER(_u64),
+                                    C.POINTER(_u64), C.POINTER(_u64)]),
+    "rl_dist_spmv_schedule": (_int, [_u64, _u64, _int, _int, _int, _ptr, _u64, C.POINTER(_u64)]),
+    "rl_dist_stencil_schedule": (_int, [C.c_char_p, C.POINTER(_u64), _int, _int, _int, _ptr, _u64,
+                                        C.POINTER(_u64)]),
+    "rl_dist_scale": (_int, [_ptr, _int, _int, _ptr, _ptr, _dbl, _u64, _ptr, _KP]),
+    "rl_dist_spmv_create": (_int, [_ptr, _int, _int, _u64, _u64, _int, _ptr, _ptr, _ptr, _ptr, _ptr,
+                                   C.POINTER(_ptr)]),
+    "rl_dist_spmv_execute": (_int, [_ptr, _ptr, _KP]),
+    "rl_dist_spmv_destroy": (_int, [_ptr]),
+    "rl_dist_stencil_create": (_int, [_ptr, _int, _int, C.c_char_p, C.POINTER(_u64), _ptr, _int, _ptr, _ptr,
+                                      C.POINTER(_ptr)]),
+    "rl_dist_stencil_run": (_int, [_ptr, _u64, _ptr, C.POINTER(_int), _KP]),
+    "rl_dist_stencil_destroy": (_int, [_ptr]),
 }
 EXPORTED_SYMBOLS = sorted(_SIGNATURES)
 
@@ -572,6 +608,23 @@ def load_spec(text: str) -> HardwareSpec:
     s = _HwSpec()
     _check(lib().rl_load_spec(text.encode(), C.byref(s)))
     return HardwareSpec._from(s)
+
+
+def load_spec_file(path) -> HardwareSpec:
+    """reference load_spec_file (hardware.cpp:239-247)."""
+    s = _HwSpec()
+    _check(lib().rl_load_spec_file(os.fsencode(path), C.byref(s)))
+    return HardwareSpec._from(s)
+
+
+def serialize_spec(spec: HardwareSpec) -> str:
+    """reference serialize_spec (hardware.cpp:249-264), byte for byte."""
+    s = spec._c()
+    n = _u64()
+    _check(lib().rl_serialize_spec(C.byref(s), None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _check(lib().rl_serialize_spec(C.byref(s), buf, n.value + 1, None))
+    return buf.value.decode()
 
 
 def builtin_spec(name: str) -> HardwareSpec:

@@ -20,6 +20,7 @@
 
 #include "../../include/rooflens_b200.h"
 #include "../../include/rooflens_b200.hpp"
+#include "boundary.h"
 #include "kernels.h"
 
 namespace rlb {
@@ -32,6 +33,10 @@ void note_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed
 }  // namespace rlb
 
 namespace rooflens::b200 {
+std::string& last_error_slot() {
+    static thread_local std::string slot;
+    return slot;
+}
 namespace {
 
 void cuda_check(cudaError_t e, const char* what) {
@@ -145,7 +150,16 @@ void spmv_csr_rows(ExecutionUnit unit, Precision p, std::uint64_t r0, std::uint6
     if (r1 < r0) throw Error(ErrorKind::InvalidRange, "row_end < row_begin");
     if (r1 == r0) return;
     require_ptr(rp, "row_ptr");
+    require_ptr(col, "col");
+    require_ptr(val, "val");
+    require_ptr(x, "x");
     require_ptr(y, "y");
+    // element alignment (the kernels pick vector loads only for 32-byte val /
+    // 16-byte col bases, spmv.cu; an element-misaligned view is rejected)
+    if ((reinterpret_cast<std::uintptr_t>(val) & 7) || (reinterpret_cast<std::uintptr_t>(x) & 7) ||
+        (reinterpret_cast<std::uintptr_t>(y) & 7) || (reinterpret_cast<std::uintptr_t>(col) & 3) ||
+        (reinterpret_cast<std::uintptr_t>(rp) & 3))
+        throw Error(ErrorKind::ValidationError, "spmv_csr: val/x/y must be 8-byte and row_ptr/col 4-byte aligned");
     cuda_check(rlb::launch_spmv(unit == ExecutionUnit::TensorCore, r0, r1, rp, col, val, x, col_base,
                                 y, long_rows, static_cast<cudaStream_t>(stream)),
                "spmv_csr");
@@ -433,6 +447,7 @@ struct rl_spmv_plan_s {
     int long_rows = 0;  // the CSR has rows the per-row kernels divert (spmv.cu)
     std::vector<cudaEvent_t> ev_x, ev_y;
     cudaEvent_t ev_join[2] = {nullptr, nullptr};
+    cudaEvent_t ev_fork = nullptr;  // s_cmp / s_out join s_in at the start of every call (and capture)
     // execute_host as a CUDA graph, captured for the last (x, y) host pair
     cudaGraphExec_t gexec = nullptr;
     const double* gx = nullptr;
@@ -456,6 +471,7 @@ struct rl_spmv_plan_s {
         for (auto e : ev_y) cudaEventDestroy(e);
         for (auto e : ev_join)
             if (e) cudaEventDestroy(e);
+        if (ev_fork) cudaEventDestroy(ev_fork);
         if (s_in) cudaStreamDestroy(s_in);
         if (s_cmp) cudaStreamDestroy(s_cmp);
         if (s_out) cudaStreamDestroy(s_out);
@@ -617,6 +633,7 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
     for (auto& e : pl->ev_x) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     for (auto& e : pl->ev_y) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     for (auto& e : pl->ev_join) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming), "event");
     if (pl->long_rows) {  // reserve the diversion buffers now: execute_host runs under graph capture
         rlb::LongRows lr{};
         ck(rlb::spmv_long_workspace(pl->s_cmp, m, lr), "plan long-row workspace");
@@ -647,6 +664,13 @@ void plan_rows(rl_spmv_plan_s* pl, uint64_t r0, uint64_t r1, const double* x, do
 // records trace events.
 template <class Mark>
 void plan_enqueue(rl_spmv_plan_s* pl, const double* x, double* y, double* y_direct, Mark&& mark) {
+    // Fork: the compute and output streams join s_in before anything else, so
+    // under graph capture every chunk is inside the graph even when a chunk
+    // waits on no x piece (a leading run of empty rows), and eagerly no
+    // chunk of this call overtakes the previous call's y copies.
+    ck(cudaEventRecord(pl->ev_fork, pl->s_in), "event");
+    ck(cudaStreamWaitEvent(pl->s_cmp, pl->ev_fork, 0), "wait");
+    ck(cudaStreamWaitEvent(pl->s_out, pl->ev_fork, 0), "wait");
     mark(pl->s_in);
     const size_t npc = pl->ev_x.size();
     for (size_t i = 0; i < npc; ++i) {
@@ -770,29 +794,6 @@ void plan_execute_host(rl_spmv_plan_s* pl, const double* x, double* y) {
 // ---------------------------------------------------------------------------
 // Error plumbing
 // ---------------------------------------------------------------------------
-thread_local std::string g_last_error;
-
-template <class F>
-int guarded(F&& f) {
-    try {
-        f();
-        g_last_error.clear();
-        return RL_OK;
-    } catch (const Error& e) {
-        g_last_error = e.what();
-        return RL_ERR_KIND_BASE + static_cast<int>(e.kind());
-    } catch (const CudaError& e) {
-        g_last_error = e.what();
-        return RL_ERR_CUDA_BASE + e.code();
-    } catch (const std::bad_alloc&) {
-        g_last_error = "CudaError: host allocation failed";
-        return RL_ERR_CUDA_BASE + 2;
-    } catch (const std::exception& e) {
-        g_last_error = std::string("ValidationError: ") + e.what();
-        return RL_ERR_KIND_BASE + static_cast<int>(ErrorKind::ValidationError);
-    }
-}
-
 void put(rl_kchar* out, const KernelCharacterization& k) {
     if (out) {
         out->work_flops = k.work_flops;
@@ -820,8 +821,7 @@ HardwareSpec spec_of(const rl_hw_spec* s) {
     h.name = std::string(s->name, strnlen(s->name, sizeof s->name));
     h.memory_bandwidth = s->memory_bandwidth;
     h.l2_cache_bytes = s->l2_cache_bytes;
-    h.peak_cuda_core = s->peak_cuda_core;
-    h.peak_tensor_core = s->peak_tensor_core;
+    std::memcpy(h.peaks, s->peaks, sizeof h.peaks);
     return h;
 }
 void spec_out(rl_hw_spec* o, const HardwareSpec& h) {
@@ -830,8 +830,7 @@ void spec_out(rl_hw_spec* o, const HardwareSpec& h) {
     std::strncpy(o->name, h.name.c_str(), sizeof o->name - 1);
     o->memory_bandwidth = h.memory_bandwidth;
     o->l2_cache_bytes = h.l2_cache_bytes;
-    o->peak_cuda_core = h.peak_cuda_core;
-    o->peak_tensor_core = h.peak_tensor_core;
+    std::memcpy(o->peaks, h.peaks, sizeof o->peaks);
 }
 }  // namespace
 
@@ -840,7 +839,7 @@ void spec_out(rl_hw_spec* o, const HardwareSpec& h) {
 // ===========================================================================
 extern "C" {
 
-const char* rl_last_error(void) { return g_last_error.c_str(); }
+const char* rl_last_error(void) { return last_error_slot().c_str(); }
 const char* rl_version(void) { return "rooflens-b200 0.1.0 (sm_100a)"; }
 uint64_t rl_kernel_launches(void) { return rlb::g_launches.load(); }
 
@@ -1075,6 +1074,23 @@ int rl_load_spec(const char* text, rl_hw_spec* out) {
         spec_out(out, load_spec(text));
     });
 }
+int rl_load_spec_file(const char* path, rl_hw_spec* out) {
+    return guarded([&] {
+        require_ptr(path, "path");
+        spec_out(out, load_spec_file(path));
+    });
+}
+int rl_serialize_spec(const rl_hw_spec* s, char* buf, uint64_t cap, uint64_t* length) {
+    return guarded([&] {
+        const std::string text = serialize_spec(spec_of(s));
+        if (length) *length = text.size();
+        if (!buf) return;
+        if (cap < text.size() + 1)
+            throw Error(ErrorKind::InvalidRange, "serialize_spec: buffer of " + std::to_string(cap) +
+                                                     " bytes cannot hold " + std::to_string(text.size() + 1));
+        std::memcpy(buf, text.c_str(), text.size() + 1);
+    });
+}
 int rl_builtin_spec(const char* name, rl_hw_spec* out) {
     return guarded([&] {
         require_ptr(name, "name");
@@ -1162,6 +1178,7 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         int* slot = nullptr;
         const std::string k(key);
         if (k == "scale_blocks_per_sm") slot = &t.scale_blocks_per_sm;
+        else if (k == "dist_graph") slot = &t.dist_graph;
         else if (k == "spmv_rows") slot = &t.spmv_rows;
         else if (k == "gemv_rows") slot = &t.gemv_rows;
         else if (k == "gemv_unroll") slot = &t.gemv_unroll;

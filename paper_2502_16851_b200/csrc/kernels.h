@@ -11,6 +11,7 @@ namespace rlb {
 
 // Kernel-variant knobs, settable through rl_tuning_set() for sweeps.
 struct Tuning {
+    int dist_graph = 1;            // rl_dist_* plans replay captured CUDA graphs after the first call
     int scale_blocks_per_sm = 32;  // STREAM grid = 148 * this (swept: tools/sweep.py)
     int scale_unroll = 8;          // 1, 2, 4, 8
     int gemv_rows = 4;             // rows per warp, CUDA-core GEMV (2, 4, 8)
@@ -106,6 +107,7 @@ struct LongRows {
     int64_t lmax;
     int64_t piece;
     uint64_t pcap;
+    bool vec;        // val 32-byte and col 16-byte aligned: vector loads allowed
 };
 constexpr int kLongIndexShift = 38;
 // long_rows: -1 unknown (divert on the device), 0 known absent (no
@@ -196,6 +198,17 @@ bool spmv_sorted_build(uint64_t m, const int32_t* rp, const int32_t* col, const 
                        std::vector<SpmvSBlock>& blks, std::vector<uint32_t>& pk, std::vector<double>& sv);
 cudaError_t launch_spmv_sorted(const SpmvSBlock* blks, int b0, int b1, const uint32_t* pk, const double* sv,
                                const int32_t* rp, const double* x, double* y, int cap, cudaStream_t s);
+
+// Distributed SpMV plan create-time check (dist_kernels.cu): out[0] = widest
+// |col - row|, out[1] = columns outside [0, n), out[2] = decreasing row_ptr
+// entries (device buffer of 3 u64).
+cudaError_t launch_band_check(uint64_t rows, const int* rp, const int* col, int64_t row0, int64_t n,
+                              unsigned long long* out, cudaStream_t s);
+// Longest-row probe of the CSR kernels' long-row diversion (spmv.cu), for
+// callers that must decide before a stream capture: 1 when [r0, r1) has rows
+// the per-row kernels divert, 0 when not, -1 when the probe failed.
+int spmv_long_rows_probe(const int* rp, const int* col, const double* val, uint64_t r0, uint64_t r1,
+                         cudaStream_t s);
 
 // Launch accounting (rl_kernel_launches): every <<<>>> site reports itself.
 void note_launch(uint64_t n = 1);

@@ -11,6 +11,8 @@
 //   bounds                                 reference bounds.cpp:56-135
 #include <algorithm>
 #include <cmath>
+#include <fstream>
+#include <sstream>
 #include <map>
 #include <numeric>
 
@@ -161,43 +163,56 @@ KernelCharacterization stencil_model(const StencilShape& shape, Precision p, std
 // ---------------------------------------------------------------------------
 // Hardware spec
 // ---------------------------------------------------------------------------
-double HardwareSpec::peak(ExecutionUnit u, Precision p) const {
-    const double v = (p != Precision::FP64) ? 0.0
-                     : (u == ExecutionUnit::CudaCore ? peak_cuda_core : peak_tensor_core);
-    if (!(v > 0.0))
-        throw Error(ErrorKind::MissingPeak, "'" + name + "' has no " +
-                                                (u == ExecutionUnit::CudaCore ? "CudaCore" : "TensorCore") +
-                                                " peak at " +
-                                                (p == Precision::FP64 ? "FP64" : p == Precision::FP32 ? "FP32" : "FP16"));
-    return v;
+namespace {
+const char* const kUnitName[] = {"CudaCore", "TensorCore"};
+const char* const kPrecName[] = {"FP64", "FP32", "FP16"};
+const char* const kPrecKey[] = {"fp64", "fp32", "fp16"};
+}  // namespace
+
+bool HardwareSpec::has_peak(ExecutionUnit u, Precision p) const {
+    return peaks[static_cast<int>(u)][static_cast<int>(p)] != 0.0;
 }
 
-void HardwareSpec::validate() const {
-    if (name.empty()) throw Error(ErrorKind::ValidationError, "spec name is empty");
-    if (!(memory_bandwidth > 0.0))
-        throw Error(ErrorKind::ValidationError, "'" + name + "': memory_bandwidth must be > 0");
-    if (l2_cache_bytes < 0.0)
-        throw Error(ErrorKind::ValidationError, "'" + name + "': l2_cache_bytes must be >= 0");
+double HardwareSpec::peak(ExecutionUnit u, Precision p) const {
+    if (!has_peak(u, p))
+        throw Error(ErrorKind::MissingPeak, "'" + name + "' has no " + kUnitName[static_cast<int>(u)] +
+                                                " peak at " + kPrecName[static_cast<int>(p)]);
+    return peaks[static_cast<int>(u)][static_cast<int>(p)];
 }
 
 namespace {
-// Full (unit, precision) peak table used while validating a document.
-using PeakTable = std::map<std::pair<int, int>, double>;
+// hardware.cpp:91-110 in the reference's order: name, bandwidth, L2, an empty
+// table, then each present entry in (unit, precision) map order.
+void validate_spec(const std::string& name, double bw, double l2, const double (&peaks)[2][3],
+                   const bool (&present)[2][3]) {
+    if (name.empty()) throw Error(ErrorKind::ValidationError, "spec name is empty");
+    if (!(bw > 0.0)) throw Error(ErrorKind::ValidationError, "'" + name + "': memory_bandwidth must be > 0");
+    if (l2 < 0.0) throw Error(ErrorKind::ValidationError, "'" + name + "': l2_cache_bytes must be >= 0");
+    bool any = false;
+    for (int u = 0; u < 2; ++u)
+        for (int p = 0; p < 3; ++p) any = any || present[u][p];
+    if (!any) throw Error(ErrorKind::ValidationError, "'" + name + "': peaks table is empty");
+    for (int u = 0; u < 2; ++u)
+        for (int p = 0; p < 3; ++p) {
+            if (!present[u][p]) continue;
+            if (!(peaks[u][p] > 0.0))
+                throw Error(ErrorKind::ValidationError, "'" + name + "': peak for " + kUnitName[u] + " " +
+                                                            kPrecName[p] + " must be > 0");
+            if (u == 1 && !present[0][p])
+                throw Error(ErrorKind::ValidationError, "'" + name + "': TensorCore peak at " + kPrecName[p] +
+                                                            " has no CudaCore counterpart");
+        }
+}
+}  // namespace
 
-void validate_peaks(const std::string& name, const PeakTable& peaks) {
-    if (peaks.empty()) throw Error(ErrorKind::ValidationError, "'" + name + "': peaks table is empty");
-    static const char* units[] = {"CudaCore", "TensorCore"};
-    static const char* precs[] = {"FP64", "FP32", "FP16"};
-    for (const auto& [key, v] : peaks) {
-        if (!(v > 0.0))
-            throw Error(ErrorKind::ValidationError, "'" + name + "': peak for " + units[key.first] +
-                                                        " " + precs[key.second] + " must be > 0");
-        if (key.first == 1 && !peaks.count({0, key.second}))
-            throw Error(ErrorKind::ValidationError, "'" + name + "': TensorCore peak at " +
-                                                        precs[key.second] + " has no CudaCore counterpart");
-    }
+void HardwareSpec::validate() const {
+    bool present[2][3];
+    for (int u = 0; u < 2; ++u)
+        for (int p = 0; p < 3; ++p) present[u][p] = peaks[u][p] != 0.0;
+    validate_spec(name, memory_bandwidth, l2_cache_bytes, peaks, present);
 }
 
+namespace {
 double number_field(const nlohmann::json& j, const std::string& key) {
     if (!j.is_number()) throw Error(ErrorKind::ParseError, "'" + key + "' must be a number");
     return j.get<double>();
@@ -212,9 +227,8 @@ void only_keys(const nlohmann::json& obj, std::initializer_list<std::string_view
 
 int precision_index(std::string key) {
     std::transform(key.begin(), key.end(), key.begin(), [](unsigned char c) { return std::tolower(c); });
-    if (key == "fp64") return 0;
-    if (key == "fp32") return 1;
-    if (key == "fp16") return 2;
+    for (int p = 0; p < 3; ++p)
+        if (key == kPrecKey[p]) return p;
     return -1;
 }
 }  // namespace
@@ -237,28 +251,64 @@ HardwareSpec load_spec(const std::string& text) {
     s.name = doc["name"].get<std::string>();
     s.memory_bandwidth = number_field(doc["memory_bandwidth_tbps"], "memory_bandwidth_tbps") * kTera;
     s.l2_cache_bytes = number_field(doc["l2_cache_mb"], "l2_cache_mb") * kMega;
-    PeakTable table;
+    bool present[2][3] = {};
     for (auto it = doc["peaks"].begin(); it != doc["peaks"].end(); ++it) {
         const int pi = precision_index(it.key());
         if (pi < 0) throw Error(ErrorKind::ParseError, "unknown precision '" + it.key() + "' in peaks");
         if (!it->is_object()) throw Error(ErrorKind::ParseError, "peaks." + it.key() + " must be a table");
         only_keys(*it, {"cuda_core_tflops", "tensor_core_tflops"}, "peaks." + it.key());
-        if (it->contains("cuda_core_tflops"))
-            table[{0, pi}] = number_field((*it)["cuda_core_tflops"], "peaks." + it.key() + ".cuda_core_tflops") * kTera;
-        if (it->contains("tensor_core_tflops"))
-            table[{1, pi}] = number_field((*it)["tensor_core_tflops"], "peaks." + it.key() + ".tensor_core_tflops") * kTera;
+        static const char* const field[] = {"cuda_core_tflops", "tensor_core_tflops"};
+        for (int u = 0; u < 2; ++u) {
+            if (!it->contains(field[u])) continue;
+            s.peaks[u][pi] = number_field((*it)[field[u]], "peaks." + it.key() + "." + field[u]) * kTera;
+            present[u][pi] = true;
+        }
     }
-    s.validate();
-    validate_peaks(s.name, table);
-    if (table.count({0, 0})) s.peak_cuda_core = table[{0, 0}];
-    if (table.count({1, 0})) s.peak_tensor_core = table[{1, 0}];
+    validate_spec(s.name, s.memory_bandwidth, s.l2_cache_bytes, s.peaks, present);
     return s;
+}
+
+HardwareSpec load_spec_file(const std::string& path) {
+    std::ifstream in(path);
+    if (!in) throw Error(ErrorKind::IoError, "cannot open spec file '" + path + "'");
+    std::ostringstream text;
+    text << in.rdbuf();
+    return load_spec(text.str());
+}
+
+std::string serialize_spec(const HardwareSpec& s) {
+    nlohmann::json peaks = nlohmann::json::object();
+    static const char* const field[] = {"cuda_core_tflops", "tensor_core_tflops"};
+    for (int u = 0; u < 2; ++u)
+        for (int p = 0; p < 3; ++p)
+            if (s.peaks[u][p] != 0.0) peaks[kPrecKey[p]][field[u]] = s.peaks[u][p] / kTera;
+    const nlohmann::json doc = {{"name", s.name},
+                                {"memory_bandwidth_tbps", s.memory_bandwidth / kTera},
+                                {"l2_cache_mb", s.l2_cache_bytes / kMega},
+                                {"peaks", peaks}};
+    return doc.dump(2) + "\n";
 }
 
 const HardwareSpec& builtin_spec(std::string_view name) {
     // Table 1 of the paper, value * unit factor.
-    static const HardwareSpec a100{"A100-80GB", 1.94 * kTera, 40.0 * kMega, 9.7 * kTera, 19.5 * kTera};
-    static const HardwareSpec gh200{"GH200", 4.00 * kTera, 50.0 * kMega, 34.0 * kTera, 67.0 * kTera};
+    static const HardwareSpec a100 = [] {
+        HardwareSpec s;
+        s.name = "A100-80GB";
+        s.memory_bandwidth = 1.94 * kTera;
+        s.l2_cache_bytes = 40.0 * kMega;
+        s.peaks[0][0] = 9.7 * kTera;
+        s.peaks[1][0] = 19.5 * kTera;
+        return s;
+    }();
+    static const HardwareSpec gh200 = [] {
+        HardwareSpec s;
+        s.name = "GH200";
+        s.memory_bandwidth = 4.00 * kTera;
+        s.l2_cache_bytes = 50.0 * kMega;
+        s.peaks[0][0] = 34.0 * kTera;
+        s.peaks[1][0] = 67.0 * kTera;
+        return s;
+    }();
     if (name == a100.name) return a100;
     if (name == gh200.name) return gh200;
     throw Error(ErrorKind::UnknownHardware, "no built-in spec named '" + std::string(name) + "'");

@@ -74,9 +74,9 @@ struct Nz4 {
 // Load the (up to) 4 nonzeros [j, j+4) of a row ending at e.
 __device__ __forceinline__ Nz4 load_nz4(const int* __restrict__ col,
                                         const double* __restrict__ val, int64_t j, int64_t e,
-                                        int col_pad, uint64_t pol) {
+                                        int col_pad, uint64_t pol, bool vec) {
     Nz4 z;
-    if (((j & 3) == 0) && j + 4 <= e) {
+    if (vec && ((j & 3) == 0) && j + 4 <= e) {
         const d4 v = sp_ld4(val + j, pol);
         const int4 ci = sp_ld4_i32(col + j, pol);
         z.v[0] = v.x; z.v[1] = v.y; z.v[2] = v.z; z.v[3] = v.w;
@@ -143,9 +143,9 @@ struct Nz4m {
     bool ok[4];
 };
 __device__ __forceinline__ Nz4m load_nz4_rng(const int* __restrict__ col, const double* __restrict__ val,
-                                             int64_t j, int64_t lo, int64_t hi, uint64_t pol) {
+                                             int64_t j, int64_t lo, int64_t hi, uint64_t pol, bool vec) {
     Nz4m z;
-    if (((j & 3) == 0) && j >= lo && j + 4 <= hi) {
+    if (vec && ((j & 3) == 0) && j >= lo && j + 4 <= hi) {
         const d4 v = sp_ld4(val + j, pol);
         const int4 ci = sp_ld4_i32(col + j, pol);
         z.v[0] = v.x; z.v[1] = v.y; z.v[2] = v.z; z.v[3] = v.w;
@@ -173,7 +173,7 @@ __device__ __forceinline__ void gather4m(double (&xv)[4], const Nz4m& z, const d
 template <int GL = 32>
 __device__ __forceinline__ double group_segment_cc(const int* __restrict__ col, const double* __restrict__ val,
                                                    const double* __restrict__ x, int64_t col_base, int64_t lo,
-                                                   int64_t hi, uint64_t pol, uint64_t polx) {
+                                                   int64_t hi, uint64_t pol, uint64_t polx, bool vec) {
     const int lane = threadIdx.x & 31, gl = lane & (GL - 1);
     const unsigned gmask = GL == 32 ? 0xffffffffu : (((1u << GL) - 1u) << (lane & ~(GL - 1)));
     constexpr int U = 4;  // 4 x 4 GL nonzeros in flight per group step (loads first, then gathers)
@@ -181,7 +181,7 @@ __device__ __forceinline__ double group_segment_cc(const int* __restrict__ col, 
     for (int64_t j0 = (lo & ~int64_t(3)) + 4 * gl; j0 < hi; j0 += 4 * GL * U) {
         Nz4m z[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) z[u] = load_nz4_rng(col, val, j0 + 4 * GL * u, lo, hi, pol);
+        for (int u = 0; u < U; ++u) z[u] = load_nz4_rng(col, val, j0 + 4 * GL * u, lo, hi, pol, vec);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             double xv[4];
@@ -202,7 +202,7 @@ __device__ __forceinline__ double group_segment_cc(const int* __restrict__ col, 
 // virtual row r's sum, valid in lane 4r + r/2 (where D[r][r] lives).
 __device__ __forceinline__ double warp_multi_tc(const int* __restrict__ col, const double* __restrict__ val,
                                                 const double* __restrict__ x, int64_t col_base, int64_t lo,
-                                                int64_t hi, uint64_t pol, uint64_t polx) {
+                                                int64_t hi, uint64_t pol, uint64_t polx, bool vec) {
     const int lane = threadIdx.x & 31, r = lane >> 2, c = lane & 3;
     const int64_t base = lo & ~int64_t(3);
     constexpr int U = 4;  // 4 steps of 16 per virtual row in flight
@@ -210,7 +210,7 @@ __device__ __forceinline__ double warp_multi_tc(const int* __restrict__ col, con
     for (int64_t off0 = 0; __any_sync(0xffffffffu, base + off0 < hi); off0 += 16 * U) {
         Nz4m z[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) z[u] = load_nz4_rng(col, val, base + off0 + 16 * u + 4 * c, lo, hi, pol);
+        for (int u = 0; u < U; ++u) z[u] = load_nz4_rng(col, val, base + off0 + 16 * u + 4 * c, lo, hi, pol, vec);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             double xv[4];
@@ -314,10 +314,10 @@ __global__ void __launch_bounds__(256, 2) spmv_long(const int* __restrict__ rp, 
             double v;
             bool leader;
             if constexpr (TC) {
-                v = warp_multi_tc(col, val, x, col_base, a, bnd, pol, polx);
+                v = warp_multi_tc(col, val, x, col_base, a, bnd, pol, polx, lr.vec);
                 leader = lane == 4 * slot + (slot >> 1);
             } else {
-                v = group_segment_cc<GL>(col, val, x, col_base, a, bnd, pol, polx);
+                v = group_segment_cc<GL>(col, val, x, col_base, a, bnd, pol, polx, lr.vec);
                 leader = gl == 0;
             }
             if (!leader || row < 0) continue;
@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(1024) spmv_cc_v4(uint64_t r0, uint64_t r1,
             skip[u] = DIV && e[u] - s[u] > 16 && divert_long(lr, wbase + 8 * u + q, s[u], e[u], c == 0);
         Nz4 z[R];
 #pragma unroll
-        for (int u = 0; u < R; ++u) z[u] = load_nz4(col, val, s[u] + 4 * c, e[u], col_pad, pol);
+        for (int u = 0; u < R; ++u) z[u] = load_nz4(col, val, s[u] + 4 * c, e[u], col_pad, pol, lr.vec);
         double acc[R];
 #pragma unroll
         for (int u = 0; u < R; ++u) {
@@ -408,7 +408,7 @@ __global__ void __launch_bounds__(1024) spmv_cc_v4(uint64_t r0, uint64_t r1,
 #pragma unroll
         for (int u = 0; u < R; ++u) {
             for (int64_t j = s[u] + 16 + 4 * c; j < e[u]; j += 16) {
-                Nz4 t = load_nz4(col, val, j, e[u], col_pad, pol);
+                Nz4 t = load_nz4(col, val, j, e[u], col_pad, pol, lr.vec);
                 double xv[4];
                 gather4<XH>(xv, t, x, col_base, polx);
 #pragma unroll
@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(1024) spmv_tc(uint64_t r0, uint64_t r1,
         for (int off = 0; off < maxlen; off += 16) {
             Nz4 z[RB];
 #pragma unroll
-            for (int q = 0; q < RB; ++q) z[q] = load_nz4(col, val, s[q] + off + 4 * c, e[q], col_pad, pol);
+            for (int q = 0; q < RB; ++q) z[q] = load_nz4(col, val, s[q] + off + 4 * c, e[q], col_pad, pol, lr.vec);
 #pragma unroll
             for (int q = 0; q < RB; ++q) {
                 double xv[4];
@@ -544,6 +544,11 @@ static int row_profile(const int* rp, const int* col, const double* val, uint64_
     return h > tuning().spmv_long_min ? 1 : 0;
 }
 
+int spmv_long_rows_probe(const int* rp, const int* col, const double* val, uint64_t r0, uint64_t r1,
+                         cudaStream_t s) {
+    return r1 > r0 ? row_profile(rp, col, val, r0, r1, s) : 0;
+}
+
 cudaError_t launch_spmv(int unit, uint64_t r0, uint64_t r1, const int* rp, const int* col,
                         const double* val, const double* x, int64_t col_base, double* y,
                         int long_rows, cudaStream_t s) {
@@ -552,6 +557,9 @@ cudaError_t launch_spmv(int unit, uint64_t r0, uint64_t r1, const int* rp, const
     if (long_rows < 0 && t.spmv_long_rows) long_rows = row_profile(rp, col, val, r0, r1, s);
     // long-row diversion (long_rows: -1 unknown, 0 none, 1 present)
     LongRows lr{};
+    // 256-bit val / 128-bit col loads need 32- / 16-byte aligned base
+    // pointers (a view at an offset may not be): else element loads only
+    lr.vec = (reinterpret_cast<uintptr_t>(val) & 31) == 0 && (reinterpret_cast<uintptr_t>(col) & 15) == 0;
     if (long_rows != 0 && t.spmv_long_rows) {
         cudaError_t e = spmv_long_workspace(s, r1 - r0, lr);
         if (e != cudaSuccess) return e;

@@ -44,6 +44,15 @@ SPEC_DOCS = {
     "negative_peak": '{"name": "x", "memory_bandwidth_tbps": 1, "l2_cache_mb": 1, "peaks": {"fp64": {"cuda_core_tflops": -1}}}',
     "empty_name": '{"name": "", "memory_bandwidth_tbps": 1, "l2_cache_mb": 1, "peaks": {"fp64": {"cuda_core_tflops": 1}}}',
 }
+# full peak tables: every precision, partial units, mixed-case keys
+MULTI_DOCS = {
+    "h100_all": '{"name": "H100-SXM", "memory_bandwidth_tbps": 3.35, "l2_cache_mb": 50, "peaks": {"fp64": {"cuda_core_tflops": 33.5, "tensor_core_tflops": 66.9}, "fp32": {"cuda_core_tflops": 66.9, "tensor_core_tflops": 494.7}, "fp16": {"cuda_core_tflops": 133.8, "tensor_core_tflops": 989.4}}}',
+    "fp32_only": SPEC_DOCS["fp32_only"],
+    "fp16_cc_only": '{"name": "y", "memory_bandwidth_tbps": 2.5, "l2_cache_mb": 0, "peaks": {"Fp16": {"cuda_core_tflops": 7.25}, "fp64": {"cuda_core_tflops": 1.5}}}',
+    "b200_fp32": '{"name": "B200", "memory_bandwidth_tbps": 6.5431, "l2_cache_mb": 126, "peaks": {"fp64": {"cuda_core_tflops": 36.43, "tensor_core_tflops": 37.15}, "fp32": {"cuda_core_tflops": 72.1}}}',
+    "zero_fp16_tc": '{"name": "z", "memory_bandwidth_tbps": 1, "l2_cache_mb": 1, "peaks": {"fp16": {"cuda_core_tflops": 3, "tensor_core_tflops": 0}}}',
+    "tc_without_cc_fp32": '{"name": "z", "memory_bandwidth_tbps": 1, "l2_cache_mb": 1, "peaks": {"fp64": {"cuda_core_tflops": 3}, "fp32": {"tensor_core_tflops": 9}}}',
+}
 
 
 def err(rc):
@@ -127,6 +136,22 @@ def main():
         rc = R.ref_load_spec(doc.encode(), *[C.byref(v) for v in vals])
         res = err(rc) if rc else dict(zip(("bw", "l2", "p_cc", "p_tc"), (v.value for v in vals)))
         cases.append({"fn": "load_spec", "args": [name], "doc": doc, **res})
+    # machine_balance / tensor_alpha / attainable / ridge_point at every (unit,
+    # precision) on full peak tables, and serialize_spec, from the reference
+    for name, doc in MULTI_DOCS.items():
+        for what, fn in enumerate(("machine_balance", "tensor_alpha", "attainable", "ridge_point")):
+            for unit in (0, 1):
+                for prec in (0, 1, 2):
+                    if fn == "tensor_alpha" and unit:
+                        continue
+                    o = C.c_double()
+                    rc = R.ref_spec_eval(doc.encode(), what, unit, prec, 0.75, C.byref(o))
+                    cases.append({"fn": "spec_eval", "args": [name, fn, unit, prec, 0.75], "doc": doc,
+                                  **(err(rc) if rc else {"value": o.value})})
+        buf = C.create_string_buffer(4096)
+        rc = R.ref_serialize_spec(doc.encode(), buf, 4096)
+        cases.append({"fn": "serialize_spec", "args": [name], "doc": doc,
+                      **(err(rc) if rc else {"text": buf.value.decode()})})
     for name in ("A100-80GB", "GH200", "B200"):
         vals = [C.c_double() for _ in range(4)]
         rc = R.ref_builtin_spec(name.encode(), *[C.byref(v) for v in vals])

@@ -69,6 +69,18 @@ def _call(fn, args, doc=None):
             s = P.load_spec(doc)
             return {"bw": s.memory_bandwidth, "l2": s.l2_cache_bytes, "p_cc": s.peak_cuda_core,
                     "p_tc": s.peak_tensor_core}
+        if fn == "spec_eval":
+            s = P.load_spec(doc)
+            _, what, unit, prec, i = args
+            if what == "machine_balance":
+                return {"value": P.machine_balance(s, unit, prec)}
+            if what == "tensor_alpha":
+                return {"value": P.tensor_alpha(s, prec)}
+            if what == "attainable":
+                return {"value": P.attainable(s, i, unit, prec)}
+            return {"value": P.ridge_point(s, unit, prec)}
+        if fn == "serialize_spec":
+            return {"text": P.serialize_spec(P.load_spec(doc))}
         if fn == "builtin_spec":
             s = P.builtin_spec(args[0])
             return {"bw": s.memory_bandwidth, "l2": s.l2_cache_bytes, "p_cc": s.peak_cuda_core,
@@ -230,3 +242,58 @@ def test_mem_cmp_ratio_and_overlapped_total_match_reference():
             with pytest.raises(P.RooflensError) as e:
                 P.overlapped_total(*t)
             assert e.value.code == rc
+
+
+def test_load_spec_file_and_round_trip(tmp_path):
+    """load_spec_file (hardware.cpp:239-247): IoError for a missing file; a
+    serialized spec loads back to the same table (hardware.cpp:249-264)."""
+    with pytest.raises(P.RooflensError) as e:
+        P.load_spec_file(tmp_path / "absent.json")
+    assert e.value.kind == "IoError" and "cannot open spec file" in str(e.value)
+    spec = P.HardwareSpec("B200", 6.5431e12, 126e6, 36.43e12, 37.15e12, fp32=(72.1e12, 0.0))
+    f = tmp_path / "b200.json"
+    f.write_text(P.serialize_spec(spec))
+    assert P.load_spec_file(f) == spec
+    assert P.machine_balance(spec, P.CUDA_CORE, 1) == 72.1e12 / 6.5431e12
+    with pytest.raises(P.RooflensError) as e:
+        P.tensor_alpha(spec, 1)
+    assert e.value.kind == "MissingPeak"
+
+
+@ref_only
+def test_random_peak_tables_match_live_reference():
+    """Every (unit, precision) evaluation and serialize_spec on random peak
+    tables (entries absent, zero, negative or positive) against the reference."""
+    R = O.ref()
+    rng = random.Random(77)
+    for _ in range(400):
+        peaks = {}
+        for pk in ("fp64", "fp32", "fp16"):
+            ent = {}
+            for fld in ("cuda_core_tflops", "tensor_core_tflops"):
+                r = rng.random()
+                if r < 0.45:
+                    continue
+                ent[fld] = 0 if r < 0.5 else (-1.5 if r < 0.53 else round(rng.uniform(0.1, 2000), 3))
+            if ent or rng.random() < 0.2:
+                peaks[rng.choice([pk, pk.upper()])] = ent
+        doc = json.dumps({"name": "r", "memory_bandwidth_tbps": round(rng.uniform(0.5, 9), 4),
+                          "l2_cache_mb": rng.choice([0, 40, 126]), "peaks": peaks})
+        for what in range(4):
+            for unit in (0, 1):
+                for prec in (0, 1, 2):
+                    o = C.c_double()
+                    rc = R.ref_spec_eval(doc.encode(), what, unit, prec, 0.3, C.byref(o))
+                    fns = (lambda s: P.machine_balance(s, unit, prec), lambda s: P.tensor_alpha(s, prec),
+                           lambda s: P.attainable(s, 0.3, unit, prec), lambda s: P.ridge_point(s, unit, prec))
+                    try:
+                        got, grc = fns[what](P.load_spec(doc)), 0
+                    except P.RooflensError as e:
+                        grc, got = e.code, None
+                    assert grc == rc, (doc, what, unit, prec)
+                    if rc == 0:
+                        assert got == o.value, (doc, what, unit, prec)
+        buf = C.create_string_buffer(4096)
+        rc = R.ref_serialize_spec(doc.encode(), buf, 4096)
+        if rc == 0:
+            assert P.serialize_spec(P.load_spec(doc)) == buf.value.decode()

@@ -294,3 +294,29 @@ def test_spmv_profile_cache_stale_is_still_correct(cuda, unit):
         P.spmv_csr(drp, dcol, dval, dx, y, unit=unit)
         torch.cuda.synchronize()
         assert O.rel_err(y.cpu().numpy(), O.spmv_csr(rp, col, val, x)) <= TOL
+
+
+@pytest.mark.parametrize("unit", UNITS)
+@pytest.mark.parametrize("val_off,col_off", [(1, 0), (0, 1), (1, 3), (2, 2), (3, 1)])
+@pytest.mark.parametrize("max_len", [16, 300])   # 300: rows go through the long-row kernel too
+def test_spmv_offset_views(cuda, unit, val_off, col_off, max_len):
+    """val / col as views at an element offset inside larger buffers: the
+    256-bit val and 128-bit col vector loads need 32- / 16-byte aligned bases,
+    so such views must take the element loads (a vector load would raise
+    cudaErrorMisalignedAddress and poison the context)."""
+    import torch
+
+    rng = np.random.default_rng(100 + val_off * 7 + col_off)
+    m, n = 3001, 4000
+    rp, col, val = _ragged(rng, m, n, max_len, empty_frac=0.05)
+    x = rng.uniform(-1, 1, n)
+    nnz = int(rp[-1])
+    vbuf = torch.empty(nnz + 8, dtype=torch.float64, device="cuda")
+    cbuf = torch.empty(nnz + 8, dtype=torch.int32, device="cuda")
+    vbuf[val_off:val_off + nnz] = torch.from_numpy(val).cuda()
+    cbuf[col_off:col_off + nnz] = torch.from_numpy(col).cuda()
+    d_rp, d_x = _to_dev(torch, rp, x)
+    y = torch.full((m,), float("nan"), dtype=torch.float64, device="cuda")
+    P.spmv_csr(d_rp, cbuf[col_off:col_off + nnz], vbuf[val_off:val_off + nnz], d_x, y, unit=unit)
+    torch.cuda.synchronize()
+    assert O.rel_err(y.cpu().numpy(), O.spmv_csr(rp, col, val, x)) <= TOL
