@@ -358,8 +358,11 @@ struct Replay {
         ck(e, "graph instantiate");
         launches = rl_kernel_launches() - before;
     }
-    void replay() {
-        ck(cudaGraphLaunch(exec, s), "graph launch");
+    // The instantiated graph carries its own fork/join between the plan's
+    // stream and the comm stream, so a replay is ONE launch into the caller's
+    // stream: ordered after the caller's prior work, before its later work.
+    void replay(cudaStream_t caller) {
+        ck(cudaGraphLaunch(exec, caller), "graph launch");
         rlb::note_launch(launches);
     }
     void enter(cudaStream_t caller) {
@@ -503,18 +506,14 @@ void spmv_body(rl_dist_spmv_s* pl) {
 void spmv_execute(rl_dist_spmv_s* pl, cudaStream_t caller) {
     require(pl, "plan");
     Replay& r = pl->rp;
-    r.enter(caller);
+    if (!r.exec && r.warmed && graphs_on()) r.capture([&] { spmv_body(pl); });
     if (r.exec) {
-        r.replay();
-    } else {
-        if (r.warmed && graphs_on()) {
-            r.capture([&] { spmv_body(pl); });
-            r.replay();
-        } else {
-            spmv_body(pl);
-        }
-        r.warmed = true;
+        r.replay(caller);
+        return;
     }
+    r.enter(caller);
+    spmv_body(pl);
+    r.warmed = true;
     r.leave(caller);
 }
 
@@ -621,7 +620,6 @@ KernelCharacterization stencil_run(rl_dist_stencil_s* pl, uint64_t steps, cudaSt
     const unsigned __int128 q = (unsigned __int128)pl->per_step.traffic_bytes * steps;
     if ((w >> 64) || (q >> 64)) throw Error(ErrorKind::InvalidRange, "stencil accounting overflows 64-bit count");
     Replay& r = pl->rp;
-    r.enter(caller);
     uint64_t t = 0;
     if (!r.exec && r.warmed && graphs_on() && steps >= 2)
         r.capture([&] {
@@ -629,10 +627,13 @@ KernelCharacterization stencil_run(rl_dist_stencil_s* pl, uint64_t steps, cudaSt
             stencil_step(pl, false);
         });
     if (r.exec)
-        for (; t + 2 <= steps; t += 2) r.replay();
-    for (; t < steps; ++t) stencil_step(pl, (t & 1) == 0);
+        for (; t + 2 <= steps; t += 2) r.replay(caller);
+    if (t < steps) {  // eager: the first call, or the odd last timestep
+        r.enter(caller);
+        for (; t < steps; ++t) stencil_step(pl, (t & 1) == 0);
+        r.leave(caller);
+    }
     r.warmed = true;
-    r.leave(caller);
     if (result_in_v) *result_in_v = (int)(steps & 1);
     return {pl->per_step.kernel_name, (uint64_t)w, (uint64_t)q};
 }

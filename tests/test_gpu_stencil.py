@@ -4,6 +4,8 @@ Bar (BASELINE.json north_star): 1e-12 norm-wise relative error.  The
 Dirichlet ring must be untouched (bit-exact), which also checks that no
 kernel writes outside the interior.
 """
+import functools
+
 import numpy as np
 import pytest
 
@@ -188,37 +190,41 @@ def test_stencil_generator_matches_oracle(cuda):
         assert O.bit_mismatches(u.cpu().numpy(), O.stencil_init(shape, 1, 77)) == 0
 
 
-@pytest.mark.slow
-@pytest.mark.parametrize("unit", UNITS)
-def test_2d5pt_full_grid(cuda, unit):
-    """BASELINE configs[2] grid (16384^2), 2 steps against the oracle."""
-    import torch
-
-    shape = (16384, 16384)
-    u = torch.empty(shape, dtype=torch.float64, device="cuda")
-    P.stencil_init(u, 1, 2025)
-    v = u.clone()
-    P.stencil("2d5pt", u, v, 2, unit=unit)
-    torch.cuda.synchronize()
-    u0 = O.stencil_init(shape, 1, 2025)
-    assert O.rel_err(u.cpu().numpy(), O.stencil("2d5pt", u0, 2)) <= TOL
+@functools.lru_cache(maxsize=3)
+def _full_run_oracle(preset):
+    """The oracle over a whole BASELINE run: 100 timesteps of 16384^2 (2D) or
+    50 of 512^3 (3D) -- a few seconds on the box's cores."""
+    shape, steps = ((16384, 16384), 100) if preset == "2d5pt" else ((512, 512, 512), 50)
+    return shape, steps, O.stencil(preset, O.stencil_init(shape, 1, 2025), steps)
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("preset", ["3d7pt", "3d27pt"])
-@pytest.mark.parametrize("unit", UNITS)
-def test_3d_full_grid(cuda, preset, unit):
-    """BASELINE configs[3]/[4] grid (512^3), 2 steps against the oracle."""
+@pytest.mark.parametrize("preset", ["2d5pt", "3d7pt", "3d27pt"])
+@pytest.mark.parametrize("variant", ["cc", "tc", "tc_pure"])
+def test_full_baseline_run(cuda, preset, variant):
+    """BASELINE configs[2..4] end to end: the full grid AND the full timestep
+    count (100 for 2D, 50 for 3D) against the oracle at 1e-12, ring untouched;
+    tc_pure is the full banded DMMA form (no DFMA taps)."""
     import torch
 
-    shape = (512, 512, 512)
-    u = torch.empty(shape, dtype=torch.float64, device="cuda")
-    P.stencil_init(u, 1, 2025)
-    v = u.clone()
-    P.stencil(preset, u, v, 2, unit=unit)
-    torch.cuda.synchronize()
-    u0 = O.stencil_init(shape, 1, 2025)
-    assert O.rel_err(u.cpu().numpy(), O.stencil(preset, u0, 2)) <= TOL
+    shape, steps, ref = _full_run_oracle(preset)
+    unit = P.CUDA_CORE if variant == "cc" else P.TENSOR_CORE
+    keys = {"stencil_tc2d_hybrid": 0, "stencil_tc3d_hybrid": 0} if variant == "tc_pure" else {}
+    prev = {k: P.tuning_set(k, v) for k, v in keys.items()}
+    try:
+        u = torch.empty(shape, dtype=torch.float64, device="cuda")
+        P.stencil_init(u, 1, 2025)
+        v = u.clone()
+        P.stencil(preset, u, v, steps, unit=unit)
+        torch.cuda.synchronize()
+    finally:
+        for k, val in prev.items():
+            P.tuning_set(k, val)
+    out = (u if steps % 2 == 0 else v).cpu().numpy()
+    del u, v
+    assert O.rel_err(out, ref) <= TOL
+    ring = _ring_mask(shape, 1)
+    assert not out[ring].any()
 
 
 @pytest.mark.parametrize("shape", [(64, 128), (130, 258), (301, 516), (1030, 1026)])
