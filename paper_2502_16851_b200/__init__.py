@@ -519,10 +519,11 @@ class SpmvPlan:
         return t.value == 1, int(b.value)
 
     def layout(self) -> str:
-        """"csr", "tiled" (spmv_tiled.cu) or "sorted" (column-sorted blocks, spmv_sorted.cu)."""
+        """"csr", "tiled" (spmv_tiled.cu), "sorted" (column-sorted blocks, spmv_sorted.cu) or
+        "chunked" (x chunks staged in shared memory, spmv_chunked.cu)."""
         t = _int()
         _check(lib().rl_spmv_plan_info(self._h, C.byref(t), None))
-        return {0: "csr", 1: "tiled", 2: "sorted"}[t.value]
+        return {0: "csr", 1: "tiled", 2: "sorted", 3: "chunked"}[t.value]
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:

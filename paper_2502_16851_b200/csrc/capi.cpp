@@ -427,6 +427,15 @@ struct rl_spmv_plan_s {
     double *val = nullptr, *x = nullptr, *y = nullptr;
     // column-tiled layout (CUDA-core plans): segments, tile table, block table
     bool tiled = false;
+    // column-chunked layout (K16, spmv_chunked.cu)
+    bool chunked = false;
+    int crw = 0;
+    rlb::SpmvCBlock* cblk = nullptr;
+    rlb::SpmvChunk* cchunks = nullptr;
+    unsigned* cwofs = nullptr;
+    double* cval = nullptr;
+    unsigned* cmeta = nullptr;
+    std::vector<uint32_t> cblk_r0;
     // column-sorted block layout (spmv_sorted.cu)
     bool sorted = false;
     int scap = 0;
@@ -461,6 +470,8 @@ struct rl_spmv_plan_s {
         if (x) cudaFree(x);
         if (y) cudaFree(y);
         if (sblk) cudaFree(sblk);
+        for (void* p : {(void*)cblk, (void*)cchunks, (void*)cwofs, (void*)cval, (void*)cmeta})
+            if (p) cudaFree(p);
         if (spk) cudaFree(spk);
         if (ssv) cudaFree(ssv);
         if (segs) cudaFree(segs);
@@ -520,7 +531,29 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
         std::vector<rlb::SpmvSBlock> sb;
         std::vector<uint32_t> spk;
         std::vector<double> ssv;
-        if (unit == ExecutionUnit::CudaCore && rlb::tuning().spmv_plan_sorted && nnz > 0) {
+        // K16 when the staged x windows stay small next to the gathers they
+        // replace (<= 12 staged bytes per nonzero; every gather moves a 32-byte sector)
+        if (unit == ExecutionUnit::CudaCore && rlb::tuning().spmv_plan_chunked && nnz > 0) {
+            rlb::SpmvChunkedLayout L;
+            if (rlb::spmv_chunked_build(m, n, rp, col, val, L) && L.x_bytes <= 12 * nnz) {
+                pl->chunked = true;
+                pl->crw = L.rw;
+                auto up = [&](auto*& dst, const auto& v) {
+                    using T = std::remove_reference_t<decltype(*dst)>;
+                    ck(cudaMalloc(&dst, std::max<size_t>(v.size(), 1) * sizeof(T)), "plan alloc");
+                    if (!v.empty()) ck(cudaMemcpy(dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "plan upload");
+                };
+                up(pl->cblk, L.blocks);
+                up(pl->cchunks, L.chunks);
+                up(pl->cwofs, L.wofs);
+                up(pl->cval, L.val);
+                up(pl->cmeta, L.meta);
+                for (const auto& b : L.blocks) pl->cblk_r0.push_back(b.row0);
+                pl->layout_bytes = L.val.size() * 12 + L.wofs.size() * 4 + L.blocks.size() * sizeof(rlb::SpmvCBlock) +
+                                   L.chunks.size() * sizeof(rlb::SpmvChunk);
+            }
+        }
+        if (!pl->chunked && unit == ExecutionUnit::CudaCore && rlb::tuning().spmv_plan_sorted && nnz > 0) {
             for (uint64_t i = 0; i < m; ++i)
                 for (int32_t k = rp[i]; k < rp[i + 1]; ++k)
                     if (col[k] < 0 || (uint64_t)col[k] >= n)
@@ -531,7 +564,9 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
         }
         ck(cudaMalloc(&pl->rp, (m + 1) * 4), "plan alloc");
         ck(cudaMemcpy(pl->rp, rp, (m + 1) * 4, cudaMemcpyHostToDevice), "plan upload");
-        if (pl->sorted) {
+        if (pl->chunked) {
+            // the layout replaces row_ptr/col/val
+        } else if (pl->sorted) {
             ck(cudaMalloc(&pl->sblk, sb.size() * sizeof(rlb::SpmvSBlock)), "plan alloc");
             const uint64_t ne = spk.size();  // entries incl. 4-alignment padding
             ck(cudaMalloc(&pl->spk, ne * 4), "plan alloc");
@@ -571,6 +606,12 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
         if (c < nch) acc += (taper && (c == 0 || c == nch - 1)) ? 1 : 2;
     }
     pl->chunk_row.back() = m;
+    if (pl->chunked) {  // pipeline chunks = waves of blocks (one block per SM each)
+        const uint64_t nb = pl->cblk_r0.size(), wv = std::max<uint64_t>(1, nb / rlb::kNumSMsHost);
+        pl->chunk_row.clear();
+        for (uint64_t c = 0; c <= wv; ++c) pl->chunk_row.push_back(c == wv ? m : pl->cblk_r0[nb * c / wv]);
+        nch = pl->chunk_row.size() - 1;
+    }
     if (pl->sorted) {  // chunk boundaries on block starts
         for (size_t c = 1; c + 1 < pl->chunk_row.size(); ++c) {
             auto it = std::lower_bound(pl->sblk_r0.begin(), pl->sblk_r0.end(), (uint32_t)pl->chunk_row[c]);
@@ -643,6 +684,14 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
 
 // Rows [r0, r1) of y = A x on the plan's layout (r0/r1 block-aligned when tiled).
 void plan_rows(rl_spmv_plan_s* pl, uint64_t r0, uint64_t r1, const double* x, double* y, cudaStream_t s) {
+    if (pl->chunked) {  // r0 / r1 on block starts
+        const auto& v = pl->cblk_r0;
+        const int b0 = (int)(std::lower_bound(v.begin(), v.end(), (uint32_t)r0) - v.begin());
+        const int b1 = r1 >= pl->m ? (int)v.size() : (int)(std::lower_bound(v.begin(), v.end(), (uint32_t)r1) - v.begin());
+        ck(rlb::launch_spmv_chunked(pl->cblk + b0, b1 - b0, pl->cchunks, pl->cwofs, pl->cval, pl->cmeta, x, y, pl->crw, s),
+           "spmv (chunked plan)");
+        return;
+    }
     if (pl->sorted) {
         const auto& v = pl->sblk_r0;
         const int b0 = (int)(std::lower_bound(v.begin(), v.end(), (uint32_t)r0) - v.begin());
@@ -961,8 +1010,8 @@ int rl_spmv_plan_execute(rl_spmv_plan pl, const double* x, double* y, rl_stream 
         require_ptr(pl, "plan");
         require_ptr(x, "x");
         require_ptr(y, "y");
-        if (pl->tiled && (reinterpret_cast<uintptr_t>(x) & 15))
-            throw Error(ErrorKind::ValidationError, "tiled plan needs a 16-byte aligned x");
+        if ((pl->tiled || pl->chunked) && (reinterpret_cast<uintptr_t>(x) & 15))
+            throw Error(ErrorKind::ValidationError, "this plan's layout stages x with bulk copies: x must be 16-byte aligned");
         plan_rows(pl, 0, pl->m, x, y, static_cast<cudaStream_t>(s));
         put(out, pl->kc);
     });
@@ -970,7 +1019,7 @@ int rl_spmv_plan_execute(rl_spmv_plan pl, const double* x, double* y, rl_stream 
 int rl_spmv_plan_info(rl_spmv_plan pl, int* tiled, uint64_t* layout_bytes) {
     return guarded([&] {
         require_ptr(pl, "plan");
-        if (tiled) *tiled = pl->tiled ? 1 : (pl->sorted ? 2 : 0);
+        if (tiled) *tiled = pl->tiled ? 1 : (pl->sorted ? 2 : (pl->chunked ? 3 : 0));
         if (layout_bytes) *layout_bytes = pl->layout_bytes;
     });
 }
@@ -1196,6 +1245,7 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         else if (k == "spmv_plan_taper") slot = &t.spmv_plan_taper;
         else if (k == "spmv_plan_xpieces") slot = &t.spmv_plan_xpieces;
         else if (k == "spmv_plan_sorted") slot = &t.spmv_plan_sorted;
+        else if (k == "spmv_plan_chunked") slot = &t.spmv_plan_chunked;
         else if (k == "spmv_sorted_cap") slot = &t.spmv_sorted_cap;
         else if (k == "spmv_sorted_pipe") slot = &t.spmv_sorted_pipe;
         else if (k == "spmv_plan_ygroups") slot = &t.spmv_plan_ygroups;

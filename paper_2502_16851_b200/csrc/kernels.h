@@ -28,6 +28,7 @@ struct Tuning {
     int spmv_long_piece = 512;     // ... cut into pieces of this many nonzeros, balanced over the warps
     int spmv_long_group = 8;       // lanes per piece of the CUDA-core long-row kernel (8, 16, 32)
     int spmv_plan_chunks = 16;     // pipelined row/x chunks of rl_spmv_plan_execute_host
+    int spmv_plan_chunked = 1;     // 1: CUDA-core plans use the column-chunked layout (K16, spmv_chunked.cu) when the staged x stays <= 12 B per nonzero
     int spmv_plan_sorted = 0;      // 1: CUDA-core plans use the column-sorted block layout when eligible (spmv_sorted.cu; halves the L2 requests but measured 0.287 vs 0.274 ms: latency-bound)
     int spmv_sorted_cap = 16384;   // ... slot grid per block (16384: 1024 threads, 1 CTA/SM; 8192: 512 threads, 3 CTAs/SM)
     int spmv_sorted_pipe = 0;      // ... cap 12288: software-pipelined kernel (two product buffers, 1 CTA/SM)
@@ -209,6 +210,36 @@ cudaError_t launch_band_check(uint64_t rows, const int* rp, const int* col, int6
 // the per-row kernels divert, 0 when not, -1 when the probe failed.
 int spmv_long_rows_probe(const int* rp, const int* col, const double* val, uint64_t r0, uint64_t r1,
                          cudaStream_t s);
+
+// K16: column-chunked layout (spmv_chunked.cu): x windows staged in shared
+// memory per row block; the default CUDA-core plan layout for banded/local
+// matrices (staged x bytes <= 12 per nonzero).
+constexpr int kNumSMsHost = 148;     // B200 SM count (host-side copy of common.cuh's kNumSMs)
+constexpr int kSpmvChunk = 4096;      // x columns per staged chunk (32 KB)
+constexpr int kSpmvChunkStages = 3;   // ring depth
+struct SpmvCBlock {
+    uint32_t row0, rows;  // rows [row0, row0 + rows)
+    int rw;               // rows per warp (block rows = 32 rw)
+    int c0, c1;           // chunk records [c0, c1)
+};
+struct SpmvChunk {
+    int32_t col0;   // first column (even)
+    int32_t ncols;  // staged columns (even)
+};
+struct SpmvChunkedLayout {
+    int rw = 0;
+    std::vector<SpmvCBlock> blocks;
+    std::vector<SpmvChunk> chunks;
+    std::vector<unsigned> wofs;   // (chunk, warp) segment starts, + 1 end
+    std::vector<double> val;      // entries
+    std::vector<unsigned> meta;   // row-in-warp << 16 | column-in-chunk (0xFFFF: padding)
+    uint64_t x_bytes = 0;         // x bytes staged per call
+};
+bool spmv_chunked_build(uint64_t m, uint64_t n, const int32_t* rp, const int32_t* col, const double* val,
+                        SpmvChunkedLayout& layout);
+cudaError_t launch_spmv_chunked(const SpmvCBlock* blks, int nblk, const SpmvChunk* chunks, const unsigned* wofs,
+                                const double* val2, const unsigned* meta2, const double* x, double* y, int rw,
+                                cudaStream_t s);
 
 // Launch accounting (rl_kernel_launches): every <<<>>> site reports itself.
 void note_launch(uint64_t n = 1);

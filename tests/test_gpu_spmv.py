@@ -320,3 +320,71 @@ def test_spmv_offset_views(cuda, unit, val_off, col_off, max_len):
     P.spmv_csr(d_rp, cbuf[col_off:col_off + nnz], vbuf[val_off:val_off + nnz], d_x, y, unit=unit)
     torch.cuda.synchronize()
     assert O.rel_err(y.cpu().numpy(), O.spmv_csr(rp, col, val, x)) <= TOL
+
+
+@pytest.mark.parametrize("case", ["band", "ragged", "empty_block", "long_rows", "narrow"])
+def test_spmv_plan_chunked_layout(cuda, case):
+    """K16 (spmv_chunked.cu): x windows staged in shared memory per row block.
+    Banded / local matrices take it; the result matches the oracle through
+    both rl_spmv_plan_execute (device x, y) and execute_host, on repeated
+    calls with new x."""
+    import torch
+
+    rng = np.random.default_rng({"band": 1, "ragged": 2, "empty_block": 3, "long_rows": 4, "narrow": 5}[case])
+    if case == "band":
+        m = n = 300_000
+        rp, col, val = O.gen_band_csr(m, 0, n, 16, 20000, 9)
+    elif case == "narrow":
+        m = n = 70_001 + 1   # even n
+        rp, col, val = O.gen_band_csr(m, 0, n, 5, 3, 4)
+    else:
+        m = n = 200_000
+        hbw = 6000
+        lens = rng.integers(0, 40, size=m)
+        if case == "empty_block":
+            lens[50_000:90_000] = 0
+        if case == "long_rows":
+            lens[rng.choice(m, 20, replace=False)] = 3000
+        rp = np.zeros(m + 1, np.int64)
+        rp[1:] = np.cumsum(lens)
+        cols = []
+        for i, l in enumerate(lens):
+            lo, hi = max(0, i - hbw), min(n, i + hbw + 1)
+            cols.append(np.sort(rng.choice(np.arange(lo, hi), size=min(l, hi - lo), replace=False)))
+        lens = np.array([c.size for c in cols])
+        rp[1:] = np.cumsum(lens)
+        col = np.concatenate(cols).astype(np.int32)
+        rp = rp.astype(np.int32)
+        val = rng.uniform(-1, 1, size=col.size)
+    plan = P.SpmvPlan(rp, col, val, n)
+    try:
+        assert plan.layout() == "chunked"
+        for call in range(3):
+            x = O.fill_uniform(n, 40 + call, 4, 0, 1)
+            ref = O.spmv_csr(rp, col, val, x)
+            dx = torch.from_numpy(x).cuda()
+            dy = torch.full((m,), float("nan"), dtype=torch.float64, device="cuda")
+            plan.execute(dx, dy)
+            torch.cuda.synchronize()
+            assert O.rel_err(dy.cpu().numpy(), ref) <= TOL, call
+            hx = torch.from_numpy(x).pin_memory()
+            hy = torch.full((m,), float("nan"), dtype=torch.float64).pin_memory()
+            plan.execute_host(hx, hy)
+            assert O.rel_err(hy.numpy(), ref) <= TOL, call
+    finally:
+        plan.close()
+
+
+def test_spmv_plan_chunked_declined_for_scattered_columns(cuda):
+    """A matrix whose rows reach across all of x would stage far more x than
+    it gathers: the plan keeps the CSR kernels."""
+    rng = np.random.default_rng(8)
+    m = n = 100_000
+    lens = np.full(m, 8)
+    rp = np.zeros(m + 1, np.int32)
+    rp[1:] = np.cumsum(lens)
+    col = np.concatenate([np.sort(rng.choice(n, 8, replace=False)) for _ in range(m)]).astype(np.int32)
+    val = rng.uniform(-1, 1, col.size)
+    plan = P.SpmvPlan(rp, col, val, n)
+    assert plan.layout() != "chunked"
+    plan.close()
