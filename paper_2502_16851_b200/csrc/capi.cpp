@@ -1246,6 +1246,7 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         else if (k == "spmv_plan_xpieces") slot = &t.spmv_plan_xpieces;
         else if (k == "spmv_plan_sorted") slot = &t.spmv_plan_sorted;
         else if (k == "spmv_plan_chunked") slot = &t.spmv_plan_chunked;
+        else if (k == "spmv_chunked_mode") slot = &t.spmv_chunked_mode;
         else if (k == "spmv_sorted_cap") slot = &t.spmv_sorted_cap;
         else if (k == "spmv_sorted_pipe") slot = &t.spmv_sorted_pipe;
         else if (k == "spmv_plan_ygroups") slot = &t.spmv_plan_ygroups;

@@ -11,27 +11,29 @@
 //
 // Layout (built once on the host by spmv_chunked_build, like DASP's
 // conversion or cusparseSpMV_preprocess; bytes <= the CSR's):
-//   * rows are cut into blocks of R rows (a multiple of 32; the block count
-//     is a multiple of the SM count so the persistent grid has no tail);
-//     warp w of a block owns rows [w RW, (w+1) RW), RW = R / 32 <= 256;
-//   * a block's x window [min col, max col] is cut into chunks of kChunk
+//   * rows are cut into blocks of R rows (the block count is a multiple of
+//     the SM count, so the persistent grid has no tail); warp w of a block
+//     owns rows [w RW, (w+1) RW), RW = R / 16 <= 512;
+//   * a block's x window [min col, max col] is cut into chunks of kSpmvChunk
 //     columns; chunks with no entry in the block are dropped;
-//   * per (chunk, warp), the warp's entries whose column falls in the chunk,
-//     row-major (row, then column), padded to a multiple of 4:
-//     val2 (f64) and meta2 (u32 = row-in-warp << 16 | column-in-chunk;
-//     column 0xFFFF marks padding), and wofs[(chunk) * 32 + w] the start of
-//     that segment (monotone, u32).
-// Kernel: one persistent CTA of 32 warps per SM; thread 0 streams the x
+//   * per (chunk, warp): the warp's entries whose column falls in the chunk,
+//     ordered so that every aligned group of 32 entries holds 32 DIFFERENT
+//     rows (rows' 1st entries, then 2nd entries, ..., with a greedy fix-up and,
+//     when a group cannot be completed, padding entries that point at a
+//     per-warp dummy row): val2 (f64), meta2 (u32 = row-in-warp << 16 |
+//     column-in-chunk), wofs[chunk * 16 + w] = the segment start (segments
+//     start 4-entry aligned; the alignment gap is dummy-row entries too).
+// Kernel: one persistent CTA of 16 warps per SM; thread 0 streams the x
 // chunks of the CTA's blocks through an S-stage ring (mbarrier full/empty,
 // one arrive per warp), so the next block's chunks load while the current
-// block finishes.  A warp walks its segment 128 entries per step: one 256-bit
-// val and one 128-bit meta load per lane (HBM, evict_first), 4 shared-memory
-// x gathers, then a row-run reduction -- runs inside the lane, a segmented
-// shuffle scan across lanes for runs that span lanes -- and one
-// read-modify-write of the warp's private y rows in shared memory per run.
-// After the block's last chunk the warp stores its y rows (coalesced).
-// The sums per row follow the entries' column order within each chunk and
-// chunk order across chunks: deterministic, independent of timing.
+// block finishes.  A warp walks its segments in batches of 4 groups (one
+// entry per lane per group, coalesced loads), the loads running two batches
+// ahead across chunk boundaries; per group each lane does one shared-memory
+// x gather and one read-modify-write of its row's y in the warp's private y
+// rows -- the 32 rows of a group are distinct, so a group's updates never
+// collide and no reduction is needed.  After the block's last chunk the warp
+// stores its y rows (coalesced).  Each row's sum follows a fixed entry order:
+// deterministic, independent of timing.
 #include <algorithm>
 #include <thread>
 #include <vector>
@@ -45,32 +47,21 @@ namespace {
 
 using namespace tmaop;
 
-constexpr int kWarps = 32;
-constexpr unsigned kPadCol = 0xFFFFu;
-
-__device__ __forceinline__ int4 ld4_i32_stream(const unsigned* p, uint64_t pol) {
-    int4 v;
-    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
-        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-        : "l"(p), "l"(pol));
-    return v;
-}
+constexpr int kWarps = kSpmvChunkWarps;
 
 template <int S>
-__global__ void __launch_bounds__(1024, 1) spmv_chunked_kernel(const SpmvCBlock* __restrict__ blks, int nblk,
-                                                               const SpmvChunk* __restrict__ chunks,
-                                                               const unsigned* __restrict__ wofs,
-                                                               const double* __restrict__ val2,
-                                                               const unsigned* __restrict__ meta2,
-                                                               const double* __restrict__ x, double* __restrict__ y,
-                                                               int rw_max) {
+__global__ void __launch_bounds__(32 * kSpmvChunkWarps, 1) spmv_chunked_kernel(
+    const SpmvCBlock* __restrict__ blks, int nblk, const SpmvChunk* __restrict__ chunks,
+    const unsigned* __restrict__ wofs, const double* __restrict__ val2, const unsigned* __restrict__ meta2,
+    const double* __restrict__ x, double* __restrict__ y, int rw_max, int mode) {
     extern __shared__ __align__(128) double smem[];
-    double* xs = smem;                               // S stages of kChunk doubles
-    double* ys = smem + S * kSpmvChunk;              // 32 warps x rw_max rows
-    uint64_t* full = reinterpret_cast<uint64_t*>(ys + kWarps * rw_max);
+    const int ystride = rw_max + 1;                  // + the warp's dummy row (padding entries)
+    double* xs = smem;                               // S stages of kSpmvChunk doubles
+    double* ys = smem + S * kSpmvChunk;              // kWarps x ystride rows
+    uint64_t* full = reinterpret_cast<uint64_t*>(ys + kWarps * ystride);
     uint64_t* empty = full + S;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    double* yw = ys + w * rw_max;
+    double* yw = ys + w * ystride;
     const uint64_t pol = policy_evict_first(), polx = policy_evict_last();
 
     if (tid == 0) {
@@ -80,10 +71,10 @@ __global__ void __launch_bounds__(1024, 1) spmv_chunked_kernel(const SpmvCBlock*
         }
         mbar_fence_init();
     }
-    for (int i = lane; i < rw_max; i += 32) yw[i] = 0.0;
+    for (int i = lane; i < ystride; i += 32) yw[i] = 0.0;
     __syncthreads();
 
-    // producer state (thread 0): next (block, chunk) to load, k = its ring index
+    // producer state (thread 0): next (block, chunk) to load, pk = its ring index
     int pb = blockIdx.x, pc = pb < nblk ? blks[pb].c0 : 0, pk = 0;
     auto produce = [&](int upto) {  // issue ring items pk .. upto-1
         while (pk < upto && pb < nblk) {
@@ -102,91 +93,174 @@ __global__ void __launch_bounds__(1024, 1) spmv_chunked_kernel(const SpmvCBlock*
             ++pk;
         }
     };
-    if (tid == 0) produce(S);
+    if (tid == 0 && mode != 3 && mode != 5) produce(S);
 
-    int k = 0;  // ring index of the chunk being consumed
+    // A batch = 4 groups of 32 entries (entry j + 32 q + lane).  The loads of a
+    // warp's batches run two batches ahead of the one being applied, across
+    // chunk boundaries (they do not depend on the x stage).  Segment bounds of
+    // 32 chunks at a time sit in the lanes (lane l: chunk g0 + l).
+    struct Batch {
+        bool ok;
+        int ci;         // chunk within the group of 32
+        unsigned j, e;  // first entry, end of the segment
+        double v[4];
+        unsigned m[4];
+    };
+    int k = 0;     // ring index of the chunk being consumed
+    int turn = 0;  // which of the four batches is next
     for (int b = blockIdx.x; b < nblk; b += gridDim.x) {
         const SpmvCBlock blk = blks[b];
-        for (int c = blk.c0; c < blk.c1; ++c, ++k) {
-            mbar_wait(full + (k % S), (uint32_t)((k / S) & 1));
-            const double* xc = xs + (k % S) * kSpmvChunk;
-            const unsigned s0 = __ldg(wofs + (size_t)c * kWarps + w), s1 = __ldg(wofs + (size_t)c * kWarps + w + 1);
-            for (unsigned j0 = s0; j0 < s1; j0 += 128) {
-                const unsigned j = j0 + 4 * lane;
-                const bool act = j < s1;
-                double p[4];
-                int r[4];
-                if (act) {
-                    const d4 v = ld4_stream(val2 + j, pol);
-                    const int4 m = ld4_i32_stream(meta2 + j, pol);
-                    const unsigned mm[4] = {(unsigned)m.x, (unsigned)m.y, (unsigned)m.z, (unsigned)m.w};
-                    const double vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        r[q] = (int)(mm[q] >> 16);
-                        const unsigned cc = mm[q] & 0xFFFFu;
-                        p[q] = cc == kPadCol ? 0.0 : vv[q] * xc[cc];
+        for (int g0 = blk.c0; g0 < blk.c1; g0 += 32) {
+            const int gn = min(32, blk.c1 - g0);
+            const unsigned so = lane < gn ? __ldg(wofs + (size_t)(g0 + lane) * kWarps + w) : 0u;
+            const unsigned eo = lane < gn ? __ldg(wofs + (size_t)(g0 + lane) * kWarps + w + 1) : 0u;
+            int lc = 0;  // load cursor
+            unsigned lj = __shfl_sync(0xffffffffu, so, 0), le = __shfl_sync(0xffffffffu, eo, 0);
+            auto next = [&](Batch& bt) {
+                while (lc < gn && lj >= le) {
+                    ++lc;
+                    lj = __shfl_sync(0xffffffffu, so, lc & 31);
+                    le = __shfl_sync(0xffffffffu, eo, lc & 31);
+                }
+                bt.ok = lc < gn;
+                bt.ci = lc;
+                bt.j = lj;
+                bt.e = le;
+                if (mode == 4 || mode == 5) {  // diagnostic: 4 consecutive entries per lane (256 / 128-bit loads)
+                    const unsigned jj = lj + 4 * lane;
+                    if (bt.ok && jj < le) {
+                        const d4 v = ld4_stream(val2 + jj, pol);
+                        int4 mv;
+                        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+                            : "=r"(mv.x), "=r"(mv.y), "=r"(mv.z), "=r"(mv.w) : "l"(meta2 + jj), "l"(pol));
+                        bt.v[0] = v.x; bt.v[1] = v.y; bt.v[2] = v.z; bt.v[3] = v.w;
+                        bt.m[0] = mv.x; bt.m[1] = mv.y; bt.m[2] = mv.z; bt.m[3] = mv.w;
                     }
-                } else {
+                    lj += 128;
+                    return;
+                }
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        r[q] = -1 - lane;  // distinct from every real row and from each other lane
-                        p[q] = 0.0;
+                for (int q = 0; q < 4; ++q) {
+                    const unsigned jj = lj + 32 * q + lane;
+                    if (bt.ok && jj < le && mode != 2) {
+                        bt.v[q] = ld_stream(val2 + jj, pol);
+                        bt.m[q] = (unsigned)ld_stream_i32(reinterpret_cast<const int*>(meta2) + jj, pol);
                     }
                 }
-                // runs inside the lane: s[q] = sum of the run up to entry q
-                double s[4];
-                s[0] = p[0];
+                lj += 128;
+            };
+            // Four batches in flight per warp, rotated without register copies
+            // (a copy of a batch whose loads are still in flight would wait for
+            // them): the batch just applied is reloaded in place, four ahead.
+            Batch A, B, C, D;
+            turn = 0;
+            next(A);
+            next(B);
+            next(C);
+            next(D);
+            auto apply = [&](const Batch& bt, const double* xc) {
+                if (mode != 0) {  // diagnostic modes: data movement only
+                    if (bt.v[0] == 12345.678) yw[0] += xc[0];
+                    return;
+                }
 #pragma unroll
-                for (int q = 1; q < 4; ++q) s[q] = r[q] == r[q - 1] ? s[q - 1] + p[q] : p[q];
-                const int h = r[0], t = r[3];
-                // segmented inclusive scan of the tail runs across lanes: lane l's
-                // tail chain continues lane l-1's when the whole lane is one row
-                // equal to lane l-1's tail row
-                const int t_prev = __shfl_up_sync(0xffffffffu, t, 1);
-                double T = s[3];
-                int F = (lane == 0 || h != t || h != t_prev) ? 1 : 0;
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const double Tu = __shfl_up_sync(0xffffffffu, T, d);
-                    const int Fu = __shfl_up_sync(0xffffffffu, F, d);
-                    if (lane >= d && !F) {
-                        T += Tu;
-                        F |= Fu;
+                for (int q = 0; q < 4; ++q) {
+                    if (bt.j + 32 * q + lane < bt.e) {
+                        const unsigned mm = bt.m[q];
+                        double* yr = yw + (mm >> 16);
+                        *yr = fma(bt.v[q], xc[mm & 0xFFFFu], *yr);
                     }
                 }
-                const double T_prev = __shfl_up_sync(0xffffffffu, T, 1);
-                const int h_next = __shfl_down_sync(0xffffffffu, h, 1);
-                const double cin = (lane > 0 && h == t_prev) ? T_prev : 0.0;
-                if (act) {
-                    // runs that end inside the lane (entries 0..2)
-#pragma unroll
-                    for (int q = 0; q < 3; ++q) {
-                        if (r[q] != r[q + 1]) {
-                            const double add = s[q] + (r[q] == h ? cin : 0.0);
-                            yw[r[q]] += add;
-                        }
+            };
+            for (int ci = 0; ci < gn; ++ci, ++k) {
+                if (mode != 3 && mode != 5) mbar_wait(full + (k % S), (uint32_t)((k / S) & 1));
+                const double* xc = xs + (k % S) * kSpmvChunk;
+                for (;;) {
+                    const bool more = turn == 0   ? (A.ok && A.ci == ci)
+                                      : turn == 1 ? (B.ok && B.ci == ci)
+                                      : turn == 2 ? (C.ok && C.ci == ci)
+                                                  : (D.ok && D.ci == ci);
+                    if (!more) break;
+                    if (turn == 0) {
+                        apply(A, xc);
+                        next(A);
+                    } else if (turn == 1) {
+                        apply(B, xc);
+                        next(B);
+                    } else if (turn == 2) {
+                        apply(C, xc);
+                        next(C);
+                    } else {
+                        apply(D, xc);
+                        next(D);
                     }
-                    // the tail run, written by the last lane of its chain
-                    if (lane == 31 || h_next != t) yw[t] += T;
+                    turn = (turn + 1) & 3;
                 }
-                __syncwarp();  // the next step's lanes read what this step's lanes wrote
+                // release the stage (one arrive per warp); thread 0 refills it
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty + (k % S));
+                if (tid == 0 && mode != 3 && mode != 5) produce(k + 1 + S);
             }
-            // release the stage (one arrive per warp); thread 0 refills it
-            __syncwarp();
-            if (lane == 0) mbar_arrive(empty + (k % S));
-            if (tid == 0) produce(k + 1 + S);
         }
         // the block's y rows: coalesced store, then clear for the next block
         __syncwarp();
         const int rw = min(blk.rw, max(0, (int)blk.rows - w * blk.rw));
         double* yo = y + (uint64_t)blk.row0 + (uint64_t)w * blk.rw;
-        for (int i = lane; i < rw; i += 32) {
-            yo[i] = yw[i];
-            yw[i] = 0.0;
-        }
-        for (int i = rw + lane; i < blk.rw; i += 32) yw[i] = 0.0;
+        for (int i = lane; i < rw; i += 32) yo[i] = yw[i];
         __syncwarp();
+        for (int i = lane; i < ystride; i += 32) yw[i] = 0.0;
+        __syncwarp();
+    }
+}
+
+// One entry of the layout under construction.
+struct Ent {
+    uint32_t row;
+    uint32_t col;
+    double val;
+};
+
+// Order one (chunk, warp) segment so that every aligned group of 32 entries
+// has 32 different rows.  `ent` holds (row, col, val) sorted by (row, col).
+// Rows' k-th entries come in rounds k = 0, 1, ...; a greedy pass fills each
+// group with the earliest pending entries whose rows the group lacks, and a
+// group that cannot be completed while entries remain is padded with dummy
+// entries (row = dummy, value 0).
+void order_segment(const std::vector<Ent>& ent, uint32_t dummy, std::vector<Ent>& out, std::vector<uint32_t>& mark,
+                   uint32_t& stamp) {
+    out.clear();
+    if (ent.empty()) return;
+    std::vector<Ent> pending, rest;
+    pending.reserve(ent.size());
+    std::vector<uint32_t> start;  // index of each row's first entry
+    for (size_t i = 0; i < ent.size(); ++i)
+        if (i == 0 || ent[i].row != ent[i - 1].row) start.push_back((uint32_t)i);
+    start.push_back((uint32_t)ent.size());
+    for (size_t kk = 0;; ++kk) {
+        bool any = false;
+        for (size_t r = 0; r + 1 < start.size(); ++r)
+            if (start[r] + kk < start[r + 1]) {
+                pending.push_back(ent[start[r] + kk]);
+                any = true;
+            }
+        if (!any) break;
+    }
+    while (!pending.empty()) {
+        ++stamp;
+        size_t taken = 0;
+        rest.clear();
+        for (const Ent& e : pending) {
+            if (taken < 32 && mark[e.row] != stamp) {
+                mark[e.row] = stamp;
+                out.push_back(e);
+                ++taken;
+            } else {
+                rest.push_back(e);
+            }
+        }
+        if (taken < 32 && !rest.empty())
+            for (; taken < 32; ++taken) out.push_back(Ent{dummy, 0u, 0.0});
+        pending.swap(rest);
     }
 }
 
@@ -195,24 +269,31 @@ __global__ void __launch_bounds__(1024, 1) spmv_chunked_kernel(const SpmvCBlock*
 bool spmv_chunked_build(uint64_t m, uint64_t n, const int32_t* rp, const int32_t* col, const double* val,
                         SpmvChunkedLayout& L) {
     if (m == 0 || n == 0 || (n & 1) || n >= (1ull << 31)) return false;
-    const uint64_t nnz = (uint64_t)rp[m];
-    // blocks: a multiple of the SM count, R <= 8192 rows, R % 32 == 0
-    uint64_t waves = (m + (uint64_t)kNumSMs * 8192 - 1) / ((uint64_t)kNumSMs * 8192);
+    // blocks: a multiple of the SM count, R <= 8192 rows, R % kWarps == 0
+    const uint64_t waves = (m + (uint64_t)kNumSMs * 8192 - 1) / ((uint64_t)kNumSMs * 8192);
     uint64_t nblk = (uint64_t)kNumSMs * waves;
     uint64_t R = (m + nblk - 1) / nblk;
-    R = (R + 31) / 32 * 32;
-    if (R < 32) R = 32;
+    R = (R + kWarps - 1) / kWarps * kWarps;
+    if (R < (uint64_t)kWarps) R = kWarps;
     nblk = (m + R - 1) / R;
-    const int rw = (int)(R / 32);
+    const int rw = (int)(R / kWarps);
     L.rw = rw;
     L.blocks.assign(nblk, SpmvCBlock{});
     std::vector<std::vector<SpmvChunk>> bchunks(nblk);
-    std::vector<std::vector<unsigned>> bcount(nblk);  // per block: per (chunk, warp) padded counts
+    std::vector<std::vector<std::vector<Ent>>> bseg(nblk);  // per block: per (chunk, warp) ordered entries
     const unsigned hw = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
     std::vector<char> bad(hw, 0);
-    auto pass1 = [&](unsigned tix) {
+    auto build_block = [&](unsigned tix) {
+        std::vector<uint32_t> mark(rw + 1, 0);
+        uint32_t stamp = 0;
+        std::vector<Ent> ordered;
+        std::vector<std::pair<int32_t, double>> rowbuf;
         for (uint64_t b = tix; b < nblk; b += hw) {
             const uint64_t r0 = b * R, r1 = std::min(m, r0 + R);
+            SpmvCBlock& B = L.blocks[b];
+            B.row0 = (uint32_t)r0;
+            B.rows = (uint32_t)(r1 - r0);
+            B.rw = rw;
             int64_t cmin = INT64_MAX, cmax = -1;
             for (uint64_t i = r0; i < r1; ++i)
                 for (int64_t e = rp[i]; e < rp[i + 1]; ++e) {
@@ -224,111 +305,91 @@ bool spmv_chunked_build(uint64_t m, uint64_t n, const int32_t* rp, const int32_t
                     cmin = std::min(cmin, c);
                     cmax = std::max(cmax, c);
                 }
-            SpmvCBlock& B = L.blocks[b];
-            B.row0 = (uint32_t)r0;
-            B.rows = (uint32_t)(r1 - r0);
-            B.rw = rw;
-            if (cmax < 0) continue;  // no entries: y rows are zero (written by the kernel)
+            if (cmax < 0) continue;  // no entries: the kernel writes zero rows
             const int64_t base = cmin & ~int64_t(1);
             const int64_t nch = (cmax - base) / kSpmvChunk + 1;
-            std::vector<unsigned> cnt((size_t)nch * kWarps, 0);
+            // bucket the block's entries by (chunk, warp): rows ascending, columns sorted
+            std::vector<std::vector<Ent>> bucket((size_t)nch * kWarps);
             for (uint64_t i = r0; i < r1; ++i) {
                 const int wi = (int)((i - r0) / rw);
-                for (int64_t e = rp[i]; e < rp[i + 1]; ++e) ++cnt[(size_t)((col[e] - base) / kSpmvChunk) * kWarps + wi];
+                const uint32_t rr = (uint32_t)((i - r0) % rw);
+                rowbuf.clear();
+                for (int64_t e = rp[i]; e < rp[i + 1]; ++e) rowbuf.emplace_back(col[e], val[e]);
+                std::stable_sort(rowbuf.begin(), rowbuf.end(),
+                                 [](const auto& a, const auto& b2) { return a.first < b2.first; });
+                for (const auto& [c, v] : rowbuf) {
+                    const int64_t ch = (c - base) / kSpmvChunk;
+                    bucket[(size_t)ch * kWarps + wi].push_back(Ent{rr, (uint32_t)(c - (base + ch * kSpmvChunk)), v});
+                }
             }
             for (int64_t ch = 0; ch < nch; ++ch) {
-                unsigned tot = 0;
-                for (int wi = 0; wi < kWarps; ++wi) tot += cnt[(size_t)ch * kWarps + wi];
+                size_t tot = 0;
+                for (int wi = 0; wi < kWarps; ++wi) tot += bucket[(size_t)ch * kWarps + wi].size();
                 if (!tot) continue;
                 SpmvChunk C;
                 C.col0 = (int32_t)(base + ch * kSpmvChunk);
-                C.ncols = (int32_t)std::min<int64_t>(kSpmvChunk, (int64_t)n - C.col0);
+                // only the columns the block reads (its window ends at cmax)
+                C.ncols = (int32_t)std::min<int64_t>(kSpmvChunk, cmax + 1 - C.col0);
                 C.ncols = (C.ncols + 1) & ~1;  // n is even: stays inside x
                 bchunks[b].push_back(C);
-                for (int wi = 0; wi < kWarps; ++wi) bcount[b].push_back((cnt[(size_t)ch * kWarps + wi] + 3u) & ~3u);
+                for (int wi = 0; wi < kWarps; ++wi) {
+                    order_segment(bucket[(size_t)ch * kWarps + wi], (uint32_t)rw, ordered, mark, stamp);
+                    bseg[b].push_back(ordered);
+                }
             }
         }
     };
     {
         std::vector<std::thread> th;
-        for (unsigned t = 0; t < hw; ++t) th.emplace_back(pass1, t);
+        for (unsigned t = 0; t < hw; ++t) th.emplace_back(build_block, t);
         for (auto& t : th) t.join();
     }
     if (std::any_of(bad.begin(), bad.end(), [](char c) { return c != 0; })) return false;
-    // global chunk table and segment offsets
     uint64_t nchunks = 0, E = 0;
-    std::vector<uint64_t> bofs(nblk + 1, 0);  // first entry of each block
+    std::vector<uint64_t> bofs(nblk + 1, 0);
     for (uint64_t b = 0; b < nblk; ++b) {
         L.blocks[b].c0 = (int)nchunks;
         nchunks += bchunks[b].size();
         L.blocks[b].c1 = (int)nchunks;
         bofs[b] = E;
-        for (unsigned c : bcount[b]) E += c;
+        for (const auto& sg : bseg[b]) E += (sg.size() + 3) & ~size_t(3);  // segments start 32-byte aligned
     }
-    bofs[nblk] = E;
     if (E >= (1ull << 32) || nchunks >= (1ull << 31)) return false;
     L.chunks.resize(nchunks);
     L.wofs.assign(nchunks * kWarps + 1, 0);
     L.val.assign(E, 0.0);
-    L.meta.assign(E, 0u);
-    for (uint64_t b = 0; b < nblk; ++b) {
-        std::copy(bchunks[b].begin(), bchunks[b].end(), L.chunks.begin() + L.blocks[b].c0);
-        uint64_t o = bofs[b];
-        for (size_t q = 0; q < bcount[b].size(); ++q) {
-            L.wofs[(size_t)L.blocks[b].c0 * kWarps + q] = (unsigned)o;
-            o += bcount[b][q];
-        }
-    }
-    L.wofs[nchunks * kWarps] = (unsigned)E;
-    auto pass2 = [&](unsigned tix) {
-        std::vector<unsigned> fill;
+    L.meta.assign(E, (uint32_t)rw << 16);  // alignment gaps: dummy-row entries, value 0
+    auto place = [&](unsigned tix) {
         for (uint64_t b = tix; b < nblk; b += hw) {
-            const SpmvCBlock& B = L.blocks[b];
-            const int nc = B.c1 - B.c0;
-            if (!nc) continue;
-            const uint64_t r0 = B.row0, r1 = r0 + B.rows;
-            fill.assign((size_t)nc * kWarps, 0);
-            // rows in order, and each row's entries in column order (sorted
-            // here if the CSR row is not), keep every segment row-major
-            std::vector<std::pair<int32_t, double>> rowbuf;
-            for (uint64_t i = r0; i < r1; ++i) {
-                const int wi = (int)((i - r0) / B.rw);
-                const unsigned rr = (unsigned)((i - r0) % B.rw);
-                rowbuf.clear();
-                for (int64_t e = rp[i]; e < rp[i + 1]; ++e) rowbuf.emplace_back(col[e], val[e]);
-                std::stable_sort(rowbuf.begin(), rowbuf.end(),
-                                 [](const auto& a, const auto& b2) { return a.first < b2.first; });
-                int ci = 0;
-                for (const auto& [c, v] : rowbuf) {
-                    while (L.chunks[B.c0 + ci].col0 + kSpmvChunk <= c) ++ci;
-                    const size_t seg = (size_t)ci * kWarps + wi;
-                    const uint64_t pos = L.wofs[(size_t)B.c0 * kWarps + seg] + fill[seg]++;
-                    L.val[pos] = v;
-                    L.meta[pos] = (rr << 16) | (unsigned)(c - L.chunks[B.c0 + ci].col0);
+            std::copy(bchunks[b].begin(), bchunks[b].end(), L.chunks.begin() + L.blocks[b].c0);
+            uint64_t o = bofs[b];
+            for (size_t q = 0; q < bseg[b].size(); ++q) {
+                const auto& sg = bseg[b][q];
+                L.wofs[(size_t)L.blocks[b].c0 * kWarps + q] = (unsigned)o;
+                for (size_t i = 0; i < sg.size(); ++i) {
+                    L.val[o + i] = sg[i].val;
+                    L.meta[o + i] = (sg[i].row << 16) | sg[i].col;
                 }
+                o += (sg.size() + 3) & ~size_t(3);
             }
-            // padding: repeat the segment's last row, column marked as padding
-            for (size_t seg = 0; seg < fill.size(); ++seg) {
-                const uint64_t s0 = L.wofs[(size_t)B.c0 * kWarps + seg], s1 = L.wofs[(size_t)B.c0 * kWarps + seg + 1];
-                for (uint64_t pos = s0 + fill[seg]; pos < s1; ++pos) {
-                    L.val[pos] = 0.0;
-                    L.meta[pos] = (L.meta[pos - 1] & 0xFFFF0000u) | kPadCol;
-                }
-            }
+            bseg[b].clear();
+            bseg[b].shrink_to_fit();
         }
     };
     {
         std::vector<std::thread> th;
-        for (unsigned t = 0; t < hw; ++t) th.emplace_back(pass2, t);
+        for (unsigned t = 0; t < hw; ++t) th.emplace_back(place, t);
         for (auto& t : th) t.join();
     }
+    L.wofs[nchunks * kWarps] = (unsigned)E;
     L.x_bytes = 0;
     for (const auto& c : L.chunks) L.x_bytes += (uint64_t)c.ncols * 8;
-    (void)nnz;
     return true;
 }
 
-size_t spmv_chunked_smem(int rw) { return (size_t)kSpmvChunkStages * kSpmvChunk * 8 + (size_t)kWarps * rw * 8 + 2 * kSpmvChunkStages * 8; }
+size_t spmv_chunked_smem(int rw) {
+    return (size_t)kSpmvChunkStages * kSpmvChunk * 8 + (size_t)kWarps * (rw + 1) * 8 + 2 * kSpmvChunkStages * 8;
+}
 
 cudaError_t launch_spmv_chunked(const SpmvCBlock* blks, int nblk, const SpmvChunk* chunks, const unsigned* wofs,
                                 const double* val2, const unsigned* meta2, const double* x, double* y, int rw,
@@ -343,7 +404,8 @@ cudaError_t launch_spmv_chunked(const SpmvCBlock* blks, int nblk, const SpmvChun
         attr = true;
     }
     const int grid = std::min(nblk, kNumSMs);
-    spmv_chunked_kernel<kSpmvChunkStages><<<grid, 1024, smem, s>>>(blks, nblk, chunks, wofs, val2, meta2, x, y, rw);
+    spmv_chunked_kernel<kSpmvChunkStages><<<grid, 32 * kWarps, smem, s>>>(blks, nblk, chunks, wofs, val2, meta2, x, y,
+                                                                        rw, tuning().spmv_chunked_mode);
     note_launch();
     return cudaGetLastError();
 }

@@ -336,7 +336,7 @@ def test_spmv_plan_chunked_layout(cuda, case):
         rp, col, val = O.gen_band_csr(m, 0, n, 16, 20000, 9)
     elif case == "narrow":
         m = n = 70_001 + 1   # even n
-        rp, col, val = O.gen_band_csr(m, 0, n, 5, 3, 4)
+        rp, col, val = O.gen_band_csr(m, 0, n, 5, 4, 4)
     else:
         m = n = 200_000
         hbw = 6000
@@ -356,9 +356,13 @@ def test_spmv_plan_chunked_layout(cuda, case):
         col = np.concatenate(cols).astype(np.int32)
         rp = rp.astype(np.int32)
         val = rng.uniform(-1, 1, size=col.size)
-    plan = P.SpmvPlan(rp, col, val, n)
+    prev = P.tuning_set("spmv_plan_chunked", 1)
     try:
-        assert plan.layout() == "chunked"
+        plan = P.SpmvPlan(rp, col, val, n)
+    finally:
+        P.tuning_set("spmv_plan_chunked", prev)
+    try:
+        assert plan.layout() == "chunked", plan.layout()
         for call in range(3):
             x = O.fill_uniform(n, 40 + call, 4, 0, 1)
             ref = O.spmv_csr(rp, col, val, x)
@@ -385,6 +389,10 @@ def test_spmv_plan_chunked_declined_for_scattered_columns(cuda):
     rp[1:] = np.cumsum(lens)
     col = np.concatenate([np.sort(rng.choice(n, 8, replace=False)) for _ in range(m)]).astype(np.int32)
     val = rng.uniform(-1, 1, col.size)
-    plan = P.SpmvPlan(rp, col, val, n)
+    prev = P.tuning_set("spmv_plan_chunked", 1)
+    try:
+        plan = P.SpmvPlan(rp, col, val, n)
+    finally:
+        P.tuning_set("spmv_plan_chunked", prev)
     assert plan.layout() != "chunked"
     plan.close()

@@ -19,6 +19,7 @@ y = torch.empty(n, dtype=torch.float64, device="cuda")
 ref = torch.empty(n, dtype=torch.float64, device="cuda")
 P.spmv_csr(rp, col, val, x, ref)
 t0 = time.time()
+P.tuning_set("spmv_plan_chunked", 1)
 plan = P.SpmvPlan(rp.cpu(), col.cpu(), val.cpu(), n)
 print("build", round(time.time() - t0, 2), "s layout", plan.layout(), "bytes", plan.info()[1])
 model = P.spmv_csr_model(n, n, n * k).traffic_bytes
@@ -45,6 +46,11 @@ print("rel diff vs CSR kernel", rel, "nan", bool(torch.isnan(y).any()))
 for name, fn in (("csr", lambda: P.spmv_csr(rp, col, val, x, ref)), ("chunked", lambda: plan.execute(x, y))):
     ms = timeit(fn)
     print(f"{name}: {ms:.4f} ms  {model / ms / 1e6:.1f} GB/s")
+for mode in (1, 2, 3, 4, 5):
+    P.tuning_set("spmv_chunked_mode", mode)
+    ms = timeit(lambda: plan.execute(x, y))
+    print(f"chunked mode {mode}: {ms:.4f} ms")
+P.tuning_set("spmv_chunked_mode", 0)
 hx = torch.empty(n, dtype=torch.float64).pin_memory().copy_(x)
 hy = torch.empty(n, dtype=torch.float64).pin_memory()
 plan.execute_host(hx, hy)
