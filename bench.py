@@ -847,8 +847,14 @@ def dist_one_gpu(torch, P, D, hbm):
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / reps
     gbs = P.spmv_csr_model(n, n, n * k).traffic_bytes / (ms * 1e-3) / 1e9
+    # the Python -> ctypes call overhead inside host_us_per_call
+    t0 = time.perf_counter()
+    for _ in range(1000):
+        comm.info()
+    ctypes_us = (time.perf_counter() - t0) / 1000 * 1e6
     out["spmv_2parts"] = {"gbs": round(gbs, 1), "frac_of_measured_peak": round(gbs / hbm, 4),
                           "ms_per_call": round(ms, 4), "host_us_per_call": round(host * 1e6, 2),
+                          "python_call_overhead_us": round(ctypes_us, 2),
                           "halo_bytes_per_call": 2 * 2 * hb * 8}
     plan.close()
     del tens

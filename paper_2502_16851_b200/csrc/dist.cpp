@@ -326,8 +326,9 @@ void post_exchange(rl_dist_s* d, const std::vector<rl_dist_op>& ops, Buf&& buffe
 struct Replay {
     cudaStream_t s = nullptr;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_start = nullptr, ev_halo = nullptr;
-    cudaGraphExec_t exec = nullptr;
-    uint64_t launches = 0;  // library kernels per replay
+    cudaGraphExec_t exec = nullptr;       // one call (SpMV) / two timesteps (stencil)
+    cudaGraphExec_t exec_long = nullptr;  // stencil: kLongSteps timesteps
+    uint64_t launches = 0, launches_long = 0;  // library kernels per replay
     bool warmed = false;
     void create() {
         ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
@@ -336,12 +337,17 @@ struct Replay {
     }
     void destroy() {
         if (exec) cudaGraphExecDestroy(exec);
+        if (exec_long) cudaGraphExecDestroy(exec_long);
         for (cudaEvent_t e : {ev_in, ev_out, ev_start, ev_halo})
             if (e) cudaEventDestroy(e);
         if (s) cudaStreamDestroy(s);
     }
     template <class Body>
     void capture(Body&& body) {
+        capture_into(exec, launches, body);
+    }
+    template <class Body>
+    void capture_into(cudaGraphExec_t& out, uint64_t& nlaunch, Body&& body) {
         const uint64_t before = rl_kernel_launches();
         ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "graph capture");
         cudaGraph_t g = nullptr;
@@ -353,10 +359,10 @@ struct Replay {
             throw;
         }
         ck(cudaStreamEndCapture(s, &g), "graph capture");
-        const cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
+        const cudaError_t e = cudaGraphInstantiate(&out, g, 0);
         cudaGraphDestroy(g);
         ck(e, "graph instantiate");
-        launches = rl_kernel_launches() - before;
+        nlaunch = rl_kernel_launches() - before;
     }
     // The instantiated graph carries its own fork/join between the plan's
     // stream and the comm stream, so a replay is ONE launch into the caller's
@@ -364,6 +370,10 @@ struct Replay {
     void replay(cudaStream_t caller) {
         ck(cudaGraphLaunch(exec, caller), "graph launch");
         rlb::note_launch(launches);
+    }
+    void replay_long(cudaStream_t caller) {
+        ck(cudaGraphLaunch(exec_long, caller), "graph launch");
+        rlb::note_launch(launches_long);
     }
     void enter(cudaStream_t caller) {
         ck(cudaEventRecord(ev_in, caller), "event");
@@ -376,6 +386,7 @@ struct Replay {
 };
 
 bool graphs_on() { return rlb::tuning().dist_graph != 0; }
+constexpr int kLongSteps = 10;  // even: a long graph starts and ends in u
 
 }  // namespace
 
@@ -626,6 +637,14 @@ KernelCharacterization stencil_run(rl_dist_stencil_s* pl, uint64_t steps, cudaSt
             stencil_step(pl, true);
             stencil_step(pl, false);
         });
+    // long runs: kLongSteps timesteps per graph launch (host cost per
+    // timestep ~ one graph launch / kLongSteps)
+    if (r.exec && !r.exec_long && steps >= kLongSteps)
+        r.capture_into(r.exec_long, r.launches_long, [&] {
+            for (int i = 0; i < kLongSteps; ++i) stencil_step(pl, (i & 1) == 0);
+        });
+    if (r.exec_long)
+        for (; t + kLongSteps <= steps; t += kLongSteps) r.replay_long(caller);
     if (r.exec)
         for (; t + 2 <= steps; t += 2) r.replay(caller);
     if (t < steps) {  // eager: the first call, or the odd last timestep

@@ -126,7 +126,8 @@ def test_dist_stencil_parts_on_one_gpu(comm, L, unit, preset, gshape):
 
     r = P.stencil_preset(preset)[2]
     parts = [D.SlabPartition(preset, gshape, L, i) for i in range(L)]
-    for seed, steps in ((5, 3), (6, 4), (7, 6)):   # eager, then graph replays (+ an odd tail in the first)
+    # eager first; then 2-timestep graph replays; 23 = two 10-timestep graphs + a pair + an odd eager step
+    for seed, steps in ((5, 3), (6, 4), (7, 23)):
         bufs = [_ghost_poisoned(torch, preset, gshape, p, seed) for p in parts]
         plan = D.DistStencil(comm, preset, gshape, [b[0] for b in bufs], [b[1] for b in bufs], unit=unit)
         try:
