@@ -28,7 +28,7 @@ struct Tuning {
     int spmv_long_piece = 512;     // ... cut into pieces of this many nonzeros, balanced over the warps
     int spmv_long_group = 8;       // lanes per piece of the CUDA-core long-row kernel (8, 16, 32)
     int spmv_plan_chunks = 16;     // pipelined row/x chunks of rl_spmv_plan_execute_host
-    int spmv_chunked_mode = 0;     // K16 diagnostics: 0 normal; data movement only: 1 all, 2 x staging, 3 val/meta, 4/5 as 1/3 with 4-entry vector loads
+    int spmv_chunked_mode = 0;     // K16 diagnostics: 0 normal; data movement only: 1 all, 2 x staging, 3 val/meta
     int spmv_plan_chunked = 0;     // 1: CUDA-core plans use the column-chunked layout (K16, spmv_chunked.cu) when the staged x stays <= 12 B per nonzero (measured 0.30-0.35 vs CSR 0.287 ms: opt-in)
     int spmv_plan_sorted = 0;      // 1: CUDA-core plans use the column-sorted block layout when eligible (spmv_sorted.cu; halves the L2 requests but measured 0.287 vs 0.274 ms: latency-bound)
     int spmv_sorted_cap = 16384;   // ... slot grid per block (16384: 1024 threads, 1 CTA/SM; 8192: 512 threads, 3 CTAs/SM)
@@ -219,6 +219,7 @@ constexpr int kNumSMsHost = 148;     // B200 SM count (host-side copy of common.
 constexpr int kSpmvChunk = 4096;      // x columns per staged chunk (32 KB)
 constexpr int kSpmvChunkStages = 4;   // ring depth
 constexpr int kSpmvChunkWarps = 16;   // warps per CTA (one CTA per SM; rows per warp <= 512)
+constexpr int kSpmvChunkBatches = 4;  // 128-entry batches in flight per warp
 struct SpmvCBlock {
     uint32_t row0, rows;  // rows [row0, row0 + rows)
     int rw;               // rows per warp (block rows = kSpmvChunkWarps rw)

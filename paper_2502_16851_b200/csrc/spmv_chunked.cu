@@ -93,15 +93,14 @@ __global__ void __launch_bounds__(32 * kSpmvChunkWarps, 1) spmv_chunked_kernel(
             ++pk;
         }
     };
-    if (tid == 0 && mode != 3 && mode != 5) produce(S);
+    if (tid == 0 && mode != 3) produce(S);
 
     // A batch = 4 groups of 32 entries (entry j + 32 q + lane).  The loads of a
     // warp's batches run two batches ahead of the one being applied, across
     // chunk boundaries (they do not depend on the x stage).  Segment bounds of
     // 32 chunks at a time sit in the lanes (lane l: chunk g0 + l).
     struct Batch {
-        bool ok;
-        int ci;         // chunk within the group of 32
+        int ci;         // chunk within the group of 32 (gn: no batch)
         unsigned j, e;  // first entry, end of the segment
         double v[4];
         unsigned m[4];
@@ -122,42 +121,30 @@ __global__ void __launch_bounds__(32 * kSpmvChunkWarps, 1) spmv_chunked_kernel(
                     lj = __shfl_sync(0xffffffffu, so, lc & 31);
                     le = __shfl_sync(0xffffffffu, eo, lc & 31);
                 }
-                bt.ok = lc < gn;
                 bt.ci = lc;
                 bt.j = lj;
                 bt.e = le;
-                if (mode == 4 || mode == 5) {  // diagnostic: 4 consecutive entries per lane (256 / 128-bit loads)
-                    const unsigned jj = lj + 4 * lane;
-                    if (bt.ok && jj < le) {
-                        const d4 v = ld4_stream(val2 + jj, pol);
-                        int4 mv;
-                        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
-                            : "=r"(mv.x), "=r"(mv.y), "=r"(mv.z), "=r"(mv.w) : "l"(meta2 + jj), "l"(pol));
-                        bt.v[0] = v.x; bt.v[1] = v.y; bt.v[2] = v.z; bt.v[3] = v.w;
-                        bt.m[0] = mv.x; bt.m[1] = mv.y; bt.m[2] = mv.z; bt.m[3] = mv.w;
-                    }
-                    lj += 128;
-                    return;
-                }
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const unsigned jj = lj + 32 * q + lane;
-                    if (bt.ok && jj < le && mode != 2) {
+                    if (lc < gn && jj < le && mode != 2) {
                         bt.v[q] = ld_stream(val2 + jj, pol);
                         bt.m[q] = (unsigned)ld_stream_i32(reinterpret_cast<const int*>(meta2) + jj, pol);
                     }
                 }
                 lj += 128;
             };
-            // Four batches in flight per warp, rotated without register copies
-            // (a copy of a batch whose loads are still in flight would wait for
-            // them): the batch just applied is reloaded in place, four ahead.
+            // kSpmvChunkBatches (3 or 4) batches in flight per warp, rotated
+            // without register copies (a copy of a batch whose loads are still in
+            // flight would wait for them): the batch just applied is reloaded in
+            // place, NB ahead.
+            constexpr int NB = kSpmvChunkBatches;
             Batch A, B, C, D;
             turn = 0;
             next(A);
             next(B);
             next(C);
-            next(D);
+            if constexpr (NB == 4) next(D);
             auto apply = [&](const Batch& bt, const double* xc) {
                 if (mode != 0) {  // diagnostic modes: data movement only
                     if (bt.v[0] == 12345.678) yw[0] += xc[0];
@@ -173,13 +160,17 @@ __global__ void __launch_bounds__(32 * kSpmvChunkWarps, 1) spmv_chunked_kernel(
                 }
             };
             for (int ci = 0; ci < gn; ++ci, ++k) {
-                if (mode != 3 && mode != 5) mbar_wait(full + (k % S), (uint32_t)((k / S) & 1));
+                if (mode != 3) mbar_wait(full + (k % S), (uint32_t)((k / S) & 1));
                 const double* xc = xs + (k % S) * kSpmvChunk;
                 for (;;) {
-                    const bool more = turn == 0   ? (A.ok && A.ci == ci)
-                                      : turn == 1 ? (B.ok && B.ci == ci)
-                                      : turn == 2 ? (C.ok && C.ci == ci)
-                                                  : (D.ok && D.ci == ci);
+                    bool more;
+                    if constexpr (NB == 4)
+                        more = turn == 0 ? (A.ci == ci) : turn == 1 ? (B.ci == ci)
+                                                              : turn == 2 ? (C.ci == ci)
+                                                                          : (D.ci == ci);
+                    else
+                        more = turn == 0 ? (A.ci == ci) : turn == 1 ? (B.ci == ci)
+                                                                          : (C.ci == ci);
                     if (!more) break;
                     if (turn == 0) {
                         apply(A, xc);
@@ -187,19 +178,19 @@ __global__ void __launch_bounds__(32 * kSpmvChunkWarps, 1) spmv_chunked_kernel(
                     } else if (turn == 1) {
                         apply(B, xc);
                         next(B);
-                    } else if (turn == 2) {
+                    } else if (NB == 3 || turn == 2) {
                         apply(C, xc);
                         next(C);
                     } else {
                         apply(D, xc);
                         next(D);
                     }
-                    turn = (turn + 1) & 3;
+                    turn = turn + 1 == NB ? 0 : turn + 1;
                 }
                 // release the stage (one arrive per warp); thread 0 refills it
                 __syncwarp();
                 if (lane == 0) mbar_arrive(empty + (k % S));
-                if (tid == 0 && mode != 3 && mode != 5) produce(k + 1 + S);
+                if (tid == 0 && mode != 3) produce(k + 1 + S);
             }
         }
         // the block's y rows: coalesced store, then clear for the next block
