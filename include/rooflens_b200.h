@@ -183,12 +183,13 @@ RL_API int rl_stencil_host(rl_unit unit, rl_precision precision, const char* pre
                     double* v, rl_kchar* out);
 /* SpMV plan: the CSR matrix is uploaded once (the iterative-solver pattern:
  * A is fixed, x changes every step) and each execute moves only x in and y
- * out.  CUDA-core plans (even n) re-lay A once into column tiles so every x
- * value comes from shared memory (the role of cusparseSpMV_preprocess / DASP's
- * conversion): 8192-row blocks, <= 2048-column tiles, 10 bytes per nonzero.  execute_host pipelines the x upload, the row-chunk kernels and the y
- * download on three streams: row chunk c starts as soon as the x prefix it
- * references (max column, computed at creation) has arrived.  The plan owns
- * its device buffers; no allocation happens in execute. */
+ * out.  The plan keeps A as CSR; two opt-in CUDA-core layouts built once at
+ * creation exist as measured alternatives (tuning keys spmv_plan_sorted,
+ * spmv_plan_chunked; K15/K16).  execute_host pipelines the x
+ * upload, the row-chunk kernels and the y download on three streams: row
+ * chunk c starts as soon as the x prefix it references (max column, computed
+ * at creation) has arrived.  The plan owns its device buffers; no allocation
+ * happens in execute. */
 typedef struct rl_spmv_plan_s* rl_spmv_plan;
 RL_API int rl_spmv_plan_create(rl_unit unit, rl_precision precision, uint64_t m, uint64_t n,
                                uint64_t nnz, const int32_t* row_ptr, const int32_t* col,
@@ -197,9 +198,9 @@ RL_API int rl_spmv_plan_execute_host(rl_spmv_plan plan, const double* x, double*
 RL_API int rl_spmv_plan_execute(rl_spmv_plan plan, const double* x_dev, double* y_dev,
                                 rl_stream stream, rl_kchar* out);
 RL_API int rl_spmv_plan_destroy(rl_spmv_plan plan);
-/* Layout of a plan: *tiled = 1 for the column-tiled CUDA-core layout (see
- * DESIGN.md), *layout_bytes = device bytes one execute streams for A. */
-RL_API int rl_spmv_plan_info(rl_spmv_plan plan, int* tiled, uint64_t* layout_bytes);
+/* Layout of a plan: *layout = 0 CSR, 2 column-sorted blocks (K15), 3
+ * column-chunked (K16); *layout_bytes = device bytes one execute streams for A. */
+RL_API int rl_spmv_plan_info(rl_spmv_plan plan, int* layout, uint64_t* layout_bytes);
 
 /* Release the device/pinned workspaces cached by the _host entry points. */
 RL_API int rl_host_workspace_release(void);

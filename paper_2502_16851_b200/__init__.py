@@ -512,18 +512,18 @@ class SpmvPlan:
         return _kc(k)
 
     def info(self):
-        """(tiled, layout_bytes): whether the column-tiled layout is used and the
-        bytes one execute streams for A."""
+        """(layout, layout_bytes): the layout name and the bytes one execute
+        streams for A."""
         t, b = _int(), _u64()
         _check(lib().rl_spmv_plan_info(self._h, C.byref(t), C.byref(b)))
-        return t.value == 1, int(b.value)
+        return self.layout(), int(b.value)
 
     def layout(self) -> str:
-        """"csr", "tiled" (spmv_tiled.cu), "sorted" (column-sorted blocks, spmv_sorted.cu) or
-        "chunked" (x chunks staged in shared memory, spmv_chunked.cu)."""
+        """"csr", "sorted" (column-sorted blocks, spmv_sorted.cu) or "chunked"
+        (x chunks staged in shared memory, spmv_chunked.cu)."""
         t = _int()
         _check(lib().rl_spmv_plan_info(self._h, C.byref(t), None))
-        return {0: "csr", 1: "tiled", 2: "sorted", 3: "chunked"}[t.value]
+        return {0: "csr", 2: "sorted", 3: "chunked"}[t.value]
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:

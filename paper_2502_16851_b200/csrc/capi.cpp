@@ -226,10 +226,12 @@ KernelCharacterization stencil_temporal(ExecutionUnit unit, Precision p, const S
     if (u == v) throw Error(ErrorKind::ValidationError, "u and v must be distinct buffers");
     if (t > 8) throw Error(ErrorKind::InvalidRange, "temporal depth > 8 is not implemented");
     const rlb::StencilDesc d = make_desc(shape, dims, weights);
-    const bool use_tb = t >= 2 && rlb::tuning().stencil_tb && rlb::stencil_tb_supported(d, (int)t, u, v);
-    const bool use_tb3r = t >= 2 && rlb::tuning().stencil_tb3_mode && rlb::stencil_tb3r_supported(d, (int)t, u, v);
+    const bool use_tb = t >= 2 && rlb::stencil_tb_supported(d, (int)t, u, v);
+    // 3d7pt: the register-blocked TMA kernel; the z-column kernel covers the
+    // shapes it refuses (odd nx, unaligned rows)
+    const bool use_tb3r = t >= 2 && rlb::stencil_tb3r_supported(d, (int)t, u, v);
     const bool use_tb3 = t >= 2 && (use_tb3r || rlb::stencil_tb3_supported(d, (int)t));
-    const bool ok2d = d.preset == rlb::kP2d5 && (use_tb || (t == 2 && rlb::stencil_tma_eligible(d, u, v)));
+    const bool ok2d = d.preset == rlb::kP2d5 && use_tb;
     if (t >= 2 && (unit != ExecutionUnit::CudaCore || !(ok2d || use_tb3)))
         throw Error(ErrorKind::ValidationError,
                     "temporal depth >= 2 is implemented on the CUDA core for 2d5pt (t <= 8; even depths need "
@@ -251,8 +253,6 @@ KernelCharacterization stencil_temporal(ExecutionUnit unit, Precision p, const S
             cuda_check(rlb::launch_stencil_tb3(d, (int)t, 1, outer - 1, src, dst, s), "stencil (3D temporal blocking)");
         } else if (i < fused && use_tb) {
             cuda_check(rlb::launch_stencil_tb(d, (int)t, 1, outer - 1, src, dst, s), "stencil (temporal blocking)");
-        } else if (i < fused && t == 2) {
-            cuda_check(rlb::launch_stencil_tma_t2(d, 1, outer - 1, src, dst, s), "stencil (temporal depth 2)");
         } else {
             sweep(unit, d, 0, outer, src, dst, s);
         }
@@ -425,8 +425,6 @@ struct rl_spmv_plan_s {
     uint64_t m = 0, n = 0, nnz = 0;
     int32_t *rp = nullptr, *col = nullptr;
     double *val = nullptr, *x = nullptr, *y = nullptr;
-    // column-tiled layout (CUDA-core plans): segments, tile table, block table
-    bool tiled = false;
     // column-chunked layout (K16, spmv_chunked.cu)
     bool chunked = false;
     int crw = 0;
@@ -443,10 +441,6 @@ struct rl_spmv_plan_s {
     uint32_t* spk = nullptr;
     double* ssv = nullptr;
     std::vector<uint32_t> sblk_r0;
-    uint8_t* segs = nullptr;
-    rlb::SpmvTile* tiles = nullptr;
-    int* blk_tiles = nullptr;
-    uint64_t nblocks = 0;
     uint64_t layout_bytes = 0;
     std::vector<uint64_t> chunk_row;   // chunk c = rows [chunk_row[c], chunk_row[c+1])
     std::vector<uint64_t> chunk_xend;  // x prefix [0, chunk_xend[c]) chunk c reads
@@ -474,9 +468,6 @@ struct rl_spmv_plan_s {
             if (p) cudaFree(p);
         if (spk) cudaFree(spk);
         if (ssv) cudaFree(ssv);
-        if (segs) cudaFree(segs);
-        if (tiles) cudaFree(tiles);
-        if (blk_tiles) cudaFree(blk_tiles);
         if (gexec) cudaGraphExecDestroy(gexec);
         for (auto e : ev_x) cudaEventDestroy(e);
         for (auto e : ev_y) cudaEventDestroy(e);
@@ -509,23 +500,7 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
     pl->kc = k;
     ck(cudaMalloc(&pl->x, std::max<uint64_t>(n, 2) * 8), "plan alloc");
     ck(cudaMalloc(&pl->y, m * 8), "plan alloc");
-    pl->tiled = unit == ExecutionUnit::CudaCore && rlb::tuning().spmv_plan_tiled && n % 2 == 0;
-    if (pl->tiled) {
-        std::vector<uint8_t> segs;
-        std::vector<rlb::SpmvTile> tiles;
-        std::vector<int> blk;
-        rlb::spmv_tiled_build(m, n, rp, col, val, segs, tiles, blk);
-        pl->nblocks = blk.size() - 1;
-        pl->layout_bytes = segs.size();
-        ck(cudaMalloc(&pl->segs, std::max<size_t>(segs.size(), 16)), "plan alloc");
-        ck(cudaMalloc(&pl->tiles, std::max<size_t>(tiles.size(), 1) * sizeof(rlb::SpmvTile)), "plan alloc");
-        ck(cudaMalloc(&pl->blk_tiles, blk.size() * sizeof(int)), "plan alloc");
-        if (!segs.empty()) ck(cudaMemcpy(pl->segs, segs.data(), segs.size(), cudaMemcpyHostToDevice), "plan upload");
-        if (!tiles.empty())
-            ck(cudaMemcpy(pl->tiles, tiles.data(), tiles.size() * sizeof(rlb::SpmvTile), cudaMemcpyHostToDevice),
-               "plan upload");
-        ck(cudaMemcpy(pl->blk_tiles, blk.data(), blk.size() * sizeof(int), cudaMemcpyHostToDevice), "plan upload");
-    } else {
+    {
         // column-sorted blocks (spmv_sorted.cu) for CUDA-core plans whose rows
         // all fit (<= 64 nonzeros, block column span < 2^18); else the CSR
         std::vector<rlb::SpmvSBlock> sb;
@@ -585,9 +560,8 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
             pl->layout_bytes = (m + 1) * 4 + nnz * 12;
         }
     }
-    // pipeline chunks: whole tiled blocks when tiled
-    const uint64_t unitrows = pl->tiled ? (uint64_t)rlb::kSpmvTiledRows : 1;
-    const uint64_t units = (m + unitrows - 1) / unitrows;
+    const uint64_t unitrows = 1;
+    const uint64_t units = m;
     {
         int64_t maxlen = 0;
         for (uint64_t i = 0; i < m; ++i) maxlen = std::max<int64_t>(maxlen, (int64_t)rp[i + 1] - rp[i]);
@@ -682,7 +656,7 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
     return pl.release();
 }
 
-// Rows [r0, r1) of y = A x on the plan's layout (r0/r1 block-aligned when tiled).
+// Rows [r0, r1) of y = A x on the plan's layout (r0/r1 block-aligned for the block layouts).
 void plan_rows(rl_spmv_plan_s* pl, uint64_t r0, uint64_t r1, const double* x, double* y, cudaStream_t s) {
     if (pl->chunked) {  // r0 / r1 on block starts
         const auto& v = pl->cblk_r0;
@@ -699,11 +673,7 @@ void plan_rows(rl_spmv_plan_s* pl, uint64_t r0, uint64_t r1, const double* x, do
         ck(rlb::launch_spmv_sorted(pl->sblk, b0, b1, pl->spk, pl->ssv, pl->rp, x, y, pl->scap, s), "spmv (sorted plan)");
         return;
     }
-    if (pl->tiled) {
-        const uint64_t b0 = r0 / rlb::kSpmvTiledRows;
-        const uint64_t b1 = (r1 + rlb::kSpmvTiledRows - 1) / rlb::kSpmvTiledRows;
-        ck(rlb::launch_spmv_tiled(pl->m, pl->segs, pl->tiles, pl->blk_tiles, b0, b1, x, y, s), "spmv (tiled plan)");
-    } else {
+    {
         spmv_csr_rows(pl->unit, Precision::FP64, r0, r1, pl->rp, pl->col, pl->val, x, 0, y, s, pl->long_rows);
     }
 }
@@ -1010,7 +980,7 @@ int rl_spmv_plan_execute(rl_spmv_plan pl, const double* x, double* y, rl_stream 
         require_ptr(pl, "plan");
         require_ptr(x, "x");
         require_ptr(y, "y");
-        if ((pl->tiled || pl->chunked) && (reinterpret_cast<uintptr_t>(x) & 15))
+        if (pl->chunked && (reinterpret_cast<uintptr_t>(x) & 15))
             throw Error(ErrorKind::ValidationError, "this plan's layout stages x with bulk copies: x must be 16-byte aligned");
         plan_rows(pl, 0, pl->m, x, y, static_cast<cudaStream_t>(s));
         put(out, pl->kc);
@@ -1019,7 +989,7 @@ int rl_spmv_plan_execute(rl_spmv_plan pl, const double* x, double* y, rl_stream 
 int rl_spmv_plan_info(rl_spmv_plan pl, int* tiled, uint64_t* layout_bytes) {
     return guarded([&] {
         require_ptr(pl, "plan");
-        if (tiled) *tiled = pl->tiled ? 1 : (pl->sorted ? 2 : (pl->chunked ? 3 : 0));
+        if (tiled) *tiled = pl->sorted ? 2 : (pl->chunked ? 3 : 0);
         if (layout_bytes) *layout_bytes = pl->layout_bytes;
     });
 }
@@ -1220,77 +1190,92 @@ int rl_fp64_peak_launch(rl_unit u, uint64_t iters, rl_stream s, double* sink, do
     });
 }
 
+// Tuning keys.  Product keys select a documented variant a caller may want
+// (the tensor-core stencil form, plan layouts, graph replay, the long-row
+// path); the rest are sweep knobs of the kernels' launch shapes, accepted
+// only with RL_DEV_TUNING=1 in the environment (tests and tools/sweep.py).
 int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
     return guarded([&] {
         require_ptr(key, "key");
-        rlb::Tuning& t = rlb::tuning();
-        int* slot = nullptr;
+        struct Key {
+            const char* name;
+            int rlb::Tuning::*field;
+            bool product;
+        };
+        static const Key keys[] = {
+        {"scale_blocks_per_sm", &rlb::Tuning::scale_blocks_per_sm, false},
+        {"dist_graph", &rlb::Tuning::dist_graph, true},
+        {"spmv_rows", &rlb::Tuning::spmv_rows, false},
+        {"gemv_rows", &rlb::Tuning::gemv_rows, false},
+        {"gemv_unroll", &rlb::Tuning::gemv_unroll, false},
+        {"spmv_blocks_per_sm", &rlb::Tuning::spmv_blocks_per_sm, false},
+        {"spmv_sched", &rlb::Tuning::spmv_sched, false},
+        {"spmv_threads", &rlb::Tuning::spmv_threads, false},
+        {"spmv_plan_chunks", &rlb::Tuning::spmv_plan_chunks, true},
+        {"spmv_plan_zero_copy", &rlb::Tuning::spmv_plan_zero_copy, false},
+        {"spmv_long_rows", &rlb::Tuning::spmv_long_rows, true},
+        {"spmv_long_min", &rlb::Tuning::spmv_long_min, true},
+        {"spmv_long_piece", &rlb::Tuning::spmv_long_piece, false},
+        {"spmv_long_group", &rlb::Tuning::spmv_long_group, false},
+        {"spmv_plan_graph", &rlb::Tuning::spmv_plan_graph, true},
+        {"spmv_plan_taper", &rlb::Tuning::spmv_plan_taper, false},
+        {"spmv_plan_xpieces", &rlb::Tuning::spmv_plan_xpieces, false},
+        {"spmv_plan_sorted", &rlb::Tuning::spmv_plan_sorted, true},
+        {"spmv_plan_chunked", &rlb::Tuning::spmv_plan_chunked, true},
+        {"spmv_chunked_mode", &rlb::Tuning::spmv_chunked_mode, false},
+        {"spmv_sorted_cap", &rlb::Tuning::spmv_sorted_cap, false},
+        {"spmv_sorted_pipe", &rlb::Tuning::spmv_sorted_pipe, false},
+        {"spmv_plan_ygroups", &rlb::Tuning::spmv_plan_ygroups, false},
+        {"stencil_r_ctas_per_sm", &rlb::Tuning::stencil_r_ctas_per_sm, false},
+        {"stencil_tb_waves", &rlb::Tuning::stencil_tb_waves, false},
+        {"stencil_tb_tma", &rlb::Tuning::stencil_tb_tma, false},
+        {"stencil_tb3_chunks", &rlb::Tuning::stencil_tb3_chunks, false},
+        {"stencil_tb3_shape", &rlb::Tuning::stencil_tb3_shape, false},
+        {"stencil_tb3_l2promo", &rlb::Tuning::stencil_tb3_l2promo, false},
+        {"stencil3d_cc_stages", &rlb::Tuning::stencil3d_cc_stages, false},
+        {"stencil_tc_concat", &rlb::Tuning::stencil_tc_concat, false},
+        {"stencil_cc27x2", &rlb::Tuning::stencil_cc27x2, false},
+        {"stencil_r_cc_stages", &rlb::Tuning::stencil_r_cc_stages, false},
+        {"stencil_r_tc_stages", &rlb::Tuning::stencil_r_tc_stages, false},
+        {"stencil_r_sym", &rlb::Tuning::stencil_r_sym, false},
+        {"stencil_r_l2promo", &rlb::Tuning::stencil_r_l2promo, false},
+        {"spmv_tc_blocks_per_sm", &rlb::Tuning::spmv_tc_blocks_per_sm, false},
+        {"spmv_tc_threads", &rlb::Tuning::spmv_tc_threads, false},
+        {"spmv_tc_rows", &rlb::Tuning::spmv_tc_rows, false},
+        {"spmv_l1_carveout", &rlb::Tuning::spmv_l1_carveout, false},
+        {"spmv_xhint", &rlb::Tuning::spmv_xhint, false},
+        {"scale_unroll", &rlb::Tuning::scale_unroll, false},
+        {"stencil2d_rows", &rlb::Tuning::stencil2d_rows, false},
+        {"stencil3d_zchunk", &rlb::Tuning::stencil3d_zchunk, false},
+        {"tc_stencil_zchunk", &rlb::Tuning::tc_stencil_zchunk, false},
+        {"stencil_tma", &rlb::Tuning::stencil_tma, true},
+        {"stencil_ctas_per_sm", &rlb::Tuning::stencil_ctas_per_sm, false},
+        {"stencil_rows_per_thread", &rlb::Tuning::stencil_rows_per_thread, false},
+        {"stencil2d_rows_per_thread", &rlb::Tuning::stencil2d_rows_per_thread, false},
+        {"stencil_tc_ctas_per_sm", &rlb::Tuning::stencil_tc_ctas_per_sm, false},
+        {"stencil_tc3d_ctas_per_sm", &rlb::Tuning::stencil_tc3d_ctas_per_sm, false},
+        {"stencil_tc3d_mode", &rlb::Tuning::stencil_tc3d_mode, false},
+        {"stencil_tc1_ctas_per_sm", &rlb::Tuning::stencil_tc1_ctas_per_sm, false},
+        {"stencil_tc3d_hybrid", &rlb::Tuning::stencil_tc3d_hybrid, true},
+        {"stencil_tch_ctas_per_sm", &rlb::Tuning::stencil_tch_ctas_per_sm, false},
+        {"stencil_tch_k8", &rlb::Tuning::stencil_tch_k8, false},
+        {"stencil_tch_stages", &rlb::Tuning::stencil_tch_stages, false},
+        {"stencil3d_balance", &rlb::Tuning::stencil3d_balance, false},
+        {"stencil_tc2d_hybrid", &rlb::Tuning::stencil_tc2d_hybrid, true},
+        {"stencil_tch_tpw", &rlb::Tuning::stencil_tch_tpw, false},
+        };
+        static const bool dev = [] {
+            const char* e = std::getenv("RL_DEV_TUNING");
+            return e != nullptr && e[0] == '1';
+        }();
         const std::string k(key);
-        if (k == "scale_blocks_per_sm") slot = &t.scale_blocks_per_sm;
-        else if (k == "dist_graph") slot = &t.dist_graph;
-        else if (k == "spmv_rows") slot = &t.spmv_rows;
-        else if (k == "gemv_rows") slot = &t.gemv_rows;
-        else if (k == "gemv_unroll") slot = &t.gemv_unroll;
-        else if (k == "spmv_blocks_per_sm") slot = &t.spmv_blocks_per_sm;
-        else if (k == "spmv_sched") slot = &t.spmv_sched;
-        else if (k == "spmv_threads") slot = &t.spmv_threads;
-        else if (k == "spmv_plan_chunks") slot = &t.spmv_plan_chunks;
-        else if (k == "spmv_plan_zero_copy") slot = &t.spmv_plan_zero_copy;
-        else if (k == "spmv_plan_tiled") slot = &t.spmv_plan_tiled;
-        else if (k == "spmv_long_rows") slot = &t.spmv_long_rows;
-        else if (k == "spmv_long_min") slot = &t.spmv_long_min;
-        else if (k == "spmv_long_piece") slot = &t.spmv_long_piece;
-        else if (k == "spmv_long_group") slot = &t.spmv_long_group;
-        else if (k == "spmv_plan_graph") slot = &t.spmv_plan_graph;
-        else if (k == "spmv_plan_taper") slot = &t.spmv_plan_taper;
-        else if (k == "spmv_plan_xpieces") slot = &t.spmv_plan_xpieces;
-        else if (k == "spmv_plan_sorted") slot = &t.spmv_plan_sorted;
-        else if (k == "spmv_plan_chunked") slot = &t.spmv_plan_chunked;
-        else if (k == "spmv_chunked_mode") slot = &t.spmv_chunked_mode;
-        else if (k == "spmv_sorted_cap") slot = &t.spmv_sorted_cap;
-        else if (k == "spmv_sorted_pipe") slot = &t.spmv_sorted_pipe;
-        else if (k == "spmv_plan_ygroups") slot = &t.spmv_plan_ygroups;
-        else if (k == "stencil_r_ctas_per_sm") slot = &t.stencil_r_ctas_per_sm;
-        else if (k == "stencil_tb_waves") slot = &t.stencil_tb_waves;
-        else if (k == "stencil_tb") slot = &t.stencil_tb;
-        else if (k == "stencil_tb_tma") slot = &t.stencil_tb_tma;
-        else if (k == "stencil_tb3_mode") slot = &t.stencil_tb3_mode;
-        else if (k == "stencil_tb3_chunks") slot = &t.stencil_tb3_chunks;
-        else if (k == "stencil_tb3_shape") slot = &t.stencil_tb3_shape;
-        else if (k == "stencil_tb3_l2promo") slot = &t.stencil_tb3_l2promo;
-        else if (k == "stencil3d_cc_stages") slot = &t.stencil3d_cc_stages;
-        else if (k == "stencil_tc_concat") slot = &t.stencil_tc_concat;
-        else if (k == "stencil_cc27x2") slot = &t.stencil_cc27x2;
-        else if (k == "stencil_r_cc_stages") slot = &t.stencil_r_cc_stages;
-        else if (k == "stencil_r_tc_stages") slot = &t.stencil_r_tc_stages;
-        else if (k == "stencil_r_sym") slot = &t.stencil_r_sym;
-        else if (k == "stencil_r_l2promo") slot = &t.stencil_r_l2promo;
-        else if (k == "spmv_tc_blocks_per_sm") slot = &t.spmv_tc_blocks_per_sm;
-        else if (k == "spmv_tc_threads") slot = &t.spmv_tc_threads;
-        else if (k == "spmv_tc_rows") slot = &t.spmv_tc_rows;
-        else if (k == "spmv_l1_carveout") slot = &t.spmv_l1_carveout;
-        else if (k == "spmv_xhint") slot = &t.spmv_xhint;
-        else if (k == "scale_unroll") slot = &t.scale_unroll;
-        else if (k == "stencil2d_rows") slot = &t.stencil2d_rows;
-        else if (k == "stencil3d_zchunk") slot = &t.stencil3d_zchunk;
-        else if (k == "tc_stencil_zchunk") slot = &t.tc_stencil_zchunk;
-        else if (k == "stencil_tma") slot = &t.stencil_tma;
-        else if (k == "stencil_ctas_per_sm") slot = &t.stencil_ctas_per_sm;
-        else if (k == "stencil_rows_per_thread") slot = &t.stencil_rows_per_thread;
-        else if (k == "stencil2d_rows_per_thread") slot = &t.stencil2d_rows_per_thread;
-        else if (k == "stencil_t2_ctas_per_sm") slot = &t.stencil_t2_ctas_per_sm;
-        else if (k == "stencil_tc_ctas_per_sm") slot = &t.stencil_tc_ctas_per_sm;
-        else if (k == "stencil_tc3d_ctas_per_sm") slot = &t.stencil_tc3d_ctas_per_sm;
-        else if (k == "stencil_tc3d_mode") slot = &t.stencil_tc3d_mode;
-        else if (k == "stencil_tc1_ctas_per_sm") slot = &t.stencil_tc1_ctas_per_sm;
-        else if (k == "stencil_tc3d_hybrid") slot = &t.stencil_tc3d_hybrid;
-        else if (k == "stencil_tch_ctas_per_sm") slot = &t.stencil_tch_ctas_per_sm;
-        else if (k == "stencil_tch_k8") slot = &t.stencil_tch_k8;
-        else if (k == "stencil_tch_stages") slot = &t.stencil_tch_stages;
-        else if (k == "stencil3d_balance") slot = &t.stencil3d_balance;
-        else if (k == "stencil_tc2d_hybrid") slot = &t.stencil_tc2d_hybrid;
-        else if (k == "stencil_tch_tpw") slot = &t.stencil_tch_tpw;
-        else throw Error(ErrorKind::ValidationError, "unknown tuning key '" + k + "'");
+        const Key* hit = nullptr;
+        for (const Key& e : keys)
+            if (k == e.name) hit = &e;
+        if (!hit) throw Error(ErrorKind::ValidationError, "unknown tuning key '" + k + "'");
+        if (!hit->product && !dev)
+            throw Error(ErrorKind::ValidationError, "'" + k + "' is a developer sweep key (set RL_DEV_TUNING=1)");
+        int* slot = &(rlb::tuning().*(hit->field));
         if (previous) *previous = *slot;
         if (value < -1) throw Error(ErrorKind::InvalidRange, "tuning values must be >= -1");
         *slot = static_cast<int>(value);

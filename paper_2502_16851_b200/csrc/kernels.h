@@ -33,7 +33,6 @@ struct Tuning {
     int spmv_plan_sorted = 0;      // 1: CUDA-core plans use the column-sorted block layout when eligible (spmv_sorted.cu; halves the L2 requests but measured 0.287 vs 0.274 ms: latency-bound)
     int spmv_sorted_cap = 16384;   // ... slot grid per block (16384: 1024 threads, 1 CTA/SM; 8192: 512 threads, 3 CTAs/SM)
     int spmv_sorted_pipe = 0;      // ... cap 12288: software-pipelined kernel (two product buffers, 1 CTA/SM)
-    int spmv_plan_tiled = 0;       // 1: CUDA-core plans use the column-tiled layout (spmv_tiled.cu; 0.30 ms vs CSR 0.28 ms on the BASELINE matrix)
     int spmv_plan_xpieces = 0;     // max x upload pieces (first = chunk 0's prefix); 0: one per chunk
     int spmv_plan_ygroups = 0;     // y download copies (groups of consecutive chunks); 0: one per chunk
     int spmv_plan_taper = 0;       // 1: half-size first/last pipeline chunks (measured no gain)
@@ -48,7 +47,6 @@ struct Tuning {
     int stencil_ctas_per_sm = 1;   // grid sizing target, TMA CUDA-core kernels
     int stencil_rows_per_thread = 0;   // 3D TMA CUDA-core kernels: 2, 4 or 8 (CTA = 64*16/this threads); 0 = per preset
     int stencil2d_rows_per_thread = 4; // 2D TMA CUDA-core kernel (swept: tools/sweep.py)
-    int stencil_t2_ctas_per_sm = 8;    // temporal-depth-2 2d5pt kernel (swept)
     int stencil_cc27x2 = 1;            // 3d27pt CC class weights: two columns per thread kernel
     int stencil_tc_concat = 1;         // 3d27pt TC one-plane: class products concatenated along K (10 DMMA/tile)
     int stencil3d_cc_stages = 4;       // 3D CUDA-core TMA ring depth (4, 6, 8)
@@ -68,8 +66,6 @@ struct Tuning {
     int stencil_r_ctas_per_sm = 32;
     int stencil_tb_waves = 4;          // register temporal blocking: grid = this many waves of resident warps
     int stencil_tb_tma = 4;            // 2d5pt depth >= this streams rows through a per-warp TMA ring (0: never; register queue)
-    int stencil_tb = 1;                // 1: temporal depth t >= 2 runs the register kernel (0: smem t=2 kernel)
-    int stencil_tb3_mode = 1;          // 3d7pt t >= 2: 1 register-blocked TMA kernel (stencil_tb3r.cu), 0 the z-column kernel
     int stencil_tb3_shape = 0;         // stencil_tb3r rows per warp x warps: 0/1 4x8, 2 2x16, 3 4x16 (t=2)
     int stencil_tb3_chunks = 0;        // z chunks per tile for stencil_tb3r (0: auto)
     int stencil_tb3_l2promo = 2;       // TMA L2 promotion of the stencil_tb3r boxes (0 none .. 3 256 B)
@@ -163,27 +159,9 @@ bool stencil_tb3r_supported(const StencilDesc& d, int t, const double* u, const 
 cudaError_t launch_stencil_tb3r(const StencilDesc& d, int t, uint64_t o0, uint64_t o1, const double* u, double* v,
                                 cudaStream_t s);
 
-// Two fused timesteps of 2d5pt (temporal blocking, CUDA core, TMA-eligible grids).
-cudaError_t launch_stencil_tma_t2(const StencilDesc& d, uint64_t o0, uint64_t o1, const double* u,
-                                  double* v, cudaStream_t s);
-
 // Dense GEMV y = A*x, row-major A (m x n).
 cudaError_t launch_gemv(int unit, uint64_t m, uint64_t n, const double* A, const double* x, double* y,
                         cudaStream_t s);
-
-// Column-tiled SpMV (rl_spmv_plan's layout for the CUDA core; spmv_tiled.cu).
-struct SpmvTile {
-    uint64_t seg_offset;  // byte offset of the tile's segment
-    int32_t col_base;     // first column (even)
-    int32_t width;        // columns in the x slice (even)
-    int32_t entries;
-    int32_t seg_bytes;    // multiple of 16
-};
-constexpr int kSpmvTiledRows = 8192;  // rows per tiled block
-void spmv_tiled_build(uint64_t m, uint64_t n, const int32_t* rp, const int32_t* col, const double* val,
-                      std::vector<uint8_t>& segs, std::vector<SpmvTile>& tiles, std::vector<int>& blk_tiles);
-cudaError_t launch_spmv_tiled(uint64_t m, const uint8_t* segs, const SpmvTile* tiles, const int* blk_tiles,
-                              uint64_t b0, uint64_t b1, const double* x, double* y, cudaStream_t s);
 
 // Column-sorted block layout (rl_spmv_plan's default CUDA-core layout when
 // eligible; spmv_sorted.cu).

@@ -362,97 +362,6 @@ __global__ void __launch_bounds__(32 * kTY / RYT) st3d_tma_cc27x2(const __grid_c
 }
 
 // ===========================================================================
-// CUDA core, 2d5pt, temporal depth 2 (SURVEY.md §8f "next" #1; PAPER.md:223-236,
-// reference stencil_model(shape, P, t) and min_temporal_depth).  A stage holds
-// rows y0-2 .. y0+17 (box 68 x 20); step 1 is computed into a shared-memory
-// tile for rows y0-1 .. y0+16 and columns x0-1 .. x0+64 (Dirichlet points
-// keep u), step 2 reads that tile and writes rows y0 .. y0+15.  HBM sees one
-// read of u and one write of v per two timesteps.
-// ===========================================================================
-constexpr int kBYT = kTY + 4;  // 20 staged rows
-__host__ __device__ constexpr int stage_doubles_tb(int bx) { return ((kBYT * bx * 8 + 127) / 128) * 128 / 8; }
-
-template <int S>
-__global__ void __launch_bounds__(256) st2d_tma_cc_t2(const __grid_constant__ CUtensorMap tm,
-                                                      double* __restrict__ v, uint64_t nx, uint64_t ny,
-                                                      uint64_t y_begin, uint64_t y_end, int seg_rows,
-                                                      int strips, StencilDesc d) {
-    constexpr int BX = kBX, STAGE = stage_doubles_tb(BX);
-    constexpr int WR = kTY + 2, WC = kTX + 2;  // intermediate tile: 18 x 66
-    extern __shared__ __align__(128) double smem[];
-    Ring<S, STAGE> ring(smem);
-    double* W = smem + S * STAGE + 2 * S;  // after the ring's 2*S barriers (8 B each)
-    const int tid = threadIdx.x, nthr = blockDim.x;
-    const int64_t x0 = (int64_t)(blockIdx.x % strips) * kTX;
-    const uint64_t ya = y_begin + (uint64_t)(blockIdx.x / strips) * seg_rows;
-    if (ya >= y_end) return;
-    const uint64_t yb = min(ya + (uint64_t)seg_rows, y_end);
-    const int nblk = (int)((yb - ya + kTY - 1) / kTY);
-    ring.init(nthr / 32);
-    auto issue = [&](int k) {
-        mbar_expect_tx(ring.full + (k % S), kBYT * BX * 8);
-        tma2d(ring.stage(k), &tm, ring.full + (k % S), (int)(x0 - kCofs), (int)(ya + (uint64_t)k * kTY) - 2);
-    };
-    if (tid == 0)
-        for (int k = 0; k < S && k < nblk; ++k) issue(k);
-    const double w0 = d.w[0], w1 = d.w[1], w2 = d.w[2], w3 = d.w[3], w4 = d.w[4];
-    for (int k = 0; k < nblk; ++k) {
-        ring.wait_full(k);
-        const double* T = ring.stage(k);
-        const int64_t yrow0 = (int64_t)(ya + (uint64_t)k * kTY);  // global row of output row 0
-        // step 1 into W: W[i][j] = w(y = yrow0 - 1 + i, x = x0 - 1 + j); stage row of y is
-        // y - yrow0 + 2, stage column of x is x - x0 + 2.  Thread (q, g): column q+1 of W,
-        // rows g, g+4, ...; threads q = 0 / 63 also do W columns 0 / 65.
-        const int q = tid & 63, g = tid >> 6;
-        auto w_at = [&](int i, int j) {
-            const int64_t y = yrow0 - 1 + i, x = x0 - 1 + j;
-            const int sr = i + 1, sc = j + 1;
-            const double c = T[sr * BX + sc];
-            if (y <= 0 || y >= (int64_t)ny - 1 || x <= 0 || x >= (int64_t)nx - 1) return c;  // Dirichlet
-            double a = w0 * c;
-            a = fma(w1, T[(sr - 1) * BX + sc], a);
-            a = fma(w2, T[(sr + 1) * BX + sc], a);
-            a = fma(w3, T[sr * BX + sc - 1], a);
-            a = fma(w4, T[sr * BX + sc + 1], a);
-            return a;
-        };
-#pragma unroll
-        for (int i = g; i < WR; i += 4) {
-            W[i * WC + q + 1] = w_at(i, q + 1);
-            if (q == 0) W[i * WC] = w_at(i, 0);
-            if (q == 63) W[i * WC + WC - 1] = w_at(i, WC - 1);
-        }
-        ring.release(k);
-        __syncthreads();  // W complete
-        if (tid == 0 && k + S < nblk) {
-            ring.wait_empty(k);
-            issue(k + S);
-        }
-        // step 2: thread (q, g) writes rows 4g .. 4g+3 of column x0 + q
-        {
-            const int64_t x = x0 + q;
-            const int j = q + 1;
-            double cp = W[(4 * g) * WC + j], c = W[(4 * g + 1) * WC + j];
-#pragma unroll
-            for (int rr = 0; rr < 4; ++rr) {
-                const int i = 4 * g + rr + 1;
-                const double cn = W[(i + 1) * WC + j];
-                double a = w0 * c;
-                a = fma(w1, cp, a);
-                a = fma(w2, cn, a);
-                a = fma(w3, W[i * WC + j - 1], a);
-                a = fma(w4, W[i * WC + j + 1], a);
-                const uint64_t y = (uint64_t)(yrow0 + 4 * g + rr);
-                if (y < yb && x >= 1 && x <= (int64_t)nx - 2) v[y * nx + x] = a;
-                cp = c;
-                c = cn;
-            }
-        }
-        __syncthreads();  // W is rewritten by the next stage
-    }
-}
-
-// ===========================================================================
 // Tensor core, 2d5pt: 16 8x8 tiles per stage; warp w -> row block w>>1,
 // column blocks 4*(w&1) .. +3.
 // ===========================================================================
@@ -1257,32 +1166,6 @@ bool encode_map_3d(void* map, const double* base, uint64_t nx, uint64_t ny, uint
     return fn(static_cast<CUtensorMap*>(map), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), gdim,
               gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
               promo[l2_promotion & 3], CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-cudaError_t launch_stencil_tma_t2(const StencilDesc& d, uint64_t o0, uint64_t o1, const double* u,
-                                  double* v, cudaStream_t s) {
-    auto fn = encode_fn();
-    if (!fn) return cudaErrorNotSupported;
-    CUtensorMap m;
-    cuuint64_t gdim[2] = {d.nx, d.ny};
-    cuuint64_t gstride[1] = {d.nx * 8};
-    cuuint32_t box[2] = {(cuuint32_t)kBX, (cuuint32_t)kBYT};
-    cuuint32_t estride[2] = {1, 1};
-    if (fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(u), gdim, gstride, box, estride,
-           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        return cudaErrorInvalidValue;
-    constexpr int S = 4;
-    const int strips = (int)((d.nx + kTX - 1) / kTX);
-    const int nseg = split_count(strips, o1 - o0, 64, tuning().stencil_t2_ctas_per_sm);
-    const int seg_rows = (int)(((o1 - o0 + nseg - 1) / nseg + kTY - 1) / kTY * kTY);
-    const int segs = (int)((o1 - o0 + seg_rows - 1) / seg_rows);
-    const size_t sm = (size_t)S * stage_doubles_tb(kBX) * 8 + 2 * S * 8 + (kTY + 2) * (kTX + 2) * 8;
-    cudaError_t e;
-    if ((e = prep(st2d_tma_cc_t2<S>, sm)) != cudaSuccess) return e;
-    st2d_tma_cc_t2<S><<<(unsigned)(strips * segs), 256, sm, s>>>(m, v, d.nx, d.ny, o0, o1, seg_rows, strips, d);
-    note_launch();
-    return cudaGetLastError();
 }
 
 bool stencil_tma_eligible(const StencilDesc& d, const double* u, const double* v) {

@@ -3,6 +3,9 @@ import sys
 
 import pytest
 
+# the tests sweep kernel variants through rl_tuning_set's developer keys
+os.environ.setdefault("RL_DEV_TUNING", "1")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

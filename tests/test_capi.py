@@ -80,15 +80,42 @@ def test_no_cpu_fallback_without_gpu():
 
 
 def test_every_documented_tuning_key_is_settable():
-    """INTEGRATION.md's tuning table lists exactly the keys rl_tuning_set
-    accepts; setting one returns the previous value (restored here)."""
+    """INTEGRATION.md's two tuning tables (product keys, developer keys) list
+    exactly the keys rl_tuning_set accepts; setting one returns the previous
+    value (restored here)."""
     import re
 
     text = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "INTEGRATION.md")).read()
-    table = text[text.index("| family | keys |"):]
-    table = table[:table.index("\n\n")]
-    keys = re.findall(r"`([a-z0-9_]+)`", table)
-    assert len(keys) >= 40
+    keys = []
+    for head in ("| product key | selects |", "| family | keys |"):
+        table = text[text.index(head):]
+        end = table.find("\n\n")
+        table = table if end < 0 else table[:end]
+        keys += [k for row in table.splitlines()[2:] for k in re.findall(r"`([a-z0-9_]+)`", row.split("|")[1 if head.startswith("| product") else 2])]
+    assert len(keys) >= 50 and len(set(keys)) == len(keys)
     for k in keys:
         prev = P.tuning_set(k, 1)
         assert P.tuning_set(k, prev) == 1, k
+    src = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                            "paper_2502_16851_b200", "csrc", "capi.cpp")).read()
+    accepted = set(re.findall(r'\{"([a-z0-9_]+)", &rlb::Tuning::', src))
+    assert accepted == set(keys)
+
+
+def test_developer_tuning_keys_need_the_opt_in():
+    """Without RL_DEV_TUNING=1 only the product keys are settable; launch-shape
+    sweep knobs are refused with ValidationError (fresh process: the opt-in is
+    read once)."""
+    import subprocess
+    import sys
+
+    code = ("import paper_2502_16851_b200 as P\n"
+            "P.tuning_set('stencil_tc3d_hybrid', 1)\n"
+            "P.tuning_set('dist_graph', 1)\n"
+            "try:\n    P.tuning_set('spmv_threads', 512)\nexcept P.RooflensError as e:\n"
+            "    print(e.kind, 'developer sweep key' in str(e))\n")
+    env = {k: v for k, v in os.environ.items() if k != "RL_DEV_TUNING"}
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                         check=True).stdout.split()
+    assert out == ["ValidationError", "True"]

@@ -69,23 +69,12 @@ def test_stencil_host(cuda, unit, preset, shape, steps):
     assert kc.traffic_bytes == 16 * int(np.prod([s - 2 for s in shape])) * steps
 
 
-@pytest.fixture
-def tiled_plans():
-    """The column-tiled plan layout is opt-in (tuning key spmv_plan_tiled)."""
-    P.tuning_set("spmv_plan_tiled", 1)
-    yield
-    P.tuning_set("spmv_plan_tiled", 0)
-
-
-def _plan_check(torch, rp, col, val, ncols, unit, expect_tiled):
-    """expect_tiled: True / False (tiled or not), or a layout name."""
+def _plan_check(torch, rp, col, val, ncols, unit, expect_layout):
+    """expect_layout: the plan's layout name ("csr", "sorted", "chunked")."""
     x = np.random.default_rng(5).uniform(-1, 1, ncols)
     ref = O.spmv_csr(rp, col, val, x)
     plan = P.SpmvPlan(rp, col, val, ncols, unit=unit)
-    if isinstance(expect_tiled, str):
-        assert plan.layout() == expect_tiled
-    else:
-        assert plan.info()[0] == expect_tiled
+    assert plan.layout() == expect_layout
     y = np.full(rp.size - 1, np.nan)
     plan.execute_host(x, y)
     assert O.rel_err(y, ref) <= 1e-12
@@ -176,18 +165,10 @@ def test_sorted_plan_ragged_and_fallbacks(cuda, sorted_plans):
     _plan_check(torch, rp, col, val, n, P.CUDA_CORE, "csr" if span >= 1 << 18 else "sorted")
 
 
-@pytest.mark.parametrize("m,n,k,hb", [(8192 * 3 + 17, 8192 * 3 + 18, 16, 65536), (100000, 100000, 16, 65536),
-                                      (50000, 50000, 7, 300), (20000, 20000, 40, 20000)])
-def test_tiled_plan_banded(cuda, tiled_plans, m, n, k, hb):
-    import torch
-
-    rp, col, val = O.gen_band_csr(m, 0, n, k, hb, 31)
-    _plan_check(torch, rp, col, val, n, P.CUDA_CORE, n % 2 == 0)
-
-
-def test_tiled_plan_ragged_dense_and_empty(cuda, tiled_plans):
-    """Empty rows, rows denser than a tile segment (forces tile splitting),
-    a rectangular matrix and an odd column count (CSR fallback)."""
+@pytest.mark.parametrize("unit", UNITS)
+def test_plan_ragged_dense_and_empty(cuda, unit):
+    """Empty rows, very dense rows, a rectangular matrix and an odd column
+    count through the default (CSR) plan layout."""
     import torch
 
     rng = np.random.default_rng(11)
@@ -199,19 +180,18 @@ def test_tiled_plan_ragged_dense_and_empty(cuda, tiled_plans):
     rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
     col = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(np.int32)
     val = rng.uniform(-1, 1, rp[-1])
-    _plan_check(torch, rp, col, val, n, P.CUDA_CORE, True)
-    _plan_check(torch, rp, col, val, n + 1, P.CUDA_CORE, False)   # odd n -> CSR kernel
-    _plan_check(torch, rp, col, val, n, P.TENSOR_CORE, False)     # TC plans keep CSR
+    _plan_check(torch, rp, col, val, n, unit, "csr")
+    _plan_check(torch, rp, col, val, n + 1, unit, "csr")
 
 
-@pytest.mark.parametrize("tiled", [0, 1])
-def test_plan_graph_replay_pinned(cuda, tiled):
+@pytest.mark.parametrize("chunked", [0, 1])
+def test_plan_graph_replay_pinned(cuda, chunked):
     """Pinned x/y: execute_host runs as a captured CUDA graph.  New x
     contents are picked up on replay, a new (x, y) pair re-captures, and the
     launch counter advances per replay."""
     import torch
 
-    P.tuning_set("spmv_plan_tiled", tiled)
+    P.tuning_set("spmv_plan_chunked", chunked)
     try:
         m = n = 70000
         rp, col, val = O.gen_band_csr(m, 0, n, 12, 9000, 17)
@@ -229,7 +209,7 @@ def test_plan_graph_replay_pinned(cuda, tiled):
                 assert O.rel_err(ys[j].numpy(), ref) <= 1e-12
         plan.close()
     finally:
-        P.tuning_set("spmv_plan_tiled", 0)
+        P.tuning_set("spmv_plan_chunked", 0)
 
 
 def test_plan_with_long_rows_pinned(cuda):

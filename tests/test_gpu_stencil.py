@@ -251,46 +251,37 @@ def test_2d5pt_temporal_depth2(cuda, shape, steps):
 
 @pytest.mark.parametrize("t", [2, 3, 4, 5, 6, 7, 8])
 @pytest.mark.parametrize("shape", [(20, 24), (65, 130), (301, 517), (513, 1026)])
-@pytest.mark.parametrize("kernel", [0, 1])
-def test_2d5pt_temporal_depth_t(cuda, t, shape, kernel):
-    """Temporal depth t (register kernel; kernel 0 = the smem t = 2 kernel
-    where it applies) equals t * k single timesteps, with custom weights,
-    odd and even nx (odd depths only run the scalar-load path), and an
-    untouched Dirichlet ring."""
+def test_2d5pt_temporal_depth_t(cuda, t, shape):
+    """Temporal depth t (register kernel, stencil_tb.cu) equals t * k single
+    timesteps, with custom weights, odd and even nx (odd depths only run the
+    scalar-load path), and an untouched Dirichlet ring."""
     import torch
 
-    if kernel == 0 and (t != 2 or shape[1] % 2):
-        pytest.skip("the shared-memory kernel is t = 2 with even nx only")
     if t % 2 == 0 and shape[1] % 2:
         pytest.skip("even depths need 16-byte rows")
-    P.tuning_set("stencil_tb", kernel)
-    try:
-        u0 = O.stencil_init(shape, 1, 23)
-        w = np.array([0.4, 0.2, 0.1, 0.17, 0.13])
-        steps = 2 * t + 1
-        u = torch.from_numpy(u0.copy()).cuda()
-        v = torch.from_numpy(u0.copy()).cuda()
-        kc, out = P.stencil_temporal("2d5pt", u, v, steps, t, weights=w)
-        torch.cuda.synchronize()
-        ref = O.stencil("2d5pt", u0, steps, w)
-        got = out.cpu().numpy()
-        assert O.rel_err(got, ref) <= TOL
-        ring = _ring_mask(shape, 1)
-        assert O.bit_mismatches(got[ring], u0[ring]) == 0
-        pts = (shape[0] - 2) * (shape[1] - 2)
-        assert kc.traffic_bytes == 16 * pts * 3  # 2 fused sweeps + 1 single step
-    finally:
-        P.tuning_set("stencil_tb", 1)
+    u0 = O.stencil_init(shape, 1, 23)
+    w = np.array([0.4, 0.2, 0.1, 0.17, 0.13])
+    steps = 2 * t + 1
+    u = torch.from_numpy(u0.copy()).cuda()
+    v = torch.from_numpy(u0.copy()).cuda()
+    kc, out = P.stencil_temporal("2d5pt", u, v, steps, t, weights=w)
+    torch.cuda.synchronize()
+    ref = O.stencil("2d5pt", u0, steps, w)
+    got = out.cpu().numpy()
+    assert O.rel_err(got, ref) <= TOL
+    ring = _ring_mask(shape, 1)
+    assert O.bit_mismatches(got[ring], u0[ring]) == 0
+    pts = (shape[0] - 2) * (shape[1] - 2)
+    assert kc.traffic_bytes == 16 * pts * 3  # 2 fused sweeps + 1 single step
 
 
-@pytest.mark.parametrize("mode", [1, 0])
 @pytest.mark.parametrize("t", [2, 3, 4])
 @pytest.mark.parametrize("shape", [(9, 10, 11), (20, 24, 68), (33, 40, 70), (64, 50, 97), (37, 130, 126),
                                    (70, 29, 200)])
-def test_3d7pt_temporal_depth_t(cuda, mode, t, shape):
+def test_3d7pt_temporal_depth_t(cuda, t, shape):
     """3d7pt temporal depth t equals single timesteps; custom weights; the
-    Dirichlet shell stays bit-exact.  mode 1: the register-blocked TMA kernel
-    (stencil_tb3r.cu; odd nx falls back), mode 0: the z-column kernel."""
+    Dirichlet shell stays bit-exact.  Even nx: the register-blocked TMA kernel
+    (stencil_tb3r.cu); odd nx: the z-column kernel (stencil_tb3.cu)."""
     import torch
 
     u0 = O.stencil_init(shape, 1, 29)
@@ -298,12 +289,8 @@ def test_3d7pt_temporal_depth_t(cuda, mode, t, shape):
     steps = 2 * t + 1
     u = torch.from_numpy(u0.copy()).cuda()
     v = torch.from_numpy(u0.copy()).cuda()
-    P.tuning_set("stencil_tb3_mode", mode)
-    try:
-        kc, out = P.stencil_temporal("3d7pt", u, v, steps, t, weights=w)
-        torch.cuda.synchronize()
-    finally:
-        P.tuning_set("stencil_tb3_mode", 1)
+    kc, out = P.stencil_temporal("3d7pt", u, v, steps, t, weights=w)
+    torch.cuda.synchronize()
     got = out.cpu().numpy()
     assert O.rel_err(got, O.stencil("3d7pt", u0, steps, w)) <= TOL
     ring = _ring_mask(shape, 1)

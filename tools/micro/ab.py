@@ -4,6 +4,8 @@ back-to-back sweeps see on this box): for each round, every variant runs one
 
 python tools/micro/ab.py 3d27pt tc "stencil_tc3d_hybrid=1" "stencil_tc3d_hybrid=0" ...
 (a variant "cc" runs the CUDA-core unit with default tuning)"""
+import os
+os.environ.setdefault("RL_DEV_TUNING", "1")  # sweep knobs (rl_tuning_set developer keys)
 import math
 import os
 import statistics

@@ -1,4 +1,6 @@
 """Device-side time of the tiled plan kernel vs the CSR kernel (BASELINE matrix)."""
+import os
+os.environ.setdefault("RL_DEV_TUNING", "1")  # sweep knobs (rl_tuning_set developer keys)
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch

@@ -1,4 +1,6 @@
 """rl_spmv_plan_execute_host timing vs chunk count / zero-copy (BASELINE matrix)."""
+import os
+os.environ.setdefault("RL_DEV_TUNING", "1")  # sweep knobs (rl_tuning_set developer keys)
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch

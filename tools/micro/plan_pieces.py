@@ -2,6 +2,8 @@
 call vs row chunks, x upload pieces and y copy groups; checks y each config.
 python tools/micro/plan_pieces.py "chunks,xpieces,ygroups" ..."""
 import os
+os.environ.setdefault("RL_DEV_TUNING", "1")  # sweep knobs (rl_tuning_set developer keys)
+import os
 import sys
 import time
 

@@ -1,6 +1,8 @@
 """One traced rl_spmv_plan_execute_host call per chunk count (RL_PLAN_TRACE=1
 prints event times in us: x pieces on s_in, chunk begin/end on s_cmp, y
 chunks on s_out) plus the steady-state time of 20 calls."""
+import os
+os.environ.setdefault("RL_DEV_TUNING", "1")  # sweep knobs (rl_tuning_set developer keys)
 import os, sys, time
 if os.environ.get("TRACE", "1") == "1":
     os.environ["RL_PLAN_TRACE"] = "1"

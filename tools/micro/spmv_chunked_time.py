@@ -1,5 +1,7 @@
 """K16 (column-chunked plan layout) vs the CSR kernel on the BASELINE matrix:
 correctness against the CSR kernel and device time per call."""
+import os
+os.environ.setdefault("RL_DEV_TUNING", "1")  # sweep knobs (rl_tuning_set developer keys)
 import sys
 import time
 

@@ -1,6 +1,8 @@
 """SpMV on skewed row-length matrices (power-law, a few dense rows) vs
 cuSPARSE via torch: checks the CSR kernels' load balance beyond the
 uniform BASELINE matrix."""
+import os
+os.environ.setdefault("RL_DEV_TUNING", "1")  # sweep knobs (rl_tuning_set developer keys)
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np

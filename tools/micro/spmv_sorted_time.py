@@ -1,6 +1,8 @@
 """BASELINE SpMV: CSR kernel (rl_spmv_csr) vs the plan's column-sorted block
 layout (rl_spmv_plan_execute, device x/y), interleaved; checks both."""
 import os
+os.environ.setdefault("RL_DEV_TUNING", "1")  # sweep knobs (rl_tuning_set developer keys)
+import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))

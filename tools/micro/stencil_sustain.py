@@ -3,6 +3,8 @@ power sampled by NVML, to separate kernel cost from power-cap throttling.
 
 python tools/micro/stencil_sustain.py 3d27pt tc [key=val ...] (steps=200)"""
 import os
+os.environ.setdefault("RL_DEV_TUNING", "1")  # sweep knobs (rl_tuning_set developer keys)
+import os
 import sys
 import threading
 import time

@@ -1,3 +1,5 @@
+import os
+os.environ.setdefault("RL_DEV_TUNING", "1")  # sweep knobs (rl_tuning_set developer keys)
 import os, sys
 sys.path.insert(0, ".")
 import torch

@@ -1,5 +1,7 @@
 """ms per timestep of 3d7pt temporal blocking at 512^3 for each (t, shape):
 python tools/micro/tb3_time.py [t,...] [shape,...]"""
+import os
+os.environ.setdefault("RL_DEV_TUNING", "1")  # sweep knobs (rl_tuning_set developer keys)
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch

@@ -2,8 +2,10 @@
 
   python tools/prof_kernels.py [names...]   names: stream_cc stream_tc spmv_cc spmv_tc
         2d5pt_cc 2d5pt_tc 3d7pt_cc 3d7pt_tc 3d27pt_cc 3d27pt_tc (default: all);
-        also 2d9pt_* 2d13pt_* 2d49pt_* gemv_* spmvtiled_cc
+        also 2d9pt_* 2d13pt_* 2d49pt_* gemv_* spmvchunked_cc
 """
+import os
+os.environ.setdefault("RL_DEV_TUNING", "1")  # sweep knobs (rl_tuning_set developer keys)
 import os
 import sys
 
@@ -45,7 +47,7 @@ def run(name):
         y = torch.empty(m, dtype=torch.float64, device="cuda")
         for _ in range(REPS):
             P.gemv(A, x, y, unit=unit)
-    elif kern == "spmvtiled":
+    elif kern == "spmvchunked":
         n, k, hb = 1 << 22, 16, 65536
         rp = torch.empty(n + 1, dtype=torch.int32, device="cuda")
         col = torch.empty(n * k, dtype=torch.int32, device="cuda")
@@ -54,7 +56,7 @@ def run(name):
         y = torch.empty(n, dtype=torch.float64, device="cuda")
         P.gen_band_csr(n, 0, n, k, hb, 1, rp, col, val)
         P.fill_uniform(x, 1, 4, 0, 1)
-        P.tuning_set("spmv_plan_tiled", 1)
+        P.tuning_set("spmv_plan_chunked", 1)
         plan = P.SpmvPlan(rp.cpu(), col.cpu(), val.cpu(), n)
         for _ in range(REPS):
             plan.execute(x, y)

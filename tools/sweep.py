@@ -1,5 +1,7 @@
 """Tuning sweeps over the rl_tuning_set knobs (CUDA-event timing, GB/s of
 algorithmic bytes).  python tools/sweep.py stream|spmv|... > out.jsonl"""
+import os
+os.environ.setdefault("RL_DEV_TUNING", "1")  # sweep knobs (rl_tuning_set developer keys)
 import itertools
 import json
 import os
@@ -76,26 +78,15 @@ def gemv():
         sweep(f"gemv_{'cc' if unit == 0 else 'tc'}", lambda: P.gemv(A, x, y, unit=unit), nbytes, {})
 
 
-def temporal():
-    import math
-    u = torch.empty((16384, 16384), dtype=torch.float64, device="cuda")
-    P.stencil_init(u, 1, 1)
-    v = u.clone()
-    nbytes = 16 * math.prod(s - 2 for s in u.shape)  # per fused sweep (t = 2)
-    sweep("2d5pt_t2", lambda: P.stencil_temporal("2d5pt", u, v, 2, 2), nbytes,
-          {"stencil_t2_ctas_per_sm": [8, 12, 16, 24, 32, 48]})
-
-
 def temporal_t():
     """2d5pt at 16384^2: ms per timestep for temporal depth 1..8 (register
-    kernel), plus the shared-memory t = 2 kernel."""
+    kernel)."""
     u = torch.empty((16384, 16384), dtype=torch.float64, device="cuda")
     P.stencil_init(u, 1, 1)
     v = u.clone()
     waves_list = [int(x) for x in os.environ.get("TB_WAVES", "1").split(",")]
-    cases = [(1, 1, 1), (2, 0, 1)] + [(t, 1, w) for t in range(2, 9) for w in waves_list]
+    cases = [(1, 1, 1)] + [(t, 1, w) for t in range(2, 9) for w in waves_list]
     for t, tb, waves in cases:
-        P.tuning_set("stencil_tb", tb)
         P.tuning_set("stencil_tb_waves", waves)
         steps = 8 * t
         fn = (lambda: P.stencil("2d5pt", u, v, steps)) if t == 1 else \
@@ -104,16 +95,15 @@ def temporal_t():
         print(json.dumps({"kernel": "2d5pt_temporal", "t": t, "register_kernel": tb, "waves": waves,
                           "ms_per_timestep": round(ms, 4),
                           "timestep_gbs_equiv": round(16 * 16382 ** 2 / ms / 1e6, 1)}), flush=True)
-    P.tuning_set("stencil_tb", 1)
 
 
 def temporal_3d():
-    """3d7pt at 512^3: ms per timestep for temporal depth 1..4, both 3D
-    temporal kernels (TB3_MODES), z-chunk counts from TB3_CHUNKS (0 = auto)."""
+    """3d7pt at 512^3: ms per timestep for temporal depth 1..4 (register-blocked
+    kernel), z-chunk counts from TB3_CHUNKS (0 = auto)."""
     u = torch.empty((512, 512, 512), dtype=torch.float64, device="cuda")
     P.stencil_init(u, 1, 1)
     v = u.clone()
-    modes = [int(x) for x in os.environ.get("TB3_MODES", "1,0").split(",")]
+    modes = [1]
     chunks = [int(x) for x in os.environ.get("TB3_CHUNKS", "0").split(",")]
     shapes = [int(x) for x in os.environ.get("TB3_SHAPES", "0").split(",")]
     for t in (1, 2, 3, 4):
@@ -121,7 +111,6 @@ def temporal_3d():
           for shp in (shapes if t > 1 and mode == 1 else [0]):
             for ch in (chunks if t > 1 and mode == 1 else [0]):
                 P.tuning_set("stencil_tb3_shape", shp)
-                P.tuning_set("stencil_tb3_mode", mode)
                 P.tuning_set("stencil_tb3_chunks", ch)
                 steps = 4 * t
                 fn = (lambda: P.stencil("3d7pt", u, v, steps)) if t == 1 else \
@@ -130,7 +119,6 @@ def temporal_3d():
                 print(json.dumps({"kernel": "3d7pt_temporal", "t": t, "mode": mode, "shape": shp, "chunks": ch,
                                   "ms_per_timestep": round(ms, 4),
                                   "timestep_gbs_equiv": round(16 * 510 ** 3 / ms / 1e6, 1)}), flush=True)
-    P.tuning_set("stencil_tb3_mode", 1)
     P.tuning_set("stencil_tb3_chunks", 0)
     P.tuning_set("stencil_tb3_shape", 0)
 
@@ -249,8 +237,6 @@ if __name__ == "__main__":
             stencil3d_tc()
         elif w == "stencil":
             stencils()
-        elif w == "temporal":
-            temporal()
         elif w == "temporal_t":
             temporal_t()
         elif w == "temporal_3d":
