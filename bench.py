@@ -1084,6 +1084,11 @@ def main():
         line["fp64_peaks_tflops"] = peaks
         line["fp64_peaks_tflops_runs"] = peaks_runs
         line["bounds"] = bounds
+        # the measured B200 as a reference-schema spec document (serialize_spec,
+        # hardware.cpp:249-264); profiles/B200-measured.json is this object
+        spec = P.HardwareSpec("B200-measured", hbm * 1e9, 126e6, peaks["cuda_core"] * 1e12,
+                              peaks["tensor_core"] * 1e12)
+        line["hardware_spec"] = json.loads(P.serialize_spec(spec))
         line["per_kernel_clocks"] = clk2.summary()
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.workload)

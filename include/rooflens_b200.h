@@ -302,6 +302,51 @@ RL_API int rl_workload_ceiling(double intensity, double balance, double* out);
 RL_API int rl_min_temporal_depth(double balance, double single_step_intensity, uint64_t* out);
 RL_API int rl_tc_scale_trick_throughput(double peak_tc, uint64_t m, uint64_t n, double* out);
 
+/* SpeedupBound as a reportable object (bounds.hpp:27-45): value, BoundKind
+ * ordinal (bounds.hpp:27-32: 0 exact un-overlapped, 1 kernel ceiling, 2
+ * tensor-core ceiling, 3 workload ceiling) and the reference's assumption and
+ * warning strings (bounds.cpp:64-108).  `text` receives the n_assumptions
+ * assumption lines then the n_warnings warning lines, each '\n'-terminated,
+ * NUL-terminated; *length (optional) gets the full length without the NUL; a
+ * null `text` only sizes; a short buffer is InvalidRange. */
+typedef struct {
+    double value;
+    int kind;
+    int n_assumptions;
+    int n_warnings;
+} rl_speedup_bound;
+/* to_string(BoundKind) (bounds.cpp:27-35); "?" for an unknown ordinal. */
+RL_API const char* rl_bound_kind_name(int kind);
+/* unoverlapped_bound (bounds.cpp:64-70). */
+RL_API int rl_unoverlapped_bound(double t_cmp, double t_mem, double t_others, double alpha,
+                                 rl_speedup_bound* out, char* text, uint64_t capacity, uint64_t* length);
+/* kernel_speedup_ceiling (bounds.cpp:72-85), with its I >= B warning text. */
+RL_API int rl_kernel_ceiling_bound(double alpha, double balance, double intensity, rl_speedup_bound* out,
+                                   char* text, uint64_t capacity, uint64_t* length);
+/* tensor_core_ceiling (bounds.cpp:87-96). */
+RL_API int rl_tensor_core_bound(double alpha, rl_speedup_bound* out, char* text, uint64_t capacity,
+                                uint64_t* length);
+/* workload_ceiling (bounds.cpp:98-108). */
+RL_API int rl_workload_bound(double intensity, double balance, rl_speedup_bound* out, char* text,
+                             uint64_t capacity, uint64_t* length);
+
+/* rooflens::build_analysis + render_text / render_json / render_csv
+ * (report.hpp:19-48; the reference declares them without an implementation,
+ * the behaviour follows SPEC.md cli_report): classification against the
+ * CUDA-core balance at `precision` (or *balance_override when non-null), the
+ * kernel / tensor-core / workload ceilings, the temporal-depth section when
+ * single_step_intensity is non-null, notes and the verdict ("tensor cores
+ * cannot exceed X× on this kernel/machine", X = min bound to 3 significant
+ * digits).  Text uses 4 significant digits; json / csv full precision.
+ * Buffer convention as rl_serialize_spec. */
+#define RL_REPORT_TEXT 0
+#define RL_REPORT_JSON 1
+#define RL_REPORT_CSV 2
+RL_API int rl_analysis_render(const rl_hw_spec* spec, rl_precision precision, const char* kernel_name,
+                              uint64_t work_flops, uint64_t traffic_bytes, const double* balance_override,
+                              const double* single_step_intensity, int format, char* buffer,
+                              uint64_t capacity, uint64_t* length);
+
 /* ---------------------------------------------------------------------------
  * Multi-GPU (north_star): one process per GPU, NCCL
  * point-to-point over NVLink/NVSwitch, the kernels above as per-part compute.

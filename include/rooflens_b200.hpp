@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cstdint>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <string_view>
@@ -154,5 +155,46 @@ double tensor_core_ceiling(double alpha);
 double workload_ceiling(double intensity, double balance);
 std::uint64_t min_temporal_depth(double balance, double single_step_intensity);
 double tc_scale_trick_throughput(double peak_tc, std::uint64_t m, std::uint64_t n);
+
+// Bounds as reportable objects (bounds.hpp:27-45, bounds.cpp:64-108): the
+// value plus the assumption and warning strings the reference attaches.
+enum class BoundKind { ExactUnoverlapped, KernelCeiling, TensorCoreCeiling, WorkloadCeiling };
+const char* to_string(BoundKind kind);  // bounds.cpp:27-35
+struct SpeedupBound {
+    double value = 1.0;
+    BoundKind kind = BoundKind::ExactUnoverlapped;
+    std::vector<std::string> assumptions;
+    std::vector<std::string> warnings;
+};
+SpeedupBound unoverlapped_bound(double t_cmp, double t_mem, double t_others, double alpha);
+SpeedupBound kernel_ceiling_bound(double alpha, double balance, double intensity);
+SpeedupBound tensor_core_bound(double alpha);
+SpeedupBound workload_bound(double intensity, double balance);
+
+// Analysis report (report.hpp:19-48; declared by the reference, implemented
+// here from SPEC.md cli_report): classification, every applicable ceiling,
+// the temporal-depth section for stencils, and the one-line verdict.
+struct AnalysisReport {
+    HardwareSpec machine;
+    Precision precision = Precision::FP64;
+    double balance = 0.0;
+    bool balance_overridden = false;
+    std::optional<double> alpha;  // absent when the spec has no tensor-core peak at `precision`
+    KernelCharacterization kernel;
+    Boundedness boundedness = Boundedness::MemoryBound;
+    double attainable_flops = 0.0;  // CUDA-core roofline at the kernel's intensity
+    std::vector<SpeedupBound> bounds;
+    std::optional<double> single_step_intensity;
+    std::optional<std::uint64_t> min_depth;
+    std::vector<std::string> notes;
+    std::string verdict;
+};
+AnalysisReport build_analysis(const HardwareSpec& spec, Precision precision,
+                              const KernelCharacterization& kernel,
+                              std::optional<double> balance_override = {},
+                              std::optional<double> single_step_intensity = {});
+std::string render_text(const AnalysisReport& report);  // 4 significant digits
+std::string render_json(const AnalysisReport& report);  // full precision
+std::string render_csv(const AnalysisReport& report);   // full precision
 
 }  // namespace rooflens::b200

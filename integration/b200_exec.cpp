@@ -5,10 +5,13 @@
 // (hardware.hpp:19-21) have rl_unit / rl_precision's ordinals.
 #include "b200_exec.hpp"
 
+#include <cstring>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "rooflens/error.hpp"
+#include "rooflens/report.hpp"
 #include "rooflens_b200.h"
 
 namespace rooflens {
@@ -80,5 +83,131 @@ KernelCharacterization dist_scale(const B200Comm& comm, ExecutionUnit unit, Prec
     check(rl_dist_scale(static_cast<rl_dist>(comm.handle()), U(unit), Pr(precision), a, b, q, n_global, stream, &k));
     return kc("scale", k);
 }
+
+// ---------------------------------------------------------------------------
+// report.hpp:40-48.  The reference declares build_analysis / render_* without
+// defining them; librooflens_b200.so implements them (csrc/report.cpp) and
+// this adapter supplies the reference's symbols over it.
+// ---------------------------------------------------------------------------
+namespace {
+
+rl_hw_spec c_spec(const HardwareSpec& h) {
+    rl_hw_spec s{};
+    std::strncpy(s.name, h.name.c_str(), sizeof s.name - 1);
+    s.memory_bandwidth = h.memory_bandwidth;
+    s.l2_cache_bytes = h.l2_cache_bytes;
+    for (const auto& [key, peak] : h.peaks)
+        s.peaks[static_cast<int>(key.first)][static_cast<int>(key.second)] = peak;
+    return s;
+}
+
+template <class F>
+SpeedupBound bound_of(F&& call) {
+    rl_speedup_bound b{};
+    uint64_t n = 0;
+    check(call(&b, nullptr, 0, &n));
+    std::string text(n + 1, '\0');
+    check(call(&b, text.data(), n + 1, nullptr));
+    SpeedupBound r;
+    r.value = b.value;
+    r.kind = static_cast<BoundKind>(b.kind);
+    std::size_t at = 0;
+    for (int i = 0; i < b.n_assumptions + b.n_warnings; ++i) {
+        const std::size_t nl = text.find('\n', at);
+        (i < b.n_assumptions ? r.assumptions : r.warnings).push_back(text.substr(at, nl - at));
+        at = nl + 1;
+    }
+    return r;
+}
+
+std::string render(const AnalysisReport& r, int format) {
+    const rl_hw_spec s = c_spec(r.machine);
+    const double* bo = r.balance_overridden ? &r.balance : nullptr;
+    const double* si = r.single_step_intensity ? &*r.single_step_intensity : nullptr;
+    uint64_t n = 0;
+    auto call = [&](char* buf, uint64_t cap, uint64_t* len) {
+        return rl_analysis_render(&s, Pr(r.precision), r.kernel.kernel_name.c_str(), r.kernel.work_flops,
+                                  r.kernel.traffic_bytes, bo, si, format, buf, cap, len);
+    };
+    check(call(nullptr, 0, &n));
+    std::string out(n + 1, '\0');
+    check(call(out.data(), n + 1, nullptr));
+    out.resize(n);
+    return out;
+}
+
+// (field, value) rows of the csv encoding (RFC-4180 quoting).
+std::vector<std::pair<std::string, std::string>> csv_rows(const std::string& text) {
+    std::vector<std::pair<std::string, std::string>> rows;
+    std::vector<std::string> cells;
+    std::string cell;
+    bool quoted = false;
+    for (std::size_t i = 0; i < text.size(); ++i) {
+        const char c = text[i];
+        if (quoted) {
+            if (c == '"' && i + 1 < text.size() && text[i + 1] == '"') cell += '"', ++i;
+            else if (c == '"') quoted = false;
+            else cell += c;
+        } else if (c == '"') {
+            quoted = true;
+        } else if (c == ',') {
+            cells.push_back(cell), cell.clear();
+        } else if (c == '\n') {
+            cells.push_back(cell), cell.clear();
+            if (cells.size() == 2) rows.emplace_back(cells[0], cells[1]);
+            cells.clear();
+        } else {
+            cell += c;
+        }
+    }
+    return rows;
+}
+
+}  // namespace
+
+AnalysisReport build_analysis(const HardwareSpec& spec, Precision precision, const KernelCharacterization& kernel,
+                              std::optional<double> balance_override, std::optional<double> single_step_intensity) {
+    const rl_hw_spec s = c_spec(spec);
+    AnalysisReport r;
+    r.machine = spec;
+    r.precision = precision;
+    r.kernel = kernel;
+    r.balance_overridden = balance_override.has_value();
+    r.single_step_intensity = single_step_intensity;
+    if (balance_override) r.balance = *balance_override;
+    // the library validates everything (spec, intensity, override) and
+    // carries the notes and verdict; the numbers come from the same C-ABI
+    for (const auto& [field, value] : csv_rows(render(r, RL_REPORT_CSV))) {
+        if (field == "note") r.notes.push_back(value);
+        else if (field == "verdict") r.verdict = value;
+    }
+    if (!balance_override) check(rl_machine_balance(&s, RL_CUDA_CORE, Pr(precision), &r.balance));
+    const double I = kernel.intensity();
+    r.boundedness = static_cast<Boundedness>(rl_classify(I, r.balance));
+    if (spec.has_peak(ExecutionUnit::TensorCore, precision)) {
+        check(rl_tensor_alpha(&s, Pr(precision), &r.alpha));
+        const double a = r.alpha < 1.0 ? 1.0 : r.alpha;
+        const double B = r.balance;
+        r.bounds.push_back(bound_of([&](rl_speedup_bound* b, char* t, uint64_t c, uint64_t* l) {
+            return rl_kernel_ceiling_bound(a, B, I, b, t, c, l);
+        }));
+        r.bounds.push_back(bound_of([&](rl_speedup_bound* b, char* t, uint64_t c, uint64_t* l) {
+            return rl_tensor_core_bound(a, b, t, c, l);
+        }));
+    }
+    r.bounds.push_back(bound_of([&](rl_speedup_bound* b, char* t, uint64_t c, uint64_t* l) {
+        return rl_workload_bound(I, r.balance, b, t, c, l);
+    }));
+    if (single_step_intensity) {
+        std::uint64_t t = 0;
+        check(rl_min_temporal_depth(r.balance, *single_step_intensity, &t));
+        r.min_depth = t;
+    }
+    return r;
+}
+
+std::string render_text(const AnalysisReport& r) { return render(r, RL_REPORT_TEXT); }
+std::string render_json(const AnalysisReport& r) { return render(r, RL_REPORT_JSON); }
+std::string render_csv(const AnalysisReport& r) { return render(r, RL_REPORT_CSV); }
 
 }  // namespace rooflens

@@ -64,6 +64,8 @@ _REF_SIGS = {
     "ref_overlapped_total": (_int, [_dbl, _dbl, _dbl, _DP]),
     "ref_sample_curve": (_int, [_dbl, _dbl, _dbl, _int, _dbl, _dbl, _u64, _ptr, _ptr, _u64, _U64P]),
     "ref_kernel_speedup_ceiling": (_int, [_dbl, _dbl, _dbl, _DP, C.POINTER(_int)]),
+    "ref_bound_text": (_int, [_int, _dbl, _dbl, _dbl, _dbl, _DP, C.POINTER(_int), C.POINTER(_int),
+                              C.POINTER(_int), C.c_char_p, C.c_uint64, C.c_char_p, C.c_uint64]),
     "ref_tensor_core_ceiling": (_int, [_dbl, _DP]),
     "ref_workload_ceiling": (_int, [_dbl, _dbl, _DP]),
     "ref_unoverlapped_speedup": (_int, [_dbl, _dbl, _dbl, _dbl, _DP]),

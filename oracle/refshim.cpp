@@ -200,6 +200,34 @@ int ref_kernel_speedup_ceiling(double alpha, double balance, double intensity, d
     });
 }
 
+// The reference's SpeedupBound for bound `kind` (0 unoverlapped(t_cmp=a,
+// t_mem=b, t_others=c, alpha=d), 1 kernel ceiling(a=alpha, b=balance,
+// c=intensity), 2 tensor-core ceiling(a=alpha), 3 workload ceiling(a=I,
+// b=balance)): value, BoundKind, to_string(kind) and its assumption and
+// warning lines ('\n'-terminated) into text.
+int ref_bound_text(int kind, double a, double b, double c, double d, double* value, int* bkind,
+                   int* n_assumptions, int* n_warnings, char* text, uint64_t cap, char* kind_name,
+                   uint64_t kind_cap) {
+    return guarded([&] {
+        SpeedupBound r = kind == 0   ? unoverlapped_bound(TimeBreakdown{a, b, c}, d)
+                         : kind == 1 ? kernel_speedup_ceiling(a, b, c)
+                         : kind == 2 ? tensor_core_ceiling(a)
+                                     : workload_ceiling(a, b);
+        *value = r.value;
+        *bkind = static_cast<int>(r.kind);
+        *n_assumptions = static_cast<int>(r.assumptions.size());
+        *n_warnings = static_cast<int>(r.warnings.size());
+        std::string t;
+        for (auto& x : r.assumptions) t += x + "\n";
+        for (auto& x : r.warnings) t += x + "\n";
+        if (t.size() + 1 > cap) throw Error(ErrorKind::InvalidRange, "capacity");
+        std::memcpy(text, t.c_str(), t.size() + 1);
+        std::string kn = to_string(r.kind);
+        if (kn.size() + 1 > kind_cap) throw Error(ErrorKind::InvalidRange, "capacity");
+        std::memcpy(kind_name, kn.c_str(), kn.size() + 1);
+    });
+}
+
 int ref_tensor_core_ceiling(double alpha, double* out) {
     return guarded([&] { *out = tensor_core_ceiling(alpha).value; });
 }

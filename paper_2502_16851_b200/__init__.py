@@ -35,6 +35,7 @@ __all__ = [
     "stencil_host", "SpmvPlan", "mtx_stats", "mtx_read_csr", "matrix_analysis", "fill_uniform", "gen_band_csr", "stencil_init", "load_spec", "load_spec_file", "serialize_spec", "builtin_spec",
     "machine_balance", "tensor_alpha", "attainable", "classify", "ridge_point", "sample_curve", "mem_cmp_ratio", "overlapped_total", "unoverlapped_speedup",
     "kernel_speedup_ceiling", "tensor_core_ceiling", "workload_ceiling", "min_temporal_depth",
+    "speedup_bound", "analysis_report",
     "tc_scale_trick_throughput", "fp64_peak_launch", "tuning_set", "kernel_launches",
     "ERROR_KINDS", "EXPORTED_SYMBOLS",
 ]
@@ -185,6 +186,13 @@ _SIGNATURES = {
     "rl_workload_ceiling": (_int, [_dbl, _dbl, C.POINTER(_dbl)]),
     "rl_min_temporal_depth": (_int, [_dbl, _dbl, C.POINTER(_u64)]),
     "rl_tc_scale_trick_throughput": (_int, [_dbl, _u64, _u64, C.POINTER(_dbl)]),
+    "rl_bound_kind_name": (C.c_char_p, [_int]),
+    "rl_unoverlapped_bound": (_int, [_dbl, _dbl, _dbl, _dbl, _ptr, C.c_char_p, _u64, C.POINTER(_u64)]),
+    "rl_kernel_ceiling_bound": (_int, [_dbl, _dbl, _dbl, _ptr, C.c_char_p, _u64, C.POINTER(_u64)]),
+    "rl_tensor_core_bound": (_int, [_dbl, _ptr, C.c_char_p, _u64, C.POINTER(_u64)]),
+    "rl_workload_bound": (_int, [_dbl, _dbl, _ptr, C.c_char_p, _u64, C.POINTER(_u64)]),
+    "rl_analysis_render": (_int, [_HP, _int, C.c_char_p, _u64, _u64, C.POINTER(_dbl), C.POINTER(_dbl), _int,
+                                  C.c_char_p, _u64, C.POINTER(_u64)]),
     "rl_fp64_peak_launch": (_int, [_int, _u64, _ptr, _ptr, C.POINTER(_dbl)]),
     "rl_tuning_set": (_int, [C.c_char_p, _i64, C.POINTER(_i64)]),
     # multi-GPU (dist.py wraps these)
@@ -717,6 +725,50 @@ def min_temporal_depth(balance, single_step_intensity) -> int:
 
 def tc_scale_trick_throughput(peak_tc, m, n) -> float:
     return _d1(lib().rl_tc_scale_trick_throughput, float(peak_tc), int(m), int(n))
+
+
+class _SpeedupBound(C.Structure):
+    _fields_ = [("value", C.c_double), ("kind", C.c_int), ("n_assumptions", C.c_int),
+                ("n_warnings", C.c_int)]
+
+
+BOUND_FUNCS = {"unoverlapped": "rl_unoverlapped_bound", "kernel": "rl_kernel_ceiling_bound",
+               "tensor_core": "rl_tensor_core_bound", "workload": "rl_workload_bound"}
+
+
+def speedup_bound(which: str, *args) -> dict:
+    """A reportable SpeedupBound (bounds.hpp:27-45): which = unoverlapped
+    (t_cmp, t_mem, t_others, alpha) | kernel (alpha, balance, intensity) |
+    tensor_core (alpha) | workload (intensity, balance).  Returns
+    {value, kind, kind_name, assumptions, warnings}."""
+    fn = getattr(lib(), BOUND_FUNCS[which])
+    b, n = _SpeedupBound(), _u64()
+    fargs = [float(a) for a in args]
+    _check(fn(*fargs, C.byref(b), None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _check(fn(*fargs, C.byref(b), buf, n.value + 1, None))
+    lines = buf.value.decode().split("\n")[:-1]
+    return {"value": b.value, "kind": b.kind, "kind_name": lib().rl_bound_kind_name(b.kind).decode(),
+            "assumptions": lines[:b.n_assumptions], "warnings": lines[b.n_assumptions:]}
+
+
+REPORT_FORMATS = {"text": 0, "json": 1, "csv": 2}
+
+
+def analysis_report(spec: HardwareSpec, kernel_name: str, kc: KernelCharacterization, fmt: str = "text",
+                    balance_override=None, single_step_intensity=None, precision: int = FP64) -> str:
+    """rooflens::build_analysis + render_text/json/csv (report.hpp:19-48)
+    through rl_analysis_render."""
+    s = spec._c()
+    bo = C.byref(_dbl(balance_override)) if balance_override is not None else None
+    si = C.byref(_dbl(single_step_intensity)) if single_step_intensity is not None else None
+    args = (C.byref(s), precision, kernel_name.encode(), int(kc.work_flops), int(kc.traffic_bytes), bo, si,
+            REPORT_FORMATS[fmt])
+    n = _u64()
+    _check(lib().rl_analysis_render(*args, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _check(lib().rl_analysis_render(*args, buf, n.value + 1, None))
+    return buf.value.decode()
 
 
 # ----------------------------------------------------------------------------

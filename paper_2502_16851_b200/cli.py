@@ -27,7 +27,8 @@ import math
 import os
 import sys
 
-from . import (CUDA_CORE, FP64, TENSOR_CORE, HardwareSpec, RooflensError, attainable, builtin_spec,
+from . import (CUDA_CORE, FP16, FP32, FP64, TENSOR_CORE, HardwareSpec, RooflensError, analysis_report,
+               attainable, builtin_spec, load_spec_file,
                classify, gemv_model, sample_curve as _sample_curve, kernel_speedup_ceiling, load_spec, machine_balance, matrix_analysis,
                min_temporal_depth, mtx_stats, scale_model, spmv_csr_model, stencil_model, stencil_preset,
                tensor_alpha, tensor_core_ceiling, workload_ceiling)
@@ -41,23 +42,23 @@ class UsageError(Exception):
     pass
 
 
+SPEC_DOC = os.path.join(ROOT, "profiles", "B200-measured.json")
+
+
 def measured_b200() -> HardwareSpec:
-    """B200 from this repo's measurements: HBM from MEASURED_PEAKS.json, FP64
-    peaks from the last bench line under profiles/ (K11), if present."""
-    bw = 6543.1e9
-    pcc, ptc = 36.4e12, 37.1e12
+    """The measured B200: profiles/B200-measured.json, the reference-schema
+    document bench.py emits as `hardware_spec` (measured HBM copy bandwidth,
+    K11 FP64 DFMA/DMMA peaks), read through load_spec_file
+    (hardware.cpp:239-247)."""
+    if os.path.exists(SPEC_DOC):
+        return load_spec_file(SPEC_DOC)
+    bw = 6548.8e9
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             bw = float(json.load(f)["hbm_gbs"]) * 1e9
     except Exception:
         pass
-    try:
-        with open(os.path.join(ROOT, "profiles", "bench_r1.json")) as f:
-            pk = json.load(f)["fp64_peaks_tflops"]
-            pcc, ptc = pk["cuda_core"] * 1e12, pk["tensor_core"] * 1e12
-    except Exception:
-        pass
-    return HardwareSpec("B200-measured", bw, 126e6, pcc, ptc)
+    return HardwareSpec("B200-measured", bw, 126e6, 36.4e12, 37.0e12)
 
 
 def resolve_hw(name: str) -> HardwareSpec:
@@ -80,81 +81,36 @@ def fmt4(x: float) -> str:
 
 
 # ---------------------------------------------------------------------------
-# analysis report (report.hpp:19-35 AnalysisReport)
+# analysis report: rooflens::build_analysis + render_* (report.hpp:19-48) in
+# the library (csrc/report.cpp, rl_analysis_render)
 # ---------------------------------------------------------------------------
 def build_analysis(spec: HardwareSpec, kernel_name: str, kc, balance_override=None,
-                   single_step_intensity=None) -> dict:
-    balance = machine_balance(spec, CUDA_CORE) if balance_override is None else float(balance_override)
-    I = kc.intensity
-    rep = {
-        "machine": {"name": spec.name, "memory_bandwidth": spec.memory_bandwidth,
-                    "peak_cuda_core": spec.peak_cuda_core, "peak_tensor_core": spec.peak_tensor_core},
-        "precision": "FP64", "balance": balance, "balance_overridden": balance_override is not None,
-        "kernel": {"name": kernel_name, "work_flops": kc.work_flops, "traffic_bytes": kc.traffic_bytes,
-                   "intensity": I},
-        "boundedness": BOUNDEDNESS[classify(I, balance)],
-        "bounds": [], "notes": [],
-    }
-    alpha = None
-    if spec.peak_tensor_core > 0:
-        alpha = tensor_alpha(spec)
-        rep["alpha"] = alpha
-        a = max(alpha, 1.0)
-        kv, nw = kernel_speedup_ceiling(a, balance, I)
-        rep["bounds"].append({"kind": "kernel ceiling", "value": kv, "warnings": nw})
-        rep["bounds"].append({"kind": "tensor-core ceiling", "value": tensor_core_ceiling(a)})
-        if alpha < 1.0:
-            rep["notes"].append("alpha < 1: ceilings evaluated at alpha = 1")
-    rep["bounds"].append({"kind": "workload ceiling", "value": workload_ceiling(I, balance)})
-    rep["attainable_flops"] = attainable(spec, I)
-    if single_step_intensity is not None:
-        rep["single_step_intensity"] = single_step_intensity
-        rep["min_temporal_depth"] = min_temporal_depth(balance, single_step_intensity)
-    x = min(b["value"] for b in rep["bounds"])
-    rep["verdict"] = f"tensor cores cannot exceed {x:.3g}x on this kernel/machine"
-    return rep
+                   single_step_intensity=None, precision: int = FP64) -> dict:
+    return json.loads(analysis_report(spec, kernel_name, kc, "json", balance_override, single_step_intensity,
+                                      precision))
 
 
-def render(rep: dict, fmt: str) -> str:
-    if fmt == "json":
-        return json.dumps(rep, indent=1, sort_keys=True) + "\n"
-    rows = [("machine", rep["machine"]["name"]), ("kernel", rep["kernel"]["name"]),
-            ("work_flops", rep["kernel"]["work_flops"]), ("traffic_bytes", rep["kernel"]["traffic_bytes"]),
-            ("intensity", rep["kernel"]["intensity"]), ("balance", rep["balance"]),
-            ("boundedness", rep["boundedness"]), ("attainable_flops", rep["attainable_flops"])]
-    if "alpha" in rep:
-        rows.append(("alpha", rep["alpha"]))
-    rows += [(b["kind"], b["value"]) for b in rep["bounds"]]
-    if "min_temporal_depth" in rep:
-        rows.append(("min_temporal_depth", rep["min_temporal_depth"]))
-    rows.append(("verdict", rep["verdict"]))
-    if fmt == "csv":
-        out = io.StringIO()
-        w = csv.writer(out, lineterminator="\n")
-        w.writerow(["field", "value"])
-        for k, v in rows:
-            w.writerow([k, repr(v) if isinstance(v, float) else v])
-        return out.getvalue()
-    width = max(len(k) for k, _ in rows)
-    return "".join(f"{k:<{width}}  {fmt4(v) if isinstance(v, float) else v}\n" for k, v in rows)
+def render(spec: HardwareSpec, kernel_name: str, kc, fmt: str, balance_override=None,
+           single_step_intensity=None, precision: int = FP64) -> str:
+    return analysis_report(spec, kernel_name, kc, fmt, balance_override, single_step_intensity, precision)
 
 
 def kernel_of(args):
-    k = args.kernel
+    k, p = args.kernel, getattr(args, "prec", FP64)
     if k == "scale":
-        return "scale", scale_model(args.n or 1), None
+        return "scale", scale_model(args.n or 1, p), None
     if k == "gemv":
         if not (args.m and args.n):
             raise UsageError("gemv needs --m and --n")
-        return "gemv", gemv_model(args.m, args.n), None
+        return "gemv", gemv_model(args.m, args.n, p), None
     if k == "spmv-csr":
         if not (args.m and args.nnz):
             raise UsageError("spmv-csr needs --m, --nnz (and --n for rectangular)")
-        return "spmv-csr", spmv_csr_model(args.m, args.n or args.m, args.nnz), None
+        return "spmv-csr", spmv_csr_model(args.m, args.n or args.m, args.nnz, precision=p), None
     if k == "stencil":
         shape = args.shape or "2d5pt"
         t = args.t or 1
-        return shape, stencil_model(shape, FP64, t), stencil_model(shape, FP64, 1).intensity
+        return shape, stencil_model(shape, p, t), stencil_model(shape, p, 1).intensity
     raise UsageError(f"unknown kernel {k}")
 
 
@@ -182,8 +138,7 @@ def cmd_hardware(args, out):
 def cmd_analyze(args, out):
     spec = resolve_hw(args.hw)
     name, kc, i1 = kernel_of(args)
-    rep = build_analysis(spec, name, kc, args.balance_override, i1)
-    out.write(render(rep, args.format))
+    out.write(render(spec, name, kc, args.format, args.balance_override, i1, args.prec))
     return 0
 
 
@@ -336,9 +291,9 @@ def cmd_measure(args, out):
                        "frac_of_hbm": gbs * 1e9 / spec.memory_bandwidth,
                        "achieved_flops": kc.work_flops / (ms * 1e-3)}
     if args.format == "json":
-        out.write(render(rep, "json"))
+        out.write(json.dumps(rep, indent=1) + "\n")
     else:
-        out.write(render(rep, "text"))
+        out.write(render(spec, k, kc, "text"))
         out.write(f"measured_gbs  {fmt4(gbs)}\nfrac_of_hbm   {fmt4(rep['measured']['frac_of_hbm'])}\n")
     return 0
 
@@ -347,8 +302,8 @@ def main(argv=None, out=None) -> int:
     out = out or sys.stdout
     ap = argparse.ArgumentParser(prog="rooflens-b200")
     ap.add_argument("--format", default="text", choices=["text", "json", "csv"])
-    # SPEC.md cli_report global flag; this build (like the reference's spec
-    # slice, hardware.hpp:43-58) carries FP64 peaks only
+    # SPEC.md cli_report global flag: analysis at any precision the spec has
+    # peaks for; the kernels (measure) execute in FP64 only
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32", "fp16"])
     sub = ap.add_subparsers(dest="cmd", required=True)
     h = sub.add_parser("hardware")
@@ -387,8 +342,9 @@ def main(argv=None, out=None) -> int:
         return 0 if e.code == 0 else 1
     if getattr(args, "format", None) is None:
         args.format = "text"
-    if args.precision != "fp64":
-        print(f"ValidationError: precision {args.precision} is not supported (FP64 only)", file=sys.stderr)
+    args.prec = {"fp64": FP64, "fp32": FP32, "fp16": FP16}[args.precision]
+    if args.precision != "fp64" and args.cmd == "measure":
+        print(f"ValidationError: the kernels execute in FP64 only (got {args.precision})", file=sys.stderr)
         return 2
     try:
         return {"hardware": cmd_hardware, "analyze": cmd_analyze, "matrix": cmd_matrix,

@@ -1180,6 +1180,70 @@ int rl_tc_scale_trick_throughput(double p, uint64_t m, uint64_t n, double* out) 
     return guarded([&] { *out = tc_scale_trick_throughput(p, m, n); });
 }
 
+namespace {
+// Copy `text` (NUL-terminated) into a caller buffer: *length (optional) gets
+// the full length; a null buffer only sizes; a short buffer is InvalidRange.
+void text_out(const std::string& text, char* buf, uint64_t cap, uint64_t* length, const char* what) {
+    if (length) *length = text.size();
+    if (!buf) return;
+    if (cap < text.size() + 1)
+        throw Error(ErrorKind::InvalidRange, std::string(what) + ": buffer of " + std::to_string(cap) +
+                                                 " bytes cannot hold " + std::to_string(text.size() + 1));
+    std::memcpy(buf, text.c_str(), text.size() + 1);
+}
+
+void bound_out(const SpeedupBound& b, rl_speedup_bound* out, char* text, uint64_t cap, uint64_t* length) {
+    require_ptr(out, "out");
+    out->value = b.value;
+    out->kind = static_cast<int>(b.kind);
+    out->n_assumptions = static_cast<int>(b.assumptions.size());
+    out->n_warnings = static_cast<int>(b.warnings.size());
+    std::string t;
+    for (const std::string& a : b.assumptions) t += a + "\n";
+    for (const std::string& w : b.warnings) t += w + "\n";
+    text_out(t, text, cap, length, "speedup bound text");
+}
+}  // namespace
+
+const char* rl_bound_kind_name(int kind) {
+    return (kind >= 0 && kind <= 3) ? to_string(static_cast<BoundKind>(kind)) : "?";
+}
+int rl_unoverlapped_bound(double tc, double tm, double to, double a, rl_speedup_bound* out, char* text,
+                          uint64_t cap, uint64_t* length) {
+    return guarded([&] { bound_out(unoverlapped_bound(tc, tm, to, a), out, text, cap, length); });
+}
+int rl_kernel_ceiling_bound(double a, double b, double i, rl_speedup_bound* out, char* text, uint64_t cap,
+                            uint64_t* length) {
+    return guarded([&] { bound_out(kernel_ceiling_bound(a, b, i), out, text, cap, length); });
+}
+int rl_tensor_core_bound(double a, rl_speedup_bound* out, char* text, uint64_t cap, uint64_t* length) {
+    return guarded([&] { bound_out(tensor_core_bound(a), out, text, cap, length); });
+}
+int rl_workload_bound(double i, double b, rl_speedup_bound* out, char* text, uint64_t cap, uint64_t* length) {
+    return guarded([&] { bound_out(workload_bound(i, b), out, text, cap, length); });
+}
+
+int rl_analysis_render(const rl_hw_spec* spec, rl_precision p, const char* kernel_name, uint64_t work_flops,
+                       uint64_t traffic_bytes, const double* balance_override,
+                       const double* single_step_intensity, int format, char* buf, uint64_t cap,
+                       uint64_t* length) {
+    return guarded([&] {
+        require_ptr(spec, "spec");
+        if (format < RL_REPORT_TEXT || format > RL_REPORT_CSV)
+            throw Error(ErrorKind::ValidationError, "report format must be text, json or csv");
+        KernelCharacterization k;
+        k.kernel_name = kernel_name ? kernel_name : "";
+        k.work_flops = work_flops;
+        k.traffic_bytes = traffic_bytes;
+        std::optional<double> bo, si;
+        if (balance_override) bo = *balance_override;
+        if (single_step_intensity) si = *single_step_intensity;
+        const AnalysisReport r = build_analysis(spec_of(spec), prec_of(p), k, bo, si);
+        text_out(format == RL_REPORT_TEXT ? render_text(r) : format == RL_REPORT_JSON ? render_json(r) : render_csv(r),
+                 buf, cap, length, "analysis report");
+    });
+}
+
 int rl_fp64_peak_launch(rl_unit u, uint64_t iters, rl_stream s, double* sink, double* flops) {
     return guarded([&] {
         require_ptr(sink, "sink");

@@ -2,6 +2,7 @@
 // the reference's headers (tests/test_integration.py).  Prints one line per
 // probe: "<probe> <outcome>" where outcome is ok:<W>/<Q>, the rooflens
 // ErrorKind ordinal as kind:<k>, or runtime:<text> for a CUDA / NCCL status.
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -9,7 +10,9 @@
 #include <string>
 
 #include "b200_exec.hpp"
+#include "rooflens/bounds.hpp"
 #include "rooflens/error.hpp"
+#include "rooflens/report.hpp"
 
 using namespace rooflens;
 
@@ -52,5 +55,41 @@ int main() {
     // here, so only probed when the caller says no device is present.
     if (std::getenv("RL_PROBE_NO_DEVICE"))
         probe("scale_exec", [&] { return scale(ExecutionUnit::CudaCore, Precision::FP64, a, b, 3.0, 8, nullptr); });
+    // report.hpp through the adapter: the bounds equal the reference's own
+    // bounds.cpp objects (value, kind, assumption and warning text)
+    try {
+        const HardwareSpec& gh = builtin_spec("GH200");
+        KernelCharacterization k = stencil_model(stencil_preset("3d27pt"), Precision::FP64, 1);
+        const AnalysisReport r = build_analysis(gh, Precision::FP64, k, 9.99, k.intensity());
+        const double a = tensor_alpha(gh, Precision::FP64);
+        const SpeedupBound want[3] = {kernel_speedup_ceiling(a, 9.99, k.intensity()), tensor_core_ceiling(a),
+                                      workload_ceiling(k.intensity(), 9.99)};
+        bool same = r.bounds.size() == 3;
+        for (int i = 0; same && i < 3; ++i)
+            same = r.bounds[i].value == want[i].value && r.bounds[i].kind == want[i].kind &&
+                   r.bounds[i].assumptions == want[i].assumptions && r.bounds[i].warnings == want[i].warnings;
+        std::printf("report_bounds %s\n", same ? "same" : "differ");
+        std::printf("report_alpha %s\n", r.alpha == a ? "same" : "differ");
+        std::printf("report_min_depth %llu\n", (unsigned long long)r.min_depth.value_or(0));
+        std::printf("report_verdict %s\n", r.verdict.c_str());
+        std::printf("report_notes %zu\n", r.notes.size());
+        const std::string j = render_json(r);
+        std::printf("render_json %s\n", j.find("\"verdict\"") != std::string::npos ? "has_verdict" : "no_verdict");
+        const KernelCharacterization c = scale_model(4, Precision::FP64);
+        const AnalysisReport w = build_analysis(builtin_spec("A100-80GB"), Precision::FP64,
+                                                gemv_model(100000, 100000, Precision::FP64));
+        std::printf("report_gemv_workload %.6f\n", w.bounds.back().value);
+        const std::string txt = render_text(w);
+        std::printf("render_text_lines %zu\n", (size_t)std::count(txt.begin(), txt.end(), '\n'));
+        (void)c;
+    } catch (const Error& e) {
+        std::printf("report_bounds kind:%d:%s\n", static_cast<int>(e.kind()), e.what());
+    }
+    try {
+        build_analysis(builtin_spec("A100-80GB"), Precision::FP64, scale_model(4, Precision::FP64), 0.0);
+        std::printf("report_zero_balance ok\n");
+    } catch (const Error& e) {
+        std::printf("report_zero_balance kind:%d\n", static_cast<int>(e.kind()));
+    }
     return 0;
 }

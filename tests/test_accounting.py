@@ -297,3 +297,91 @@ def test_random_peak_tables_match_live_reference():
         rc = R.ref_serialize_spec(doc.encode(), buf, 4096)
         if rc == 0:
             assert P.serialize_spec(P.load_spec(doc)) == buf.value.decode()
+
+
+# ---------------------------------------------------------------------------
+# SpeedupBound text (bounds.hpp:27-45) and the analysis report (report.hpp)
+# ---------------------------------------------------------------------------
+def _ref_bound(kind, a, b=0.0, c=0.0, d=0.0):
+    import ctypes as C
+
+    v, k, na, nw = C.c_double(), C.c_int(), C.c_int(), C.c_int()
+    text, kname = C.create_string_buffer(4096), C.create_string_buffer(64)
+    rc = O.ref().ref_bound_text(kind, a, b, c, d, C.byref(v), C.byref(k), C.byref(na), C.byref(nw), text, 4096,
+                                kname, 64)
+    if rc:
+        return rc
+    lines = text.value.decode().split("\n")[:-1]
+    return {"value": v.value, "kind": k.value, "kind_name": kname.value.decode(),
+            "assumptions": lines[:na.value], "warnings": lines[na.value:]}
+
+
+BOUND_CASES = [
+    ("unoverlapped", 0, (1.0, 3.0, 0.5, 2.0)), ("unoverlapped", 0, (0.0, 1.0, 0.0, 4.0)),
+    ("kernel", 1, (2.01, 5.0, 0.0625)), ("kernel", 1, (1.97, 8.5, 9.0)), ("kernel", 1, (1.0, 5.0, 5.0)),
+    ("tensor_core", 2, (2.0,)), ("tensor_core", 2, (1.0172,)),
+    ("workload", 3, (0.25, 5.0)), ("workload", 3, (6.75, 5.56)),
+]
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("which,kind,args", BOUND_CASES)
+def test_speedup_bound_text_matches_reference(which, kind, args):
+    ours = P.speedup_bound(which, *args)
+    ref = _ref_bound(kind, *args)
+    assert ours == ref
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("which,kind,args", [("kernel", 1, (0.5, 5.0, 1.0)), ("kernel", 1, (2.0, 5.0, 0.0)),
+                                             ("workload", 3, (1.0, 0.0)), ("unoverlapped", 0, (-1.0, 1.0, 0.0, 2.0)),
+                                             ("unoverlapped", 0, (0.0, 0.0, 0.0, 2.0))])
+def test_speedup_bound_errors_match_reference(which, kind, args):
+    with pytest.raises(P.RooflensError) as e:
+        P.speedup_bound(which, *args)
+    assert e.value.code == _ref_bound(kind, *args)
+
+
+def test_analysis_report_fields():
+    """build_analysis (report.hpp:40-44): the verdict's X is the min bound to
+    3 significant digits; the json/csv numbers are the C-ABI's own values;
+    text is 4 significant digits; output is deterministic."""
+    import csv
+    import io
+    import json
+
+    spec = P.builtin_spec("A100-80GB")
+    kc = P.spmv_csr_model(1 << 22, 1 << 22, 1 << 26)
+    j = json.loads(P.analysis_report(spec, "spmv-csr", kc, "json"))
+    a = P.tensor_alpha(spec)
+    B = P.machine_balance(spec)
+    vals = {b["kind"]: b["value"] for b in j["bounds"]}
+    assert vals["kernel ceiling"] == P.kernel_speedup_ceiling(a, B, kc.intensity)[0]
+    assert vals["tensor-core ceiling"] == P.tensor_core_ceiling(a)
+    assert vals["workload ceiling"] == P.workload_ceiling(kc.intensity, B)
+    assert j["verdict"] == f"tensor cores cannot exceed {min(vals.values()):.3g}x on this kernel/machine"
+    assert j["boundedness"] == "memory-bound" and j["alpha"] == a and j["balance"] == B
+    assert [b["assumptions"] for b in j["bounds"]] == [
+        P.speedup_bound("kernel", a, B, kc.intensity)["assumptions"], P.speedup_bound("tensor_core", a)["assumptions"],
+        P.speedup_bound("workload", kc.intensity, B)["assumptions"]]
+    rows = list(csv.reader(io.StringIO(P.analysis_report(spec, "spmv-csr", kc, "csv"))))
+    d = {k: v for k, v in rows[1:]}
+    assert float(d["kernel ceiling"]) == vals["kernel ceiling"] and int(d["traffic_bytes"]) == kc.traffic_bytes
+    txt = P.analysis_report(spec, "spmv-csr", kc, "text")
+    assert f"{vals['kernel ceiling']:.4g}" in txt and txt == P.analysis_report(spec, "spmv-csr", kc, "text")
+    # compute-bound kernel: the kernel-ceiling warning travels into the report
+    j = json.loads(P.analysis_report(spec, "2d49pt", P.stencil_model("2d49pt"), "json"))
+    assert j["boundedness"] == "compute-bound" and j["bounds"][0]["warnings"]
+    # stencil section (PAPER.md:229-232: t > 15.98 on GH200 at B = 9.99)
+    j = json.loads(P.analysis_report(P.builtin_spec("GH200"), "2d5pt", P.stencil_model("2d5pt"), "json",
+                                     balance_override=9.99, single_step_intensity=0.625))
+    assert j["min_temporal_depth"] == 16 and j["balance_overridden"] and j["balance"] == 9.99
+    # a spec without a tensor-core peak: workload ceiling only, with a note
+    j = json.loads(P.analysis_report(P.HardwareSpec("cc-only", 1e12, 1e6, 1e13), "scale", P.scale_model(10), "json"))
+    assert [b["kind"] for b in j["bounds"]] == ["workload ceiling"] and "alpha" not in j
+    with pytest.raises(P.RooflensError) as e:
+        P.analysis_report(spec, "scale", P.scale_model(10), "json", balance_override=0.0)
+    assert e.value.kind == "ZeroBalance"
+    with pytest.raises(P.RooflensError) as e:
+        P.analysis_report(spec, "scale", P.scale_model(10), "json", precision=P.FP16)
+    assert e.value.kind == "MissingPeak"

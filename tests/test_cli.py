@@ -125,6 +125,31 @@ def test_measure_mtx_file(cuda, tmp_path):
     assert run("measure", "--kernel", "scale", "--mtx", str(path))[0] == 1
 
 
-def test_precision_flag():
+def test_precision_flag(tmp_path):
+    """Analysis runs at any precision the spec has peaks for (MissingPeak ->
+    exit 2 otherwise); the kernels (measure) are FP64 only."""
     assert run("--precision", "fp64", "hardware", "list")[0] == 0
-    assert run("--precision", "fp32", "hardware", "list")[0] == 2
+    assert run("--precision", "fp32", "measure", "--kernel", "scale")[0] == 2
+    doc = tmp_path / "s.json"
+    doc.write_text(json.dumps({"name": "X", "memory_bandwidth_tbps": 2.0, "l2_cache_mb": 40,
+                               "peaks": {"fp64": {"cuda_core_tflops": 10.0},
+                                         "fp32": {"cuda_core_tflops": 20.0, "tensor_core_tflops": 160.0}}}))
+    rc, txt = run("--precision", "fp32", "analyze", "--hw", str(doc), "--kernel", "scale", "--n", "1000",
+                  "--format", "json")
+    rep = json.loads(txt)
+    assert rc == 0 and rep["precision"] == "FP32" and rep["alpha"] == 8.0
+    assert rep["kernel"]["traffic_bytes"] == 8000 and rep["balance"] == 10.0
+    assert run("--precision", "fp16", "analyze", "--hw", str(doc), "--kernel", "scale", "--n", "8")[0] == 2
+
+
+def test_measured_b200_spec_document():
+    """The measured B200 is a reference-schema spec document
+    (profiles/B200-measured.json, written from bench.py's `hardware_spec`),
+    read through load_spec_file and round-tripping serialize_spec."""
+    spec = cli.measured_b200()
+    assert spec == P.load_spec_file(cli.SPEC_DOC)
+    assert P.serialize_spec(spec) == open(cli.SPEC_DOC).read()
+    assert 5.0 < P.machine_balance(spec) < 6.5 and 0.9 < P.tensor_alpha(spec) < 1.2
+    rc, txt = run("analyze", "--hw", "B200-measured", "--kernel", "spmv-csr", "--m", "4194304", "--nnz",
+                  "67108864", "--format", "json")
+    assert rc == 0 and json.loads(txt)["machine"]["name"] == "B200-measured"

@@ -249,4 +249,31 @@ def test_plan_short_rows(cuda):
     rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
     col = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(np.int32)
     val = rng.uniform(-1, 1, rp[-1])
-    _plan_check(torch, rp, col, val, n, P.CUDA_CORE, False)
+    _plan_check(torch, rp, col, val, n, P.CUDA_CORE, "csr")
+
+
+def test_plan_graph_leading_empty_rows(cuda):
+    """The first row chunks have no nonzeros (their x prefix is empty): the
+    captured graph still contains their kernels and y copies, so replays with
+    a poisoned y rewrite every row (capture fork event)."""
+    import torch
+
+    rng = np.random.default_rng(3)
+    m = n = 64000
+    lens = rng.integers(1, 20, m)
+    lens[: m // 4] = 0
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    col = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(np.int32)
+    val = rng.uniform(-1, 1, rp[-1])
+    plan = P.SpmvPlan(rp, col, val, n)
+    hx = torch.from_numpy(rng.uniform(-1, 1, n)).pin_memory()
+    hy = torch.empty(m, dtype=torch.float64).pin_memory()
+    for _ in range(3):
+        hy.fill_(float("nan"))
+        hx.copy_(torch.from_numpy(rng.uniform(-1, 1, n)))
+        plan.execute_host(hx, hy)
+        y = hy.numpy()
+        assert not np.isnan(y).any()
+        assert (y[: m // 4] == 0).all()
+        assert O.rel_err(y, O.spmv_csr(rp, col, val, hx.numpy())) <= 1e-12
+    plan.close()

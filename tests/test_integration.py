@@ -59,3 +59,18 @@ def test_no_device_is_a_cuda_status_not_a_fallback(probes):
     if torch.cuda.is_available():
         pytest.skip("a device is present")
     assert probes["scale_exec"].startswith("runtime:CudaError")
+
+
+def test_report_api_through_the_adapter(probes):
+    """report.hpp's build_analysis / render_* (declared by the reference, no
+    definition there) link against the adapter; its bounds are the
+    reference's own bounds.cpp objects, value and text."""
+    assert probes["report_bounds"] == "same"
+    assert probes["report_alpha"] == "same"
+    assert probes["report_min_depth"] == "3"  # 3d27pt: 3 * 3.375 > 9.99
+    assert probes["report_verdict"].startswith("tensor cores cannot exceed 1.")
+    assert int(probes["report_notes"]) == 2
+    assert probes["render_json"] == "has_verdict"
+    assert abs(float(probes["report_gemv_workload"]) - 1.05) < 1e-3
+    assert int(probes["render_text_lines"]) >= 14
+    assert probes["report_zero_balance"] == "kind:9"  # ZeroBalance
