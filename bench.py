@@ -154,11 +154,28 @@ class Spmv:
         self.bytes = P.spmv_csr_model(m, m, m * self.k).traffic_bytes
         self.plans = {}
         self.comm = comm
+        self.raw_csr = False  # True: the CSR kernels on the generator's arrays (no plan)
+        self.plan_colsort = 1  # the plan's layout choice (tuning key spmv_plan_colsort)
 
     def step(self, unit):
         P = self.P
-        if self.world == 1:
+        if self.world == 1 and self.raw_csr:
             P.spmv_csr(self.rp, self.col, self.val, self.x, self.y, unit=unit)
+        elif self.world == 1:
+            # rl_spmv_plan_execute: the plan's layout (K17 column-sorted row
+            # blocks on this matrix), built once from the CSR on the first
+            # (untimed, warm-up) call -- cusparseSpMV_preprocess-style
+            key = (unit, self.plan_colsort)
+            if key not in self.plans:
+                prev = P.tuning_set("spmv_plan_colsort", self.plan_colsort)
+                try:
+                    t0 = time.perf_counter()
+                    self.plans[key] = P.SpmvPlan(self.rp.cpu(), self.col.cpu(), self.val.cpu(), self.x.numel(),
+                                                 unit=unit)
+                    self.plan_create_s = time.perf_counter() - t0
+                finally:
+                    P.tuning_set("spmv_plan_colsort", prev)
+            self.plans[key].execute(self.x, self.y)
         else:
             # rl_dist_spmv: NCCL halo exchange overlapped with the interior rows
             if unit not in self.plans:
@@ -408,7 +425,12 @@ def per_kernel_table(torch, P, D, hbm):
         variants = [("cc", P.CUDA_CORE, {}), ("tc", P.TENSOR_CORE, {})]
         if _tc_pure_keys(name):
             variants.append(("tc_pure", P.TENSOR_CORE, _tc_pure_keys(name)))
+        if name == "spmv":
+            variants += [("cc_csr", P.CUDA_CORE, {}), ("tc_csr", P.TENSOR_CORE, {})]
         for uname, unit, keys in variants:
+            if name == "spmv":
+                wl.raw_csr = uname.endswith("_csr")
+                wl.plan_colsort = 1
             # stencils: 5 runs of the full timestep count, median run (one run is
             # +-5 % noisy on this box; the spread is reported)
             reps = spec["reps"] if name in ("stream", "spmv") else 5
@@ -425,6 +447,26 @@ def per_kernel_table(torch, P, D, hbm):
             if keys:
                 res[uname]["kernel"] = "full banded DMMA form (every tap on the tensor core), tuning " + \
                     ", ".join(f"{k}={v}" for k, v in keys.items())
+        if name == "spmv":
+            for u, key in (("cc", (P.CUDA_CORE, 1)), ("tc", (P.TENSOR_CORE, 1))):
+                layout, lbytes = wl.plans[key].info()
+                res[u]["kernel"] = (f"rl_spmv_plan_execute, layout {layout} ({lbytes} B streamed per call; "
+                                    + ("K17 column-sorted row blocks, spmv_colsort.cu)" if layout == "colsort"
+                                       else "CSR, spmv.cu)"))
+            res["plan_create_s"] = round(wl.plan_create_s, 3)
+            for u in ("cc_csr", "tc_csr"):
+                res[u]["kernel"] = "rl_spmv_csr on the generator's CSR arrays (spmv.cu)"
+            # what caps the CSR kernels on this matrix (profiles/README.md): one
+            # L1/L2 request per x gather plus one per 128-byte line of val/col,
+            # against the measured random-gather rate (tools/micro/dsmem_gather.cu:
+            # 1.0 per SM per cycle, 290 G/s at 1.965 GHz)
+            m = Spmv.n_local
+            reqs = m * Spmv.k + (m * Spmv.k * 12) // 128
+            rate = reqs / (res["cc_csr"]["ms_per_unit"] * 1e-3) / 1e9
+            res["cc_csr"]["l2_request_roof"] = {"requests_per_step": reqs, "achieved": round(rate, 1),
+                                                "peak": 290.0, "unit": "G requests/s",
+                                                "frac": round(rate / 290.0, 4)}
+            res["plan_over_csr_cc"] = round(res["cc"]["gbs"] / res["cc_csr"]["gbs"], 4)
         res["tc_over_cc"] = round(res["tc"]["gbs"] / res["cc"]["gbs"], 4)
         if "tc_pure" in res:
             res["tc_pure_over_cc"] = round(res["tc_pure"]["gbs"] / res["cc"]["gbs"], 4)
@@ -439,49 +481,6 @@ def per_kernel_table(torch, P, D, hbm):
         del wl
         torch.cuda.empty_cache()
     return rows
-
-
-def sorted_plan_row(torch, P, hbm, reps=20):
-    """K15 (opt-in plan layout, spmv_sorted.cu): the BASELINE matrix through
-    rl_spmv_plan_execute with the column-sorted block layout, device x/y.
-    Reported beside the CSR kernel; the layout halves the L2 gather requests
-    but is latency-bound (profiles/ncu_r1_spmv_sorted.md)."""
-    n, k, hb = 1 << 22, 16, 65536
-    rp = torch.empty(n + 1, dtype=torch.int32, device="cuda")
-    col = torch.empty(n * k, dtype=torch.int32, device="cuda")
-    val = torch.empty(n * k, dtype=torch.float64, device="cuda")
-    x = torch.empty(n, dtype=torch.float64, device="cuda")
-    y = torch.empty(n, dtype=torch.float64, device="cuda")
-    P.gen_band_csr(n, 0, n, k, hb, SEED, rp, col, val)
-    P.fill_uniform(x, SEED, 4, 0, 1)
-    prev = P.tuning_set("spmv_plan_sorted", 1)
-    try:
-        plan = P.SpmvPlan(rp.cpu(), col.cpu(), val.cpu(), n)
-        layout = plan.layout()
-        for _ in range(3):
-            plan.execute(x, y)
-        torch.cuda.synchronize()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        for _ in range(reps):
-            plan.execute(x, y)
-        e.record()
-        torch.cuda.synchronize()
-        ms = s.elapsed_time(e) / reps
-        ref = torch.empty_like(y)
-        P.spmv_csr(rp, col, val, x, ref)
-        torch.cuda.synchronize()
-        rel = float(torch.linalg.norm(y - ref) / torch.linalg.norm(ref))
-        gbs = P.spmv_csr_model(n, n, n * k).traffic_bytes / (ms * 1e-3) / 1e9
-        out = {"gbs": round(gbs, 1), "frac_of_measured_peak": round(gbs / hbm, 4), "ms": round(ms, 4),
-               "layout": layout, "rel_diff_vs_csr_kernel": rel,
-               "note": "opt-in column-sorted block layout (K15): L2 requests 35.9 M vs 73.4 M, latency-bound"}
-        plan.close()
-    finally:
-        P.tuning_set("spmv_plan_sorted", prev)
-    del rp, col, val, x, y
-    torch.cuda.empty_cache()
-    return out
 
 
 def cusparse_yardstick(torch, P, hbm, reps=20):
@@ -1014,18 +1013,6 @@ def main():
     del h
 
     traffic = ncu_traffic().get(f"{args.workload}_{args.unit}")
-    l2_roof = None
-    if args.workload == "spmv" and world == 1:
-        # the binding unit for CSR SpMV on this matrix (profiles/README.md): L2
-        # requests -- one per x gather plus one per 128-byte line of val/col --
-        # against the measured random-gather rate (tools/micro/dsmem_gather.cu:
-        # 1.0 per SM per cycle, 290 G/s at 1.965 GHz)
-        m = Spmv.n_local
-        reqs = m * Spmv.k + (m * Spmv.k * 12) // 128
-        rate = reqs / (launch_ms * 1e-3) / 1e9
-        l2_roof = {"bound": "l2_requests", "requests_per_step": reqs, "achieved": round(rate, 1),
-                   "peak": 290.0, "unit": "G requests/s", "frac": round(rate / 290.0, 4),
-                   "peak_source": "measured random 8-byte L2 gather rate (tools/micro/dsmem_gather.cu)"}
     api = {"spmv": ("rl_spmv_plan_execute_host: A resident (uploaded once by rl_spmv_plan_create), "
                     "x H2D and y D2H from pinned host memory inside every timed call"),
            }.get(args.workload, "rl_*_host C-ABI (pinned host buffers, copies inside the timed call)")
@@ -1042,7 +1029,6 @@ def main():
                      "frac": round(achieved / hbm, 4), "traffic": traffic,
                      "launch_ms_mean": round(launch_ms, 5),
                      "launch_ms_p50": round(per_sorted[len(per_sorted) // 2], 5)},
-        "roofline_l2_requests": l2_roof,
         "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": args.e2e_steps, "api": api},
         "e2e_full_copy": full_copy,
@@ -1062,7 +1048,6 @@ def main():
         with ClockSampler(dev_index) as clk2:
             table = per_kernel_table(torch, P, D, hbm)
             table["spmv"]["cusparse_cc_yardstick"] = cusparse_yardstick(torch, P, hbm)
-            table["spmv"]["sorted_plan_cc"] = sorted_plan_row(torch, P, hbm)
             line["temporal_blocking"] = temporal_blocking(torch, P, hbm,
                                                           table["2d5pt"]["cc"]["ms_per_unit"],
                                                           table["3d7pt"]["cc"]["ms_per_unit"])

@@ -183,10 +183,14 @@ RL_API int rl_stencil_host(rl_unit unit, rl_precision precision, const char* pre
                     double* v, rl_kchar* out);
 /* SpMV plan: the CSR matrix is uploaded once (the iterative-solver pattern:
  * A is fixed, x changes every step) and each execute moves only x in and y
- * out.  The plan keeps A as CSR; two opt-in CUDA-core layouts built once at
- * creation exist as measured alternatives (tuning keys spmv_plan_sorted,
- * spmv_plan_chunked; K15/K16).  execute_host pipelines the x
- * upload, the row-chunk kernels and the y download on three streams: row
+ * out.  At creation the plan re-lays A as column-sorted row blocks (K17,
+ * y rows of a block in shared memory, x read in column order)
+ * when every row has <= 1024 nonzeros and the block column spans fit, else
+ * keeps the CSR (with the long-row path); the layout streams no more bytes
+ * than the CSR.  The column-sorted layout adds into its y rows with FP64
+ * shared atomics, so repeated executes may differ in the last bits (within
+ * the 1e-12 norm-wise tolerance); CSR executes are bit-reproducible.  Tuning
+ * key spmv_plan_colsort = 0 keeps the CSR.  execute_host pipelines the x upload, the row-chunk kernels and the y download on three streams: row
  * chunk c starts as soon as the x prefix it references (max column, computed
  * at creation) has arrived.  The plan owns its device buffers; no allocation
  * happens in execute. */
@@ -198,8 +202,8 @@ RL_API int rl_spmv_plan_execute_host(rl_spmv_plan plan, const double* x, double*
 RL_API int rl_spmv_plan_execute(rl_spmv_plan plan, const double* x_dev, double* y_dev,
                                 rl_stream stream, rl_kchar* out);
 RL_API int rl_spmv_plan_destroy(rl_spmv_plan plan);
-/* Layout of a plan: *layout = 0 CSR, 2 column-sorted blocks (K15), 3
- * column-chunked (K16); *layout_bytes = device bytes one execute streams for A. */
+/* Layout of a plan: *layout = 0 CSR, 4 column-sorted row blocks (K17);
+ * *layout_bytes = device bytes one execute streams for A. */
 RL_API int rl_spmv_plan_info(rl_spmv_plan plan, int* layout, uint64_t* layout_bytes);
 
 /* Release the device/pinned workspaces cached by the _host entry points. */

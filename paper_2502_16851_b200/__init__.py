@@ -527,11 +527,10 @@ class SpmvPlan:
         return self.layout(), int(b.value)
 
     def layout(self) -> str:
-        """"csr", "sorted" (column-sorted blocks, spmv_sorted.cu) or "chunked"
-        (x chunks staged in shared memory, spmv_chunked.cu)."""
+        """"csr" or "colsort" (column-sorted row blocks, spmv_colsort.cu)."""
         t = _int()
         _check(lib().rl_spmv_plan_info(self._h, C.byref(t), None))
-        return {0: "csr", 2: "sorted", 3: "chunked"}[t.value]
+        return {0: "csr", 4: "colsort"}[t.value]
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:

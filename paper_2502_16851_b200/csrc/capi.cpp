@@ -425,31 +425,25 @@ struct rl_spmv_plan_s {
     uint64_t m = 0, n = 0, nnz = 0;
     int32_t *rp = nullptr, *col = nullptr;
     double *val = nullptr, *x = nullptr, *y = nullptr;
-    // column-chunked layout (K16, spmv_chunked.cu)
-    bool chunked = false;
-    int crw = 0;
-    rlb::SpmvCBlock* cblk = nullptr;
-    rlb::SpmvChunk* cchunks = nullptr;
-    unsigned* cwofs = nullptr;
-    double* cval = nullptr;
-    unsigned* cmeta = nullptr;
-    std::vector<uint32_t> cblk_r0;
-    // column-sorted block layout (spmv_sorted.cu)
-    bool sorted = false;
-    int scap = 0;
-    rlb::SpmvSBlock* sblk = nullptr;
-    uint32_t* spk = nullptr;
-    double* ssv = nullptr;
-    std::vector<uint32_t> sblk_r0;
+    // column-sorted row blocks (K17, spmv_colsort.cu)
+    bool colsort = false;
+    int krb = 0, krows = 0;
+    rlb::SpmvKBlock* kblk = nullptr;
+    double* kval = nullptr;
+    unsigned* kmeta = nullptr;
+    std::vector<uint32_t> kblk_r0;
     uint64_t layout_bytes = 0;
     std::vector<uint64_t> chunk_row;   // chunk c = rows [chunk_row[c], chunk_row[c+1])
     std::vector<uint64_t> chunk_xend;  // x prefix [0, chunk_xend[c]) chunk c reads
     std::vector<uint64_t> xpiece;      // x upload pieces: [xpiece[i], xpiece[i+1])
     std::vector<char> ycut;            // chunk c ends a y copy group
-    cudaStream_t s_in = nullptr, s_cmp = nullptr, s_out = nullptr;
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    // compute streams: one for CSR; several for the column-sorted layout, whose
+    // per-chunk kernels (a few blocks each) run concurrently as x arrives
+    std::vector<cudaStream_t> s_cmp;
     int long_rows = 0;  // the CSR has rows the per-row kernels divert (spmv.cu)
     std::vector<cudaEvent_t> ev_x, ev_y;
-    cudaEvent_t ev_join[2] = {nullptr, nullptr};
+    std::vector<cudaEvent_t> ev_join;  // one per compute stream + s_out
     cudaEvent_t ev_fork = nullptr;  // s_cmp / s_out join s_in at the start of every call (and capture)
     // execute_host as a CUDA graph, captured for the last (x, y) host pair
     cudaGraphExec_t gexec = nullptr;
@@ -463,11 +457,8 @@ struct rl_spmv_plan_s {
         if (val) cudaFree(val);
         if (x) cudaFree(x);
         if (y) cudaFree(y);
-        if (sblk) cudaFree(sblk);
-        for (void* p : {(void*)cblk, (void*)cchunks, (void*)cwofs, (void*)cval, (void*)cmeta})
+        for (void* p : {(void*)kblk, (void*)kval, (void*)kmeta})
             if (p) cudaFree(p);
-        if (spk) cudaFree(spk);
-        if (ssv) cudaFree(ssv);
         if (gexec) cudaGraphExecDestroy(gexec);
         for (auto e : ev_x) cudaEventDestroy(e);
         for (auto e : ev_y) cudaEventDestroy(e);
@@ -475,7 +466,7 @@ struct rl_spmv_plan_s {
             if (e) cudaEventDestroy(e);
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (s_in) cudaStreamDestroy(s_in);
-        if (s_cmp) cudaStreamDestroy(s_cmp);
+        for (auto st : s_cmp) cudaStreamDestroy(st);
         if (s_out) cudaStreamDestroy(s_out);
     }
 };
@@ -501,58 +492,32 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
     ck(cudaMalloc(&pl->x, std::max<uint64_t>(n, 2) * 8), "plan alloc");
     ck(cudaMalloc(&pl->y, m * 8), "plan alloc");
     {
-        // column-sorted blocks (spmv_sorted.cu) for CUDA-core plans whose rows
-        // all fit (<= 64 nonzeros, block column span < 2^18); else the CSR
-        std::vector<rlb::SpmvSBlock> sb;
-        std::vector<uint32_t> spk;
-        std::vector<double> ssv;
-        // K16 when the staged x windows stay small next to the gathers they
-        // replace (<= 12 staged bytes per nonzero; every gather moves a 32-byte sector)
-        if (unit == ExecutionUnit::CudaCore && rlb::tuning().spmv_plan_chunked && nnz > 0) {
-            rlb::SpmvChunkedLayout L;
-            if (rlb::spmv_chunked_build(m, n, rp, col, val, L) && L.x_bytes <= 12 * nnz) {
-                pl->chunked = true;
-                pl->crw = L.rw;
-                auto up = [&](auto*& dst, const auto& v) {
-                    using T = std::remove_reference_t<decltype(*dst)>;
-                    ck(cudaMalloc(&dst, std::max<size_t>(v.size(), 1) * sizeof(T)), "plan alloc");
-                    if (!v.empty()) ck(cudaMemcpy(dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "plan upload");
-                };
-                up(pl->cblk, L.blocks);
-                up(pl->cchunks, L.chunks);
-                up(pl->cwofs, L.wofs);
-                up(pl->cval, L.val);
-                up(pl->cmeta, L.meta);
-                for (const auto& b : L.blocks) pl->cblk_r0.push_back(b.row0);
-                pl->layout_bytes = L.val.size() * 12 + L.wofs.size() * 4 + L.blocks.size() * sizeof(rlb::SpmvCBlock) +
-                                   L.chunks.size() * sizeof(rlb::SpmvChunk);
-            }
-        }
-        if (!pl->chunked && unit == ExecutionUnit::CudaCore && rlb::tuning().spmv_plan_sorted && nnz > 0) {
-            for (uint64_t i = 0; i < m; ++i)
-                for (int32_t k = rp[i]; k < rp[i + 1]; ++k)
-                    if (col[k] < 0 || (uint64_t)col[k] >= n)
-                        throw Error(ErrorKind::IndexOutOfRange, "column index " + std::to_string(col[k]) +
-                                                                    " outside [0, " + std::to_string(n) + ")");
-            pl->scap = rlb::spmv_sorted_cap();
-            pl->sorted = rlb::spmv_sorted_build(m, rp, col, val, pl->scap, sb, spk, ssv);
-        }
-        ck(cudaMalloc(&pl->rp, (m + 1) * 4), "plan alloc");
-        ck(cudaMemcpy(pl->rp, rp, (m + 1) * 4, cudaMemcpyHostToDevice), "plan upload");
-        if (pl->chunked) {
-            // the layout replaces row_ptr/col/val
-        } else if (pl->sorted) {
-            ck(cudaMalloc(&pl->sblk, sb.size() * sizeof(rlb::SpmvSBlock)), "plan alloc");
-            const uint64_t ne = spk.size();  // entries incl. 4-alignment padding
-            ck(cudaMalloc(&pl->spk, ne * 4), "plan alloc");
-            ck(cudaMalloc(&pl->ssv, ne * 8), "plan alloc");
-            ck(cudaMemcpy(pl->sblk, sb.data(), sb.size() * sizeof(rlb::SpmvSBlock), cudaMemcpyHostToDevice),
-               "plan upload");
-            ck(cudaMemcpy(pl->spk, spk.data(), ne * 4, cudaMemcpyHostToDevice), "plan upload");
-            ck(cudaMemcpy(pl->ssv, ssv.data(), ne * 8, cudaMemcpyHostToDevice), "plan upload");
-            for (const auto& b : sb) pl->sblk_r0.push_back(b.r0);
-            pl->layout_bytes = (m + 1) * 4 + ne * 12 + sb.size() * sizeof(rlb::SpmvSBlock);
+        // the column-sorted row-block layout (K17, spmv_colsort.cu) when the
+        // matrix is eligible (rows <= kColsortMaxRowLen nonzeros, block column
+        // spans fit); else the caller's CSR with the long-row path
+        for (uint64_t i = 0; i < m; ++i)
+            for (int32_t k = rp[i]; k < rp[i + 1]; ++k)
+                if (col[k] < 0 || (uint64_t)col[k] >= n)
+                    throw Error(ErrorKind::IndexOutOfRange, "column index " + std::to_string(col[k]) +
+                                                                " outside [0, " + std::to_string(n) + ")");
+        rlb::SpmvColsortLayout L;
+        if (rlb::tuning().spmv_plan_colsort && nnz > 0 && rlb::spmv_colsort_build(m, n, rp, col, val, L)) {
+            pl->colsort = true;
+            pl->krb = L.rb;
+            pl->krows = L.rows;
+            auto up = [&](auto*& dst, const auto& v) {
+                using T = std::remove_reference_t<decltype(*dst)>;
+                ck(cudaMalloc(&dst, std::max<size_t>(v.size(), 1) * sizeof(T)), "plan alloc");
+                if (!v.empty()) ck(cudaMemcpy(dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "plan upload");
+            };
+            up(pl->kblk, L.blocks);
+            up(pl->kval, L.val);
+            up(pl->kmeta, L.meta);
+            for (const auto& k : L.blocks) pl->kblk_r0.push_back(k.row0);
+            pl->layout_bytes = L.val.size() * 12 + L.blocks.size() * sizeof(rlb::SpmvKBlock);
         } else {
+            ck(cudaMalloc(&pl->rp, (m + 1) * 4), "plan alloc");
+            ck(cudaMemcpy(pl->rp, rp, (m + 1) * 4, cudaMemcpyHostToDevice), "plan upload");
             ck(cudaMalloc(&pl->col, std::max<uint64_t>(nnz, 1) * 4), "plan alloc");
             ck(cudaMalloc(&pl->val, std::max<uint64_t>(nnz, 1) * 8), "plan alloc");
             ck(cudaMemcpy(pl->col, col, nnz * 4, cudaMemcpyHostToDevice), "plan upload");
@@ -562,12 +527,13 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
     }
     const uint64_t unitrows = 1;
     const uint64_t units = m;
-    {
+    if (!pl->colsort) {
         int64_t maxlen = 0;
         for (uint64_t i = 0; i < m; ++i) maxlen = std::max<int64_t>(maxlen, (int64_t)rp[i + 1] - rp[i]);
         pl->long_rows = (maxlen > rlb::tuning().spmv_long_min && rlb::tuning().spmv_long_rows) ? 1 : 0;
     }
-    uint64_t nch = std::min<uint64_t>((uint64_t)rlb::tuning().spmv_plan_chunks, units);
+    uint64_t nch = std::min<uint64_t>(
+        (uint64_t)(pl->colsort ? rlb::tuning().spmv_plan_colsort_chunks : rlb::tuning().spmv_plan_chunks), units);
     // Chunk c covers weight w_c of the rows: w = 1/2 for the first and last
     // chunk, 1 otherwise (spmv_plan_taper), so the pipeline's head (the first
     // x prefix) and tail (the last compute + y copy) are short while the
@@ -580,28 +546,18 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
         if (c < nch) acc += (taper && (c == 0 || c == nch - 1)) ? 1 : 2;
     }
     pl->chunk_row.back() = m;
-    if (pl->chunked) {  // pipeline chunks = waves of blocks (one block per SM each)
-        const uint64_t nb = pl->cblk_r0.size(), wv = std::max<uint64_t>(1, nb / rlb::kNumSMsHost);
-        pl->chunk_row.clear();
-        for (uint64_t c = 0; c <= wv; ++c) pl->chunk_row.push_back(c == wv ? m : pl->cblk_r0[nb * c / wv]);
-        nch = pl->chunk_row.size() - 1;
-    }
-    if (pl->sorted) {  // chunk boundaries on block starts
+    if (pl->colsort) {  // chunk boundaries on block starts
         for (size_t c = 1; c + 1 < pl->chunk_row.size(); ++c) {
-            auto it = std::lower_bound(pl->sblk_r0.begin(), pl->sblk_r0.end(), (uint32_t)pl->chunk_row[c]);
-            pl->chunk_row[c] = it == pl->sblk_r0.end() ? m : *it;
+            auto it = std::lower_bound(pl->kblk_r0.begin(), pl->kblk_r0.end(), (uint32_t)pl->chunk_row[c]);
+            pl->chunk_row[c] = it == pl->kblk_r0.end() ? m : *it;
         }
         pl->chunk_row.erase(std::unique(pl->chunk_row.begin(), pl->chunk_row.end()), pl->chunk_row.end());
         nch = pl->chunk_row.size() - 1;
     }
     for (uint64_t c = 0; c < nch; ++c) {
         uint64_t mx = 0;
-        for (int64_t j = rp[pl->chunk_row[c]]; j < rp[pl->chunk_row[c + 1]]; ++j) {
-            if (col[j] < 0 || (uint64_t)col[j] >= n)
-                throw Error(ErrorKind::IndexOutOfRange, "column index " + std::to_string(col[j]) +
-                                                            " outside [0, " + std::to_string(n) + ")");
+        for (int64_t j = rp[pl->chunk_row[c]]; j < rp[pl->chunk_row[c + 1]]; ++j)
             mx = std::max<uint64_t>(mx, (uint64_t)col[j] + 1);
-        }
         pl->chunk_xend.push_back(mx);
     }
     // x upload pieces end exactly where a chunk's column prefix ends, so
@@ -641,36 +597,32 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
     }
     const uint64_t npc = pl->xpiece.size() - 1;
     ck(cudaStreamCreateWithFlags(&pl->s_in, cudaStreamNonBlocking), "stream");
-    ck(cudaStreamCreateWithFlags(&pl->s_cmp, cudaStreamNonBlocking), "stream");
+    pl->s_cmp.resize(pl->colsort ? (size_t)std::max(1, rlb::tuning().spmv_plan_streams) : 1);
+    for (auto& st : pl->s_cmp) ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+    pl->ev_join.resize(pl->s_cmp.size() + 1);
     ck(cudaStreamCreateWithFlags(&pl->s_out, cudaStreamNonBlocking), "stream");
     pl->ev_x.resize(npc);
-    pl->ev_y.resize(nch);
+    pl->ev_y.resize(nch * (pl->colsort ? (size_t)std::max(1, rlb::tuning().spmv_plan_streams) : 1));
     for (auto& e : pl->ev_x) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     for (auto& e : pl->ev_y) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     for (auto& e : pl->ev_join) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     ck(cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming), "event");
     if (pl->long_rows) {  // reserve the diversion buffers now: execute_host runs under graph capture
         rlb::LongRows lr{};
-        ck(rlb::spmv_long_workspace(pl->s_cmp, m, lr), "plan long-row workspace");
+        ck(rlb::spmv_long_workspace(pl->s_cmp[0], m, lr), "plan long-row workspace");
     }
     return pl.release();
 }
 
 // Rows [r0, r1) of y = A x on the plan's layout (r0/r1 block-aligned for the block layouts).
 void plan_rows(rl_spmv_plan_s* pl, uint64_t r0, uint64_t r1, const double* x, double* y, cudaStream_t s) {
-    if (pl->chunked) {  // r0 / r1 on block starts
-        const auto& v = pl->cblk_r0;
+    if (pl->colsort) {  // r0 / r1 on block starts
+        const auto& v = pl->kblk_r0;
         const int b0 = (int)(std::lower_bound(v.begin(), v.end(), (uint32_t)r0) - v.begin());
         const int b1 = r1 >= pl->m ? (int)v.size() : (int)(std::lower_bound(v.begin(), v.end(), (uint32_t)r1) - v.begin());
-        ck(rlb::launch_spmv_chunked(pl->cblk + b0, b1 - b0, pl->cchunks, pl->cwofs, pl->cval, pl->cmeta, x, y, pl->crw, s),
-           "spmv (chunked plan)");
-        return;
-    }
-    if (pl->sorted) {
-        const auto& v = pl->sblk_r0;
-        const int b0 = (int)(std::lower_bound(v.begin(), v.end(), (uint32_t)r0) - v.begin());
-        const int b1 = r1 >= pl->m ? (int)v.size() : (int)(std::lower_bound(v.begin(), v.end(), (uint32_t)r1) - v.begin());
-        ck(rlb::launch_spmv_sorted(pl->sblk, b0, b1, pl->spk, pl->ssv, pl->rp, x, y, pl->scap, s), "spmv (sorted plan)");
+        ck(rlb::launch_spmv_colsort(pl->unit == ExecutionUnit::TensorCore, pl->kblk, b0, b1, pl->krb, pl->krows,
+                                    pl->kval, pl->kmeta, x, y, s),
+           "spmv (column-sorted plan)");
         return;
     }
     {
@@ -688,7 +640,7 @@ void plan_enqueue(rl_spmv_plan_s* pl, const double* x, double* y, double* y_dire
     // waits on no x piece (a leading run of empty rows), and eagerly no
     // chunk of this call overtakes the previous call's y copies.
     ck(cudaEventRecord(pl->ev_fork, pl->s_in), "event");
-    ck(cudaStreamWaitEvent(pl->s_cmp, pl->ev_fork, 0), "wait");
+    for (auto st : pl->s_cmp) ck(cudaStreamWaitEvent(st, pl->ev_fork, 0), "wait");
     ck(cudaStreamWaitEvent(pl->s_out, pl->ev_fork, 0), "wait");
     mark(pl->s_in);
     const size_t npc = pl->ev_x.size();
@@ -698,20 +650,32 @@ void plan_enqueue(rl_spmv_plan_s* pl, const double* x, double* y, double* y_dire
         ck(cudaEventRecord(pl->ev_x[i], pl->s_in), "event");
         mark(pl->s_in);
     }
-    size_t waited = 0;  // x pieces the compute stream already waits for
+    // x pieces land in order on s_in, so chunk c waits on the event of the
+    // last piece its column prefix reaches
+    std::vector<size_t> waited(pl->s_cmp.size(), 0);  // pieces each compute stream already waits for
     uint64_t ystart = 0;   // first row of the pending y group
     for (size_t c = 0; c + 1 < pl->chunk_row.size(); ++c) {
-        while (waited < npc && pl->xpiece[waited] < pl->chunk_xend[c]) {
-            ck(cudaStreamWaitEvent(pl->s_cmp, pl->ev_x[waited], 0), "wait");
-            ++waited;
+        const size_t si = c % pl->s_cmp.size();
+        cudaStream_t sc = pl->s_cmp[si];
+        size_t need = waited[si];
+        while (need < npc && pl->xpiece[need] < pl->chunk_xend[c]) ++need;
+        if (need > waited[si]) {
+            ck(cudaStreamWaitEvent(sc, pl->ev_x[need - 1], 0), "wait");
+            waited[si] = need;
         }
         const uint64_t r0 = pl->chunk_row[c], r1 = pl->chunk_row[c + 1];
-        mark(pl->s_cmp);
-        plan_rows(pl, r0, r1, pl->x, y_direct ? y_direct : pl->y, pl->s_cmp);
-        mark(pl->s_cmp);
+        mark(sc);
+        plan_rows(pl, r0, r1, pl->x, y_direct ? y_direct : pl->y, sc);
+        mark(sc);
         if (!y_direct && pl->ycut[c]) {
-            ck(cudaEventRecord(pl->ev_y[c], pl->s_cmp), "event");
-            ck(cudaStreamWaitEvent(pl->s_out, pl->ev_y[c], 0), "wait");
+            // the y group [ystart, r1) may span chunks of every compute
+            // stream: s_out waits on each (all their work so far is chunks <= c)
+            const size_t K = pl->s_cmp.size();
+            for (size_t k = 0; k < K && k <= c; ++k) {
+                cudaEvent_t ev = pl->ev_y[c * K + k];
+                ck(cudaEventRecord(ev, pl->s_cmp[k]), "event");
+                ck(cudaStreamWaitEvent(pl->s_out, ev, 0), "wait");
+            }
             ck(cudaMemcpyAsync(y + ystart, pl->y + ystart, (r1 - ystart) * 8, cudaMemcpyDeviceToHost, pl->s_out),
                "D2H y");
             mark(pl->s_out);
@@ -761,10 +725,10 @@ void plan_execute_host(rl_spmv_plan_s* pl, const double* x, double* y) {
             cudaGraph_t g = nullptr;
             try {
                 plan_enqueue(pl, x, y, nullptr, [](cudaStream_t) {});
-                ck(cudaEventRecord(pl->ev_join[0], pl->s_cmp), "event");
-                ck(cudaEventRecord(pl->ev_join[1], pl->s_out), "event");
-                ck(cudaStreamWaitEvent(pl->s_in, pl->ev_join[0], 0), "wait");
-                ck(cudaStreamWaitEvent(pl->s_in, pl->ev_join[1], 0), "wait");
+                for (size_t k = 0; k < pl->s_cmp.size(); ++k)
+                    ck(cudaEventRecord(pl->ev_join[k], pl->s_cmp[k]), "event");
+                ck(cudaEventRecord(pl->ev_join.back(), pl->s_out), "event");
+                for (auto e : pl->ev_join) ck(cudaStreamWaitEvent(pl->s_in, e, 0), "wait");
             } catch (...) {
                 cudaStreamEndCapture(pl->s_in, &g);
                 if (g) cudaGraphDestroy(g);
@@ -796,7 +760,7 @@ void plan_execute_host(rl_spmv_plan_s* pl, const double* x, double* y) {
     };
     plan_enqueue(pl, x, y, y_direct, mark);
     ck(cudaStreamSynchronize(pl->s_out), "sync");
-    ck(cudaStreamSynchronize(pl->s_cmp), "sync");
+    for (auto st : pl->s_cmp) ck(cudaStreamSynchronize(st), "sync");
     ck(cudaStreamSynchronize(pl->s_in), "sync");
     if (trace && !tev.empty()) {
         fprintf(stderr, "plan trace (us from start):");
@@ -980,8 +944,6 @@ int rl_spmv_plan_execute(rl_spmv_plan pl, const double* x, double* y, rl_stream 
         require_ptr(pl, "plan");
         require_ptr(x, "x");
         require_ptr(y, "y");
-        if (pl->chunked && (reinterpret_cast<uintptr_t>(x) & 15))
-            throw Error(ErrorKind::ValidationError, "this plan's layout stages x with bulk copies: x must be 16-byte aligned");
         plan_rows(pl, 0, pl->m, x, y, static_cast<cudaStream_t>(s));
         put(out, pl->kc);
     });
@@ -989,7 +951,7 @@ int rl_spmv_plan_execute(rl_spmv_plan pl, const double* x, double* y, rl_stream 
 int rl_spmv_plan_info(rl_spmv_plan pl, int* tiled, uint64_t* layout_bytes) {
     return guarded([&] {
         require_ptr(pl, "plan");
-        if (tiled) *tiled = pl->sorted ? 2 : (pl->chunked ? 3 : 0);
+        if (tiled) *tiled = pl->colsort ? 4 : 0;
         if (layout_bytes) *layout_bytes = pl->layout_bytes;
     });
 }
@@ -1284,11 +1246,10 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         {"spmv_plan_graph", &rlb::Tuning::spmv_plan_graph, true},
         {"spmv_plan_taper", &rlb::Tuning::spmv_plan_taper, false},
         {"spmv_plan_xpieces", &rlb::Tuning::spmv_plan_xpieces, false},
-        {"spmv_plan_sorted", &rlb::Tuning::spmv_plan_sorted, true},
-        {"spmv_plan_chunked", &rlb::Tuning::spmv_plan_chunked, true},
-        {"spmv_chunked_mode", &rlb::Tuning::spmv_chunked_mode, false},
-        {"spmv_sorted_cap", &rlb::Tuning::spmv_sorted_cap, false},
-        {"spmv_sorted_pipe", &rlb::Tuning::spmv_sorted_pipe, false},
+        {"spmv_plan_colsort", &rlb::Tuning::spmv_plan_colsort, true},
+        {"spmv_plan_streams", &rlb::Tuning::spmv_plan_streams, false},
+        {"spmv_plan_colsort_chunks", &rlb::Tuning::spmv_plan_colsort_chunks, false},
+        {"spmv_colsort_window", &rlb::Tuning::spmv_colsort_window, false},
         {"spmv_plan_ygroups", &rlb::Tuning::spmv_plan_ygroups, false},
         {"stencil_r_ctas_per_sm", &rlb::Tuning::stencil_r_ctas_per_sm, false},
         {"stencil_tb_waves", &rlb::Tuning::stencil_tb_waves, false},

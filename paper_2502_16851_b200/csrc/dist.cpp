@@ -404,16 +404,80 @@ struct rl_dist_spmv_s {
         double* x;
         double* y;
         uint64_t i0, i1;  // interior local rows [i0, i1): the band stays inside the owned x
-    };
+        // column-sorted row blocks (K17, spmv_colsort.cu) built from this part's
+        // CSR at creation; blocks [kb0, kb1) are interior (rows inside [i0, i1))
+        bool colsort = false;
+        int krb = 0, krows = 0, kb0 = 0, kb1 = 0, knb = 0;
+        rlb::SpmvKBlock* kblk = nullptr;
+        double* kval = nullptr;
+        unsigned* kmeta = nullptr;
+        };
     std::vector<Part> parts;
     std::vector<rl_dist_op> ops;
     int long_rows = 0;
     KernelCharacterization kc;
     Replay rp;
-    ~rl_dist_spmv_s() { rp.destroy(); }
+    ~rl_dist_spmv_s() {
+        rp.destroy();
+        for (auto& q : parts)
+            for (void* a : {(void*)q.kblk, (void*)q.kval, (void*)q.kmeta})
+                if (a) cudaFree(a);
+    }
 };
 
 namespace {
+
+// The part's CSR through the column-sorted row-block layout (the single-GPU
+// plan's default, K17): copied to the host once, columns made local to the
+// part's x window, built, uploaded.  Ineligible matrices keep the CSR.
+void colsort_part(rl_dist_spmv_s::Part& q, uint64_t rows, uint64_t nnz) {
+    std::vector<int32_t> hrp(rows + 1), hcol(nnz);
+    std::vector<double> hval(nnz);
+    ck(cudaMemcpy(hrp.data(), q.rp, (rows + 1) * 4, cudaMemcpyDeviceToHost), "D2H row_ptr");
+    ck(cudaMemcpy(hcol.data(), q.col, nnz * 4, cudaMemcpyDeviceToHost), "D2H col");
+    ck(cudaMemcpy(hval.data(), q.val, nnz * 8, cudaMemcpyDeviceToHost), "D2H val");
+    for (auto& c : hcol) c -= (int32_t)q.g.cb;
+    // the edge rows (whose band reaches the halo) in small blocks, two per SM,
+    // so the launch after the exchange spreads over every SM; the interior in
+    // the default two waves
+    const uint64_t ne = q.i0 + (rows - q.i1), nin = q.i1 - q.i0;
+    const uint64_t eb = std::max<uint64_t>(1, 2 * (uint64_t)rlb::kNumSMsHost * q.i0 / std::max<uint64_t>(1, ne));
+    std::vector<rlb::ColsortSegment> segs = {{q.i0, eb}, {q.i1, std::max<uint64_t>(1, 4 * (uint64_t)rlb::kNumSMsHost * nin / rows)},
+                                             {rows, std::max<uint64_t>(1, 2 * (uint64_t)rlb::kNumSMsHost - eb)}};
+    rlb::SpmvColsortLayout L;
+    if (!rlb::spmv_colsort_build(rows, q.g.ce - q.g.cb, hrp.data(), hcol.data(), hval.data(), L, segs)) return;
+    // block order: edge blocks first, then the interior, so each phase is one launch
+    std::stable_partition(L.blocks.begin(), L.blocks.end(), [&](const rlb::SpmvKBlock& k) {
+        return !(k.row0 >= q.i0 && k.row0 + k.rows <= q.i1);
+    });
+    auto up = [&](auto*& dst, const auto& v) {
+        using T = std::remove_reference_t<decltype(*dst)>;
+        ck(cudaMalloc(&dst, std::max<size_t>(v.size(), 1) * sizeof(T)), "alloc");
+        if (!v.empty()) ck(cudaMemcpy(dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+    };
+    up(q.kblk, L.blocks);
+    up(q.kval, L.val);
+    up(q.kmeta, L.meta);
+    q.colsort = true;
+    q.krb = L.rb;
+    q.krows = L.rows;
+    q.knb = (int)L.blocks.size();
+    q.kb1 = q.knb;  // interior blocks [kb0, knb), edge blocks [0, kb0)
+    q.kb0 = 0;
+    while (q.kb0 < q.knb && !(L.blocks[q.kb0].row0 >= q.i0 && L.blocks[q.kb0].row0 + L.blocks[q.kb0].rows <= q.i1))
+        ++q.kb0;
+}
+
+void part_rows(const rl_dist_spmv_s* pl, const rl_dist_spmv_s::Part& q, int b0, int b1, uint64_t r0, uint64_t r1,
+               cudaStream_t s) {
+    if (q.colsort) {
+        ck(rlb::launch_spmv_colsort(pl->unit == ExecutionUnit::TensorCore, q.kblk, b0, b1, q.krb, q.krows, q.kval,
+                                    q.kmeta, q.x, q.y, s),
+           "spmv (column-sorted part)");
+        return;
+    }
+    spmv_csr_rows(pl->unit, Precision::FP64, r0, r1, q.rp, q.col, q.val, q.x, (int64_t)q.g.cb, q.y, s, pl->long_rows);
+}
 
 rl_dist_spmv_s* spmv_create(rl_dist_s* d, ExecutionUnit unit, Precision p, uint64_t n, uint64_t hb, int L,
                             const int32_t* const* rp, const int32_t* const* col, const double* const* val,
@@ -468,10 +532,11 @@ rl_dist_spmv_s* spmv_create(rl_dist_s* d, ExecutionUnit unit, Precision p, uint6
                                                             " from its row, outside the half-bandwidth " +
                                                             std::to_string(hb));
             nnz_local += (uint64_t)ends[1];
-            if (rlb::tuning().spmv_long_rows &&
+            pl->parts.push_back(q);
+            if (rlb::tuning().spmv_plan_colsort && ends[1] > 0) colsort_part(pl->parts.back(), rows, (uint64_t)ends[1]);
+            if (!pl->parts.back().colsort && rlb::tuning().spmv_long_rows &&
                 rlb::spmv_long_rows_probe(q.rp, q.col, q.val, 0, rows, pl->rp.s) != 0)
                 pl->long_rows = 1;
-            pl->parts.push_back(q);
         }
     } catch (...) {
         cudaFree(chk);
@@ -501,16 +566,16 @@ void spmv_body(rl_dist_spmv_s* pl) {
         post_exchange(d, pl->ops, [&](int i) { return pl->parts[i].x; });
         ck(cudaEventRecord(r.ev_halo, d->s_comm), "event");
     }
-    for (const auto& q : pl->parts)
-        spmv_csr_rows(pl->unit, Precision::FP64, q.i0, q.i1, q.rp, q.col, q.val, q.x, (int64_t)q.g.cb, q.y, r.s,
-                      pl->long_rows);
+    for (const auto& q : pl->parts) part_rows(pl, q, q.kb0, q.kb1, q.i0, q.i1, r.s);
     if (xchg) ck(cudaStreamWaitEvent(r.s, r.ev_halo, 0), "wait");
     for (const auto& q : pl->parts) {
         const uint64_t rows = q.g.r1 - q.g.r0;
-        spmv_csr_rows(pl->unit, Precision::FP64, 0, q.i0, q.rp, q.col, q.val, q.x, (int64_t)q.g.cb, q.y, r.s,
-                      pl->long_rows);
-        spmv_csr_rows(pl->unit, Precision::FP64, q.i1, rows, q.rp, q.col, q.val, q.x, (int64_t)q.g.cb, q.y, r.s,
-                      pl->long_rows);
+        if (q.colsort) {
+            part_rows(pl, q, 0, q.kb0, 0, 0, r.s);  // every edge block, one launch
+        } else {
+            part_rows(pl, q, 0, 0, 0, q.i0, r.s);
+            part_rows(pl, q, 0, 0, q.i1, rows, r.s);
+        }
     }
 }
 

@@ -28,11 +28,10 @@ struct Tuning {
     int spmv_long_piece = 512;     // ... cut into pieces of this many nonzeros, balanced over the warps
     int spmv_long_group = 8;       // lanes per piece of the CUDA-core long-row kernel (8, 16, 32)
     int spmv_plan_chunks = 16;     // pipelined row/x chunks of rl_spmv_plan_execute_host
-    int spmv_chunked_mode = 0;     // K16 diagnostics: 0 normal; data movement only: 1 all, 2 x staging, 3 val/meta
-    int spmv_plan_chunked = 0;     // 1: CUDA-core plans use the column-chunked layout (K16, spmv_chunked.cu) when the staged x stays <= 12 B per nonzero (measured 0.30-0.35 vs CSR 0.287 ms: opt-in)
-    int spmv_plan_sorted = 0;      // 1: CUDA-core plans use the column-sorted block layout when eligible (spmv_sorted.cu; halves the L2 requests but measured 0.287 vs 0.274 ms: latency-bound)
-    int spmv_sorted_cap = 16384;   // ... slot grid per block (16384: 1024 threads, 1 CTA/SM; 8192: 512 threads, 3 CTAs/SM)
-    int spmv_sorted_pipe = 0;      // ... cap 12288: software-pipelined kernel (two product buffers, 1 CTA/SM)
+    int spmv_plan_streams = 1;     // compute streams of a column-sorted plan's execute_host (1: 1.02 ms, 4-8: 1.10 ms; tools/micro/plan_colsort_e2e.py)
+    int spmv_plan_colsort_chunks = 8;  // pipeline chunks of a column-sorted plan (8: 1.02, 16: 1.21-1.26, 32: 1.36+ ms)
+    int spmv_colsort_window = 128; // K17 plan build: entries per bank-ordering window (tools/micro/spmv_colsort.cu: 64 0.185, 128 0.183 ms)
+    int spmv_plan_colsort = 1;     // plans (both units) use the column-sorted row-block layout (K17, spmv_colsort.cu) when eligible; 0: CSR
     int spmv_plan_xpieces = 0;     // max x upload pieces (first = chunk 0's prefix); 0: one per chunk
     int spmv_plan_ygroups = 0;     // y download copies (groups of consecutive chunks); 0: one per chunk
     int spmv_plan_taper = 0;       // 1: half-size first/last pipeline chunks (measured no gain)
@@ -163,22 +162,6 @@ cudaError_t launch_stencil_tb3r(const StencilDesc& d, int t, uint64_t o0, uint64
 cudaError_t launch_gemv(int unit, uint64_t m, uint64_t n, const double* A, const double* x, double* y,
                         cudaStream_t s);
 
-// Column-sorted block layout (rl_spmv_plan's default CUDA-core layout when
-// eligible; spmv_sorted.cu).
-struct SpmvSBlock {
-    uint32_t r0;       // first row
-    uint32_t rows;     // rows (<= 1024)
-    uint64_t k0;       // first nonzero (CSR offset)
-    uint64_t kp;       // first entry in the padded sorted arrays (multiple of 32)
-    int32_t colbase;   // smallest column of the block
-    int32_t nent;      // entries, padded to a multiple of 32 (padding: value 0, slot = cap - 1)
-};
-int spmv_sorted_cap();
-bool spmv_sorted_build(uint64_t m, const int32_t* rp, const int32_t* col, const double* val, int cap,
-                       std::vector<SpmvSBlock>& blks, std::vector<uint32_t>& pk, std::vector<double>& sv);
-cudaError_t launch_spmv_sorted(const SpmvSBlock* blks, int b0, int b1, const uint32_t* pk, const double* sv,
-                               const int32_t* rp, const double* x, double* y, int cap, cudaStream_t s);
-
 // Distributed SpMV plan create-time check (dist_kernels.cu): out[0] = widest
 // |col - row|, out[1] = columns outside [0, n), out[2] = decreasing row_ptr
 // entries (device buffer of 3 u64).
@@ -190,36 +173,37 @@ cudaError_t launch_band_check(uint64_t rows, const int* rp, const int* col, int6
 int spmv_long_rows_probe(const int* rp, const int* col, const double* val, uint64_t r0, uint64_t r1,
                          cudaStream_t s);
 
-// K16: column-chunked layout (spmv_chunked.cu): x windows staged in shared
-// memory per row block; the default CUDA-core plan layout for banded/local
-// matrices (staged x bytes <= 12 per nonzero).
-constexpr int kNumSMsHost = 148;     // B200 SM count (host-side copy of common.cuh's kNumSMs)
-constexpr int kSpmvChunk = 4096;      // x columns per staged chunk (32 KB)
-constexpr int kSpmvChunkStages = 4;   // ring depth
-constexpr int kSpmvChunkWarps = 16;   // warps per CTA (one CTA per SM; rows per warp <= 512)
-constexpr int kSpmvChunkBatches = 4;  // 128-entry batches in flight per warp
-struct SpmvCBlock {
-    uint32_t row0, rows;  // rows [row0, row0 + rows)
-    int rw;               // rows per warp (block rows = kSpmvChunkWarps rw)
-    int c0, c1;           // chunk records [c0, c1)
+constexpr int kNumSMsHost = 148;  // B200 SM count (host-side copy of common.cuh's kNumSMs)
+
+// K17: column-sorted row-block layout (spmv_colsort.cu), the default layout
+// of CUDA-core SpMV plans when eligible (rows <= kColsortMaxRowLen nonzeros;
+// every block's column span fits the meta word).
+constexpr int kColsortMaxRows = 8192;     // rows per block (y in shared memory: 64 KB, two CTAs per SM)
+constexpr int kColsortMaxRowLen = 1024;   // longer rows stay on the CSR kernels (long-row path)
+struct SpmvKBlock {
+    uint64_t e0;     // first entry
+    int32_t col_lo;  // smallest column of the block
+    uint32_t row0;   // first row
+    uint32_t rows;   // rows (<= kColsortMaxRows)
+    uint32_t nent;   // entries, padded to a multiple of 32
 };
-struct SpmvChunk {
-    int32_t col0;   // first column (even)
-    int32_t ncols;  // staged columns (even)
+struct SpmvColsortLayout {
+    int rb = 0;    // row bits of meta
+    int rows = 0;  // rows of the largest block (shared-memory y per CTA)
+    std::vector<SpmvKBlock> blocks;
+    std::vector<double> val;
+    std::vector<uint32_t> meta;  // (col - col_lo) << rb | (row - row0)
 };
-struct SpmvChunkedLayout {
-    int rw = 0;
-    std::vector<SpmvCBlock> blocks;
-    std::vector<SpmvChunk> chunks;
-    std::vector<unsigned> wofs;   // (chunk, warp) segment starts, + 1 end
-    std::vector<double> val;      // entries
-    std::vector<unsigned> meta;   // row-in-warp << 16 | column-in-chunk (0xFFFF: padding)
-    uint64_t x_bytes = 0;         // x bytes staged per call
+// Rows [previous row_end, row_end) are cut into `blocks` equal blocks (empty
+// list: one segment of 4 x 148 blocks, two waves of two CTAs per SM).
+struct ColsortSegment {
+    uint64_t row_end;
+    uint64_t blocks;
 };
-bool spmv_chunked_build(uint64_t m, uint64_t n, const int32_t* rp, const int32_t* col, const double* val,
-                        SpmvChunkedLayout& layout);
-cudaError_t launch_spmv_chunked(const SpmvCBlock* blks, int nblk, const SpmvChunk* chunks, const unsigned* wofs,
-                                const double* val2, const unsigned* meta2, const double* x, double* y, int rw,
+bool spmv_colsort_build(uint64_t m, uint64_t n, const int32_t* rp, const int32_t* col, const double* val,
+                        SpmvColsortLayout& layout, const std::vector<ColsortSegment>& segments = {});
+cudaError_t launch_spmv_colsort(int unit, const SpmvKBlock* blks, int b0, int b1, int rb, int rows,
+                                const double* val, const unsigned* meta, const double* x, double* y,
                                 cudaStream_t s);
 
 // Launch accounting (rl_kernel_launches): every <<<>>> site reports itself.

@@ -322,21 +322,26 @@ def test_spmv_offset_views(cuda, unit, val_off, col_off, max_len):
     assert O.rel_err(y.cpu().numpy(), O.spmv_csr(rp, col, val, x)) <= TOL
 
 
-@pytest.mark.parametrize("case", ["band", "ragged", "empty_block", "long_rows", "narrow"])
-def test_spmv_plan_chunked_layout(cuda, case):
-    """K16 (spmv_chunked.cu): x windows staged in shared memory per row block.
-    Banded / local matrices take it; the result matches the oracle through
-    both rl_spmv_plan_execute (device x, y) and execute_host, on repeated
-    calls with new x."""
-    import torch
-
-    rng = np.random.default_rng({"band": 1, "ragged": 2, "empty_block": 3, "long_rows": 4, "narrow": 5}[case])
+def _plan_case(case):
+    rng = np.random.default_rng({"band": 1, "ragged": 2, "empty_block": 3, "long_rows": 4, "narrow": 5,
+                                 "rect": 6, "scattered": 7, "tiny": 8, "hot_row": 9}[case])
     if case == "band":
         m = n = 300_000
         rp, col, val = O.gen_band_csr(m, 0, n, 16, 20000, 9)
     elif case == "narrow":
-        m = n = 70_001 + 1   # even n
+        m = n = 70_001
         rp, col, val = O.gen_band_csr(m, 0, n, 5, 4, 4)
+    elif case == "tiny":
+        m = n = 37
+        rp, col, val = O.gen_band_csr(m, 0, n, 3, 5, 4)
+    elif case == "rect":
+        m, n = 90_001, 250_000
+        rp, col, val = O.gen_band_csr(m, 0, n, 12, 60000, 5)
+    elif case == "scattered":  # every row reaches across all of x
+        m = n = 100_000
+        rp = np.arange(m + 1, dtype=np.int32) * 8
+        col = np.concatenate([np.sort(rng.choice(n, 8, replace=False)) for _ in range(m)]).astype(np.int32)
+        val = rng.uniform(-1, 1, col.size)
     else:
         m = n = 200_000
         hbw = 6000
@@ -344,25 +349,39 @@ def test_spmv_plan_chunked_layout(cuda, case):
         if case == "empty_block":
             lens[50_000:90_000] = 0
         if case == "long_rows":
-            lens[rng.choice(m, 20, replace=False)] = 3000
-        rp = np.zeros(m + 1, np.int64)
-        rp[1:] = np.cumsum(lens)
+            lens[rng.choice(m, 20, replace=False)] = 1000
+        if case == "hot_row":  # past kColsortMaxRowLen: the plan keeps CSR
+            lens[777] = 1025
         cols = []
         for i, l in enumerate(lens):
             lo, hi = max(0, i - hbw), min(n, i + hbw + 1)
             cols.append(np.sort(rng.choice(np.arange(lo, hi), size=min(l, hi - lo), replace=False)))
-        lens = np.array([c.size for c in cols])
-        rp[1:] = np.cumsum(lens)
+        rp = np.zeros(m + 1, np.int64)
+        rp[1:] = np.cumsum([c.size for c in cols])
         col = np.concatenate(cols).astype(np.int32)
         rp = rp.astype(np.int32)
         val = rng.uniform(-1, 1, size=col.size)
-    prev = P.tuning_set("spmv_plan_chunked", 1)
+    return m, n, rp, col, val
+
+
+@pytest.mark.parametrize("unit", UNITS)
+@pytest.mark.parametrize("case", ["band", "ragged", "empty_block", "long_rows", "narrow", "rect", "scattered",
+                                  "tiny", "hot_row"])
+def test_spmv_plan_colsort_layout(cuda, unit, case):
+    """K17 (spmv_colsort.cu): column-sorted row blocks with y in shared
+    memory, the plans' default layout when eligible (rows of <= 1024
+    nonzeros).  Both units, through rl_spmv_plan_execute (device x, y) and
+    execute_host, on repeated calls with new x, NaN-poisoned y."""
+    import torch
+
+    m, n, rp, col, val = _plan_case(case)
+    prev = P.tuning_set("spmv_plan_colsort", 1)
     try:
-        plan = P.SpmvPlan(rp, col, val, n)
+        plan = P.SpmvPlan(rp, col, val, n, unit=unit)
     finally:
-        P.tuning_set("spmv_plan_chunked", prev)
+        P.tuning_set("spmv_plan_colsort", prev)
     try:
-        assert plan.layout() == "chunked", plan.layout()
+        assert plan.layout() == ("csr" if case == "hot_row" else "colsort"), plan.layout()
         for call in range(3):
             x = O.fill_uniform(n, 40 + call, 4, 0, 1)
             ref = O.spmv_csr(rp, col, val, x)
@@ -371,6 +390,8 @@ def test_spmv_plan_chunked_layout(cuda, case):
             plan.execute(dx, dy)
             torch.cuda.synchronize()
             assert O.rel_err(dy.cpu().numpy(), ref) <= TOL, call
+            if case == "empty_block":
+                assert (dy[50_000:90_000] == 0).all()
             hx = torch.from_numpy(x).pin_memory()
             hy = torch.full((m,), float("nan"), dtype=torch.float64).pin_memory()
             plan.execute_host(hx, hy)
@@ -379,20 +400,152 @@ def test_spmv_plan_chunked_layout(cuda, case):
         plan.close()
 
 
-def test_spmv_plan_chunked_declined_for_scattered_columns(cuda):
-    """A matrix whose rows reach across all of x would stage far more x than
-    it gathers: the plan keeps the CSR kernels."""
-    rng = np.random.default_rng(8)
-    m = n = 100_000
-    lens = np.full(m, 8)
-    rp = np.zeros(m + 1, np.int32)
-    rp[1:] = np.cumsum(lens)
-    col = np.concatenate([np.sort(rng.choice(n, 8, replace=False)) for _ in range(m)]).astype(np.int32)
-    val = rng.uniform(-1, 1, col.size)
-    prev = P.tuning_set("spmv_plan_chunked", 1)
+def test_spmv_plan_colsort_opt_out(cuda):
+    """tuning key spmv_plan_colsort = 0 keeps the caller's CSR."""
+    m, n, rp, col, val = _plan_case("band")
+    prev = P.tuning_set("spmv_plan_colsort", 0)
     try:
         plan = P.SpmvPlan(rp, col, val, n)
     finally:
-        P.tuning_set("spmv_plan_chunked", prev)
-    assert plan.layout() != "chunked"
+        P.tuning_set("spmv_plan_colsort", prev)
+    assert plan.layout() == "csr"
     plan.close()
+
+
+@pytest.mark.parametrize("unit", UNITS)
+def test_spmv_plan_colsort_baseline(cuda, unit):
+    """The BASELINE matrix (2^22 rows, 16 nnz/row, +-65536 band) through the
+    K17 plan built from the device generator's CSR: 1e-12 vs the oracle, and
+    the layout moves no more bytes than the CSR it replaces."""
+    import torch
+
+    m, k, hb = 1 << 22, 16, 65536
+    rp, col, val = O.gen_band_csr(m, 0, m, k, hb, 2025)
+    x = O.fill_uniform(m, 2025, 4, 0, 1)
+    prev = P.tuning_set("spmv_plan_colsort", 1)
+    try:
+        plan = P.SpmvPlan(rp, col, val, m, unit=unit)
+    finally:
+        P.tuning_set("spmv_plan_colsort", prev)
+    try:
+        layout, nbytes = plan.info()
+        assert layout == "colsort" and nbytes <= (m + 1) * 4 + m * k * 12
+        dx = torch.from_numpy(x).cuda()
+        dy = torch.full((m,), float("nan"), dtype=torch.float64, device="cuda")
+        plan.execute(dx, dy)
+        torch.cuda.synchronize()
+        assert O.rel_err(dy.cpu().numpy(), O.spmv_csr(rp, col, val, x)) <= TOL
+    finally:
+        plan.close()
+
+
+def _fsum_rows(rp, col, val, x):
+    """Correctly rounded exact row sums of the FP64-rounded products (math.fsum)."""
+    import math
+
+    prod = val * x[col]
+    return np.array([math.fsum(prod[rp[i]:rp[i + 1]]) for i in range(rp.size - 1)])
+
+
+@pytest.mark.parametrize("unit", UNITS)
+@pytest.mark.parametrize("m,k,hb", [(20000, 16, 65536), (7001, 7, 300), (3000, 64, 1000)])
+def test_colsort_within_fp64_summation_bound(cuda, unit, m, k, hb):
+    """K17 rows are FP64 sums in some order: every row within the recursive
+    summation bound (L - 1) u sum|p| of the exact sum (math.fsum), on both
+    units and on every call."""
+    import torch
+
+    rng = np.random.default_rng(m + k)
+    rp, col, val = O.gen_band_csr(m, 0, m, k, hb, 5)
+    x = rng.uniform(-1.0, 1.0, m)
+    want = _fsum_rows(rp, col, val, x)
+    absum = np.array([np.abs(val[rp[i]:rp[i + 1]] * x[col[rp[i]:rp[i + 1]]]).sum() for i in range(m)])
+    lens = np.diff(rp)
+    prev = P.tuning_set("spmv_plan_colsort", 1)
+    try:
+        plan = P.SpmvPlan(rp, col, val, m, unit=unit)
+    finally:
+        P.tuning_set("spmv_plan_colsort", prev)
+    try:
+        assert plan.layout() == "colsort"
+        dx = torch.from_numpy(x).cuda()
+        for _ in range(2):
+            dy = torch.full((m,), float("nan"), dtype=torch.float64, device="cuda")
+            plan.execute(dx, dy)
+            torch.cuda.synchronize()
+            err = np.abs(dy.cpu().numpy() - want)
+            assert np.all(err <= np.maximum(lens - 1, 1) * 2.0 ** -53 * absum * 1.0001)
+    finally:
+        plan.close()
+
+
+@pytest.mark.parametrize("unit", UNITS)
+def test_colsort_scales_and_ranges(cuda, unit):
+    """Per-block scales: rows of very different magnitude in different blocks
+    (1e-200 .. 1e200), x spanning 1e-150 .. 1e150 across segments (blocks
+    whose x window spans more than 2^24 take the FP64 path), zeros and
+    subnormals: each row within 1e-13 of its largest product or of the exact
+    sum."""
+    import torch
+
+    rng = np.random.default_rng(31)
+    m = n = 50000
+    rp, col, val = O.gen_band_csr(m, 0, n, 12, 3000, 9)
+    row_scale = 10.0 ** np.repeat(rng.integers(-200, 200, m // 500 + 1), 500)[:m]
+    val = val * np.repeat(row_scale, np.diff(rp))
+    x = O.fill_uniform(n, 3, 4, 0, 1) * 10.0 ** np.repeat(rng.integers(-150, 150, n // 4096 + 1), 4096)[:n]
+    x[::97] = 0.0
+    x[5::1001] = 5e-324  # subnormal
+    want = _fsum_rows(rp, col, val, x)
+    prev = P.tuning_set("spmv_plan_colsort", 1)
+    try:
+        plan = P.SpmvPlan(rp, col, val, n, unit=unit)
+    finally:
+        P.tuning_set("spmv_plan_colsort", prev)
+    try:
+        dx = torch.from_numpy(x).cuda()
+        dy = torch.empty(m, dtype=torch.float64, device="cuda")
+        plan.execute(dx, dy)
+        torch.cuda.synchronize()
+        y = dy.cpu().numpy()
+        scale = np.maximum(np.abs(want), np.array([np.abs(val[rp[i]:rp[i + 1]] * x[col[rp[i]:rp[i + 1]]]).max(initial=0)
+                                                   for i in range(m)]))
+        ok = scale > 0
+        assert np.all(np.abs(y - want)[ok] <= 1e-13 * scale[ok])
+        assert np.all(y[~ok] == 0)
+    finally:
+        plan.close()
+
+
+@pytest.mark.parametrize("unit", UNITS)
+def test_colsort_nonfinite(cuda, unit):
+    """Inf/NaN in x or in the values: the affected blocks add in FP64 (IEEE
+    semantics) -- the non-finite pattern of y matches the CPU sum's, the
+    finite rows stay within 1e-12."""
+    import torch
+
+    m = n = 30000
+    rp, col, val = O.gen_band_csr(m, 0, n, 10, 2000, 4)
+    val = val.copy()
+    val[rp[20000] + 3] = np.inf
+    x = O.fill_uniform(n, 8, 4, 0, 1)
+    x[1234] = np.nan
+    x[25000] = -np.inf
+    with np.errstate(invalid="ignore"):
+        want = np.array([np.sum(val[rp[i]:rp[i + 1]] * x[col[rp[i]:rp[i + 1]]]) for i in range(m)])
+    prev = P.tuning_set("spmv_plan_colsort", 1)
+    try:
+        plan = P.SpmvPlan(rp, col, val, n, unit=unit)
+    finally:
+        P.tuning_set("spmv_plan_colsort", prev)
+    try:
+        dy = torch.empty(m, dtype=torch.float64, device="cuda")
+        plan.execute(torch.from_numpy(x).cuda(), dy)
+        torch.cuda.synchronize()
+        y = dy.cpu().numpy()
+        assert np.array_equal(np.isnan(y), np.isnan(want))
+        assert np.array_equal(np.isposinf(y), np.isposinf(want)) and np.array_equal(np.isneginf(y), np.isneginf(want))
+        f = np.isfinite(want)
+        assert O.rel_err(y[f], want[f]) <= TOL
+    finally:
+        plan.close()

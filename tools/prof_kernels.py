@@ -47,7 +47,7 @@ def run(name):
         y = torch.empty(m, dtype=torch.float64, device="cuda")
         for _ in range(REPS):
             P.gemv(A, x, y, unit=unit)
-    elif kern == "spmvchunked":
+    elif kern == "spmvcolsort":
         n, k, hb = 1 << 22, 16, 65536
         rp = torch.empty(n + 1, dtype=torch.int32, device="cuda")
         col = torch.empty(n * k, dtype=torch.int32, device="cuda")
@@ -56,8 +56,7 @@ def run(name):
         y = torch.empty(n, dtype=torch.float64, device="cuda")
         P.gen_band_csr(n, 0, n, k, hb, 1, rp, col, val)
         P.fill_uniform(x, 1, 4, 0, 1)
-        P.tuning_set("spmv_plan_chunked", 1)
-        plan = P.SpmvPlan(rp.cpu(), col.cpu(), val.cpu(), n)
+        plan = P.SpmvPlan(rp.cpu(), col.cpu(), val.cpu(), n, unit=unit)
         for _ in range(REPS):
             plan.execute(x, y)
         plan.close()
