@@ -523,40 +523,50 @@ def cusparse_yardstick(torch, P, hbm, reps=20):
     return out
 
 
-def temporal_blocking(torch, P, hbm, t1_ms_per_step, t1_ms_per_step_3d=None, depths=(2, 3, 4, 5, 7),
-                      depths_3d=(2, 3, 4)):
-    """2d5pt (16384^2, 100 timesteps) and 3d7pt (512^3, 50
-    timesteps) with temporal depth t on the BASELINE grids: floor(steps/t)
-    fused sweeps + the remainder as single steps.  Model bytes are
-    stencil_model(preset, FP64, t): 16 B per point per fused sweep (reference
-    kernels.cpp:137-155)."""
+def temporal_blocking(torch, P, hbm, t1_ms, balance=None):
+    """temporal depth t on the BASELINE grids -- 2d5pt
+    (16384^2, 100 timesteps) on both units, 3d7pt and 3d27pt (512^3, 50
+    timesteps) on the CUDA core: floor(steps/t) fused sweeps + the remainder
+    as single steps.  Model bytes are stencil_model(preset, FP64, t): 16 B per
+    point per fused sweep (reference kernels.cpp:137-155).  t1_ms: the
+    single-step ms per timestep per (preset, unit) from the kernel table.
+    min_temporal_depth (bounds.cpp:111-125) at the measured balance is the
+    depth from which the fused sweep is compute-bound."""
     out = {}
-    for preset, shape, steps, ds, t1 in (("2d5pt", (16384, 16384), 100, depths, t1_ms_per_step),
-                                          ("3d7pt", (512, 512, 512), 50, depths_3d, t1_ms_per_step_3d)):
+    runs = (("2d5pt", (16384, 16384), 100, ((2, 3, 4, 5, 7), (2, 3, 4))),
+            ("3d7pt", (512, 512, 512), 50, ((2, 3, 4), ())),
+            ("3d27pt", (512, 512, 512), 50, ((2, 3, 4), ())))
+    for preset, shape, steps, (ds_cc, ds_tc) in runs:
         u = torch.empty(shape, dtype=torch.float64, device="cuda")
         P.stencil_init(u, 1, SEED)
         v = u.clone()
-        for t in ds:
-            P.stencil_temporal(preset, u, v, 2 * t, t)
-            torch.cuda.synchronize()
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record()
-            kc, _ = P.stencil_temporal(preset, u, v, steps, t)
-            e.record()
-            torch.cuda.synchronize()
-            ms = s.elapsed_time(e)
-            gbs = kc.traffic_bytes / (ms * 1e-3) / 1e9
-            row = {"ms_per_timestep": round(ms / steps, 4), "model_gbs": round(gbs, 1),
-                   "frac_of_measured_peak": round(gbs / hbm, 4)}
-            if t1:
-                row["timestep_speedup_vs_t1"] = round(t1 / (ms / steps), 3)
-            out[f"{preset}_t{t}"] = row
+        for uname, unit, ds in (("cc", P.CUDA_CORE, ds_cc), ("tc", P.TENSOR_CORE, ds_tc)):
+            for t in ds:
+                P.stencil_temporal(preset, u, v, 2 * t, t, unit=unit)
+                torch.cuda.synchronize()
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record()
+                kc, _ = P.stencil_temporal(preset, u, v, steps, t, unit=unit)
+                e.record()
+                torch.cuda.synchronize()
+                ms = s.elapsed_time(e)
+                gbs = kc.traffic_bytes / (ms * 1e-3) / 1e9
+                row = {"ms_per_timestep": round(ms / steps, 4), "model_gbs": round(gbs, 1),
+                       "frac_of_measured_peak": round(gbs / hbm, 4),
+                       "tflops": round(kc.work_flops / (ms * 1e-3) / 1e12, 2)}
+                t1 = t1_ms.get((preset, uname))
+                if t1:
+                    row["timestep_speedup_vs_t1"] = round(t1 / (ms / steps), 3)
+                out[f"{preset}_t{t}" + ("" if uname == "cc" else "_tc")] = row
+        if balance:
+            out[f"{preset}_min_temporal_depth"] = P.min_temporal_depth(balance, P.stencil_model(preset).intensity)
         del u, v
         torch.cuda.empty_cache()
-    out["note"] = ("2d5pt: register-pipelined strips (stencil_tb.cu); 3d7pt: register-blocked TMA tiles, one "
-                   "barrier per plane (stencil_tb3r.cu).  One HBM read + write per t timesteps; bytes = "
-                   "stencil_model(t) per fused sweep, so model_gbs falls as t rises while the per-timestep "
-                   "time drops")
+    out["note"] = ("2d5pt CC: register-pipelined strips (stencil_tb.cu); 2d5pt TC: overlapped 64x64 tiles in "
+                   "shared memory, each level the x-band-on-DMMA form (stencil_tbtc.cu); 3d7pt: register-blocked "
+                   "TMA tiles (stencil_tb3r.cu); 3d27pt: z-column kernel with three partial-sum planes per level "
+                   "(stencil_tb3.cu).  One HBM read + write per t timesteps; bytes = stencil_model(t) per fused "
+                   "sweep, so model_gbs falls as t rises while the per-timestep time drops")
     return out
 
 
@@ -1048,9 +1058,10 @@ def main():
         with ClockSampler(dev_index) as clk2:
             table = per_kernel_table(torch, P, D, hbm)
             table["spmv"]["cusparse_cc_yardstick"] = cusparse_yardstick(torch, P, hbm)
-            line["temporal_blocking"] = temporal_blocking(torch, P, hbm,
-                                                          table["2d5pt"]["cc"]["ms_per_unit"],
-                                                          table["3d7pt"]["cc"]["ms_per_unit"])
+            t1 = {(pr, un): table[pr][un]["ms_per_unit"] for pr in ("2d5pt", "3d7pt", "3d27pt") for un in ("cc", "tc")}
+            pk0 = peaks_runs[0] if peaks_runs else None
+            line["temporal_blocking"] = temporal_blocking(
+                torch, P, hbm, t1, pk0["cuda_core"] * 1e12 / (hbm * 1e9) if pk0 else None)
             line["next_rows"] = {"gemv": gemv_rows(torch, P, hbm), **stencil_preset_rows(torch, P, hbm)}
             line["dist_one_gpu"] = dist_one_gpu(torch, P, D, hbm)
         # K11 again at the end (after the power-capped stretch): alpha range

@@ -231,11 +231,13 @@ KernelCharacterization stencil_temporal(ExecutionUnit unit, Precision p, const S
     // shapes it refuses (odd nx, unaligned rows)
     const bool use_tb3r = t >= 2 && rlb::stencil_tb3r_supported(d, (int)t, u, v);
     const bool use_tb3 = t >= 2 && (use_tb3r || rlb::stencil_tb3_supported(d, (int)t));
+    const bool use_tbtc = t >= 2 && unit == ExecutionUnit::TensorCore && rlb::stencil_tbtc_supported(d, (int)t, u, v);
     const bool ok2d = d.preset == rlb::kP2d5 && use_tb;
-    if (t >= 2 && (unit != ExecutionUnit::CudaCore || !(ok2d || use_tb3)))
+    if (t >= 2 && !(unit == ExecutionUnit::CudaCore ? (ok2d || use_tb3) : use_tbtc))
         throw Error(ErrorKind::ValidationError,
                     "temporal depth >= 2 is implemented on the CUDA core for 2d5pt (t <= 8; even depths need "
-                    "an even nx and 16-byte aligned rows) and 3d7pt (t <= 4)");
+                    "an even nx and 16-byte aligned rows), 3d7pt and 3d27pt (t <= 4), and on the tensor core "
+                    "for 2d5pt (t <= 4, even nx, 16-byte aligned u and v)");
     const std::uint64_t fused = steps / t, rem = steps % t;
     const unsigned __int128 pts = interior_points(d);
     const unsigned __int128 w = pts * ((unsigned __int128)fused * kt.work_flops + (unsigned __int128)rem * k1.work_flops);
@@ -247,7 +249,9 @@ KernelCharacterization stencil_temporal(ExecutionUnit unit, Precision p, const S
     for (std::uint64_t i = 0; i < fused + rem; ++i, ++sweeps) {
         const double* src = (sweeps & 1) ? v : u;
         double* dst = (sweeps & 1) ? u : v;
-        if (i < fused && use_tb3r) {
+        if (i < fused && use_tbtc) {
+            cuda_check(rlb::launch_stencil_tbtc(d, (int)t, src, dst, s), "stencil (tensor-core temporal blocking)");
+        } else if (i < fused && use_tb3r) {
             cuda_check(rlb::launch_stencil_tb3r(d, (int)t, 1, outer - 1, src, dst, s), "stencil (3D temporal blocking)");
         } else if (i < fused && use_tb3) {
             cuda_check(rlb::launch_stencil_tb3(d, (int)t, 1, outer - 1, src, dst, s), "stencil (3D temporal blocking)");

@@ -154,6 +154,11 @@ cudaError_t launch_stencil_tb3(const StencilDesc& d, int t, uint64_t o0, uint64_
 // 3d7pt with temporal depth t (2..4), register-blocked and skewed: TMA plane
 // tiles, one barrier per input plane (stencil_tb3r.cu).  Needs an even nx
 // and 16-byte aligned u / v.
+// 2d5pt temporal blocking on the tensor core (stencil_tbtc.cu): overlapped
+// 64 x 64 tiles in shared memory, each level the x-band-on-DMMA form; one
+// launch = one fused sweep of t timesteps over the interior (t = 2..4).
+bool stencil_tbtc_supported(const StencilDesc& d, int t, const double* u, const double* v);
+cudaError_t launch_stencil_tbtc(const StencilDesc& d, int t, const double* u, double* v, cudaStream_t s);
 bool stencil_tb3r_supported(const StencilDesc& d, int t, const double* u, const double* v);
 cudaError_t launch_stencil_tb3r(const StencilDesc& d, int t, uint64_t o0, uint64_t o1, const double* u, double* v,
                                 cudaStream_t s);

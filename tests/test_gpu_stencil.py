@@ -298,12 +298,64 @@ def test_3d7pt_temporal_depth_t(cuda, t, shape):
     assert kc.traffic_bytes == 16 * int(np.prod([s - 2 for s in shape])) * 3
 
 
+@pytest.mark.parametrize("t", [2, 3, 4])
+@pytest.mark.parametrize("shape", [(9, 10, 11), (20, 24, 68), (37, 130, 126), (70, 29, 200)])
+@pytest.mark.parametrize("weights", ["default", "general"])
+def test_3d27pt_temporal_depth_t(cuda, t, shape, weights):
+    """3d27pt temporal depth t (stencil_tb3.cu, three partial-sum planes per
+    level, weights from the parameter bank): equals single timesteps for the
+    BASELINE class weights and for 27 unrelated weights; Dirichlet shell
+    bit-exact; stencil_model(t) bytes."""
+    import torch
+
+    u0 = O.stencil_init(shape, 1, 31)
+    w = None if weights == "default" else np.random.default_rng(t).uniform(0.0, 1.0 / 27, 27)
+    steps = 2 * t + 1
+    u = torch.from_numpy(u0.copy()).cuda()
+    v = torch.from_numpy(u0.copy()).cuda()
+    kc, out = P.stencil_temporal("3d27pt", u, v, steps, t, weights=w)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    assert O.rel_err(got, O.stencil("3d27pt", u0, steps, w)) <= TOL
+    ring = _ring_mask(shape, 1)
+    assert O.bit_mismatches(got[ring], u0[ring]) == 0
+    pts = int(np.prod([s - 2 for s in shape]))
+    assert kc.traffic_bytes == 16 * pts * 3 and kc.work_flops == pts * 54 * (2 * t + 1)
+
+
+@pytest.mark.parametrize("t", [2, 3, 4])
+@pytest.mark.parametrize("shape", [(20, 24), (65, 130), (130, 66), (301, 516), (1030, 1026)])
+def test_2d5pt_temporal_tensor_core(cuda, t, shape):
+    """2d5pt temporal depth t on the tensor core (stencil_tbtc.cu: overlapped
+    64 x 64 tiles, each level the x-band-on-DMMA form) equals single
+    timesteps with custom weights; tiles straddling the grid edge; Dirichlet
+    ring bit-exact; stencil_model(t) bytes."""
+    import torch
+
+    u0 = O.stencil_init(shape, 1, 37)
+    w = np.array([0.4, 0.2, 0.1, 0.17, 0.13])
+    steps = 2 * t + 1
+    u = torch.from_numpy(u0.copy()).cuda()
+    v = torch.from_numpy(u0.copy()).cuda()
+    kc, out = P.stencil_temporal("2d5pt", u, v, steps, t, weights=w, unit=P.TENSOR_CORE)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    assert O.rel_err(got, O.stencil("2d5pt", u0, steps, w)) <= TOL
+    ring = _ring_mask(shape, 1)
+    assert O.bit_mismatches(got[ring], u0[ring]) == 0
+    pts = (shape[0] - 2) * (shape[1] - 2)
+    assert kc.traffic_bytes == 16 * pts * 3
+
+
 def test_temporal_depth_restrictions(cuda):
     import torch
 
     u = torch.zeros((20, 24, 64), dtype=torch.float64, device="cuda")
     with pytest.raises(P.RooflensError) as e:
-        P.stencil_temporal("3d27pt", u, u.clone(), 4, 2)
+        P.stencil_temporal("3d27pt", u, u.clone(), 10, 5)
+    assert e.value.kind == "ValidationError"
+    with pytest.raises(P.RooflensError) as e:
+        P.stencil_temporal("3d7pt", u, u.clone(), 4, 2, unit=P.TENSOR_CORE)
     assert e.value.kind == "ValidationError"
     with pytest.raises(P.RooflensError) as e:
         P.stencil_temporal("3d7pt", u, u.clone(), 10, 5)
@@ -315,7 +367,11 @@ def test_temporal_depth_restrictions(cuda):
         P.stencil_temporal("2d5pt", u[0], u[1].clone(), 18, 9)
     assert e.value.kind == "InvalidRange"
     with pytest.raises(P.RooflensError) as e:
-        P.stencil_temporal("2d5pt", u[0], u[1].clone(), 4, 2, unit=P.TENSOR_CORE)
+        P.stencil_temporal("2d5pt", u[0], u[1].clone(), 10, 5, unit=P.TENSOR_CORE)
+    assert e.value.kind == "ValidationError"
+    with pytest.raises(P.RooflensError) as e:  # odd nx: no 16-byte rows for the box
+        P.stencil_temporal("2d5pt", u[0, :, :63].contiguous(), u[1, :, :63].contiguous(), 4, 2,
+                           unit=P.TENSOR_CORE)
     assert e.value.kind == "ValidationError"
 
 
