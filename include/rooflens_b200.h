@@ -148,10 +148,11 @@ RL_API int rl_stencil(rl_unit unit, rl_precision precision, const char* preset,
 /* Temporal blocking (stencil_model's temporal_depth t, kernels.cpp:137-155;
  * PAPER.md:223-236): `steps` timesteps executed as steps/t fused sweeps of t
  * timesteps each (plus steps%t single sweeps).  HBM sees one read of u and one
- * write of v per fused sweep.  t = 1 behaves like rl_stencil; on the CUDA
- * core t = 2..8 is implemented for 2d5pt (even t: even nx and 16-byte
- * aligned rows) and t = 2..4 for 3d7pt; t > 8 is InvalidRange, other presets
- * / depths / the tensor core are ValidationError.
+ * write of v per fused sweep.  t = 1 behaves like rl_stencil.  CUDA core:
+ * t = 2..8 for 2d5pt (even t: even nx and 16-byte aligned rows), t = 2..4 for
+ * 3d7pt and 3d27pt (any weights).  Tensor core: t = 2..4 for 2d5pt (even nx,
+ * 16-byte aligned u and v; each level the x-band-on-DMMA form).  t > 8 is
+ * InvalidRange; other presets / depths / units are ValidationError.
  * Buffers swap once per sweep: *result_in_v (optional) reports where the
  * final field is.  kchar = stencil_model(preset, FP64, t) x points x (steps/t)
  * + stencil_model(preset, FP64, 1) x points x (steps%t). */
