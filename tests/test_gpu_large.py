@@ -102,3 +102,35 @@ def test_spmv_large_rows(cuda, unit):
     assert int(rp[-1]) == m * k
     del rp, col, val, x, y
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("unit", UNITS)
+def test_spmv_plan_colsort_large(cuda, unit):
+    """2^24 rows, 8 nonzeros per row, +-65536 band through the column-sorted
+    plan: blocks capped at 8192 rows (2048 blocks, ~7 waves), rows sampled
+    across the whole range against a host recomputation."""
+    import torch
+
+    m, k, hb = 1 << 24, 8, 65536
+    rp = torch.empty(m + 1, dtype=torch.int32, device="cuda")
+    col = torch.empty(m * k, dtype=torch.int32, device="cuda")
+    val = torch.empty(m * k, dtype=torch.float64, device="cuda")
+    x = torch.empty(m, dtype=torch.float64, device="cuda")
+    P.gen_band_csr(m, 0, m, k, hb, 5, rp, col, val)
+    P.fill_uniform(x, 5, 4, 0, 1)
+    plan = P.SpmvPlan(rp.cpu(), col.cpu(), val.cpu(), m, unit=unit)
+    try:
+        assert plan.layout() == "colsort"
+        y = torch.full((m,), float("nan"), dtype=torch.float64, device="cuda")
+        plan.execute(x, y)
+        torch.cuda.synchronize()
+        assert not torch.isnan(y).any()
+        rows = np.concatenate([np.random.default_rng(1).integers(0, m, 4000), np.arange(m - 64, m)])
+        r = torch.from_numpy(rows).cuda()
+        idx = rp[r].long()[:, None] + torch.arange(k, device="cuda")[None, :]
+        ref = (val[idx] * x[col[idx].long()]).sum(dim=1)
+        assert float(torch.linalg.norm(y[r] - ref) / torch.linalg.norm(ref)) <= TOL
+    finally:
+        plan.close()
+    del rp, col, val, x
+    torch.cuda.empty_cache()

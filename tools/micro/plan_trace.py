@@ -20,6 +20,7 @@ for arg in (sys.argv[1:] or ["8", "16", "32"]):
     chunks, _, taper = arg.partition(":")
     chunks = int(chunks)
     P.tuning_set("spmv_plan_chunks", chunks)
+    P.tuning_set("spmv_plan_colsort_chunks", chunks)
     P.tuning_set("spmv_plan_taper", int(taper or 1))
     plan = P.SpmvPlan(hrp, hcol, hval, n)
     for _ in range(3):
