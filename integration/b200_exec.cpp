@@ -65,6 +65,42 @@ KernelCharacterization stencil(ExecutionUnit unit, Precision precision, const St
     return kc(shape.name, k);
 }
 
+KernelCharacterization stencil_temporal(ExecutionUnit unit, Precision precision, const StencilShape& shape,
+                                        const std::uint64_t dims[3], const double* weights, std::uint64_t steps,
+                                        std::uint64_t t, double* u, double* v, void* stream, bool* result_in_v) {
+    rl_kchar k{};
+    int in_v = 0;
+    check(rl_stencil_temporal(U(unit), Pr(precision), shape.name.c_str(), dims, weights, steps, t, u, v, stream,
+                              &in_v, &k));
+    if (result_in_v) *result_in_v = in_v != 0;
+    return kc(shape.name, k);
+}
+
+SpmvPlan::SpmvPlan(ExecutionUnit unit, Precision precision, const SparseMatrixStats& s, const std::int32_t* rp,
+                   const std::int32_t* col, const double* val) {
+    rl_spmv_plan p = nullptr;
+    check(rl_spmv_plan_create(U(unit), Pr(precision), s.rows, s.cols, s.nnz, rp, col, val, &p));
+    h_ = p;
+}
+SpmvPlan::~SpmvPlan() {
+    if (h_) rl_spmv_plan_destroy(static_cast<rl_spmv_plan>(h_));
+}
+KernelCharacterization SpmvPlan::execute_host(const double* x, double* y) {
+    rl_kchar k{};
+    check(rl_spmv_plan_execute_host(static_cast<rl_spmv_plan>(h_), x, y, &k));
+    return kc("spmv-csr", k);
+}
+KernelCharacterization SpmvPlan::execute(const double* x, double* y, void* stream) {
+    rl_kchar k{};
+    check(rl_spmv_plan_execute(static_cast<rl_spmv_plan>(h_), x, y, stream, &k));
+    return kc("spmv-csr", k);
+}
+std::string SpmvPlan::layout() const {
+    int l = 0;
+    check(rl_spmv_plan_info(static_cast<rl_spmv_plan>(h_), &l, nullptr));
+    return l == 4 ? "colsort" : "csr";
+}
+
 void B200Comm::unique_id(std::uint8_t id[128]) { check(rl_dist_unique_id(id)); }
 
 B200Comm::B200Comm(int world, int rank, const std::uint8_t id[128]) {
@@ -82,6 +118,41 @@ KernelCharacterization dist_scale(const B200Comm& comm, ExecutionUnit unit, Prec
     rl_kchar k{};
     check(rl_dist_scale(static_cast<rl_dist>(comm.handle()), U(unit), Pr(precision), a, b, q, n_global, stream, &k));
     return kc("scale", k);
+}
+
+DistSpmv::DistSpmv(const B200Comm& comm, ExecutionUnit unit, Precision precision, std::uint64_t n, std::uint64_t hb,
+                   const std::int32_t* rp, const std::int32_t* col, const double* val, double* x, double* y) {
+    rl_dist_spmv p = nullptr;
+    check(rl_dist_spmv_create(static_cast<rl_dist>(comm.handle()), U(unit), Pr(precision), n, hb, 1, &rp, &col, &val,
+                              &x, &y, &p));
+    h_ = p;
+}
+DistSpmv::~DistSpmv() {
+    if (h_) rl_dist_spmv_destroy(static_cast<rl_dist_spmv>(h_));
+}
+KernelCharacterization DistSpmv::execute(void* stream) {
+    rl_kchar k{};
+    check(rl_dist_spmv_execute(static_cast<rl_dist_spmv>(h_), stream, &k));
+    return kc("spmv-csr", k);
+}
+
+DistStencil::DistStencil(const B200Comm& comm, ExecutionUnit unit, Precision precision, const StencilShape& shape,
+                         const std::uint64_t dims[3], const double* weights, double* u, double* v)
+    : name_(shape.name) {
+    rl_dist_stencil p = nullptr;
+    check(rl_dist_stencil_create(static_cast<rl_dist>(comm.handle()), U(unit), Pr(precision), shape.name.c_str(), dims,
+                                 weights, 1, &u, &v, &p));
+    h_ = p;
+}
+DistStencil::~DistStencil() {
+    if (h_) rl_dist_stencil_destroy(static_cast<rl_dist_stencil>(h_));
+}
+KernelCharacterization DistStencil::run(std::uint64_t steps, void* stream, bool* result_in_v) {
+    rl_kchar k{};
+    int in_v = 0;
+    check(rl_dist_stencil_run(static_cast<rl_dist_stencil>(h_), steps, stream, &in_v, &k));
+    if (result_in_v) *result_in_v = in_v != 0;
+    return kc(name_, k);
 }
 
 // ---------------------------------------------------------------------------

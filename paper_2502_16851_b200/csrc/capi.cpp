@@ -487,6 +487,14 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
     if (nnz > 0x7fffffffull || m > 0x7fffffffull || n > 0x7fffffffull)
         throw Error(ErrorKind::InvalidRange, "int32 CSR indices cannot address this matrix");
     if ((uint64_t)rp[m] != nnz) throw Error(ErrorKind::ValidationError, "row_ptr[m] != nnz");
+    // host-side validation first: nothing is allocated for a malformed CSR
+    if (rp[0] != 0) throw Error(ErrorKind::ValidationError, "row_ptr[0] != 0");
+    for (uint64_t i = 0; i < m; ++i)
+        if (rp[i + 1] < rp[i]) throw Error(ErrorKind::ValidationError, "row_ptr decreases at row " + std::to_string(i));
+    for (uint64_t j = 0; j < nnz; ++j)
+        if (col[j] < 0 || (uint64_t)col[j] >= n)
+            throw Error(ErrorKind::IndexOutOfRange, "column index " + std::to_string(col[j]) + " outside [0, " +
+                                                        std::to_string(n) + ")");
     auto pl = std::make_unique<rl_spmv_plan_s>();
     pl->unit = unit;
     pl->m = m;
@@ -499,11 +507,6 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
         // the column-sorted row-block layout (K17, spmv_colsort.cu) when the
         // matrix is eligible (rows <= kColsortMaxRowLen nonzeros, block column
         // spans fit); else the caller's CSR with the long-row path
-        for (uint64_t i = 0; i < m; ++i)
-            for (int32_t k = rp[i]; k < rp[i + 1]; ++k)
-                if (col[k] < 0 || (uint64_t)col[k] >= n)
-                    throw Error(ErrorKind::IndexOutOfRange, "column index " + std::to_string(col[k]) +
-                                                                " outside [0, " + std::to_string(n) + ")");
         rlb::SpmvColsortLayout L;
         if (rlb::tuning().spmv_plan_colsort && nnz > 0 && rlb::spmv_colsort_build(m, n, rp, col, val, L)) {
             pl->colsort = true;

@@ -55,6 +55,29 @@ int main() {
     // here, so only probed when the caller says no device is present.
     if (std::getenv("RL_PROBE_NO_DEVICE"))
         probe("scale_exec", [&] { return scale(ExecutionUnit::CudaCore, Precision::FP64, a, b, 3.0, 8, nullptr); });
+    // SpMV plan: host-side validation before any device allocation
+    {
+        const std::int32_t rp[3] = {0, 1, 2}, colbad[2] = {0, 7};
+        const double vv[2] = {1.0, 2.0};
+        SparseMatrixStats s2{2, 2, 2};
+        probe("plan_bad_column", [&] {
+            SpmvPlan p(ExecutionUnit::CudaCore, Precision::FP64, s2, rp, colbad, vv);
+            return KernelCharacterization{};
+        });
+        const std::int32_t rpdec[3] = {0, 2, 1}, colok[2] = {0, 1};
+        probe("plan_decreasing_rows", [&] {
+            SpmvPlan p(ExecutionUnit::CudaCore, Precision::FP64, SparseMatrixStats{2, 2, 1}, rpdec, colok, vv);
+            return KernelCharacterization{};
+        });
+    }
+    // temporal depth past 8: InvalidRange before any device work
+    {
+        std::uint64_t d3[3] = {8, 8, 8};
+        probe("temporal_depth_9", [&] {
+            return stencil_temporal(ExecutionUnit::CudaCore, Precision::FP64, stencil_preset("3d7pt"), d3, nullptr, 18,
+                                    9, a, b, nullptr, nullptr);
+        });
+    }
     // report.hpp through the adapter: the bounds equal the reference's own
     // bounds.cpp objects (value, kind, assumption and warning text)
     try {

@@ -74,3 +74,11 @@ def test_report_api_through_the_adapter(probes):
     assert abs(float(probes["report_gemv_workload"]) - 1.05) < 1e-3
     assert int(probes["render_text_lines"]) >= 14
     assert probes["report_zero_balance"] == "kind:9"  # ZeroBalance
+
+
+def test_plan_and_temporal_validation_through_the_adapter(probes):
+    """SpmvPlan / stencil_temporal wrappers: malformed inputs raise the
+    reference's ErrorKinds before any device allocation (no GPU needed)."""
+    assert probes["plan_bad_column"].startswith("kind:14:IndexOutOfRange")
+    assert probes["plan_decreasing_rows"].startswith("kind:2:ValidationError")
+    assert probes["temporal_depth_9"].startswith("kind:10:InvalidRange")
