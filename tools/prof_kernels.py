@@ -1,8 +1,10 @@
 """Run each hot kernel a few times at its BASELINE config (for ncu captures).
 
-  python tools/prof_kernels.py [names...]   names: stream_cc stream_tc spmv_cc spmv_tc
-        2d5pt_cc 2d5pt_tc 3d7pt_cc 3d7pt_tc 3d27pt_cc 3d27pt_tc (default: all);
-        also 2d9pt_* 2d13pt_* 2d49pt_* gemv_* spmvchunked_cc
+  python tools/prof_kernels.py [names...]   names: stream_cc stream_tc spmv_cc spmv_tc (the
+        plan: K17 column-sorted blocks) spmvcsr_cc spmvcsr_tc (raw CSR kernels) 2d5pt_cc 2d5pt_tc
+        3d7pt_cc 3d7pt_tc 3d27pt_cc 3d27pt_tc (default: all of these);
+        also 2d9pt_* 2d13pt_* 2d49pt_* gemv_*, temporal tb<preset>t<depth>_<unit>
+        (e.g. tb2d5ptt4_cc, tb2d5ptt4_tc, tb3d7ptt2_cc, tb3d27ptt2_cc)
 """
 import os
 os.environ.setdefault("RL_DEV_TUNING", "1")  # sweep knobs (rl_tuning_set developer keys)
@@ -27,7 +29,7 @@ def run(name):
         a = torch.empty_like(b)
         for _ in range(REPS):
             P.scale(a, b, 3.0, unit=unit)
-    elif kern == "spmv":
+    elif kern == "spmvcsr":
         n, k, hb = 1 << 22, 16, 65536
         rp = torch.empty(n + 1, dtype=torch.int32, device="cuda")
         col = torch.empty(n * k, dtype=torch.int32, device="cuda")
@@ -47,7 +49,7 @@ def run(name):
         y = torch.empty(m, dtype=torch.float64, device="cuda")
         for _ in range(REPS):
             P.gemv(A, x, y, unit=unit)
-    elif kern == "spmvcolsort":
+    elif kern == "spmv":
         n, k, hb = 1 << 22, 16, 65536
         rp = torch.empty(n + 1, dtype=torch.int32, device="cuda")
         col = torch.empty(n * k, dtype=torch.int32, device="cuda")
@@ -60,6 +62,13 @@ def run(name):
         for _ in range(REPS):
             plan.execute(x, y)
         plan.close()
+    elif kern.startswith("tb"):
+        preset, t = kern[2:].rsplit("t", 1)
+        shape = (16384, 16384) if preset.startswith("2d") else (512, 512, 512)
+        u = torch.empty(shape, dtype=torch.float64, device="cuda")
+        P.stencil_init(u, 1, 1)
+        v = u.clone()
+        P.stencil_temporal(preset, u, v, REPS * int(t), int(t), unit=unit)
     else:
         shape = (16384, 16384) if kern.startswith("2d") else (512, 512, 512)
         u = torch.empty(shape, dtype=torch.float64, device="cuda")
@@ -70,8 +79,8 @@ def run(name):
 
 
 if __name__ == "__main__":
-    names = sys.argv[1:] or ["stream_cc", "stream_tc", "spmv_cc", "spmv_tc", "2d5pt_cc", "2d5pt_tc",
-                             "3d7pt_cc", "3d7pt_tc", "3d27pt_cc", "3d27pt_tc"]
+    names = sys.argv[1:] or ["stream_cc", "stream_tc", "spmv_cc", "spmv_tc", "spmvcsr_cc", "spmvcsr_tc",
+                             "2d5pt_cc", "2d5pt_tc", "3d7pt_cc", "3d7pt_tc", "3d27pt_cc", "3d27pt_tc"]
     # PROF_TUNE="key=val,key=val": rl_tuning_set before the runs
     for kv in filter(None, os.environ.get("PROF_TUNE", "").split(",")):
         k, v = kv.split("=")
