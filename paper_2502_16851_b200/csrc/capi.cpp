@@ -541,16 +541,18 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
     }
     uint64_t nch = std::min<uint64_t>(
         (uint64_t)(pl->colsort ? rlb::tuning().spmv_plan_colsort_chunks : rlb::tuning().spmv_plan_chunks), units);
-    // Chunk c covers weight w_c of the rows: w = 1/2 for the first and last
-    // chunk, 1 otherwise (spmv_plan_taper), so the pipeline's head (the first
-    // x prefix) and tail (the last compute + y copy) are short while the
-    // middle copies stay large.
-    const bool taper = rlb::tuning().spmv_plan_taper && nch >= 3;
-    const uint64_t wsum = taper ? 2 * nch - 2 : 2 * nch;  // in half units
+    // Chunk c covers weight w_c of the rows: with spmv_plan_taper = k > 0 the
+    // first and last chunks weigh 1 and the others k + 1, so the pipeline's
+    // head (the first x prefix) and tail (the last compute + y copy) are short
+    // while the middle copies stay large; k = 0: equal chunks.
+    const uint64_t tk = (uint64_t)std::max(0, rlb::tuning().spmv_plan_taper);
+    const bool taper = tk > 0 && nch >= 3;
+    const uint64_t wmid = taper ? tk + 1 : 1;
+    const uint64_t wsum = taper ? wmid * (nch - 2) + 2 : nch;
     uint64_t acc = 0;
     for (uint64_t c = 0; c <= nch; ++c) {
         pl->chunk_row.push_back(std::min<uint64_t>(m, units * acc / wsum * unitrows));
-        if (c < nch) acc += (taper && (c == 0 || c == nch - 1)) ? 1 : 2;
+        if (c < nch) acc += (taper && (c == 0 || c == nch - 1)) ? 1 : wmid;
     }
     pl->chunk_row.back() = m;
     if (pl->colsort) {  // chunk boundaries on block starts

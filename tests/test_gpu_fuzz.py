@@ -40,6 +40,53 @@ def test_fuzz_scale(cuda, case, unit):
 
 @pytest.mark.parametrize("case", range(CASES))
 @pytest.mark.parametrize("unit", UNITS)
+def test_fuzz_spmv_plan(cuda, case, unit):
+    """Random CSR structures through rl_spmv_plan (the K17 column-sorted
+    layout whenever every row has <= 1024 nonzeros, else CSR): empty rows,
+    a long row, local and scattered columns, rectangular shapes, both the
+    device and the host entry points."""
+    import torch
+
+    rng = _rng(500 + case)
+    m, n = int(rng.integers(1, 40000)), int(rng.integers(1, 40000))
+    lens = rng.integers(0, 48, m)
+    lens[rng.random(m) < 0.15] = 0
+    if m > 3 and case % 3 == 0:
+        lens[int(rng.integers(0, m))] = min(n, int(rng.integers(200, 1500)))  # sometimes past 1024
+    lens = np.minimum(lens, n)
+    if lens.sum() == 0:
+        lens[0] = 1
+    local = case % 2 == 0  # banded columns, else scattered over all of x
+    cols = []
+    for i, l in enumerate(lens):
+        if local:
+            c0 = min(max(0, i * n // max(m, 1) - 500), max(0, n - 1000))
+            span = min(n - c0, 1000)
+            cols.append(np.sort(rng.choice(span, min(l, span), replace=False)) + c0)
+        else:
+            cols.append(np.sort(rng.choice(n, l, replace=False)))
+    lens = np.array([c.size for c in cols])
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    col = np.concatenate(cols).astype(np.int32)
+    val = rng.uniform(-1, 1, rp[-1])
+    x = rng.uniform(-1, 1, n)
+    ref = O.spmv_csr(rp, col, val, x)
+    plan = P.SpmvPlan(rp, col, val, n, unit=unit)
+    try:
+        assert plan.layout() == ("colsort" if lens.max() <= 1024 else "csr")
+        dy = torch.full((m,), float("nan"), dtype=torch.float64, device="cuda")
+        plan.execute(torch.from_numpy(x).cuda(), dy)
+        torch.cuda.synchronize()
+        assert O.rel_err(dy.cpu().numpy(), ref) <= TOL
+        hy = np.full(m, np.nan)
+        plan.execute_host(x, hy)
+        assert O.rel_err(hy, ref) <= TOL
+    finally:
+        plan.close()
+
+
+@pytest.mark.parametrize("case", range(CASES))
+@pytest.mark.parametrize("unit", UNITS)
 def test_fuzz_spmv(cuda, case, unit):
     import torch
 

@@ -15,10 +15,10 @@ yref = torch.empty(n, dtype=torch.float64, device="cuda"); P.spmv_csr(rp, col, v
 pin = lambda t: t.cpu().pin_memory()
 hrp, hcol, hval, hx = pin(rp), pin(col), pin(val), pin(x)
 t0 = time.perf_counter()
-configs = [(c, s, z) for z in (0, 1) for c in (4, 8, 16) for s in (1, 4)]
-for chunks, streams, zc in configs:
-    taper = 0
-    P.tuning_set("spmv_plan_zero_copy", zc)
+configs = [(c, s, t) for c in (6, 8, 10, 12) for t in (0, 1, 3, 7) for s in (1,)]
+for chunks, streams, taper in configs:
+    zc = 0
+    P.tuning_set("spmv_plan_taper", taper)
     P.tuning_set("spmv_plan_colsort_chunks", chunks)
     P.tuning_set("spmv_plan_streams", streams)
     P.tuning_set("spmv_plan_taper", taper)
@@ -32,6 +32,6 @@ for chunks, streams, zc in configs:
         plan.execute_host(hx, hy)
     dt = (time.perf_counter() - t1) / 20
     err = O.rel_err(hy.numpy(), yref)
-    print(f"{plan.layout()} chunks {chunks:3d} streams {streams} zero_copy {zc}: {dt*1e3:.3f} ms/call "
+    print(f"{plan.layout()} chunks {chunks:3d} streams {streams} taper {taper}: {dt*1e3:.3f} ms/call "
           f"{889192452/dt/1e9:.1f} GB/s relerr {err:.1e} (create {tc:.2f} s)", flush=True)
     plan.close()
