@@ -564,8 +564,8 @@ def temporal_blocking(torch, P, hbm, t1_ms, balance=None):
         torch.cuda.empty_cache()
     out["note"] = ("2d5pt CC: register-pipelined strips (stencil_tb.cu); 2d5pt TC: overlapped 64x64 tiles in "
                    "shared memory, each level the x-band-on-DMMA form (stencil_tbtc.cu); 3d7pt: register-blocked "
-                   "TMA tiles (stencil_tb3r.cu); 3d27pt: z-column kernel with three partial-sum planes per level "
-                   "(stencil_tb3.cu).  One HBM read + write per t timesteps; bytes = stencil_model(t) per fused "
+                   "TMA tiles (stencil_tb3r.cu); 3d27pt: t = 2 register-blocked partial-sum planes (stencil_tb27r.cu), "
+                   "t = 3, 4 the z-column kernel (stencil_tb3.cu).  One HBM read + write per t timesteps; bytes = stencil_model(t) per fused "
                    "sweep, so model_gbs falls as t rises while the per-timestep time drops")
     return out
 

@@ -230,6 +230,7 @@ KernelCharacterization stencil_temporal(ExecutionUnit unit, Precision p, const S
     // 3d7pt: the register-blocked TMA kernel; the z-column kernel covers the
     // shapes it refuses (odd nx, unaligned rows)
     const bool use_tb3r = t >= 2 && rlb::stencil_tb3r_supported(d, (int)t, u, v);
+    const bool use_tb27r = t >= 2 && rlb::tuning().stencil_tb27r && rlb::stencil_tb27r_supported(d, (int)t, u, v);
     const bool use_tb3 = t >= 2 && (use_tb3r || rlb::stencil_tb3_supported(d, (int)t));
     const bool use_tbtc = t >= 2 && unit == ExecutionUnit::TensorCore && rlb::stencil_tbtc_supported(d, (int)t, u, v);
     const bool ok2d = d.preset == rlb::kP2d5 && use_tb;
@@ -251,6 +252,8 @@ KernelCharacterization stencil_temporal(ExecutionUnit unit, Precision p, const S
         double* dst = (sweeps & 1) ? u : v;
         if (i < fused && use_tbtc) {
             cuda_check(rlb::launch_stencil_tbtc(d, (int)t, src, dst, s), "stencil (tensor-core temporal blocking)");
+        } else if (i < fused && use_tb27r) {
+            cuda_check(rlb::launch_stencil_tb27r(d, (int)t, 1, outer - 1, src, dst, s), "stencil (3D temporal blocking)");
         } else if (i < fused && use_tb3r) {
             cuda_check(rlb::launch_stencil_tb3r(d, (int)t, 1, outer - 1, src, dst, s), "stencil (3D temporal blocking)");
         } else if (i < fused && use_tb3) {
@@ -1256,6 +1259,7 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         {"spmv_plan_taper", &rlb::Tuning::spmv_plan_taper, false},
         {"spmv_plan_xpieces", &rlb::Tuning::spmv_plan_xpieces, false},
         {"spmv_plan_colsort", &rlb::Tuning::spmv_plan_colsort, true},
+        {"stencil_tb27r", &rlb::Tuning::stencil_tb27r, false},
         {"spmv_plan_streams", &rlb::Tuning::spmv_plan_streams, false},
         {"spmv_plan_colsort_chunks", &rlb::Tuning::spmv_plan_colsort_chunks, false},
         {"spmv_colsort_window", &rlb::Tuning::spmv_colsort_window, false},

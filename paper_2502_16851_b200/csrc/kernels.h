@@ -31,6 +31,7 @@ struct Tuning {
     int spmv_plan_streams = 1;     // compute streams of a column-sorted plan's execute_host (1: 1.02 ms, 4-8: 1.10 ms; tools/micro/plan_colsort_e2e.py)
     int spmv_plan_colsort_chunks = 8;  // pipeline chunks of a column-sorted plan (8: 1.02, 16: 1.21-1.26, 32: 1.36+ ms)
     int spmv_colsort_window = 128; // K17 plan build: entries per bank-ordering window (tools/micro/spmv_colsort.cu: 64 0.185, 128 0.183 ms)
+    int stencil_tb27r = 1;         // 3d27pt t = 2 (class weights): the register-blocked kernel (stencil_tb27r.cu); 0: z-column
     int spmv_plan_colsort = 1;     // plans (both units) use the column-sorted row-block layout (K17, spmv_colsort.cu) when eligible; 0: CSR
     int spmv_plan_xpieces = 0;     // max x upload pieces (first = chunk 0's prefix); 0: one per chunk
     int spmv_plan_ygroups = 0;     // y download copies (groups of consecutive chunks); 0: one per chunk
@@ -159,6 +160,10 @@ cudaError_t launch_stencil_tb3(const StencilDesc& d, int t, uint64_t o0, uint64_
 // launch = one fused sweep of t timesteps over the interior (t = 2..4).
 bool stencil_tbtc_supported(const StencilDesc& d, int t, const double* u, const double* v);
 cudaError_t launch_stencil_tbtc(const StencilDesc& d, int t, const double* u, double* v, cudaStream_t s);
+// 3d27pt (class weights), temporal depth 2, register-blocked (stencil_tb27r.cu).
+bool stencil_tb27r_supported(const StencilDesc& d, int t, const double* u, const double* v);
+cudaError_t launch_stencil_tb27r(const StencilDesc& d, int t, uint64_t o0, uint64_t o1, const double* u, double* v,
+                                 cudaStream_t s);
 bool stencil_tb3r_supported(const StencilDesc& d, int t, const double* u, const double* v);
 cudaError_t launch_stencil_tb3r(const StencilDesc& d, int t, uint64_t o0, uint64_t o1, const double* u, double* v,
                                 cudaStream_t s);
