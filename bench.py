@@ -1068,6 +1068,17 @@ def main():
         peaks_runs.append(fp64_peaks(torch, P))
         bounds = add_bounds(P, table, peaks_runs, hbm)
         add_bounds(P, line["next_rows"], peaks_runs, hbm)
+        # temporal rows on both units: TC/CC per depth against the kernel ceiling
+        # at the fused sweep's intensity t * I1 (bounds.cpp:72-85)
+        tb = line["temporal_blocking"]
+        i1 = P.stencil_model("2d5pt").intensity
+        for t in (2, 3, 4):
+            cc, tc = tb.get(f"2d5pt_t{t}"), tb.get(f"2d5pt_t{t}_tc")
+            if cc and tc:
+                tb[f"2d5pt_t{t}_tc"]["tc_over_cc"] = round(cc["ms_per_timestep"] / tc["ms_per_timestep"], 4)
+                ceils = [P.kernel_speedup_ceiling(max(pk["tensor_core"] / pk["cuda_core"], 1.0),
+                                                  pk["cuda_core"] * 1e12 / (hbm * 1e9), t * i1)[0] for pk in peaks_runs]
+                tb[f"2d5pt_t{t}_tc"]["bound"] = round(max(ceils), 4)
         peaks = peaks_runs[0]
         balance = peaks["cuda_core"] * 1e12 / (hbm * 1e9)
         for res in line["next_rows"].values():
