@@ -101,12 +101,16 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         int x0, y0;
         origin(k, x0, y0);
         mbar_wait(full, (uint32_t)(it & 1));
+        // each warp computes the same compute tiles at every level, so a lane's
+        // level-l output pair is its centre value at level l + 1 (registers)
+        // (T = 4: the extra registers spill, the centre comes from shared memory)
+        constexpr bool kRegCentre = T <= 3;
+        double2 ct[kTilesPerWarp];
         for (int l = 1; l <= T; ++l) {
             const double* src = buf[l == 1 ? 0 : (l & 1 ? 2 : 1)];
             double* dst = buf[l & 1 ? 1 : 2];
             static_assert(kTilesPerWarp * kWarps >= G::NT * G::NT, "every compute tile has a warp");
             double a[kTilesPerWarp][3], d0[kTilesPerWarp], d1[kTilesPerWarp];
-            double2 ct[kTilesPerWarp];
 #pragma unroll
             for (int q = 0; q < kTilesPerWarp; ++q) {  // loads of all the warp's tiles first
                 const int tt = min(warp + q * kWarps, G::NT * G::NT - 1);
@@ -115,7 +119,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
                 const int col = 2 + 8 * tj + 2 * c;
 #pragma unroll
                 for (int kb = 0; kb < 3; ++kb) a[q][kb] = pr[8 * tj + 4 * kb + c];
-                ct[q] = *reinterpret_cast<const double2*>(pr + col);
+                if (l == 1 || !kRegCentre) ct[q] = *reinterpret_cast<const double2*>(pr + col);
                 const double2 up = *reinterpret_cast<const double2*>(pr - G::BW + col);
                 const double2 dn = *reinterpret_cast<const double2*>(pr + G::BW + col);
                 d0[q] = fma(wyp, dn.x, fma(wym, up.x, w0 * ct[q].x));
@@ -137,6 +141,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
                 const double o0 = (by || gx <= 0 || gx >= nx - 1) ? ct[q].x : d0[q];
                 const double o1 = (by || gx + 1 <= 0 || gx + 1 >= nx - 1) ? ct[q].y : d1[q];
                 *reinterpret_cast<double2*>(dst + row * G::BW + col) = make_double2(o0, o1);
+                ct[q] = make_double2(o0, o1);
             }
             __syncthreads();
             if (l == 1 && tid == 0 && k + (int)gridDim.x < tiles) issue(k + gridDim.x);  // input buffer is free
