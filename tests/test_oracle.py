@@ -171,3 +171,17 @@ def test_default_weights_rule():
     assert np.allclose(w, (1.0 / (1 + manh)) / 10.0, rtol=0, atol=0)
     assert O.default_weights("2d5pt").tolist() == [0.5, 0.125, 0.125, 0.125, 0.125]
     assert O.default_weights("3d7pt").tolist() == [0.4] + [0.1] * 6
+
+
+def test_oracle_against_committed_golden_vectors():
+    """oracle/oracle.c against tests/golden/kernels.npz (numpy / math.fsum
+    restatements, independent of the oracle): STREAM bit-exact, SpMV and the
+    stencils within 1e-14."""
+    import os
+
+    G = np.load(os.path.join(os.path.dirname(__file__), "golden", "kernels.npz"))
+    assert O.bit_mismatches(O.scale(G["scale_b"], float(G["scale_q"])), G["scale_a"]) == 0
+    y = O.spmv_csr(G["spmv_rp"], G["spmv_col"], G["spmv_val"], G["spmv_x"])
+    assert O.rel_err(y, G["spmv_y"]) <= 1e-14
+    for preset, key, steps in (("2d5pt", "s2d", 3), ("3d7pt", "s3d7", 2), ("3d27pt", "s3d27", 2)):
+        assert O.rel_err(O.stencil(preset, G[f"{key}_u0"], steps), G[f"{key}_v"]) <= 1e-14, preset
