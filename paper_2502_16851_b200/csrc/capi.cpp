@@ -439,6 +439,12 @@ struct rl_spmv_plan_s {
     double* kval = nullptr;
     unsigned* kmeta = nullptr;
     std::vector<uint32_t> kblk_r0;
+    rlb::ColsortRun krun{};  // fixed-point mode state (null grid: FP64 atomics)
+    rlb::ColsortRun colsort_run() const {
+        rlb::ColsortRun r = krun;
+        r.rp = rp, r.col = col, r.val = val, r.col_base = 0;
+        return r;
+    }
     uint64_t layout_bytes = 0;
     std::vector<uint64_t> chunk_row;   // chunk c = rows [chunk_row[c], chunk_row[c+1])
     std::vector<uint64_t> chunk_xend;  // x prefix [0, chunk_xend[c]) chunk c reads
@@ -464,7 +470,7 @@ struct rl_spmv_plan_s {
         if (val) cudaFree(val);
         if (x) cudaFree(x);
         if (y) cudaFree(y);
-        for (void* p : {(void*)kblk, (void*)kval, (void*)kmeta})
+        for (void* p : {(void*)kblk, (void*)kval, (void*)kmeta, (void*)krun.grid, (void*)krun.list, (void*)krun.count})
             if (p) cudaFree(p);
         if (gexec) cudaGraphExecDestroy(gexec);
         for (auto e : ev_x) cudaEventDestroy(e);
@@ -511,7 +517,8 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
         // matrix is eligible (rows <= kColsortMaxRowLen nonzeros, block column
         // spans fit); else the caller's CSR with the long-row path
         rlb::SpmvColsortLayout L;
-        if (rlb::tuning().spmv_plan_colsort && nnz > 0 && rlb::spmv_colsort_build(m, n, rp, col, val, L)) {
+        if (rlb::tuning().spmv_plan_colsort && nnz > 0 &&
+            rlb::spmv_colsort_build(m, n, rp, col, val, L, {}, rlb::colsort_classes(unit == ExecutionUnit::TensorCore))) {
             pl->colsort = true;
             pl->krb = L.rb;
             pl->krows = L.rows;
@@ -525,7 +532,20 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
             up(pl->kmeta, L.meta);
             for (const auto& k : L.blocks) pl->kblk_r0.push_back(k.row0);
             pl->layout_bytes = L.val.size() * 12 + L.blocks.size() * sizeof(rlb::SpmvKBlock);
-        } else {
+            if (rlb::colsort_fixed_for(unit == ExecutionUnit::TensorCore)) {
+                // fixed-point rows: per-block grid, the flagged-row list and the
+                // CSR the FP64 row kernel reads for the rows it hands over
+                std::vector<int> g;
+                for (const auto& k : L.blocks) g.push_back(rlb::colsort_initial_grid(k));
+                up(pl->krun.grid, g);
+                ck(cudaMalloc(&pl->krun.list, std::max<uint64_t>(m, 1) * sizeof(int)), "plan alloc");
+                ck(cudaMalloc(&pl->krun.count, 2 * sizeof(unsigned)), "plan alloc");
+                ck(cudaMemset(pl->krun.count, 0, 2 * sizeof(unsigned)), "plan alloc");
+                pl->krun.done = pl->krun.count + 1;
+                pl->krun.rows = (unsigned)m;
+            }
+        }
+        if (!pl->colsort || pl->krun.grid) {
             ck(cudaMalloc(&pl->rp, (m + 1) * 4), "plan alloc");
             ck(cudaMemcpy(pl->rp, rp, (m + 1) * 4, cudaMemcpyHostToDevice), "plan upload");
             ck(cudaMalloc(&pl->col, std::max<uint64_t>(nnz, 1) * 4), "plan alloc");
@@ -609,12 +629,12 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
     }
     const uint64_t npc = pl->xpiece.size() - 1;
     ck(cudaStreamCreateWithFlags(&pl->s_in, cudaStreamNonBlocking), "stream");
-    pl->s_cmp.resize(pl->colsort ? (size_t)std::max(1, rlb::tuning().spmv_plan_streams) : 1);
+    pl->s_cmp.resize(pl->colsort && !pl->krun.grid ? (size_t)std::max(1, rlb::tuning().spmv_plan_streams) : 1);
     for (auto& st : pl->s_cmp) ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
     pl->ev_join.resize(pl->s_cmp.size() + 1);
     ck(cudaStreamCreateWithFlags(&pl->s_out, cudaStreamNonBlocking), "stream");
     pl->ev_x.resize(npc);
-    pl->ev_y.resize(nch * (pl->colsort ? (size_t)std::max(1, rlb::tuning().spmv_plan_streams) : 1));
+    pl->ev_y.resize(nch * pl->s_cmp.size());
     for (auto& e : pl->ev_x) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     for (auto& e : pl->ev_y) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     for (auto& e : pl->ev_join) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -633,7 +653,7 @@ void plan_rows(rl_spmv_plan_s* pl, uint64_t r0, uint64_t r1, const double* x, do
         const int b0 = (int)(std::lower_bound(v.begin(), v.end(), (uint32_t)r0) - v.begin());
         const int b1 = r1 >= pl->m ? (int)v.size() : (int)(std::lower_bound(v.begin(), v.end(), (uint32_t)r1) - v.begin());
         ck(rlb::launch_spmv_colsort(pl->unit == ExecutionUnit::TensorCore, pl->kblk, b0, b1, pl->krb, pl->krows,
-                                    pl->kval, pl->kmeta, x, y, s),
+                                    pl->kval, pl->kmeta, x, y, pl->colsort_run(), s),
            "spmv (column-sorted plan)");
         return;
     }
@@ -1259,10 +1279,12 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         {"spmv_plan_taper", &rlb::Tuning::spmv_plan_taper, false},
         {"spmv_plan_xpieces", &rlb::Tuning::spmv_plan_xpieces, false},
         {"spmv_plan_colsort", &rlb::Tuning::spmv_plan_colsort, true},
+        {"spmv_colsort_fixed", &rlb::Tuning::spmv_colsort_fixed, true},
         {"stencil_tb27r", &rlb::Tuning::stencil_tb27r, false},
         {"spmv_plan_streams", &rlb::Tuning::spmv_plan_streams, false},
         {"spmv_plan_colsort_chunks", &rlb::Tuning::spmv_plan_colsort_chunks, false},
         {"spmv_colsort_window", &rlb::Tuning::spmv_colsort_window, false},
+        {"spmv_colsort_classes", &rlb::Tuning::spmv_colsort_classes, false},
         {"spmv_plan_ygroups", &rlb::Tuning::spmv_plan_ygroups, false},
         {"stencil_r_ctas_per_sm", &rlb::Tuning::stencil_r_ctas_per_sm, false},
         {"stencil_tb_waves", &rlb::Tuning::stencil_tb_waves, false},

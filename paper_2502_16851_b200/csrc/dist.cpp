@@ -411,7 +411,13 @@ struct rl_dist_spmv_s {
         rlb::SpmvKBlock* kblk = nullptr;
         double* kval = nullptr;
         unsigned* kmeta = nullptr;
-        };
+        rlb::ColsortRun krun{};  // fixed-point mode state (null grid: FP64 atomics)
+        rlb::ColsortRun colsort_run() const {
+            rlb::ColsortRun r = krun;
+            r.rp = rp, r.col = col, r.val = val, r.col_base = (int64_t)g.cb;
+            return r;
+        }
+    };
     std::vector<Part> parts;
     std::vector<rl_dist_op> ops;
     int long_rows = 0;
@@ -420,7 +426,7 @@ struct rl_dist_spmv_s {
     ~rl_dist_spmv_s() {
         rp.destroy();
         for (auto& q : parts)
-            for (void* a : {(void*)q.kblk, (void*)q.kval, (void*)q.kmeta})
+            for (void* a : {(void*)q.kblk, (void*)q.kval, (void*)q.kmeta, (void*)q.krun.grid, (void*)q.krun.list, (void*)q.krun.count})
                 if (a) cudaFree(a);
     }
 };
@@ -430,7 +436,7 @@ namespace {
 // The part's CSR through the column-sorted row-block layout (the single-GPU
 // plan's default, K17): copied to the host once, columns made local to the
 // part's x window, built, uploaded.  Ineligible matrices keep the CSR.
-void colsort_part(rl_dist_spmv_s::Part& q, uint64_t rows, uint64_t nnz) {
+void colsort_part(rl_dist_spmv_s::Part& q, uint64_t rows, uint64_t nnz, bool tc) {
     std::vector<int32_t> hrp(rows + 1), hcol(nnz);
     std::vector<double> hval(nnz);
     ck(cudaMemcpy(hrp.data(), q.rp, (rows + 1) * 4, cudaMemcpyDeviceToHost), "D2H row_ptr");
@@ -445,7 +451,9 @@ void colsort_part(rl_dist_spmv_s::Part& q, uint64_t rows, uint64_t nnz) {
     std::vector<rlb::ColsortSegment> segs = {{q.i0, eb}, {q.i1, std::max<uint64_t>(1, 4 * (uint64_t)rlb::kNumSMsHost * nin / rows)},
                                              {rows, std::max<uint64_t>(1, 2 * (uint64_t)rlb::kNumSMsHost - eb)}};
     rlb::SpmvColsortLayout L;
-    if (!rlb::spmv_colsort_build(rows, q.g.ce - q.g.cb, hrp.data(), hcol.data(), hval.data(), L, segs)) return;
+    if (!rlb::spmv_colsort_build(rows, q.g.ce - q.g.cb, hrp.data(), hcol.data(), hval.data(), L, segs,
+                                 rlb::colsort_classes(tc)))
+        return;
     // block order: edge blocks first, then the interior, so each phase is one launch
     std::stable_partition(L.blocks.begin(), L.blocks.end(), [&](const rlb::SpmvKBlock& k) {
         return !(k.row0 >= q.i0 && k.row0 + k.rows <= q.i1);
@@ -461,6 +469,16 @@ void colsort_part(rl_dist_spmv_s::Part& q, uint64_t rows, uint64_t nnz) {
     q.colsort = true;
     q.krb = L.rb;
     q.krows = L.rows;
+    if (rlb::colsort_fixed_for(tc)) {
+        std::vector<int> g;
+        for (const auto& k : L.blocks) g.push_back(rlb::colsort_initial_grid(k));
+        up(q.krun.grid, g);
+        ck(cudaMalloc(&q.krun.list, std::max<uint64_t>(rows, 1) * sizeof(int)), "alloc");
+        ck(cudaMalloc(&q.krun.count, 2 * sizeof(unsigned)), "alloc");
+        ck(cudaMemset(q.krun.count, 0, 2 * sizeof(unsigned)), "alloc");
+        q.krun.done = q.krun.count + 1;
+        q.krun.rows = (unsigned)rows;
+    }
     q.knb = (int)L.blocks.size();
     q.kb1 = q.knb;  // interior blocks [kb0, knb), edge blocks [0, kb0)
     q.kb0 = 0;
@@ -472,7 +490,7 @@ void part_rows(const rl_dist_spmv_s* pl, const rl_dist_spmv_s::Part& q, int b0, 
                cudaStream_t s) {
     if (q.colsort) {
         ck(rlb::launch_spmv_colsort(pl->unit == ExecutionUnit::TensorCore, q.kblk, b0, b1, q.krb, q.krows, q.kval,
-                                    q.kmeta, q.x, q.y, s),
+                                    q.kmeta, q.x, q.y, q.colsort_run(), s),
            "spmv (column-sorted part)");
         return;
     }
@@ -533,7 +551,8 @@ rl_dist_spmv_s* spmv_create(rl_dist_s* d, ExecutionUnit unit, Precision p, uint6
                                                             std::to_string(hb));
             nnz_local += (uint64_t)ends[1];
             pl->parts.push_back(q);
-            if (rlb::tuning().spmv_plan_colsort && ends[1] > 0) colsort_part(pl->parts.back(), rows, (uint64_t)ends[1]);
+            if (rlb::tuning().spmv_plan_colsort && ends[1] > 0)
+                colsort_part(pl->parts.back(), rows, (uint64_t)ends[1], unit == ExecutionUnit::TensorCore);
             if (!pl->parts.back().colsort && rlb::tuning().spmv_long_rows &&
                 rlb::spmv_long_rows_probe(q.rp, q.col, q.val, 0, rows, pl->rp.s) != 0)
                 pl->long_rows = 1;

@@ -32,6 +32,9 @@ struct Tuning {
     int spmv_plan_colsort_chunks = 8;  // pipeline chunks of a column-sorted plan (8: 1.02, 16: 1.21-1.26, 32: 1.36+ ms)
     int spmv_colsort_window = 128; // K17 plan build: entries per bank-ordering window (tools/micro/spmv_colsort.cu: 64 0.185, 128 0.183 ms)
     int stencil_tb27r = 1;         // 3d27pt t = 2 (class weights): the register-blocked kernel (stencil_tb27r.cu); 0: z-column
+    int spmv_colsort_classes = 0;  // K17 bank-ordering group 1..32 (0: 1 = none on the fixed-point grid, 16 for FP64 rows)
+    int spmv_colsort_fixed = 1;    // K17 rows on a 64-bit fixed-point grid (+ FP64 row kernel for flagged rows):
+                                   // 1 CUDA-core unit only, 2 both units, 0 neither (FP64 shared atomics)
     int spmv_plan_colsort = 1;     // plans (both units) use the column-sorted row-block layout (K17, spmv_colsort.cu) when eligible; 0: CSR
     int spmv_plan_xpieces = 0;     // max x upload pieces (first = chunk 0's prefix); 0: one per chunk
     int spmv_plan_ygroups = 0;     // y download copies (groups of consecutive chunks); 0: one per chunk
@@ -73,6 +76,11 @@ struct Tuning {
     int stencil_r_sym = 1;             // 2d49pt CC: pair mirror-symmetric columns (fewer FP64 ops)    // 2d9pt/2d13pt/2d49pt TMA kernels: row segments so the grid is this deep
 };
 Tuning& tuning();
+// whether a K17 layout for this unit accumulates on the fixed-point grid
+inline bool colsort_fixed_for(bool tc) {
+    const int f = tuning().spmv_colsort_fixed;
+    return f == 2 || (f == 1 && !tc);
+}
 
 struct StencilDesc {
     int preset;          // see StencilPreset
@@ -196,7 +204,27 @@ struct SpmvKBlock {
     uint32_t row0;   // first row
     uint32_t rows;   // rows (<= kColsortMaxRows)
     uint32_t nent;   // entries, padded to a multiple of 32
+    int16_t ev;      // largest IEEE exponent field of the block's finite values
+    uint8_t hl;      // the longest row has <= 2^hl entries
+    uint8_t flags;   // bit 0: a value is Inf/NaN
 };
+constexpr int kColsortQuantum = 8;         // grid exponents are multiples of this
+constexpr int kColsortFp64 = -0x40000000;  // grid code: the block adds in FP64 (shared CAS atomics)
+// Fixed-point mode state (null grid: FP64 atomics only): the per-block grid
+// exponents of the last call, the rows handed to the FP64 row kernel, and the
+// CSR that kernel sums them from (columns minus col_base index x).
+struct ColsortRun {
+    int* grid;
+    int* list;        // capacity: `rows`
+    unsigned* count;  // entries in `list` (reset by the row kernel)
+    unsigned* done;   // CTAs of the row kernel finished (reset by its last CTA)
+    unsigned rows;
+    const int* rp;
+    const int* col;
+    const double* val;
+    int64_t col_base;
+};
+int colsort_initial_grid(const SpmvKBlock& k);
 struct SpmvColsortLayout {
     int rb = 0;    // row bits of meta
     int rows = 0;  // rows of the largest block (shared-memory y per CTA)
@@ -211,10 +239,17 @@ struct ColsortSegment {
     uint64_t blocks;
 };
 bool spmv_colsort_build(uint64_t m, uint64_t n, const int32_t* rp, const int32_t* col, const double* val,
-                        SpmvColsortLayout& layout, const std::vector<ColsortSegment>& segments = {});
+                        SpmvColsortLayout& layout, const std::vector<ColsortSegment>& segments = {},
+                        int classes = 16);
+// bank-ordering classes of a K17 layout for this unit (1: plain column order on the
+// fixed-point grid, 16: FP64 rows)
+inline int colsort_classes(bool tc) {
+    const int c = tuning().spmv_colsort_classes;
+    return c ? c : (colsort_fixed_for(tc) ? 1 : 16);
+}
 cudaError_t launch_spmv_colsort(int unit, const SpmvKBlock* blks, int b0, int b1, int rb, int rows,
                                 const double* val, const unsigned* meta, const double* x, double* y,
-                                cudaStream_t s);
+                                const ColsortRun& run, cudaStream_t s);
 
 // Launch accounting (rl_kernel_launches): every <<<>>> site reports itself.
 void note_launch(uint64_t n = 1);

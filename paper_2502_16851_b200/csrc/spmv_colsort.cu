@@ -15,23 +15,42 @@
 //             multiple of 32 with (val = 0, column col_lo, row = rows): the
 //             padding adds into a scratch slot past the block's rows that is
 //             never written back.
-// Within each window of 128 sorted entries the host orders the entries so
-// every aligned half-warp of 16 has distinct row % 16 where the window allows:
-// the 64-bit shared-memory accesses of a half-warp then hit distinct bank
-// pairs (tools/micro/spmv_colsort.cu: 0.2017 -> 0.1829 ms).
+// FP64 rows: within each window of 128 sorted entries the host orders the
+// entries so every aligned half-warp of 16 has distinct row % 16 where the
+// window allows: the 64-bit shared-memory accesses of a half-warp then hit
+// distinct bank pairs (tools/micro/spmv_colsort.cu: 0.2017 -> 0.1829 ms).
+// The fixed-point grid's 32-bit atomics gain nothing from such an order and
+// keep the plain column order, which reads x from the fewest lines
+// (tools/micro/colsort_banks.py: 0.1593 ms vs 0.1601-0.1617 with groups).
 //
 // CUDA core: 1024-thread CTAs, two per SM (y rows <= 8192 -> 64 KB each),
 // persistent over the blocks; each thread streams entries e, e+1024, e+2048
 // (val/meta evict_first, x gathers evict_last so x stays in L2), multiplies
-// and adds into its row with a shared-memory FP64 atomicAdd (a CAS loop on
-// sm_100a): FP64 arithmetic throughout, but the order of a row's additions is
-// not fixed, so repeated calls may differ in the last bits (within the 1e-12
-// norm-wise tolerance; the CSR kernels are the bit-reproducible path).
-// Measured alternatives (profiles/spmv_colsort_r2.md): exact 96-bit
-// fixed-point rows on native 32-bit shared atomics (bit-reproducible) ran
-// 0.185-0.21 ms -- the three atomics per entry saturate the MIO queue -- and a
-// 64-bit grid 0.154 ms but loses relative precision on rows far below their
-// block's largest product.
+// and adds the product into its row in shared memory.
+//
+// Row sums (spmv_colsort_fixed = 1, the CUDA-core default): on a 64-bit
+// fixed-point grid per block, q = RN(p 2^S) with S = 62 - hl - Et, where
+// |p| < 2^Et for every product of the block and a row has <= 2^hl of them, so
+// |row sum| <= 2^62 and nothing wraps; a q is added as two native 32-bit
+// shared atomics (low word, then high word plus the carry the first one's old
+// value gives).  Integer additions commute: the result does not depend on the
+// order, calls are bit-identical.  Et comes from the block's previous call
+// (plan creation: a guess assuming |x| < 1) and is checked against this
+// call's largest product; a mismatch redoes the block on the grid the data
+// calls for (Et rounded up to a multiple of 8, so x drifting by less than
+// 2^8 costs no redo).  Rows whose sum holds fewer than 45 + hl bits of the
+// grid (sum far below the block's largest product, or cancelling; ~0.1% of
+// the BASELINE rows) are summed again in FP64 from the CSR by 4 lanes each in
+// a fixed order, so every row is within 2^-46 of its own magnitude or within
+// the FP64 recursive-summation bound.  Inf/NaN products switch the block to
+// FP64 atomics (IEEE propagation).
+// spmv_colsort_fixed = 0 (and the tensor-core unit at 1): shared-memory FP64
+// atomicAdd (a CAS loop on sm_100a), FP64 arithmetic but the order of a row's
+// additions is not fixed, so repeated calls may differ in the last bits.
+// Measured (profiles/spmv_colsort_r2.md): CAS 0.178 ms, 64-bit grid 0.162 ms
+// (0.155 + the FP64 row kernel; summing the flagged rows inside the main
+// kernel stalls its stream: 0.191 ms); exact 96-bit rows (three atomics per entry)
+// 0.185-0.21 ms, MIO-bound.
 // Tensor core: the same layout and accumulation; the 32 products of a warp
 // step come out of 4 DMMA m8n8k4 (A and B masked to the k = j slot: lane
 // 4c+j's product is D_j[c][c]; 8 of the 64 outputs of each MMA are useful,
@@ -57,86 +76,232 @@ __device__ __forceinline__ unsigned ld_meta(const unsigned* p, uint64_t pol) {
     return v;
 }
 
-template <bool TC>
-__global__ void __launch_bounds__(kThreads, 2)
-    spmv_colsort(const SpmvKBlock* __restrict__ blks, int b0, int b1, int rb, const double* __restrict__ val,
-                 const unsigned* __restrict__ meta, const double* __restrict__ x, double* __restrict__ y) {
-    extern __shared__ double ys[];
+// Grid exponent a block's products call for: Et with |p| <= 2^Et, rounded up
+// to a multiple of kColsortQuantum so the grid -- and the result -- depends on
+// the data alone; kColsortFp64 when a product is Inf/NaN; `keep` when every
+// product is zero (any grid gives 0).
+__device__ __forceinline__ int grid_of(double mx, double nf, int keep) {
+    if (nf != nf || mx > 1.7976931348623157e308) return kColsortFp64;
+    if (mx == 0.0) return keep;
+    const int ea = ilogb(mx) + 1;  // |p| < 2^ea
+    return (ea >= 0 ? (ea + kColsortQuantum - 1) / kColsortQuantum : -((-ea) / kColsortQuantum)) * kColsortQuantum;
+}
+
+// One product onto the block's 64-bit grid: q = RN(p 2^S) (|q| < 2^62), low
+// word by a native shared atomic whose old value gives the carry, high word
+// (with the carry) by a second one.  Integer sums do not depend on order.
+__device__ __forceinline__ void add64(unsigned* __restrict__ lo, unsigned* __restrict__ hi, unsigned row, double p,
+                                      double f) {
+    const long long q = __double2ll_rn(p * f);
+    const unsigned l = (unsigned)q;
+    const unsigned old = atomicAdd(lo + row, l);
+    atomicAdd(hi + row, (unsigned)(q >> 32) + ((old + l) < old ? 1u : 0u));
+}
+
+// TRACK: keep the largest |product| and an Inf/NaN witness (the grid check)
+template <bool TC, bool FIXED, bool TRACK>
+__device__ __forceinline__ void block_entries(double* __restrict__ ys, unsigned* __restrict__ lo,
+                                              unsigned* __restrict__ hi, const double* __restrict__ vb,
+                                              const unsigned* __restrict__ mb, const double* __restrict__ xb,
+                                              unsigned nent, int rb, double f, uint64_t pol, uint64_t polx,
+                                              double& mx, double& nf) {
     const unsigned rmask = (1u << rb) - 1;
-    const uint64_t pol = policy_evict_first(), polx = policy_evict_last();
     const int lane = threadIdx.x & 31;
-    for (int b = b0 + blockIdx.x; b < b1; b += gridDim.x) {
-        const SpmvKBlock blk = blks[b];
-        for (unsigned i = threadIdx.x; i <= blk.rows; i += kThreads) ys[i] = 0.0;  // + the padding slot
-        __syncthreads();
-        const double* xb = x + blk.col_lo;
-        const double* vb = val + blk.e0;
-        const unsigned* mb = meta + blk.e0;
-        auto step = [&](double v, unsigned mt, double xv) {
-            if (!TC) {
-                atomicAdd(&ys[mt & rmask], v * xv);
-            } else {
-                // product of lane 4c+j is D_j[c][c], held by lane 4c + (c >> 1) in slot c & 1;
-                // one shuffle per MMA brings it back to lane 4c+j, then one full-warp add
-                const int c = lane >> 2;
-                const int home = 4 * c + (c >> 1);
-                double p = 0.0;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    // both operands masked to the k = j slot, so an Inf/NaN of another
-                    // entry never meets a zero of this one (Inf * 0 = NaN)
-                    double d0, d1;
-                    const bool mine = (lane & 3) == j;
-                    dmma_m8n8k4(d0, d1, mine ? v : 0.0, mine ? xv : 0.0, 0.0, 0.0);
-                    const double q = __shfl_sync(0xffffffffu, (c & 1) ? d1 : d0, home);
-                    if (mine) p = q;
-                }
-                atomicAdd(&ys[mt & rmask], p);
-            }
-        };
-        // nent is a multiple of 32: every warp step is full
-        unsigned e = threadIdx.x;
-        constexpr int U = TC ? 2 : kUnroll;  // the tensor-core step needs more registers
-        for (; e + (U - 1) * kThreads < blk.nent; e += U * kThreads) {
-            double v[U], xv[U];
-            unsigned mt[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                v[u] = ld_stream(vb + e + u * kThreads, pol);
-                mt[u] = ld_meta(mb + e + u * kThreads, pol);
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) xv[u] = ld_policy(xb + (mt[u] >> rb), polx);
-#pragma unroll
-            for (int u = 0; u < U; ++u) step(v[u], mt[u], xv[u]);
+    auto add = [&](unsigned row, double p) {
+        if (TRACK) {
+            mx = fmax(mx, fabs(p));
+            nf = fma(p, 0.0, nf);  // NaN iff some product is Inf / NaN
         }
-        // tail: whole warps only (nent is a multiple of 32), so the TC shuffles stay full
-        for (; e - lane < blk.nent; e += kThreads) {
-            const double v = ld_stream(vb + e, pol);
-            const unsigned mt = ld_meta(mb + e, pol);
-            step(v, mt, ld_policy(xb + (mt >> rb), polx));
+        if (FIXED) add64(lo, hi, row, p, f);
+        else atomicAdd(ys + row, p);
+    };
+    auto step = [&](double v, unsigned mt, double xv) {
+        if (!TC) {
+            add(mt & rmask, v * xv);
+        } else {
+            // product of lane 4c+j is D_j[c][c], held by lane 4c + (c >> 1) in slot c & 1;
+            // one shuffle per MMA brings it back to lane 4c+j, then one full-warp add
+            const int c = lane >> 2;
+            const int home = 4 * c + (c >> 1);
+            double p = 0.0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                // both operands masked to the k = j slot, so an Inf/NaN of another
+                // entry never meets a zero of this one (Inf * 0 = NaN)
+                double d0, d1;
+                const bool mine = (lane & 3) == j;
+                dmma_m8n8k4(d0, d1, mine ? v : 0.0, mine ? xv : 0.0, 0.0, 0.0);
+                const double q = __shfl_sync(0xffffffffu, (c & 1) ? d1 : d0, home);
+                if (mine) p = q;
+            }
+            add(mt & rmask, p);
         }
-        __syncthreads();
-        for (unsigned i = threadIdx.x; i < blk.rows; i += kThreads) y[blk.row0 + i] = ys[i];
-        __syncthreads();
+    };
+    // nent is a multiple of 32: every warp step is full
+    unsigned e = threadIdx.x;
+    constexpr int U = TC ? 2 : kUnroll;  // the tensor-core step needs more registers
+    for (; e + (U - 1) * kThreads < nent; e += U * kThreads) {
+        double v[U], xv[U];
+        unsigned mt[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            v[u] = ld_stream(vb + e + u * kThreads, pol);
+            mt[u] = ld_meta(mb + e + u * kThreads, pol);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) xv[u] = ld_policy(xb + (mt[u] >> rb), polx);
+#pragma unroll
+        for (int u = 0; u < U; ++u) step(v[u], mt[u], xv[u]);
+    }
+    // tail: whole warps only (nent is a multiple of 32), so the TC shuffles stay full
+    for (; e - lane < nent; e += kThreads) {
+        const double v = ld_stream(vb + e, pol);
+        const unsigned mt = ld_meta(mb + e, pol);
+        step(v, mt, ld_policy(xb + (mt >> rb), polx));
     }
 }
 
-// Order the entries of one window so that each aligned group of 16 (a
-// half-warp of 64-bit shared accesses) takes one entry from as many distinct
-// row % 16 classes (bank pairs) as the window has, largest classes first.
-void bank_order(std::vector<std::pair<uint64_t, double>>& t, size_t w0, size_t w1, unsigned rmask,
+template <bool TC>
+__global__ void __launch_bounds__(kThreads, 2)
+    spmv_colsort(const SpmvKBlock* __restrict__ blks, int b0, int b1, int rb, const double* __restrict__ val,
+                 const unsigned* __restrict__ meta, const double* __restrict__ x, double* __restrict__ y,
+                 ColsortRun run) {
+    // shared: (rows + 1) doubles (FP64 mode) or the grid's low and high words
+    // (2 (rows + 1) words, fixed-point mode) -- the same bytes
+    extern __shared__ double ys[];
+    __shared__ double s_red[2][kThreads / 32];
+    const uint64_t pol = policy_evict_first(), polx = policy_evict_last();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int b = b0 + blockIdx.x; b < b1; b += gridDim.x) {
+        const SpmvKBlock blk = blks[b];
+        const unsigned stride = blk.rows + 1;
+        unsigned* lo = reinterpret_cast<unsigned*>(ys);
+        unsigned* hi = lo + stride;
+        // the grid of the last call (plan creation: a guess from the block's
+        // values with |x| < 1), checked against this call's products below
+        int et = run.grid ? run.grid[b] : kColsortFp64;
+        for (int pass = 0;; ++pass) {
+            const int S = 62 - (int)blk.hl - et;
+            const bool fixed = et != kColsortFp64 && S >= -1000 && S <= 1000;
+            for (unsigned i = threadIdx.x; i < 2 * stride; i += kThreads) lo[i] = 0u;  // = stride doubles
+            __syncthreads();
+            double mx = 0.0, nf = 0.0;
+            if (fixed)
+                block_entries<TC, true, true>(ys, lo, hi, val + blk.e0, meta + blk.e0, x + blk.col_lo, blk.nent, rb,
+                                              scalbn(1.0, S), pol, polx, mx, nf);
+            else if (run.grid)
+                block_entries<TC, false, true>(ys, lo, hi, val + blk.e0, meta + blk.e0, x + blk.col_lo, blk.nent, rb,
+                                               0.0, pol, polx, mx, nf);
+            else
+                block_entries<TC, false, false>(ys, lo, hi, val + blk.e0, meta + blk.e0, x + blk.col_lo, blk.nent,
+                                                rb, 0.0, pol, polx, mx, nf);
+            if (run.grid) {  // block-wide largest |product| and Inf/NaN witness
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                    nf += __shfl_xor_sync(0xffffffffu, nf, o);
+                }
+                if (lane == 0) s_red[0][warp] = mx, s_red[1][warp] = nf;
+            }
+            __syncthreads();
+            if (run.grid) {
+                mx = 0.0;
+                nf = 0.0;
+#pragma unroll 8
+                for (int w = 0; w < kThreads / 32; ++w) mx = fmax(mx, s_red[0][w]), nf += s_red[1][w];
+            }
+            // The grid the data calls for.  A fixed-point pass on another grid is
+            // redone (too fine a grid may have wrapped, a coarser one rounds
+            // differently), and so is an FP64 pass the data would allow on a
+            // grid, so the result depends on the data alone.
+            const int want = run.grid ? grid_of(mx, nf, fixed ? et : 0) : kColsortFp64;
+            const bool again = pass < 2 && (fixed ? want != et : want != kColsortFp64);
+            if (threadIdx.x == 0 && run.grid) run.grid[b] = want;
+            if (!again) {
+                if (fixed) {
+                    // rows whose sum holds fewer than 45 + hl bits of the grid (it
+                    // lies far below the block's largest product, or cancels) are
+                    // summed again by the FP64 row kernel, so every row is within 2^-46 relative
+                    const long long lim = 1ll << (45 + (int)blk.hl);
+                    const double inv = scalbn(1.0, -S);
+                    for (unsigned i = threadIdx.x; i < blk.rows; i += kThreads) {
+                        const long long V = (long long)(((unsigned long long)hi[i] << 32) | lo[i]);
+                        const bool flag = mx > 0.0 && V > -lim && V < lim;
+                        if (!flag) y[blk.row0 + i] = __ll2double_rn(V) * inv;
+                        const unsigned am = __activemask();
+                        const unsigned bal = __ballot_sync(am, flag);
+                        if (bal) {
+                            const int lead = __ffs(am) - 1;
+                            unsigned base = 0;
+                            if (lane == lead) base = atomicAdd(run.count, (unsigned)__popc(bal));
+                            base = __shfl_sync(am, base, lead);
+                            if (flag) run.list[base + __popc(bal & ((1u << lane) - 1))] = (int)(blk.row0 + i);
+                        }
+                    }
+                } else {
+                    for (unsigned i = threadIdx.x; i < blk.rows; i += kThreads) y[blk.row0 + i] = ys[i];
+                }
+                __syncthreads();
+                break;
+            }
+            et = want;
+            __syncthreads();
+        }
+    }
+}
+
+// The rows the fixed-point blocks handed over, summed in FP64 by 4 lanes each
+// (lane c takes entries c, c+4, ... in CSR order, then a fixed xor tree:
+// bit-reproducible); 8 rows per warp.  The list entry is read beside the
+// count (the list has room for every row) to save one dependent load.  The
+// last CTA to finish resets the count for the next call.
+__global__ void __launch_bounds__(256) spmv_flagged_rows(ColsortRun run, const double* __restrict__ x,
+                                                         double* __restrict__ y) {
+    const int c = threadIdx.x & 3;
+    const unsigned ng = gridDim.x * 64, g0 = blockIdx.x * 64 + (threadIdx.x >> 2);
+    const int r0 = g0 < run.rows ? __ldcg(run.list + g0) : 0;
+    const unsigned n = __ldcg(run.count);
+    for (unsigned i0 = 0; i0 < n; i0 += ng) {  // uniform trip count per warp (full-mask shuffles)
+        const unsigned i = i0 + g0;
+        double sum = 0.0;
+        int r = -1;
+        if (i < n) {
+            r = i0 == 0 ? r0 : __ldcg(run.list + i);
+            const int a = __ldg(run.rp + r), e = __ldg(run.rp + r + 1);
+            for (int j = a + c; j < e; j += 4)
+                sum = fma(__ldg(run.val + j), __ldg(x + (__ldg(run.col + j) - run.col_base)), sum);
+        }
+        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+        if (c == 0 && r >= 0) y[r] = sum;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(run.done, 1u) == gridDim.x - 1) {
+            *run.count = 0;
+            *run.done = 0;
+            __threadfence();
+        }
+    }
+}
+
+// Order the entries of one window so that each aligned group of g takes one
+// entry from as many distinct row % g classes as the window has, largest
+// classes first: g = 16 for FP64 rows (a half-warp of 64-bit accesses, bank
+// pairs), g = 32 for the fixed-point grid's 32-bit words (a warp, banks).
+void bank_order(std::vector<std::pair<uint64_t, double>>& t, size_t w0, size_t w1, unsigned rmask, int g,
                 std::vector<std::pair<uint64_t, double>>& out) {
-    std::vector<std::pair<uint64_t, double>> cls[16];
-    for (size_t i = w0; i < w1; ++i) cls[(t[i].first & rmask) & 15].push_back(t[i]);
+    std::vector<std::pair<uint64_t, double>> cls[32];
+    for (size_t i = w0; i < w1; ++i) cls[(t[i].first & rmask) % g].push_back(t[i]);
     size_t left = w1 - w0;
     out.clear();
     while (left) {
-        int order[16];
-        for (int c = 0; c < 16; ++c) order[c] = c;
-        std::stable_sort(order, order + 16, [&](int a, int b) { return cls[a].size() > cls[b].size(); });
+        int order[32];
+        for (int c = 0; c < g; ++c) order[c] = c;
+        std::stable_sort(order, order + g, [&](int a, int b) { return cls[a].size() > cls[b].size(); });
         int taken = 0;
-        for (int oi = 0; oi < 16 && left; ++oi) {
+        for (int oi = 0; oi < g && left; ++oi) {
             auto& c = cls[order[oi]];
             if (c.empty()) continue;
             out.push_back(c.back());
@@ -144,9 +309,9 @@ void bank_order(std::vector<std::pair<uint64_t, double>>& t, size_t w0, size_t w
             --left;
             ++taken;
         }
-        while (taken < 16 && left) {  // fewer than 16 classes left: conflicts unavoidable
+        while (taken < g && left) {  // fewer than g classes left: conflicts unavoidable
             int big = 0;
-            for (int c = 1; c < 16; ++c)
+            for (int c = 1; c < g; ++c)
                 if (cls[c].size() > cls[big].size()) big = c;
             out.push_back(cls[big].back());
             cls[big].pop_back();
@@ -159,7 +324,7 @@ void bank_order(std::vector<std::pair<uint64_t, double>>& t, size_t w0, size_t w
 }  // namespace
 
 bool spmv_colsort_build(uint64_t m, uint64_t n, const int32_t* rp, const int32_t* col, const double* val,
-                        SpmvColsortLayout& L, const std::vector<ColsortSegment>& segments_in) {
+                        SpmvColsortLayout& L, const std::vector<ColsortSegment>& segments_in, int classes) {
     (void)n;
     if (m == 0 || rp[m] == 0) return false;
     int64_t maxlen = 0;
@@ -210,8 +375,24 @@ bool spmv_colsort_build(uint64_t m, uint64_t n, const int32_t* rp, const int32_t
             k.rows = (uint32_t)(r1 - r0);
             k.nent = (uint32_t)((cnt + 31) / 32 * 32);
             int32_t lo = INT32_MAX;
-            for (int64_t j = rp[r0]; j < rp[r1]; ++j) lo = std::min(lo, col[j]);
+            int ev = 0;
+            bool nonfinite = false;
+            for (int64_t j = rp[r0]; j < rp[r1]; ++j) {
+                lo = std::min(lo, col[j]);
+                uint64_t bits;
+                std::memcpy(&bits, &val[j], 8);
+                const int f = (int)((bits >> 52) & 0x7FF);
+                if (f == 0x7FF) nonfinite = true;
+                else ev = std::max(ev, f);
+            }
             k.col_lo = cnt ? lo : 0;
+            k.ev = (int16_t)ev;
+            k.flags = nonfinite ? 1 : 0;
+            int64_t mlen = 0;
+            for (uint64_t r = r0; r < r1; ++r) mlen = std::max<int64_t>(mlen, (int64_t)rp[r + 1] - rp[r]);
+            int hl = 0;
+            while ((1ll << hl) < mlen) ++hl;  // a row sums <= 2^hl products: |V| <= 2^62
+            k.hl = (uint8_t)hl;
             e += k.nent;
         }
         L.val.assign(e, 0.0);
@@ -228,8 +409,9 @@ bool spmv_colsort_build(uint64_t m, uint64_t n, const int32_t* rp, const int32_t
                         t.push_back({((uint64_t)(col[j] - k.col_lo) << rb) | (r - r0), val[j]});
                 std::sort(t.begin(), t.end(), [](const auto& a, const auto& c) { return a.first < c.first; });
                 const size_t win = (size_t)std::max(32, tuning().spmv_colsort_window);
-                for (size_t w0 = 0; w0 < t.size(); w0 += win)
-                    bank_order(t, w0, std::min(t.size(), w0 + win), rmask, scratch);
+                const int g = std::min(32, std::max(1, classes));
+                for (size_t w0 = 0; g > 1 && w0 < t.size(); w0 += win)
+                    bank_order(t, w0, std::min(t.size(), w0 + win), rmask, g, scratch);
                 for (size_t i = 0; i < t.size(); ++i) {
                     L.meta[k.e0 + i] = (uint32_t)t[i].first;
                     L.val[k.e0 + i] = t[i].second;
@@ -246,9 +428,15 @@ bool spmv_colsort_build(uint64_t m, uint64_t n, const int32_t* rp, const int32_t
     }
 }
 
+int colsort_initial_grid(const SpmvKBlock& k) {
+    if (k.flags & 1) return kColsortFp64;
+    const int ea = std::max((int)k.ev, 1) - 1022;  // |x| < 1 assumed: |p| < 2^(ev - 1023 + 1)
+    return (ea >= 0 ? (ea + kColsortQuantum - 1) / kColsortQuantum : -((-ea) / kColsortQuantum)) * kColsortQuantum;
+}
+
 cudaError_t launch_spmv_colsort(int unit, const SpmvKBlock* blks, int b0, int b1, int rb, int rows,
                                 const double* val, const unsigned* meta, const double* x, double* y,
-                                cudaStream_t s) {
+                                const ColsortRun& run, cudaStream_t s) {
     if (b1 <= b0) return cudaSuccess;
     const size_t smem = (size_t)(rows + 1) * 8;
     const int grid = std::min(b1 - b0, 2 * kNumSMs);
@@ -256,12 +444,15 @@ cudaError_t launch_spmv_colsort(int unit, const SpmvKBlock* blks, int b0, int b1
     if (unit) {
         e = cudaFuncSetAttribute(spmv_colsort<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        spmv_colsort<true><<<grid, kThreads, smem, s>>>(blks, b0, b1, rb, val, meta, x, y);
+        spmv_colsort<true><<<grid, kThreads, smem, s>>>(blks, b0, b1, rb, val, meta, x, y, run);
     } else {
         e = cudaFuncSetAttribute(spmv_colsort<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        spmv_colsort<false><<<grid, kThreads, smem, s>>>(blks, b0, b1, rb, val, meta, x, y);
+        spmv_colsort<false><<<grid, kThreads, smem, s>>>(blks, b0, b1, rb, val, meta, x, y, run);
     }
+    note_launch();
+    if ((e = cudaGetLastError()) != cudaSuccess || !run.grid) return e;
+    spmv_flagged_rows<<<2 * kNumSMs, 256, 0, s>>>(run, x, y);
     note_launch();
     return cudaGetLastError();
 }

@@ -450,9 +450,9 @@ def _fsum_rows(rp, col, val, x):
 @pytest.mark.parametrize("unit", UNITS)
 @pytest.mark.parametrize("m,k,hb", [(20000, 16, 65536), (7001, 7, 300), (3000, 64, 1000)])
 def test_colsort_within_fp64_summation_bound(cuda, unit, m, k, hb):
-    """K17 rows are FP64 sums in some order: every row within the recursive
-    summation bound (L - 1) u sum|p| of the exact sum (math.fsum), on both
-    units and on every call."""
+    """K17 rows against the exact sum (math.fsum): within the recursive
+    summation bound (L - 1) u sum|p| or within 2^-46 of the row's magnitude
+    (fixed-point rows), on both units and on every call."""
     import torch
 
     rng = np.random.default_rng(m + k)
@@ -474,7 +474,10 @@ def test_colsort_within_fp64_summation_bound(cuda, unit, m, k, hb):
             plan.execute(dx, dy)
             torch.cuda.synchronize()
             err = np.abs(dy.cpu().numpy() - want)
-            assert np.all(err <= np.maximum(lens - 1, 1) * 2.0 ** -53 * absum * 1.0001)
+            # FP64 rows (atomics or the row kernel): the recursive-summation bound;
+            # fixed-point rows: within 2^-46 of their own magnitude
+            assert np.all(err <= np.maximum(np.maximum(lens - 1, 1) * 2.0 ** -53 * absum * 1.0001,
+                                            2.0 ** -46 * np.abs(want)))
     finally:
         plan.close()
 
@@ -547,5 +550,58 @@ def test_colsort_nonfinite(cuda, unit):
         assert np.array_equal(np.isposinf(y), np.isposinf(want)) and np.array_equal(np.isneginf(y), np.isneginf(want))
         f = np.isfinite(want)
         assert O.rel_err(y[f], want[f]) <= TOL
+    finally:
+        plan.close()
+
+
+@pytest.mark.parametrize("unit", UNITS)
+@pytest.mark.parametrize("fixed", [1, 2, 0])
+def test_colsort_small_rows_spikes_and_determinism(cuda, unit, fixed):
+    """Rows whose sum cancels or whose products all lie far below the block's
+    largest (an x spike of 1e12 in every block's window) leave the 64-bit grid
+    for the FP64 row kernel: every row within the FP64 recursive-summation
+    bound of the exact sum.  Fixed-point results are bit-identical call to
+    call (spmv_colsort_fixed: 1 the CUDA-core unit, 2 both); x = 0 gives exact
+    zeros."""
+    import torch
+
+    rng = np.random.default_rng(77)
+    m = n = 60000
+    rp, col, val = O.gen_band_csr(m, 0, n, 12, 4000, 6)
+    val = val.copy()
+    # cancelling rows: second half of each row the negated first half, same x
+    for i in range(0, m, 97):
+        a, b = rp[i], rp[i + 1]
+        h = (b - a) // 2
+        val[a + h:a + 2 * h] = -val[a:a + h]
+    x = rng.uniform(-1, 1, n)
+    x[::5000] = 1e12  # spikes
+    want = _fsum_rows(rp, col, val, x)
+    absum = np.array([np.abs(val[rp[i]:rp[i + 1]] * x[col[rp[i]:rp[i + 1]]]).sum() for i in range(m)])
+    lens = np.diff(rp)
+    prev = P.tuning_set("spmv_colsort_fixed", fixed)
+    try:
+        plan = P.SpmvPlan(rp, col, val, n, unit=unit)
+    finally:
+        P.tuning_set("spmv_colsort_fixed", prev)
+    try:
+        dx = torch.from_numpy(x).cuda()
+        outs = []
+        for _ in range(3):
+            dy = torch.full((m,), float("nan"), dtype=torch.float64, device="cuda")
+            plan.execute(dx, dy)
+            torch.cuda.synchronize()
+            outs.append(dy.clone())
+        got = outs[-1].cpu().numpy()
+        err = np.abs(got - want)
+        assert np.all(err <= np.maximum(np.maximum(lens - 1, 1) * 2.0 ** -53 * absum * 1.0001,
+                                        2.0 ** -46 * np.abs(want)))
+        if fixed == 2 or (fixed == 1 and unit == P.CUDA_CORE):
+            assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
+        dz = torch.zeros(n, dtype=torch.float64, device="cuda")
+        dy = torch.full((m,), float("nan"), dtype=torch.float64, device="cuda")
+        plan.execute(dz, dy)
+        torch.cuda.synchronize()
+        assert (dy == 0).all()
     finally:
         plan.close()

@@ -16,6 +16,8 @@ pin = lambda t: t.cpu().pin_memory()
 hrp, hcol, hval, hx = pin(rp), pin(col), pin(val), pin(x)
 t0 = time.perf_counter()
 configs = [(c, s, t) for c in (6, 8, 10, 12) for t in (0, 1, 3, 7) for s in (1,)]
+if len(sys.argv) > 1:  # e.g. "8,1,1 6,1,1": chunks,streams,taper triples
+    configs = [tuple(int(v) for v in a.split(",")) for a in sys.argv[1:]]
 for chunks, streams, taper in configs:
     zc = 0
     P.tuning_set("spmv_plan_taper", taper)
