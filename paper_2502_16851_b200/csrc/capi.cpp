@@ -518,7 +518,8 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
         // spans fit); else the caller's CSR with the long-row path
         rlb::SpmvColsortLayout L;
         if (rlb::tuning().spmv_plan_colsort && nnz > 0 &&
-            rlb::spmv_colsort_build(m, n, rp, col, val, L, {}, rlb::colsort_classes(unit == ExecutionUnit::TensorCore))) {
+            rlb::spmv_colsort_build(m, n, rp, col, val, L, {}, rlb::colsort_classes(unit == ExecutionUnit::TensorCore),
+                                    unit == ExecutionUnit::TensorCore)) {
             pl->colsort = true;
             pl->krb = L.rb;
             pl->krows = L.rows;
@@ -1285,6 +1286,8 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         {"spmv_plan_colsort_chunks", &rlb::Tuning::spmv_plan_colsort_chunks, false},
         {"spmv_colsort_window", &rlb::Tuning::spmv_colsort_window, false},
         {"spmv_colsort_classes", &rlb::Tuning::spmv_colsort_classes, false},
+        {"spmv_colsort_tc_shape", &rlb::Tuning::spmv_colsort_tc_shape, false},
+        {"spmv_colsort_cc_shape", &rlb::Tuning::spmv_colsort_cc_shape, false},
         {"spmv_plan_ygroups", &rlb::Tuning::spmv_plan_ygroups, false},
         {"stencil_r_ctas_per_sm", &rlb::Tuning::stencil_r_ctas_per_sm, false},
         {"stencil_tb_waves", &rlb::Tuning::stencil_tb_waves, false},

@@ -452,7 +452,7 @@ void colsort_part(rl_dist_spmv_s::Part& q, uint64_t rows, uint64_t nnz, bool tc)
                                              {rows, std::max<uint64_t>(1, 2 * (uint64_t)rlb::kNumSMsHost - eb)}};
     rlb::SpmvColsortLayout L;
     if (!rlb::spmv_colsort_build(rows, q.g.ce - q.g.cb, hrp.data(), hcol.data(), hval.data(), L, segs,
-                                 rlb::colsort_classes(tc)))
+                                 rlb::colsort_classes(tc), tc))
         return;
     // block order: edge blocks first, then the interior, so each phase is one launch
     std::stable_partition(L.blocks.begin(), L.blocks.end(), [&](const rlb::SpmvKBlock& k) {

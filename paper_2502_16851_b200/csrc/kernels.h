@@ -33,8 +33,12 @@ struct Tuning {
     int spmv_colsort_window = 128; // K17 plan build: entries per bank-ordering window (tools/micro/spmv_colsort.cu: 64 0.185, 128 0.183 ms)
     int stencil_tb27r = 1;         // 3d27pt t = 2 (class weights): the register-blocked kernel (stencil_tb27r.cu); 0: z-column
     int spmv_colsort_classes = 0;  // K17 bank-ordering group 1..32 (0: 1 = none on the fixed-point grid, 16 for FP64 rows)
-    int spmv_colsort_fixed = 1;    // K17 rows on a 64-bit fixed-point grid (+ FP64 row kernel for flagged rows):
+    int spmv_colsort_fixed = 2;    // K17 rows on a 64-bit fixed-point grid (+ FP64 row kernel for flagged rows):
                                    // 1 CUDA-core unit only, 2 both units, 0 neither (FP64 shared atomics)
+    int spmv_colsort_tc_shape = 7; // K17 tensor-core CTA shape (threads x entries per step): 0 1024x3, 1 768x3, 4 1024x2;
+                                   // software-pipelined 5 1024x1, 6 768x2, 7 640x3, 8 512x4, 9 1024x2
+                                   // (tools/micro/spmv_shapes.py, median of 15 interleaved bursts: TC 7 0.184 vs 0 0.207 ms)
+    int spmv_colsort_cc_shape = 6; // ... CUDA-core kernel, same codes (CC 6 0.171, 8 0.170, 0 0.175 ms)
     int spmv_plan_colsort = 1;     // plans (both units) use the column-sorted row-block layout (K17, spmv_colsort.cu) when eligible; 0: CSR
     int spmv_plan_xpieces = 0;     // max x upload pieces (first = chunk 0's prefix); 0: one per chunk
     int spmv_plan_ygroups = 0;     // y download copies (groups of consecutive chunks); 0: one per chunk
@@ -240,7 +244,7 @@ struct ColsortSegment {
 };
 bool spmv_colsort_build(uint64_t m, uint64_t n, const int32_t* rp, const int32_t* col, const double* val,
                         SpmvColsortLayout& layout, const std::vector<ColsortSegment>& segments = {},
-                        int classes = 16);
+                        int classes = 16, bool tc_lanes = false);
 // bank-ordering classes of a K17 layout for this unit (1: plain column order on the
 // fixed-point grid, 16: FP64 rows)
 inline int colsort_classes(bool tc) {

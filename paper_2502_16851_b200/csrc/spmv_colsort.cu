@@ -51,11 +51,21 @@
 // (0.155 + the FP64 row kernel; summing the flagged rows inside the main
 // kernel stalls its stream: 0.191 ms); exact 96-bit rows (three atomics per entry)
 // 0.185-0.21 ms, MIO-bound.
-// Tensor core: the same layout and accumulation; the 32 products of a warp
-// step come out of 4 DMMA m8n8k4 (A and B masked to the k = j slot: lane
-// 4c+j's product is D_j[c][c]; 8 of the 64 outputs of each MMA are useful,
-// the most a K = 4 product of per-entry operands allows), shuffled back to
-// their lanes for the same shared-memory add.
+// Tensor core: the same blocks and accumulation; the 32 products of a warp
+// step come out of TWO DMMA m8n8k4.  A product of per-entry operands is
+// isolated in an output only when that output's other three k terms are zero,
+// so each MMA's k slots own disjoint quadrants of the 8x8 output: k's A
+// column is non-zero on 4 rows M_k, its B row on 4 columns N_k, the four
+// M_k x N_k tile the output, and a bijection M_k -> N_k pairs 4 (val, x)
+// per k -- 16 isolated products per MMA (the most four disjoint rectangles in
+// 8x8 allow), 32 per two.  The second MMA uses the complementary A and B
+// slots and the opposite diagonal, so every lane owns exactly one A operand,
+// one B operand and one useful output across the pair.  The host stores each
+// 32-entry group permuted to those roles (tc_roles): val in A-slot order, the
+// column bits of meta in B-slot order, the row bits in output order -- the
+// same 12 B per entry, no shuffles (the FP64 fallback below unpermutes with
+// two).  Measured against the round's first form (4 masked DMMA per step,
+// 8 useful outputs each, shuffled home): see profiles/spmv_colsort_r2.md.
 #include <algorithm>
 #include <cstring>
 #include <thread>
@@ -68,6 +78,20 @@ namespace rlb {
 
 namespace {
 constexpr int kThreads = 1024;
+
+// Tensor-core lane roles of the entry whose value sits in A slot `la` = 4m+k
+// (A[m][k]): which MMA of the pair (first: rows 0-3 with k < 2, rows 4-7 with
+// k >= 2), its B slot lb (B[k][n] is held by lane 4n+k) and the lane ld whose
+// output D[m][n] holds its product (lane 4m + n/2, element n & 1 = m & 1).
+// First MMA: k even -> columns 0-3, k odd -> 4-7, n = m mod 4 (+4); second:
+// the other half, n = (m mod 4) ^ 2 (+4).
+__host__ __device__ __forceinline__ void tc_roles(int la, int& lb, int& ld) {
+    const int m = la >> 2, k = la & 3;
+    const bool first = ((la >> 4) & 1) == ((la >> 1) & 1);
+    const int n = first ? (m & 3) + ((k & 1) << 2) : ((m & 3) ^ 2) + ((k & 1) ? 0 : 4);
+    lb = 4 * n + k;
+    ld = 4 * m + (n >> 1);
+}
 constexpr int kUnroll = 3;  // entry loads in flight per thread (measured: U2 0.183, U3 0.173, U4 0.193 ms)
 
 __device__ __forceinline__ unsigned ld_meta(const unsigned* p, uint64_t pol) {
@@ -79,11 +103,15 @@ __device__ __forceinline__ unsigned ld_meta(const unsigned* p, uint64_t pol) {
 // Grid exponent a block's products call for: Et with |p| <= 2^Et, rounded up
 // to a multiple of kColsortQuantum so the grid -- and the result -- depends on
 // the data alone; kColsortFp64 when a product is Inf/NaN; `keep` when every
-// product is zero (any grid gives 0).
-__device__ __forceinline__ int grid_of(double mx, double nf, int keep) {
-    if (nf != nf || mx > 1.7976931348623157e308) return kColsortFp64;
-    if (mx == 0.0) return keep;
-    const int ea = ilogb(mx) + 1;  // |p| < 2^ea
+// product is zero (any grid gives 0).  The products are tracked as integers:
+// mh = the largest high word of |p| (IEEE order is integer order for
+// non-negative doubles, Inf/NaN the largest: exponent field 0x7FF), ml = the OR
+// of the low words (a product with a zero high word is still non-zero).
+__device__ __forceinline__ int grid_of(unsigned mh, unsigned ml, int keep) {
+    if (mh >= 0x7ff00000u) return kColsortFp64;
+    if ((mh | ml) == 0u) return keep;
+    const int e = (int)(mh >> 20);
+    const int ea = e ? e - 1022 : -1022;  // |p| < 2^ea
     return (ea >= 0 ? (ea + kColsortQuantum - 1) / kColsortQuantum : -((-ea) / kColsortQuantum)) * kColsortQuantum;
 }
 
@@ -99,77 +127,131 @@ __device__ __forceinline__ void add64(unsigned* __restrict__ lo, unsigned* __res
 }
 
 // TRACK: keep the largest |product| and an Inf/NaN witness (the grid check)
-template <bool TC, bool FIXED, bool TRACK>
+template <bool TC, bool FIXED, bool TRACK, int NT, int UF, bool PIPE>
 __device__ __forceinline__ void block_entries(double* __restrict__ ys, unsigned* __restrict__ lo,
                                               unsigned* __restrict__ hi, const double* __restrict__ vb,
                                               const unsigned* __restrict__ mb, const double* __restrict__ xb,
                                               unsigned nent, int rb, double f, uint64_t pol, uint64_t polx,
-                                              double& mx, double& nf) {
+                                              unsigned& mh, unsigned& ml) {
     const unsigned rmask = (1u << rb) - 1;
     const int lane = threadIdx.x & 31;
     auto add = [&](unsigned row, double p) {
-        if (TRACK) {
-            mx = fmax(mx, fabs(p));
-            nf = fma(p, 0.0, nf);  // NaN iff some product is Inf / NaN
+        if (TRACK) {  // integer ops only: the FP64 pipe is the tensor core's too
+            mh = max(mh, (unsigned)__double2hiint(p) & 0x7fffffffu);
+            ml |= (unsigned)__double2loint(p);
         }
         if (FIXED) add64(lo, hi, row, p, f);
         else atomicAdd(ys + row, p);
     };
+    // tensor core, lane-permuted layout: this lane's A operand (v) and B
+    // operand (xv) belong to the first MMA or the second, and so does its output
+    const bool a_first = ((lane >> 4) & 1) == ((lane >> 1) & 1);
+    const bool b_first = (lane & 1) == ((lane >> 4) & 1);
+    const bool d_first = (lane & 1) == ((lane >> 3) & 1);
+    const bool d_odd = (lane >> 2) & 1;
+    int lb = 0, ld = 0;
+    tc_roles(lane, lb, ld);
     auto step = [&](double v, unsigned mt, double xv) {
         if (!TC) {
             add(mt & rmask, v * xv);
+        } else if (FIXED) {
+            // two DMMA give the warp's 32 products, one per lane, no data exchange.
+            // A zero operand meeting an Inf/NaN x makes a neighbour's product NaN:
+            // the block's witness then sends it to the FP64 pass below.
+            double d10, d11, d20, d21;
+            dmma_m8n8k4(d10, d11, a_first ? v : 0.0, b_first ? xv : 0.0, 0.0, 0.0);
+            dmma_m8n8k4(d20, d21, a_first ? 0.0 : v, b_first ? 0.0 : xv, 0.0, 0.0);
+            add(mt & rmask, d_first ? (d_odd ? d11 : d10) : (d_odd ? d21 : d20));
         } else {
-            // product of lane 4c+j is D_j[c][c], held by lane 4c + (c >> 1) in slot c & 1;
-            // one shuffle per MMA brings it back to lane 4c+j, then one full-warp add
+            // FP64 pass (and Inf/NaN data): bring this A slot's x and row home
+            // with two shuffles, then 4 DMMA with both operands masked to one k
+            // slot, so an Inf/NaN never meets another entry's zero (Inf * 0 = NaN).
+            // The product of lane 4c+j is D_j[c][c], held by lane 4c + (c >> 1) in
+            // slot c & 1; one shuffle per MMA brings it back.
+            const double xa = __shfl_sync(0xffffffffu, xv, lb);
+            const unsigned ra = __shfl_sync(0xffffffffu, mt & rmask, ld);
             const int c = lane >> 2;
             const int home = 4 * c + (c >> 1);
             double p = 0.0;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                // both operands masked to the k = j slot, so an Inf/NaN of another
-                // entry never meets a zero of this one (Inf * 0 = NaN)
                 double d0, d1;
                 const bool mine = (lane & 3) == j;
-                dmma_m8n8k4(d0, d1, mine ? v : 0.0, mine ? xv : 0.0, 0.0, 0.0);
+                dmma_m8n8k4(d0, d1, mine ? v : 0.0, mine ? xa : 0.0, 0.0, 0.0);
                 const double q = __shfl_sync(0xffffffffu, (c & 1) ? d1 : d0, home);
                 if (mine) p = q;
             }
-            add(mt & rmask, p);
+            add(ra, p);
         }
     };
     // nent is a multiple of 32: every warp step is full
     unsigned e = threadIdx.x;
-    constexpr int U = TC ? 2 : kUnroll;  // the tensor-core step needs more registers
-    for (; e + (U - 1) * kThreads < nent; e += U * kThreads) {
-        double v[U], xv[U];
+    constexpr int U = (TC && !FIXED) ? 2 : UF;  // the FP64 tensor-core step needs more registers
+    if (PIPE && FIXED) {
+        // software-pipelined: the next U entries' val/meta loads are in flight
+        // while this step gathers x and adds, so the stream never waits on the
+        // x gather and the add chain
+        double v[U];
         unsigned mt[U];
+        if (e + (U - 1) * NT < nent) {
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            v[u] = ld_stream(vb + e + u * kThreads, pol);
-            mt[u] = ld_meta(mb + e + u * kThreads, pol);
+            for (int u = 0; u < U; ++u) {
+                v[u] = ld_stream(vb + e + u * NT, pol);
+                mt[u] = ld_meta(mb + e + u * NT, pol);
+            }
+            for (;;) {
+                const bool more = e + (2 * U - 1) * NT < nent;
+                double vn[U], xv[U];
+                unsigned mn[U];
+                if (more) {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        vn[u] = ld_stream(vb + e + (U + u) * NT, pol);
+                        mn[u] = ld_meta(mb + e + (U + u) * NT, pol);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) xv[u] = ld_policy(xb + (mt[u] >> rb), polx);
+#pragma unroll
+                for (int u = 0; u < U; ++u) step(v[u], mt[u], xv[u]);
+                e += U * NT;
+                if (!more) break;
+#pragma unroll
+                for (int u = 0; u < U; ++u) v[u] = vn[u], mt[u] = mn[u];
+            }
         }
+    } else {
+        for (; e + (U - 1) * NT < nent; e += U * NT) {
+            double v[U], xv[U];
+            unsigned mt[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) xv[u] = ld_policy(xb + (mt[u] >> rb), polx);
+            for (int u = 0; u < U; ++u) {
+                v[u] = ld_stream(vb + e + u * NT, pol);
+                mt[u] = ld_meta(mb + e + u * NT, pol);
+            }
 #pragma unroll
-        for (int u = 0; u < U; ++u) step(v[u], mt[u], xv[u]);
+            for (int u = 0; u < U; ++u) xv[u] = ld_policy(xb + (mt[u] >> rb), polx);
+#pragma unroll
+            for (int u = 0; u < U; ++u) step(v[u], mt[u], xv[u]);
+        }
     }
     // tail: whole warps only (nent is a multiple of 32), so the TC shuffles stay full
-    for (; e - lane < nent; e += kThreads) {
+    for (; e - lane < nent; e += NT) {
         const double v = ld_stream(vb + e, pol);
         const unsigned mt = ld_meta(mb + e, pol);
         step(v, mt, ld_policy(xb + (mt >> rb), polx));
     }
 }
 
-template <bool TC>
-__global__ void __launch_bounds__(kThreads, 2)
+template <bool TC, int NT, int UF, bool PIPE>
+__global__ void __launch_bounds__(NT, 2)
     spmv_colsort(const SpmvKBlock* __restrict__ blks, int b0, int b1, int rb, const double* __restrict__ val,
                  const unsigned* __restrict__ meta, const double* __restrict__ x, double* __restrict__ y,
                  ColsortRun run) {
     // shared: (rows + 1) doubles (FP64 mode) or the grid's low and high words
     // (2 (rows + 1) words, fixed-point mode) -- the same bytes
     extern __shared__ double ys[];
-    __shared__ double s_red[2][kThreads / 32];
+    __shared__ unsigned s_red[2][NT / 32];
     const uint64_t pol = policy_evict_first(), polx = policy_evict_last();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int b = b0 + blockIdx.x; b < b1; b += gridDim.x) {
@@ -183,38 +265,35 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int pass = 0;; ++pass) {
             const int S = 62 - (int)blk.hl - et;
             const bool fixed = et != kColsortFp64 && S >= -1000 && S <= 1000;
-            for (unsigned i = threadIdx.x; i < 2 * stride; i += kThreads) lo[i] = 0u;  // = stride doubles
+            for (unsigned i = threadIdx.x; i < 2 * stride; i += NT) lo[i] = 0u;  // = stride doubles
             __syncthreads();
-            double mx = 0.0, nf = 0.0;
+            unsigned mh = 0u, ml = 0u;
             if (fixed)
-                block_entries<TC, true, true>(ys, lo, hi, val + blk.e0, meta + blk.e0, x + blk.col_lo, blk.nent, rb,
-                                              scalbn(1.0, S), pol, polx, mx, nf);
+                block_entries<TC, true, true, NT, UF, PIPE>(ys, lo, hi, val + blk.e0, meta + blk.e0, x + blk.col_lo, blk.nent, rb,
+                                              scalbn(1.0, S), pol, polx, mh, ml);
             else if (run.grid)
-                block_entries<TC, false, true>(ys, lo, hi, val + blk.e0, meta + blk.e0, x + blk.col_lo, blk.nent, rb,
-                                               0.0, pol, polx, mx, nf);
+                block_entries<TC, false, true, NT, UF, PIPE>(ys, lo, hi, val + blk.e0, meta + blk.e0, x + blk.col_lo, blk.nent, rb,
+                                               0.0, pol, polx, mh, ml);
             else
-                block_entries<TC, false, false>(ys, lo, hi, val + blk.e0, meta + blk.e0, x + blk.col_lo, blk.nent,
-                                                rb, 0.0, pol, polx, mx, nf);
-            if (run.grid) {  // block-wide largest |product| and Inf/NaN witness
-#pragma unroll
-                for (int o = 16; o; o >>= 1) {
-                    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-                    nf += __shfl_xor_sync(0xffffffffu, nf, o);
-                }
-                if (lane == 0) s_red[0][warp] = mx, s_red[1][warp] = nf;
+                block_entries<TC, false, false, NT, UF, PIPE>(ys, lo, hi, val + blk.e0, meta + blk.e0, x + blk.col_lo, blk.nent,
+                                                rb, 0.0, pol, polx, mh, ml);
+            if (run.grid) {  // block-wide largest |product| (with the Inf/NaN witness)
+                mh = __reduce_max_sync(0xffffffffu, mh);
+                ml = __reduce_or_sync(0xffffffffu, ml);
+                if (lane == 0) s_red[0][warp] = mh, s_red[1][warp] = ml;
             }
             __syncthreads();
             if (run.grid) {
-                mx = 0.0;
-                nf = 0.0;
+                mh = 0u;
+                ml = 0u;
 #pragma unroll 8
-                for (int w = 0; w < kThreads / 32; ++w) mx = fmax(mx, s_red[0][w]), nf += s_red[1][w];
+                for (int w = 0; w < NT / 32; ++w) mh = max(mh, s_red[0][w]), ml |= s_red[1][w];
             }
             // The grid the data calls for.  A fixed-point pass on another grid is
             // redone (too fine a grid may have wrapped, a coarser one rounds
             // differently), and so is an FP64 pass the data would allow on a
             // grid, so the result depends on the data alone.
-            const int want = run.grid ? grid_of(mx, nf, fixed ? et : 0) : kColsortFp64;
+            const int want = run.grid ? grid_of(mh, ml, fixed ? et : 0) : kColsortFp64;
             const bool again = pass < 2 && (fixed ? want != et : want != kColsortFp64);
             if (threadIdx.x == 0 && run.grid) run.grid[b] = want;
             if (!again) {
@@ -224,9 +303,9 @@ __global__ void __launch_bounds__(kThreads, 2)
                     // summed again by the FP64 row kernel, so every row is within 2^-46 relative
                     const long long lim = 1ll << (45 + (int)blk.hl);
                     const double inv = scalbn(1.0, -S);
-                    for (unsigned i = threadIdx.x; i < blk.rows; i += kThreads) {
+                    for (unsigned i = threadIdx.x; i < blk.rows; i += NT) {
                         const long long V = (long long)(((unsigned long long)hi[i] << 32) | lo[i]);
-                        const bool flag = mx > 0.0 && V > -lim && V < lim;
+                        const bool flag = (mh | ml) != 0u && V > -lim && V < lim;
                         if (!flag) y[blk.row0 + i] = __ll2double_rn(V) * inv;
                         const unsigned am = __activemask();
                         const unsigned bal = __ballot_sync(am, flag);
@@ -239,13 +318,26 @@ __global__ void __launch_bounds__(kThreads, 2)
                         }
                     }
                 } else {
-                    for (unsigned i = threadIdx.x; i < blk.rows; i += kThreads) y[blk.row0 + i] = ys[i];
+                    for (unsigned i = threadIdx.x; i < blk.rows; i += NT) y[blk.row0 + i] = ys[i];
                 }
                 __syncthreads();
                 break;
             }
             et = want;
             __syncthreads();
+        }
+    }
+}
+
+// The last CTA of a flagged-row kernel resets the list for the next call.
+__device__ __forceinline__ void flagged_rows_done(const ColsortRun& run) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(run.done, 1u) == gridDim.x - 1) {
+            *run.count = 0;
+            *run.done = 0;
+            __threadfence();
         }
     }
 }
@@ -275,15 +367,45 @@ __global__ void __launch_bounds__(256) spmv_flagged_rows(ColsortRun run, const d
         sum += __shfl_xor_sync(0xffffffffu, sum, 2);
         if (c == 0 && r >= 0) y[r] = sum;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        if (atomicAdd(run.done, 1u) == gridDim.x - 1) {
-            *run.count = 0;
-            *run.done = 0;
-            __threadfence();
+    flagged_rows_done(run);
+}
+
+// Tensor-core form of the flagged-row kernel: a warp takes 8 listed rows as
+// the rows of an m8n8k4 A fragment, lane 4r+k holding A[r][k] = val and
+// B[k][r] = x of row r's entry 4s+k at step s; D[r][r] accumulates row r in
+// the MMA (a fixed order: bit-reproducible).  Off-diagonal outputs mix rows
+// and are dropped; the diagonal only ever meets its own row's operands, so
+// Inf/NaN propagate as in FP64.
+__global__ void __launch_bounds__(256) spmv_flagged_rows_tc(ColsortRun run, const double* __restrict__ x,
+                                                            double* __restrict__ y) {
+    const int lane = threadIdx.x & 31, r = lane >> 2, k = lane & 3;
+    const unsigned warps = gridDim.x * 8, w0 = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const unsigned n = __ldcg(run.count);
+    for (unsigned g = w0 * 8; g < n; g += warps * 8) {  // warp-uniform
+        const unsigned i = g + r;
+        int a = 0, e = 0, row = -1;
+        if (i < n) {
+            row = __ldcg(run.list + i);
+            a = __ldg(run.rp + row);
+            e = __ldg(run.rp + row + 1);
         }
+        int steps = (e - a + 3) >> 2;
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) steps = max(steps, __shfl_xor_sync(0xffffffffu, steps, o));
+        double d0 = 0.0, d1 = 0.0;
+        for (int s = 0; s < steps; ++s) {
+            const int j = a + 4 * s + k;
+            double av = 0.0, bv = 0.0;
+            if (j < e) {
+                av = __ldg(run.val + j);
+                bv = __ldg(x + (__ldg(run.col + j) - run.col_base));
+            }
+            dmma_m8n8k4(d0, d1, av, bv, d0, d1);
+        }
+        // D[r][r] sits on lane 4r + (r >> 1), element r & 1
+        if (row >= 0 && k == (r >> 1)) y[row] = (r & 1) ? d1 : d0;
     }
+    flagged_rows_done(run);
 }
 
 // Order the entries of one window so that each aligned group of g takes one
@@ -324,7 +446,8 @@ void bank_order(std::vector<std::pair<uint64_t, double>>& t, size_t w0, size_t w
 }  // namespace
 
 bool spmv_colsort_build(uint64_t m, uint64_t n, const int32_t* rp, const int32_t* col, const double* val,
-                        SpmvColsortLayout& L, const std::vector<ColsortSegment>& segments_in, int classes) {
+                        SpmvColsortLayout& L, const std::vector<ColsortSegment>& segments_in, int classes,
+                        bool tc_lanes) {
     (void)n;
     if (m == 0 || rp[m] == 0) return false;
     int64_t maxlen = 0;
@@ -412,11 +535,25 @@ bool spmv_colsort_build(uint64_t m, uint64_t n, const int32_t* rp, const int32_t
                 const int g = std::min(32, std::max(1, classes));
                 for (size_t w0 = 0; g > 1 && w0 < t.size(); w0 += win)
                     bank_order(t, w0, std::min(t.size(), w0 + win), rmask, g, scratch);
-                for (size_t i = 0; i < t.size(); ++i) {
-                    L.meta[k.e0 + i] = (uint32_t)t[i].first;
-                    L.val[k.e0 + i] = t[i].second;
+                while (t.size() < k.nent) t.push_back({k.rows, 0.0});  // padding: column col_lo, scratch row
+                if (!tc_lanes) {
+                    for (size_t i = 0; i < t.size(); ++i) {
+                        L.meta[k.e0 + i] = (uint32_t)t[i].first;
+                        L.val[k.e0 + i] = t[i].second;
+                    }
+                } else {
+                    // each 32-entry group in the tensor-core roles: value in its A
+                    // slot, column bits in its B slot, row bits in its output lane
+                    for (size_t g = 0; g < t.size(); g += 32)
+                        for (int la = 0; la < 32; ++la) {
+                            int lb, ld;
+                            tc_roles(la, lb, ld);
+                            const uint64_t key = t[g + la].first;
+                            L.val[k.e0 + g + la] = t[g + la].second;
+                            L.meta[k.e0 + g + lb] |= (uint32_t)(key & ~(uint64_t)rmask);
+                            L.meta[k.e0 + g + ld] |= (uint32_t)(key & rmask);
+                        }
                 }
-                for (size_t i = t.size(); i < k.nent; ++i) L.meta[k.e0 + i] = k.rows;  // scratch slot
             }
         };
         const unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
@@ -434,25 +571,44 @@ int colsort_initial_grid(const SpmvKBlock& k) {
     return (ea >= 0 ? (ea + kColsortQuantum - 1) / kColsortQuantum : -((-ea) / kColsortQuantum)) * kColsortQuantum;
 }
 
+template <bool TC, int NT, int UF, bool PIPE = false>
+cudaError_t launch_main(const SpmvKBlock* blks, int b0, int b1, int rb, size_t smem, const double* val,
+                        const unsigned* meta, const double* x, double* y, const ColsortRun& run, cudaStream_t s) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(spmv_colsort<TC, NT, UF, PIPE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    spmv_colsort<TC, NT, UF, PIPE><<<std::min(b1 - b0, 2 * kNumSMs), NT, smem, s>>>(blks, b0, b1, rb, val, meta, x, y, run);
+    return cudaSuccess;
+}
+
+template <bool TC>
+cudaError_t launch_shape(int shape, const SpmvKBlock* blks, int b0, int b1, int rb, size_t smem, const double* val,
+                         const unsigned* meta, const double* x, double* y, const ColsortRun& run, cudaStream_t s) {
+    switch (shape) {
+        case 1: return launch_main<TC, 768, 3>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
+        case 4: return launch_main<TC, 1024, 2>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
+        case 5: return launch_main<TC, 1024, 1, true>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
+        case 6: return launch_main<TC, 768, 2, true>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
+        case 7: return launch_main<TC, 640, 3, true>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
+        case 8: return launch_main<TC, 512, 4, true>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
+        case 9: return launch_main<TC, 1024, 2, true>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
+        default: return launch_main<TC, kThreads, kUnroll>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
+    }
+}
+
 cudaError_t launch_spmv_colsort(int unit, const SpmvKBlock* blks, int b0, int b1, int rb, int rows,
                                 const double* val, const unsigned* meta, const double* x, double* y,
                                 const ColsortRun& run, cudaStream_t s) {
     if (b1 <= b0) return cudaSuccess;
     const size_t smem = (size_t)(rows + 1) * 8;
-    const int grid = std::min(b1 - b0, 2 * kNumSMs);
-    cudaError_t e;
-    if (unit) {
-        e = cudaFuncSetAttribute(spmv_colsort<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        spmv_colsort<true><<<grid, kThreads, smem, s>>>(blks, b0, b1, rb, val, meta, x, y, run);
-    } else {
-        e = cudaFuncSetAttribute(spmv_colsort<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        spmv_colsort<false><<<grid, kThreads, smem, s>>>(blks, b0, b1, rb, val, meta, x, y, run);
-    }
+    cudaError_t e =
+        unit ? launch_shape<true>(tuning().spmv_colsort_tc_shape, blks, b0, b1, rb, smem, val, meta, x, y, run, s)
+             : launch_shape<false>(tuning().spmv_colsort_cc_shape, blks, b0, b1, rb, smem, val, meta, x, y, run, s);
+    if (e != cudaSuccess) return e;
     note_launch();
     if ((e = cudaGetLastError()) != cudaSuccess || !run.grid) return e;
-    spmv_flagged_rows<<<2 * kNumSMs, 256, 0, s>>>(run, x, y);
+    if (unit) spmv_flagged_rows_tc<<<2 * kNumSMs, 256, 0, s>>>(run, x, y);
+    else spmv_flagged_rows<<<2 * kNumSMs, 256, 0, s>>>(run, x, y);
     note_launch();
     return cudaGetLastError();
 }

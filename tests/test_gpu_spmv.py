@@ -605,3 +605,54 @@ def test_colsort_small_rows_spikes_and_determinism(cuda, unit, fixed):
         assert (dy == 0).all()
     finally:
         plan.close()
+
+
+@pytest.mark.parametrize("unit", UNITS)
+def test_colsort_cta_shapes_bit_identical(cuda, unit):
+    """K17 on the 64-bit grid: every CTA shape (plain and software-pipelined
+    loops, 512-1024 threads) adds the same integer products, so the results
+    are bit-identical across shapes; the tensor core's two quadrant DMMA give
+    each product RN(val * x), so its grid rows equal the CUDA core's (rows the
+    FP64 row kernels re-sum are compared at 1e-15)."""
+    import torch
+
+    m = n = 150000
+    rp, col, val = O.gen_band_csr(m, 0, n, 16, 20000, 9)
+    x = O.fill_uniform(n, 9, 4, 0, 1)
+    want = O.spmv_csr(rp, col, val, x)
+    key = "spmv_colsort_tc_shape" if unit == P.TENSOR_CORE else "spmv_colsort_cc_shape"
+    prev = [P.tuning_set("spmv_colsort_fixed", 2), P.tuning_set("spmv_plan_colsort", 1)]
+    plans = {}
+    try:
+        for u in UNITS:
+            plans[u] = P.SpmvPlan(rp, col, val, n, unit=u)
+        dx = torch.from_numpy(x).cuda()
+        outs = {}
+        for sh in (0, 1, 4, 5, 6, 7, 8, 9):
+            old = P.tuning_set(key, sh)
+            try:
+                dy = torch.full((m,), float("nan"), dtype=torch.float64, device="cuda")
+                plans[unit].execute(dx, dy)
+                torch.cuda.synchronize()
+                outs[sh] = dy.cpu().numpy()
+            finally:
+                P.tuning_set(key, old)
+        ref = outs[0]
+        assert O.rel_err(ref, want) <= TOL
+        for sh, y in outs.items():
+            assert np.array_equal(y, ref), sh
+        other = [u for u in UNITS if u != unit][0]
+        dy = torch.full((m,), float("nan"), dtype=torch.float64, device="cuda")
+        plans[other].execute(dx, dy)
+        torch.cuda.synchronize()
+        yo = dy.cpu().numpy()
+        same = yo == ref
+        assert same.mean() > 0.99
+        absum = np.array(
+            [np.abs(val[rp[i]:rp[i + 1]] * x[col[rp[i]:rp[i + 1]]]).sum() for i in np.flatnonzero(~same)])
+        assert np.all(np.abs(yo - ref)[~same] <= 2 * 16 * 2.0 ** -53 * absum)
+    finally:
+        for p in plans.values():
+            p.close()
+        P.tuning_set("spmv_colsort_fixed", prev[0])
+        P.tuning_set("spmv_plan_colsort", prev[1])
