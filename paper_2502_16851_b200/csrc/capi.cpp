@@ -434,7 +434,7 @@ struct rl_spmv_plan_s {
     double *val = nullptr, *x = nullptr, *y = nullptr;
     // column-sorted row blocks (K17, spmv_colsort.cu)
     bool colsort = false;
-    int krb = 0, krows = 0;
+    int krb = 0, krows = 0, kvec = 1;
     rlb::SpmvKBlock* kblk = nullptr;
     double* kval = nullptr;
     unsigned* kmeta = nullptr;
@@ -519,9 +519,10 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
         rlb::SpmvColsortLayout L;
         if (rlb::tuning().spmv_plan_colsort && nnz > 0 &&
             rlb::spmv_colsort_build(m, n, rp, col, val, L, {}, rlb::colsort_classes(unit == ExecutionUnit::TensorCore),
-                                    unit == ExecutionUnit::TensorCore)) {
+                                    unit == ExecutionUnit::TensorCore, rlb::tuning().spmv_colsort_vec)) {
             pl->colsort = true;
             pl->krb = L.rb;
+            pl->kvec = L.vec;
             pl->krows = L.rows;
             auto up = [&](auto*& dst, const auto& v) {
                 using T = std::remove_reference_t<decltype(*dst)>;
@@ -653,7 +654,7 @@ void plan_rows(rl_spmv_plan_s* pl, uint64_t r0, uint64_t r1, const double* x, do
         const auto& v = pl->kblk_r0;
         const int b0 = (int)(std::lower_bound(v.begin(), v.end(), (uint32_t)r0) - v.begin());
         const int b1 = r1 >= pl->m ? (int)v.size() : (int)(std::lower_bound(v.begin(), v.end(), (uint32_t)r1) - v.begin());
-        ck(rlb::launch_spmv_colsort(pl->unit == ExecutionUnit::TensorCore, pl->kblk, b0, b1, pl->krb, pl->krows,
+        ck(rlb::launch_spmv_colsort(pl->unit == ExecutionUnit::TensorCore, pl->kvec, pl->kblk, b0, b1, pl->krb, pl->krows,
                                     pl->kval, pl->kmeta, x, y, pl->colsort_run(), s),
            "spmv (column-sorted plan)");
         return;
@@ -1288,6 +1289,7 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         {"spmv_colsort_classes", &rlb::Tuning::spmv_colsort_classes, false},
         {"spmv_colsort_tc_shape", &rlb::Tuning::spmv_colsort_tc_shape, false},
         {"spmv_colsort_cc_shape", &rlb::Tuning::spmv_colsort_cc_shape, false},
+        {"spmv_colsort_vec", &rlb::Tuning::spmv_colsort_vec, false},
         {"spmv_plan_ygroups", &rlb::Tuning::spmv_plan_ygroups, false},
         {"stencil_r_ctas_per_sm", &rlb::Tuning::stencil_r_ctas_per_sm, false},
         {"stencil_tb_waves", &rlb::Tuning::stencil_tb_waves, false},

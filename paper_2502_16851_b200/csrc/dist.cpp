@@ -407,7 +407,7 @@ struct rl_dist_spmv_s {
         // column-sorted row blocks (K17, spmv_colsort.cu) built from this part's
         // CSR at creation; blocks [kb0, kb1) are interior (rows inside [i0, i1))
         bool colsort = false;
-        int krb = 0, krows = 0, kb0 = 0, kb1 = 0, knb = 0;
+        int krb = 0, krows = 0, kb0 = 0, kb1 = 0, knb = 0, kvec = 1;
         rlb::SpmvKBlock* kblk = nullptr;
         double* kval = nullptr;
         unsigned* kmeta = nullptr;
@@ -452,7 +452,7 @@ void colsort_part(rl_dist_spmv_s::Part& q, uint64_t rows, uint64_t nnz, bool tc)
                                              {rows, std::max<uint64_t>(1, 2 * (uint64_t)rlb::kNumSMsHost - eb)}};
     rlb::SpmvColsortLayout L;
     if (!rlb::spmv_colsort_build(rows, q.g.ce - q.g.cb, hrp.data(), hcol.data(), hval.data(), L, segs,
-                                 rlb::colsort_classes(tc), tc))
+                                 rlb::colsort_classes(tc), tc, rlb::tuning().spmv_colsort_vec))
         return;
     // block order: edge blocks first, then the interior, so each phase is one launch
     std::stable_partition(L.blocks.begin(), L.blocks.end(), [&](const rlb::SpmvKBlock& k) {
@@ -468,6 +468,7 @@ void colsort_part(rl_dist_spmv_s::Part& q, uint64_t rows, uint64_t nnz, bool tc)
     up(q.kmeta, L.meta);
     q.colsort = true;
     q.krb = L.rb;
+    q.kvec = L.vec;
     q.krows = L.rows;
     if (rlb::colsort_fixed_for(tc)) {
         std::vector<int> g;
@@ -489,7 +490,7 @@ void colsort_part(rl_dist_spmv_s::Part& q, uint64_t rows, uint64_t nnz, bool tc)
 void part_rows(const rl_dist_spmv_s* pl, const rl_dist_spmv_s::Part& q, int b0, int b1, uint64_t r0, uint64_t r1,
                cudaStream_t s) {
     if (q.colsort) {
-        ck(rlb::launch_spmv_colsort(pl->unit == ExecutionUnit::TensorCore, q.kblk, b0, b1, q.krb, q.krows, q.kval,
+        ck(rlb::launch_spmv_colsort(pl->unit == ExecutionUnit::TensorCore, q.kvec, q.kblk, b0, b1, q.krb, q.krows, q.kval,
                                     q.kmeta, q.x, q.y, q.colsort_run(), s),
            "spmv (column-sorted part)");
         return;

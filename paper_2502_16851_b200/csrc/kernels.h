@@ -35,10 +35,13 @@ struct Tuning {
     int spmv_colsort_classes = 0;  // K17 bank-ordering group 1..32 (0: 1 = none on the fixed-point grid, 16 for FP64 rows)
     int spmv_colsort_fixed = 2;    // K17 rows on a 64-bit fixed-point grid (+ FP64 row kernel for flagged rows):
                                    // 1 CUDA-core unit only, 2 both units, 0 neither (FP64 shared atomics)
-    int spmv_colsort_tc_shape = 7; // K17 tensor-core CTA shape (threads x entries per step): 0 1024x3, 1 768x3, 4 1024x2;
-                                   // software-pipelined 5 1024x1, 6 768x2, 7 640x3, 8 512x4, 9 1024x2
-                                   // (tools/micro/spmv_shapes.py, median of 15 interleaved bursts: TC 7 0.184 vs 0 0.207 ms)
-    int spmv_colsort_cc_shape = 6; // ... CUDA-core kernel, same codes (CC 6 0.171, 8 0.170, 0 0.175 ms)
+    int spmv_colsort_vec = 2;      // K17 plan build: entries per thread unit (2: paired 128-bit val / 64-bit meta loads; 1: one entry)
+    int spmv_colsort_tc_shape = 13; // K17 CTA shape (threads x units per step, p = software-pipelined loop):
+                                    // 0 1024x3, 1 768x3, 4 1024x2, 10 1024x1; p: 5 1024x1, 6 768x2, 7 640x3, 8 512x4,
+                                    // 11 512x2, 12 640x2, 13 768x1, 14 512x3, 15 384x4, 16 512x1
+                                    // (tools/micro/spmv_shapes.py, 60 interleaved bursts of 25 calls, medians:
+                                    // TC vec 2 shape 13 0.186 ms, vec 2 11 0.194, vec 1 0 0.222, vec 1 7 0.225)
+    int spmv_colsort_cc_shape = 11; // ... CUDA-core kernel (vec 2 11 0.168, vec 2 13 0.169, vec 1 0 0.169 ms)
     int spmv_plan_colsort = 1;     // plans (both units) use the column-sorted row-block layout (K17, spmv_colsort.cu) when eligible; 0: CSR
     int spmv_plan_xpieces = 0;     // max x upload pieces (first = chunk 0's prefix); 0: one per chunk
     int spmv_plan_ygroups = 0;     // y download copies (groups of consecutive chunks); 0: one per chunk
@@ -232,6 +235,7 @@ int colsort_initial_grid(const SpmvKBlock& k);
 struct SpmvColsortLayout {
     int rb = 0;    // row bits of meta
     int rows = 0;  // rows of the largest block (shared-memory y per CTA)
+    int vec = 1;   // entries per thread unit (2: paired 128-bit val / 64-bit meta loads)
     std::vector<SpmvKBlock> blocks;
     std::vector<double> val;
     std::vector<uint32_t> meta;  // (col - col_lo) << rb | (row - row0)
@@ -244,14 +248,14 @@ struct ColsortSegment {
 };
 bool spmv_colsort_build(uint64_t m, uint64_t n, const int32_t* rp, const int32_t* col, const double* val,
                         SpmvColsortLayout& layout, const std::vector<ColsortSegment>& segments = {},
-                        int classes = 16, bool tc_lanes = false);
+                        int classes = 16, bool tc_lanes = false, int vec = 1);
 // bank-ordering classes of a K17 layout for this unit (1: plain column order on the
 // fixed-point grid, 16: FP64 rows)
 inline int colsort_classes(bool tc) {
     const int c = tuning().spmv_colsort_classes;
     return c ? c : (colsort_fixed_for(tc) ? 1 : 16);
 }
-cudaError_t launch_spmv_colsort(int unit, const SpmvKBlock* blks, int b0, int b1, int rb, int rows,
+cudaError_t launch_spmv_colsort(int unit, int vec, const SpmvKBlock* blks, int b0, int b1, int rb, int rows,
                                 const double* val, const unsigned* meta, const double* x, double* y,
                                 const ColsortRun& run, cudaStream_t s);
 

@@ -94,6 +94,12 @@ __host__ __device__ __forceinline__ void tc_roles(int la, int& lb, int& ld) {
 }
 constexpr int kUnroll = 3;  // entry loads in flight per thread (measured: U2 0.183, U3 0.173, U4 0.193 ms)
 
+__device__ __forceinline__ void ld_stream2(const double* p, uint64_t pol, double& a, double& b) {
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(a), "=d"(b) : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ void ld_meta2(const unsigned* p, uint64_t pol, unsigned& a, unsigned& b) {
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;" : "=r"(a), "=r"(b) : "l"(p), "l"(pol));
+}
 __device__ __forceinline__ unsigned ld_meta(const unsigned* p, uint64_t pol) {
     unsigned v;
     asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
@@ -127,7 +133,7 @@ __device__ __forceinline__ void add64(unsigned* __restrict__ lo, unsigned* __res
 }
 
 // TRACK: keep the largest |product| and an Inf/NaN witness (the grid check)
-template <bool TC, bool FIXED, bool TRACK, int NT, int UF, bool PIPE>
+template <bool TC, bool FIXED, bool TRACK, int NT, int UF, bool PIPE, int V>
 __device__ __forceinline__ void block_entries(double* __restrict__ ys, unsigned* __restrict__ lo,
                                               unsigned* __restrict__ hi, const double* __restrict__ vb,
                                               const unsigned* __restrict__ mb, const double* __restrict__ xb,
@@ -184,66 +190,82 @@ __device__ __forceinline__ void block_entries(double* __restrict__ ys, unsigned*
             add(ra, p);
         }
     };
-    // nent is a multiple of 32: every warp step is full
-    unsigned e = threadIdx.x;
-    constexpr int U = (TC && !FIXED) ? 2 : UF;  // the FP64 tensor-core step needs more registers
+    // A thread takes units of V consecutive entries (V = 2: one 128-bit val and
+    // one 64-bit meta load per unit); nent is a multiple of 32 V, so every warp
+    // step is full.  Unit i covers entries [V i, V i + V).
+    auto load = [&](unsigned i, double (&v)[V], unsigned (&m)[V]) {
+        if (V == 1) {
+            v[0] = ld_stream(vb + i, pol);
+            m[0] = ld_meta(mb + i, pol);
+        } else {
+            ld_stream2(vb + 2 * i, pol, v[0], v[V - 1]);
+            ld_meta2(mb + 2 * i, pol, m[0], m[V - 1]);
+        }
+    };
+    unsigned i = threadIdx.x;
+    constexpr int U = (TC && !FIXED) ? (V == 1 ? 2 : 1) : UF;  // the FP64 tensor-core step needs more registers
     if (PIPE && FIXED) {
-        // software-pipelined: the next U entries' val/meta loads are in flight
+        // software-pipelined: the next U units' val/meta loads are in flight
         // while this step gathers x and adds, so the stream never waits on the
         // x gather and the add chain
-        double v[U];
-        unsigned mt[U];
-        if (e + (U - 1) * NT < nent) {
+        double v[U][V];
+        unsigned mt[U][V];
+        if (V * (i + (U - 1) * NT) < nent) {
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                v[u] = ld_stream(vb + e + u * NT, pol);
-                mt[u] = ld_meta(mb + e + u * NT, pol);
-            }
+            for (int u = 0; u < U; ++u) load(i + u * NT, v[u], mt[u]);
             for (;;) {
-                const bool more = e + (2 * U - 1) * NT < nent;
-                double vn[U], xv[U];
-                unsigned mn[U];
+                const bool more = V * (i + (2 * U - 1) * NT) < nent;
+                double vn[U][V], xv[U][V];
+                unsigned mn[U][V];
                 if (more) {
 #pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        vn[u] = ld_stream(vb + e + (U + u) * NT, pol);
-                        mn[u] = ld_meta(mb + e + (U + u) * NT, pol);
-                    }
+                    for (int u = 0; u < U; ++u) load(i + (U + u) * NT, vn[u], mn[u]);
                 }
 #pragma unroll
-                for (int u = 0; u < U; ++u) xv[u] = ld_policy(xb + (mt[u] >> rb), polx);
+                for (int u = 0; u < U; ++u)
 #pragma unroll
-                for (int u = 0; u < U; ++u) step(v[u], mt[u], xv[u]);
-                e += U * NT;
+                    for (int k = 0; k < V; ++k) xv[u][k] = ld_policy(xb + (mt[u][k] >> rb), polx);
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+#pragma unroll
+                    for (int k = 0; k < V; ++k) step(v[u][k], mt[u][k], xv[u][k]);
+                i += U * NT;
                 if (!more) break;
 #pragma unroll
-                for (int u = 0; u < U; ++u) v[u] = vn[u], mt[u] = mn[u];
+                for (int u = 0; u < U; ++u)
+#pragma unroll
+                    for (int k = 0; k < V; ++k) v[u][k] = vn[u][k], mt[u][k] = mn[u][k];
             }
         }
     } else {
-        for (; e + (U - 1) * NT < nent; e += U * NT) {
-            double v[U], xv[U];
-            unsigned mt[U];
+        for (; V * (i + (U - 1) * NT) < nent; i += U * NT) {
+            double v[U][V], xv[U][V];
+            unsigned mt[U][V];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                v[u] = ld_stream(vb + e + u * NT, pol);
-                mt[u] = ld_meta(mb + e + u * NT, pol);
-            }
+            for (int u = 0; u < U; ++u) load(i + u * NT, v[u], mt[u]);
 #pragma unroll
-            for (int u = 0; u < U; ++u) xv[u] = ld_policy(xb + (mt[u] >> rb), polx);
+            for (int u = 0; u < U; ++u)
 #pragma unroll
-            for (int u = 0; u < U; ++u) step(v[u], mt[u], xv[u]);
+                for (int k = 0; k < V; ++k) xv[u][k] = ld_policy(xb + (mt[u][k] >> rb), polx);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int k = 0; k < V; ++k) step(v[u][k], mt[u][k], xv[u][k]);
         }
     }
-    // tail: whole warps only (nent is a multiple of 32), so the TC shuffles stay full
-    for (; e - lane < nent; e += NT) {
-        const double v = ld_stream(vb + e, pol);
-        const unsigned mt = ld_meta(mb + e, pol);
-        step(v, mt, ld_policy(xb + (mt >> rb), polx));
+    // tail: whole warps only (nent is a multiple of 32 V), so the TC steps stay full
+    for (; V * (i - lane) < nent; i += NT) {
+        double v[V], xv[V];
+        unsigned mt[V];
+        load(i, v, mt);
+#pragma unroll
+        for (int k = 0; k < V; ++k) xv[k] = ld_policy(xb + (mt[k] >> rb), polx);
+#pragma unroll
+        for (int k = 0; k < V; ++k) step(v[k], mt[k], xv[k]);
     }
 }
 
-template <bool TC, int NT, int UF, bool PIPE>
+template <bool TC, int NT, int UF, bool PIPE, int V>
 __global__ void __launch_bounds__(NT, 2)
     spmv_colsort(const SpmvKBlock* __restrict__ blks, int b0, int b1, int rb, const double* __restrict__ val,
                  const unsigned* __restrict__ meta, const double* __restrict__ x, double* __restrict__ y,
@@ -269,13 +291,13 @@ __global__ void __launch_bounds__(NT, 2)
             __syncthreads();
             unsigned mh = 0u, ml = 0u;
             if (fixed)
-                block_entries<TC, true, true, NT, UF, PIPE>(ys, lo, hi, val + blk.e0, meta + blk.e0, x + blk.col_lo, blk.nent, rb,
+                block_entries<TC, true, true, NT, UF, PIPE, V>(ys, lo, hi, val + blk.e0, meta + blk.e0, x + blk.col_lo, blk.nent, rb,
                                               scalbn(1.0, S), pol, polx, mh, ml);
             else if (run.grid)
-                block_entries<TC, false, true, NT, UF, PIPE>(ys, lo, hi, val + blk.e0, meta + blk.e0, x + blk.col_lo, blk.nent, rb,
+                block_entries<TC, false, true, NT, UF, PIPE, V>(ys, lo, hi, val + blk.e0, meta + blk.e0, x + blk.col_lo, blk.nent, rb,
                                                0.0, pol, polx, mh, ml);
             else
-                block_entries<TC, false, false, NT, UF, PIPE>(ys, lo, hi, val + blk.e0, meta + blk.e0, x + blk.col_lo, blk.nent,
+                block_entries<TC, false, false, NT, UF, PIPE, V>(ys, lo, hi, val + blk.e0, meta + blk.e0, x + blk.col_lo, blk.nent,
                                                 rb, 0.0, pol, polx, mh, ml);
             if (run.grid) {  // block-wide largest |product| (with the Inf/NaN witness)
                 mh = __reduce_max_sync(0xffffffffu, mh);
@@ -447,7 +469,8 @@ void bank_order(std::vector<std::pair<uint64_t, double>>& t, size_t w0, size_t w
 
 bool spmv_colsort_build(uint64_t m, uint64_t n, const int32_t* rp, const int32_t* col, const double* val,
                         SpmvColsortLayout& L, const std::vector<ColsortSegment>& segments_in, int classes,
-                        bool tc_lanes) {
+                        bool tc_lanes, int vec) {
+    vec = vec == 2 ? 2 : 1;
     (void)n;
     if (m == 0 || rp[m] == 0) return false;
     int64_t maxlen = 0;
@@ -487,6 +510,7 @@ bool spmv_colsort_build(uint64_t m, uint64_t n, const int32_t* rp, const int32_t
         if (!fits) continue;
         L.rb = rb;
         L.rows = (int)Rmax;
+        L.vec = vec;
         L.blocks.assign(nb, SpmvKBlock{});
         uint64_t e = 0;
         for (uint64_t b = 0; b < nb; ++b) {
@@ -496,7 +520,8 @@ bool spmv_colsort_build(uint64_t m, uint64_t n, const int32_t* rp, const int32_t
             k.e0 = e;
             k.row0 = (uint32_t)r0;
             k.rows = (uint32_t)(r1 - r0);
-            k.nent = (uint32_t)((cnt + 31) / 32 * 32);
+            const uint64_t gsz = 32 * (uint64_t)vec;  // a warp step's entries
+            k.nent = (uint32_t)((cnt + gsz - 1) / gsz * gsz);
             int32_t lo = INT32_MAX;
             int ev = 0;
             bool nonfinite = false;
@@ -544,15 +569,18 @@ bool spmv_colsort_build(uint64_t m, uint64_t n, const int32_t* rp, const int32_t
                 } else {
                     // each 32-entry group in the tensor-core roles: value in its A
                     // slot, column bits in its B slot, row bits in its output lane
-                    for (size_t g = 0; g < t.size(); g += 32)
-                        for (int la = 0; la < 32; ++la) {
-                            int lb, ld;
-                            tc_roles(la, lb, ld);
-                            const uint64_t key = t[g + la].first;
-                            L.val[k.e0 + g + la] = t[g + la].second;
-                            L.meta[k.e0 + g + lb] |= (uint32_t)(key & ~(uint64_t)rmask);
-                            L.meta[k.e0 + g + ld] |= (uint32_t)(key & rmask);
-                        }
+                    // (vec = 2: a lane's two entries sit side by side, so the warp
+                    // step's even and odd entries are two such groups)
+                    for (size_t g = 0; g < t.size(); g += 32 * vec)
+                        for (int par = 0; par < vec; ++par)
+                            for (int la = 0; la < 32; ++la) {
+                                int lb, ld;
+                                tc_roles(la, lb, ld);
+                                const uint64_t key = t[g + vec * la + par].first;
+                                L.val[k.e0 + g + vec * la + par] = t[g + vec * la + par].second;
+                                L.meta[k.e0 + g + vec * lb + par] |= (uint32_t)(key & ~(uint64_t)rmask);
+                                L.meta[k.e0 + g + vec * ld + par] |= (uint32_t)(key & rmask);
+                            }
                 }
             }
         };
@@ -571,39 +599,52 @@ int colsort_initial_grid(const SpmvKBlock& k) {
     return (ea >= 0 ? (ea + kColsortQuantum - 1) / kColsortQuantum : -((-ea) / kColsortQuantum)) * kColsortQuantum;
 }
 
-template <bool TC, int NT, int UF, bool PIPE = false>
+template <bool TC, int NT, int UF, bool PIPE, int V>
 cudaError_t launch_main(const SpmvKBlock* blks, int b0, int b1, int rb, size_t smem, const double* val,
                         const unsigned* meta, const double* x, double* y, const ColsortRun& run, cudaStream_t s) {
     const cudaError_t e =
-        cudaFuncSetAttribute(spmv_colsort<TC, NT, UF, PIPE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(spmv_colsort<TC, NT, UF, PIPE, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    spmv_colsort<TC, NT, UF, PIPE><<<std::min(b1 - b0, 2 * kNumSMs), NT, smem, s>>>(blks, b0, b1, rb, val, meta, x, y, run);
+    spmv_colsort<TC, NT, UF, PIPE, V>
+        <<<std::min(b1 - b0, 2 * kNumSMs), NT, smem, s>>>(blks, b0, b1, rb, val, meta, x, y, run);
     return cudaSuccess;
 }
 
-template <bool TC>
+// CTA shape codes (tuning spmv_colsort_{cc,tc}_shape): threads x units per
+// step, plain or software-pipelined loop; V = 2 layouts (entries paired per
+// thread) take the V = 2 instantiations of the same shapes.
+template <bool TC, int V>
 cudaError_t launch_shape(int shape, const SpmvKBlock* blks, int b0, int b1, int rb, size_t smem, const double* val,
                          const unsigned* meta, const double* x, double* y, const ColsortRun& run, cudaStream_t s) {
     switch (shape) {
-        case 1: return launch_main<TC, 768, 3>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
-        case 4: return launch_main<TC, 1024, 2>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
-        case 5: return launch_main<TC, 1024, 1, true>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
-        case 6: return launch_main<TC, 768, 2, true>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
-        case 7: return launch_main<TC, 640, 3, true>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
-        case 8: return launch_main<TC, 512, 4, true>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
-        case 9: return launch_main<TC, 1024, 2, true>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
-        default: return launch_main<TC, kThreads, kUnroll>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
+        case 1: return launch_main<TC, 768, 3, false, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
+        case 4: return launch_main<TC, 1024, 2, false, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
+        case 5: return launch_main<TC, 1024, 1, true, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
+        case 6: return launch_main<TC, 768, 2, true, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
+        case 7: return launch_main<TC, 640, 3, true, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
+        case 8: return launch_main<TC, 512, 4, true, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
+        case 10: return launch_main<TC, 1024, 1, false, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
+        case 11: return launch_main<TC, 512, 2, true, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
+        case 12: return launch_main<TC, 640, 2, true, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
+        case 13: return launch_main<TC, 768, 1, true, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
+        case 14: return launch_main<TC, 512, 3, true, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
+        case 15: return launch_main<TC, 384, 4, true, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
+        case 16: return launch_main<TC, 512, 1, true, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
+        default: return launch_main<TC, kThreads, kUnroll, false, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
     }
 }
 
-cudaError_t launch_spmv_colsort(int unit, const SpmvKBlock* blks, int b0, int b1, int rb, int rows,
+cudaError_t launch_spmv_colsort(int unit, int vec, const SpmvKBlock* blks, int b0, int b1, int rb, int rows,
                                 const double* val, const unsigned* meta, const double* x, double* y,
                                 const ColsortRun& run, cudaStream_t s) {
     if (b1 <= b0) return cudaSuccess;
     const size_t smem = (size_t)(rows + 1) * 8;
-    cudaError_t e =
-        unit ? launch_shape<true>(tuning().spmv_colsort_tc_shape, blks, b0, b1, rb, smem, val, meta, x, y, run, s)
-             : launch_shape<false>(tuning().spmv_colsort_cc_shape, blks, b0, b1, rb, smem, val, meta, x, y, run, s);
+    const int cs = tuning().spmv_colsort_cc_shape, ts = tuning().spmv_colsort_tc_shape;
+    cudaError_t e = vec == 2
+        ? (unit ? launch_shape<true, 2>(ts, blks, b0, b1, rb, smem, val, meta, x, y, run, s)
+                : launch_shape<false, 2>(cs, blks, b0, b1, rb, smem, val, meta, x, y, run, s))
+        : (unit ? launch_shape<true, 1>(ts, blks, b0, b1, rb, smem, val, meta, x, y, run, s)
+                : launch_shape<false, 1>(cs, blks, b0, b1, rb, smem, val, meta, x, y, run, s));
     if (e != cudaSuccess) return e;
     note_launch();
     if ((e = cudaGetLastError()) != cudaSuccess || !run.grid) return e;

@@ -610,10 +610,11 @@ def test_colsort_small_rows_spikes_and_determinism(cuda, unit, fixed):
 @pytest.mark.parametrize("unit", UNITS)
 def test_colsort_cta_shapes_bit_identical(cuda, unit):
     """K17 on the 64-bit grid: every CTA shape (plain and software-pipelined
-    loops, 512-1024 threads) adds the same integer products, so the results
-    are bit-identical across shapes; the tensor core's two quadrant DMMA give
-    each product RN(val * x), so its grid rows equal the CUDA core's (rows the
-    FP64 row kernels re-sum are compared at 1e-15)."""
+    loops, 384-1024 threads) and both thread-unit widths (one entry, or two
+    paired entries per thread) add the same integer products, so the results
+    are bit-identical; the tensor core's two quadrant DMMA give each product
+    RN(val * x), so its grid rows equal the CUDA core's (rows the FP64 row
+    kernels re-sum differ within the FP64 summation bound)."""
     import torch
 
     m = n = 150000
@@ -621,29 +622,34 @@ def test_colsort_cta_shapes_bit_identical(cuda, unit):
     x = O.fill_uniform(n, 9, 4, 0, 1)
     want = O.spmv_csr(rp, col, val, x)
     key = "spmv_colsort_tc_shape" if unit == P.TENSOR_CORE else "spmv_colsort_cc_shape"
-    prev = [P.tuning_set("spmv_colsort_fixed", 2), P.tuning_set("spmv_plan_colsort", 1)]
+    prev = [P.tuning_set("spmv_colsort_fixed", 2), P.tuning_set("spmv_plan_colsort", 1),
+            P.tuning_set("spmv_colsort_vec", 2)]
     plans = {}
     try:
-        for u in UNITS:
-            plans[u] = P.SpmvPlan(rp, col, val, n, unit=u)
+        for vec in (1, 2):
+            P.tuning_set("spmv_colsort_vec", vec)
+            for u in UNITS:
+                plans[(u, vec)] = P.SpmvPlan(rp, col, val, n, unit=u)
+        P.tuning_set("spmv_colsort_vec", prev[2])
         dx = torch.from_numpy(x).cuda()
         outs = {}
-        for sh in (0, 1, 4, 5, 6, 7, 8, 9):
-            old = P.tuning_set(key, sh)
-            try:
-                dy = torch.full((m,), float("nan"), dtype=torch.float64, device="cuda")
-                plans[unit].execute(dx, dy)
-                torch.cuda.synchronize()
-                outs[sh] = dy.cpu().numpy()
-            finally:
-                P.tuning_set(key, old)
-        ref = outs[0]
+        for vec in (1, 2):
+            for sh in (0, 1, 4, 5, 6, 7, 8, 10, 11, 12, 13, 14, 15, 16):
+                old = P.tuning_set(key, sh)
+                try:
+                    dy = torch.full((m,), float("nan"), dtype=torch.float64, device="cuda")
+                    plans[(unit, vec)].execute(dx, dy)
+                    torch.cuda.synchronize()
+                    outs[(vec, sh)] = dy.cpu().numpy()
+                finally:
+                    P.tuning_set(key, old)
+        ref = outs[(1, 0)]
         assert O.rel_err(ref, want) <= TOL
         for sh, y in outs.items():
             assert np.array_equal(y, ref), sh
         other = [u for u in UNITS if u != unit][0]
         dy = torch.full((m,), float("nan"), dtype=torch.float64, device="cuda")
-        plans[other].execute(dx, dy)
+        plans[(other, 2)].execute(dx, dy)
         torch.cuda.synchronize()
         yo = dy.cpu().numpy()
         same = yo == ref
@@ -656,3 +662,4 @@ def test_colsort_cta_shapes_bit_identical(cuda, unit):
             p.close()
         P.tuning_set("spmv_colsort_fixed", prev[0])
         P.tuning_set("spmv_plan_colsort", prev[1])
+        P.tuning_set("spmv_colsort_vec", prev[2])

@@ -17,8 +17,11 @@ B = 889192452
 hrp, hcol, hval = rp.cpu(), col.cpu(), val.cpu()
 P.spmv_csr(rp, col, val, x, yref, unit=P.CUDA_CORE)
 torch.cuda.synchronize()
-shapes = [int(a) for a in sys.argv[1].split(",")] if len(sys.argv) > 1 else [0, 1, 4, 5, 6, 7, 8, 9]
-units = sys.argv[2].split(",") if len(sys.argv) > 2 else ["tc", "cc"]
+# configs "unit:vec:shape,..." (default: the sweep below)
+cfgs = [tuple(c.split(":")) for c in sys.argv[1].split(",")] if len(sys.argv) > 1 else \
+    [("cc", "1", "0"), ("cc", "1", "6"), ("cc", "2", "10"), ("cc", "2", "5"), ("cc", "2", "11"),
+     ("tc", "1", "7"), ("tc", "2", "11"), ("tc", "2", "5"), ("tc", "2", "6")]
+cfgs = [(u, int(v), int(sh)) for u, v, sh in cfgs]
 
 
 def timeit(fn, reps=200):
@@ -34,21 +37,41 @@ def timeit(fn, reps=200):
     return s.elapsed_time(e) / reps
 
 
-plans = {u: P.SpmvPlan(hrp, hcol, hval, n, unit=P.TENSOR_CORE if u == "tc" else P.CUDA_CORE) for u in units}
+plans = {}
+for u, v in sorted({(u, v) for u, v, _ in cfgs}):
+    P.tuning_set("spmv_colsort_vec", v)
+    plans[(u, v)] = P.SpmvPlan(hrp, hcol, hval, n, unit=P.TENSOR_CORE if u == "tc" else P.CUDA_CORE)
+P.tuning_set("spmv_colsort_vec", 1)
 res = {}
-for rnd in range(int(os.environ.get("ROUNDS", "15"))):  # interleaved short bursts: clocks drift under load
-    for u in units:
-        for sh in shapes:
-            P.tuning_set(f"spmv_colsort_{u}_shape", sh)
-            ms = timeit(lambda: plans[u].execute(x, y), reps=30)
-            res.setdefault((u, sh), []).append(ms)
-for u in units:
-    for sh in shapes:
+# interleaved at call granularity (clocks and power drift under load): every
+# round calls each config once between its own pair of events
+N = int(os.environ.get("ROUNDS", "400"))
+evs = {c: [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(N)] for c in cfgs}
+for c in cfgs:  # warm
+    P.tuning_set(f"spmv_colsort_{c[0]}_shape", c[2])
+    for _ in range(3):
+        plans[(c[0], c[1])].execute(x, y)
+torch.cuda.synchronize()
+BURST = int(os.environ.get("BURST", "1"))  # back-to-back calls between one event pair (bench-like when > 1)
+for r in range(N):
+    for c in cfgs:
+        u, v, sh = c
         P.tuning_set(f"spmv_colsort_{u}_shape", sh)
-        plans[u].execute(x, y); torch.cuda.synchronize(); y1 = y.clone()
-        plans[u].execute(x, y); torch.cuda.synchronize()
-        rel = float((y - yref).norm() / yref.norm())
-        ms = sorted(res[(u, sh)])[len(res[(u, sh)]) // 2]
-        print(f"{u} shape {sh}: median {ms:.4f} ms min {min(res[(u, sh)]):.4f} {B / ms / 1e6:.0f} GB/s "
-              f"rel {rel:.2e} identical {bool(torch.equal(y, y1))}", flush=True)
-    P.tuning_set(f"spmv_colsort_{u}_shape", 0)
+        a, b = evs[c][r]
+        a.record()
+        for _ in range(BURST):
+            plans[(u, v)].execute(x, y)
+        b.record()
+torch.cuda.synchronize()
+for c in cfgs:
+    res[c] = [a.elapsed_time(b) / BURST for a, b in evs[c]]
+for u, v, sh in cfgs:
+    P.tuning_set(f"spmv_colsort_{u}_shape", sh)
+    pl = plans[(u, v)]
+    pl.execute(x, y); torch.cuda.synchronize(); y1 = y.clone()
+    pl.execute(x, y); torch.cuda.synchronize()
+    rel = float((y - yref).norm() / yref.norm())
+    r = sorted(res[(u, v, sh)])
+    ms = r[len(r) // 2]
+    print(f"{u} vec {v} shape {sh}: median {ms:.4f} ms min {r[0]:.4f} {B / ms / 1e6:.0f} GB/s "
+          f"rel {rel:.2e} identical {bool(torch.equal(y, y1))}", flush=True)
