@@ -1290,6 +1290,7 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         {"spmv_colsort_tc_shape", &rlb::Tuning::spmv_colsort_tc_shape, false},
         {"spmv_colsort_cc_shape", &rlb::Tuning::spmv_colsort_cc_shape, false},
         {"spmv_colsort_vec", &rlb::Tuning::spmv_colsort_vec, false},
+        {"spmv_colsort_spread", &rlb::Tuning::spmv_colsort_spread, false},
         {"spmv_plan_ygroups", &rlb::Tuning::spmv_plan_ygroups, false},
         {"stencil_r_ctas_per_sm", &rlb::Tuning::stencil_r_ctas_per_sm, false},
         {"stencil_tb_waves", &rlb::Tuning::stencil_tb_waves, false},

@@ -35,6 +35,7 @@ struct Tuning {
     int spmv_colsort_classes = 0;  // K17 bank-ordering group 1..32 (0: 1 = none on the fixed-point grid, 16 for FP64 rows)
     int spmv_colsort_fixed = 2;    // K17 rows on a 64-bit fixed-point grid (+ FP64 row kernel for flagged rows):
                                    // 1 CUDA-core unit only, 2 both units, 0 neither (FP64 shared atomics)
+    int spmv_colsort_spread = 1;   // K17 plan build (vec > 1): deal each bank class over the entry parities of a warp step
     int spmv_colsort_vec = 2;      // K17 plan build: entries per thread unit (2: paired 128-bit val / 64-bit meta loads; 1: one entry)
     int spmv_colsort_tc_shape = 13; // K17 CTA shape (threads x units per step, p = software-pipelined loop):
                                     // 0 1024x3, 1 768x3, 4 1024x2, 10 1024x1; p: 5 1024x1, 6 768x2, 7 640x3, 8 512x4,

@@ -465,12 +465,44 @@ void bank_order(std::vector<std::pair<uint64_t, double>>& t, size_t w0, size_t w
     }
     std::copy(out.begin(), out.end(), t.begin() + w0);
 }
+// vec > 1: a warp step's 32 vec entries go to vec shared-atomic instructions
+// of 32 (entry parity = the lane's k-th entry).  Which entry takes which
+// (parity, lane) slot changes neither the bytes nor the x lines the step
+// reads, so the host deals each row % 32 bank class over the parities: a
+// parity's 32 atomics then meet fewer repeated banks (random rows: ~3.5
+// wavefronts per instruction before).  Entry of (parity p, lane j) goes to
+// position g0 + vec j + p.
+void spread_banks(std::vector<std::pair<uint64_t, double>>& t, size_t g0, int vec, unsigned rmask,
+                  std::vector<std::pair<uint64_t, double>>& out) {
+    std::vector<std::pair<uint64_t, double>> cls[32];
+    const size_t n = 32 * (size_t)vec;
+    for (size_t i = g0; i < g0 + n; ++i) cls[(t[i].first & rmask) & 31].push_back(t[i]);
+    int order[32];
+    for (int c = 0; c < 32; ++c) order[c] = c;
+    std::stable_sort(order, order + 32, [&](int a, int b) { return cls[a].size() > cls[b].size(); });
+    int fill[4] = {0, 0, 0, 0};
+    out.assign(n, {0, 0.0});
+    for (int oi = 0; oi < 32; ++oi) {
+        int used[4] = {0, 0, 0, 0};  // this class's entries per parity so far
+        for (auto& e : cls[order[oi]]) {
+            // the parity this class has used least, then the one with the most room
+            int best = -1;
+            for (int q = 0; q < vec; ++q)
+                if (fill[q] < 32 && (best < 0 || used[q] < used[best] || (used[q] == used[best] && fill[q] < fill[best])))
+                    best = q;
+            out[(size_t)vec * fill[best] + best] = e;
+            ++fill[best];
+            ++used[best];
+        }
+    }
+    std::copy(out.begin(), out.end(), t.begin() + g0);
+}
 }  // namespace
 
 bool spmv_colsort_build(uint64_t m, uint64_t n, const int32_t* rp, const int32_t* col, const double* val,
                         SpmvColsortLayout& L, const std::vector<ColsortSegment>& segments_in, int classes,
                         bool tc_lanes, int vec) {
-    vec = vec == 2 ? 2 : 1;
+    vec = vec == 2 ? 2 : 1;  // (vec = 4, 256-bit val units, measured no faster: profiles/spmv_colsort_r2.md)
     (void)n;
     if (m == 0 || rp[m] == 0) return false;
     int64_t maxlen = 0;
@@ -561,6 +593,8 @@ bool spmv_colsort_build(uint64_t m, uint64_t n, const int32_t* rp, const int32_t
                 for (size_t w0 = 0; g > 1 && w0 < t.size(); w0 += win)
                     bank_order(t, w0, std::min(t.size(), w0 + win), rmask, g, scratch);
                 while (t.size() < k.nent) t.push_back({k.rows, 0.0});  // padding: column col_lo, scratch row
+                if (vec > 1 && tuning().spmv_colsort_spread)
+                    for (size_t g0 = 0; g0 < t.size(); g0 += 32 * vec) spread_banks(t, g0, vec, rmask, scratch);
                 if (!tc_lanes) {
                     for (size_t i = 0; i < t.size(); ++i) {
                         L.meta[k.e0 + i] = (uint32_t)t[i].first;

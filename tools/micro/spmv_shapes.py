@@ -21,7 +21,7 @@ torch.cuda.synchronize()
 cfgs = [tuple(c.split(":")) for c in sys.argv[1].split(",")] if len(sys.argv) > 1 else \
     [("cc", "1", "0"), ("cc", "1", "6"), ("cc", "2", "10"), ("cc", "2", "5"), ("cc", "2", "11"),
      ("tc", "1", "7"), ("tc", "2", "11"), ("tc", "2", "5"), ("tc", "2", "6")]
-cfgs = [(u, int(v), int(sh)) for u, v, sh in cfgs]
+cfgs = [(c[0], int(c[1]), int(c[2]), int(c[3]) if len(c) > 3 else 1) for c in cfgs]  # unit, vec, shape, spread
 
 
 def timeit(fn, reps=200):
@@ -38,10 +38,12 @@ def timeit(fn, reps=200):
 
 
 plans = {}
-for u, v in sorted({(u, v) for u, v, _ in cfgs}):
+for u, v, sp in sorted({(c[0], c[1], c[3]) for c in cfgs}):
     P.tuning_set("spmv_colsort_vec", v)
-    plans[(u, v)] = P.SpmvPlan(hrp, hcol, hval, n, unit=P.TENSOR_CORE if u == "tc" else P.CUDA_CORE)
-P.tuning_set("spmv_colsort_vec", 1)
+    P.tuning_set("spmv_colsort_spread", sp)
+    plans[(u, v, sp)] = P.SpmvPlan(hrp, hcol, hval, n, unit=P.TENSOR_CORE if u == "tc" else P.CUDA_CORE)
+P.tuning_set("spmv_colsort_vec", 2)
+P.tuning_set("spmv_colsort_spread", 1)
 res = {}
 # interleaved at call granularity (clocks and power drift under load): every
 # round calls each config once between its own pair of events
@@ -50,28 +52,28 @@ evs = {c: [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing
 for c in cfgs:  # warm
     P.tuning_set(f"spmv_colsort_{c[0]}_shape", c[2])
     for _ in range(3):
-        plans[(c[0], c[1])].execute(x, y)
+        plans[(c[0], c[1], c[3])].execute(x, y)
 torch.cuda.synchronize()
 BURST = int(os.environ.get("BURST", "1"))  # back-to-back calls between one event pair (bench-like when > 1)
 for r in range(N):
     for c in cfgs:
-        u, v, sh = c
+        u, v, sh, sp = c
         P.tuning_set(f"spmv_colsort_{u}_shape", sh)
         a, b = evs[c][r]
         a.record()
         for _ in range(BURST):
-            plans[(u, v)].execute(x, y)
+            plans[(u, v, sp)].execute(x, y)
         b.record()
 torch.cuda.synchronize()
 for c in cfgs:
     res[c] = [a.elapsed_time(b) / BURST for a, b in evs[c]]
-for u, v, sh in cfgs:
+for u, v, sh, sp in cfgs:
     P.tuning_set(f"spmv_colsort_{u}_shape", sh)
-    pl = plans[(u, v)]
+    pl = plans[(u, v, sp)]
     pl.execute(x, y); torch.cuda.synchronize(); y1 = y.clone()
     pl.execute(x, y); torch.cuda.synchronize()
     rel = float((y - yref).norm() / yref.norm())
-    r = sorted(res[(u, v, sh)])
+    r = sorted(res[(u, v, sh, sp)])
     ms = r[len(r) // 2]
-    print(f"{u} vec {v} shape {sh}: median {ms:.4f} ms min {r[0]:.4f} {B / ms / 1e6:.0f} GB/s "
+    print(f"{u} vec {v} shape {sh} spread {sp}: median {ms:.4f} ms min {r[0]:.4f} {B / ms / 1e6:.0f} GB/s "
           f"rel {rel:.2e} identical {bool(torch.equal(y, y1))}", flush=True)
