@@ -486,6 +486,26 @@ struct rl_spmv_plan_s {
 
 namespace {
 
+// Row blocks of a plan's K17 layout: spmv_plan_colsort_blocks blocks over
+// all rows (0: the builder's default, 4 x 148); spmv_plan_edge_blocks > 0
+// cuts the first and last of the execute_host pipeline's chunks into that
+// many blocks each, so those chunks run on every SM (the pipeline's head
+// and tail wait on them).
+std::vector<rlb::ColsortSegment> plan_segments(uint64_t m) {
+    const auto& t = rlb::tuning();
+    const uint64_t nb = t.spmv_plan_colsort_blocks > 0 ? (uint64_t)t.spmv_plan_colsort_blocks : 4 * (uint64_t)rlb::kNumSMsHost;
+    const uint64_t eb = (uint64_t)std::max(0, t.spmv_plan_edge_blocks);
+    const uint64_t nch = (uint64_t)std::max(1, t.spmv_plan_colsort_chunks);
+    if (eb == 0 || nch < 3) return {{m, nb}};
+    // rows of an edge chunk: the chunk weights of plan_create (taper k: edge
+    // chunks weigh 1, the others k + 1)
+    const uint64_t tk = (uint64_t)std::max(0, t.spmv_plan_taper);
+    const uint64_t wsum = tk ? (tk + 1) * (nch - 2) + 2 : nch;
+    const uint64_t e = m / wsum;
+    const uint64_t mid = nb - std::min(nb - 1, 2 * nb / wsum);
+    return {{e, eb}, {m - e, std::max<uint64_t>(1, mid)}, {m, eb}};
+}
+
 rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_t n, uint64_t nnz,
                             const int32_t* rp, const int32_t* col, const double* val) {
     KernelCharacterization k = spmv_csr_model({m, n, nnz}, kDefaultIndexBytes, p);
@@ -518,7 +538,7 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
         // spans fit); else the caller's CSR with the long-row path
         rlb::SpmvColsortLayout L;
         if (rlb::tuning().spmv_plan_colsort && nnz > 0 &&
-            rlb::spmv_colsort_build(m, n, rp, col, val, L, {}, rlb::colsort_classes(unit == ExecutionUnit::TensorCore),
+            rlb::spmv_colsort_build(m, n, rp, col, val, L, plan_segments(m), rlb::colsort_classes(unit == ExecutionUnit::TensorCore),
                                     unit == ExecutionUnit::TensorCore, rlb::tuning().spmv_colsort_vec)) {
             pl->colsort = true;
             pl->krb = L.rb;
@@ -699,7 +719,8 @@ void plan_enqueue(rl_spmv_plan_s* pl, const double* x, double* y, double* y_dire
         }
         const uint64_t r0 = pl->chunk_row[c], r1 = pl->chunk_row[c + 1];
         mark(sc);
-        plan_rows(pl, r0, r1, pl->x, y_direct ? y_direct : pl->y, sc);
+        if (!rlb::tuning().spmv_plan_probe_nocompute)  // developer probe: the copy pipeline alone
+            plan_rows(pl, r0, r1, pl->x, y_direct ? y_direct : pl->y, sc);
         mark(sc);
         if (!y_direct && pl->ycut[c]) {
             // the y group [ystart, r1) may span chunks of every compute
@@ -978,7 +999,12 @@ int rl_spmv_plan_execute(rl_spmv_plan pl, const double* x, double* y, rl_stream 
         require_ptr(pl, "plan");
         require_ptr(x, "x");
         require_ptr(y, "y");
-        plan_rows(pl, 0, pl->m, x, y, static_cast<cudaStream_t>(s));
+        if (rlb::tuning().spmv_plan_dev_chunks) {  // developer probe: the execute_host chunks, no copies
+            for (size_t c = 0; c + 1 < pl->chunk_row.size(); ++c)
+                plan_rows(pl, pl->chunk_row[c], pl->chunk_row[c + 1], x, y, static_cast<cudaStream_t>(s));
+        } else {
+            plan_rows(pl, 0, pl->m, x, y, static_cast<cudaStream_t>(s));
+        }
         put(out, pl->kc);
     });
 }
@@ -1290,6 +1316,10 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         {"spmv_colsort_tc_shape", &rlb::Tuning::spmv_colsort_tc_shape, false},
         {"spmv_colsort_cc_shape", &rlb::Tuning::spmv_colsort_cc_shape, false},
         {"spmv_colsort_vec", &rlb::Tuning::spmv_colsort_vec, false},
+        {"spmv_plan_colsort_blocks", &rlb::Tuning::spmv_plan_colsort_blocks, false},
+        {"spmv_plan_edge_blocks", &rlb::Tuning::spmv_plan_edge_blocks, false},
+        {"spmv_plan_dev_chunks", &rlb::Tuning::spmv_plan_dev_chunks, false},
+        {"spmv_plan_probe_nocompute", &rlb::Tuning::spmv_plan_probe_nocompute, false},
         {"spmv_colsort_spread", &rlb::Tuning::spmv_colsort_spread, false},
         {"spmv_plan_ygroups", &rlb::Tuning::spmv_plan_ygroups, false},
         {"stencil_r_ctas_per_sm", &rlb::Tuning::stencil_r_ctas_per_sm, false},

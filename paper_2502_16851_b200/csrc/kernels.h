@@ -35,6 +35,10 @@ struct Tuning {
     int spmv_colsort_classes = 0;  // K17 bank-ordering group 1..32 (0: 1 = none on the fixed-point grid, 16 for FP64 rows)
     int spmv_colsort_fixed = 2;    // K17 rows on a 64-bit fixed-point grid (+ FP64 row kernel for flagged rows):
                                    // 1 CUDA-core unit only, 2 both units, 0 neither (FP64 shared atomics)
+    int spmv_plan_colsort_blocks = 0; // K17 plan: row blocks over all rows (0: 4 x 148)
+    int spmv_plan_dev_chunks = 0;     // developer probe: rl_spmv_plan_execute runs the execute_host chunks one by one
+    int spmv_plan_probe_nocompute = 0; // developer probe: execute_host moves x and y but launches no kernel
+    int spmv_plan_edge_blocks = 0;    // K17 plan: blocks of the first / last execute_host chunk each (0: uniform blocks)
     int spmv_colsort_spread = 1;   // K17 plan build (vec > 1): deal each bank class over the entry parities of a warp step
     int spmv_colsort_vec = 2;      // K17 plan build: entries per thread unit (2: paired 128-bit val / 64-bit meta loads; 1: one entry)
     int spmv_colsort_tc_shape = 13; // K17 CTA shape (threads x units per step, p = software-pipelined loop):
