@@ -443,6 +443,7 @@ struct rl_spmv_plan_s {
     rlb::ColsortRun colsort_run() const {
         rlb::ColsortRun r = krun;
         r.rp = rp, r.col = col, r.val = val, r.col_base = 0;
+        r.fuse = rlb::tuning().spmv_colsort_fuse;
         return r;
     }
     uint64_t layout_bytes = 0;
@@ -1316,6 +1317,7 @@ int rl_tuning_set(const char* key, int64_t value, int64_t* previous) {
         {"spmv_colsort_tc_shape", &rlb::Tuning::spmv_colsort_tc_shape, false},
         {"spmv_colsort_cc_shape", &rlb::Tuning::spmv_colsort_cc_shape, false},
         {"spmv_colsort_vec", &rlb::Tuning::spmv_colsort_vec, false},
+        {"spmv_colsort_fuse", &rlb::Tuning::spmv_colsort_fuse, false},
         {"spmv_plan_colsort_blocks", &rlb::Tuning::spmv_plan_colsort_blocks, false},
         {"spmv_plan_edge_blocks", &rlb::Tuning::spmv_plan_edge_blocks, false},
         {"spmv_plan_dev_chunks", &rlb::Tuning::spmv_plan_dev_chunks, false},

@@ -415,6 +415,7 @@ struct rl_dist_spmv_s {
         rlb::ColsortRun colsort_run() const {
             rlb::ColsortRun r = krun;
             r.rp = rp, r.col = col, r.val = val, r.col_base = (int64_t)g.cb;
+            r.fuse = rlb::tuning().spmv_colsort_fuse;
             return r;
         }
     };

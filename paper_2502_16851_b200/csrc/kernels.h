@@ -39,6 +39,7 @@ struct Tuning {
     int spmv_plan_dev_chunks = 0;     // developer probe: rl_spmv_plan_execute runs the execute_host chunks one by one
     int spmv_plan_probe_nocompute = 0; // developer probe: execute_host moves x and y but launches no kernel
     int spmv_plan_edge_blocks = 0;    // K17 plan: blocks of the first / last execute_host chunk each (0: uniform blocks)
+    int spmv_colsort_fuse = 1;     // K17: flagged rows re-summed at each CTA's end inside the main kernel (0: a separate row kernel)
     int spmv_colsort_spread = 1;   // K17 plan build (vec > 1): deal each bank class over the entry parities of a warp step
     int spmv_colsort_vec = 2;      // K17 plan build: entries per thread unit (2: paired 128-bit val / 64-bit meta loads; 1: one entry)
     int spmv_colsort_tc_shape = 13; // K17 CTA shape (threads x units per step, p = software-pipelined loop):
@@ -235,6 +236,7 @@ struct ColsortRun {
     const int* col;
     const double* val;
     int64_t col_base;
+    int fuse;  // 1: the main kernel re-sums its flagged rows (list indexed by block row0; no row kernel)
 };
 int colsort_initial_grid(const SpmvKBlock& k);
 struct SpmvColsortLayout {

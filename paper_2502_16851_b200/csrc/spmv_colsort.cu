@@ -265,6 +265,66 @@ __device__ __forceinline__ void block_entries(double* __restrict__ ys, unsigned*
     }
 }
 
+// Re-sum listed rows in FP64 from the CSR, by threads [t, T) of the caller
+// (T a multiple of 32): CUDA core, 4 lanes per row (lane c takes entries c,
+// c + 4, ... in CSR order, then a fixed xor tree); tensor core, 8 rows per
+// warp as the rows of an m8n8k4 A fragment (lane 4r+k holds A[r][k] = val and
+// B[k][r] = x of row r's entry 4s+k at step s; D[r][r] accumulates row r, so
+// the diagonal only meets its own row's operands and Inf/NaN propagate as in
+// FP64).  Both orders are fixed: bit-reproducible.  Trip counts are uniform
+// per warp (full-mask shuffles).
+template <bool TC>
+__device__ __forceinline__ void resum_rows(const int* __restrict__ list, unsigned n, const ColsortRun& run,
+                                           const double* __restrict__ x, double* __restrict__ y, unsigned t,
+                                           unsigned T) {
+    const int lane = t & 31;
+    if (!TC) {
+        const int c = lane & 3;
+        for (unsigned i0 = 0; i0 < n; i0 += T / 4) {
+            const unsigned i = i0 + t / 4;
+            double sum = 0.0;
+            int r = -1;
+            if (i < n) {
+                r = __ldcg(list + i);
+                const int a = __ldg(run.rp + r), e = __ldg(run.rp + r + 1);
+                for (int j = a + c; j < e; j += 4)
+                    sum = fma(__ldg(run.val + j), __ldg(x + (__ldg(run.col + j) - run.col_base)), sum);
+            }
+            sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+            sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+            if (c == 0 && r >= 0) y[r] = sum;
+        }
+    } else {
+        const int r = lane >> 2, k = lane & 3;
+        for (unsigned g = (t / 32) * 8; g < n; g += (T / 32) * 8) {
+            const unsigned i = g + r;
+            int a = 0, e = 0, row = -1;
+            if (i < n) {
+                row = __ldcg(list + i);
+                a = __ldg(run.rp + row);
+                e = __ldg(run.rp + row + 1);
+            }
+            int steps = (e - a + 3) >> 2;
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) steps = max(steps, __shfl_xor_sync(0xffffffffu, steps, o));
+            double d0 = 0.0, d1 = 0.0;
+            for (int s = 0; s < steps; ++s) {
+                const int j = a + 4 * s + k;
+                double av = 0.0, bv = 0.0;
+                if (j < e) {
+                    av = __ldg(run.val + j);
+                    bv = __ldg(x + (__ldg(run.col + j) - run.col_base));
+                }
+                dmma_m8n8k4(d0, d1, av, bv, d0, d1);
+            }
+            // D[r][r] sits on lane 4r + (r >> 1), element r & 1
+            if (row >= 0 && k == (r >> 1)) y[row] = (r & 1) ? d1 : d0;
+        }
+    }
+}
+
+constexpr int kDefer = 4;  // blocks per CTA whose flagged rows wait for the CTA's end
+
 template <bool TC, int NT, int UF, bool PIPE, int V>
 __global__ void __launch_bounds__(NT, 2)
     spmv_colsort(const SpmvKBlock* __restrict__ blks, int b0, int b1, int rb, const double* __restrict__ val,
@@ -274,9 +334,14 @@ __global__ void __launch_bounds__(NT, 2)
     // (2 (rows + 1) words, fixed-point mode) -- the same bytes
     extern __shared__ double ys[];
     __shared__ unsigned s_red[2][NT / 32];
+    // fused flagged rows (run.fuse): a block's flagged rows are listed at
+    // run.list[row0 ...] (room for every row of the block) and re-summed at the
+    // CTA's end, so no barrier of a later block waits on them
+    __shared__ unsigned s_fcnt, s_dcnt[kDefer], s_drow0[kDefer];
     const uint64_t pol = policy_evict_first(), polx = policy_evict_last();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int b = b0 + blockIdx.x; b < b1; b += gridDim.x) {
+    int jb = 0;  // this CTA's blocks so far
+    for (int b = b0 + blockIdx.x; b < b1; b += gridDim.x, ++jb) {
         const SpmvKBlock blk = blks[b];
         const unsigned stride = blk.rows + 1;
         unsigned* lo = reinterpret_cast<unsigned*>(ys);
@@ -288,6 +353,7 @@ __global__ void __launch_bounds__(NT, 2)
             const int S = 62 - (int)blk.hl - et;
             const bool fixed = et != kColsortFp64 && S >= -1000 && S <= 1000;
             for (unsigned i = threadIdx.x; i < 2 * stride; i += NT) lo[i] = 0u;  // = stride doubles
+            if (threadIdx.x == 0) s_fcnt = 0u;
             __syncthreads();
             unsigned mh = 0u, ml = 0u;
             if (fixed)
@@ -334,20 +400,39 @@ __global__ void __launch_bounds__(NT, 2)
                         if (bal) {
                             const int lead = __ffs(am) - 1;
                             unsigned base = 0;
-                            if (lane == lead) base = atomicAdd(run.count, (unsigned)__popc(bal));
+                            if (lane == lead)
+                                base = run.fuse ? atomicAdd(&s_fcnt, (unsigned)__popc(bal))
+                                                : atomicAdd(run.count, (unsigned)__popc(bal));
                             base = __shfl_sync(am, base, lead);
-                            if (flag) run.list[base + __popc(bal & ((1u << lane) - 1))] = (int)(blk.row0 + i);
+                            if (flag)
+                                run.list[(run.fuse ? blk.row0 : 0u) + base + __popc(bal & ((1u << lane) - 1))] =
+                                    (int)(blk.row0 + i);
                         }
                     }
                 } else {
                     for (unsigned i = threadIdx.x; i < blk.rows; i += NT) y[blk.row0 + i] = ys[i];
                 }
                 __syncthreads();
+                if (run.fuse && fixed) {
+                    if (jb < kDefer) {
+                        if (threadIdx.x == 0) s_dcnt[jb] = s_fcnt, s_drow0[jb] = blk.row0;
+                    } else {  // more blocks than the deferral slots: re-sum now
+                        __threadfence_block();
+                        resum_rows<TC>(run.list + blk.row0, s_fcnt, run, x, y, threadIdx.x, NT);
+                    }
+                } else if (run.fuse && jb < kDefer && threadIdx.x == 0) {
+                    s_dcnt[jb] = 0u;
+                }
                 break;
             }
             et = want;
             __syncthreads();
         }
+    }
+    if (run.fuse && run.grid) {
+        __syncthreads();
+        for (int j = 0; j < jb && j < kDefer; ++j)
+            if (s_dcnt[j]) resum_rows<TC>(run.list + s_drow0[j], s_dcnt[j], run, x, y, threadIdx.x, NT);
     }
 }
 
@@ -682,6 +767,7 @@ cudaError_t launch_spmv_colsort(int unit, int vec, const SpmvKBlock* blks, int b
     if (e != cudaSuccess) return e;
     note_launch();
     if ((e = cudaGetLastError()) != cudaSuccess || !run.grid) return e;
+    if (run.fuse) return cudaSuccess;  // flagged rows re-summed inside the main kernel
     if (unit) spmv_flagged_rows_tc<<<2 * kNumSMs, 256, 0, s>>>(run, x, y);
     else spmv_flagged_rows<<<2 * kNumSMs, 256, 0, s>>>(run, x, y);
     note_launch();

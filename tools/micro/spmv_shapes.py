@@ -21,7 +21,8 @@ torch.cuda.synchronize()
 cfgs = [tuple(c.split(":")) for c in sys.argv[1].split(",")] if len(sys.argv) > 1 else \
     [("cc", "1", "0"), ("cc", "1", "6"), ("cc", "2", "10"), ("cc", "2", "5"), ("cc", "2", "11"),
      ("tc", "1", "7"), ("tc", "2", "11"), ("tc", "2", "5"), ("tc", "2", "6")]
-cfgs = [(c[0], int(c[1]), int(c[2]), int(c[3]) if len(c) > 3 else 1) for c in cfgs]  # unit, vec, shape, spread
+cfgs = [(c[0], int(c[1]), int(c[2]), int(c[3]) if len(c) > 3 else 1, int(c[4]) if len(c) > 4 else 1)
+        for c in cfgs]  # unit, vec, shape, spread, fuse
 
 
 def timeit(fn, reps=200):
@@ -51,14 +52,16 @@ N = int(os.environ.get("ROUNDS", "400"))
 evs = {c: [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(N)] for c in cfgs}
 for c in cfgs:  # warm
     P.tuning_set(f"spmv_colsort_{c[0]}_shape", c[2])
+    P.tuning_set("spmv_colsort_fuse", c[4])
     for _ in range(3):
         plans[(c[0], c[1], c[3])].execute(x, y)
 torch.cuda.synchronize()
 BURST = int(os.environ.get("BURST", "1"))  # back-to-back calls between one event pair (bench-like when > 1)
 for r in range(N):
     for c in cfgs:
-        u, v, sh, sp = c
+        u, v, sh, sp, fu = c
         P.tuning_set(f"spmv_colsort_{u}_shape", sh)
+        P.tuning_set("spmv_colsort_fuse", fu)
         a, b = evs[c][r]
         a.record()
         for _ in range(BURST):
@@ -67,13 +70,14 @@ for r in range(N):
 torch.cuda.synchronize()
 for c in cfgs:
     res[c] = [a.elapsed_time(b) / BURST for a, b in evs[c]]
-for u, v, sh, sp in cfgs:
+for u, v, sh, sp, fu in cfgs:
     P.tuning_set(f"spmv_colsort_{u}_shape", sh)
+    P.tuning_set("spmv_colsort_fuse", fu)
     pl = plans[(u, v, sp)]
     pl.execute(x, y); torch.cuda.synchronize(); y1 = y.clone()
     pl.execute(x, y); torch.cuda.synchronize()
     rel = float((y - yref).norm() / yref.norm())
-    r = sorted(res[(u, v, sh, sp)])
+    r = sorted(res[(u, v, sh, sp, fu)])
     ms = r[len(r) // 2]
-    print(f"{u} vec {v} shape {sh} spread {sp}: median {ms:.4f} ms min {r[0]:.4f} {B / ms / 1e6:.0f} GB/s "
+    print(f"{u} vec {v} shape {sh} spread {sp} fuse {fu}: median {ms:.4f} ms min {r[0]:.4f} {B / ms / 1e6:.0f} GB/s "
           f"rel {rel:.2e} identical {bool(torch.equal(y, y1))}", flush=True)
