@@ -736,18 +736,11 @@ template <bool TC, int V>
 cudaError_t launch_shape(int shape, const SpmvKBlock* blks, int b0, int b1, int rb, size_t smem, const double* val,
                          const unsigned* meta, const double* x, double* y, const ColsortRun& run, cudaStream_t s) {
     switch (shape) {
-        case 1: return launch_main<TC, 768, 3, false, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
-        case 4: return launch_main<TC, 1024, 2, false, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
-        case 5: return launch_main<TC, 1024, 1, true, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
-        case 6: return launch_main<TC, 768, 2, true, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
         case 7: return launch_main<TC, 640, 3, true, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
         case 8: return launch_main<TC, 512, 4, true, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
         case 10: return launch_main<TC, 1024, 1, false, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
         case 11: return launch_main<TC, 512, 2, true, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
-        case 12: return launch_main<TC, 640, 2, true, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
         case 13: return launch_main<TC, 768, 1, true, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
-        case 14: return launch_main<TC, 512, 3, true, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
-        case 15: return launch_main<TC, 384, 4, true, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
         case 16: return launch_main<TC, 512, 1, true, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
         default: return launch_main<TC, kThreads, kUnroll, false, V>(blks, b0, b1, rb, smem, val, meta, x, y, run, s);
     }

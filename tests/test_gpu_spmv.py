@@ -634,7 +634,7 @@ def test_colsort_cta_shapes_bit_identical(cuda, unit):
         dx = torch.from_numpy(x).cuda()
         outs = {}
         for vec in (1, 2):
-            for sh in (0, 1, 4, 5, 6, 7, 8, 10, 11, 12, 13, 14, 15, 16):
+            for sh in (0, 7, 8, 10, 11, 13, 16):
                 old = P.tuning_set(key, sh)
                 try:
                     dy = torch.full((m,), float("nan"), dtype=torch.float64, device="cuda")
