@@ -663,3 +663,50 @@ def test_colsort_cta_shapes_bit_identical(cuda, unit):
         P.tuning_set("spmv_colsort_fixed", prev[0])
         P.tuning_set("spmv_plan_colsort", prev[1])
         P.tuning_set("spmv_colsort_vec", prev[2])
+
+
+@pytest.mark.parametrize("unit", UNITS)
+@pytest.mark.parametrize("blocks", [0, 2400])
+def test_colsort_fused_flagged_rows_match_row_kernel(cuda, unit, blocks):
+    """Flagged rows re-summed inside the main kernel (spmv_colsort_fuse = 1:
+    at the CTA's end for its first 4 blocks, at the block's end past that --
+    2400 blocks on 296 CTAs exercise both) give the same bits as the separate
+    FP64 row kernel (fuse = 0): the same rows, the same fixed summation order
+    per unit.  Rows cancel (half of each row negates the other half) so that
+    many rows are flagged."""
+    import torch
+
+    m = n = 300000
+    rp, col, val = O.gen_band_csr(m, 0, n, 16, 30000, 12)
+    val = val.copy()
+    for i in range(0, m, 3):
+        a, b = rp[i], rp[i + 1]
+        h = (b - a) // 2
+        val[a + h:a + 2 * h] = -val[a:a + h]
+    x = O.fill_uniform(n, 12, 4, 0, 1)
+    want = O.spmv_csr(rp, col, val, x)
+    prev = [P.tuning_set("spmv_colsort_fixed", 2), P.tuning_set("spmv_plan_colsort", 1),
+            P.tuning_set("spmv_plan_colsort_blocks", blocks)]
+    try:
+        plan = P.SpmvPlan(rp, col, val, n, unit=unit)
+    finally:
+        P.tuning_set("spmv_plan_colsort_blocks", prev[2])
+    try:
+        assert plan.layout() == "colsort"
+        dx = torch.from_numpy(x).cuda()
+        outs = []
+        for fuse in (1, 0, 1):
+            old = P.tuning_set("spmv_colsort_fuse", fuse)
+            try:
+                dy = torch.full((m,), float("nan"), dtype=torch.float64, device="cuda")
+                plan.execute(dx, dy)
+                torch.cuda.synchronize()
+                outs.append(dy.cpu().numpy())
+            finally:
+                P.tuning_set("spmv_colsort_fuse", old)
+        assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+        assert O.rel_err(outs[0], want) <= TOL
+    finally:
+        plan.close()
+        P.tuning_set("spmv_colsort_fixed", prev[0])
+        P.tuning_set("spmv_plan_colsort", prev[1])
