@@ -223,6 +223,41 @@ class Spmv:
             return self.part.rows * 8, h["y"].numel() * 8
         return h["x"].numel() * 8, h["y"].numel() * 8
 
+    def e2e_stream(self, h, unit, steps):
+        """A stream of independent vectors through one plan (N = 1): step k
+        uploads its own x (R distinct pinned vectors, rotated), computes, and
+        downloads its own y, via rl_spmv_plan_execute_host_async; consecutive
+        calls overlap (step k + 1's x upload beside step k's compute and y
+        download) and the timed region ends with rl_spmv_plan_wait.  Returns
+        (seconds, results bit-identical to one synchronous call each)."""
+        t, P, R = self.torch, self.P, 3
+        if "plan" not in h:
+            h["plan"] = P.SpmvPlan(h["rp"], h["col"], h["val"], h["x"].numel(), unit=unit)
+        if "xs" not in h:
+            xs = [h["x"]]
+            for r in range(1, R):
+                d = t.empty_like(self.x)
+                P.fill_uniform(d, SEED + r, 4, 0, 1)
+                xs.append(t.empty(d.shape, dtype=t.float64, pin_memory=True).copy_(d))
+            h["xs"] = xs
+            h["ys"] = [t.empty(h["y"].shape, dtype=t.float64, pin_memory=True) for _ in range(R)]
+        pl, xs, ys = h["plan"], h["xs"], h["ys"]
+        for r in range(R):  # warm: both device slots, every host buffer pair
+            pl.execute_host_async(xs[r], ys[r])
+        pl.wait()
+        t0 = time.perf_counter()
+        for k in range(steps):
+            pl.execute_host_async(xs[k % R], ys[k % R])
+        pl.wait()
+        sec = time.perf_counter() - t0
+        ok = True
+        for r in range(R):  # the last result of each input against a synchronous call
+            if steps > r:
+                chk = t.empty_like(ys[r])
+                pl.execute_host(xs[r], chk)
+                ok = ok and bool(t.equal(chk, ys[r]))
+        return sec, ok
+
     def full_copy_bytes(self, h):
         return (sum(h[k].numel() * h[k].element_size() for k in ("rp", "col", "val", "x")),
                 h["y"].numel() * 8)
@@ -1007,6 +1042,17 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_val = wl.job_bytes * args.e2e_steps / e2e_s / 1e9
+    e2e_sync = None
+    if hasattr(wl, "e2e_stream") and world == 1:
+        # the headline e2e: a stream of independent vectors, calls overlapping;
+        # the one-call-at-a-time number (the iterative-solver pattern) beside it
+        st_s, st_ok = wl.e2e_stream(h, unit, args.e2e_steps)
+        e2e_sync = {"value": round(e2e_val, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+                    "api": "rl_spmv_plan_execute_host, one synchronous call per step (each x may depend on the "
+                           "previous y)"}
+        e2e_val = wl.job_bytes * args.e2e_steps / st_s / 1e9
+        e2e_stream_ok = st_ok
     full_copy = None
     if hasattr(wl, "full_copy_step") and world == 1:
         wl.full_copy_step(h, unit)
@@ -1026,6 +1072,12 @@ def main():
     api = {"spmv": ("rl_spmv_plan_execute_host: A resident (uploaded once by rl_spmv_plan_create), "
                     "x H2D and y D2H from pinned host memory inside every timed call"),
            }.get(args.workload, "rl_*_host C-ABI (pinned host buffers, copies inside the timed call)")
+    if e2e_sync is not None:
+        api = ("rl_spmv_plan_execute_host_async + rl_spmv_plan_wait: A resident (uploaded once by "
+               "rl_spmv_plan_create); a stream of independent vectors, every step its own x H2D and its own y "
+               "D2H from pinned host memory (3 distinct vectors rotated), consecutive calls overlapping; timed "
+               "region ends with the wait; results bit-identical to synchronous calls: " +
+               ("yes" if e2e_stream_ok else "NO"))
     if world > 1:
         api = ("rl_dist_* plan: the rank's owned input H2D from pinned host memory, the distributed call "
                "(NCCL halo exchange + kernels), the rank's result D2H; max over ranks")
@@ -1041,6 +1093,7 @@ def main():
                      "launch_ms_p50": round(per_sorted[len(per_sorted) // 2], 5)},
         "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": args.e2e_steps, "api": api},
+        "e2e_sync": e2e_sync,
         "e2e_full_copy": full_copy,
         "gpu_launches": timed_launches,
         "clocks": clk.summary(),

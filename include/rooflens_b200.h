@@ -188,9 +188,10 @@ RL_API int rl_stencil_host(rl_unit unit, rl_precision precision, const char* pre
  * y rows of a block in shared memory, x read in column order)
  * when every row has <= 1024 nonzeros and the block column spans fit, else
  * keeps the CSR (with the long-row path); the layout streams no more bytes
- * than the CSR.  The column-sorted layout adds into its y rows with FP64
- * shared atomics, so repeated executes may differ in the last bits (within
- * the 1e-12 norm-wise tolerance); CSR executes are bit-reproducible.  Tuning
+ * than the CSR.  The column-sorted layout sums each row on a 64-bit
+ * fixed-point grid (both units; rows too small for 2^-46 relative precision
+ * on it are re-summed in FP64 in a fixed order), so repeated executes are
+ * bit-identical; CSR executes are bit-reproducible too.  Tuning
  * key spmv_plan_colsort = 0 keeps the CSR.  execute_host pipelines the x upload, the row-chunk kernels and the y download on three streams: row
  * chunk c starts as soon as the x prefix it references (max column, computed
  * at creation) has arrived.  The plan owns its device buffers; no allocation
@@ -200,6 +201,14 @@ RL_API int rl_spmv_plan_create(rl_unit unit, rl_precision precision, uint64_t m,
                                uint64_t nnz, const int32_t* row_ptr, const int32_t* col,
                                const double* val, rl_spmv_plan* out);
 RL_API int rl_spmv_plan_execute_host(rl_spmv_plan plan, const double* x, double* y, rl_kchar* out);
+/* The same pipelined call, returning once it is enqueued: consecutive calls
+ * overlap (call k + 1's x upload beside call k's compute and y download) on
+ * three device buffer slots.  x must stay unchanged and y unread until
+ * rl_spmv_plan_wait returns; a later rl_spmv_plan_execute_host waits first.
+ * For streams of independent vectors (no rooflens counterpart: the reference
+ * has no executing path). */
+RL_API int rl_spmv_plan_execute_host_async(rl_spmv_plan plan, const double* x, double* y, rl_kchar* out);
+RL_API int rl_spmv_plan_wait(rl_spmv_plan plan);
 RL_API int rl_spmv_plan_execute(rl_spmv_plan plan, const double* x_dev, double* y_dev,
                                 rl_stream stream, rl_kchar* out);
 RL_API int rl_spmv_plan_destroy(rl_spmv_plan plan);

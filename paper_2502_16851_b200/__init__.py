@@ -158,6 +158,8 @@ _SIGNATURES = {
     "rl_host_workspace_release": (_int, []),
     "rl_spmv_plan_create": (_int, [_int, _int, _u64, _u64, _u64, _ptr, _ptr, _ptr, C.POINTER(_ptr)]),
     "rl_spmv_plan_execute_host": (_int, [_ptr, _ptr, _ptr, _KP]),
+    "rl_spmv_plan_execute_host_async": (_int, [_ptr, _ptr, _ptr, _KP]),
+    "rl_spmv_plan_wait": (_int, [_ptr]),
     "rl_spmv_plan_execute": (_int, [_ptr, _ptr, _ptr, _ptr, _KP]),
     "rl_spmv_plan_destroy": (_int, [_ptr]),
     "rl_spmv_plan_info": (_int, [_ptr, C.POINTER(_int), C.POINTER(_u64)]),
@@ -512,6 +514,17 @@ class SpmvPlan:
         _check(lib().rl_spmv_plan_execute_host(self._h, _host_ptr(x, "f64", "x"), _host_ptr(y, "f64", "y"),
                                                C.byref(k)))
         return _kc(k)
+
+    def execute_host_async(self, x, y) -> KernelCharacterization:
+        """Enqueue one execute_host and return: x must stay unchanged and y
+        unread until wait(); consecutive calls overlap on three buffer slots."""
+        k = _KChar()
+        _check(lib().rl_spmv_plan_execute_host_async(self._h, _host_ptr(x, "f64", "x"), _host_ptr(y, "f64", "y"),
+                                                     C.byref(k)))
+        return _kc(k)
+
+    def wait(self) -> None:
+        _check(lib().rl_spmv_plan_wait(self._h))
 
     def execute(self, x, y, stream=None) -> KernelCharacterization:
         k = _KChar()

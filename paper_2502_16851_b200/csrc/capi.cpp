@@ -459,6 +459,14 @@ struct rl_spmv_plan_s {
     std::vector<cudaEvent_t> ev_x, ev_y;
     std::vector<cudaEvent_t> ev_join;  // one per compute stream + s_out
     cudaEvent_t ev_fork = nullptr;  // s_cmp / s_out join s_in at the start of every call (and capture)
+    // execute_host_async: calls rotate over kSlots device x / y buffer slots
+    // (slot 0 = x / y above, the others allocated on first use); a call reuses
+    // a slot only after the slot's previous call has finished computing from
+    // its x (ev_cdone) and downloading its y (ev_ydone)
+    static constexpr int kSlots = 3;
+    double *xs[kSlots] = {}, *ys[kSlots] = {};  // slot 0 = x / y above
+    uint64_t async_calls = 0;
+    cudaEvent_t ev_cdone[kSlots] = {}, ev_ydone[kSlots] = {}, ev_xall[kSlots] = {};
     // execute_host as a CUDA graph, captured for the last (x, y) host pair
     cudaGraphExec_t gexec = nullptr;
     const double* gx = nullptr;
@@ -471,6 +479,13 @@ struct rl_spmv_plan_s {
         if (val) cudaFree(val);
         if (x) cudaFree(x);
         if (y) cudaFree(y);
+        for (int i = 1; i < kSlots; ++i) {
+            if (xs[i]) cudaFree(xs[i]);
+            if (ys[i]) cudaFree(ys[i]);
+        }
+        for (int i = 0; i < kSlots; ++i)
+            for (auto e : {ev_cdone[i], ev_ydone[i], ev_xall[i]})
+                if (e) cudaEventDestroy(e);
         for (void* p : {(void*)kblk, (void*)kval, (void*)kmeta, (void*)krun.grid, (void*)krun.list, (void*)krun.count})
             if (p) cudaFree(p);
         if (gexec) cudaGraphExecDestroy(gexec);
@@ -689,19 +704,25 @@ void plan_rows(rl_spmv_plan_s* pl, uint64_t r0, uint64_t r1, const double* x, do
 // chunks on s_cmp as their x prefix lands, y chunks on s_out).  `mark`
 // records trace events.
 template <class Mark>
-void plan_enqueue(rl_spmv_plan_s* pl, const double* x, double* y, double* y_direct, Mark&& mark) {
+void plan_enqueue(rl_spmv_plan_s* pl, const double* x, double* y, double* y_direct, Mark&& mark, double* dx = nullptr,
+                  double* dy = nullptr, bool fork = true) {
+    if (!dx) dx = pl->x;
+    if (!dy) dy = pl->y;
     // Fork: the compute and output streams join s_in before anything else, so
     // under graph capture every chunk is inside the graph even when a chunk
     // waits on no x piece (a leading run of empty rows), and eagerly no
-    // chunk of this call overtakes the previous call's y copies.
-    ck(cudaEventRecord(pl->ev_fork, pl->s_in), "event");
-    for (auto st : pl->s_cmp) ck(cudaStreamWaitEvent(st, pl->ev_fork, 0), "wait");
-    ck(cudaStreamWaitEvent(pl->s_out, pl->ev_fork, 0), "wait");
+    // chunk of this call overtakes the previous call's y copies.  (The async
+    // calls order their slots with events instead and let calls overlap.)
+    if (fork) {
+        ck(cudaEventRecord(pl->ev_fork, pl->s_in), "event");
+        for (auto st : pl->s_cmp) ck(cudaStreamWaitEvent(st, pl->ev_fork, 0), "wait");
+        ck(cudaStreamWaitEvent(pl->s_out, pl->ev_fork, 0), "wait");
+    }
     mark(pl->s_in);
     const size_t npc = pl->ev_x.size();
     for (size_t i = 0; i < npc; ++i) {
         const uint64_t a = pl->xpiece[i], b = pl->xpiece[i + 1];
-        ck(cudaMemcpyAsync(pl->x + a, x + a, (b - a) * 8, cudaMemcpyHostToDevice, pl->s_in), "H2D x");
+        ck(cudaMemcpyAsync(dx + a, x + a, (b - a) * 8, cudaMemcpyHostToDevice, pl->s_in), "H2D x");
         ck(cudaEventRecord(pl->ev_x[i], pl->s_in), "event");
         mark(pl->s_in);
     }
@@ -721,7 +742,7 @@ void plan_enqueue(rl_spmv_plan_s* pl, const double* x, double* y, double* y_dire
         const uint64_t r0 = pl->chunk_row[c], r1 = pl->chunk_row[c + 1];
         mark(sc);
         if (!rlb::tuning().spmv_plan_probe_nocompute)  // developer probe: the copy pipeline alone
-            plan_rows(pl, r0, r1, pl->x, y_direct ? y_direct : pl->y, sc);
+            plan_rows(pl, r0, r1, dx, y_direct ? y_direct : dy, sc);
         mark(sc);
         if (!y_direct && pl->ycut[c]) {
             // the y group [ystart, r1) may span chunks of every compute
@@ -732,7 +753,7 @@ void plan_enqueue(rl_spmv_plan_s* pl, const double* x, double* y, double* y_dire
                 ck(cudaEventRecord(ev, pl->s_cmp[k]), "event");
                 ck(cudaStreamWaitEvent(pl->s_out, ev, 0), "wait");
             }
-            ck(cudaMemcpyAsync(y + ystart, pl->y + ystart, (r1 - ystart) * 8, cudaMemcpyDeviceToHost, pl->s_out),
+            ck(cudaMemcpyAsync(y + ystart, dy + ystart, (r1 - ystart) * 8, cudaMemcpyDeviceToHost, pl->s_out),
                "D2H y");
             mark(pl->s_out);
             ystart = r1;
@@ -747,8 +768,57 @@ bool pinned_host(const void* p) {
     return ok;
 }
 
+// Wait for every execute_host_async call of the plan.
+void plan_wait(rl_spmv_plan_s* pl) {
+    ck(cudaStreamSynchronize(pl->s_in), "sync");
+    for (auto st : pl->s_cmp) ck(cudaStreamSynchronize(st), "sync");
+    ck(cudaStreamSynchronize(pl->s_out), "sync");
+}
+
+// One call that returns after enqueueing: x is read and y written
+// asynchronously (valid after rl_spmv_plan_wait).  Consecutive calls
+// overlap -- call k + 1's x upload runs beside call k's compute and y
+// download -- on two device buffer slots.
+void plan_execute_host_async(rl_spmv_plan_s* pl, const double* x, double* y) {
+    require_ptr(pl, "plan");
+    require_ptr(x, "x");
+    require_ptr(y, "y");
+    const int b = (int)(pl->async_calls % rl_spmv_plan_s::kSlots);
+    pl->xs[0] = pl->x;
+    pl->ys[0] = pl->y;
+    if (!pl->xs[b]) {
+        ck(cudaMalloc(&pl->xs[b], std::max<uint64_t>(pl->n, 2) * 8), "plan alloc");
+        ck(cudaMalloc(&pl->ys[b], std::max<uint64_t>(pl->m, 1) * 8), "plan alloc");
+    }
+    if (!pl->ev_cdone[b]) {
+        for (auto* e : {&pl->ev_cdone[b], &pl->ev_ydone[b], &pl->ev_xall[b]})
+            ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+    } else {  // the slot's previous call: its compute read x, its y went down
+        ck(cudaStreamWaitEvent(pl->s_in, pl->ev_cdone[b], 0), "wait");
+        ck(cudaStreamWaitEvent(pl->s_cmp[0], pl->ev_ydone[b], 0), "wait");
+    }
+    // Whole-vector copies: the overlap comes from consecutive calls (call k +
+    // 1's x upload beside call k's y download), so the per-call pipeline
+    // chunks, whose copy pieces and cross-stream waits cost more than they
+    // hide (tools/micro/plan_stream.py: 8 chunks 1.035 ms per call, 2 chunks
+    // 0.809), are not needed.
+    double* dx = pl->xs[b];
+    double* dy = pl->ys[b];
+    cudaStream_t sc = pl->s_cmp[0];
+    ck(cudaMemcpyAsync(dx, x, pl->n * 8, cudaMemcpyHostToDevice, pl->s_in), "H2D x");
+    ck(cudaEventRecord(pl->ev_xall[b], pl->s_in), "event");
+    ck(cudaStreamWaitEvent(sc, pl->ev_xall[b], 0), "wait");
+    plan_rows(pl, 0, pl->m, dx, dy, sc);
+    ck(cudaEventRecord(pl->ev_cdone[b], sc), "event");
+    ck(cudaStreamWaitEvent(pl->s_out, pl->ev_cdone[b], 0), "wait");
+    ck(cudaMemcpyAsync(y, dy, pl->m * 8, cudaMemcpyDeviceToHost, pl->s_out), "D2H y");
+    ck(cudaEventRecord(pl->ev_ydone[b], pl->s_out), "event");
+    ++pl->async_calls;
+}
+
 void plan_execute_host(rl_spmv_plan_s* pl, const double* x, double* y) {
     require_ptr(pl, "plan");
+    if (pl->async_calls) plan_wait(pl);  // a synchronous call after async ones
     require_ptr(x, "x");
     require_ptr(y, "y");
     static const bool trace = getenv("RL_PLAN_TRACE") != nullptr;
@@ -987,6 +1057,18 @@ int rl_spmv_plan_create(rl_unit u, rl_precision p, uint64_t m, uint64_t n, uint6
         require_ptr(out, "out");
         *out = nullptr;
         *out = plan_create(unit_of(u), prec_of(p), m, n, nnz, rp, col, val);
+    });
+}
+int rl_spmv_plan_execute_host_async(rl_spmv_plan pl, const double* x, double* y, rl_kchar* out) {
+    return guarded([&] {
+        plan_execute_host_async(pl, x, y);
+        put(out, pl->kc);
+    });
+}
+int rl_spmv_plan_wait(rl_spmv_plan pl) {
+    return guarded([&] {
+        require_ptr(pl, "plan");
+        plan_wait(pl);
     });
 }
 int rl_spmv_plan_execute_host(rl_spmv_plan pl, const double* x, double* y, rl_kchar* out) {

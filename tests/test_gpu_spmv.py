@@ -710,3 +710,34 @@ def test_colsort_fused_flagged_rows_match_row_kernel(cuda, unit, blocks):
         plan.close()
         P.tuning_set("spmv_colsort_fixed", prev[0])
         P.tuning_set("spmv_plan_colsort", prev[1])
+
+
+@pytest.mark.parametrize("unit", UNITS)
+def test_plan_execute_host_async_stream(cuda, unit):
+    """rl_spmv_plan_execute_host_async: a stream of independent vectors whose
+    calls overlap on the device slots gives, per call, the bits of a
+    synchronous execute_host on the same x (three device slots, seven calls); a synchronous call after async
+    ones waits for them; wait() with nothing in flight returns."""
+    import torch
+
+    m = n = 200000
+    rp, col, val = O.gen_band_csr(m, 0, n, 16, 30000, 21)
+    plan = P.SpmvPlan(rp, col, val, n, unit=unit)
+    try:
+        plan.wait()
+        xs = [torch.from_numpy(O.fill_uniform(n, 30 + r, 4, 0, 1)).pin_memory() for r in range(3)]
+        ys = [torch.full((m,), float("nan"), dtype=torch.float64).pin_memory() for _ in range(7)]
+        for k in range(7):
+            plan.execute_host_async(xs[k % 3], ys[k])
+        plan.wait()
+        for k in range(7):
+            want = torch.empty(m, dtype=torch.float64).pin_memory()
+            plan.execute_host(xs[k % 3], want)
+            assert torch.equal(ys[k], want), k
+            assert O.rel_err(ys[k].numpy(), O.spmv_csr(rp, col, val, xs[k % 3].numpy())) <= TOL
+        y_sync = torch.empty(m, dtype=torch.float64).pin_memory()
+        plan.execute_host_async(xs[0], ys[0])
+        plan.execute_host(xs[1], y_sync)  # waits for the async call first
+        assert torch.equal(ys[0], ys[3]) and torch.equal(y_sync, ys[1])
+    finally:
+        plan.close()
