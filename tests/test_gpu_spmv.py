@@ -713,7 +713,8 @@ def test_colsort_fused_flagged_rows_match_row_kernel(cuda, unit, blocks):
 
 
 @pytest.mark.parametrize("unit", UNITS)
-def test_plan_execute_host_async_stream(cuda, unit):
+@pytest.mark.parametrize("colsort", [1, 0])
+def test_plan_execute_host_async_stream(cuda, unit, colsort):
     """rl_spmv_plan_execute_host_async: a stream of independent vectors whose
     calls overlap on the device slots gives, per call, the bits of a
     synchronous execute_host on the same x (three device slots, seven calls); a synchronous call after async
@@ -722,8 +723,13 @@ def test_plan_execute_host_async_stream(cuda, unit):
 
     m = n = 200000
     rp, col, val = O.gen_band_csr(m, 0, n, 16, 30000, 21)
-    plan = P.SpmvPlan(rp, col, val, n, unit=unit)
+    prev = P.tuning_set("spmv_plan_colsort", colsort)
     try:
+        plan = P.SpmvPlan(rp, col, val, n, unit=unit)
+    finally:
+        P.tuning_set("spmv_plan_colsort", prev)
+    try:
+        assert plan.layout() == ("colsort" if colsort else "csr")
         plan.wait()
         xs = [torch.from_numpy(O.fill_uniform(n, 30 + r, 4, 0, 1)).pin_memory() for r in range(3)]
         ys = [torch.full((m,), float("nan"), dtype=torch.float64).pin_memory() for _ in range(7)]
