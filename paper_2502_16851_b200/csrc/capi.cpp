@@ -1099,7 +1099,14 @@ int rl_spmv_plan_info(rl_spmv_plan pl, int* tiled, uint64_t* layout_bytes) {
     });
 }
 int rl_spmv_plan_destroy(rl_spmv_plan pl) {
-    return guarded([&] { delete pl; });
+    return guarded([&] {
+        if (pl && pl->async_calls) {  // async calls still in flight read / write the plan's buffers
+            cudaStreamSynchronize(pl->s_in);
+            for (auto st : pl->s_cmp) cudaStreamSynchronize(st);
+            cudaStreamSynchronize(pl->s_out);
+        }
+        delete pl;
+    });
 }
 int rl_host_workspace_release(void) {
     return guarded([&] {
