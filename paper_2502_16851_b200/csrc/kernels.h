@@ -40,7 +40,9 @@ struct Tuning {
     int spmv_plan_probe_nocompute = 0; // developer probe: execute_host moves x and y but launches no kernel
     int spmv_plan_edge_blocks = 0;    // K17 plan: blocks of the first / last execute_host chunk each (0: uniform blocks)
     int spmv_colsort_fuse = 1;     // K17: flagged rows re-summed at each CTA's end inside the main kernel (0: a separate row kernel)
-    int spmv_colsort_spread = 1;   // K17 plan build (vec > 1): deal each bank class over the entry parities of a warp step
+    int spmv_colsort_spread = 2;   // K17 plan build (vec > 1), which entries of a warp step share an instruction (parity):
+                                   // 2 contiguous halves of the sorted step (fewest x lines per gather: CC 0.1604 vs 0.1652 ms),
+                                   // 1 each bank class dealt over the parities, 0 alternate entries
     int spmv_colsort_vec = 2;      // K17 plan build: entries per thread unit (2: paired 128-bit val / 64-bit meta loads; 1: one entry)
     int spmv_colsort_tc_shape = 13; // K17 CTA shape (threads x units per step; p = software-pipelined loop):
                                     // 0 1024x3, 10 1024x1; p: 7 640x3, 8 512x4, 11 512x2, 13 768x1, 16 512x1

@@ -678,8 +678,14 @@ bool spmv_colsort_build(uint64_t m, uint64_t n, const int32_t* rp, const int32_t
                 for (size_t w0 = 0; g > 1 && w0 < t.size(); w0 += win)
                     bank_order(t, w0, std::min(t.size(), w0 + win), rmask, g, scratch);
                 while (t.size() < k.nent) t.push_back({k.rows, 0.0});  // padding: column col_lo, scratch row
-                if (vec > 1 && tuning().spmv_colsort_spread)
+                if (vec > 1 && tuning().spmv_colsort_spread == 1)
                     for (size_t g0 = 0; g0 < t.size(); g0 += 32 * vec) spread_banks(t, g0, vec, rmask, scratch);
+                if (vec > 1 && tuning().spmv_colsort_spread == 2)  // halves: parity p = sorted entries [32p, 32p + 32)
+                    for (size_t g0 = 0; g0 < t.size(); g0 += 32 * vec) {
+                        scratch.assign(t.begin() + g0, t.begin() + g0 + 32 * vec);
+                        for (int j = 0; j < 32; ++j)
+                            for (int par = 0; par < vec; ++par) t[g0 + vec * j + par] = scratch[32 * par + j];
+                    }
                 if (!tc_lanes) {
                     for (size_t i = 0; i < t.size(); ++i) {
                         L.meta[k.e0 + i] = (uint32_t)t[i].first;
