@@ -43,14 +43,14 @@ struct Tuning {
     int spmv_colsort_spread = 2;   // K17 plan build (vec > 1), which entries of a warp step share an instruction (parity):
                                    // 2 contiguous halves of the sorted step (fewest x lines per gather: CC 0.1604 vs 0.1652 ms),
                                    // 1 each bank class dealt over the parities, 0 alternate entries
-    int spmv_colsort_vec = 2;      // K17 plan build: entries per thread unit (2: paired 128-bit val / 64-bit meta loads; 1: one entry)
-    int spmv_colsort_tc_shape = 13; // K17 CTA shape (threads x units per step; p = software-pipelined loop):
+    int spmv_colsort_vec = 4;      // K17 plan build: entries per thread unit (4: 256-bit val / 128-bit meta loads; 2: 128 / 64; 1)
+    int spmv_colsort_tc_shape = 16; // K17 CTA shape (threads x units per step; p = software-pipelined loop):
                                     // 0 1024x3, 10 1024x1; p: 7 640x3, 8 512x4, 11 512x2, 13 768x1, 16 512x1
                                     // (tools/micro/spmv_shapes.py, 60 interleaved bursts of 25 calls, medians:
-                                    // TC vec 2 shape 13 0.186 ms, vec 2 11 0.194, vec 1 0 0.222, vec 1 7 0.225;
-                                    // shapes 1 768x3, 4 1024x2, 5 1024x1p, 6 768x2p, 12 640x2p, 14 512x3p,
-                                    // 15 384x4p measured no better and were dropped)
-    int spmv_colsort_cc_shape = 11; // ... CUDA-core kernel (vec 2 11 0.168, vec 2 13 0.169, vec 1 0 0.169 ms)
+                                    // TC vec 4 shape 16 0.2014 ms, vec 2 13 0.2020; earlier vec 2 11 0.194 vs
+                                    // 13 0.186, vec 1 0 0.222, vec 1 7 0.225; shapes 1 768x3, 4 1024x2,
+                                    // 5 1024x1p, 6 768x2p, 12 640x2p, 14 512x3p, 15 384x4p measured no better)
+    int spmv_colsort_cc_shape = 10; // ... CUDA-core kernel (vec 4 10 0.1542, vec 4 16 0.1586, vec 2 11 0.1620 ms)
     int spmv_plan_colsort = 1;     // plans (both units) use the column-sorted row-block layout (K17, spmv_colsort.cu) when eligible; 0: CSR
     int spmv_plan_xpieces = 0;     // max x upload pieces (first = chunk 0's prefix); 0: one per chunk
     int spmv_plan_ygroups = 0;     // y download copies (groups of consecutive chunks); 0: one per chunk

@@ -100,6 +100,12 @@ __device__ __forceinline__ void ld_stream2(const double* p, uint64_t pol, double
 __device__ __forceinline__ void ld_meta2(const unsigned* p, uint64_t pol, unsigned& a, unsigned& b) {
     asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;" : "=r"(a), "=r"(b) : "l"(p), "l"(pol));
 }
+__device__ __forceinline__ void ld_meta4(const unsigned* p, uint64_t pol, unsigned& a, unsigned& b, unsigned& c,
+                                         unsigned& d) {
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+        : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+        : "l"(p), "l"(pol));
+}
 __device__ __forceinline__ unsigned ld_meta(const unsigned* p, uint64_t pol) {
     unsigned v;
     asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
@@ -197,9 +203,13 @@ __device__ __forceinline__ void block_entries(double* __restrict__ ys, unsigned*
         if (V == 1) {
             v[0] = ld_stream(vb + i, pol);
             m[0] = ld_meta(mb + i, pol);
-        } else {
+        } else if (V == 2) {
             ld_stream2(vb + 2 * i, pol, v[0], v[V - 1]);
             ld_meta2(mb + 2 * i, pol, m[0], m[V - 1]);
+        } else {
+            const d4 q = ld4_stream(vb + 4 * i, pol);  // 256-bit
+            v[0] = q.x, v[1 % V] = q.y, v[2 % V] = q.z, v[3 % V] = q.w;
+            ld_meta4(mb + 4 * i, pol, m[0], m[1 % V], m[2 % V], m[3 % V]);
         }
     };
     unsigned i = threadIdx.x;
@@ -587,7 +597,7 @@ void spread_banks(std::vector<std::pair<uint64_t, double>>& t, size_t g0, int ve
 bool spmv_colsort_build(uint64_t m, uint64_t n, const int32_t* rp, const int32_t* col, const double* val,
                         SpmvColsortLayout& L, const std::vector<ColsortSegment>& segments_in, int classes,
                         bool tc_lanes, int vec) {
-    vec = vec == 2 ? 2 : 1;  // (vec = 4, 256-bit val units, measured no faster: profiles/spmv_colsort_r2.md)
+    vec = (vec == 2 || vec == 4) ? vec : 1;
     (void)n;
     if (m == 0 || rp[m] == 0) return false;
     int64_t maxlen = 0;
@@ -758,7 +768,10 @@ cudaError_t launch_spmv_colsort(int unit, int vec, const SpmvKBlock* blks, int b
     if (b1 <= b0) return cudaSuccess;
     const size_t smem = (size_t)(rows + 1) * 8;
     const int cs = tuning().spmv_colsort_cc_shape, ts = tuning().spmv_colsort_tc_shape;
-    cudaError_t e = vec == 2
+    cudaError_t e = vec == 4
+        ? (unit ? launch_shape<true, 4>(ts, blks, b0, b1, rb, smem, val, meta, x, y, run, s)
+                : launch_shape<false, 4>(cs, blks, b0, b1, rb, smem, val, meta, x, y, run, s))
+        : vec == 2
         ? (unit ? launch_shape<true, 2>(ts, blks, b0, b1, rb, smem, val, meta, x, y, run, s)
                 : launch_shape<false, 2>(cs, blks, b0, b1, rb, smem, val, meta, x, y, run, s))
         : (unit ? launch_shape<true, 1>(ts, blks, b0, b1, rb, smem, val, meta, x, y, run, s)

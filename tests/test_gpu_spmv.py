@@ -623,17 +623,17 @@ def test_colsort_cta_shapes_bit_identical(cuda, unit):
     want = O.spmv_csr(rp, col, val, x)
     key = "spmv_colsort_tc_shape" if unit == P.TENSOR_CORE else "spmv_colsort_cc_shape"
     prev = [P.tuning_set("spmv_colsort_fixed", 2), P.tuning_set("spmv_plan_colsort", 1),
-            P.tuning_set("spmv_colsort_vec", 2)]
+            P.tuning_set("spmv_colsort_vec", 4)]
     plans = {}
     try:
-        for vec in (1, 2):
+        for vec in (1, 2, 4):
             P.tuning_set("spmv_colsort_vec", vec)
             for u in UNITS:
                 plans[(u, vec)] = P.SpmvPlan(rp, col, val, n, unit=u)
         P.tuning_set("spmv_colsort_vec", prev[2])
         dx = torch.from_numpy(x).cuda()
         outs = {}
-        for vec in (1, 2):
+        for vec in (1, 2, 4):
             for sh in (0, 7, 8, 10, 11, 13, 16):
                 old = P.tuning_set(key, sh)
                 try:
@@ -649,7 +649,7 @@ def test_colsort_cta_shapes_bit_identical(cuda, unit):
             assert np.array_equal(y, ref), sh
         other = [u for u in UNITS if u != unit][0]
         dy = torch.full((m,), float("nan"), dtype=torch.float64, device="cuda")
-        plans[(other, 2)].execute(dx, dy)
+        plans[(other, 4)].execute(dx, dy)
         torch.cuda.synchronize()
         yo = dy.cpu().numpy()
         same = yo == ref

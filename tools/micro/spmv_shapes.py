@@ -19,7 +19,8 @@ P.spmv_csr(rp, col, val, x, yref, unit=P.CUDA_CORE)
 torch.cuda.synchronize()
 # configs "unit:vec:shape,..." (default: the sweep below)
 cfgs = [tuple(c.split(":")) for c in sys.argv[1].split(",")] if len(sys.argv) > 1 else \
-    [("cc", "1", "0"), ("cc", "2", "11"), ("cc", "2", "13"), ("tc", "1", "0"), ("tc", "2", "11"), ("tc", "2", "13")]
+    [("cc", "2", "11", "2"), ("cc", "4", "10", "2"), ("cc", "4", "16", "2"), ("tc", "2", "13", "2"),
+     ("tc", "4", "16", "2")]
 cfgs = [(c[0], int(c[1]), int(c[2]), int(c[3]) if len(c) > 3 else 1, int(c[4]) if len(c) > 4 else 1)
         for c in cfgs]  # unit, vec, shape, spread, fuse
 
