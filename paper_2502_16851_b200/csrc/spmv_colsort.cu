@@ -427,8 +427,9 @@ __global__ void __launch_bounds__(NT, 2)
                     if (jb < kDefer) {
                         if (threadIdx.x == 0) s_dcnt[jb] = s_fcnt, s_drow0[jb] = blk.row0;
                     } else {  // more blocks than the deferral slots: re-sum now
-                        __threadfence_block();
-                        resum_rows<TC>(run.list + blk.row0, s_fcnt, run, x, y, threadIdx.x, NT);
+                        const unsigned nf = s_fcnt;
+                        __syncthreads();  // every thread has nf before thread 0 resets s_fcnt for the next block
+                        resum_rows<TC>(run.list + blk.row0, nf, run, x, y, threadIdx.x, NT);
                     }
                 } else if (run.fuse && jb < kDefer && threadIdx.x == 0) {
                     s_dcnt[jb] = 0u;
