@@ -590,7 +590,7 @@ rl_spmv_plan_s* plan_create(ExecutionUnit unit, Precision p, uint64_t m, uint64_
             ck(cudaMalloc(&pl->val, std::max<uint64_t>(nnz, 1) * 8), "plan alloc");
             ck(cudaMemcpy(pl->col, col, nnz * 4, cudaMemcpyHostToDevice), "plan upload");
             ck(cudaMemcpy(pl->val, val, nnz * 8, cudaMemcpyHostToDevice), "plan upload");
-            pl->layout_bytes = (m + 1) * 4 + nnz * 12;
+            if (!pl->colsort) pl->layout_bytes = (m + 1) * 4 + nnz * 12;  // (a K17 plan keeps the CSR only for re-summed rows)
         }
     }
     const uint64_t unitrows = 1;
