@@ -10,10 +10,16 @@ u = torch.empty((512, 512, 512), dtype=torch.float64, device="cuda")
 P.stencil_init(u, 1, 1)
 v = u.clone()
 B = P.stencil_model("3d27pt").traffic_bytes * 510 ** 3
-shapes = {"default": {}, "k8": {"stencil_tch_k8": 1}, "tpw2": {"stencil_tch_tpw": 2, "stencil_tch_ctas_per_sm": 8},
-          "cc": None}
+shapes = {"default": {}, "ctas8": {"stencil_tch_ctas_per_sm": 8}, "ctas12": {"stencil_tch_ctas_per_sm": 12},
+          "ctas24": {"stencil_tch_ctas_per_sm": 24}, "stages3": {"stencil_tch_stages": 3},
+          "tpw2": {"stencil_tch_tpw": 2, "stencil_tch_ctas_per_sm": 8}, "cc": None}
+if len(sys.argv) > 1:  # name=key:val,key:val ...
+    shapes = {"default": {}, "cc": None}
+    for a in sys.argv[1:]:
+        name, _, kv = a.partition("=")
+        shapes[name] = {k: int(v) for k, v in (x.split(":") for x in kv.split(","))}
 res = {k: [] for k in shapes}
-for rnd in range(5):
+for rnd in range(int(os.environ.get('ROUNDS', '7'))):
     for name, keys in shapes.items():
         prev = {}
         for k, val in (keys or {}).items():
