@@ -19,27 +19,35 @@ int main() {
     cudaHostAlloc(&hy, n, cudaHostAllocMapped);
     cudaMalloc(&dx, n);
     cudaMalloc(&dy, n);
-    cudaStream_t s1, s2;
+    cudaStream_t s1, s2, s3;
     cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking);
-    std::vector<cudaEvent_t> ev(64);
+    cudaStreamCreateWithFlags(&s3, cudaStreamNonBlocking);
+    std::vector<cudaEvent_t> ev(64), ev2(64);
+    for (auto& e : ev2) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     for (auto& e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     cudaEvent_t a, b, f;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     cudaEventCreateWithFlags(&f, cudaEventDisableTiming);
     auto run = [&](int P, int lag, int mode, bool graph) {
-        // mode 0: D2H CE copies with waits; 1: no waits; 2: SM copy kernel per y piece with waits
+        // mode 0: D2H CE copies with waits; 1: no waits; 2: SM copy kernel per y piece with waits;
+        // 3: the plan's two hops (a third stream waits on the H2D event and records its own, D2H waits on that)
         auto body = [&] {
             cudaEventRecord(f, s1);
             cudaStreamWaitEvent(s2, f, 0);
+            cudaStreamWaitEvent(s3, f, 0);
             const size_t pc = n / P;
             for (int p = 0; p < P; ++p) {
                 cudaMemcpyAsync(dx + p * pc, hx + p * pc, pc, cudaMemcpyHostToDevice, s1);
                 cudaEventRecord(ev[p], s1);
             }
             for (int p = 0; p < P; ++p) {
-                if (mode != 1) cudaStreamWaitEvent(s2, ev[std::min(P - 1, p + lag)], 0);
+                if (mode == 3) {
+                    cudaStreamWaitEvent(s3, ev[std::min(P - 1, p + lag)], 0);
+                    cudaEventRecord(ev2[p], s3);
+                    cudaStreamWaitEvent(s2, ev2[p], 0);
+                } else if (mode != 1) cudaStreamWaitEvent(s2, ev[std::min(P - 1, p + lag)], 0);
                 if (mode == 2)
                     copy_kernel<<<64, 1024, 0, s2>>>((const int4*)(dy + p * pc), (int4*)(hy + p * pc), pc / 16);
                 else
@@ -47,6 +55,8 @@ int main() {
             }
             cudaEventRecord(ev[63], s2);
             cudaStreamWaitEvent(s1, ev[63], 0);
+            cudaEventRecord(ev2[63], s3);
+            cudaStreamWaitEvent(s1, ev2[63], 0);
         };
         cudaGraphExec_t ge = nullptr;
         if (graph) {
@@ -73,7 +83,9 @@ int main() {
     };
     for (int graph = 0; graph < 2; ++graph)
         for (int P : {1, 2, 4, 8, 16})
-            printf("graph %d pieces %2d: no waits %.3f ms, CE waits lag 1 %.3f, lag 0 %.3f, SM y copies lag 1 %.3f\n",
-                   graph, P, run(P, 1, 1, graph), run(P, 1, 0, graph), run(P, 0, 0, graph), run(P, 1, 2, graph));
+            printf("graph %d pieces %2d: no waits %.3f ms, CE waits lag 1 %.3f, lag 0 %.3f, SM y copies lag 1 %.3f, "
+                   "two hops lag 0 %.3f\n",
+                   graph, P, run(P, 1, 1, graph), run(P, 1, 0, graph), run(P, 0, 0, graph), run(P, 1, 2, graph),
+                   run(P, 0, 3, graph));
     return 0;
 }
